@@ -1,0 +1,139 @@
+/*
+ * fftpde.h -- C ABI of the B200-native 2D FFT-PDE hot path (arXiv 2412.12308).
+ *
+ * Every compute call runs hand-written sm_100a CUDA kernels (libfftpde.so);
+ * there is no CPU fallback and no cuFFT.  PAPER.md below is the paper's LaTeX
+ * source, cited by line; R1..R16 are the
+ * readings of its silent or garbled points.
+ *
+ * Conventions (all calls)
+ * -----------------------
+ * Grids: [batch][ny][nx], C-contiguous, x fastest, interleaved complex
+ *   (FFTPDE_C128: double re,im = 16 B/pt; FFTPDE_C64: float re,im = 8 B/pt).
+ *   Element (b,k,j) is p_{jk} at x_j = j Lx/nx, y_k = k Ly/ny.
+ * Spectra: natural order, index a <-> fold(a) = a (a <= n/2) else a - n
+ *   (R2).  Angular wavenumber k_a = 2 pi fold(a)/Lx (R4).
+ * Forward transform: P_ab = sum_jk p_jk e^{+2 pi i aj/nx} e^{+2 pi i bk/ny},
+ *   unnormalised (2D_DFT; eq:DFT PAPER.md:119-124; R1, R3).
+ * Inverse transform: conjugate kernel times 1/(nx ny).
+ * Axis lengths: powers of two, 1 <= n <= 8192 per axis in
+ *   this build (larger -> FFTPDE_ERR_UNSUPPORTED).
+ *
+ * Ownership: the caller owns every device buffer -- inputs, outputs and the
+ *   workspace of fftpde_workspace_size() bytes (allocate it with torch).  The
+ *   plan owns host-side state only and never calls cudaMalloc.
+ * Execution: compute calls are asynchronous on the plan's stream (set with
+ *   fftpde_set_stream; default: the legacy default stream).  Argument checks
+ *   are synchronous and happen before anything is enqueued.  Launch errors
+ *   are returned as FFTPDE_ERR_CUDA; device faults surface at the caller's
+ *   next synchronisation.
+ * Aliasing: in == out is allowed everywhere; inputs are otherwise not written.
+ * Alignment: device pointers must be 16-byte aligned (128-bit access).
+ * Threads: one host thread per plan at a time; distinct plans are independent.
+ */
+#ifndef FFTPDE_H
+#define FFTPDE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fftpde_plan_s *fftpde_plan;
+
+typedef enum { FFTPDE_C64 = 0, FFTPDE_C128 = 1 } fftpde_dtype;
+
+typedef enum {
+    FFTPDE_OK = 0,
+    FFTPDE_ERR_INVALID_ARG = 1,  /* null pointer, bad dtype, non-finite/non-positive L, dt<0 (diffuse), nsteps<0, misaligned */
+    FFTPDE_ERR_EMPTY = 2,        /* a zero-sized axis or batch ("rejects empty input") */
+    FFTPDE_ERR_NOT_POW2_X = 3,   /* nx not a power of two (radix-2 restriction) */
+    FFTPDE_ERR_NOT_POW2_Y = 4,   /* ny not a power of two */
+    FFTPDE_ERR_UNSUPPORTED = 5,  /* axis longer than this build supports, or batch outside the plan */
+    FFTPDE_ERR_WORKSPACE = 6,    /* workspace missing or smaller than fftpde_workspace_size() */
+    FFTPDE_ERR_CUDA = 7,         /* a CUDA runtime call or kernel launch failed */
+    FFTPDE_ERR_NCCL = 8          /* reserved for the sharded path */
+} fftpde_status;
+
+/* Create a plan for batch grids of ny x nx points on the periodic domain
+ * [0,Lx) x [0,Ly) with complex dtype `dtype` on CUDA device
+ * `device`.  Validates the arguments and builds the host tables (twiddles
+ * w_n^m = e^{+2 pi i m/n} per index in fp64, kx^2, ky^2).  *plan is NULL on
+ * error. */
+fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t batch,
+                             fftpde_dtype dtype, double Lx, double Ly, int device);
+
+/* Bytes of device workspace the plan needs (tables + operator tables). */
+size_t fftpde_workspace_size(fftpde_plan plan);
+
+/* Hand the plan a device workspace of >= fftpde_workspace_size() bytes,
+ * 256-byte aligned; the plan uploads its tables into it on its stream.  The
+ * caller keeps it alive until fftpde_destroy. */
+fftpde_status fftpde_set_workspace(fftpde_plan plan, void *dev_ptr, size_t bytes);
+
+/* Stream for all subsequent calls (a cudaStream_t, e.g. torch's
+ * torch.cuda.current_stream().cuda_stream); NULL = legacy default stream. */
+fftpde_status fftpde_set_stream(fftpde_plan plan, void *cuda_stream);
+
+fftpde_status fftpde_destroy(fftpde_plan plan);
+const char *fftpde_status_string(fftpde_status status);
+
+/* Number of CUDA kernels the library enqueued since the plan was created
+ * (instrumentation for bench.py's gpu_launches). */
+int64_t fftpde_launch_count(fftpde_plan plan);
+
+/* ---- transforms ------------------------------------------------------------
+ * fftpde_forward: out = DFT2(in), + sign, unnormalised, natural order
+ *   (2D_DFT PAPER.md:246-249, computed as row transforms then column
+ *   transforms).
+ * fftpde_inverse: out = iDFT2(in) = conj kernel x 1/(nx ny).
+ * Both act on the plan's whole batch. */
+fftpde_status fftpde_forward(fftpde_plan plan, const void *in, void *out);
+fftpde_status fftpde_inverse(fftpde_plan plan, const void *in, void *out);
+
+/* ---- solvers ---------------------------------------------------------------
+ * fftpde_poisson: solve nabla^2 u = rho (eq:Poisson PAPER.md:286-291):
+ *   u = iDFT2( m .* DFT2(rho) ), m = -1/|k|^2, m(0,0) = 0
+ *   (eq:SolutionPoisson PAPER.md:329-331; zeroing k=0 == subtracting the mean,
+ *   eq:Poisson2 PAPER.md:308-325; R5).  The input mean is ignored and u has
+ *   zero mean.
+ * fftpde_diffuse: nsteps exact steps of u_t = D nabla^2 u from u0
+ *   (ec:solCalorFourier PAPER.md:376-386, coefficient D per R6): each step is
+ *   DFT2, multiply by exp(-D |k|^2 dt), iDFT2, and materialises u (R8).
+ *   D >= 0, dt >= 0, nsteps >= 0 (0 copies u0 to u).  k = 0 is kept.
+ * fftpde_wave_step: nsteps exact steps of u_tt = c^2 nabla^2 u (s = 0,
+ *   eq:wave_equation PAPER.md:417-424) on the state (u, ut) in place: with
+ *   kappa = c|k|, (U,V) <- (C U + S1 V, S2 U + C V), C = cos(kappa dt),
+ *   S1 = sin(kappa dt)/kappa, S2 = -kappa sin(kappa dt); at kappa = 0,
+ *   S1 = dt, S2 = 0 (eq:OmegaZero/OmegaNonZero PAPER.md:459-471; R7).
+ *   Any finite dt (negative reverses time), c >= 0, nsteps >= 0.
+ *   The propagator tables are computed on the host in fp64 for each new
+ *   (c, dt) and uploaded into the workspace on the plan's stream. */
+fftpde_status fftpde_poisson(fftpde_plan plan, const void *rho, void *u);
+fftpde_status fftpde_diffuse(fftpde_plan plan, const void *u0, void *u,
+                             double D, double dt, int64_t nsteps);
+fftpde_status fftpde_wave_step(fftpde_plan plan, void *u, void *ut,
+                               double c, double dt, int64_t nsteps);
+
+/* ---- batched variants -------------------------------------------------------
+ * Same semantics over `batch` grids (1 <= batch <= the plan's batch) whose
+ * starts are `stride` elements apart (stride >= nx*ny, multiple of 8). */
+fftpde_status fftpde_forward_batched(fftpde_plan plan, const void *in, void *out,
+                                     int64_t batch, int64_t stride);
+fftpde_status fftpde_inverse_batched(fftpde_plan plan, const void *in, void *out,
+                                     int64_t batch, int64_t stride);
+fftpde_status fftpde_poisson_batched(fftpde_plan plan, const void *rho, void *u,
+                                     int64_t batch, int64_t stride);
+fftpde_status fftpde_diffuse_batched(fftpde_plan plan, const void *u0, void *u,
+                                     int64_t batch, int64_t stride,
+                                     double D, double dt, int64_t nsteps);
+fftpde_status fftpde_wave_step_batched(fftpde_plan plan, void *u, void *ut,
+                                       int64_t batch, int64_t stride,
+                                       double c, double dt, int64_t nsteps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FFTPDE_H */

@@ -1,0 +1,249 @@
+// fft_core.cuh -- register-resident Stockham FFT building blocks for sm_100a.
+//
+// What is computed (PAPER.md = the paper's LaTeX source):
+//   P_k = sum_j p_j w_N^{jk}, w_N = e^{+2 pi i/N}   (eq:DFT)
+// i.e. the paper's forward sign.  The inverse is conj(FFT(conj(P))) / N
+// (PAPER.md:157-159): callers conjugate on load/store and fold 1/N into the
+// k-space multiplier.
+//
+// How (not the paper's recursive radix-2 text, which is prior art, but the
+// same result): a self-sorting Stockham factorisation N = E^s * r with radix
+// E = 16 (built as 4x4) in registers, a final radix r in {2,4,8,16}, and an
+// exchange through shared memory between stages.  Thread t of a transform
+// holds x[t + TPT*e] (e < E, TPT = N/E threads) on entry and X[t + TPT*e] on
+// exit, so global loads and stores are unit-stride across threads.
+// Twiddles come from a per-length table w_N^m (m < N) computed on the host in
+// fp64 per index (never by recurrence) and rounded once to fp32 for c64.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fftpde {
+
+template <typename T> struct cplx_t;
+template <> struct cplx_t<double> { using type = double2; };
+template <> struct cplx_t<float> { using type = float2; };
+
+template <typename C> __device__ __forceinline__ C cadd(C a, C b) { return {a.x + b.x, a.y + b.y}; }
+template <typename C> __device__ __forceinline__ C csub(C a, C b) { return {a.x - b.x, a.y - b.y}; }
+// a * i
+template <typename C> __device__ __forceinline__ C cmul_i(C a) { return {-a.y, a.x}; }
+template <typename C> __device__ __forceinline__ C cconj(C a) { return {a.x, -a.y}; }
+template <typename C> __device__ __forceinline__ C cmul(C a, C w)
+{
+    return {a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x};
+}
+template <typename C, typename T> __device__ __forceinline__ C cscale(C a, T s) { return {a.x * s, a.y * s}; }
+
+// multiply by w_8 = (1+i)/sqrt2 and w_8^3 = (-1+i)/sqrt2
+template <typename C> __device__ __forceinline__ C cmul_w8(C a)
+{
+    using T = decltype(a.x);
+    const T h = (T)0.70710678118654752440084436210485;
+    return {(a.x - a.y) * h, (a.x + a.y) * h};
+}
+template <typename C> __device__ __forceinline__ C cmul_w83(C a)
+{
+    using T = decltype(a.x);
+    const T h = (T)0.70710678118654752440084436210485;
+    return {-(a.x + a.y) * h, (a.x - a.y) * h};
+}
+
+// ---------------------------------------------------------------------------
+// Small DFTs with the + sign, in place, natural order in and out.
+
+template <typename C> __device__ __forceinline__ void dft2(C &a0, C &a1)
+{
+    C t = a0;
+    a0 = cadd(t, a1);
+    a1 = csub(t, a1);
+}
+
+// X_k = sum_n a_n i^{nk}
+template <typename C> __device__ __forceinline__ void dft4(C &a0, C &a1, C &a2, C &a3)
+{
+    C t0 = cadd(a0, a2), t1 = csub(a0, a2), t2 = cadd(a1, a3), t3 = cmul_i(csub(a1, a3));
+    a0 = cadd(t0, t2);
+    a2 = csub(t0, t2);
+    a1 = cadd(t1, t3);
+    a3 = csub(t1, t3);
+}
+
+// radix-8 as 2 x 4: n = 4 n1 + n2, k = k1 + 2 k2
+template <typename C> __device__ __forceinline__ void dft8(C (&v)[8])
+{
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) dft2(v[n2], v[n2 + 4]);   // Y[n2][k1] at v[n2 + 4 k1]
+    v[5] = cmul_w8(v[5]);
+    v[6] = cmul_i(v[6]);
+    v[7] = cmul_w83(v[7]);
+    dft4(v[0], v[1], v[2], v[3]);                          // k1 = 0 -> X[2 k2]     at v[k2]
+    dft4(v[4], v[5], v[6], v[7]);                          // k1 = 1 -> X[1 + 2 k2] at v[4 + k2]
+    C o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = v[4 * (k % 2) + k / 2];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = o[k];
+}
+
+// radix-16 as 4 x 4: n = 4 n1 + n2, k = k1 + 4 k2, internal twiddle w16^{n2 k1}
+template <typename C> __device__ __forceinline__ void dft16(C (&v)[16])
+{
+    using T = decltype(v[0].x);
+    const T c1 = (T)0.92387953251128675612818318939679;   // cos(pi/8)
+    const T s1 = (T)0.38268343236508977172845998403040;   // sin(pi/8)
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) dft4(v[n2], v[n2 + 4], v[n2 + 8], v[n2 + 12]);
+    // v[n2 + 4 k1] = Y[n2][k1]; multiply by w16^{n2 k1}
+    const C w1 = {c1, s1}, w3 = {s1, c1}, w9 = {-c1, -s1};
+    v[5] = cmul(v[5], w1);          // n2=1,k1=1: w^1
+    v[6] = cmul_w8(v[6]);           // n2=2,k1=1: w^2
+    v[7] = cmul(v[7], w3);          // n2=3,k1=1: w^3
+    v[9] = cmul_w8(v[9]);           // n2=1,k1=2: w^2
+    v[10] = cmul_i(v[10]);          // n2=2,k1=2: w^4
+    v[11] = cmul_w83(v[11]);        // n2=3,k1=2: w^6
+    v[13] = cmul(v[13], w3);        // n2=1,k1=3: w^3
+    v[14] = cmul_w83(v[14]);        // n2=2,k1=3: w^6
+    v[15] = cmul(v[15], w9);        // n2=3,k1=3: w^9
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) dft4(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+    C o[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) o[k] = v[4 * (k % 4) + k / 4];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = o[k];
+}
+
+template <int R, typename C> __device__ __forceinline__ void dft_r(C (&v)[R]);
+template <> __device__ __forceinline__ void dft_r<1, double2>(double2 (&)[1]) {}
+template <> __device__ __forceinline__ void dft_r<1, float2>(float2 (&)[1]) {}
+template <> __device__ __forceinline__ void dft_r<2, double2>(double2 (&v)[2]) { dft2(v[0], v[1]); }
+template <> __device__ __forceinline__ void dft_r<2, float2>(float2 (&v)[2]) { dft2(v[0], v[1]); }
+template <> __device__ __forceinline__ void dft_r<4, double2>(double2 (&v)[4]) { dft4(v[0], v[1], v[2], v[3]); }
+template <> __device__ __forceinline__ void dft_r<4, float2>(float2 (&v)[4]) { dft4(v[0], v[1], v[2], v[3]); }
+template <> __device__ __forceinline__ void dft_r<8, double2>(double2 (&v)[8]) { dft8(v); }
+template <> __device__ __forceinline__ void dft_r<8, float2>(float2 (&v)[8]) { dft8(v); }
+template <> __device__ __forceinline__ void dft_r<16, double2>(double2 (&v)[16]) { dft16(v); }
+template <> __device__ __forceinline__ void dft_r<16, float2>(float2 (&v)[16]) { dft16(v); }
+
+// ---------------------------------------------------------------------------
+// Compile-time shape of one length-N transform.
+template <int N_> struct Shape {
+    static constexpr int N = N_;
+    static constexpr int E = N_ < 16 ? N_ : 16;        // elements per thread
+    static constexpr int TPT = N_ / E;                   // threads per transform
+    static constexpr int LOGE = E == 16 ? 4 : E == 8 ? 3 : E == 4 ? 2 : E == 2 ? 1 : 0;
+    // padded smem index: one pad slot every E elements (conflict-free stage-1 scatter)
+    static constexpr int PADDED = N_ + (N_ >> LOGE);
+    // number of full radix-E stages before the last one, and the last radix
+    static constexpr int STAGES = []() { int ns = 1, s = 0; while (ns * E < N_) { ns *= E; ++s; } return s; }();
+    static constexpr int NS_LAST = []() { int ns = 1; while (ns * E < N_) ns *= E; return ns; }();
+    static constexpr int R_LAST = N_ / NS_LAST;
+};
+
+// Twiddle load through the read-only path.  volatile: one load per use, so the
+// compiler neither keeps a whole table of twiddles live across transforms (CSE)
+// nor hoists them far ahead of their use (register pressure).
+__device__ __forceinline__ double2 ldtw(const double2 *p)
+{
+    double2 r;
+    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ float2 ldtw(const float2 *p)
+{
+    float2 r;
+    asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
+    return r;
+}
+
+// Identity the compiler cannot see through: keeps per-transform index
+// arithmetic (twiddle addresses) from being shared across the several
+// transforms of one kernel, which would keep ~60 address registers live.
+__device__ __forceinline__ int opaque(int x)
+{
+    int y;
+    asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+
+template <typename P> __device__ __forceinline__ P *opaque_ptr(P *x)
+{
+    P *y;
+    asm volatile("mov.b64 %0, %1;" : "=l"(y) : "l"(x));
+    return y;
+}
+
+__device__ __forceinline__ int padidx(int p, int loge) { return p + (p >> loge); }
+
+// Exchange buffer of one transform: element p lives at base[pad(p) * STRIDE],
+// pad(p) = p + p / 2^LOGE (one pad slot every E elements).  For an access
+// p0 + d where p0 or d is a multiple of 2^LOGE, pad(p0 + d) = pad(p0) + pad(d),
+// so every access of a stage is one base register plus an immediate offset.
+template <typename C, int LOGE, int STRIDE> struct SmemView {
+    C *base;
+    __device__ __forceinline__ C *ptr(int p) const { return base + padidx(p, LOGE) * STRIDE; }
+    static __device__ __forceinline__ constexpr int off(int d) { return (d + (d >> LOGE)) * STRIDE; }
+    __device__ __forceinline__ C &at(int p) const { return base[padidx(p, LOGE) * STRIDE]; }
+};
+
+// Forward FFT (+ sign) of one length-N sequence held as v[e] = x[t + TPT e].
+// On exit v[e] = X[t + TPT e].  `sync` synchronises all threads that share the
+// smem buffers (warp or CTA); smem is free again when this returns.
+// tw: device table w_N^m, m in [0, N).
+template <int N, typename C, typename View, typename Sync>
+__device__ __forceinline__ void fft_forward(C (&v)[Shape<N>::E], const View &sm, int t,
+                                            const C *__restrict__ tw, Sync sync)
+{
+    using S = Shape<N>;
+    constexpr int E = S::E, TPT = S::TPT;
+    int Ns = 1;
+#pragma unroll
+    for (int s = 0; s < S::STAGES; ++s) {
+        const int k = t & (Ns - 1);
+        if (s > 0) {
+            const int step = opaque((N / (Ns * E)) * k);   // twiddle w_{Ns E}^{m k} = w_N^{m k N/(Ns E)}
+#pragma unroll
+            for (int m = 1; m < E; ++m) v[m] = cmul(v[m], ldtw(&tw[m * step]));
+        }
+        dft_r<E>(v);
+        // scatter X_m of butterfly t to (t / Ns) Ns E + k + m Ns; base or m Ns is a multiple of E
+        C *wp = sm.ptr((t - k) * E + k);
+#pragma unroll
+        for (int m = 0; m < E; ++m) wp[View::off(m * Ns)] = v[m];
+        sync();
+        if constexpr (TPT % E == 0) {
+            const C *rp = sm.ptr(t);
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = rp[View::off(m * TPT)];
+        } else {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = sm.at(t + m * TPT);
+        }
+        sync();
+        Ns *= E;
+    }
+    // last stage: radix R = N / Ns, E/R butterflies per thread, j = t + q TPT,
+    // inputs x[j + m N/R] = slot q + m E/R, outputs X[j + m Ns] -> same slots.
+    constexpr int R = S::R_LAST;
+    constexpr int Q = E / R;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        C u[R];
+#pragma unroll
+        for (int m = 0; m < R; ++m) u[m] = v[q + m * Q];
+        if (S::NS_LAST > 1) {
+            const int j = opaque(t + q * TPT);          // twiddle w_N^{m j}
+#pragma unroll
+            for (int m = 1; m < R; ++m) u[m] = cmul(u[m], ldtw(&tw[m * j]));
+        }
+        dft_r<R>(u);
+#pragma unroll
+        for (int m = 0; m < R; ++m) v[q + m * Q] = u[m];
+    }
+}
+
+struct SyncCTA { __device__ __forceinline__ void operator()() const { __syncthreads(); } };
+struct SyncWarp { __device__ __forceinline__ void operator()() const { __syncwarp(); } };
+
+} // namespace fftpde

@@ -1,0 +1,519 @@
+// fftpde_api.cu -- the C ABI (include/fftpde.h): plans, host tables, dispatch.
+//
+// Host-side responsibilities (everything on the device is in kernels.cuh):
+//   * argument validation (synchronous, before anything is enqueued);
+//   * fp64 tables: twiddles w_n^m = e^{+2 pi i m/n} per index (eq:DFT,
+//     PAPER.md:124), |k|^2 per axis with k = 2 pi fold(a)/L (PAPER.md:106-109,
+//     175, 253-258, 296-303; R2, R4), the diffusion factors
+//     exp(-D k^2 dt) (ec:solCalorFourier PAPER.md:378-386) and the wave
+//     propagator quadrant (eq:OmegaZero/NonZero PAPER.md:459-471);
+//   * the pass sequence of each call (3 passes per solve step).
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/fftpde.h"
+#include "launch.h"
+
+using namespace fftpde;
+
+struct fftpde_plan_s {
+    int64_t nx = 0, ny = 0, batch = 0;
+    fftpde_dtype dtype = FFTPDE_C128;
+    double Lx = 1.0, Ly = 1.0;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    unsigned char *ws = nullptr;
+    size_t ws_bytes = 0;
+    // workspace offsets (bytes)
+    size_t o_twx = 0, o_twy = 0, o_kx2 = 0, o_ky2 = 0, o_ex = 0, o_ey = 0, o_wc = 0, o_ws1 = 0, o_ws2 = 0;
+    size_t need = 0;
+    int64_t qx = 0, qy = 0;   // quadrant extents nx/2+1, ny/2+1
+    // host tables (fp64)
+    std::vector<double> twx, twy;   // interleaved re, im
+    std::vector<double> kx2, ky2;
+    bool diff_valid = false;
+    double diff_D = 0, diff_dt = 0;
+    bool wave_valid = false;
+    double wave_c = 0, wave_dt = 0;
+    int64_t launches = 0;
+};
+
+namespace {
+
+bool is_pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// w_n^m = exp(+2 pi i m/n).  m is reduced exactly modulo n, the angle is
+// folded by symmetry into [0, pi/4] and evaluated in long double, then
+// rounded once; quarter-turn values are exact.
+void unit_root(int64_t n, int64_t m, double &re, double &im)
+{
+    int64_t r = m % n;
+    if (r < 0) r += n;
+    bool conj = false;
+    if (2 * r > n) { r = n - r; conj = true; }            // e^{-i t} = conj e^{i t}
+    bool mirror = false;                                    // angle in (pi/2, pi]: pi - t
+    if (4 * r > n) { r = n - 2 * r; mirror = true; } else { r = 2 * r; }
+    // now angle = pi * r / n  with r in [0, n/2] (units of pi/n)
+    bool swap = false;                                      // angle in (pi/4, pi/2]: pi/2 - t
+    if (4 * r > n) { r = n - 2 * r; swap = true; } else { r = 2 * r; }
+    // now angle = (pi/2) r / n, r in [0, n/2] -> angle in [0, pi/4]
+    const long double phi = (long double)r / (long double)n * 1.5707963267948966192313216916397514L;
+    long double c = cosl(phi), s = sinl(phi);
+    if (swap) { long double t = c; c = s; s = t; }
+    if (mirror) c = -c;
+    if (conj) s = -s;
+    re = (double)c;
+    im = (double)s;
+}
+
+void build_twiddles(int64_t n, std::vector<double> &tw)
+{
+    tw.resize(2 * (size_t)n);
+    for (int64_t m = 0; m < n; ++m) unit_root(n, m, tw[2 * m], tw[2 * m + 1]);
+}
+
+// (2 pi fold(a) / L)^2, fold(a) = a for a <= n/2 else a - n
+void build_k2(int64_t n, double L, std::vector<double> &k2)
+{
+    k2.resize((size_t)n);
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int64_t a = 0; a < n; ++a) {
+        const int64_t f = (2 * a <= n) ? a : a - n;
+        const double k = two_pi * (double)f / L;
+        k2[(size_t)a] = k * k;
+    }
+}
+
+template <typename T> std::vector<T> cast_vec(const std::vector<double> &v)
+{
+    std::vector<T> o(v.size());
+    for (size_t i = 0; i < v.size(); ++i) o[i] = (T)v[i];
+    return o;
+}
+
+size_t elem_real(const fftpde_plan p) { return p->dtype == FFTPDE_C128 ? 8 : 4; }
+size_t elem_cplx(const fftpde_plan p) { return 2 * elem_real(p); }
+
+fftpde_status cuda_status(cudaError_t e) { return e == cudaSuccess ? FFTPDE_OK : FFTPDE_ERR_CUDA; }
+
+// Upload a double host vector as the plan's real type.
+fftpde_status upload(fftpde_plan p, size_t off, const std::vector<double> &v)
+{
+    cudaError_t e;
+    if (p->dtype == FFTPDE_C128) {
+        e = cudaMemcpyAsync(p->ws + off, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice,
+                            p->stream);
+    } else {
+        std::vector<float> f = cast_vec<float>(v);
+        e = cudaMemcpyAsync(p->ws + off, f.data(), f.size() * sizeof(float), cudaMemcpyHostToDevice,
+                            p->stream);
+        // pageable source: the call returns after staging, so f may be freed
+    }
+    return cuda_status(e);
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev)
+    {
+        if (cudaGetDevice(&prev) != cudaSuccess) { ok = false; return; }
+        if (prev != dev && cudaSetDevice(dev) != cudaSuccess) ok = false;
+    }
+    ~DeviceGuard()
+    {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+template <typename T> OpTables<T> tables(fftpde_plan p)
+{
+    OpTables<T> t;
+    t.kx2 = (const T *)(p->ws + p->o_kx2);
+    t.ky2 = (const T *)(p->ws + p->o_ky2);
+    t.ex = (const T *)(p->ws + p->o_ex);
+    t.ey = (const T *)(p->ws + p->o_ey);
+    t.wC = (const T *)(p->ws + p->o_wc);
+    t.wS1 = (const T *)(p->ws + p->o_ws1);
+    t.wS2 = (const T *)(p->ws + p->o_ws2);
+    t.qpitch = p->qy;
+    t.scale = (T)(1.0 / ((double)p->nx * (double)p->ny));
+    return t;
+}
+
+fftpde_status check_ptr(fftpde_plan p, const void *ptr)
+{
+    (void)p;
+    if (!ptr) return FFTPDE_ERR_INVALID_ARG;
+    if (((uintptr_t)ptr & 15u) != 0) return FFTPDE_ERR_INVALID_ARG;
+    return FFTPDE_OK;
+}
+
+fftpde_status check_call(fftpde_plan p, int64_t batch, int64_t stride)
+{
+    if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (!p->ws) return FFTPDE_ERR_WORKSPACE;
+    if (batch == 0) return FFTPDE_ERR_EMPTY;
+    if (batch < 0 || stride < p->nx * p->ny) return FFTPDE_ERR_INVALID_ARG;
+    if (batch > p->batch) return FFTPDE_ERR_UNSUPPORTED;
+    if (batch > 1 && (stride % 8) != 0) return FFTPDE_ERR_INVALID_ARG;
+    return FFTPDE_OK;
+}
+
+// ---- pass sequences --------------------------------------------------------
+template <typename T> struct Passes {
+    fftpde_plan p;
+    int64_t batch, stride;
+    const void *twx() const { return p->ws + p->o_twx; }
+    const void *twy() const { return p->ws + p->o_twy; }
+    cudaError_t rows(const void *in, void *out, int conj)
+    {
+        ++p->launches;
+        return launch_rows<T>(p->nx, in, out, p->ny, stride, batch, conj, twx(), p->stream);
+    }
+    cudaError_t cols(const void *in, void *out, int op)
+    {
+        ++p->launches;
+        return launch_cols<T>(p->ny, in, out, p->nx, stride, batch, op, twy(), tables<T>(p), p->stream);
+    }
+    cudaError_t wave_cols(void *U, void *V)
+    {
+        ++p->launches;
+        return launch_wave_cols<T>(p->ny, U, V, p->nx, stride, batch, twy(), tables<T>(p), p->stream);
+    }
+    bool small() const { return small_supported<T>(p->nx, p->ny); }
+    cudaError_t small_op(const void *in, void *out, int op)
+    {
+        ++p->launches;
+        return launch_small<T>(p->nx, p->ny, in, out, stride, batch, op, twx(), twy(), tables<T>(p),
+                               p->stream);
+    }
+    // one step of a diagonal k-space operator: DFT2 -> multiply -> iDFT2
+    cudaError_t solve_step(const void *in, void *out, int op)
+    {
+        if (small()) return small_op(in, out, op);
+        cudaError_t e = rows(in, out, 0);
+        if (e == cudaSuccess) e = cols(out, out, op);
+        if (e == cudaSuccess) e = rows(out, out, 1);
+        return e;
+    }
+    cudaError_t forward(const void *in, void *out)
+    {
+        if (small()) return small_op(in, out, COL_FWD);
+        cudaError_t e = rows(in, out, 0);
+        if (e == cudaSuccess) e = cols(out, out, COL_FWD);
+        return e;
+    }
+    cudaError_t inverse(const void *in, void *out)
+    {
+        if (small()) return small_op(in, out, COL_INV);
+        cudaError_t e = cols(in, out, COL_INV);
+        if (e == cudaSuccess) e = rows(out, out, 1);
+        return e;
+    }
+    cudaError_t wave(void *U, void *V, int64_t nsteps)
+    {
+        cudaError_t e = cudaSuccess;
+        for (int64_t s = 0; s < nsteps && e == cudaSuccess; ++s) {
+            e = rows(U, U, 0);
+            if (e == cudaSuccess) e = rows(V, V, 0);
+            if (e == cudaSuccess) e = wave_cols(U, V);
+            if (e == cudaSuccess) e = rows(U, U, 1);
+            if (e == cudaSuccess) e = rows(V, V, 1);
+        }
+        return e;
+    }
+};
+
+template <typename F> fftpde_status dispatch(fftpde_plan p, int64_t batch, int64_t stride, F &&f)
+{
+    DeviceGuard g(p->device);
+    if (!g.ok) return FFTPDE_ERR_CUDA;
+    cudaError_t e;
+    if (p->dtype == FFTPDE_C128) {
+        Passes<double> ps{p, batch, stride};
+        e = f(ps);
+    } else {
+        Passes<float> ps{p, batch, stride};
+        e = f(ps);
+    }
+    return cuda_status(e);
+}
+
+fftpde_status ensure_diffusion_tables(fftpde_plan p, double D, double dt)
+{
+    if (p->diff_valid && p->diff_D == D && p->diff_dt == dt) return FFTPDE_OK;
+    const double scale = 1.0 / ((double)p->nx * (double)p->ny);
+    std::vector<double> ex((size_t)p->nx), ey((size_t)p->ny);
+    for (int64_t a = 0; a < p->nx; ++a) ex[(size_t)a] = std::exp(-D * p->kx2[(size_t)a] * dt) * scale;
+    for (int64_t b = 0; b < p->ny; ++b) ey[(size_t)b] = std::exp(-D * p->ky2[(size_t)b] * dt);
+    fftpde_status s = upload(p, p->o_ex, ex);
+    if (s == FFTPDE_OK) s = upload(p, p->o_ey, ey);
+    if (s != FFTPDE_OK) return s;
+    p->diff_valid = true;
+    p->diff_D = D;
+    p->diff_dt = dt;
+    return FFTPDE_OK;
+}
+
+fftpde_status ensure_wave_tables(fftpde_plan p, double c, double dt)
+{
+    if (p->wave_valid && p->wave_c == c && p->wave_dt == dt) return FFTPDE_OK;
+    const double scale = 1.0 / ((double)p->nx * (double)p->ny);
+    const size_t n = (size_t)(p->qx * p->qy);
+    std::vector<double> C(n), S1(n), S2(n);
+    for (int64_t qa = 0; qa < p->qx; ++qa) {
+        for (int64_t qb = 0; qb < p->qy; ++qb) {
+            const size_t i = (size_t)(qa * p->qy + qb);
+            const double k2 = p->kx2[(size_t)qa] + p->ky2[(size_t)qb];
+            const double kappa = c * std::sqrt(k2);
+            if (kappa == 0.0) {            // eq:OmegaZero: u <- u + dt v, v unchanged
+                C[i] = scale;
+                S1[i] = dt * scale;
+                S2[i] = 0.0;
+            } else {                       // eq:OmegaNonZero and its time derivative
+                const double sn = std::sin(kappa * dt);
+                C[i] = std::cos(kappa * dt) * scale;
+                S1[i] = (sn / kappa) * scale;
+                S2[i] = (-kappa * sn) * scale;
+            }
+        }
+    }
+    fftpde_status s = upload(p, p->o_wc, C);
+    if (s == FFTPDE_OK) s = upload(p, p->o_ws1, S1);
+    if (s == FFTPDE_OK) s = upload(p, p->o_ws2, S2);
+    if (s != FFTPDE_OK) return s;
+    p->wave_valid = true;
+    p->wave_c = c;
+    p->wave_dt = dt;
+    return FFTPDE_OK;
+}
+
+fftpde_status copy_grids(fftpde_plan p, const void *src, void *dst, int64_t batch, int64_t stride)
+{
+    if (src == dst) return FFTPDE_OK;
+    DeviceGuard g(p->device);
+    const size_t ec = elem_cplx(p);
+    cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)stride * ec, src, (size_t)stride * ec,
+                                      (size_t)(p->nx * p->ny) * ec, (size_t)batch,
+                                      cudaMemcpyDeviceToDevice, p->stream);
+    return cuda_status(e);
+}
+
+} // namespace
+
+// ============================================================================
+extern "C" {
+
+const char *fftpde_status_string(fftpde_status s)
+{
+    switch (s) {
+    case FFTPDE_OK: return "ok";
+    case FFTPDE_ERR_INVALID_ARG: return "invalid argument";
+    case FFTPDE_ERR_EMPTY: return "empty input (zero-sized axis or batch)";
+    case FFTPDE_ERR_NOT_POW2_X: return "nx is not a power of two (radix-2 restriction)";
+    case FFTPDE_ERR_NOT_POW2_Y: return "ny is not a power of two (radix-2 restriction)";
+    case FFTPDE_ERR_UNSUPPORTED: return "unsupported size for this build";
+    case FFTPDE_ERR_WORKSPACE: return "workspace missing or too small";
+    case FFTPDE_ERR_CUDA: return "CUDA error";
+    case FFTPDE_ERR_NCCL: return "NCCL error";
+    }
+    return "unknown status";
+}
+
+fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t batch,
+                             fftpde_dtype dtype, double Lx, double Ly, int device)
+{
+    if (!plan) return FFTPDE_ERR_INVALID_ARG;
+    *plan = nullptr;
+    if (dtype != FFTPDE_C64 && dtype != FFTPDE_C128) return FFTPDE_ERR_INVALID_ARG;
+    if (nx == 0 || ny == 0 || batch == 0) return FFTPDE_ERR_EMPTY;
+    if (nx < 0 || ny < 0 || batch < 0) return FFTPDE_ERR_INVALID_ARG;
+    if (!is_pow2(nx)) return FFTPDE_ERR_NOT_POW2_X;
+    if (!is_pow2(ny)) return FFTPDE_ERR_NOT_POW2_Y;
+    if (nx > kMaxLen || ny > kMaxLen || batch > 65535) return FFTPDE_ERR_UNSUPPORTED;
+    if (!std::isfinite(Lx) || !std::isfinite(Ly) || !(Lx > 0) || !(Ly > 0)) return FFTPDE_ERR_INVALID_ARG;
+    if (device < 0) return FFTPDE_ERR_INVALID_ARG;
+
+    fftpde_plan p = new (std::nothrow) fftpde_plan_s;
+    if (!p) return FFTPDE_ERR_INVALID_ARG;
+    p->nx = nx; p->ny = ny; p->batch = batch; p->dtype = dtype;
+    p->Lx = Lx; p->Ly = Ly; p->device = device;
+    p->qx = nx / 2 + 1;
+    p->qy = ny / 2 + 1;
+    build_twiddles(nx, p->twx);
+    build_twiddles(ny, p->twy);
+    build_k2(nx, Lx, p->kx2);
+    build_k2(ny, Ly, p->ky2);
+
+    const size_t er = elem_real(p), ec = elem_cplx(p);
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return o; };
+    p->o_twx = take((size_t)nx * ec);
+    p->o_twy = take((size_t)ny * ec);
+    p->o_kx2 = take((size_t)nx * er);
+    p->o_ky2 = take((size_t)ny * er);
+    p->o_ex = take((size_t)nx * er);
+    p->o_ey = take((size_t)ny * er);
+    const size_t q = (size_t)(p->qx * p->qy) * er;
+    p->o_wc = take(q);
+    p->o_ws1 = take(q);
+    p->o_ws2 = take(q);
+    p->need = off;
+    *plan = p;
+    return FFTPDE_OK;
+}
+
+size_t fftpde_workspace_size(fftpde_plan plan) { return plan ? plan->need : 0; }
+
+fftpde_status fftpde_set_stream(fftpde_plan plan, void *cuda_stream)
+{
+    if (!plan) return FFTPDE_ERR_INVALID_ARG;
+    plan->stream = (cudaStream_t)cuda_stream;
+    return FFTPDE_OK;
+}
+
+fftpde_status fftpde_set_workspace(fftpde_plan plan, void *dev_ptr, size_t bytes)
+{
+    if (!plan || !dev_ptr) return FFTPDE_ERR_INVALID_ARG;
+    if (((uintptr_t)dev_ptr & 255u) != 0) return FFTPDE_ERR_INVALID_ARG;
+    if (bytes < plan->need) return FFTPDE_ERR_WORKSPACE;
+    DeviceGuard g(plan->device);
+    if (!g.ok) return FFTPDE_ERR_CUDA;
+    plan->ws = (unsigned char *)dev_ptr;
+    plan->ws_bytes = bytes;
+    plan->diff_valid = plan->wave_valid = false;
+    fftpde_status s;
+    cudaError_t e;
+    if (plan->dtype == FFTPDE_C128) {
+        e = cudaMemcpyAsync(plan->ws + plan->o_twx, plan->twx.data(), plan->twx.size() * 8,
+                            cudaMemcpyHostToDevice, plan->stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(plan->ws + plan->o_twy, plan->twy.data(), plan->twy.size() * 8,
+                                cudaMemcpyHostToDevice, plan->stream);
+        s = cuda_status(e);
+    } else {
+        s = upload(plan, plan->o_twx, plan->twx);
+        if (s == FFTPDE_OK) s = upload(plan, plan->o_twy, plan->twy);
+    }
+    if (s == FFTPDE_OK) s = upload(plan, plan->o_kx2, plan->kx2);
+    if (s == FFTPDE_OK) s = upload(plan, plan->o_ky2, plan->ky2);
+    if (s != FFTPDE_OK) plan->ws = nullptr;
+    return s;
+}
+
+fftpde_status fftpde_destroy(fftpde_plan plan)
+{
+    delete plan;
+    return FFTPDE_OK;
+}
+
+int64_t fftpde_launch_count(fftpde_plan plan) { return plan ? plan->launches : 0; }
+
+// ---- batched entry points ----------------------------------------------------
+fftpde_status fftpde_forward_batched(fftpde_plan p, const void *in, void *out, int64_t batch,
+                                     int64_t stride)
+{
+    fftpde_status s = check_call(p, batch, stride);
+    if (s == FFTPDE_OK) s = check_ptr(p, in);
+    if (s == FFTPDE_OK) s = check_ptr(p, out);
+    if (s != FFTPDE_OK) return s;
+    return dispatch(p, batch, stride, [&](auto &ps) { return ps.forward(in, out); });
+}
+
+fftpde_status fftpde_inverse_batched(fftpde_plan p, const void *in, void *out, int64_t batch,
+                                     int64_t stride)
+{
+    fftpde_status s = check_call(p, batch, stride);
+    if (s == FFTPDE_OK) s = check_ptr(p, in);
+    if (s == FFTPDE_OK) s = check_ptr(p, out);
+    if (s != FFTPDE_OK) return s;
+    return dispatch(p, batch, stride, [&](auto &ps) { return ps.inverse(in, out); });
+}
+
+fftpde_status fftpde_poisson_batched(fftpde_plan p, const void *rho, void *u, int64_t batch,
+                                     int64_t stride)
+{
+    fftpde_status s = check_call(p, batch, stride);
+    if (s == FFTPDE_OK) s = check_ptr(p, rho);
+    if (s == FFTPDE_OK) s = check_ptr(p, u);
+    if (s != FFTPDE_OK) return s;
+    return dispatch(p, batch, stride, [&](auto &ps) { return ps.solve_step(rho, u, COL_POISSON); });
+}
+
+fftpde_status fftpde_diffuse_batched(fftpde_plan p, const void *u0, void *u, int64_t batch,
+                                     int64_t stride, double D, double dt, int64_t nsteps)
+{
+    fftpde_status s = check_call(p, batch, stride);
+    if (s == FFTPDE_OK) s = check_ptr(p, u0);
+    if (s == FFTPDE_OK) s = check_ptr(p, u);
+    if (s != FFTPDE_OK) return s;
+    if (!std::isfinite(D) || !std::isfinite(dt) || D < 0 || dt < 0 || nsteps < 0)
+        return FFTPDE_ERR_INVALID_ARG;
+    if (nsteps == 0) return copy_grids(p, u0, u, batch, stride);
+    {
+        DeviceGuard g(p->device);
+        s = ensure_diffusion_tables(p, D, dt);
+    }
+    if (s != FFTPDE_OK) return s;
+    return dispatch(p, batch, stride, [&](auto &ps) {
+        cudaError_t e = cudaSuccess;
+        for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k)
+            e = ps.solve_step(k == 0 ? u0 : u, u, COL_DIFFUSE);
+        return e;
+    });
+}
+
+fftpde_status fftpde_wave_step_batched(fftpde_plan p, void *u, void *ut, int64_t batch,
+                                       int64_t stride, double c, double dt, int64_t nsteps)
+{
+    fftpde_status s = check_call(p, batch, stride);
+    if (s == FFTPDE_OK) s = check_ptr(p, u);
+    if (s == FFTPDE_OK) s = check_ptr(p, ut);
+    if (s != FFTPDE_OK) return s;
+    if (u == ut) return FFTPDE_ERR_INVALID_ARG;
+    if (!std::isfinite(c) || !std::isfinite(dt) || c < 0 || nsteps < 0) return FFTPDE_ERR_INVALID_ARG;
+    if (nsteps == 0) return FFTPDE_OK;
+    {
+        DeviceGuard g(p->device);
+        s = ensure_wave_tables(p, c, dt);
+    }
+    if (s != FFTPDE_OK) return s;
+    return dispatch(p, batch, stride, [&](auto &ps) { return ps.wave(u, ut, nsteps); });
+}
+
+// ---- whole-plan entry points --------------------------------------------------
+fftpde_status fftpde_forward(fftpde_plan p, const void *in, void *out)
+{
+    if (!p) return FFTPDE_ERR_INVALID_ARG;
+    return fftpde_forward_batched(p, in, out, p->batch, p->nx * p->ny);
+}
+fftpde_status fftpde_inverse(fftpde_plan p, const void *in, void *out)
+{
+    if (!p) return FFTPDE_ERR_INVALID_ARG;
+    return fftpde_inverse_batched(p, in, out, p->batch, p->nx * p->ny);
+}
+fftpde_status fftpde_poisson(fftpde_plan p, const void *rho, void *u)
+{
+    if (!p) return FFTPDE_ERR_INVALID_ARG;
+    return fftpde_poisson_batched(p, rho, u, p->batch, p->nx * p->ny);
+}
+fftpde_status fftpde_diffuse(fftpde_plan p, const void *u0, void *u, double D, double dt, int64_t nsteps)
+{
+    if (!p) return FFTPDE_ERR_INVALID_ARG;
+    return fftpde_diffuse_batched(p, u0, u, p->batch, p->nx * p->ny, D, dt, nsteps);
+}
+fftpde_status fftpde_wave_step(fftpde_plan p, void *u, void *ut, double c, double dt, int64_t nsteps)
+{
+    if (!p) return FFTPDE_ERR_INVALID_ARG;
+    return fftpde_wave_step_batched(p, u, ut, p->batch, p->nx * p->ny, c, dt, nsteps);
+}
+
+} // extern "C"

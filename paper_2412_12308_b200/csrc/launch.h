@@ -1,0 +1,47 @@
+// launch.h -- host-side launchers of the pass kernels (internal to libfftpde.so).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fftpde {
+
+enum ColOp { COL_FWD = 0, COL_INV = 1, COL_POISSON = 2, COL_DIFFUSE = 3 };
+
+// Device tables of the k-space multipliers; every multiplier includes the
+// 1/(nx ny) of the inverse transform (exact: a power of two).
+template <typename T> struct OpTables {
+    const T *kx2, *ky2;      // |k|^2 per axis: (2 pi fold(a)/L)^2          (Poisson)
+    const T *ex, *ey;        // exp(-D kx^2 dt)/(nx ny), exp(-D ky^2 dt)    (diffusion)
+    const T *wC, *wS1, *wS2; // wave quadrant tables [qa][qb], scale folded in
+    int64_t qpitch;          // ny/2 + 1
+    T scale;                 // 1/(nx ny)
+};
+
+constexpr int64_t kMaxLen = 8192;   // single-pass axis length limit of this build
+
+// Row transforms of `batch` grids: length n along x, ny rows per grid, grids
+// `stride` elements apart.  conj != 0 gives the inverse direction (unscaled).
+template <typename T>
+cudaError_t launch_rows(int64_t n, const void *in, void *out, int64_t ny, int64_t stride,
+                        int64_t batch, int conj, const void *tw, cudaStream_t st);
+
+// Column pass along y (length ny) over nx columns, op in ColOp.
+template <typename T>
+cudaError_t launch_cols(int64_t ny, const void *in, void *out, int64_t nx, int64_t stride,
+                        int64_t batch, int op, const void *tw, const OpTables<T> &tab,
+                        cudaStream_t st);
+
+// Wave column pass: both fields, in place.
+template <typename T>
+cudaError_t launch_wave_cols(int64_t ny, void *U, void *V, int64_t nx, int64_t stride,
+                             int64_t batch, const void *tw, const OpTables<T> &tab,
+                             cudaStream_t st);
+
+// Single-CTA whole-grid solve (small square grids).
+template <typename T> bool small_supported(int64_t nx, int64_t ny);
+template <typename T>
+cudaError_t launch_small(int64_t nx, int64_t ny, const void *in, void *out, int64_t stride,
+                         int64_t batch, int op, const void *twx, const void *twy,
+                         const OpTables<T> &tab, cudaStream_t st);
+
+} // namespace fftpde

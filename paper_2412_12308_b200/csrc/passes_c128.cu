@@ -1,0 +1,14 @@
+// passes_c128.cu -- instantiation unit of the pass launchers for c128 (double).
+#include "dispatch.cuh"
+
+namespace fftpde {
+template cudaError_t launch_rows<double>(int64_t, const void *, void *, int64_t, int64_t, int64_t, int,
+                                     const void *, cudaStream_t);
+template cudaError_t launch_cols<double>(int64_t, const void *, void *, int64_t, int64_t, int64_t, int,
+                                     const void *, const OpTables<double> &, cudaStream_t);
+template cudaError_t launch_wave_cols<double>(int64_t, void *, void *, int64_t, int64_t, int64_t,
+                                          const void *, const OpTables<double> &, cudaStream_t);
+template bool small_supported<double>(int64_t, int64_t);
+template cudaError_t launch_small<double>(int64_t, int64_t, const void *, void *, int64_t, int64_t, int,
+                                     const void *, const void *, const OpTables<double> &, cudaStream_t);
+} // namespace fftpde

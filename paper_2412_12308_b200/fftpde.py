@@ -1,0 +1,244 @@
+"""Thin ctypes binding of libfftpde.so (include/fftpde.h).
+
+Argument marshalling only: every step of the path runs in the library's sm_100a
+kernels.  PyTorch provides device memory (the workspace and outputs are torch
+tensors) and the stream (``torch.cuda.current_stream()``).  There is no CPU
+fallback: if the library or a CUDA device is missing, the calls raise.
+
+Tensors are ``[ny, nx]`` or ``[B, ny, nx]`` complex128 / complex64, C-contiguous,
+x fastest.  Inputs may live on the host (CPU tensors): they
+are staged through pinned memory to the plan's device and the result is copied
+back, all on the current stream (this is what bench.py's ``e2e`` times).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libfftpde.so")
+
+# fftpde_status
+OK, ERR_INVALID_ARG, ERR_EMPTY, ERR_NOT_POW2_X, ERR_NOT_POW2_Y, ERR_UNSUPPORTED, ERR_WORKSPACE, \
+    ERR_CUDA, ERR_NCCL = range(9)
+C64, C128 = 0, 1
+
+EXPORTS = [
+    "fftpde_plan_2d", "fftpde_workspace_size", "fftpde_set_workspace", "fftpde_set_stream",
+    "fftpde_destroy", "fftpde_status_string", "fftpde_launch_count",
+    "fftpde_forward", "fftpde_inverse", "fftpde_poisson", "fftpde_diffuse", "fftpde_wave_step",
+    "fftpde_forward_batched", "fftpde_inverse_batched", "fftpde_poisson_batched",
+    "fftpde_diffuse_batched", "fftpde_wave_step_batched",
+]
+
+
+class FFTPDEError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {status_string(status)} (status {status})")
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libfftpde.so (built in-tree by __graft_entry__.build()); raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"libfftpde.so not found at {path}: run __graft_entry__.build() "
+                           "(there is no CPU fallback)")
+    L = ctypes.CDLL(path)
+    p, i64, dbl, u = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
+    st = ctypes.c_int
+    sig = {
+        "fftpde_plan_2d": (st, [ctypes.POINTER(p), i64, i64, i64, u, dbl, dbl, u]),
+        "fftpde_workspace_size": (ctypes.c_size_t, [p]),
+        "fftpde_set_workspace": (st, [p, p, ctypes.c_size_t]),
+        "fftpde_set_stream": (st, [p, p]),
+        "fftpde_destroy": (st, [p]),
+        "fftpde_status_string": (ctypes.c_char_p, [st]),
+        "fftpde_launch_count": (i64, [p]),
+        "fftpde_forward": (st, [p, p, p]),
+        "fftpde_inverse": (st, [p, p, p]),
+        "fftpde_poisson": (st, [p, p, p]),
+        "fftpde_diffuse": (st, [p, p, p, dbl, dbl, i64]),
+        "fftpde_wave_step": (st, [p, p, p, dbl, dbl, i64]),
+        "fftpde_forward_batched": (st, [p, p, p, i64, i64]),
+        "fftpde_inverse_batched": (st, [p, p, p, i64, i64]),
+        "fftpde_poisson_batched": (st, [p, p, p, i64, i64]),
+        "fftpde_diffuse_batched": (st, [p, p, p, i64, i64, dbl, dbl, i64]),
+        "fftpde_wave_step_batched": (st, [p, p, p, i64, i64, dbl, dbl, i64]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def status_string(status: int) -> str:
+    return load_library().fftpde_status_string(status).decode()
+
+
+def _check(status: int, what: str):
+    if status != OK:
+        raise FFTPDEError(status, what)
+
+
+_DT = {torch.complex128: C128, torch.complex64: C64}
+
+
+class Plan:
+    """A 2D FFT-PDE plan for ``batch`` grids of ``ny x nx`` on [0,Lx) x [0,Ly).
+
+    Mirrors fftpde_plan_2d + workspace (a torch uint8 tensor) + stream."""
+
+    def __init__(self, nx: int, ny: int, batch: int = 1, dtype=torch.complex128,
+                 Lx: float = 1.0, Ly: float = 1.0, device=None):
+        if dtype not in _DT:
+            raise TypeError("dtype must be torch.complex128 or torch.complex64")
+        if not torch.cuda.is_available():
+            raise RuntimeError("fftpde needs a CUDA device (no CPU fallback)")
+        self.lib = load_library()
+        self.device = torch.device(device if device is not None else "cuda", )
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self.nx, self.ny, self.batch, self.dtype = int(nx), int(ny), int(batch), dtype
+        self.Lx, self.Ly = float(Lx), float(Ly)
+        h = ctypes.c_void_p()
+        _check(self.lib.fftpde_plan_2d(ctypes.byref(h), self.nx, self.ny, self.batch, _DT[dtype],
+                                       self.Lx, self.Ly, self.device.index), "fftpde_plan_2d")
+        self._h = h
+        nbytes = self.lib.fftpde_workspace_size(h)
+        self.workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        self._bind_stream()
+        _check(self.lib.fftpde_set_workspace(h, self.workspace.data_ptr(), self.workspace.numel()),
+               "fftpde_set_workspace")
+
+    # -- plumbing -----------------------------------------------------------------
+    def _bind_stream(self):
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        _check(self.lib.fftpde_set_stream(self._h, s), "fftpde_set_stream")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.fftpde_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.fftpde_launch_count(self._h))
+
+    def _grid(self, x: torch.Tensor, name: str):
+        if x.dtype != self.dtype:
+            raise TypeError(f"{name}: dtype {x.dtype} does not match the plan's {self.dtype}")
+        if x.dim() == 2:
+            B = 1
+        elif x.dim() == 3:
+            B = x.shape[0]
+        else:
+            raise ValueError(f"{name}: expected [ny, nx] or [B, ny, nx]")
+        if tuple(x.shape[-2:]) != (self.ny, self.nx):
+            raise ValueError(f"{name}: shape {tuple(x.shape)} does not match plan ({self.ny}, {self.nx})")
+        if B > self.batch:
+            raise ValueError(f"{name}: batch {B} exceeds the plan's {self.batch}")
+        return B
+
+    def _to_dev(self, x: torch.Tensor):
+        """(device tensor, was_host).  Host tensors go through pinned memory."""
+        if x.device.type == "cpu":
+            src = x.contiguous()
+            if not src.is_pinned():
+                src = src.pin_memory()
+            return src.to(self.device, non_blocking=True), True
+        if x.device != self.device:
+            raise ValueError(f"tensor on {x.device}, plan on {self.device}")
+        return x.contiguous(), False
+
+    def _finish(self, out_dev: torch.Tensor, host: bool):
+        if host:
+            out = torch.empty(out_dev.shape, dtype=out_dev.dtype, pin_memory=True)
+            out.copy_(out_dev, non_blocking=True)
+            torch.cuda.current_stream(self.device).synchronize()
+            return out
+        return out_dev
+
+    def _out(self, like: torch.Tensor, out):
+        if out is None:
+            return torch.empty_like(like)
+        if out.shape != like.shape or out.dtype != like.dtype or out.device != like.device \
+                or not out.is_contiguous():
+            raise ValueError("out: must be a contiguous tensor like the input on the plan's device")
+        return out
+
+    # -- transforms and solvers -----------------------------------------------------
+    def forward(self, x: torch.Tensor, out=None) -> torch.Tensor:
+        """DFT2 with the paper's + sign, unnormalised."""
+        B = self._grid(x, "x")
+        xd, host = self._to_dev(x)
+        o = self._out(xd, None if host else out)
+        self._bind_stream()
+        _check(self.lib.fftpde_forward_batched(self._h, xd.data_ptr(), o.data_ptr(), B,
+                                               self.nx * self.ny), "fftpde_forward")
+        return self._finish(o, host)
+
+    def inverse(self, X: torch.Tensor, out=None) -> torch.Tensor:
+        """iDFT2: conjugate kernel, times 1/(nx ny)."""
+        B = self._grid(X, "X")
+        xd, host = self._to_dev(X)
+        o = self._out(xd, None if host else out)
+        self._bind_stream()
+        _check(self.lib.fftpde_inverse_batched(self._h, xd.data_ptr(), o.data_ptr(), B,
+                                               self.nx * self.ny), "fftpde_inverse")
+        return self._finish(o, host)
+
+    def poisson(self, rho: torch.Tensor, out=None) -> torch.Tensor:
+        """u with nabla^2 u = rho - mean(rho), zero mean (eq:SolutionPoisson)."""
+        B = self._grid(rho, "rho")
+        rd, host = self._to_dev(rho)
+        o = self._out(rd, None if host else out)
+        self._bind_stream()
+        _check(self.lib.fftpde_poisson_batched(self._h, rd.data_ptr(), o.data_ptr(), B,
+                                               self.nx * self.ny), "fftpde_poisson")
+        return self._finish(o, host)
+
+    def diffuse(self, u0: torch.Tensor, D: float, dt: float, nsteps: int, out=None) -> torch.Tensor:
+        """nsteps exact diffusion steps exp(-D|k|^2 dt) (ec:solCalorFourier)."""
+        B = self._grid(u0, "u0")
+        ud, host = self._to_dev(u0)
+        o = self._out(ud, None if host else out)
+        self._bind_stream()
+        _check(self.lib.fftpde_diffuse_batched(self._h, ud.data_ptr(), o.data_ptr(), B,
+                                               self.nx * self.ny, float(D), float(dt), int(nsteps)),
+               "fftpde_diffuse")
+        return self._finish(o, host)
+
+    def wave_step(self, u: torch.Tensor, ut: torch.Tensor, c: float, dt: float, nsteps: int):
+        """nsteps exact wave steps on (u, ut) (eq:OmegaZero/NonZero).
+
+        Device tensors are updated in place and returned; host tensors are copied."""
+        B = self._grid(u, "u")
+        if self._grid(ut, "ut") != B:
+            raise ValueError("u and ut batch differ")
+        ud, host = self._to_dev(u)
+        vd, _ = self._to_dev(ut)
+        if not host and (ud.data_ptr() != u.data_ptr() or vd.data_ptr() != ut.data_ptr()):
+            raise ValueError("wave_step updates in place: pass contiguous device tensors")
+        self._bind_stream()
+        _check(self.lib.fftpde_wave_step_batched(self._h, ud.data_ptr(), vd.data_ptr(), B,
+                                                 self.nx * self.ny, float(c), float(dt), int(nsteps)),
+               "fftpde_wave_step")
+        if host:
+            return self._finish(ud, True), self._finish(vd, True)
+        return ud, vd

@@ -1,0 +1,248 @@
+"""Parity of the CUDA path (through the C-ABI binding) with the fp64 CPU oracle.
+
+Element-by-element relative L2 on the same seeded inputs.  Tolerances are
+BASELINE.json north_star's: 1e-12 for complex128, 1e-5 for complex64 (the
+complex64 input is upcast exactly for the oracle).  Needs a CUDA device.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2412_12308_b200 import fftpde as F
+from paper_2412_12308_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+C128, C64 = torch.complex128, torch.complex64
+TOL = {C128: 1e-12, C64: 1e-5}
+NP = {C128: np.complex128, C64: np.complex64}
+
+
+def rel(a, b):
+    a = np.asarray(a, np.complex128).ravel()
+    b = np.asarray(b, np.complex128).ravel()
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def dev(x, dtype=C128):
+    return torch.from_numpy(np.ascontiguousarray(x).astype(NP[dtype])).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy().astype(np.complex128)
+
+
+def noise(shape, seed, dtype=C128):
+    return I.white_noise(shape, seed, dtype=NP[dtype])
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    F.load_library()            # fails loudly if libfftpde.so is missing
+    torch.cuda.init()
+
+
+# ---------------------------------------------------------------- transforms
+
+def test_spec_examples_through_abi():
+    # SPEC.md:62-64 (eq:DFT, + sign) on a 1 x 4 grid, and the inverses SPEC.md:72-73
+    p = F.Plan(4, 1, dtype=C128)
+    cases = [([1, 1, 1, 1], [4, 0, 0, 0]), ([1, 0, 0, 0], [1, 1, 1, 1]), ([0, 1, 0, 0], [1, 1j, -1, -1j])]
+    for x, X in cases:
+        out = host(p.forward(dev(np.array([x], complex))))
+        assert np.max(np.abs(out - np.array([X]))) <= 1e-15
+        back = host(p.inverse(dev(np.array([X], complex))))
+        assert np.max(np.abs(back - np.array([x]))) <= 1e-15
+
+
+def _lengths():
+    return [2 ** k for k in range(0, 14)]
+
+
+@pytest.mark.parametrize("dtype", [C128, C64])
+@pytest.mark.parametrize("n", _lengths())
+def test_forward_inverse_every_length_both_axes(dtype, n):
+    # length n along y with a few x lengths, and along x with a few y lengths;
+    # batch 3 so CTAs span grid boundaries
+    for (ny, nx) in {(n, min(8192, max(1, 2 ** 18 // n))), (min(8192, max(1, 2 ** 18 // n)), n),
+                     (n, 2), (2, n)}:
+        B = 3 if nx * ny <= 2 ** 16 else 1
+        x = noise((B, ny, nx), 1000 + n + nx, dtype)
+        p = F.Plan(nx, ny, batch=B, dtype=dtype)
+        X = host(p.forward(dev(x, dtype)))
+        Xo = O.fft2(x.astype(np.complex128))
+        assert rel(X, Xo) <= TOL[dtype], (ny, nx)
+        xb = host(p.inverse(dev(Xo, dtype)))
+        assert rel(xb, O.fft2(Xo, inverse=True)) <= TOL[dtype], (ny, nx)
+
+
+@pytest.mark.parametrize("dtype", [C128, C64])
+def test_in_place_and_strided_batch(dtype):
+    ny, nx, B = 128, 256, 4
+    p = F.Plan(nx, ny, batch=B, dtype=dtype)
+    x = noise((B, ny, nx), 7, dtype)
+    t = dev(x, dtype)
+    p.forward(t, out=t)                                          # in place
+    assert rel(host(t), O.fft2(x.astype(np.complex128))) <= TOL[dtype]
+    # grids 'stride' elements apart inside a larger buffer
+    stride = nx * ny + 64
+    buf = torch.zeros(B * stride, dtype=dtype, device="cuda")
+    for b in range(B):
+        buf[b * stride: b * stride + nx * ny] = dev(x[b].ravel(), dtype)
+    st = p.lib.fftpde_poisson_batched(p._h, buf.data_ptr(), buf.data_ptr(), B, stride)
+    assert st == F.OK
+    got = host(buf)
+    ref = O.poisson(x.astype(np.complex128))
+    for b in range(B):
+        assert rel(got[b * stride: b * stride + nx * ny].reshape(ny, nx), ref[b]) <= TOL[dtype]
+        assert np.all(got[b * stride + nx * ny: (b + 1) * stride] == 0)   # gaps untouched
+
+
+# ---------------------------------------------------------------- C1 Poisson
+
+def test_c1_poisson_full():
+    d = I.c1_inputs(64)
+    p = F.Plan(64, 64, dtype=C128)
+    for part in (d.rho, d.rho_sin, d.rho_blobs):
+        u = host(p.poisson(dev(part)))
+        assert rel(u, O.poisson(part)) <= 1e-12
+        assert abs(u.mean()) <= 1e-14 * np.abs(u).max()
+    x = I.axis(64)
+    u = host(p.poisson(dev(d.rho_sin)))
+    assert rel(u, np.outer(np.sin(2 * np.pi * x), np.sin(2 * np.pi * x))) <= 1e-13
+
+
+@pytest.mark.parametrize("dtype", [C128, C64])
+@pytest.mark.parametrize("shape", [(1, 64), (64, 1), (2, 2), (16, 16), (32, 32), (64, 32), (32, 128),
+                                   (8, 1024), (512, 16)])
+def test_poisson_shapes(dtype, shape):
+    ny, nx = shape
+    Lx, Ly = 1.7, 0.6
+    x = noise((2, ny, nx), 11 + nx, dtype)
+    p = F.Plan(nx, ny, batch=2, dtype=dtype, Lx=Lx, Ly=Ly)
+    u = host(p.poisson(dev(x, dtype)))
+    assert rel(u, O.poisson(x.astype(np.complex128), Lx, Ly)) <= TOL[dtype]
+
+
+# ---------------------------------------------------------------- C2 diffusion
+
+def test_c2_diffusion_prefix_vs_stepped_oracle():
+    g = I.c2_inputs(1024)
+    p = F.Plan(1024, 1024, dtype=C128)
+    u = host(p.diffuse(dev(g.u0), 1e-3, 0.01, 20))
+    assert rel(u, O.diffuse(g.u0, 1e-3, 0.01, 20)) <= 1e-12
+
+
+def test_c2_diffusion_full_vs_collapsed_and_heat_kernel():
+    g = I.c2_inputs(1024)
+    p = F.Plan(1024, 1024, dtype=C128)
+    u = host(p.diffuse(dev(g.u0), 1e-3, 0.01, 200))
+    assert rel(u, O.diffuse(g.u0, 1e-3, 0.01, 200, collapsed=True)) <= 1e-12
+    # exact periodic heat kernel (closed form), T = 2
+    x = I.axis(1024)
+    exact = np.zeros((1024, 1024))
+    for (cx, cy), s, a in zip(g.centres, g.sigmas, g.amps):
+        s2 = s * s + 4e-3 * 2.0
+        gx = sum(np.exp(-(x - cx - m) ** 2 / s2) for m in range(-2, 3))
+        gy = sum(np.exp(-(x - cy - m) ** 2 / s2) for m in range(-2, 3))
+        exact += a * (s * s / s2) * np.outer(gy, gx)
+    assert rel(u, exact) <= 1e-12
+    assert abs(u.mean() / g.u0.mean() - 1) <= 1e-12               # Fig. 4
+
+
+@pytest.mark.parametrize("dtype", [C128, C64])
+def test_diffusion_shapes_and_zero_steps(dtype):
+    ny, nx = 64, 256
+    x = noise((3, ny, nx), 5, dtype)
+    p = F.Plan(nx, ny, batch=3, dtype=dtype, Lx=2.0, Ly=0.5)
+    u = host(p.diffuse(dev(x, dtype), 0.003, 0.02, 7))
+    assert rel(u, O.diffuse(x.astype(np.complex128), 0.003, 0.02, 7, 2.0, 0.5)) <= TOL[dtype]
+    t = dev(x, dtype)
+    u0 = host(p.diffuse(t, 0.003, 0.02, 0))
+    assert np.array_equal(u0, x.astype(np.complex128))           # nsteps = 0 copies
+
+
+# ---------------------------------------------------------------- C3 wave
+
+def test_c3_wave_prefix_vs_stepped_oracle():
+    w = I.c3_inputs(512)
+    p = F.Plan(512, 512, dtype=C128)
+    u, v = dev(w.u), dev(w.ut)
+    p.wave_step(u, v, 1.0, 1e-4 * 8, 50)
+    uo, vo = O.wave(w.u, w.ut, 1.0, 1e-4 * 8, 50)
+    assert rel(host(u), uo) <= 1e-12
+    assert rel(host(v), vo) <= 1e-12
+
+
+def test_c3_wave_full_vs_collapsed():
+    w = I.c3_inputs(4096)
+    p = F.Plan(4096, 4096, dtype=C128)
+    u, v = dev(w.u), dev(w.ut)
+    p.wave_step(u, v, 1.0, 1e-4, 500)
+    uo, vo = O.wave(w.u, w.ut, 1.0, 1e-4, 500, collapsed=True)
+    uh, vh = host(u), host(v)
+    assert rel(uh, uo) <= 1e-12
+    assert rel(vh, vo) <= 1e-12
+    # mean law of eq:OmegaZero with u_t(0) = 0 (Fig. 6)
+    assert abs(uh.mean() / w.u.mean() - 1) <= 1e-12
+
+
+@pytest.mark.parametrize("dtype", [C128, C64])
+def test_wave_shapes_reversal(dtype):
+    ny, nx = 128, 64
+    u0 = noise((2, ny, nx), 21, dtype)
+    v0 = noise((2, ny, nx), 22, dtype)
+    p = F.Plan(nx, ny, batch=2, dtype=dtype, Lx=1.3, Ly=0.9)
+    u, v = dev(u0, dtype), dev(v0, dtype)
+    p.wave_step(u, v, 0.7, 3e-3, 9)
+    uo, vo = O.wave(u0.astype(np.complex128), v0.astype(np.complex128), 0.7, 3e-3, 9, 1.3, 0.9)
+    assert rel(host(u), uo) <= TOL[dtype] and rel(host(v), vo) <= 4 * TOL[dtype]
+    p.wave_step(u, v, 0.7, -3e-3, 9)                              # time reversal
+    assert rel(host(u), u0) <= 10 * TOL[dtype]
+
+
+def test_wave_zero_speed_and_zero_steps():
+    ny, nx = 32, 32
+    u0, v0 = noise((ny, nx), 31), noise((ny, nx), 32)
+    p = F.Plan(nx, ny)
+    u, v = dev(u0), dev(v0)
+    p.wave_step(u, v, 0.0, 0.5, 3)                                # c = 0: u <- u + T v
+    assert rel(host(u), u0 + 1.5 * v0) <= 1e-13 and rel(host(v), v0) <= 1e-14
+    p.wave_step(u, v, 1.0, 0.5, 0)
+
+
+# ---------------------------------------------------------------- C4 batched Poisson
+
+def test_c4_batched_poisson_full_batch_sampled():
+    s = I.c4_inputs(512, 256)
+    p = F.Plan(512, 512, batch=256, dtype=C64)
+    u = p.poisson(dev(s, C64))
+    torch.cuda.synchronize()
+    for g in (0, 1, 77, 128, 200, 255):
+        ref = O.poisson(s[g].astype(np.complex128))
+        assert rel(u[g].cpu().numpy(), ref) <= 1e-5, g
+
+
+# ---------------------------------------------------------------- errors
+
+def test_errors_are_reported():
+    with pytest.raises(F.FFTPDEError) as e:
+        F.Plan(48, 64)
+    assert e.value.status == F.ERR_NOT_POW2_X
+    with pytest.raises(F.FFTPDEError) as e:
+        F.Plan(64, 96)
+    assert e.value.status == F.ERR_NOT_POW2_Y
+    with pytest.raises(F.FFTPDEError) as e:
+        F.Plan(64, 0)
+    assert e.value.status == F.ERR_EMPTY
+    p = F.Plan(64, 64)
+    with pytest.raises(F.FFTPDEError) as e:
+        p.diffuse(dev(noise((64, 64), 1)), -1.0, 0.1, 1)
+    assert e.value.status == F.ERR_INVALID_ARG
+    with pytest.raises(TypeError):
+        p.poisson(dev(noise((64, 64), 1), C64))
