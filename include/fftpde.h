@@ -28,7 +28,8 @@
  *   are returned as FFTPDE_ERR_CUDA; device faults surface at the caller's
  *   next synchronisation.
  * Aliasing: in == out is allowed everywhere; inputs are otherwise not written.
- * Alignment: device pointers must be 16-byte aligned (128-bit access).
+ * Alignment: device pointers must be aligned to one complex element
+ *   (16 B for FFTPDE_C128, 8 B for FFTPDE_C64).
  * Threads: one host thread per plan at a time; distinct plans are independent.
  */
 #ifndef FFTPDE_H
@@ -47,7 +48,7 @@ typedef enum { FFTPDE_C64 = 0, FFTPDE_C128 = 1 } fftpde_dtype;
 
 typedef enum {
     FFTPDE_OK = 0,
-    FFTPDE_ERR_INVALID_ARG = 1,  /* null pointer, bad dtype, non-finite/non-positive L, dt<0 (diffuse), nsteps<0, misaligned */
+    FFTPDE_ERR_INVALID_ARG = 1,  /* null pointer, bad dtype, non-finite/non-positive L, dt<0 (diffuse), nsteps<0, misaligned, stride < nx*ny */
     FFTPDE_ERR_EMPTY = 2,        /* a zero-sized axis or batch ("rejects empty input") */
     FFTPDE_ERR_NOT_POW2_X = 3,   /* nx not a power of two (radix-2 restriction) */
     FFTPDE_ERR_NOT_POW2_Y = 4,   /* ny not a power of two */
@@ -119,7 +120,7 @@ fftpde_status fftpde_wave_step(fftpde_plan plan, void *u, void *ut,
 
 /* ---- batched variants -------------------------------------------------------
  * Same semantics over `batch` grids (1 <= batch <= the plan's batch) whose
- * starts are `stride` elements apart (stride >= nx*ny, multiple of 8). */
+ * starts are `stride` elements apart (stride >= nx*ny). */
 fftpde_status fftpde_forward_batched(fftpde_plan plan, const void *in, void *out,
                                      int64_t batch, int64_t stride);
 fftpde_status fftpde_inverse_batched(fftpde_plan plan, const void *in, void *out,

@@ -148,11 +148,11 @@ template <typename T> OpTables<T> tables(fftpde_plan p)
     return t;
 }
 
+// element-aligned device pointer (16 B for complex128, 8 B for complex64)
 fftpde_status check_ptr(fftpde_plan p, const void *ptr)
 {
-    (void)p;
     if (!ptr) return FFTPDE_ERR_INVALID_ARG;
-    if (((uintptr_t)ptr & 15u) != 0) return FFTPDE_ERR_INVALID_ARG;
+    if (((uintptr_t)ptr % elem_cplx(p)) != 0) return FFTPDE_ERR_INVALID_ARG;
     return FFTPDE_OK;
 }
 
@@ -163,7 +163,6 @@ fftpde_status check_call(fftpde_plan p, int64_t batch, int64_t stride)
     if (batch == 0) return FFTPDE_ERR_EMPTY;
     if (batch < 0 || stride < p->nx * p->ny) return FFTPDE_ERR_INVALID_ARG;
     if (batch > p->batch) return FFTPDE_ERR_UNSUPPORTED;
-    if (batch > 1 && (stride % 8) != 0) return FFTPDE_ERR_INVALID_ARG;
     return FFTPDE_OK;
 }
 
