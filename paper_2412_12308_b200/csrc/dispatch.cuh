@@ -2,7 +2,9 @@
 // Included by the per-dtype instantiation units (passes_c128.cu, passes_c64.cu).
 #pragma once
 #include <atomic>
+#include <algorithm>
 #include "kernels.cuh"
+#include "pipe.cuh"
 
 namespace fftpde {
 
@@ -27,53 +29,85 @@ template <typename K> struct SmemOptIn {
 };
 
 // ---- launch shapes ---------------------------------------------------------
-// rows: ROWS rows per CTA so a CTA has >= 256 threads
-template <int N> struct RowCfg {
+
+// Persistent pipelined line pass: grid = resident CTAs (occupancy x SMs).
+template <typename T, int N, bool COLS> struct PipeCfg {
+    using C = typename cplx_t<T>::type;
     static constexpr int TPT = Shape<N>::TPT;
-    static constexpr int ROWS = TPT >= 256 ? 1 : 256 / TPT;
-};
-// columns: W adjacent columns per CTA (c128: 256 threads; c64: up to 512 threads
-// so that a row segment is >= 64 B)
-template <typename T, int N> struct ColCfg {
-    static constexpr int TPT = Shape<N>::TPT;
-    static constexpr int TARGET = sizeof(T) == 8 ? 256 : 512;
+    static constexpr int TARGET = (COLS && sizeof(T) == 4) ? 512 : 256;   // threads per CTA
     static constexpr int W = TPT >= TARGET ? 1 : TARGET / TPT;
+    static constexpr int NBUF = PipeSmem<C, N, W, COLS, 2>::BYTES <= 200 * 1024 ? 2 : 1;
+    // a persistent thread's twiddles stay in registers when the budget allows
+    static constexpr bool TWREG = W * TPT <= 256 && Shape<N>::STAGES <= 2;
+    using L = PipeSmem<C, N, W, COLS, NBUF>;
 };
+
+inline int sm_count()
+{
+    static std::atomic<int> cached{0};
+    int v = cached.load();
+    if (v) return v;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+    cached.store(v);
+    return v;
+}
+
+template <typename T, int N, bool COLS, int OP>
+cudaError_t pipe_n(const void *in, void *out, PipeArgs args, const void *tw, const OpTables<T> &tab,
+                   cudaStream_t st)
+{
+    using C = typename cplx_t<T>::type;
+    using Cfg = PipeCfg<T, N, COLS>;
+    constexpr int W = Cfg::W;
+    constexpr int THREADS = W * Shape<N>::TPT;
+    const size_t smem = Cfg::L::BYTES;
+    auto k = pipe_kernel<T, N, W, COLS, OP, Cfg::NBUF, 1, Cfg::TWREG>;
+    static SmemOptIn<decltype(k)> opt;
+    cudaError_t e = opt(k, smem);
+    if (e != cudaSuccess) return e;
+    static std::atomic<int> per_sm{0};
+    int occ = per_sm.load();
+    if (!occ) {
+        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, THREADS, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+        per_sm.store(occ);
+    }
+    args.groups = (args.nlines + W - 1) / W;
+    const int64_t batch = args.ntiles;                  // caller passes the batch here
+    args.ntiles = batch * args.groups;
+    const int64_t grid = std::min<int64_t>(args.ntiles, (int64_t)occ * sm_count());
+    k<<<(unsigned)grid, THREADS, smem, st>>>((const C *)in, (C *)out, args, (const C *)tw, tab);
+    return cudaGetLastError();
+}
 
 template <typename T, int N>
 cudaError_t rows_n(const void *in, void *out, int64_t ny, int64_t stride, int64_t batch,
                    int conj, const void *tw, cudaStream_t st)
 {
-    using C = typename cplx_t<T>::type;
-    constexpr int ROWS = RowCfg<N>::ROWS;
-    constexpr int THREADS = ROWS * Shape<N>::TPT;
-    const size_t smem = (size_t)ROWS * Shape<N>::PADDED * sizeof(C);
-    auto k = row_fft_kernel<T, N, ROWS>;
-    static SmemOptIn<decltype(k)> opt;
-    cudaError_t e = opt(k, smem);
-    if (e != cudaSuccess) return e;
-    const int64_t total = batch * ny;
-    const int64_t grid = (total + ROWS - 1) / ROWS;
-    k<<<(unsigned)grid, THREADS, smem, st>>>((const C *)in, (C *)out, ny, stride, total, conj,
-                                             (const C *)tw);
-    return cudaGetLastError();
+    PipeArgs a{ny, N, 1, stride, batch, 0, conj ? PIPE_INV : PIPE_FWD};
+    OpTables<T> tab{};
+    tab.scale = (T)1;
+    if (conj) return pipe_n<T, N, false, PIPE_INV>(in, out, a, tw, tab, st);
+    return pipe_n<T, N, false, PIPE_FWD>(in, out, a, tw, tab, st);
 }
 
 template <typename T, int N>
 cudaError_t cols_n(const void *in, void *out, int64_t nx, int64_t stride, int64_t batch, int op,
                    const void *tw, const OpTables<T> &tab, cudaStream_t st)
 {
-    using C = typename cplx_t<T>::type;
-    constexpr int W = ColCfg<T, N>::W;
-    constexpr int THREADS = W * Shape<N>::TPT;
-    const size_t smem = ColSmem<C, N, W>::BYTES;
-    auto k = col_fused_kernel<T, N, W>;
-    static SmemOptIn<decltype(k)> opt;
-    cudaError_t e = opt(k, smem);
-    if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)((nx + W - 1) / W), (unsigned)batch);
-    k<<<grid, THREADS, smem, st>>>((const C *)in, (C *)out, nx, stride, op, (const C *)tw, tab);
-    return cudaGetLastError();
+    PipeArgs a{nx, 1, nx, stride, batch, 0, op};
+    switch (op) {
+    case COL_FWD: return pipe_n<T, N, true, PIPE_FWD>(in, out, a, tw, tab, st);
+    case COL_INV: return pipe_n<T, N, true, PIPE_INV_SCALED>(in, out, a, tw, tab, st);
+    case COL_POISSON: return pipe_n<T, N, true, PIPE_POISSON>(in, out, a, tw, tab, st);
+    case COL_DIFFUSE: return pipe_n<T, N, true, PIPE_DIFFUSE>(in, out, a, tw, tab, st);
+    default: return cudaErrorInvalidValue;
+    }
 }
 
 template <typename T, int N>
@@ -93,19 +127,32 @@ cudaError_t wave_cols_n(void *U, void *V, int64_t nx, int64_t stride, int64_t ba
     return cudaGetLastError();
 }
 
+template <typename T, int N, int OP>
+cudaError_t small_op_n(const void *in, void *out, int64_t stride, int64_t batch, const void *twx,
+                       const void *twy, const OpTables<T> &tab, cudaStream_t st)
+{
+    using C = typename cplx_t<T>::type;
+    using L = SmallLayout<C, N, N>;
+    auto k = small_solve_kernel<T, N, N, OP>;
+    static SmemOptIn<decltype(k)> opt;
+    cudaError_t e = opt(k, L::BYTES);
+    if (e != cudaSuccess) return e;
+    k<<<(unsigned)batch, L::THREADS, L::BYTES, st>>>((const C *)in, (C *)out, stride,
+                                                      (const C *)twx, (const C *)twy, tab);
+    return cudaGetLastError();
+}
+
 template <typename T, int N>
 cudaError_t small_n(const void *in, void *out, int64_t stride, int64_t batch, int op,
                     const void *twx, const void *twy, const OpTables<T> &tab, cudaStream_t st)
 {
-    using C = typename cplx_t<T>::type;
-    using L = SmallLayout<C, N, N>;
-    auto k = small_solve_kernel<T, N, N>;
-    static SmemOptIn<decltype(k)> opt;
-    cudaError_t e = opt(k, L::BYTES);
-    if (e != cudaSuccess) return e;
-    k<<<(unsigned)batch, L::THREADS, L::BYTES, st>>>((const C *)in, (C *)out, stride, op,
-                                                      (const C *)twx, (const C *)twy, tab);
-    return cudaGetLastError();
+    switch (op) {
+    case COL_FWD: return small_op_n<T, N, COL_FWD>(in, out, stride, batch, twx, twy, tab, st);
+    case COL_INV: return small_op_n<T, N, COL_INV>(in, out, stride, batch, twx, twy, tab, st);
+    case COL_POISSON: return small_op_n<T, N, COL_POISSON>(in, out, stride, batch, twx, twy, tab, st);
+    case COL_DIFFUSE: return small_op_n<T, N, COL_DIFFUSE>(in, out, stride, batch, twx, twy, tab, st);
+    default: return cudaErrorInvalidValue;
+    }
 }
 
 // ---- length dispatch -------------------------------------------------------

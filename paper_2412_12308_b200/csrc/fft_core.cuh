@@ -1,10 +1,12 @@
 // fft_core.cuh -- register-resident Stockham FFT building blocks for sm_100a.
 //
 // What is computed (PAPER.md = the paper's LaTeX source):
-//   P_k = sum_j p_j w_N^{jk}, w_N = e^{+2 pi i/N}   (eq:DFT)
-// i.e. the paper's forward sign.  The inverse is conj(FFT(conj(P))) / N
-// (PAPER.md:157-159): callers conjugate on load/store and fold 1/N into the
-// k-space multiplier.
+//   forward  P_k = sum_j p_j w_N^{+jk}, w_N = e^{2 pi i/N}   (eq:DFT)
+//   inverse  p_j = sum_k P_k w_N^{-jk}  (the iDFT kernel of PAPER.md:151-153; the
+//            1/N is folded into the caller's k-space multiplier)
+// The direction is a compile-time flag: the inverse uses the conjugate radix
+// kernels and conjugate twiddles, which costs the same instructions as the
+// forward (no conjugation passes).
 //
 // How (not the paper's recursive radix-2 text, which is prior art, but the
 // same result): a self-sorting Stockham factorisation N = E^s * r with radix
@@ -12,8 +14,8 @@
 // exchange through shared memory between stages.  Thread t of a transform
 // holds x[t + TPT*e] (e < E, TPT = N/E threads) on entry and X[t + TPT*e] on
 // exit, so global loads and stores are unit-stride across threads.
-// Twiddles come from a per-length table w_N^m (m < N) computed on the host in
-// fp64 per index (never by recurrence) and rounded once to fp32 for c64.
+// Twiddles come from a stage-major table computed on the host in fp64 per
+// index (never by recurrence) and rounded once to fp32 for complex64.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -26,31 +28,40 @@ template <> struct cplx_t<float> { using type = float2; };
 
 template <typename C> __device__ __forceinline__ C cadd(C a, C b) { return {a.x + b.x, a.y + b.y}; }
 template <typename C> __device__ __forceinline__ C csub(C a, C b) { return {a.x - b.x, a.y - b.y}; }
-// a * i
-template <typename C> __device__ __forceinline__ C cmul_i(C a) { return {-a.y, a.x}; }
 template <typename C> __device__ __forceinline__ C cconj(C a) { return {a.x, -a.y}; }
-template <typename C> __device__ __forceinline__ C cmul(C a, C w)
-{
-    return {a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x};
-}
 template <typename C, typename T> __device__ __forceinline__ C cscale(C a, T s) { return {a.x * s, a.y * s}; }
 
-// multiply by w_8 = (1+i)/sqrt2 and w_8^3 = (-1+i)/sqrt2
-template <typename C> __device__ __forceinline__ C cmul_w8(C a)
+// a * w (forward) or a * conj(w) (inverse)
+template <bool INV, typename C> __device__ __forceinline__ C cmulw(C a, C w)
 {
-    using T = decltype(a.x);
-    const T h = (T)0.70710678118654752440084436210485;
-    return {(a.x - a.y) * h, (a.x + a.y) * h};
+    if constexpr (!INV) return {a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x};
+    else return {a.x * w.x + a.y * w.y, a.y * w.x - a.x * w.y};
 }
-template <typename C> __device__ __forceinline__ C cmul_w83(C a)
+// a * i^{+1} (forward) or a * i^{-1} (inverse)
+template <bool INV, typename C> __device__ __forceinline__ C cmul_i(C a)
+{
+    if constexpr (!INV) return {-a.y, a.x};
+    else return {a.y, -a.x};
+}
+// a * w_8^{+-1} = a (1 +- i)/sqrt2
+template <bool INV, typename C> __device__ __forceinline__ C cmul_w8(C a)
 {
     using T = decltype(a.x);
     const T h = (T)0.70710678118654752440084436210485;
-    return {-(a.x + a.y) * h, (a.x - a.y) * h};
+    if constexpr (!INV) return {(a.x - a.y) * h, (a.x + a.y) * h};
+    else return {(a.x + a.y) * h, (a.y - a.x) * h};
+}
+// a * w_8^{+-3} = a (-1 +- i)/sqrt2
+template <bool INV, typename C> __device__ __forceinline__ C cmul_w83(C a)
+{
+    using T = decltype(a.x);
+    const T h = (T)0.70710678118654752440084436210485;
+    if constexpr (!INV) return {-(a.x + a.y) * h, (a.x - a.y) * h};
+    else return {(a.y - a.x) * h, -(a.x + a.y) * h};
 }
 
 // ---------------------------------------------------------------------------
-// Small DFTs with the + sign, in place, natural order in and out.
+// Small DFTs X_k = sum_n a_n w_R^{+-nk}, in place, natural order in and out.
 
 template <typename C> __device__ __forceinline__ void dft2(C &a0, C &a1)
 {
@@ -59,26 +70,25 @@ template <typename C> __device__ __forceinline__ void dft2(C &a0, C &a1)
     a1 = csub(t, a1);
 }
 
-// X_k = sum_n a_n i^{nk}
-template <typename C> __device__ __forceinline__ void dft4(C &a0, C &a1, C &a2, C &a3)
+template <bool INV, typename C> __device__ __forceinline__ void dft4(C &a0, C &a1, C &a2, C &a3)
 {
-    C t0 = cadd(a0, a2), t1 = csub(a0, a2), t2 = cadd(a1, a3), t3 = cmul_i(csub(a1, a3));
+    C t0 = cadd(a0, a2), t1 = csub(a0, a2), t2 = cadd(a1, a3), t3 = cmul_i<INV>(csub(a1, a3));
     a0 = cadd(t0, t2);
     a2 = csub(t0, t2);
     a1 = cadd(t1, t3);
     a3 = csub(t1, t3);
 }
 
-// radix-8 as 2 x 4: n = 4 n1 + n2, k = k1 + 2 k2
-template <typename C> __device__ __forceinline__ void dft8(C (&v)[8])
+// radix-8 as 2 x 4: n = 4 n1 + n2, k = k1 + 2 k2, internal twiddle w_8^{n2 k1}
+template <bool INV, typename C> __device__ __forceinline__ void dft8(C (&v)[8])
 {
 #pragma unroll
     for (int n2 = 0; n2 < 4; ++n2) dft2(v[n2], v[n2 + 4]);   // Y[n2][k1] at v[n2 + 4 k1]
-    v[5] = cmul_w8(v[5]);
-    v[6] = cmul_i(v[6]);
-    v[7] = cmul_w83(v[7]);
-    dft4(v[0], v[1], v[2], v[3]);                          // k1 = 0 -> X[2 k2]     at v[k2]
-    dft4(v[4], v[5], v[6], v[7]);                          // k1 = 1 -> X[1 + 2 k2] at v[4 + k2]
+    v[5] = cmul_w8<INV>(v[5]);
+    v[6] = cmul_i<INV>(v[6]);
+    v[7] = cmul_w83<INV>(v[7]);
+    dft4<INV>(v[0], v[1], v[2], v[3]);                     // k1 = 0 -> X[2 k2]     at v[k2]
+    dft4<INV>(v[4], v[5], v[6], v[7]);                     // k1 = 1 -> X[1 + 2 k2] at v[4 + k2]
     C o[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) o[k] = v[4 * (k % 2) + k / 2];
@@ -87,26 +97,26 @@ template <typename C> __device__ __forceinline__ void dft8(C (&v)[8])
 }
 
 // radix-16 as 4 x 4: n = 4 n1 + n2, k = k1 + 4 k2, internal twiddle w16^{n2 k1}
-template <typename C> __device__ __forceinline__ void dft16(C (&v)[16])
+template <bool INV, typename C> __device__ __forceinline__ void dft16(C (&v)[16])
 {
     using T = decltype(v[0].x);
     const T c1 = (T)0.92387953251128675612818318939679;   // cos(pi/8)
     const T s1 = (T)0.38268343236508977172845998403040;   // sin(pi/8)
 #pragma unroll
-    for (int n2 = 0; n2 < 4; ++n2) dft4(v[n2], v[n2 + 4], v[n2 + 8], v[n2 + 12]);
+    for (int n2 = 0; n2 < 4; ++n2) dft4<INV>(v[n2], v[n2 + 4], v[n2 + 8], v[n2 + 12]);
     // v[n2 + 4 k1] = Y[n2][k1]; multiply by w16^{n2 k1}
     const C w1 = {c1, s1}, w3 = {s1, c1}, w9 = {-c1, -s1};
-    v[5] = cmul(v[5], w1);          // n2=1,k1=1: w^1
-    v[6] = cmul_w8(v[6]);           // n2=2,k1=1: w^2
-    v[7] = cmul(v[7], w3);          // n2=3,k1=1: w^3
-    v[9] = cmul_w8(v[9]);           // n2=1,k1=2: w^2
-    v[10] = cmul_i(v[10]);          // n2=2,k1=2: w^4
-    v[11] = cmul_w83(v[11]);        // n2=3,k1=2: w^6
-    v[13] = cmul(v[13], w3);        // n2=1,k1=3: w^3
-    v[14] = cmul_w83(v[14]);        // n2=2,k1=3: w^6
-    v[15] = cmul(v[15], w9);        // n2=3,k1=3: w^9
+    v[5] = cmulw<INV>(v[5], w1);     // n2=1,k1=1: w^1
+    v[6] = cmul_w8<INV>(v[6]);       // n2=2,k1=1: w^2
+    v[7] = cmulw<INV>(v[7], w3);     // n2=3,k1=1: w^3
+    v[9] = cmul_w8<INV>(v[9]);       // n2=1,k1=2: w^2
+    v[10] = cmul_i<INV>(v[10]);      // n2=2,k1=2: w^4
+    v[11] = cmul_w83<INV>(v[11]);    // n2=3,k1=2: w^6
+    v[13] = cmulw<INV>(v[13], w3);   // n2=1,k1=3: w^3
+    v[14] = cmul_w83<INV>(v[14]);    // n2=2,k1=3: w^6
+    v[15] = cmulw<INV>(v[15], w9);   // n2=3,k1=3: w^9
 #pragma unroll
-    for (int k1 = 0; k1 < 4; ++k1) dft4(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+    for (int k1 = 0; k1 < 4; ++k1) dft4<INV>(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
     C o[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) o[k] = v[4 * (k % 4) + k / 4];
@@ -114,17 +124,14 @@ template <typename C> __device__ __forceinline__ void dft16(C (&v)[16])
     for (int k = 0; k < 16; ++k) v[k] = o[k];
 }
 
-template <int R, typename C> __device__ __forceinline__ void dft_r(C (&v)[R]);
-template <> __device__ __forceinline__ void dft_r<1, double2>(double2 (&)[1]) {}
-template <> __device__ __forceinline__ void dft_r<1, float2>(float2 (&)[1]) {}
-template <> __device__ __forceinline__ void dft_r<2, double2>(double2 (&v)[2]) { dft2(v[0], v[1]); }
-template <> __device__ __forceinline__ void dft_r<2, float2>(float2 (&v)[2]) { dft2(v[0], v[1]); }
-template <> __device__ __forceinline__ void dft_r<4, double2>(double2 (&v)[4]) { dft4(v[0], v[1], v[2], v[3]); }
-template <> __device__ __forceinline__ void dft_r<4, float2>(float2 (&v)[4]) { dft4(v[0], v[1], v[2], v[3]); }
-template <> __device__ __forceinline__ void dft_r<8, double2>(double2 (&v)[8]) { dft8(v); }
-template <> __device__ __forceinline__ void dft_r<8, float2>(float2 (&v)[8]) { dft8(v); }
-template <> __device__ __forceinline__ void dft_r<16, double2>(double2 (&v)[16]) { dft16(v); }
-template <> __device__ __forceinline__ void dft_r<16, float2>(float2 (&v)[16]) { dft16(v); }
+template <int R, bool INV, typename C> __device__ __forceinline__ void dft_r(C (&v)[R])
+{
+    if constexpr (R == 2) dft2(v[0], v[1]);
+    else if constexpr (R == 4) dft4<INV>(v[0], v[1], v[2], v[3]);
+    else if constexpr (R == 8) dft8<INV>(v);
+    else if constexpr (R == 16) dft16<INV>(v);
+    else static_assert(R == 1, "radix");
+}
 
 // ---------------------------------------------------------------------------
 // Compile-time shape of one length-N transform.
@@ -139,6 +146,13 @@ template <int N_> struct Shape {
     static constexpr int STAGES = []() { int ns = 1, s = 0; while (ns * E < N_) { ns *= E; ++s; } return s; }();
     static constexpr int NS_LAST = []() { int ns = 1; while (ns * E < N_) ns *= E; return ns; }();
     static constexpr int R_LAST = N_ / NS_LAST;
+    // Stage-major twiddle table (built on the host by the same rule): for each
+    // middle stage s >= 1 (Ns = E^s) the block tw[m Ns + k] = w_{Ns E}^{m k},
+    // m < E, k < Ns; then the last stage tw[m NS_LAST + j] = w_N^{m j}, m < R_LAST.
+    // Threads of a warp have consecutive k (or j), so every twiddle load of a
+    // warp reads one contiguous run: coalesced, 4 lines per instruction.
+    static constexpr int TW_LAST_OFF = []() { int ns = E, off = 0; while (ns * E < N_) { off += E * ns; ns *= E; } return off; }();
+    static constexpr int TW_SIZE = NS_LAST > 1 ? TW_LAST_OFF + R_LAST * NS_LAST : 0;
 };
 
 // Twiddle load through the read-only path.  volatile: one load per use, so the
@@ -187,13 +201,61 @@ template <typename C, int LOGE, int STRIDE> struct SmemView {
     __device__ __forceinline__ C &at(int p) const { return base[padidx(p, LOGE) * STRIDE]; }
 };
 
-// Forward FFT (+ sign) of one length-N sequence held as v[e] = x[t + TPT e].
-// On exit v[e] = X[t + TPT e].  `sync` synchronises all threads that share the
-// smem buffers (warp or CTA); smem is free again when this returns.
-// tw: device table w_N^m, m in [0, N).
-template <int N, typename C, typename View, typename Sync>
-__device__ __forceinline__ void fft_forward(C (&v)[Shape<N>::E], const View &sm, int t,
-                                            const C *__restrict__ tw, Sync sync)
+// Twiddle providers.  mid(s, m) is w_{Ns E}^{m k} of middle stage s >= 1
+// (k = t mod Ns), last(q, m) is w_N^{m j} of the last stage (j = t + q TPT),
+// both read from the stage-major table of Shape<N>.  TwL1 loads each twiddle
+// at its use (L1-resident table); TwReg loads a thread's twiddles once (a
+// persistent kernel reuses them for every line it transforms).
+template <int N, typename C> struct TwL1 {
+    const C *tw;
+    int t;
+    __device__ __forceinline__ C mid(int s, int m) const
+    {
+        using S = Shape<N>;
+        int ns = S::E, off = 0;
+#pragma unroll
+        for (int i = 1; i < s; ++i) { off += S::E * ns; ns *= S::E; }
+        return ldtw(tw + off + opaque(t & (ns - 1)) + m * ns);
+    }
+    __device__ __forceinline__ C last(int q, int m) const
+    {
+        using S = Shape<N>;
+        return ldtw(tw + S::TW_LAST_OFF + opaque(t + q * S::TPT) + m * S::NS_LAST);
+    }
+};
+
+template <int N, typename C> struct TwReg {
+    using S = Shape<N>;
+    static constexpr int NMID = S::STAGES > 1 ? (S::STAGES - 1) * (S::E - 1) : 1;
+    static constexpr int Q = S::E / S::R_LAST;
+    static constexpr int NLAST = S::R_LAST > 1 ? Q * (S::R_LAST - 1) : 1;
+    C wm[NMID];
+    C wl[NLAST];
+    __device__ __forceinline__ void load(const C *tw, int t)
+    {
+        TwL1<N, C> l{tw, t};
+#pragma unroll
+        for (int s = 1; s < S::STAGES; ++s)
+#pragma unroll
+            for (int m = 1; m < S::E; ++m) wm[(s - 1) * (S::E - 1) + m - 1] = l.mid(s, m);
+        if (S::NS_LAST > 1) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+                for (int m = 1; m < S::R_LAST; ++m) wl[q * (S::R_LAST - 1) + m - 1] = l.last(q, m);
+        }
+    }
+    __device__ __forceinline__ C mid(int s, int m) const { return wm[(s - 1) * (S::E - 1) + m - 1]; }
+    __device__ __forceinline__ C last(int q, int m) const { return wl[q * (S::R_LAST - 1) + m - 1]; }
+};
+
+// Transform of one length-N sequence held as v[e] = x[t + TPT e]; on exit
+// v[e] = X[t + TPT e].  INV selects the conjugate kernel (inverse direction,
+// unscaled).  `sync` synchronises the threads sharing the exchange buffer
+// (warp, line or CTA); the buffer is free again when this returns.
+template <int N, bool INV, typename C, typename View, typename Tw, typename Sync>
+__device__ __forceinline__ void fft_tw(C (&v)[Shape<N>::E], const View &sm, int t, const Tw &tw,
+                                       Sync sync)
 {
     using S = Shape<N>;
     constexpr int E = S::E, TPT = S::TPT;
@@ -202,11 +264,10 @@ __device__ __forceinline__ void fft_forward(C (&v)[Shape<N>::E], const View &sm,
     for (int s = 0; s < S::STAGES; ++s) {
         const int k = t & (Ns - 1);
         if (s > 0) {
-            const int step = opaque((N / (Ns * E)) * k);   // twiddle w_{Ns E}^{m k} = w_N^{m k N/(Ns E)}
 #pragma unroll
-            for (int m = 1; m < E; ++m) v[m] = cmul(v[m], ldtw(&tw[m * step]));
+            for (int m = 1; m < E; ++m) v[m] = cmulw<INV>(v[m], tw.mid(s, m));
         }
-        dft_r<E>(v);
+        dft_r<E, INV>(v);
         // scatter X_m of butterfly t to (t / Ns) Ns E + k + m Ns; base or m Ns is a multiple of E
         C *wp = sm.ptr((t - k) * E + k);
 #pragma unroll
@@ -233,14 +294,21 @@ __device__ __forceinline__ void fft_forward(C (&v)[Shape<N>::E], const View &sm,
 #pragma unroll
         for (int m = 0; m < R; ++m) u[m] = v[q + m * Q];
         if (S::NS_LAST > 1) {
-            const int j = opaque(t + q * TPT);          // twiddle w_N^{m j}
 #pragma unroll
-            for (int m = 1; m < R; ++m) u[m] = cmul(u[m], ldtw(&tw[m * j]));
+            for (int m = 1; m < R; ++m) u[m] = cmulw<INV>(u[m], tw.last(q, m));
         }
-        dft_r<R>(u);
+        dft_r<R, INV>(u);
 #pragma unroll
         for (int m = 0; m < R; ++m) v[q + m * Q] = u[m];
     }
+}
+
+// Twiddles loaded from the table at each use.
+template <int N, bool INV, typename C, typename View, typename Sync>
+__device__ __forceinline__ void fft(C (&v)[Shape<N>::E], const View &sm, int t,
+                                    const C *__restrict__ tw, Sync sync)
+{
+    fft_tw<N, INV>(v, sm, t, TwL1<N, C>{tw, t}, sync);
 }
 
 struct SyncCTA { __device__ __forceinline__ void operator()() const { __syncthreads(); } };

@@ -72,10 +72,31 @@ void unit_root(int64_t n, int64_t m, double &re, double &im)
     im = (double)s;
 }
 
+// Stage-major twiddle table of the Stockham factorisation n = E^s * R used by
+// the kernels (fft_core.cuh Shape<n>): per middle stage (Ns = E, E^2, ...)
+// w_{Ns E}^{m k} at [m Ns + k]; then the last stage w_n^{m j} at [m Ns_last + j].
+// Each entry is w_M^q = w_n^{q n / M}, evaluated directly from its index.
 void build_twiddles(int64_t n, std::vector<double> &tw)
 {
-    tw.resize(2 * (size_t)n);
-    for (int64_t m = 0; m < n; ++m) unit_root(n, m, tw[2 * m], tw[2 * m + 1]);
+    const int64_t E = n < 16 ? n : 16;
+    tw.clear();
+    auto put = [&](int64_t M, int64_t q) {
+        double re, im;
+        unit_root(M, q, re, im);
+        tw.push_back(re);
+        tw.push_back(im);
+    };
+    int64_t ns = 1;
+    while (ns * E < n) {
+        if (ns > 1)
+            for (int64_t m = 0; m < E; ++m)
+                for (int64_t k = 0; k < ns; ++k) put(ns * E, m * k);
+        ns *= E;
+    }
+    if (ns > 1)
+        for (int64_t m = 0; m < n / ns; ++m)
+            for (int64_t j = 0; j < ns; ++j) put(n, m * j);
+    if (tw.empty()) { tw.push_back(1.0); tw.push_back(0.0); }
 }
 
 // (2 pi fold(a) / L)^2, fold(a) = a for a <= n/2 else a - n
@@ -355,8 +376,8 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     const size_t er = elem_real(p), ec = elem_cplx(p);
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return o; };
-    p->o_twx = take((size_t)nx * ec);
-    p->o_twy = take((size_t)ny * ec);
+    p->o_twx = take(p->twx.size() / 2 * ec);
+    p->o_twy = take(p->twy.size() / 2 * ec);
     p->o_kx2 = take((size_t)nx * er);
     p->o_ky2 = take((size_t)ny * er);
     p->o_ex = take((size_t)nx * er);

@@ -1,26 +1,18 @@
-// kernels.cuh -- pass kernels of the 2D FFT-PDE hot path (sm_100a).
+// kernels.cuh -- wave column pass and single-CTA small-grid solve (sm_100a).
 //
-// A solve step is three HBM passes:
-//   row_fft      : forward transform along x of every row
-//   col_fused    : forward transform along y of W adjacent columns, the k-space
-//                  operator (with 1/(nx ny) folded in), inverse transform along y
-//                  (PAPER.md:266-273 + eq:SolutionPoisson / solCalorFourier /
-//                  eq:OmegaZero-NonZero)
-//   row_fft      : inverse transform along x (conjugate in/out)
-// and a single-CTA kernel (small_solve) keeps a whole small grid in shared
-// memory for one HBM round trip (C1).
+// The row passes and the Poisson/diffusion column pass are pipe_kernel
+// (pipe.cuh).  Here:
+//   col_wave_kernel   : both wave fields of W columns: forward along y, the exact
+//                       oscillator update (eq:OmegaZero/NonZero, PAPER.md:459-471,
+//                       1/(nx ny) folded into its tables), inverse along y
+//   small_solve_kernel: a whole small grid resident in one CTA's shared memory,
+//                       rows -> columns -> operator -> inverse columns -> inverse
+//                       rows: one HBM round trip (C1).
 #pragma once
 #include "fft_core.cuh"
 #include "launch.h"
 
 namespace fftpde {
-
-// conj-on-the-fly load/store helpers
-template <typename C> __device__ __forceinline__ C ld(const C *p, bool cj)
-{
-    C v = *p;
-    return cj ? cconj(v) : v;
-}
 
 // Smem pitch (in complex elements) of one column buffer so that W columns
 // accessed by the lanes of one shared-memory phase hit distinct banks:
@@ -31,119 +23,6 @@ template <typename C, int N, int W> struct ColSmem {
     static constexpr int S = W == 1 ? RAW : ((RAW + LPP - 1) / LPP) * LPP + (W >= LPP ? 1 : LPP / W);
     static constexpr size_t BYTES = (size_t)W * S * sizeof(C);
 };
-
-// ---------------------------------------------------------------------------
-// Row pass: ROWS rows of length N per CTA, Shape<N>::TPT threads per row.
-// in/out may alias (each thread reads its own elements before writing them).
-template <typename T, int N, int ROWS>
-__global__ void __launch_bounds__(ROWS * Shape<N>::TPT)
-row_fft_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out,
-               int64_t ny, int64_t stride, int64_t total_rows, int conj_io,
-               const typename cplx_t<T>::type *__restrict__ tw)
-{
-    using C = typename cplx_t<T>::type;
-    using S = Shape<N>;
-    constexpr int E = S::E, TPT = S::TPT;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    C *smem = reinterpret_cast<C *>(smem_raw);
-
-    const int lr = threadIdx.x / TPT;
-    const int t = threadIdx.x - lr * TPT;
-    const int64_t r = (int64_t)blockIdx.x * ROWS + lr;
-    const bool active = r < total_rows;
-    const int64_t b = active ? r / ny : 0;
-    const int64_t y = active ? r - b * ny : 0;
-    const int64_t off = b * stride + y * N;
-    const bool cj = conj_io != 0;
-
-    C v[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = active ? ld(in + off + t + TPT * e, cj) : C{0, 0};
-
-    SmemView<C, S::LOGE, 1> sm{smem + lr * S::PADDED};
-    if (TPT >= 32) fft_forward<N>(v, sm, t, tw, SyncCTA{});
-    else fft_forward<N>(v, sm, t, tw, SyncWarp{});
-
-    if (active) {
-        C *dst = opaque_ptr(out + off + t);
-#pragma unroll
-        for (int e = 0; e < E; ++e) dst[TPT * e] = cj ? cconj(v[e]) : v[e];
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Column pass, general: op in {COL_FWD, COL_INV, COL_POISSON, COL_DIFFUSE}.
-// CTA = W adjacent columns x all N rows; thread (c, t) = threadIdx.x = c + W t.
-template <typename T, int N, int W>
-__global__ void __launch_bounds__(W * Shape<N>::TPT)
-col_fused_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out,
-                 int64_t nx, int64_t stride, int op,
-                 const typename cplx_t<T>::type *__restrict__ tw, OpTables<T> tab)
-{
-    using C = typename cplx_t<T>::type;
-    using S = Shape<N>;
-    using CS = ColSmem<C, N, W>;
-    constexpr int E = S::E, TPT = S::TPT;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    C *smem = reinterpret_cast<C *>(smem_raw);
-
-    const int c = threadIdx.x % W;
-    const int t = threadIdx.x / W;
-    const int64_t a = (int64_t)blockIdx.x * W + c;
-    const bool active = a < nx;
-    const int64_t base = (int64_t)blockIdx.y * stride + (active ? a : 0) + (int64_t)t * nx;
-    const int64_t estep = (int64_t)TPT * nx;          // element e of this thread: base + e*estep
-    SmemView<C, S::LOGE, 1> sm{smem + c * CS::S};
-
-    C v[E];
-    if (op == COL_INV) {
-        // standalone inverse along y: conj, scale by 1/(nx ny), forward, conj
-#pragma unroll
-        for (int e = 0; e < E; ++e)
-            v[e] = active ? cscale(cconj(in[base + e * estep]), tab.scale) : C{0, 0};
-        fft_forward<N>(v, sm, t, tw, SyncCTA{});
-        if (active) {
-            C *dst = opaque_ptr(out + base);
-#pragma unroll
-            for (int e = 0; e < E; ++e) dst[e * estep] = cconj(v[e]);
-        }
-        return;
-    }
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = active ? in[base + e * estep] : C{0, 0};
-    fft_forward<N>(v, sm, t, tw, SyncCTA{});
-    if (op == COL_FWD) {
-        if (active) {
-            C *dst = opaque_ptr(out + base);
-#pragma unroll
-            for (int e = 0; e < E; ++e) dst[e * estep] = v[e];
-        }
-        return;
-    }
-    // k-space operator at (a, b), b = t + TPT e; result conjugated for the inverse
-    if (op == COL_POISSON) {
-        const T kxa = active ? tab.kx2[a] : (T)1;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const T k2 = kxa + __ldg(&tab.ky2[t + TPT * e]);
-            const T m = k2 == (T)0 ? (T)0 : -tab.scale / k2;          // -1/|k|^2, k = 0 zeroed
-            v[e] = cconj(cscale(v[e], m));
-        }
-    } else {  // COL_DIFFUSE
-        const T exa = active ? tab.ex[a] : (T)0;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const T m = exa * __ldg(&tab.ey[t + TPT * e]);           // exp(-D|k|^2 dt)/(nx ny)
-            v[e] = cconj(cscale(v[e], m));
-        }
-    }
-    fft_forward<N>(v, sm, t, tw, SyncCTA{});
-    if (active) {
-        C *dst = opaque_ptr(out + base);
-#pragma unroll
-        for (int e = 0; e < E; ++e) dst[e * estep] = cconj(v[e]);
-    }
-}
 
 // Column pass for the wave step: both fields (U, V) of W columns, forward along
 // y, the exact oscillator update, inverse along y.  In place.  One field is in
@@ -182,13 +61,13 @@ col_wave_kernel(typename cplx_t<T>::type *U, typename cplx_t<T>::type *V,
     C v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = active ? U[base + e * estep] : C{0, 0};
-    fft_forward<N>(v, sm, t, tw, SyncCTA{});
+    fft<N, false>(v, sm, t, tw, SyncCTA{});
 #pragma unroll
     for (int e = 0; e < E; ++e) slot(e) = v[e];                        // U^ -> stash
     asm volatile("" ::: "memory");
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = active ? V[base + e * estep] : C{0, 0};
-    fft_forward<N>(v, sm, t, tw, SyncCTA{});
+    fft<N, false>(v, sm, t, tw, SyncCTA{});
     asm volatile("" ::: "memory");   // keep the table loads below the transform (register pressure)
     // quadrant index: qa = |fold(a)|, qb = |fold(b)|
     const int64_t qa = active ? (a <= nx - a ? a : nx - a) : 0;
@@ -203,22 +82,22 @@ col_wave_kernel(typename cplx_t<T>::type *U, typename cplx_t<T>::type *V,
         const C uh = slot(e), vh = v[e];
         const C un = {cc * uh.x + s1 * vh.x, cc * uh.y + s1 * vh.y};   // C U + S1 V
         const C vn = {s2 * uh.x + cc * vh.x, s2 * uh.y + cc * vh.y};   // S2 U + C V
-        slot(e) = cconj(un);
-        v[e] = cconj(vn);
+        slot(e) = un;
+        v[e] = vn;
     }
-    fft_forward<N>(v, sm, t, tw, SyncCTA{});                             // inverse of V
+    fft<N, true>(v, sm, t, tw, SyncCTA{});                               // inverse of V
     if (active) {
         C *dst = opaque_ptr(V + base);
 #pragma unroll
-        for (int e = 0; e < E; ++e) dst[e * estep] = cconj(v[e]);
+        for (int e = 0; e < E; ++e) dst[e * estep] = v[e];
     }
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = slot(e);
-    fft_forward<N>(v, sm, t, tw, SyncCTA{});                             // inverse of U
+    fft<N, true>(v, sm, t, tw, SyncCTA{});                               // inverse of U
     if (active) {
         C *dst = opaque_ptr(U + base);
 #pragma unroll
-        for (int e = 0; e < E; ++e) dst[e * estep] = cconj(v[e]);
+        for (int e = 0; e < E; ++e) dst[e * estep] = v[e];
     }
 }
 
@@ -237,11 +116,10 @@ template <typename C, int NX, int NY> struct SmallLayout {
     static constexpr size_t BYTES = (size_t)NY * PITCH * sizeof(C);
 };
 
-template <typename T, int NX, int NY>
+template <typename T, int NX, int NY, int OP>
 __global__ void __launch_bounds__(SmallLayout<typename cplx_t<T>::type, NX, NY>::THREADS)
 small_solve_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out,
-                   int64_t stride, int op,
-                   const typename cplx_t<T>::type *__restrict__ twx,
+                   int64_t stride, const typename cplx_t<T>::type *__restrict__ twx,
                    const typename cplx_t<T>::type *__restrict__ twy, OpTables<T> tab)
 {
     using C = typename cplx_t<T>::type;
@@ -249,89 +127,74 @@ small_solve_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type 
     using SX = Shape<NX>;
     using SY = Shape<NY>;
     static_assert(SX::E == SY::E, "small_solve needs one thread layout for rows and columns");
+    constexpr bool INV = OP == COL_INV;                 // plain inverse transform
+    constexpr bool SOLVE = OP == COL_POISSON || OP == COL_DIFFUSE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *g = reinterpret_cast<C *>(smem_raw);
     const int64_t off = (int64_t)blockIdx.x * stride;
     const int tid = threadIdx.x;
 
-    const bool inv_only = op == COL_INV;
-    // ---- phase 1: row transforms (forward, or conj-forward for the inverse)
+    // ---- phase 1: row transforms (forward, or inverse for COL_INV)
     {
         const int row = tid / SX::TPT, t = tid % SX::TPT;
-        const bool act = row < NY;
         C v[SX::E];
 #pragma unroll
-        for (int e = 0; e < SX::E; ++e)
-            v[e] = act ? ld(in + off + (int64_t)row * NX + t + SX::TPT * e, inv_only) : C{0, 0};
-        SmemView<C, SX::LOGE, 1> sm{g + (act ? row : 0) * L::PITCH};
-        fft_forward<NX>(v, sm, t, twx, SyncCTA{});
-        if (act) {
+        for (int e = 0; e < SX::E; ++e) v[e] = in[off + (int64_t)row * NX + t + SX::TPT * e];
+        SmemView<C, SX::LOGE, 1> sm{g + row * L::PITCH};
+        fft<NX, INV>(v, sm, t, twx, SyncCTA{});
 #pragma unroll
-            for (int e = 0; e < SX::E; ++e) sm.at(t + SX::TPT * e) = inv_only ? cconj(v[e]) : v[e];
-        }
+        for (int e = 0; e < SX::E; ++e) sm.at(t + SX::TPT * e) = v[e];
         __syncthreads();
     }
     // ---- phase 2: column transforms (+ operator + inverse columns)
     {
         const int col = tid % NX, t = tid / NX;
-        const bool act = t < SY::TPT;
         SmemView<C, 30, L::PITCH> sm{g + padidx(col, SX::LOGE)};
         C v[SY::E];
 #pragma unroll
-        for (int e = 0; e < SY::E; ++e) v[e] = act ? sm.at(t + SY::TPT * e) : C{0, 0};
+        for (int e = 0; e < SY::E; ++e) v[e] = sm.at(t + SY::TPT * e);
         __syncthreads();
-        if (inv_only) {
+        if constexpr (INV) {
 #pragma unroll
-            for (int e = 0; e < SY::E; ++e) v[e] = cscale(cconj(v[e]), tab.scale);
+            for (int e = 0; e < SY::E; ++e) v[e] = cscale(v[e], tab.scale);
         }
-        fft_forward<NY>(v, sm, t, twy, SyncCTA{});
-        if (op == COL_POISSON || op == COL_DIFFUSE) {
+        fft<NY, INV>(v, sm, t, twy, SyncCTA{});
+        if constexpr (SOLVE) {
 #pragma unroll
             for (int e = 0; e < SY::E; ++e) {
                 const int b = t + SY::TPT * e;
                 T m;
-                if (op == COL_POISSON) {
+                if constexpr (OP == COL_POISSON) {
                     const T k2 = tab.kx2[col] + tab.ky2[b];
-                    m = k2 == (T)0 ? (T)0 : -tab.scale / k2;
+                    m = k2 == (T)0 ? (T)0 : -tab.scale / k2;    // -1/|k|^2, k = 0 zeroed
                 } else {
-                    m = tab.ex[col] * tab.ey[b];
+                    m = tab.ex[col] * tab.ey[b];                // exp(-D|k|^2 dt)/(nx ny)
                 }
-                v[e] = cconj(cscale(v[e], m));
+                v[e] = cscale(v[e], m);
             }
-            fft_forward<NY>(v, sm, t, twy, SyncCTA{});
-#pragma unroll
-            for (int e = 0; e < SY::E; ++e) v[e] = cconj(v[e]);
-        } else if (inv_only) {
-#pragma unroll
-            for (int e = 0; e < SY::E; ++e) v[e] = cconj(v[e]);
+            fft<NY, true>(v, sm, t, twy, SyncCTA{});
         }
-        if (act) {
 #pragma unroll
-            for (int e = 0; e < SY::E; ++e) sm.at(t + SY::TPT * e) = v[e];
-        }
+        for (int e = 0; e < SY::E; ++e) sm.at(t + SY::TPT * e) = v[e];
         __syncthreads();
     }
-    if (op == COL_FWD || inv_only) {   // plain transform: write the grid
+    if constexpr (!SOLVE) {   // plain transform: write the grid
         for (int i = tid; i < NX * NY; i += L::THREADS) {
             const int row = i / NX, j = i % NX;
             out[off + i] = g[row * L::PITCH + padidx(j, SX::LOGE)];
         }
         return;
-    }
-    // ---- phase 3: inverse row transforms (conj, forward, conj)
-    {
+    } else {
+        // ---- phase 3: inverse row transforms
         const int row = tid / SX::TPT, t = tid % SX::TPT;
-        const bool act = row < NY;
-        SmemView<C, SX::LOGE, 1> sm{g + (act ? row : 0) * L::PITCH};
+        SmemView<C, SX::LOGE, 1> sm{g + row * L::PITCH};
         C v[SX::E];
 #pragma unroll
-        for (int e = 0; e < SX::E; ++e) v[e] = act ? cconj(sm.at(t + SX::TPT * e)) : C{0, 0};
+        for (int e = 0; e < SX::E; ++e) v[e] = sm.at(t + SX::TPT * e);
         __syncthreads();
-        fft_forward<NX>(v, sm, t, twx, SyncCTA{});
-        if (act) {
+        fft<NX, true>(v, sm, t, twx, SyncCTA{});
 #pragma unroll
-            for (int e = 0; e < SX::E; ++e) out[off + (int64_t)row * NX + t + SX::TPT * e] = cconj(v[e]);
-        }
+        for (int e = 0; e < SX::E; ++e) out[off + (int64_t)row * NX + t + SX::TPT * e] = v[e];
     }
 }
 

@@ -5,7 +5,7 @@
 
 namespace fftpde {
 
-enum ColOp { COL_FWD = 0, COL_INV = 1, COL_POISSON = 2, COL_DIFFUSE = 3 };
+enum ColOp { COL_FWD = 0, COL_INV = 1, COL_POISSON = 2, COL_DIFFUSE = 3 };   // == PipeOp
 
 // Device tables of the k-space multipliers; every multiplier includes the
 // 1/(nx ny) of the inverse transform (exact: a power of two).
