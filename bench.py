@@ -1,0 +1,456 @@
+"""bench.py -- timed run of the 2D FFT-PDE hot path (arXiv 2412.12308) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl reference]
+
+A *step* is one pass of the whole hot path over one batch of synthetic input
+(SURVEY.md 8(a) a1-a5): for the default workload c2 (BASELINE.json configs[1])
+that is one ``fftpde_diffuse`` call of 200 exact diffusion steps on a
+1024 x 1024 complex128 grid (each step a forward 2D FFT, the k-space
+multiply and an inverse 2D FFT, 3 kernel launches).  The metric is grid-points
+per second (nx*ny*batch*nsteps / time) for the whole job; rank 0 prints one
+JSON line.
+
+Timing: W untimed warm-up steps, then exactly K steps, each bracketed by CUDA
+events on the plan's stream; L2 (126 MB) is flushed with a 256 MiB write
+between timed steps (outside the events).  Barrier + synchronize on both sides
+of the timed region; the per-rank device time is reduced with MAX over ranks.
+Multi-GPU (torchrun, one process per GPU): c1-c4 fit one GPU, so N > 1 runs N
+independent replicas (weak scaling, no collective on the data path).
+
+Extra keys: ``e2e`` (the same metric through the public API with host buffers:
+pinned host -> device copy, solve, device -> host copy, every step),
+``roofline`` (dominant kernel class, algorithmic bytes / its CUDA-event time vs
+MEASURED_PEAKS.json hbm_gbs), ``cpu_baseline`` (the fp64 oracle on this host's
+cores, bounded sample; rank 0, N = 1), ``clocks`` (nvidia-smi sampled during
+the timed region), ``gpu_launches`` (library kernels in the timed region).
+
+``--impl reference`` times the CPU oracle (the reference arm of this tier) on
+the same workload, metric and unit, each step a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "2D FFT-PDE solve grid-points/sec and achieved HBM GB/s vs peak (1/2/4/8 GPU)"
+UNIT = "grid-points/s"
+L2_FLUSH_BYTES = 256 << 20
+
+THROTTLE_BITS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+    0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------- inputs
+
+def make_inputs(wl):
+    """Seeded synthetic input of the workload (numpy, host) -- paper_2412_12308_b200.inputs."""
+    import numpy as np
+    from paper_2412_12308_b200 import inputs as I
+    if wl.name.startswith("c1"):
+        return (I.c1_inputs(wl.nx).rho,)
+    if wl.name.startswith("c2"):
+        return (I.c2_inputs(wl.nx).u0,)
+    if wl.name.startswith("c3"):
+        w = I.c3_inputs(wl.nx)
+        return (w.u, w.ut)
+    if wl.name.startswith("c4"):
+        return (I.c4_inputs(wl.nx, wl.batch).astype(np.complex64),)
+    raise ValueError(wl.name)
+
+
+def alg_bytes_per_launch(wl, kernel_class):
+    """Algorithmic HBM bytes of one launch: every field the pass touches is read
+    once and written once."""
+    esz = 16 if wl.dtype == "c128" else 8
+    field = wl.nx * wl.ny * wl.batch * esz
+    if kernel_class == "wave_col_pass":
+        return 2 * 2 * field
+    return 2 * field
+
+
+# ---------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return None
+        sm, mx, reasons = [], [], set()
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+                bits = int(parts[2], 16) if parts[2].startswith("0x") else int(parts[2])
+            except ValueError:
+                continue
+            sm.append(s)
+            mx.append(m)
+            for b, name in THROTTLE_BITS.items():
+                if bits & b and name != "gpu_idle":
+                    reasons.add(name)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- dist
+
+def dist_setup(n_gpus):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(world, value):
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------- native arm
+
+def run_solve(plan, wl, dev_in, out):
+    """One step of the hot path on device buffers (the timed unit)."""
+    if wl.op == "poisson":
+        plan.poisson(dev_in[0], out=out[0])
+    elif wl.op == "diffuse":
+        plan.diffuse(dev_in[0], wl.D, wl.dt, wl.nsteps, out=out[0])
+    else:  # wave: advance a working copy (reset from the input outside the events)
+        plan.wave_step(out[0], out[1], wl.c, wl.dt, wl.nsteps)
+
+
+def reset_wave(wl, dev_in, out):
+    if wl.op == "wave":
+        out[0].copy_(dev_in[0])
+        out[1].copy_(dev_in[1])
+
+
+def native(args, wl, world, rank, local):
+    import numpy as np
+    import torch
+    from paper_2412_12308_b200 import fftpde as F
+
+    dtype = torch.complex128 if wl.dtype == "c128" else torch.complex64
+    host = make_inputs(wl)
+    dev_in = [torch.from_numpy(np.ascontiguousarray(h)).to(dtype).cuda() for h in host]
+    out = [torch.empty_like(d) for d in dev_in]
+    plan = F.Plan(wl.nx, wl.ny, batch=wl.batch, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    # warm-up (also uploads the operator tables for this (D, dt) / (c, dt))
+    for _ in range(args.warmup):
+        reset_wave(wl, dev_in, out)
+        run_solve(plan, wl, dev_in, out)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, events per step, L2 flushed between steps
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = plan.launches
+    gpu_index = torch.cuda.current_device()
+    barrier(world)
+    torch.cuda.synchronize()
+    vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+    smi_index = int(vis[gpu_index]) if len(vis) > gpu_index and vis[gpu_index].isdigit() else gpu_index
+    with ClockSampler(smi_index) as clk:
+        for i in range(args.steps):
+            reset_wave(wl, dev_in, out)
+            flush.zero_()
+            starts[i].record(stream)
+            run_solve(plan, wl, dev_in, out)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = plan.launches - launches0
+    ms_rank = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    ms_total = max_over_ranks(world, ms_rank)
+    ms_per_step = ms_total / args.steps
+    pts_per_step = wl.nx * wl.ny * wl.batch * (wl.nsteps if wl.op != "poisson" else 1)
+    value = world * pts_per_step * args.steps / (ms_total * 1e-3)
+
+    # ---- per-kernel timing (same calls, events around every launch)
+    plan.read_profile()
+    plan.set_profiling(True)
+    for i in range(args.steps):
+        reset_wave(wl, dev_in, out)
+        flush.zero_()
+        run_solve(plan, wl, dev_in, out)
+    torch.cuda.synchronize()
+    prof = plan.read_profile()
+    plan.set_profiling(False)
+    dom = max(prof.items(), key=lambda kv: kv[1][0])
+    dom_name, (dom_ms, dom_n) = dom
+    dom_avg_s = dom_ms / dom_n * 1e-3
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = alg_bytes_per_launch(wl, dom_name) / dom_avg_s / 1e9
+    total_prof = sum(v[0] for v in prof.values())
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{wl.name}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom_name)
+        except Exception:
+            traffic = None
+    roofline = {
+        "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+        "frac": round(achieved / peak, 4), "traffic": traffic,
+        "kernel": dom_name, "launches_per_step": dom_n // args.steps,
+        "avg_launch_us": round(dom_avg_s * 1e6, 2),
+        "share_of_step": round(dom_ms / total_prof, 3) if total_prof else None,
+        "alg_bytes_per_launch": alg_bytes_per_launch(wl, dom_name),
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
+                       else "fallback 6650 GB/s (B200_PROFILING.md)",
+        "per_kernel_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in prof.items()},
+    }
+
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_in = [torch.from_numpy(np.ascontiguousarray(h)).to(dtype).pin_memory() for h in host]
+        host_out = [torch.empty(h.shape, dtype=dtype, pin_memory=True) for h in host_in]
+
+        def e2e_step():
+            if wl.op == "poisson":
+                plan.poisson(host_in[0], out=host_out[0])
+            elif wl.op == "diffuse":
+                plan.diffuse(host_in[0], wl.D, wl.dt, wl.nsteps, out=host_out[0])
+            else:
+                plan.wave_step(host_in[0], host_in[1], wl.c, wl.dt, wl.nsteps)
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier(world)
+        tot = 0.0
+        for i in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2e_step()              # H2D, solve, D2H (synchronises on the result)
+            torch.cuda.synchronize()
+            tot += time.perf_counter() - t0
+        barrier(world)
+        tot = max_over_ranks(world, tot)
+        nbytes = sum(h.numel() * h.element_size() for h in host_in)
+        e2e = {"value": world * pts_per_step * args.steps / tot, "unit": UNIT,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "timer": "host perf_counter around the public-API call (pinned host buffers)"}
+
+    # ---- CPU oracle baseline (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl, host)
+
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if wl.dtype == "c128" else "f32",
+        "data": "synthetic (seeded, BASELINE.json recipe; paper_2412_12308_b200/inputs.py)",
+        "config": workload_config(wl, world),
+        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+        "gpu_launches": launches,
+        "hbm_gbs_alg": round(world * alg_step_bytes(wl) * args.steps / (ms_total * 1e-3) / 1e9, 1),
+    }
+    return line
+
+
+def alg_step_bytes(wl):
+    """Algorithmic bytes of one bench step: each state field read + written once per
+    solve step."""
+    esz = 16 if wl.dtype == "c128" else 8
+    fields = 2 if wl.op == "wave" else 1
+    steps = wl.nsteps if wl.op != "poisson" else 1
+    return 2 * fields * wl.nx * wl.ny * wl.batch * esz * steps
+
+
+def workload_config(wl, world):
+    cfg = {"workload": wl.name, "nx": wl.nx, "ny": wl.ny, "batch": wl.batch, "dtype": wl.dtype,
+           "op": wl.op, "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+           "l2": "flushed between timed steps (256 MiB write)"}
+    if wl.op == "diffuse":
+        cfg.update({"nsteps": wl.nsteps, "D": wl.D, "dt": wl.dt})
+    if wl.op == "wave":
+        cfg.update({"nsteps": wl.nsteps, "c": wl.c, "dt": wl.dt})
+    return cfg
+
+
+# ---------------------------------------------------------------------------- CPU oracle
+
+def oracle_sample(wl, host, budget_s=12.0):
+    """Time the oracle on a bounded sample of the workload; returns (pts/s, desc)."""
+    import numpy as np
+    from oracle import oracle as O
+    if wl.op == "poisson":
+        grids = host[0].astype(np.complex128)
+        if grids.ndim == 2:
+            grids = grids[None]
+        n = 0
+        t0 = time.perf_counter()
+        while n < grids.shape[0]:
+            O.poisson(grids[n], wl.Lx, wl.Ly)
+            n += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+        return wl.nx * wl.ny * n / dt, f"{n} of {wl.batch} Poisson solves ({wl.ny}x{wl.nx})"
+    if wl.op == "diffuse":
+        t0 = time.perf_counter()
+        O.diffuse(host[0], wl.D, wl.dt, 1, wl.Lx, wl.Ly)
+        one = time.perf_counter() - t0
+        k = max(1, min(wl.nsteps, int(budget_s / max(one, 1e-6))))
+        t0 = time.perf_counter()
+        O.diffuse(host[0], wl.D, wl.dt, k, wl.Lx, wl.Ly)
+        dt = time.perf_counter() - t0
+        return wl.nx * wl.ny * k / dt, f"{k} of {wl.nsteps} stepped diffusion steps ({wl.ny}x{wl.nx}, full grid)"
+    t0 = time.perf_counter()
+    O.wave(host[0], host[1], wl.c, wl.dt, 1, wl.Lx, wl.Ly)
+    one = time.perf_counter() - t0
+    k = max(1, min(wl.nsteps, int(budget_s / max(one, 1e-6))))
+    if k > 1:
+        t0 = time.perf_counter()
+        O.wave(host[0], host[1], wl.c, wl.dt, k, wl.Lx, wl.Ly)
+        dt = time.perf_counter() - t0
+    else:
+        dt = one
+    return wl.nx * wl.ny * k / dt, f"{k} of {wl.nsteps} stepped wave steps ({wl.ny}x{wl.nx}, both fields)"
+
+
+def cpu_baseline(wl, host):
+    from oracle import oracle as O
+    O.set_threads(os.cpu_count() or 1)
+    v, desc = oracle_sample(wl, host)
+    return {"value": v, "unit": UNIT, "cores": O.get_threads(), "kind": "oracle", "sample": desc}
+
+
+def reference(args, wl, world, rank):
+    """The reference arm of this tier: the fp64 CPU oracle, as it stands."""
+    if rank != 0:
+        return None
+    from oracle import oracle as O
+    O.set_threads(os.cpu_count() or 1)
+    host = make_inputs(wl)
+    for _ in range(args.warmup):
+        oracle_sample(wl, host, budget_s=2.0)
+    vals, descs = [], []
+    for _ in range(args.steps):
+        v, d = oracle_sample(wl, host, budget_s=8.0)
+        vals.append(v)
+        descs.append(d)
+    value = statistics.median(vals)
+    pts_step = wl.nx * wl.ny * wl.batch * (wl.nsteps if wl.op != "poisson" else 1)
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": pts_step / value * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json recipe)", "config": workload_config(wl, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.get_threads(), "kind": "oracle",
+                         "sample": descs[0] + "; median over steps"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse_args()
+    from paper_2412_12308_b200 import inputs as I
+    wl = I.WORKLOADS[args.workload]
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        line = reference(args, wl, world, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    world, rank, local = dist_setup(args.gpus)
+    line = native(args, wl, world, rank, local)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -85,6 +85,19 @@ const char *fftpde_status_string(fftpde_status status);
  * (instrumentation for bench.py's gpu_launches). */
 int64_t fftpde_launch_count(fftpde_plan plan);
 
+/* Per-kernel timing (instrumentation for bench.py's roofline).  While enabled,
+ * every launch is bracketed by CUDA events on the plan's stream.
+ * fftpde_read_profile synchronises on the recorded events, returns the summed
+ * device time (ms) and launch count of one kernel class since the last read,
+ * and resets them. */
+#define FFTPDE_KERNEL_ROW 0       /* row pass (forward or inverse along x) */
+#define FFTPDE_KERNEL_COL 1       /* column pass (transform, or forward + operator + inverse along y) */
+#define FFTPDE_KERNEL_WAVE_COL 2  /* wave column pass (both fields) */
+#define FFTPDE_KERNEL_SMALL 3     /* single-CTA whole-grid solve */
+#define FFTPDE_KERNEL_CLASSES 4
+fftpde_status fftpde_set_profiling(fftpde_plan plan, int enable);
+fftpde_status fftpde_read_profile(fftpde_plan plan, int kernel_class, double *total_ms, int64_t *launches);
+
 /* ---- transforms ------------------------------------------------------------
  * fftpde_forward: out = DFT2(in), + sign, unnormalised, natural order
  *   (2D_DFT PAPER.md:246-249, computed as row transforms then column

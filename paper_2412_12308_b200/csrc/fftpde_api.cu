@@ -41,6 +41,12 @@ struct fftpde_plan_s {
     bool wave_valid = false;
     double wave_c = 0, wave_dt = 0;
     int64_t launches = 0;
+    // optional per-launch timing (fftpde_set_profiling): event pairs per kernel class
+    bool profiling = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[FFTPDE_KERNEL_CLASSES];
+    std::vector<cudaEvent_t> event_pool;
+    double prof_ms[FFTPDE_KERNEL_CLASSES] = {0};
+    int64_t prof_n[FFTPDE_KERNEL_CLASSES] = {0};
 };
 
 namespace {
@@ -187,6 +193,31 @@ fftpde_status check_call(fftpde_plan p, int64_t batch, int64_t stride)
     return FFTPDE_OK;
 }
 
+cudaEvent_t pool_event(fftpde_plan p)
+{
+    if (!p->event_pool.empty()) {
+        cudaEvent_t e = p->event_pool.back();
+        p->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Launch `f` counting it, and bracket it with events when profiling.
+template <typename F> cudaError_t launch(fftpde_plan p, int cls, F &&f)
+{
+    ++p->launches;
+    if (!p->profiling) return f();
+    cudaEvent_t a = pool_event(p), b = pool_event(p);
+    cudaEventRecord(a, p->stream);
+    cudaError_t e = f();
+    cudaEventRecord(b, p->stream);
+    p->pending[cls].emplace_back(a, b);
+    return e;
+}
+
 // ---- pass sequences --------------------------------------------------------
 template <typename T> struct Passes {
     fftpde_plan p;
@@ -195,25 +226,29 @@ template <typename T> struct Passes {
     const void *twy() const { return p->ws + p->o_twy; }
     cudaError_t rows(const void *in, void *out, int conj)
     {
-        ++p->launches;
-        return launch_rows<T>(p->nx, in, out, p->ny, stride, batch, conj, twx(), p->stream);
+        return launch(p, FFTPDE_KERNEL_ROW, [&] {
+            return launch_rows<T>(p->nx, in, out, p->ny, stride, batch, conj, twx(), p->stream);
+        });
     }
     cudaError_t cols(const void *in, void *out, int op)
     {
-        ++p->launches;
-        return launch_cols<T>(p->ny, in, out, p->nx, stride, batch, op, twy(), tables<T>(p), p->stream);
+        return launch(p, FFTPDE_KERNEL_COL, [&] {
+            return launch_cols<T>(p->ny, in, out, p->nx, stride, batch, op, twy(), tables<T>(p), p->stream);
+        });
     }
     cudaError_t wave_cols(void *U, void *V)
     {
-        ++p->launches;
-        return launch_wave_cols<T>(p->ny, U, V, p->nx, stride, batch, twy(), tables<T>(p), p->stream);
+        return launch(p, FFTPDE_KERNEL_WAVE_COL, [&] {
+            return launch_wave_cols<T>(p->ny, U, V, p->nx, stride, batch, twy(), tables<T>(p), p->stream);
+        });
     }
     bool small() const { return small_supported<T>(p->nx, p->ny); }
     cudaError_t small_op(const void *in, void *out, int op)
     {
-        ++p->launches;
-        return launch_small<T>(p->nx, p->ny, in, out, stride, batch, op, twx(), twy(), tables<T>(p),
-                               p->stream);
+        return launch(p, FFTPDE_KERNEL_SMALL, [&] {
+            return launch_small<T>(p->nx, p->ny, in, out, stride, batch, op, twx(), twy(), tables<T>(p),
+                                   p->stream);
+        });
     }
     // one step of a diagonal k-space operator: DFT2 -> multiply -> iDFT2
     cudaError_t solve_step(const void *in, void *out, int op)
@@ -431,7 +466,41 @@ fftpde_status fftpde_set_workspace(fftpde_plan plan, void *dev_ptr, size_t bytes
 
 fftpde_status fftpde_destroy(fftpde_plan plan)
 {
+    if (!plan) return FFTPDE_OK;
+    for (auto &v : plan->pending)
+        for (auto &pr : v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+    for (cudaEvent_t e : plan->event_pool) cudaEventDestroy(e);
     delete plan;
+    return FFTPDE_OK;
+}
+
+fftpde_status fftpde_set_profiling(fftpde_plan plan, int enable)
+{
+    if (!plan) return FFTPDE_ERR_INVALID_ARG;
+    plan->profiling = enable != 0;
+    return FFTPDE_OK;
+}
+
+fftpde_status fftpde_read_profile(fftpde_plan plan, int kernel_class, double *total_ms, int64_t *launches)
+{
+    if (!plan || kernel_class < 0 || kernel_class >= FFTPDE_KERNEL_CLASSES || !total_ms || !launches)
+        return FFTPDE_ERR_INVALID_ARG;
+    DeviceGuard g(plan->device);
+    auto &v = plan->pending[kernel_class];
+    for (auto &pr : v) {
+        if (cudaEventSynchronize(pr.second) != cudaSuccess) return FFTPDE_ERR_CUDA;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, pr.first, pr.second) != cudaSuccess) return FFTPDE_ERR_CUDA;
+        plan->prof_ms[kernel_class] += ms;
+        plan->prof_n[kernel_class] += 1;
+        plan->event_pool.push_back(pr.first);
+        plan->event_pool.push_back(pr.second);
+    }
+    v.clear();
+    *total_ms = plan->prof_ms[kernel_class];
+    *launches = plan->prof_n[kernel_class];
+    plan->prof_ms[kernel_class] = 0;
+    plan->prof_n[kernel_class] = 0;
     return FFTPDE_OK;
 }
 

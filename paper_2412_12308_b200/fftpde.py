@@ -20,6 +20,8 @@ import torch
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libfftpde.so")
 
+KERNEL_CLASSES = {0: "row_pass", 1: "col_pass", 2: "wave_col_pass", 3: "small_solve"}
+
 # fftpde_status
 OK, ERR_INVALID_ARG, ERR_EMPTY, ERR_NOT_POW2_X, ERR_NOT_POW2_Y, ERR_UNSUPPORTED, ERR_WORKSPACE, \
     ERR_CUDA, ERR_NCCL = range(9)
@@ -28,6 +30,7 @@ C64, C128 = 0, 1
 EXPORTS = [
     "fftpde_plan_2d", "fftpde_workspace_size", "fftpde_set_workspace", "fftpde_set_stream",
     "fftpde_destroy", "fftpde_status_string", "fftpde_launch_count",
+    "fftpde_set_profiling", "fftpde_read_profile",
     "fftpde_forward", "fftpde_inverse", "fftpde_poisson", "fftpde_diffuse", "fftpde_wave_step",
     "fftpde_forward_batched", "fftpde_inverse_batched", "fftpde_poisson_batched",
     "fftpde_diffuse_batched", "fftpde_wave_step_batched",
@@ -62,6 +65,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fftpde_destroy": (st, [p]),
         "fftpde_status_string": (ctypes.c_char_p, [st]),
         "fftpde_launch_count": (i64, [p]),
+        "fftpde_set_profiling": (st, [p, u]),
+        "fftpde_read_profile": (st, [p, u, ctypes.POINTER(dbl), ctypes.POINTER(i64)]),
         "fftpde_forward": (st, [p, p, p]),
         "fftpde_inverse": (st, [p, p, p]),
         "fftpde_poisson": (st, [p, p, p]),
@@ -140,6 +145,20 @@ class Plan:
     def launches(self) -> int:
         return int(self.lib.fftpde_launch_count(self._h))
 
+    def set_profiling(self, enable: bool):
+        _check(self.lib.fftpde_set_profiling(self._h, int(bool(enable))), "fftpde_set_profiling")
+
+    def read_profile(self) -> dict:
+        """{kernel class: (total device ms, launches)} since the last read."""
+        out = {}
+        for cls, name in KERNEL_CLASSES.items():
+            ms, n = ctypes.c_double(), ctypes.c_int64()
+            _check(self.lib.fftpde_read_profile(self._h, cls, ctypes.byref(ms), ctypes.byref(n)),
+                   "fftpde_read_profile")
+            if n.value:
+                out[name] = (ms.value, n.value)
+        return out
+
     def _grid(self, x: torch.Tensor, name: str):
         if x.dtype != self.dtype:
             raise TypeError(f"{name}: dtype {x.dtype} does not match the plan's {self.dtype}")
@@ -166,9 +185,12 @@ class Plan:
             raise ValueError(f"tensor on {x.device}, plan on {self.device}")
         return x.contiguous(), False
 
-    def _finish(self, out_dev: torch.Tensor, host: bool):
+    def _finish(self, out_dev: torch.Tensor, host: bool, host_out=None):
+        """Device result, or (host inputs) its copy in pinned host memory
+        (``host_out`` if given, a pinned tensor of the right shape)."""
         if host:
-            out = torch.empty(out_dev.shape, dtype=out_dev.dtype, pin_memory=True)
+            out = host_out if host_out is not None else torch.empty(out_dev.shape, dtype=out_dev.dtype,
+                                                                    pin_memory=True)
             out.copy_(out_dev, non_blocking=True)
             torch.cuda.current_stream(self.device).synchronize()
             return out
@@ -191,7 +213,7 @@ class Plan:
         self._bind_stream()
         _check(self.lib.fftpde_forward_batched(self._h, xd.data_ptr(), o.data_ptr(), B,
                                                self.nx * self.ny), "fftpde_forward")
-        return self._finish(o, host)
+        return self._finish(o, host, out if host else None)
 
     def inverse(self, X: torch.Tensor, out=None) -> torch.Tensor:
         """iDFT2: conjugate kernel, times 1/(nx ny)."""
@@ -201,7 +223,7 @@ class Plan:
         self._bind_stream()
         _check(self.lib.fftpde_inverse_batched(self._h, xd.data_ptr(), o.data_ptr(), B,
                                                self.nx * self.ny), "fftpde_inverse")
-        return self._finish(o, host)
+        return self._finish(o, host, out if host else None)
 
     def poisson(self, rho: torch.Tensor, out=None) -> torch.Tensor:
         """u with nabla^2 u = rho - mean(rho), zero mean (eq:SolutionPoisson)."""
@@ -211,7 +233,7 @@ class Plan:
         self._bind_stream()
         _check(self.lib.fftpde_poisson_batched(self._h, rd.data_ptr(), o.data_ptr(), B,
                                                self.nx * self.ny), "fftpde_poisson")
-        return self._finish(o, host)
+        return self._finish(o, host, out if host else None)
 
     def diffuse(self, u0: torch.Tensor, D: float, dt: float, nsteps: int, out=None) -> torch.Tensor:
         """nsteps exact diffusion steps exp(-D|k|^2 dt) (ec:solCalorFourier)."""
@@ -222,7 +244,7 @@ class Plan:
         _check(self.lib.fftpde_diffuse_batched(self._h, ud.data_ptr(), o.data_ptr(), B,
                                                self.nx * self.ny, float(D), float(dt), int(nsteps)),
                "fftpde_diffuse")
-        return self._finish(o, host)
+        return self._finish(o, host, out if host else None)
 
     def wave_step(self, u: torch.Tensor, ut: torch.Tensor, c: float, dt: float, nsteps: int):
         """nsteps exact wave steps on (u, ut) (eq:OmegaZero/NonZero).
