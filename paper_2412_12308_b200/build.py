@@ -23,6 +23,8 @@ LIB = os.path.join(PKG, "libfftpde.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-O2",
               "-I" + os.path.join(ROOT, "include")]
+# development experiments only (e.g. FFTPDE_NVCC_EXTRA="-DFFTPDE_COL2_MINB=3")
+NVCC_FLAGS += [f for f in os.environ.get("FFTPDE_NVCC_EXTRA", "").split() if f]
 
 
 def nvcc() -> str:

@@ -5,6 +5,11 @@
 #include <algorithm>
 #include "kernels.cuh"
 #include "pipe.cuh"
+#include "col2.cuh"
+#ifndef FFTPDE_COL2_MINB
+#define FFTPDE_COL2_MINB 2
+#endif
+
 
 namespace fftpde {
 
@@ -155,6 +160,72 @@ cudaError_t small_n(const void *in, void *out, int64_t stride, int64_t batch, in
     }
 }
 
+// ---- two-level cluster column pass ------------------------------------------
+template <typename T, int P, int Q> struct Col2Cfg {
+    using C = typename cplx_t<T>::type;
+    static constexpr int NT = 256;
+    static constexpr int EMAX = FFTPDE_COL2_EMAX;
+    using IA = Col2Items<C, Q, NT, EMAX>;
+    using IB = Col2Items<C, P, NT, EMAX>;
+    static constexpr int CLA = P / IA::SLOTS, CLB = Q / IB::SLOTS;
+    static constexpr int CL0 = CLA > CLB ? CLA : CLB;
+    static constexpr int CL = CL0 < 1 ? 1 : CL0 > 8 ? 8 : CL0;
+    static constexpr size_t SA = (size_t)IA::SLOTS * IA::SLOT_ELEMS * sizeof(C);
+    static constexpr size_t SB = (size_t)IB::SLOTS * IB::SLOT_ELEMS * sizeof(C);
+    static constexpr size_t SMEM = SA > SB ? SA : SB;
+    static constexpr int MINB = FFTPDE_COL2_MINB;
+};
+
+template <typename T, int P, int Q, int OP>
+cudaError_t col2_n(Col2Args<T> g, int64_t batch, const OpTables<T> &tab, cudaStream_t st)
+{
+    using Cfg = Col2Cfg<T, P, Q>;
+    auto k = col2_kernel<T, P, Q, OP, Cfg::CL, Cfg::NT, Cfg::MINB, Cfg::EMAX>;
+    static SmemOptIn<decltype(k)> opt;
+    cudaError_t e = opt(k, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(Cfg::CL * g.nblocks * batch), 1, 1);
+    cfg.blockDim = dim3(Cfg::NT, 1, 1);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = Cfg::CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k, g, tab);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+template <typename T, int P, int Q>
+cudaError_t col2_op(int op, Col2Args<T> g, int64_t batch, const OpTables<T> &tab, cudaStream_t st)
+{
+    switch (op) {
+    case COL_FWD: return col2_n<T, P, Q, C2_FWD>(g, batch, tab, st);
+    case COL_INV: return col2_n<T, P, Q, C2_INV_SCALED>(g, batch, tab, st);
+    case COL_POISSON: return col2_n<T, P, Q, C2_POISSON>(g, batch, tab, st);
+    case COL_DIFFUSE: return col2_n<T, P, Q, C2_DIFFUSE>(g, batch, tab, st);
+    case 4: return col2_n<T, P, Q, C2_WAVE>(g, batch, tab, st);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+template <typename T>
+cudaError_t launch_col2(int64_t ny, int64_t P, int op, Col2Args<T> g, int64_t batch,
+                        const OpTables<T> &tab, cudaStream_t st)
+{
+    switch (ny) {
+    case 2048: return col2_op<T, 32, 64>(op, g, batch, tab, st);
+    case 4096: return col2_op<T, 64, 64>(op, g, batch, tab, st);
+    case 8192: return col2_op<T, 64, 128>(op, g, batch, tab, st);
+    default: (void)P; return cudaErrorInvalidValue;
+    }
+}
+
 // ---- length dispatch -------------------------------------------------------
 template <typename T>
 cudaError_t launch_rows(int64_t n, const void *in, void *out, int64_t ny, int64_t stride,
@@ -170,9 +241,18 @@ cudaError_t launch_rows(int64_t n, const void *in, void *out, int64_t ny, int64_
 
 template <typename T>
 cudaError_t launch_cols(int64_t ny, const void *in, void *out, int64_t nx, int64_t stride,
-                        int64_t batch, int op, const void *tw, const OpTables<T> &tab,
+                        int64_t batch, int op, const ColTw &ctw, const OpTables<T> &tab,
                         cudaStream_t st)
 {
+    using C = typename cplx_t<T>::type;
+    int64_t P = 0, Q = 0;
+    col2_split(ny, nx, (int)sizeof(C), P, Q);
+    if (P) {
+        Col2Args<T> g{(C *)out, nullptr, (const C *)in, nx, stride, nx / Col2Geom<C>::W,
+                      (const C *)ctw.twP, (const C *)ctw.twQ, (const C *)ctw.twN};
+        return launch_col2<T>(ny, P, op, g, batch, tab, st);
+    }
+    const void *tw = ctw.tw;
     switch (ny) {
 #define X(L) case L: return cols_n<T, L>(in, out, nx, stride, batch, op, tw, tab, st);
         FFTPDE_LEN_CASES(X)
@@ -183,9 +263,18 @@ cudaError_t launch_cols(int64_t ny, const void *in, void *out, int64_t nx, int64
 
 template <typename T>
 cudaError_t launch_wave_cols(int64_t ny, void *U, void *V, int64_t nx, int64_t stride,
-                             int64_t batch, const void *tw, const OpTables<T> &tab,
+                             int64_t batch, const ColTw &ctw, const OpTables<T> &tab,
                              cudaStream_t st)
 {
+    using C = typename cplx_t<T>::type;
+    int64_t P = 0, Q = 0;
+    col2_split(ny, nx, (int)sizeof(C), P, Q);
+    if (P) {
+        Col2Args<T> g{(C *)U, (C *)V, (const C *)U, nx, stride, nx / Col2Geom<C>::W,
+                      (const C *)ctw.twP, (const C *)ctw.twQ, (const C *)ctw.twN};
+        return launch_col2<T>(ny, P, 4, g, batch, tab, st);
+    }
+    const void *tw = ctw.tw;
     switch (ny) {
 #define X(L) case L: return wave_cols_n<T, L>(U, V, nx, stride, batch, tw, tab, st);
         FFTPDE_LEN_CASES(X)

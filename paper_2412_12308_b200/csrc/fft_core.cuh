@@ -135,9 +135,9 @@ template <int R, bool INV, typename C> __device__ __forceinline__ void dft_r(C (
 
 // ---------------------------------------------------------------------------
 // Compile-time shape of one length-N transform.
-template <int N_> struct Shape {
+template <int N_, int EMAX = 16> struct Shape {
     static constexpr int N = N_;
-    static constexpr int E = N_ < 16 ? N_ : 16;        // elements per thread
+    static constexpr int E = N_ < EMAX ? N_ : EMAX;    // elements per thread (the radix)
     static constexpr int TPT = N_ / E;                   // threads per transform
     static constexpr int LOGE = E == 16 ? 4 : E == 8 ? 3 : E == 4 ? 2 : E == 2 ? 1 : 0;
     // padded smem index: one pad slot every E elements (conflict-free stage-1 scatter)
@@ -206,12 +206,12 @@ template <typename C, int LOGE, int STRIDE> struct SmemView {
 // both read from the stage-major table of Shape<N>.  TwL1 loads each twiddle
 // at its use (L1-resident table); TwReg loads a thread's twiddles once (a
 // persistent kernel reuses them for every line it transforms).
-template <int N, typename C> struct TwL1 {
+template <int N, typename C, int EMAX = 16> struct TwL1 {
     const C *tw;
     int t;
     __device__ __forceinline__ C mid(int s, int m) const
     {
-        using S = Shape<N>;
+        using S = Shape<N, EMAX>;
         int ns = S::E, off = 0;
 #pragma unroll
         for (int i = 1; i < s; ++i) { off += S::E * ns; ns *= S::E; }
@@ -219,13 +219,13 @@ template <int N, typename C> struct TwL1 {
     }
     __device__ __forceinline__ C last(int q, int m) const
     {
-        using S = Shape<N>;
+        using S = Shape<N, EMAX>;
         return ldtw(tw + S::TW_LAST_OFF + opaque(t + q * S::TPT) + m * S::NS_LAST);
     }
 };
 
-template <int N, typename C> struct TwReg {
-    using S = Shape<N>;
+template <int N, typename C, int EMAX = 16> struct TwReg {
+    using S = Shape<N, EMAX>;
     static constexpr int NMID = S::STAGES > 1 ? (S::STAGES - 1) * (S::E - 1) : 1;
     static constexpr int Q = S::E / S::R_LAST;
     static constexpr int NLAST = S::R_LAST > 1 ? Q * (S::R_LAST - 1) : 1;
@@ -233,7 +233,7 @@ template <int N, typename C> struct TwReg {
     C wl[NLAST];
     __device__ __forceinline__ void load(const C *tw, int t)
     {
-        TwL1<N, C> l{tw, t};
+        TwL1<N, C, EMAX> l{tw, t};
 #pragma unroll
         for (int s = 1; s < S::STAGES; ++s)
 #pragma unroll
@@ -253,11 +253,11 @@ template <int N, typename C> struct TwReg {
 // v[e] = X[t + TPT e].  INV selects the conjugate kernel (inverse direction,
 // unscaled).  `sync` synchronises the threads sharing the exchange buffer
 // (warp, line or CTA); the buffer is free again when this returns.
-template <int N, bool INV, typename C, typename View, typename Tw, typename Sync>
-__device__ __forceinline__ void fft_tw(C (&v)[Shape<N>::E], const View &sm, int t, const Tw &tw,
+template <int N, bool INV, int EMAX = 16, typename C, typename View, typename Tw, typename Sync>
+__device__ __forceinline__ void fft_tw(C (&v)[Shape<N, EMAX>::E], const View &sm, int t, const Tw &tw,
                                        Sync sync)
 {
-    using S = Shape<N>;
+    using S = Shape<N, EMAX>;
     constexpr int E = S::E, TPT = S::TPT;
     int Ns = 1;
 #pragma unroll
@@ -304,11 +304,11 @@ __device__ __forceinline__ void fft_tw(C (&v)[Shape<N>::E], const View &sm, int 
 }
 
 // Twiddles loaded from the table at each use.
-template <int N, bool INV, typename C, typename View, typename Sync>
-__device__ __forceinline__ void fft(C (&v)[Shape<N>::E], const View &sm, int t,
+template <int N, bool INV, int EMAX = 16, typename C, typename View, typename Sync>
+__device__ __forceinline__ void fft(C (&v)[Shape<N, EMAX>::E], const View &sm, int t,
                                     const C *__restrict__ tw, Sync sync)
 {
-    fft_tw<N, INV>(v, sm, t, TwL1<N, C>{tw, t}, sync);
+    fft_tw<N, INV, EMAX>(v, sm, t, TwL1<N, C, EMAX>{tw, t}, sync);
 }
 
 struct SyncCTA { __device__ __forceinline__ void operator()() const { __syncthreads(); } };

@@ -31,6 +31,9 @@ struct fftpde_plan_s {
     size_t ws_bytes = 0;
     // workspace offsets (bytes)
     size_t o_twx = 0, o_twy = 0, o_kx2 = 0, o_ky2 = 0, o_ex = 0, o_ey = 0, o_wc = 0, o_ws1 = 0, o_ws2 = 0;
+    size_t o_twP = 0, o_twQ = 0, o_twN = 0;   // two-level column pass tables (P, Q > 0)
+    int64_t colP = 0, colQ = 0;
+    std::vector<double> twP, twQ, twN;
     size_t need = 0;
     int64_t qx = 0, qy = 0;   // quadrant extents nx/2+1, ny/2+1
     // host tables (fp64)
@@ -82,9 +85,9 @@ void unit_root(int64_t n, int64_t m, double &re, double &im)
 // the kernels (fft_core.cuh Shape<n>): per middle stage (Ns = E, E^2, ...)
 // w_{Ns E}^{m k} at [m Ns + k]; then the last stage w_n^{m j} at [m Ns_last + j].
 // Each entry is w_M^q = w_n^{q n / M}, evaluated directly from its index.
-void build_twiddles(int64_t n, std::vector<double> &tw)
+void build_twiddles(int64_t n, std::vector<double> &tw, int64_t emax = 16)
 {
-    const int64_t E = n < 16 ? n : 16;
+    const int64_t E = n < emax ? n : emax;
     tw.clear();
     auto put = [&](int64_t M, int64_t q) {
         double re, im;
@@ -115,6 +118,13 @@ void build_k2(int64_t n, double L, std::vector<double> &k2)
         const double k = two_pi * (double)f / L;
         k2[(size_t)a] = k * k;
     }
+}
+
+// Plain table w_n^m, m < n (the inter-phase twiddles w_N^{n1 k1} of the two-level pass).
+void build_plain_twiddles(int64_t n, std::vector<double> &tw)
+{
+    tw.resize(2 * (size_t)n);
+    for (int64_t m = 0; m < n; ++m) unit_root(n, m, tw[2 * m], tw[2 * m + 1]);
 }
 
 template <typename T> std::vector<T> cast_vec(const std::vector<double> &v)
@@ -230,16 +240,20 @@ template <typename T> struct Passes {
             return launch_rows<T>(p->nx, in, out, p->ny, stride, batch, conj, twx(), p->stream);
         });
     }
+    ColTw ctw() const
+    {
+        return ColTw{twy(), p->ws + p->o_twP, p->ws + p->o_twQ, p->ws + p->o_twN};
+    }
     cudaError_t cols(const void *in, void *out, int op)
     {
         return launch(p, FFTPDE_KERNEL_COL, [&] {
-            return launch_cols<T>(p->ny, in, out, p->nx, stride, batch, op, twy(), tables<T>(p), p->stream);
+            return launch_cols<T>(p->ny, in, out, p->nx, stride, batch, op, ctw(), tables<T>(p), p->stream);
         });
     }
     cudaError_t wave_cols(void *U, void *V)
     {
         return launch(p, FFTPDE_KERNEL_WAVE_COL, [&] {
-            return launch_wave_cols<T>(p->ny, U, V, p->nx, stride, batch, twy(), tables<T>(p), p->stream);
+            return launch_wave_cols<T>(p->ny, U, V, p->nx, stride, batch, ctw(), tables<T>(p), p->stream);
         });
     }
     bool small() const { return small_supported<T>(p->nx, p->ny); }
@@ -364,6 +378,21 @@ fftpde_status copy_grids(fftpde_plan p, const void *src, void *dst, int64_t batc
 
 } // namespace
 
+// Two-level column pass split ny = P Q (col2.cuh); 0 when the single-level
+// pass is used (short columns, or fewer columns than one 128-byte block).
+void fftpde::col2_split(int64_t ny, int64_t nx, int elem_bytes, int64_t &P, int64_t &Q)
+{
+    P = Q = 0;
+    const int64_t W = 128 / elem_bytes;
+    if (nx < W || nx % W) return;
+    switch (ny) {
+    case 2048: P = 32; Q = 64; break;
+    case 4096: P = 64; Q = 64; break;
+    case 8192: P = 64; Q = 128; break;
+    default: break;
+    }
+}
+
 // ============================================================================
 extern "C" {
 
@@ -407,6 +436,12 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     build_twiddles(ny, p->twy);
     build_k2(nx, Lx, p->kx2);
     build_k2(ny, Ly, p->ky2);
+    fftpde::col2_split(ny, nx, dtype == FFTPDE_C128 ? 16 : 8, p->colP, p->colQ);
+    if (p->colP) {
+        build_twiddles(p->colP, p->twP, FFTPDE_COL2_EMAX);
+        build_twiddles(p->colQ, p->twQ, FFTPDE_COL2_EMAX);
+        build_plain_twiddles(ny, p->twN);
+    }
 
     const size_t er = elem_real(p), ec = elem_cplx(p);
     size_t off = 0;
@@ -421,6 +456,11 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     p->o_wc = take(q);
     p->o_ws1 = take(q);
     p->o_ws2 = take(q);
+    if (p->colP) {
+        p->o_twP = take(p->twP.size() / 2 * ec);
+        p->o_twQ = take(p->twQ.size() / 2 * ec);
+        p->o_twN = take(p->twN.size() / 2 * ec);
+    }
     p->need = off;
     *plan = p;
     return FFTPDE_OK;
@@ -457,6 +497,11 @@ fftpde_status fftpde_set_workspace(fftpde_plan plan, void *dev_ptr, size_t bytes
     } else {
         s = upload(plan, plan->o_twx, plan->twx);
         if (s == FFTPDE_OK) s = upload(plan, plan->o_twy, plan->twy);
+    }
+    if (s == FFTPDE_OK && plan->colP) {
+        s = upload(plan, plan->o_twP, plan->twP);
+        if (s == FFTPDE_OK) s = upload(plan, plan->o_twQ, plan->twQ);
+        if (s == FFTPDE_OK) s = upload(plan, plan->o_twN, plan->twN);
     }
     if (s == FFTPDE_OK) s = upload(plan, plan->o_kx2, plan->kx2);
     if (s == FFTPDE_OK) s = upload(plan, plan->o_ky2, plan->ky2);

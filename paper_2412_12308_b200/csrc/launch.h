@@ -19,22 +19,39 @@ template <typename T> struct OpTables {
 
 constexpr int64_t kMaxLen = 8192;   // single-pass axis length limit of this build
 
+// radix (elements per thread) of the sub-transforms of the two-level column pass;
+// the host builds its P and Q twiddle tables for the same factorisation
+#ifndef FFTPDE_COL2_EMAX
+#define FFTPDE_COL2_EMAX 8
+#endif
+
 // Row transforms of `batch` grids: length n along x, ny rows per grid, grids
 // `stride` elements apart.  conj != 0 gives the inverse direction (unscaled).
 template <typename T>
 cudaError_t launch_rows(int64_t n, const void *in, void *out, int64_t ny, int64_t stride,
                         int64_t batch, int conj, const void *tw, cudaStream_t st);
 
+// Twiddle tables of the column axis: the single-level stage table of ny, and for
+// the two-level (cluster) column pass the stage tables of P and Q (ny = P Q)
+// plus the plain table w_ny^m, m < ny.
+struct ColTw {
+    const void *tw;      // stage table of ny
+    const void *twP, *twQ, *twN;
+};
+
+// Split ny = P * Q used by the two-level column pass (P = Q = 0: not used).
+void col2_split(int64_t ny, int64_t nx, int elem_bytes, int64_t &P, int64_t &Q);
+
 // Column pass along y (length ny) over nx columns, op in ColOp.
 template <typename T>
 cudaError_t launch_cols(int64_t ny, const void *in, void *out, int64_t nx, int64_t stride,
-                        int64_t batch, int op, const void *tw, const OpTables<T> &tab,
+                        int64_t batch, int op, const ColTw &tw, const OpTables<T> &tab,
                         cudaStream_t st);
 
 // Wave column pass: both fields, in place.
 template <typename T>
 cudaError_t launch_wave_cols(int64_t ny, void *U, void *V, int64_t nx, int64_t stride,
-                             int64_t batch, const void *tw, const OpTables<T> &tab,
+                             int64_t batch, const ColTw &tw, const OpTables<T> &tab,
                              cudaStream_t st);
 
 // Single-CTA whole-grid solve (small square grids).

@@ -5,9 +5,9 @@ namespace fftpde {
 template cudaError_t launch_rows<double>(int64_t, const void *, void *, int64_t, int64_t, int64_t, int,
                                      const void *, cudaStream_t);
 template cudaError_t launch_cols<double>(int64_t, const void *, void *, int64_t, int64_t, int64_t, int,
-                                     const void *, const OpTables<double> &, cudaStream_t);
+                                     const ColTw &, const OpTables<double> &, cudaStream_t);
 template cudaError_t launch_wave_cols<double>(int64_t, void *, void *, int64_t, int64_t, int64_t,
-                                          const void *, const OpTables<double> &, cudaStream_t);
+                                          const ColTw &, const OpTables<double> &, cudaStream_t);
 template bool small_supported<double>(int64_t, int64_t);
 template cudaError_t launch_small<double>(int64_t, int64_t, const void *, void *, int64_t, int64_t, int,
                                      const void *, const void *, const OpTables<double> &, cudaStream_t);

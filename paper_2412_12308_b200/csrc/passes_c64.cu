@@ -5,9 +5,9 @@ namespace fftpde {
 template cudaError_t launch_rows<float>(int64_t, const void *, void *, int64_t, int64_t, int64_t, int,
                                      const void *, cudaStream_t);
 template cudaError_t launch_cols<float>(int64_t, const void *, void *, int64_t, int64_t, int64_t, int,
-                                     const void *, const OpTables<float> &, cudaStream_t);
+                                     const ColTw &, const OpTables<float> &, cudaStream_t);
 template cudaError_t launch_wave_cols<float>(int64_t, void *, void *, int64_t, int64_t, int64_t,
-                                          const void *, const OpTables<float> &, cudaStream_t);
+                                          const ColTw &, const OpTables<float> &, cudaStream_t);
 template bool small_supported<float>(int64_t, int64_t);
 template cudaError_t launch_small<float>(int64_t, int64_t, const void *, void *, int64_t, int64_t, int,
                                      const void *, const void *, const OpTables<float> &, cudaStream_t);
