@@ -91,13 +91,14 @@ cudaError_t pipe_n(const void *in, void *out, PipeArgs args, const void *tw, con
 }
 
 template <typename T, int N>
-cudaError_t rows_n(const void *in, void *out, int64_t ny, int64_t stride, int64_t batch,
-                   int conj, const void *tw, cudaStream_t st)
+cudaError_t rows_n(const void *in, void *out, void *out2, int64_t ny, int64_t stride, int64_t batch,
+                   int dir, const void *tw, cudaStream_t st)
 {
-    PipeArgs a{ny, N, 1, stride, batch, 0, conj ? PIPE_INV : PIPE_FWD};
+    PipeArgs a{ny, N, 1, stride, batch, 0, dir, out2};
     OpTables<T> tab{};
     tab.scale = (T)1;
-    if (conj) return pipe_n<T, N, false, PIPE_INV>(in, out, a, tw, tab, st);
+    if (dir == ROW_INV) return pipe_n<T, N, false, PIPE_INV>(in, out, a, tw, tab, st);
+    if (dir == ROW_MID) return pipe_n<T, N, false, PIPE_MID>(in, out, a, tw, tab, st);
     return pipe_n<T, N, false, PIPE_FWD>(in, out, a, tw, tab, st);
 }
 
@@ -105,7 +106,7 @@ template <typename T, int N>
 cudaError_t cols_n(const void *in, void *out, int64_t nx, int64_t stride, int64_t batch, int op,
                    const void *tw, const OpTables<T> &tab, cudaStream_t st)
 {
-    PipeArgs a{nx, 1, nx, stride, batch, 0, op};
+    PipeArgs a{nx, 1, nx, stride, batch, 0, op, nullptr};
     switch (op) {
     case COL_FWD: return pipe_n<T, N, true, PIPE_FWD>(in, out, a, tw, tab, st);
     case COL_INV: return pipe_n<T, N, true, PIPE_INV_SCALED>(in, out, a, tw, tab, st);
@@ -228,11 +229,11 @@ cudaError_t launch_col2(int64_t ny, int64_t P, int op, Col2Args<T> g, int64_t ba
 
 // ---- length dispatch -------------------------------------------------------
 template <typename T>
-cudaError_t launch_rows(int64_t n, const void *in, void *out, int64_t ny, int64_t stride,
-                        int64_t batch, int conj, const void *tw, cudaStream_t st)
+cudaError_t launch_rows(int64_t n, const void *in, void *out, void *out2, int64_t ny, int64_t stride,
+                        int64_t batch, int dir, const void *tw, cudaStream_t st)
 {
     switch (n) {
-#define X(L) case L: return rows_n<T, L>(in, out, ny, stride, batch, conj, tw, st);
+#define X(L) case L: return rows_n<T, L>(in, out, out2, ny, stride, batch, dir, tw, st);
         FFTPDE_LEN_CASES(X)
 #undef X
     default: return cudaErrorInvalidValue;

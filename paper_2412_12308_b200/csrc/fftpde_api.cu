@@ -8,8 +8,10 @@
 //     exp(-D k^2 dt) (ec:solCalorFourier PAPER.md:378-386) and the wave
 //     propagator quadrant (eq:OmegaZero/NonZero PAPER.md:459-471);
 //   * the pass sequence of each call (3 passes per solve step).
+#include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -32,6 +34,7 @@ struct fftpde_plan_s {
     // workspace offsets (bytes)
     size_t o_twx = 0, o_twy = 0, o_kx2 = 0, o_ky2 = 0, o_ex = 0, o_ey = 0, o_wc = 0, o_ws1 = 0, o_ws2 = 0;
     size_t o_twP = 0, o_twQ = 0, o_twN = 0;   // two-level column pass tables (P, Q > 0)
+    size_t o_scr = 0;                          // scratch: row spectra of 2 fields (multi-step solves)
     int64_t colP = 0, colQ = 0;
     std::vector<double> twP, twQ, twN;
     size_t need = 0;
@@ -50,6 +53,15 @@ struct fftpde_plan_s {
     std::vector<cudaEvent_t> event_pool;
     double prof_ms[FFTPDE_KERNEL_CLASSES] = {0};
     int64_t prof_n[FFTPDE_KERNEL_CLASSES] = {0};
+    // CUDA graphs of multi-step solves (one host launch per solve instead of 3 per step)
+    struct Graph {
+        std::array<uint64_t, 6> key;
+        cudaGraphExec_t exec;
+        int64_t launches;
+    };
+    std::vector<Graph> graphs;
+    cudaStream_t cap_stream = nullptr;
+    bool use_graphs = true;
 };
 
 namespace {
@@ -234,11 +246,23 @@ template <typename T> struct Passes {
     int64_t batch, stride;
     const void *twx() const { return p->ws + p->o_twx; }
     const void *twy() const { return p->ws + p->o_twy; }
-    cudaError_t rows(const void *in, void *out, int conj)
+    cudaError_t rows(const void *in, void *out, int inverse)
     {
         return launch(p, FFTPDE_KERNEL_ROW, [&] {
-            return launch_rows<T>(p->nx, in, out, p->ny, stride, batch, conj, twx(), p->stream);
+            return launch_rows<T>(p->nx, in, out, nullptr, p->ny, stride, batch, inverse ? ROW_INV : ROW_FWD,
+                                  twx(), p->stream);
         });
+    }
+    // inverse rows of step s (physical field -> phys) + forward rows of step s+1 (-> spec)
+    cudaError_t rows_mid(const void *in, void *spec, void *phys)
+    {
+        return launch(p, FFTPDE_KERNEL_ROW, [&] {
+            return launch_rows<T>(p->nx, in, spec, phys, p->ny, stride, batch, ROW_MID, twx(), p->stream);
+        });
+    }
+    void *scratch(int field) const
+    {
+        return p->ws + p->o_scr + (size_t)field * (size_t)(p->batch * p->nx * p->ny) * elem_cplx(p);
     }
     ColTw ctw() const
     {
@@ -287,15 +311,57 @@ template <typename T> struct Passes {
         if (e == cudaSuccess) e = rows(out, out, 1);
         return e;
     }
+    // nsteps diffusion steps: the row spectrum lives in the workspace scratch;
+    // between column passes one fused row pass writes the physical field of
+    // step s (materialised in u) and the row spectrum of step s+1.
+    cudaError_t diffuse(const void *u0, void *u, int64_t nsteps)
+    {
+        if (small()) {
+            cudaError_t e = cudaSuccess;
+            for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k)
+                e = small_op(k == 0 ? u0 : u, u, COL_DIFFUSE);
+            return e;
+        }
+        if (stride != p->nx * p->ny) {          // custom grid stride: in place, 3 passes per step
+            cudaError_t e = cudaSuccess;
+            for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) e = solve_step(k == 0 ? u0 : u, u, COL_DIFFUSE);
+            return e;
+        }
+        void *S = scratch(0);
+        cudaError_t e = rows(u0, S, 0);
+        for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) {
+            e = cols(S, S, COL_DIFFUSE);
+            if (e != cudaSuccess) break;
+            e = (k + 1 < nsteps) ? rows_mid(S, S, u) : rows(S, u, 1);
+        }
+        return e;
+    }
     cudaError_t wave(void *U, void *V, int64_t nsteps)
     {
-        cudaError_t e = cudaSuccess;
-        for (int64_t s = 0; s < nsteps && e == cudaSuccess; ++s) {
-            e = rows(U, U, 0);
-            if (e == cudaSuccess) e = rows(V, V, 0);
-            if (e == cudaSuccess) e = wave_cols(U, V);
-            if (e == cudaSuccess) e = rows(U, U, 1);
-            if (e == cudaSuccess) e = rows(V, V, 1);
+        if (stride != p->nx * p->ny) {          // custom grid stride: in place, 5 launches per step
+            cudaError_t e = cudaSuccess;
+            for (int64_t s = 0; s < nsteps && e == cudaSuccess; ++s) {
+                e = rows(U, U, 0);
+                if (e == cudaSuccess) e = rows(V, V, 0);
+                if (e == cudaSuccess) e = wave_cols(U, V);
+                if (e == cudaSuccess) e = rows(U, U, 1);
+                if (e == cudaSuccess) e = rows(V, V, 1);
+            }
+            return e;
+        }
+        void *SU = scratch(0), *SV = scratch(1);
+        cudaError_t e = rows(U, SU, 0);
+        if (e == cudaSuccess) e = rows(V, SV, 0);
+        for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) {
+            e = wave_cols(SU, SV);
+            if (e != cudaSuccess) break;
+            if (k + 1 < nsteps) {
+                e = rows_mid(SU, SU, U);
+                if (e == cudaSuccess) e = rows_mid(SV, SV, V);
+            } else {
+                e = rows(SU, U, 1);
+                if (e == cudaSuccess) e = rows(SV, V, 1);
+            }
         }
         return e;
     }
@@ -314,6 +380,54 @@ template <typename F> fftpde_status dispatch(fftpde_plan p, int64_t batch, int64
         e = f(ps);
     }
     return cuda_status(e);
+}
+
+// Run a multi-launch sequence through a cached CUDA graph.  The sequence is
+// captured once per (kind, buffers, batch, stride, nsteps) on a private stream
+// (the caller's stream may be the legacy default stream, which cannot be
+// captured) and replayed on the plan's stream; the kernels read their operator
+// tables by pointer, so new (D, dt) / (c, dt) need no re-capture.
+template <typename F>
+fftpde_status run_graphed(fftpde_plan p, const std::array<uint64_t, 6> &key, F &&enqueue)
+{
+    if (p->profiling || !p->use_graphs) return enqueue();
+    DeviceGuard g(p->device);
+    if (!g.ok) return FFTPDE_ERR_CUDA;
+    for (auto &gr : p->graphs) {
+        if (gr.key == key) {
+            p->launches += gr.launches;
+            return cuda_status(cudaGraphLaunch(gr.exec, p->stream));
+        }
+    }
+    if (!p->cap_stream && cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+        return FFTPDE_ERR_CUDA;
+    cudaStream_t user = p->stream;
+    const int64_t l0 = p->launches;
+    if (cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeRelaxed) != cudaSuccess)
+        return FFTPDE_ERR_CUDA;
+    p->stream = p->cap_stream;
+    fftpde_status st = enqueue();
+    p->stream = user;
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(p->cap_stream, &graph);
+    const int64_t n = p->launches - l0;
+    p->launches = l0;
+    if (st != FFTPDE_OK || e != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        return st != FFTPDE_OK ? st : FFTPDE_ERR_CUDA;
+    }
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return FFTPDE_ERR_CUDA;
+    if (p->graphs.size() >= 8) {
+        cudaGraphExecDestroy(p->graphs.front().exec);
+        p->graphs.erase(p->graphs.begin());
+    }
+    p->graphs.push_back({key, exec, n});
+    p->launches += n;
+    return cuda_status(cudaGraphLaunch(exec, p->stream));
 }
 
 fftpde_status ensure_diffusion_tables(fftpde_plan p, double D, double dt)
@@ -432,6 +546,7 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     p->Lx = Lx; p->Ly = Ly; p->device = device;
     p->qx = nx / 2 + 1;
     p->qy = ny / 2 + 1;
+    p->use_graphs = std::getenv("FFTPDE_NO_GRAPHS") == nullptr;
     build_twiddles(nx, p->twx);
     build_twiddles(ny, p->twy);
     build_k2(nx, Lx, p->kx2);
@@ -456,6 +571,7 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     p->o_wc = take(q);
     p->o_ws1 = take(q);
     p->o_ws2 = take(q);
+    p->o_scr = take(2 * (size_t)(batch * nx * ny) * ec);
     if (p->colP) {
         p->o_twP = take(p->twP.size() / 2 * ec);
         p->o_twQ = take(p->twQ.size() / 2 * ec);
@@ -515,6 +631,8 @@ fftpde_status fftpde_destroy(fftpde_plan plan)
     for (auto &v : plan->pending)
         for (auto &pr : v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     for (cudaEvent_t e : plan->event_pool) cudaEventDestroy(e);
+    for (auto &gr : plan->graphs) cudaGraphExecDestroy(gr.exec);
+    if (plan->cap_stream) cudaStreamDestroy(plan->cap_stream);
     delete plan;
     return FFTPDE_OK;
 }
@@ -597,11 +715,10 @@ fftpde_status fftpde_diffuse_batched(fftpde_plan p, const void *u0, void *u, int
         s = ensure_diffusion_tables(p, D, dt);
     }
     if (s != FFTPDE_OK) return s;
-    return dispatch(p, batch, stride, [&](auto &ps) {
-        cudaError_t e = cudaSuccess;
-        for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k)
-            e = ps.solve_step(k == 0 ? u0 : u, u, COL_DIFFUSE);
-        return e;
+    const std::array<uint64_t, 6> key{1, (uint64_t)(uintptr_t)u0, (uint64_t)(uintptr_t)u, (uint64_t)batch,
+                                      (uint64_t)stride, (uint64_t)nsteps};
+    return run_graphed(p, key, [&] {
+        return dispatch(p, batch, stride, [&](auto &ps) { return ps.diffuse(u0, u, nsteps); });
     });
 }
 
@@ -620,7 +737,11 @@ fftpde_status fftpde_wave_step_batched(fftpde_plan p, void *u, void *ut, int64_t
         s = ensure_wave_tables(p, c, dt);
     }
     if (s != FFTPDE_OK) return s;
-    return dispatch(p, batch, stride, [&](auto &ps) { return ps.wave(u, ut, nsteps); });
+    const std::array<uint64_t, 6> key{2, (uint64_t)(uintptr_t)u, (uint64_t)(uintptr_t)ut, (uint64_t)batch,
+                                      (uint64_t)stride, (uint64_t)nsteps};
+    return run_graphed(p, key, [&] {
+        return dispatch(p, batch, stride, [&](auto &ps) { return ps.wave(u, ut, nsteps); });
+    });
 }
 
 // ---- whole-plan entry points --------------------------------------------------

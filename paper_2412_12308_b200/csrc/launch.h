@@ -26,10 +26,12 @@ constexpr int64_t kMaxLen = 8192;   // single-pass axis length limit of this bui
 #endif
 
 // Row transforms of `batch` grids: length n along x, ny rows per grid, grids
-// `stride` elements apart.  conj != 0 gives the inverse direction (unscaled).
+// `stride` elements apart.  dir: ROW_FWD, ROW_INV (unscaled), or ROW_MID (inverse
+// stored to out2, then forward stored to out).
+enum RowDir { ROW_FWD = 0, ROW_INV = 4, ROW_MID = 5 };   // == PipeOp values
 template <typename T>
-cudaError_t launch_rows(int64_t n, const void *in, void *out, int64_t ny, int64_t stride,
-                        int64_t batch, int conj, const void *tw, cudaStream_t st);
+cudaError_t launch_rows(int64_t n, const void *in, void *out, void *out2, int64_t ny, int64_t stride,
+                        int64_t batch, int dir, const void *tw, cudaStream_t st);
 
 // Twiddle tables of the column axis: the single-level stage table of ny, and for
 // the two-level (cluster) column pass the stage tables of P and Q (ny = P Q)

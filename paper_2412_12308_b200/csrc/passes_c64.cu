@@ -2,7 +2,7 @@
 #include "dispatch.cuh"
 
 namespace fftpde {
-template cudaError_t launch_rows<float>(int64_t, const void *, void *, int64_t, int64_t, int64_t, int,
+template cudaError_t launch_rows<float>(int64_t, const void *, void *, void *, int64_t, int64_t, int64_t, int,
                                      const void *, cudaStream_t);
 template cudaError_t launch_cols<float>(int64_t, const void *, void *, int64_t, int64_t, int64_t, int,
                                      const ColTw &, const OpTables<float> &, cudaStream_t);

@@ -20,7 +20,10 @@ namespace fftpde {
 
 // PIPE_INV is the unscaled inverse (row pass); PIPE_INV_SCALED multiplies by
 // tab.scale = 1/(nx ny) first (standalone inverse column pass).
-enum PipeOp { PIPE_FWD = 0, PIPE_INV_SCALED = 1, PIPE_POISSON = 2, PIPE_DIFFUSE = 3, PIPE_INV = 4 };
+// PIPE_MID (rows): the inverse transform of step s (stored to out2: the
+// materialised physical field) followed by the forward transform of step s+1
+// (stored to out), one HBM read for both.
+enum PipeOp { PIPE_FWD = 0, PIPE_INV_SCALED = 1, PIPE_POISSON = 2, PIPE_DIFFUSE = 3, PIPE_INV = 4, PIPE_MID = 5 };
 
 template <int BYTES> __device__ __forceinline__ void cp_async_n(void *smem, const void *gmem)
 {
@@ -54,6 +57,7 @@ struct PipeArgs {
     int64_t ntiles;       // batch * ceil(nlines / W)
     int64_t groups;       // ceil(nlines / W)
     int op;               // PipeOp
+    void *out2;           // PIPE_MID: physical-field output (same layout as out)
 };
 
 // Per-line barrier: the TPT threads of line c (line-major thread layout).
@@ -89,7 +93,7 @@ pipe_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out, P
     const int lc = COLS ? tid % W : c;                        // load/store layout
     const int lt = COLS ? tid / W : t;
     const int64_t estep = (int64_t)TPT * a.elem_stride;
-    constexpr bool INV1 = OP == PIPE_INV || OP == PIPE_INV_SCALED;   // first transform inverse
+    constexpr bool INV1 = OP == PIPE_INV || OP == PIPE_INV_SCALED || OP == PIPE_MID;   // first transform inverse
     constexpr bool TWO = OP == PIPE_POISSON || OP == PIPE_DIFFUSE;   // forward, operator, inverse
     const LineSync<TPT> lsync{1 + c};
 
@@ -179,6 +183,16 @@ pipe_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out, P
                 }
             }
             fft_tw<N, true>(v, sm, t, twp, lsync);
+        }
+        if constexpr (OP == PIPE_MID) {
+            static_assert(!COLS, "PIPE_MID is a row pass");
+            const int64_t base = line_base(tile, c, t);
+            if (base >= 0) {
+                C *dst = opaque_ptr(reinterpret_cast<C *>(a.out2) + base);
+#pragma unroll
+                for (int e = 0; e < E; ++e) dst[e * estep] = v[e];
+            }
+            fft_tw<N, false>(v, sm, t, twp, lsync);
         }
         if constexpr (!COLS) {
             const int64_t base = line_base(tile, c, t);
