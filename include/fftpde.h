@@ -16,8 +16,12 @@
  * Forward transform: P_ab = sum_jk p_jk e^{+2 pi i aj/nx} e^{+2 pi i bk/ny},
  *   unnormalised (2D_DFT; eq:DFT PAPER.md:119-124; R1, R3).
  * Inverse transform: conjugate kernel times 1/(nx ny).
- * Axis lengths: powers of two, 1 <= n <= 8192 per axis in
- *   this build (larger -> FFTPDE_ERR_UNSUPPORTED).
+ * Axis lengths: powers of two, 1 <= n <= 32768 per axis.
+ *   Axes up to 8192 use one-CTA transforms; 16384 and 32768 use two-level
+ *   cluster passes, which for columns need nx >= 128 B / element size (8
+ *   columns for complex128, 16 for complex64); otherwise FFTPDE_ERR_UNSUPPORTED.
+ *   With two-level column passes (ny >= 2048 and such nx) the plain
+ *   transforms need the default grid stride nx*ny.
  *
  * Ownership: the caller owns every device buffer -- inputs, outputs and the
  *   workspace of fftpde_workspace_size() bytes (allocate it with torch).  The

@@ -231,65 +231,66 @@ col2_kernel(Col2Args<T> g, OpTables<T> tab)
         cluster_sync_acqrel();
         phaseA(true, false);
     } else if constexpr (OP == C2_FWD) {
-        // forward only: phase A, then phase B with the result written in natural
-        // order b = k1 + Q k2 (rows k1 + Q k2) once every item has read its input
-        phaseA(false, true);
-        cluster_sync_acqrel();
-        const int slot = tid / IB::TI, lt = tid % IB::TI;
-        const int c = lt % W, t = lt / W;
-        SmemView<C, SP::LOGE, 1> sm{smem + slot * IB::SLOT_ELEMS + c * IB::S};
-        const ItemSync<IB::TI> sync{1 + slot};
-        constexpr int E = SP::E, TPT = SP::TPT;
-        constexpr int ROUNDS = (Q + CL * IB::SLOTS - 1) / (CL * IB::SLOTS);
-        static_assert(ROUNDS * E <= 64, "forward-only column pass keeps all items in registers");
-        C v[ROUNDS][E];
+        // forward only, out of place: phase A in place on the source (a scratch
+        // buffer), phase B reads it and writes the natural order b = k1 + Q k2
+        // (rows k1 + Q k2) to the destination U
+        C *srcw = const_cast<C *>(g.in);
+        Col2Args<T> gs = g;
+        gs.U = srcw;
+        // phase A on the source
+        {
+            const int slot = tid / IA::TI, lt = tid % IA::TI;
+            const int c = lt % W, t = lt / W;
+            SmemView<C, SQ::LOGE, 1> sm{smem + slot * IA::SLOT_ELEMS + c * IA::S};
+            const ItemSync<IA::TI> sync{1 + slot};
+            constexpr int E = SQ::E, TPT = SQ::TPT;
+            for (int n1 = (int)rank * IA::SLOTS + slot; n1 < P; n1 += CL * IA::SLOTS) {
+                const int64_t r0 = base + (int64_t)(n1 + P * t) * g.nx + c;
+                const int64_t rstep = (int64_t)P * TPT * g.nx;
+                C v[E];
 #pragma unroll
-        for (int r = 0; r < ROUNDS; ++r) {
-            const int k1 = (int)rank * IB::SLOTS + slot + r * CL * IB::SLOTS;
-            if (k1 < Q) {
+                for (int e = 0; e < E; ++e) v[e] = ldcg(srcw + r0 + e * rstep);
+                fft<Q, false, EMAX>(v, sm, t, g.twQ, sync);
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = cmulw<false>(v[e], ldtw(g.twN + n1 * (t + TPT * e)));
+                C *dst = opaque_ptr(srcw + r0);
+#pragma unroll
+                for (int e = 0; e < E; ++e) dst[e * rstep] = v[e];
+            }
+        }
+        cluster_sync_acqrel();
+        {
+            const int slot = tid / IB::TI, lt = tid % IB::TI;
+            const int c = lt % W, t = lt / W;
+            SmemView<C, SP::LOGE, 1> sm{smem + slot * IB::SLOT_ELEMS + c * IB::S};
+            const ItemSync<IB::TI> sync{1 + slot};
+            constexpr int E = SP::E, TPT = SP::TPT;
+            for (int k1 = (int)rank * IB::SLOTS + slot; k1 < Q; k1 += CL * IB::SLOTS) {
+                C v[E];
                 const int64_t r0 = base + (int64_t)(P * k1 + t) * g.nx + c;
 #pragma unroll
-                for (int e = 0; e < E; ++e) v[r][e] = ldcg(g.U + r0 + e * (int64_t)TPT * g.nx);
-                fft<P, false, EMAX>(v[r], sm, t, g.twP, sync);
+                for (int e = 0; e < E; ++e) v[e] = ldcg(srcw + r0 + e * (int64_t)TPT * g.nx);
+                fft<P, false, EMAX>(v, sm, t, g.twP, sync);
+#pragma unroll
+                for (int e = 0; e < E; ++e) g.U[base + (int64_t)(k1 + Q * (t + TPT * e)) * g.nx + c] = v[e];
             }
         }
-        cluster_sync_acqrel();
-#pragma unroll
-        for (int r = 0; r < ROUNDS; ++r) {
-            const int k1 = (int)rank * IB::SLOTS + slot + r * CL * IB::SLOTS;
-            if (k1 < Q) {
-#pragma unroll
-                for (int e = 0; e < E; ++e)
-                    g.U[base + (int64_t)(k1 + Q * (t + TPT * e)) * g.nx + c] = v[r][e];
-            }
-        }
-    } else {  // C2_INV_SCALED: natural-order spectrum -> inverse along y, times 1/(nx ny)
-        const int slot = tid / IB::TI, lt = tid % IB::TI;
-        const int c = lt % W, t = lt / W;
-        SmemView<C, SP::LOGE, 1> sm{smem + slot * IB::SLOT_ELEMS + c * IB::S};
-        const ItemSync<IB::TI> sync{1 + slot};
-        constexpr int E = SP::E, TPT = SP::TPT;
-        constexpr int ROUNDS = (Q + CL * IB::SLOTS - 1) / (CL * IB::SLOTS);
-        static_assert(ROUNDS * E <= 64, "inverse-only column pass keeps all items in registers");
-        C v[ROUNDS][E];
-#pragma unroll
-        for (int r = 0; r < ROUNDS; ++r) {
-            const int k1 = (int)rank * IB::SLOTS + slot + r * CL * IB::SLOTS;
-            if (k1 < Q) {
+        (void)gs;
+    } else {  // C2_INV_SCALED, out of place: natural-order spectrum in g.in -> g.U, times 1/(nx ny)
+        {
+            const int slot = tid / IB::TI, lt = tid % IB::TI;
+            const int c = lt % W, t = lt / W;
+            SmemView<C, SP::LOGE, 1> sm{smem + slot * IB::SLOT_ELEMS + c * IB::S};
+            const ItemSync<IB::TI> sync{1 + slot};
+            constexpr int E = SP::E, TPT = SP::TPT;
+            for (int k1 = (int)rank * IB::SLOTS + slot; k1 < Q; k1 += CL * IB::SLOTS) {
+                C v[E];
 #pragma unroll
                 for (int e = 0; e < E; ++e)
-                    v[r][e] = cscale(ldcg(g.in + base + (int64_t)(k1 + Q * (t + TPT * e)) * g.nx + c), tab.scale);
-                fft<P, true, EMAX>(v[r], sm, t, g.twP, sync);
-            }
-        }
-        cluster_sync_acqrel();
+                    v[e] = cscale(ldcg(g.in + base + (int64_t)(k1 + Q * (t + TPT * e)) * g.nx + c), tab.scale);
+                fft<P, true, EMAX>(v, sm, t, g.twP, sync);
 #pragma unroll
-        for (int r = 0; r < ROUNDS; ++r) {
-            const int k1 = (int)rank * IB::SLOTS + slot + r * CL * IB::SLOTS;
-            if (k1 < Q) {
-#pragma unroll
-                for (int e = 0; e < E; ++e)
-                    g.U[base + (int64_t)(P * k1 + t + TPT * e) * g.nx + c] = v[r][e];
+                for (int e = 0; e < E; ++e) g.U[base + (int64_t)(P * k1 + t + TPT * e) * g.nx + c] = v[e];
             }
         }
         cluster_sync_acqrel();

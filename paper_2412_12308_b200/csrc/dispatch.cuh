@@ -6,6 +6,7 @@
 #include "kernels.cuh"
 #include "pipe.cuh"
 #include "col2.cuh"
+#include "row2.cuh"
 #ifndef FFTPDE_COL2_MINB
 #define FFTPDE_COL2_MINB 2
 #endif
@@ -164,8 +165,10 @@ cudaError_t small_n(const void *in, void *out, int64_t stride, int64_t batch, in
 // ---- two-level cluster column pass ------------------------------------------
 template <typename T, int P, int Q> struct Col2Cfg {
     using C = typename cplx_t<T>::type;
-    static constexpr int NT = 256;
     static constexpr int EMAX = FFTPDE_COL2_EMAX;
+    static constexpr int TIMAX = Col2Geom<C>::W * (Shape<P, EMAX>::TPT > Shape<Q, EMAX>::TPT
+                                                   ? Shape<P, EMAX>::TPT : Shape<Q, EMAX>::TPT);
+    static constexpr int NT = TIMAX > 256 ? TIMAX : 256;      // a CTA holds at least one item
     using IA = Col2Items<C, Q, NT, EMAX>;
     using IB = Col2Items<C, P, NT, EMAX>;
     static constexpr int CLA = P / IA::SLOTS, CLB = Q / IB::SLOTS;
@@ -174,7 +177,7 @@ template <typename T, int P, int Q> struct Col2Cfg {
     static constexpr size_t SA = (size_t)IA::SLOTS * IA::SLOT_ELEMS * sizeof(C);
     static constexpr size_t SB = (size_t)IB::SLOTS * IB::SLOT_ELEMS * sizeof(C);
     static constexpr size_t SMEM = SA > SB ? SA : SB;
-    static constexpr int MINB = FFTPDE_COL2_MINB;
+    static constexpr int MINB = NT > 256 ? 1 : FFTPDE_COL2_MINB;
 };
 
 template <typename T, int P, int Q, int OP>
@@ -223,7 +226,53 @@ cudaError_t launch_col2(int64_t ny, int64_t P, int op, Col2Args<T> g, int64_t ba
     case 2048: return col2_op<T, 32, 64>(op, g, batch, tab, st);
     case 4096: return col2_op<T, 64, 64>(op, g, batch, tab, st);
     case 8192: return col2_op<T, 64, 128>(op, g, batch, tab, st);
+    case 16384: return col2_op<T, 128, 128>(op, g, batch, tab, st);
+    case 32768: return col2_op<T, 128, 256>(op, g, batch, tab, st);
     default: (void)P; return cudaErrorInvalidValue;
+    }
+}
+
+template <typename T, int P, int Q, bool INV>
+cudaError_t row2_n(const void *in, void *out, int64_t ny, int64_t stride, int64_t batch,
+                   const ColTw &tw, cudaStream_t st)
+{
+    using C = typename cplx_t<T>::type;
+    constexpr int EMAX = FFTPDE_COL2_EMAX, CL = 8;
+    constexpr int NT = Col2Cfg<T, P, Q>::NT;
+    using Sm = Row2Smem<T, P, Q, NT, EMAX>;
+    auto k = row2_kernel<T, P, Q, INV, CL, NT, EMAX>;
+    static SmemOptIn<decltype(k)> opt;
+    cudaError_t e = opt(k, Sm::BYTES);
+    if (e != cudaSuccess) return e;
+    const int64_t nrows = ny * batch;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(CL * nrows), 1, 1);
+    cfg.blockDim = dim3(NT, 1, 1);
+    cfg.dynamicSmemBytes = Sm::BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k, (const C *)in, (C *)out, nrows, ny, stride, (const C *)tw.twP,
+                           (const C *)tw.twQ, (const C *)tw.twN);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_rows2(int64_t nx, const void *in, void *out, int64_t ny, int64_t stride,
+                         int64_t batch, int inverse, const ColTw &tw, cudaStream_t st)
+{
+    switch (nx) {
+    case 16384: return inverse ? row2_n<T, 128, 128, true>(in, out, ny, stride, batch, tw, st)
+                               : row2_n<T, 128, 128, false>(in, out, ny, stride, batch, tw, st);
+    case 32768: return inverse ? row2_n<T, 128, 256, true>(in, out, ny, stride, batch, tw, st)
+                               : row2_n<T, 128, 256, false>(in, out, ny, stride, batch, tw, st);
+    default: return cudaErrorInvalidValue;
     }
 }
 

@@ -37,6 +37,9 @@ struct fftpde_plan_s {
     size_t o_scr = 0;                          // scratch: row spectra of 2 fields (multi-step solves)
     int64_t colP = 0, colQ = 0;
     std::vector<double> twP, twQ, twN;
+    size_t o_rtwP = 0, o_rtwQ = 0, o_rtwN = 0;   // two-level row pass tables (nx > kMaxLen)
+    int64_t rowP = 0, rowQ = 0;
+    std::vector<double> rtwP, rtwQ, rtwN;
     size_t need = 0;
     int64_t qx = 0, qy = 0;   // quadrant extents nx/2+1, ny/2+1
     // host tables (fp64)
@@ -246,9 +249,15 @@ template <typename T> struct Passes {
     int64_t batch, stride;
     const void *twx() const { return p->ws + p->o_twx; }
     const void *twy() const { return p->ws + p->o_twy; }
+    ColTw rtw() const
+    {
+        return ColTw{twx(), p->ws + p->o_rtwP, p->ws + p->o_rtwQ, p->ws + p->o_rtwN};
+    }
     cudaError_t rows(const void *in, void *out, int inverse)
     {
         return launch(p, FFTPDE_KERNEL_ROW, [&] {
+            if (p->rowP)   // long rows: two-level cluster pass
+                return launch_rows2<T>(p->nx, in, out, p->ny, stride, batch, inverse, rtw(), p->stream);
             return launch_rows<T>(p->nx, in, out, nullptr, p->ny, stride, batch, inverse ? ROW_INV : ROW_FWD,
                                   twx(), p->stream);
         });
@@ -256,6 +265,10 @@ template <typename T> struct Passes {
     // inverse rows of step s (physical field -> phys) + forward rows of step s+1 (-> spec)
     cudaError_t rows_mid(const void *in, void *spec, void *phys)
     {
+        if (p->rowP) {     // long rows: two launches
+            cudaError_t e = rows(in, phys, 1);
+            return e == cudaSuccess ? rows(phys, spec, 0) : e;
+        }
         return launch(p, FFTPDE_KERNEL_ROW, [&] {
             return launch_rows<T>(p->nx, in, spec, phys, p->ny, stride, batch, ROW_MID, twx(), p->stream);
         });
@@ -297,9 +310,15 @@ template <typename T> struct Passes {
         if (e == cudaSuccess) e = rows(out, out, 1);
         return e;
     }
+    // plain transforms; the two-level column pass is out of place through the scratch
     cudaError_t forward(const void *in, void *out)
     {
         if (small()) return small_op(in, out, COL_FWD);
+        if (p->colP) {
+            void *S = scratch(0);
+            cudaError_t e = rows(in, S, 0);
+            return e == cudaSuccess ? cols(S, out, COL_FWD) : e;
+        }
         cudaError_t e = rows(in, out, 0);
         if (e == cudaSuccess) e = cols(out, out, COL_FWD);
         return e;
@@ -307,6 +326,11 @@ template <typename T> struct Passes {
     cudaError_t inverse(const void *in, void *out)
     {
         if (small()) return small_op(in, out, COL_INV);
+        if (p->colP) {
+            void *S = scratch(0);
+            cudaError_t e = cols(in, S, COL_INV);
+            return e == cudaSuccess ? rows(S, out, 1) : e;
+        }
         cudaError_t e = cols(in, out, COL_INV);
         if (e == cudaSuccess) e = rows(out, out, 1);
         return e;
@@ -503,8 +527,17 @@ void fftpde::col2_split(int64_t ny, int64_t nx, int elem_bytes, int64_t &P, int6
     case 2048: P = 32; Q = 64; break;
     case 4096: P = 64; Q = 64; break;
     case 8192: P = 64; Q = 128; break;
+    case 16384: P = 128; Q = 128; break;
+    case 32768: P = 128; Q = 256; break;
     default: break;
     }
+}
+
+void fftpde::row2_split(int64_t nx, int64_t &P, int64_t &Q)
+{
+    P = Q = 0;
+    if (nx == 16384) { P = 128; Q = 128; }
+    if (nx == 32768) { P = 128; Q = 256; }
 }
 
 // ============================================================================
@@ -536,7 +569,12 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     if (nx < 0 || ny < 0 || batch < 0) return FFTPDE_ERR_INVALID_ARG;
     if (!is_pow2(nx)) return FFTPDE_ERR_NOT_POW2_X;
     if (!is_pow2(ny)) return FFTPDE_ERR_NOT_POW2_Y;
-    if (nx > kMaxLen || ny > kMaxLen || batch > 65535) return FFTPDE_ERR_UNSUPPORTED;
+    if (nx > kMaxLen2 || ny > kMaxLen2 || batch > 65535) return FFTPDE_ERR_UNSUPPORTED;
+    if (ny > kMaxLen) {   // long columns need the two-level pass: whole 128-byte column blocks
+        int64_t P, Q;
+        fftpde::col2_split(ny, nx, dtype == FFTPDE_C128 ? 16 : 8, P, Q);
+        if (!P) return FFTPDE_ERR_UNSUPPORTED;
+    }
     if (!std::isfinite(Lx) || !std::isfinite(Ly) || !(Lx > 0) || !(Ly > 0)) return FFTPDE_ERR_INVALID_ARG;
     if (device < 0) return FFTPDE_ERR_INVALID_ARG;
 
@@ -557,6 +595,12 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
         build_twiddles(p->colQ, p->twQ, FFTPDE_COL2_EMAX);
         build_plain_twiddles(ny, p->twN);
     }
+    fftpde::row2_split(nx, p->rowP, p->rowQ);
+    if (p->rowP) {
+        build_twiddles(p->rowP, p->rtwP, FFTPDE_COL2_EMAX);
+        build_twiddles(p->rowQ, p->rtwQ, FFTPDE_COL2_EMAX);
+        build_plain_twiddles(nx, p->rtwN);
+    }
 
     const size_t er = elem_real(p), ec = elem_cplx(p);
     size_t off = 0;
@@ -572,6 +616,11 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     p->o_ws1 = take(q);
     p->o_ws2 = take(q);
     p->o_scr = take(2 * (size_t)(batch * nx * ny) * ec);
+    if (p->rowP) {
+        p->o_rtwP = take(p->rtwP.size() / 2 * ec);
+        p->o_rtwQ = take(p->rtwQ.size() / 2 * ec);
+        p->o_rtwN = take(p->rtwN.size() / 2 * ec);
+    }
     if (p->colP) {
         p->o_twP = take(p->twP.size() / 2 * ec);
         p->o_twQ = take(p->twQ.size() / 2 * ec);
@@ -613,6 +662,11 @@ fftpde_status fftpde_set_workspace(fftpde_plan plan, void *dev_ptr, size_t bytes
     } else {
         s = upload(plan, plan->o_twx, plan->twx);
         if (s == FFTPDE_OK) s = upload(plan, plan->o_twy, plan->twy);
+    }
+    if (s == FFTPDE_OK && plan->rowP) {
+        s = upload(plan, plan->o_rtwP, plan->rtwP);
+        if (s == FFTPDE_OK) s = upload(plan, plan->o_rtwQ, plan->rtwQ);
+        if (s == FFTPDE_OK) s = upload(plan, plan->o_rtwN, plan->rtwN);
     }
     if (s == FFTPDE_OK && plan->colP) {
         s = upload(plan, plan->o_twP, plan->twP);
@@ -674,6 +728,7 @@ fftpde_status fftpde_forward_batched(fftpde_plan p, const void *in, void *out, i
                                      int64_t stride)
 {
     fftpde_status s = check_call(p, batch, stride);
+    if (s == FFTPDE_OK && p->colP && stride != p->nx * p->ny) s = FFTPDE_ERR_UNSUPPORTED;
     if (s == FFTPDE_OK) s = check_ptr(p, in);
     if (s == FFTPDE_OK) s = check_ptr(p, out);
     if (s != FFTPDE_OK) return s;
@@ -684,6 +739,7 @@ fftpde_status fftpde_inverse_batched(fftpde_plan p, const void *in, void *out, i
                                      int64_t stride)
 {
     fftpde_status s = check_call(p, batch, stride);
+    if (s == FFTPDE_OK && p->colP && stride != p->nx * p->ny) s = FFTPDE_ERR_UNSUPPORTED;
     if (s == FFTPDE_OK) s = check_ptr(p, in);
     if (s == FFTPDE_OK) s = check_ptr(p, out);
     if (s != FFTPDE_OK) return s;

@@ -17,7 +17,8 @@ template <typename T> struct OpTables {
     T scale;                 // 1/(nx ny)
 };
 
-constexpr int64_t kMaxLen = 8192;   // single-pass axis length limit of this build
+constexpr int64_t kMaxLen = 8192;    // single-CTA (one pass) axis length limit
+constexpr int64_t kMaxLen2 = 32768;  // two-level (cluster) axis length limit
 
 // radix (elements per thread) of the sub-transforms of the two-level column pass;
 // the host builds its P and Q twiddle tables for the same factorisation
@@ -43,6 +44,14 @@ struct ColTw {
 
 // Split ny = P * Q used by the two-level column pass (P = Q = 0: not used).
 void col2_split(int64_t ny, int64_t nx, int elem_bytes, int64_t &P, int64_t &Q);
+// Split nx = P * Q of the two-level row pass (rows longer than kMaxLen).
+void row2_split(int64_t nx, int64_t &P, int64_t &Q);
+
+// Two-level row pass (nx = P Q > kMaxLen): inverse != 0 selects the conjugate
+// kernel (unscaled).  Tables: stage tables of P and Q, plain w_nx^m.
+template <typename T>
+cudaError_t launch_rows2(int64_t nx, const void *in, void *out, int64_t ny, int64_t stride,
+                         int64_t batch, int inverse, const ColTw &tw, cudaStream_t st);
 
 // Column pass along y (length ny) over nx columns, op in ColOp.
 template <typename T>

@@ -61,7 +61,14 @@ def test_spec_examples_through_abi():
 
 
 def _lengths():
-    return [2 ** k for k in range(0, 14)]
+    return [2 ** k for k in range(0, 16)]
+
+
+def _shapes(n):
+    if n <= 8192:
+        return {(n, min(8192, max(1, 2 ** 18 // n))), (min(8192, max(1, 2 ** 18 // n)), n), (n, 2), (2, n)}
+    # two-level cluster passes: long columns need whole 128-byte column blocks
+    return {(n, 16), (16, n), (2, n), (n, 32)}
 
 
 @pytest.mark.parametrize("dtype", [C128, C64])
@@ -69,8 +76,7 @@ def _lengths():
 def test_forward_inverse_every_length_both_axes(dtype, n):
     # length n along y with a few x lengths, and along x with a few y lengths;
     # batch 3 so CTAs span grid boundaries
-    for (ny, nx) in {(n, min(8192, max(1, 2 ** 18 // n))), (min(8192, max(1, 2 ** 18 // n)), n),
-                     (n, 2), (2, n)}:
+    for (ny, nx) in _shapes(n):
         B = 3 if nx * ny <= 2 ** 16 else 1
         x = noise((B, ny, nx), 1000 + n + nx, dtype)
         p = F.Plan(nx, ny, batch=B, dtype=dtype)
@@ -127,6 +133,24 @@ def test_poisson_shapes(dtype, shape):
     p = F.Plan(nx, ny, batch=2, dtype=dtype, Lx=Lx, Ly=Ly)
     u = host(p.poisson(dev(x, dtype)))
     assert rel(u, O.poisson(x.astype(np.complex128), Lx, Ly)) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", [C128, C64])
+@pytest.mark.parametrize("shape", [(32768, 16), (16, 32768), (16384, 32), (8, 16384)])
+def test_long_axes_solvers(dtype, shape):
+    # two-level (cluster) row and column passes inside the solvers
+    ny, nx = shape
+    x = noise((ny, nx), 77 + nx, dtype)
+    p = F.Plan(nx, ny, dtype=dtype, Lx=1.0, Ly=2.0)
+    u = host(p.poisson(dev(x, dtype)))
+    assert rel(u, O.poisson(x.astype(np.complex128), 1.0, 2.0)) <= TOL[dtype]
+    d = host(p.diffuse(dev(x, dtype), 1e-6, 0.01, 3))
+    assert rel(d, O.diffuse(x.astype(np.complex128), 1e-6, 0.01, 3, 1.0, 2.0)) <= TOL[dtype]
+    uu, vv = dev(x, dtype), dev(noise((ny, nx), 78, dtype), dtype)
+    v0 = host(vv)
+    p.wave_step(uu, vv, 0.3, 1e-4, 2)
+    uo, vo = O.wave(x.astype(np.complex128), v0, 0.3, 1e-4, 2, 1.0, 2.0)
+    assert rel(host(uu), uo) <= TOL[dtype] and rel(host(vv), vo) <= 10 * TOL[dtype]
 
 
 # ---------------------------------------------------------------- C2 diffusion
