@@ -240,6 +240,44 @@ def test_wave_zero_speed_and_zero_steps():
     p.wave_step(u, v, 1.0, 0.5, 0)
 
 
+# ---------------------------------------------------------------- C5 diffusion 32768^2
+
+def heat_kernel_points(ks, js, n, centres, sigmas, amps, D, T):
+    """Exact periodic heat-kernel solution at grid points (k, j): each Gaussian
+    A exp(-r^2/s^2) becomes A s^2/(s^2+4DT) exp(-r^2/(s^2+4DT)) (minimum image
+    suffices: s^2 + 4DT < 2e-4, so images at distance >= 0.5 are below e^-1000)."""
+    x = js / n
+    y = ks / n
+    out = np.zeros(len(ks))
+    for (cx, cy), s, a in zip(centres, sigmas, amps):
+        s2 = s * s + 4 * D * T
+        dx = np.mod(x - cx + 0.5, 1.0) - 0.5
+        dy = np.mod(y - cy + 0.5, 1.0) - 0.5
+        out += a * (s * s / s2) * np.exp(-(dx * dx + dy * dy) / s2)
+    return out
+
+
+def test_c5_diffusion_full_size_sampled_closed_form():
+    # BASELINE configs[4] on one GPU: 32768^2 complex128, D = 1e-4, dt = 0.01, 20 steps
+    n, D, dt, steps = 32768, 1e-4, 0.01, 20
+    u0, centres, sigmas, amps = I.c5_field_torch(n)
+    p = F.Plan(n, n, dtype=C128)
+    u = p.diffuse(u0, D, dt, steps)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(5)
+    ks = rng.integers(0, n, 3000)
+    js = rng.integers(0, n, 3000)
+    # points near the Gaussian centres too (where the field is large)
+    ks = np.concatenate([ks, np.round(centres[:500, 1] * n).astype(int) % n])
+    js = np.concatenate([js, np.round(centres[:500, 0] * n).astype(int) % n])
+    got = u[torch.from_numpy(ks).cuda(), torch.from_numpy(js).cuda()].cpu().numpy()
+    exact = heat_kernel_points(ks, js, n, centres, sigmas, amps, D, steps * dt)
+    assert np.linalg.norm(got - exact) / np.linalg.norm(exact) <= 1e-12
+    assert np.max(np.abs(got.imag)) <= 1e-14
+    m0 = u0.real.double().mean().item()
+    assert abs(u.real.double().mean().item() / m0 - 1) <= 1e-12      # mean conservation (Fig. 4)
+
+
 # ---------------------------------------------------------------- C4 batched Poisson
 
 def test_c4_batched_poisson_full_batch_sampled():
