@@ -151,6 +151,31 @@ fftpde_status fftpde_wave_step_batched(fftpde_plan plan, void *u, void *ut,
                                        int64_t batch, int64_t stride,
                                        double c, double dt, int64_t nsteps);
 
+/* ---- slab (sharded) building blocks ------------------------------------------
+ * The slab decomposition of SURVEY.md 8(e): rank r of P owns rows
+ * [r ny/P, (r+1) ny/P); one step is rows -> all-to-all -> column slab pass ->
+ * all-to-all -> inverse rows.  These calls are the per-rank pieces; the
+ * exchange is done by the caller (torch.distributed / NCCL).
+ *
+ * fftpde_rows: transforms of `nrows` contiguous rows of length nx (any
+ *   nrows >= 1) along x; inverse != 0 selects the conjugate kernel (unscaled).
+ * fftpde_cols_slab: the column pass of a column slab: in/out hold the ncols
+ *   columns col0 .. col0+ncols-1 of all ny rows, row-major with row length
+ *   ncols (in == out allowed).  op = FFTPDE_OP_POISSON or FFTPDE_OP_DIFFUSE:
+ *   forward along y, the multiplier at the GLOBAL wavenumbers (k_x of column
+ *   col0 + c), inverse along y, 1/(nx ny) folded in (D, dt used by DIFFUSE).
+ *   ncols must be a power of two dividing nx; col0 a multiple of ncols.
+ * fftpde_pack_blocks: direction 0: [nrows][nblocks][bw] -> [nblocks][nrows][bw]
+ *   (row slab -> per-peer send blocks); direction 1: the inverse.  bw in
+ *   elements, bw * element size a multiple of 16 bytes. */
+#define FFTPDE_OP_POISSON 2
+#define FFTPDE_OP_DIFFUSE 3
+fftpde_status fftpde_rows(fftpde_plan plan, const void *in, void *out, int64_t nrows, int inverse);
+fftpde_status fftpde_cols_slab(fftpde_plan plan, const void *in, void *out, int64_t col0, int64_t ncols,
+                               int op, double D, double dt);
+fftpde_status fftpde_pack_blocks(fftpde_plan plan, const void *in, void *out, int64_t nrows,
+                                 int64_t nblocks, int64_t bw, int direction);
+
 #ifdef __cplusplus
 }
 #endif

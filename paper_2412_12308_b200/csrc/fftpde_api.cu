@@ -800,6 +800,87 @@ fftpde_status fftpde_wave_step_batched(fftpde_plan p, void *u, void *ut, int64_t
     });
 }
 
+// ---- slab building blocks --------------------------------------------------------
+fftpde_status fftpde_rows(fftpde_plan p, const void *in, void *out, int64_t nrows, int inverse)
+{
+    if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (!p->ws) return FFTPDE_ERR_WORKSPACE;
+    if (nrows == 0) return FFTPDE_ERR_EMPTY;
+    if (nrows < 0) return FFTPDE_ERR_INVALID_ARG;
+    fftpde_status s = check_ptr(p, in);
+    if (s == FFTPDE_OK) s = check_ptr(p, out);
+    if (s != FFTPDE_OK) return s;
+    DeviceGuard g(p->device);
+    if (!g.ok) return FFTPDE_ERR_CUDA;
+    cudaError_t e;
+    if (p->dtype == FFTPDE_C128) {
+        Passes<double> ps{p, 1, nrows * p->nx};
+        const int64_t ny0 = p->ny;
+        p->ny = nrows;                     // the row pass only uses ny as the row count
+        e = ps.rows(in, out, inverse);
+        p->ny = ny0;
+    } else {
+        Passes<float> ps{p, 1, nrows * p->nx};
+        const int64_t ny0 = p->ny;
+        p->ny = nrows;
+        e = ps.rows(in, out, inverse);
+        p->ny = ny0;
+    }
+    return cuda_status(e);
+}
+
+fftpde_status fftpde_cols_slab(fftpde_plan p, const void *in, void *out, int64_t col0, int64_t ncols,
+                               int op, double D, double dt)
+{
+    if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (!p->ws) return FFTPDE_ERR_WORKSPACE;
+    if (ncols == 0) return FFTPDE_ERR_EMPTY;
+    if (ncols < 0 || !is_pow2(ncols) || p->nx % ncols || col0 < 0 || col0 % ncols || col0 + ncols > p->nx)
+        return FFTPDE_ERR_INVALID_ARG;
+    if (op != COL_POISSON && op != COL_DIFFUSE) return FFTPDE_ERR_INVALID_ARG;
+    fftpde_status s = check_ptr(p, in);
+    if (s == FFTPDE_OK) s = check_ptr(p, out);
+    if (s != FFTPDE_OK) return s;
+    if (op == COL_DIFFUSE) {
+        if (!std::isfinite(D) || !std::isfinite(dt) || D < 0 || dt < 0) return FFTPDE_ERR_INVALID_ARG;
+        DeviceGuard g(p->device);
+        s = ensure_diffusion_tables(p, D, dt);
+        if (s != FFTPDE_OK) return s;
+    }
+    int64_t P2, Q2;
+    fftpde::col2_split(p->ny, ncols, (int)elem_cplx(p), P2, Q2);
+    if (p->ny > kMaxLen && !P2) return FFTPDE_ERR_UNSUPPORTED;
+    DeviceGuard g(p->device);
+    if (!g.ok) return FFTPDE_ERR_CUDA;
+    cudaError_t e;
+    const ColTw ctw{p->ws + p->o_twy, p->ws + p->o_twP, p->ws + p->o_twQ, p->ws + p->o_twN};
+    auto run = [&](auto tag) {
+        using T = decltype(tag);
+        OpTables<T> t = tables<T>(p);
+        t.kx2 += col0;             // global column col0 + c
+        t.ex += col0;
+        return launch(p, FFTPDE_KERNEL_COL, [&] {
+            return launch_cols<T>(p->ny, in, out, ncols, ncols * p->ny, 1, op, ctw, t, p->stream);
+        });
+    };
+    if (p->colP == 0 && P2) return FFTPDE_ERR_UNSUPPORTED;   // two-level tables not built for this plan
+    e = p->dtype == FFTPDE_C128 ? run(0.0) : run(0.0f);
+    return cuda_status(e);
+}
+
+fftpde_status fftpde_pack_blocks(fftpde_plan p, const void *in, void *out, int64_t nrows, int64_t nblocks,
+                                 int64_t bw, int direction)
+{
+    if (!p || !in || !out || in == out || nrows < 0 || nblocks < 0 || bw <= 0 || (direction != 0 && direction != 1))
+        return FFTPDE_ERR_INVALID_ARG;
+    const int64_t bytes = bw * (int64_t)elem_cplx(p);
+    if (bytes % 16 || ((uintptr_t)in & 15u) || ((uintptr_t)out & 15u)) return FFTPDE_ERR_INVALID_ARG;
+    DeviceGuard g(p->device);
+    if (!g.ok) return FFTPDE_ERR_CUDA;
+    ++p->launches;
+    return cuda_status(launch_pack(in, out, nrows, nblocks, bytes, direction, p->stream));
+}
+
 // ---- whole-plan entry points --------------------------------------------------
 fftpde_status fftpde_forward(fftpde_plan p, const void *in, void *out)
 {

@@ -72,4 +72,8 @@ cudaError_t launch_small(int64_t nx, int64_t ny, const void *in, void *out, int6
                          int64_t batch, int op, const void *twx, const void *twy,
                          const OpTables<T> &tab, cudaStream_t st);
 
+// Block transpose of the sharded path (pack.cu); bw_bytes a multiple of 16.
+cudaError_t launch_pack(const void *in, void *out, int64_t nrows, int64_t nblocks, int64_t bw_bytes,
+                        int direction, cudaStream_t st);
+
 } // namespace fftpde

@@ -34,7 +34,9 @@ EXPORTS = [
     "fftpde_forward", "fftpde_inverse", "fftpde_poisson", "fftpde_diffuse", "fftpde_wave_step",
     "fftpde_forward_batched", "fftpde_inverse_batched", "fftpde_poisson_batched",
     "fftpde_diffuse_batched", "fftpde_wave_step_batched",
+    "fftpde_rows", "fftpde_cols_slab", "fftpde_pack_blocks",
 ]
+OP_POISSON, OP_DIFFUSE = 2, 3
 
 
 class FFTPDEError(RuntimeError):
@@ -77,6 +79,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fftpde_poisson_batched": (st, [p, p, p, i64, i64]),
         "fftpde_diffuse_batched": (st, [p, p, p, i64, i64, dbl, dbl, i64]),
         "fftpde_wave_step_batched": (st, [p, p, p, i64, i64, dbl, dbl, i64]),
+        "fftpde_rows": (st, [p, p, p, i64, u]),
+        "fftpde_cols_slab": (st, [p, p, p, i64, i64, u, dbl, dbl]),
+        "fftpde_pack_blocks": (st, [p, p, p, i64, i64, i64, u]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -264,3 +269,32 @@ class Plan:
         if host:
             return self._finish(ud, True), self._finish(vd, True)
         return ud, vd
+
+    # -- slab (sharded) building blocks ------------------------------------------------
+    def rows(self, x: torch.Tensor, out: torch.Tensor, inverse: bool = False):
+        """Transforms along x of the rows of a [nrows, nx] device slab (any nrows)."""
+        if x.dim() != 2 or x.shape[1] != self.nx or out.shape != x.shape or x.dtype != self.dtype:
+            raise ValueError("rows: expected matching [nrows, nx] tensors of the plan's dtype")
+        self._bind_stream()
+        _check(self.lib.fftpde_rows(self._h, x.data_ptr(), out.data_ptr(), x.shape[0], int(inverse)),
+               "fftpde_rows")
+        return out
+
+    def cols_slab(self, x: torch.Tensor, out: torch.Tensor, col0: int, op: int, D: float = 0.0,
+                  dt: float = 0.0):
+        """Column pass (forward, operator at the global wavenumbers, inverse) of a
+        [ny, ncols] column slab holding global columns col0 .. col0+ncols-1."""
+        if x.dim() != 2 or x.shape[0] != self.ny or out.shape != x.shape or x.dtype != self.dtype:
+            raise ValueError("cols_slab: expected matching [ny, ncols] tensors of the plan's dtype")
+        self._bind_stream()
+        _check(self.lib.fftpde_cols_slab(self._h, x.data_ptr(), out.data_ptr(), int(col0), x.shape[1],
+                                         int(op), float(D), float(dt)), "fftpde_cols_slab")
+        return out
+
+    def pack_blocks(self, x: torch.Tensor, out: torch.Tensor, nrows: int, nblocks: int, bw: int,
+                    direction: int):
+        """[nrows][nblocks][bw] <-> [nblocks][nrows][bw] (direction 0 / 1)."""
+        self._bind_stream()
+        _check(self.lib.fftpde_pack_blocks(self._h, x.data_ptr(), out.data_ptr(), int(nrows), int(nblocks),
+                                           int(bw), int(direction)), "fftpde_pack_blocks")
+        return out

@@ -52,7 +52,10 @@ def test_plan_validation(lib):
     assert plan(lib, 64, 64, batch=0)[0] == F.ERR_EMPTY
     assert plan(lib, 12, 64)[0] == F.ERR_NOT_POW2_X          # offending axis named
     assert plan(lib, 64, 48)[0] == F.ERR_NOT_POW2_Y
-    assert plan(lib, 16384, 64)[0] == F.ERR_UNSUPPORTED
+    assert plan(lib, 65536, 64)[0] == F.ERR_UNSUPPORTED          # longer than 2^15
+    assert plan(lib, 32768, 64)[0] == F.OK                       # two-level row pass
+    assert plan(lib, 4, 16384)[0] == F.ERR_UNSUPPORTED           # long columns need 8 columns (c128)
+    assert plan(lib, 8, 16384)[0] == F.OK
     assert plan(lib, 64, 64, dtype=7)[0] == F.ERR_INVALID_ARG
     assert plan(lib, 64, 64, Lx=0.0)[0] == F.ERR_INVALID_ARG
     assert plan(lib, 64, 64, Ly=float("nan"))[0] == F.ERR_INVALID_ARG
