@@ -62,6 +62,8 @@ def parse_args():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="c5: use the slab-decomposed path even on one GPU (P = 1 process group)")
     return ap.parse_args()
 
 
@@ -348,6 +350,75 @@ def native(args, wl, world, rank, local):
     return line
 
 
+def sharded_native(args, wl, world, rank, local):
+    """C5 at N > 1: the slab decomposition, NCCL all-to-all between
+    the libfftpde row and column-slab passes; strong scaling (fixed 32768^2 grid)."""
+    import torch
+    from paper_2412_12308_b200 import inputs as I
+    from paper_2412_12308_b200 import sharded as S
+    dtype = torch.complex128
+    full, _, _, _ = I.c5_field_torch(wl.nx, dtype=dtype)
+    lo, hi = S.slab_rows(wl.ny, world, rank)
+    slab = full[lo:hi].contiguous()
+    del full
+    torch.cuda.empty_cache()
+    ops = S.CudaLocalOps(wl.nx, wl.ny, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly)
+    solver = S.SlabSolver(wl.nx, wl.ny, S.DistComm(), ops)
+    out = [torch.empty_like(slab)]
+    for _ in range(args.warmup):
+        solver.diffuse([slab], wl.D, wl.dt, wl.nsteps, outs=out)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    l0 = ops.launches
+    barrier(world)
+    torch.cuda.synchronize()
+    gpu_index = torch.cuda.current_device()
+    vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+    smi_index = int(vis[gpu_index]) if len(vis) > gpu_index and vis[gpu_index].isdigit() else gpu_index
+    with ClockSampler(smi_index) as clk:
+        for i in range(args.steps):
+            starts[i].record(stream)
+            solver.diffuse([slab], wl.D, wl.dt, wl.nsteps, outs=out)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms_total = max_over_ranks(world, sum(a.elapsed_time(b) for a, b in zip(starts, ends)))
+    pts = wl.nx * wl.ny * wl.nsteps
+    value = pts * args.steps / (ms_total * 1e-3)
+    ops.plan.read_profile()
+    ops.plan.set_profiling(True)
+    solver.diffuse([slab], wl.D, wl.dt, wl.nsteps, outs=out)
+    torch.cuda.synchronize()
+    prof = ops.plan.read_profile()
+    ops.plan.set_profiling(False)
+    dom_name, (dom_ms, dom_n) = max(prof.items(), key=lambda kv: kv[1][0])
+    slab_bytes = (hi - lo) * wl.nx * 16
+    achieved = 2 * slab_bytes / (dom_ms / dom_n * 1e-3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs", 6650.0)
+    a2a_bytes = slab_bytes * (world - 1) // world
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded C5 recipe, built on device)",
+        "config": {**workload_config(wl, world), "parallelism": f"slab x{world} (NCCL all-to-all)",
+                   "l2": "field (16 GiB) larger than L2"},
+        "e2e": None, "cpu_baseline": None, "clocks": clk.summary(),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None, "kernel": dom_name,
+                     "per_kernel_ms_per_solve": {k: round(v[0], 3) for k, v in prof.items()},
+                     "alltoall_bytes_per_rank": a2a_bytes, "alltoalls_per_solve": 2 * wl.nsteps},
+        "gpu_launches": ops.launches - l0,
+    }
+
+
 def alg_step_bytes(wl):
     """Algorithmic bytes of one bench step: each state field read + written once per
     solve step."""
@@ -459,6 +530,7 @@ def reference(args, wl, world, rank):
 
 def main():
     args = parse_args()
+    import torch
     from paper_2412_12308_b200 import inputs as I
     wl = I.WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -471,10 +543,17 @@ def main():
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     world, rank, local = dist_setup(args.gpus)
-    line = native(args, wl, world, rank, local)
+    if args.sharded and world == 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29533", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    if wl.name.startswith("c5") and (world > 1 or args.sharded):
+        line = sharded_native(args, wl, world, rank, local)
+    else:
+        line = native(args, wl, world, rank, local)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch.distributed as dist
         dist.destroy_process_group()
 
