@@ -7,6 +7,7 @@
 #include "pipe.cuh"
 #include "col2.cuh"
 #include "row2.cuh"
+#include "line.cuh"
 #ifndef FFTPDE_COL2_MINB
 #define FFTPDE_COL2_MINB 2
 #endif
@@ -91,13 +92,49 @@ cudaError_t pipe_n(const void *in, void *out, PipeArgs args, const void *tw, con
     return cudaGetLastError();
 }
 
+// ---- occupancy-oriented line pass (line.cuh) ----------------------------------
+// Shapes measured faster than the persistent pipe_kernel on B200
+// (tools/exp_line.cu, profiles/r01/exp_line.txt); E = 0: use pipe_kernel.
+template <typename T, int N, bool COLS> struct LinePolicy {
+    static constexpr bool C64 = sizeof(T) == 4;
+    static constexpr int E = (C64 && N == 512) ? (COLS ? 8 : 16) : 0;
+    static constexpr int W = COLS ? 8 : 4;
+    static constexpr int MINB = COLS ? 3 : 2;
+};
+
+template <typename T, int N, int E, int W, bool COLS, int OP, int MINB>
+cudaError_t line_n(const void *in, void *out, void *out2, int64_t nlines, int64_t line_stride, int64_t elem_stride,
+                   int64_t stride, int64_t batch, const void *tw, const OpTables<T> &tab, cudaStream_t st)
+{
+    using C = typename cplx_t<T>::type;
+    using L = LineSmem<C, N, E, W, COLS>;
+    auto k = line_kernel<T, N, E, W, COLS, OP, MINB>;
+    static SmemOptIn<decltype(k)> opt;
+    cudaError_t e = opt(k, L::BYTES);
+    if (e != cudaSuccess) return e;
+    LineArgs a{nlines, line_stride, elem_stride, stride, (nlines + W - 1) / W, out2};
+    const int64_t grid = batch * a.groups;
+    k<<<(unsigned)grid, W * (N / E), L::BYTES, st>>>((const C *)in, (C *)out, a, (const C *)tw, tab);
+    return cudaGetLastError();
+}
+
 template <typename T, int N>
 cudaError_t rows_n(const void *in, void *out, void *out2, int64_t ny, int64_t stride, int64_t batch,
-                   int dir, const void *tw, cudaStream_t st)
+                   int dir, const ColTw &ctw, cudaStream_t st)
 {
-    PipeArgs a{ny, N, 1, stride, batch, 0, dir, out2};
     OpTables<T> tab{};
     tab.scale = (T)1;
+    using LP = LinePolicy<T, N, false>;
+    if constexpr (LP::E > 0) {
+        const void *tw = LP::E == 8 ? ctw.tw8 : ctw.tw;
+        if (dir == ROW_INV)
+            return line_n<T, N, LP::E, LP::W, false, LN_INV, LP::MINB>(in, out, nullptr, ny, N, 1, stride, batch, tw, tab, st);
+        if (dir == ROW_MID)
+            return line_n<T, N, LP::E, LP::W, false, LN_MID, LP::MINB>(in, out, out2, ny, N, 1, stride, batch, tw, tab, st);
+        return line_n<T, N, LP::E, LP::W, false, LN_FWD, LP::MINB>(in, out, nullptr, ny, N, 1, stride, batch, tw, tab, st);
+    }
+    const void *tw = ctw.tw;
+    PipeArgs a{ny, N, 1, stride, batch, 0, dir, out2};
     if (dir == ROW_INV) return pipe_n<T, N, false, PIPE_INV>(in, out, a, tw, tab, st);
     if (dir == ROW_MID) return pipe_n<T, N, false, PIPE_MID>(in, out, a, tw, tab, st);
     return pipe_n<T, N, false, PIPE_FWD>(in, out, a, tw, tab, st);
@@ -105,8 +142,20 @@ cudaError_t rows_n(const void *in, void *out, void *out2, int64_t ny, int64_t st
 
 template <typename T, int N>
 cudaError_t cols_n(const void *in, void *out, int64_t nx, int64_t stride, int64_t batch, int op,
-                   const void *tw, const OpTables<T> &tab, cudaStream_t st)
+                   const ColTw &ctw, const OpTables<T> &tab, cudaStream_t st)
 {
+    using LP = LinePolicy<T, N, true>;
+    if constexpr (LP::E > 0) {
+        const void *tw = LP::E == 8 ? ctw.tw8 : ctw.tw;
+        switch (op) {
+        case COL_FWD: return line_n<T, N, LP::E, LP::W, true, LN_FWD, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st);
+        case COL_INV: return line_n<T, N, LP::E, LP::W, true, LN_INV_SCALED, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st);
+        case COL_POISSON: return line_n<T, N, LP::E, LP::W, true, LN_POISSON, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st);
+        case COL_DIFFUSE: return line_n<T, N, LP::E, LP::W, true, LN_DIFFUSE, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st);
+        default: return cudaErrorInvalidValue;
+        }
+    }
+    const void *tw = ctw.tw;
     PipeArgs a{nx, 1, nx, stride, batch, 0, op, nullptr};
     switch (op) {
     case COL_FWD: return pipe_n<T, N, true, PIPE_FWD>(in, out, a, tw, tab, st);
@@ -168,7 +217,7 @@ template <typename T, int P, int Q> struct Col2Cfg {
     static constexpr int EMAX = FFTPDE_COL2_EMAX;
     static constexpr int TIMAX = Col2Geom<C>::W * (Shape<P, EMAX>::TPT > Shape<Q, EMAX>::TPT
                                                    ? Shape<P, EMAX>::TPT : Shape<Q, EMAX>::TPT);
-    static constexpr int NT = TIMAX > 256 ? TIMAX : 256;      // a CTA holds at least one item
+    static constexpr int NT = TIMAX > 128 ? TIMAX : 128;      // a CTA holds at least one item
     using IA = Col2Items<C, Q, NT, EMAX>;
     using IB = Col2Items<C, P, NT, EMAX>;
     static constexpr int CLA = P / IA::SLOTS, CLB = Q / IB::SLOTS;
@@ -177,7 +226,7 @@ template <typename T, int P, int Q> struct Col2Cfg {
     static constexpr size_t SA = (size_t)IA::SLOTS * IA::SLOT_ELEMS * sizeof(C);
     static constexpr size_t SB = (size_t)IB::SLOTS * IB::SLOT_ELEMS * sizeof(C);
     static constexpr size_t SMEM = SA > SB ? SA : SB;
-    static constexpr int MINB = NT > 256 ? 1 : FFTPDE_COL2_MINB;
+    static constexpr int MINB = NT > 256 ? 1 : NT > 128 ? FFTPDE_COL2_MINB : 4;
 };
 
 template <typename T, int P, int Q, int OP>
@@ -238,7 +287,7 @@ cudaError_t row2_n(const void *in, void *out, int64_t ny, int64_t stride, int64_
 {
     using C = typename cplx_t<T>::type;
     constexpr int EMAX = FFTPDE_COL2_EMAX, CL = 8;
-    constexpr int NT = Col2Cfg<T, P, Q>::NT;
+    constexpr int NT = Col2Cfg<T, P, Q>::TIMAX > 256 ? Col2Cfg<T, P, Q>::TIMAX : 256;
     using Sm = Row2Smem<T, P, Q, NT, EMAX>;
     auto k = row2_kernel<T, P, Q, INV, CL, NT, EMAX>;
     static SmemOptIn<decltype(k)> opt;
@@ -279,7 +328,7 @@ cudaError_t launch_rows2(int64_t nx, const void *in, void *out, int64_t ny, int6
 // ---- length dispatch -------------------------------------------------------
 template <typename T>
 cudaError_t launch_rows(int64_t n, const void *in, void *out, void *out2, int64_t ny, int64_t stride,
-                        int64_t batch, int dir, const void *tw, cudaStream_t st)
+                        int64_t batch, int dir, const ColTw &tw, cudaStream_t st)
 {
     switch (n) {
 #define X(L) case L: return rows_n<T, L>(in, out, out2, ny, stride, batch, dir, tw, st);
@@ -302,9 +351,8 @@ cudaError_t launch_cols(int64_t ny, const void *in, void *out, int64_t nx, int64
                       (const C *)ctw.twP, (const C *)ctw.twQ, (const C *)ctw.twN};
         return launch_col2<T>(ny, P, op, g, batch, tab, st);
     }
-    const void *tw = ctw.tw;
     switch (ny) {
-#define X(L) case L: return cols_n<T, L>(in, out, nx, stride, batch, op, tw, tab, st);
+#define X(L) case L: return cols_n<T, L>(in, out, nx, stride, batch, op, ctw, tab, st);
         FFTPDE_LEN_CASES(X)
 #undef X
     default: return cudaErrorInvalidValue;

@@ -161,13 +161,13 @@ template <int N_, int EMAX = 16> struct Shape {
 __device__ __forceinline__ double2 ldtw(const double2 *p)
 {
     double2 r;
-    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    asm volatile("ld.global.ca.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p) : "memory");
     return r;
 }
 __device__ __forceinline__ float2 ldtw(const float2 *p)
 {
     float2 r;
-    asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
+    asm volatile("ld.global.ca.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p) : "memory");
     return r;
 }
 

@@ -32,7 +32,7 @@ struct fftpde_plan_s {
     unsigned char *ws = nullptr;
     size_t ws_bytes = 0;
     // workspace offsets (bytes)
-    size_t o_twx = 0, o_twy = 0, o_kx2 = 0, o_ky2 = 0, o_ex = 0, o_ey = 0, o_wc = 0, o_ws1 = 0, o_ws2 = 0;
+    size_t o_twx = 0, o_twy = 0, o_twx8 = 0, o_twy8 = 0, o_kx2 = 0, o_ky2 = 0, o_ex = 0, o_ey = 0, o_wc = 0, o_ws1 = 0, o_ws2 = 0;
     size_t o_twP = 0, o_twQ = 0, o_twN = 0;   // two-level column pass tables (P, Q > 0)
     size_t o_scr = 0;                          // scratch: row spectra of 2 fields (multi-step solves)
     int64_t colP = 0, colQ = 0;
@@ -43,7 +43,8 @@ struct fftpde_plan_s {
     size_t need = 0;
     int64_t qx = 0, qy = 0;   // quadrant extents nx/2+1, ny/2+1
     // host tables (fp64)
-    std::vector<double> twx, twy;   // interleaved re, im
+    std::vector<double> twx, twy;   // interleaved re, im (radix-16 stage tables)
+    std::vector<double> twx8, twy8; // radix-8 stage tables (line_kernel E = 8)
     std::vector<double> kx2, ky2;
     bool diff_valid = false;
     double diff_D = 0, diff_dt = 0;
@@ -251,7 +252,7 @@ template <typename T> struct Passes {
     const void *twy() const { return p->ws + p->o_twy; }
     ColTw rtw() const
     {
-        return ColTw{twx(), p->ws + p->o_rtwP, p->ws + p->o_rtwQ, p->ws + p->o_rtwN};
+        return ColTw{twx(), p->ws + p->o_rtwP, p->ws + p->o_rtwQ, p->ws + p->o_rtwN, p->ws + p->o_twx8};
     }
     cudaError_t rows(const void *in, void *out, int inverse)
     {
@@ -259,7 +260,7 @@ template <typename T> struct Passes {
             if (p->rowP)   // long rows: two-level cluster pass
                 return launch_rows2<T>(p->nx, in, out, p->ny, stride, batch, inverse, rtw(), p->stream);
             return launch_rows<T>(p->nx, in, out, nullptr, p->ny, stride, batch, inverse ? ROW_INV : ROW_FWD,
-                                  twx(), p->stream);
+                                  rtw(), p->stream);
         });
     }
     // inverse rows of step s (physical field -> phys) + forward rows of step s+1 (-> spec)
@@ -270,7 +271,7 @@ template <typename T> struct Passes {
             return e == cudaSuccess ? rows(phys, spec, 0) : e;
         }
         return launch(p, FFTPDE_KERNEL_ROW, [&] {
-            return launch_rows<T>(p->nx, in, spec, phys, p->ny, stride, batch, ROW_MID, twx(), p->stream);
+            return launch_rows<T>(p->nx, in, spec, phys, p->ny, stride, batch, ROW_MID, rtw(), p->stream);
         });
     }
     void *scratch(int field) const
@@ -279,7 +280,7 @@ template <typename T> struct Passes {
     }
     ColTw ctw() const
     {
-        return ColTw{twy(), p->ws + p->o_twP, p->ws + p->o_twQ, p->ws + p->o_twN};
+        return ColTw{twy(), p->ws + p->o_twP, p->ws + p->o_twQ, p->ws + p->o_twN, p->ws + p->o_twy8};
     }
     cudaError_t cols(const void *in, void *out, int op)
     {
@@ -587,6 +588,8 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     p->use_graphs = std::getenv("FFTPDE_NO_GRAPHS") == nullptr;
     build_twiddles(nx, p->twx);
     build_twiddles(ny, p->twy);
+    build_twiddles(nx, p->twx8, 8);
+    build_twiddles(ny, p->twy8, 8);
     build_k2(nx, Lx, p->kx2);
     build_k2(ny, Ly, p->ky2);
     fftpde::col2_split(ny, nx, dtype == FFTPDE_C128 ? 16 : 8, p->colP, p->colQ);
@@ -607,6 +610,8 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return o; };
     p->o_twx = take(p->twx.size() / 2 * ec);
     p->o_twy = take(p->twy.size() / 2 * ec);
+    p->o_twx8 = take(p->twx8.size() / 2 * ec);
+    p->o_twy8 = take(p->twy8.size() / 2 * ec);
     p->o_kx2 = take((size_t)nx * er);
     p->o_ky2 = take((size_t)ny * er);
     p->o_ex = take((size_t)nx * er);
@@ -663,6 +668,8 @@ fftpde_status fftpde_set_workspace(fftpde_plan plan, void *dev_ptr, size_t bytes
         s = upload(plan, plan->o_twx, plan->twx);
         if (s == FFTPDE_OK) s = upload(plan, plan->o_twy, plan->twy);
     }
+    if (s == FFTPDE_OK) s = upload(plan, plan->o_twx8, plan->twx8);
+    if (s == FFTPDE_OK) s = upload(plan, plan->o_twy8, plan->twy8);
     if (s == FFTPDE_OK && plan->rowP) {
         s = upload(plan, plan->o_rtwP, plan->rtwP);
         if (s == FFTPDE_OK) s = upload(plan, plan->o_rtwQ, plan->rtwQ);
@@ -853,7 +860,7 @@ fftpde_status fftpde_cols_slab(fftpde_plan p, const void *in, void *out, int64_t
     DeviceGuard g(p->device);
     if (!g.ok) return FFTPDE_ERR_CUDA;
     cudaError_t e;
-    const ColTw ctw{p->ws + p->o_twy, p->ws + p->o_twP, p->ws + p->o_twQ, p->ws + p->o_twN};
+    const ColTw ctw{p->ws + p->o_twy, p->ws + p->o_twP, p->ws + p->o_twQ, p->ws + p->o_twN, p->ws + p->o_twy8};
     auto run = [&](auto tag) {
         using T = decltype(tag);
         OpTables<T> t = tables<T>(p);

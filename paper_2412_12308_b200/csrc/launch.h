@@ -30,16 +30,18 @@ constexpr int64_t kMaxLen2 = 32768;  // two-level (cluster) axis length limit
 // `stride` elements apart.  dir: ROW_FWD, ROW_INV (unscaled), or ROW_MID (inverse
 // stored to out2, then forward stored to out).
 enum RowDir { ROW_FWD = 0, ROW_INV = 4, ROW_MID = 5 };   // == PipeOp values
+struct ColTw;
 template <typename T>
 cudaError_t launch_rows(int64_t n, const void *in, void *out, void *out2, int64_t ny, int64_t stride,
-                        int64_t batch, int dir, const void *tw, cudaStream_t st);
+                        int64_t batch, int dir, const ColTw &tw, cudaStream_t st);
 
 // Twiddle tables of the column axis: the single-level stage table of ny, and for
 // the two-level (cluster) column pass the stage tables of P and Q (ny = P Q)
 // plus the plain table w_ny^m, m < ny.
 struct ColTw {
-    const void *tw;      // stage table of ny
+    const void *tw;      // stage table of the axis (radix 16)
     const void *twP, *twQ, *twN;
+    const void *tw8;     // stage table of the axis (radix 8, line_kernel E = 8)
 };
 
 // Split ny = P * Q used by the two-level column pass (P = Q = 0: not used).
