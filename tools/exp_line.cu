@@ -7,6 +7,7 @@
 #include <vector>
 #include "../paper_2412_12308_b200/csrc/line.cuh"
 #include "../paper_2412_12308_b200/csrc/pipe.cuh"
+#include "../paper_2412_12308_b200/csrc/rr.cuh"
 using namespace fftpde;
 
 static const char *g_filter = nullptr;
@@ -126,6 +127,34 @@ static void wave_var(void *U, void *V, long nx, long ny, const void *tw, const O
            occ, grid);
 }
 
+// ---- rr_kernel variant
+template <typename T, int N, int W, bool COLS, int OP, int MINB>
+static void rr_var(const void *in, void *out, void *out2, long nx, long ny, long batch, const void *tw,
+                   const OpTables<T> &tab, const char *tag)
+{
+    using C = typename cplx_t<T>::type;
+    char name[160];
+    snprintf(name, sizeof name, "%s RR W=%d minb=%d", tag, W, MINB);
+    if (g_filter && !strstr(name, g_filter)) return;
+    using L = RRSmem<C, N, W, COLS>;
+    auto k = rr_kernel<T, N, W, COLS, OP, MINB>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    const int threads = W * (N / 16);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, L::BYTES);
+    LineArgs a;
+    if (COLS) a = LineArgs{nx, 1, nx, nx * ny, (nx + W - 1) / W, out2};
+    else a = LineArgs{ny, nx, 1, nx * ny, (ny + W - 1) / W, out2};
+    const long ntiles = batch * a.groups;
+    long grid = (long)occ * 148;
+    if (grid > ntiles) grid = ntiles;
+    const double fields = OP == LN_MID ? 3.0 : 2.0;
+    const double bytes = fields * (double)nx * ny * batch * sizeof(C);
+    timeit([&] { k<<<(unsigned)grid, threads, L::BYTES>>>((const C *)in, (C *)out, a, ntiles, (const C *)tw, tab); },
+           name, bytes, occ, grid);
+}
+
 // ---- pipe_kernel reference (current library configuration)
 template <typename T, int N, int W, bool COLS, int OP, int NBUF, bool TWREG>
 static void pipe_ref(const void *in, void *out, void *out2, long nx, long ny, long batch, const void *tw,
@@ -210,6 +239,8 @@ int main(int argc, char **argv)
         using D = double;
         OpTables<D> tab = make_tab<D>(4096, 4096);
         void *t16 = upload_tw<double2>(4096, 16), *t8 = upload_tw<double2>(4096, 8);
+        void *t16_2048 = upload_tw<double2>(2048, 16);
+        OpTables<D> tab2048 = make_tab<D>(8192, 2048);
         pipe_ref<D, 4096, 1, false, PIPE_MID, 2, true>(A, B, Cb, 4096, 4096, 1, t16, tab, "c3 rowsMID");
         line_var<D, 4096, 16, 1, false, LN_MID, 1>(A, B, Cb, 4096, 4096, 1, t16, tab, "c3 rowsMID");
         line_var<D, 4096, 16, 1, false, LN_MID, 2>(A, B, Cb, 4096, 4096, 1, t16, tab, "c3 rowsMID");
@@ -217,7 +248,16 @@ int main(int argc, char **argv)
         line_var<D, 4096, 8, 1, false, LN_MID, 1>(A, B, Cb, 4096, 4096, 1, t8, tab, "c3 rowsMID");
         line_var<D, 4096, 8, 1, false, LN_MID, 2>(A, B, Cb, 4096, 4096, 1, t8, tab, "c3 rowsMID");
         line_var<D, 4096, 8, 1, false, LN_MID, 3>(A, B, Cb, 4096, 4096, 1, t8, tab, "c3 rowsMID");
+        rr_var<D, 4096, 2, false, LN_MID, 1>(A, B, Cb, 4096, 4096, 1, t16, tab, "c3 rowsMID");
+        rr_var<D, 4096, 1, false, LN_MID, 2>(A, B, Cb, 4096, 4096, 1, t16, tab, "c3 rowsMID");
+        rr_var<D, 4096, 1, false, LN_MID, 1>(A, B, Cb, 4096, 4096, 1, t16, tab, "c3 rowsMID");
         pipe_ref<D, 4096, 1, false, PIPE_FWD, 2, true>(A, B, nullptr, 4096, 4096, 1, t16, tab, "c3 rowsFWD");
+        rr_var<D, 4096, 2, false, LN_FWD, 1>(A, B, nullptr, 4096, 4096, 1, t16, tab, "c3 rowsFWD");
+        rr_var<D, 4096, 1, false, LN_FWD, 2>(A, B, nullptr, 4096, 4096, 1, t16, tab, "c3 rowsFWD");
+        rr_var<D, 4096, 2, true, LN_POISSON, 1>(B, B, nullptr, 4096, 4096, 1, t16, tab, "c3 colsPOI");
+        rr_var<D, 4096, 2, true, LN_FWD, 1>(B, B, nullptr, 4096, 4096, 1, t16, tab, "c3 colsFWD");
+        rr_var<D, 2048, 4, true, LN_POISSON, 1>(B, B, nullptr, 8192, 2048, 1, t16_2048, tab2048, "c2048 colsPOI");
+        rr_var<D, 2048, 2, true, LN_POISSON, 2>(B, B, nullptr, 8192, 2048, 1, t16_2048, tab2048, "c2048 colsPOI");
         line_var<D, 4096, 16, 1, false, LN_FWD, 2>(A, B, nullptr, 4096, 4096, 1, t16, tab, "c3 rowsFWD");
         line_var<D, 4096, 16, 1, false, LN_FWD, 3>(A, B, nullptr, 4096, 4096, 1, t16, tab, "c3 rowsFWD");
         line_var<D, 4096, 8, 1, false, LN_FWD, 2>(A, B, nullptr, 4096, 4096, 1, t8, tab, "c3 rowsFWD");
