@@ -6,7 +6,7 @@
 #include "kernels.cuh"
 #include "pipe.cuh"
 #include "col2.cuh"
-#include "row2.cuh"
+#include "row2d.cuh"
 #include "line.cuh"
 #ifndef FFTPDE_COL2_MINB
 #define FFTPDE_COL2_MINB 2
@@ -281,23 +281,21 @@ cudaError_t launch_col2(int64_t ny, int64_t P, int op, Col2Args<T> g, int64_t ba
     }
 }
 
-template <typename T, int P, int Q, bool INV>
-cudaError_t row2_n(const void *in, void *out, int64_t ny, int64_t stride, int64_t batch,
-                   const ColTw &tw, cudaStream_t st)
+// ---- long rows: DSMEM four-step on a cluster (row2d.cuh) ------------------------
+template <typename T, int P, int Q, int OP>
+cudaError_t row2d_n(const void *in, void *out, void *out2, int64_t ny, int64_t stride, int64_t batch,
+                    const ColTw &tw, cudaStream_t st)
 {
     using C = typename cplx_t<T>::type;
-    constexpr int EMAX = FFTPDE_COL2_EMAX, CL = 8;
-    constexpr int NT = Col2Cfg<T, P, Q>::TIMAX > 256 ? Col2Cfg<T, P, Q>::TIMAX : 256;
-    using Sm = Row2Smem<T, P, Q, NT, EMAX>;
-    auto k = row2_kernel<T, P, Q, INV, CL, NT, EMAX>;
+    constexpr int CL = 8;
+    using G = Row2dGeom<C, P, Q, CL>;
+    auto k = row2d_kernel<T, P, Q, CL, OP>;
     static SmemOptIn<decltype(k)> opt;
-    cudaError_t e = opt(k, Sm::BYTES);
+    cudaError_t e = opt(k, G::BYTES);
     if (e != cudaSuccess) return e;
-    const int64_t nrows = ny * batch;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(CL * nrows), 1, 1);
-    cfg.blockDim = dim3(NT, 1, 1);
-    cfg.dynamicSmemBytes = Sm::BYTES;
+    cfg.blockDim = dim3(G::NT, 1, 1);
+    cfg.dynamicSmemBytes = G::BYTES;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -306,21 +304,40 @@ cudaError_t row2_n(const void *in, void *out, int64_t ny, int64_t stride, int64_
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, k, (const C *)in, (C *)out, nrows, ny, stride, (const C *)tw.twP,
+    static std::atomic<int> max_clusters{0};
+    int ncl = max_clusters.load();
+    if (!ncl) {
+        cfg.gridDim = dim3(CL, 1, 1);
+        e = cudaOccupancyMaxActiveClusters(&ncl, k, &cfg);
+        if (e != cudaSuccess) return e;
+        if (ncl < 1) ncl = 1;
+        max_clusters.store(ncl);
+    }
+    const int64_t nrows = ny * batch;
+    const int64_t g = std::min<int64_t>(nrows, ncl);          // persistent clusters
+    cfg.gridDim = dim3((unsigned)(CL * g), 1, 1);
+    e = cudaLaunchKernelEx(&cfg, k, (const C *)in, (C *)out, (C *)out2, nrows, ny, stride, (const C *)tw.twP,
                            (const C *)tw.twQ, (const C *)tw.twN);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
+template <typename T, int P, int Q>
+cudaError_t row2d_dir(const void *in, void *out, void *out2, int64_t ny, int64_t stride, int64_t batch, int dir,
+                      const ColTw &tw, cudaStream_t st)
+{
+    if (dir == ROW_INV) return row2d_n<T, P, Q, R2D_INV>(in, out, nullptr, ny, stride, batch, tw, st);
+    if (dir == ROW_MID) return row2d_n<T, P, Q, R2D_MID>(in, out, out2, ny, stride, batch, tw, st);
+    return row2d_n<T, P, Q, R2D_FWD>(in, out, nullptr, ny, stride, batch, tw, st);
+}
+
 template <typename T>
-cudaError_t launch_rows2(int64_t nx, const void *in, void *out, int64_t ny, int64_t stride,
-                         int64_t batch, int inverse, const ColTw &tw, cudaStream_t st)
+cudaError_t launch_rows2(int64_t nx, const void *in, void *out, void *out2, int64_t ny, int64_t stride,
+                         int64_t batch, int dir, const ColTw &tw, cudaStream_t st)
 {
     switch (nx) {
-    case 16384: return inverse ? row2_n<T, 128, 128, true>(in, out, ny, stride, batch, tw, st)
-                               : row2_n<T, 128, 128, false>(in, out, ny, stride, batch, tw, st);
-    case 32768: return inverse ? row2_n<T, 128, 256, true>(in, out, ny, stride, batch, tw, st)
-                               : row2_n<T, 128, 256, false>(in, out, ny, stride, batch, tw, st);
+    case 16384: return row2d_dir<T, 128, 128>(in, out, out2, ny, stride, batch, dir, tw, st);
+    case 32768: return row2d_dir<T, 128, 256>(in, out, out2, ny, stride, batch, dir, tw, st);
     default: return cudaErrorInvalidValue;
     }
 }

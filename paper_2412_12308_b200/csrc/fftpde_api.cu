@@ -39,7 +39,7 @@ struct fftpde_plan_s {
     std::vector<double> twP, twQ, twN;
     size_t o_rtwP = 0, o_rtwQ = 0, o_rtwN = 0;   // two-level row pass tables (nx > kMaxLen)
     int64_t rowP = 0, rowQ = 0;
-    std::vector<double> rtwP, rtwQ, rtwN;
+    std::vector<double> rtwP, rtwQ, rtwN;   // row2d: radix-16 stage tables of P, Q; split inter-phase table
     size_t need = 0;
     int64_t qx = 0, qy = 0;   // quadrant extents nx/2+1, ny/2+1
     // host tables (fp64)
@@ -62,7 +62,11 @@ struct fftpde_plan_s {
         std::array<uint64_t, 6> key;
         cudaGraphExec_t exec;
         int64_t launches;
+        // profiling graphs: the event pairs recorded around each kernel node
+        std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof;
     };
+    bool capturing = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> cap_prof;
     std::vector<Graph> graphs;
     cudaStream_t cap_stream = nullptr;
     bool use_graphs = true;
@@ -141,6 +145,28 @@ void build_plain_twiddles(int64_t n, std::vector<double> &tw)
 {
     tw.resize(2 * (size_t)n);
     for (int64_t m = 0; m < n; ++m) unit_root(n, m, tw[2 * m], tw[2 * m + 1]);
+}
+
+// Inter-phase twiddles w_N^{n1 k1} of the four-step row pass (row2d.cuh), as
+// products of two small tables, every entry rounded once from its exact angle:
+// S1[n1][l] = w^{n1 l}, S2[n1][h] = w^{16 n1 h}, U1[k1][l] = w^{k1 l}, U2[k1][h] = w^{16 k1 h}.
+void build_split_twiddles(int64_t n, int64_t P, int64_t Q, std::vector<double> &tw)
+{
+    tw.clear();
+    auto put = [&](int64_t m) {
+        double re, im;
+        unit_root(n, m, re, im);
+        tw.push_back(re);
+        tw.push_back(im);
+    };
+    for (int64_t a = 0; a < P; ++a)
+        for (int64_t l = 0; l < 16; ++l) put(a * l);
+    for (int64_t a = 0; a < P; ++a)
+        for (int64_t h = 0; h < Q / 16; ++h) put(16 * a * h);
+    for (int64_t k = 0; k < Q; ++k)
+        for (int64_t l = 0; l < 16; ++l) put(k * l);
+    for (int64_t k = 0; k < Q; ++k)
+        for (int64_t h = 0; h < P / 16; ++h) put(16 * k * h);
 }
 
 template <typename T> std::vector<T> cast_vec(const std::vector<double> &v)
@@ -237,10 +263,13 @@ template <typename F> cudaError_t launch(fftpde_plan p, int cls, F &&f)
     ++p->launches;
     if (!p->profiling) return f();
     cudaEvent_t a = pool_event(p), b = pool_event(p);
-    cudaEventRecord(a, p->stream);
+    // inside a stream capture, External records become event-record nodes of the graph
+    const unsigned flags = p->capturing ? cudaEventRecordExternal : 0u;
+    cudaEventRecordWithFlags(a, p->stream, flags);
     cudaError_t e = f();
-    cudaEventRecord(b, p->stream);
-    p->pending[cls].emplace_back(a, b);
+    cudaEventRecordWithFlags(b, p->stream, flags);
+    if (p->capturing) p->cap_prof.push_back({cls, {a, b}});
+    else p->pending[cls].emplace_back(a, b);
     return e;
 }
 
@@ -257,8 +286,9 @@ template <typename T> struct Passes {
     cudaError_t rows(const void *in, void *out, int inverse)
     {
         return launch(p, FFTPDE_KERNEL_ROW, [&] {
-            if (p->rowP)   // long rows: two-level cluster pass
-                return launch_rows2<T>(p->nx, in, out, p->ny, stride, batch, inverse, rtw(), p->stream);
+            if (p->rowP)   // long rows: DSMEM four-step cluster pass
+                return launch_rows2<T>(p->nx, in, out, nullptr, p->ny, stride, batch, inverse ? ROW_INV : ROW_FWD,
+                                       rtw(), p->stream);
             return launch_rows<T>(p->nx, in, out, nullptr, p->ny, stride, batch, inverse ? ROW_INV : ROW_FWD,
                                   rtw(), p->stream);
         });
@@ -266,11 +296,9 @@ template <typename T> struct Passes {
     // inverse rows of step s (physical field -> phys) + forward rows of step s+1 (-> spec)
     cudaError_t rows_mid(const void *in, void *spec, void *phys)
     {
-        if (p->rowP) {     // long rows: two launches
-            cudaError_t e = rows(in, phys, 1);
-            return e == cudaSuccess ? rows(phys, spec, 0) : e;
-        }
         return launch(p, FFTPDE_KERNEL_ROW, [&] {
+            if (p->rowP)
+                return launch_rows2<T>(p->nx, in, spec, phys, p->ny, stride, batch, ROW_MID, rtw(), p->stream);
             return launch_rows<T>(p->nx, in, spec, phys, p->ny, stride, batch, ROW_MID, rtw(), p->stream);
         });
     }
@@ -412,16 +440,40 @@ template <typename F> fftpde_status dispatch(fftpde_plan p, int64_t batch, int64
 // (the caller's stream may be the legacy default stream, which cannot be
 // captured) and replayed on the plan's stream; the kernels read their operator
 // tables by pointer, so new (D, dt) / (c, dt) need no re-capture.
-template <typename F>
-fftpde_status run_graphed(fftpde_plan p, const std::array<uint64_t, 6> &key, F &&enqueue)
+// Accumulate the kernel times of one replay of a profiling graph.
+fftpde_status collect_graph_profile(fftpde_plan p, const fftpde_plan_s::Graph &gr)
 {
-    if (p->profiling || !p->use_graphs) return enqueue();
+    if (gr.prof.empty()) return FFTPDE_OK;
+    if (cudaStreamSynchronize(p->stream) != cudaSuccess) return FFTPDE_ERR_CUDA;
+    for (auto &ev : gr.prof) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, ev.second.first, ev.second.second) != cudaSuccess) return FFTPDE_ERR_CUDA;
+        p->prof_ms[ev.first] += ms;
+        p->prof_n[ev.first] += 1;
+    }
+    return FFTPDE_OK;
+}
+
+// Run a multi-launch sequence through a cached CUDA graph.  The sequence is
+// captured once per (kind, buffers, batch, stride, nsteps) on a private stream
+// (the caller's stream may be the legacy default stream, which cannot be
+// captured) and replayed on the plan's stream; the kernels read their operator
+// tables by pointer, so new (D, dt) / (c, dt) need no re-capture.  With
+// profiling on, a separate graph is captured whose kernel nodes are bracketed
+// by event-record nodes, so per-kernel times are those of graph execution
+// (a stream launch costs ~4 us on B200, a graph kernel node ~0.6 us).
+template <typename F>
+fftpde_status run_graphed(fftpde_plan p, std::array<uint64_t, 6> key, F &&enqueue)
+{
+    if (!p->use_graphs) return enqueue();
+    if (p->profiling) key[0] |= 0x100;
     DeviceGuard g(p->device);
     if (!g.ok) return FFTPDE_ERR_CUDA;
     for (auto &gr : p->graphs) {
         if (gr.key == key) {
             p->launches += gr.launches;
-            return cuda_status(cudaGraphLaunch(gr.exec, p->stream));
+            if (cudaGraphLaunch(gr.exec, p->stream) != cudaSuccess) return FFTPDE_ERR_CUDA;
+            return collect_graph_profile(p, gr);
         }
     }
     if (!p->cap_stream && cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
@@ -431,7 +483,10 @@ fftpde_status run_graphed(fftpde_plan p, const std::array<uint64_t, 6> &key, F &
     if (cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeRelaxed) != cudaSuccess)
         return FFTPDE_ERR_CUDA;
     p->stream = p->cap_stream;
+    p->capturing = true;
+    p->cap_prof.clear();
     fftpde_status st = enqueue();
+    p->capturing = false;
     p->stream = user;
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(p->cap_stream, &graph);
@@ -447,12 +502,15 @@ fftpde_status run_graphed(fftpde_plan p, const std::array<uint64_t, 6> &key, F &
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return FFTPDE_ERR_CUDA;
     if (p->graphs.size() >= 8) {
+        for (auto &ev : p->graphs.front().prof) { p->event_pool.push_back(ev.second.first); p->event_pool.push_back(ev.second.second); }
         cudaGraphExecDestroy(p->graphs.front().exec);
         p->graphs.erase(p->graphs.begin());
     }
-    p->graphs.push_back({key, exec, n});
+    p->graphs.push_back({key, exec, n, std::move(p->cap_prof)});
+    p->cap_prof.clear();
     p->launches += n;
-    return cuda_status(cudaGraphLaunch(exec, p->stream));
+    if (cudaGraphLaunch(exec, p->stream) != cudaSuccess) return FFTPDE_ERR_CUDA;
+    return collect_graph_profile(p, p->graphs.back());
 }
 
 fftpde_status ensure_diffusion_tables(fftpde_plan p, double D, double dt)
@@ -600,9 +658,9 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     }
     fftpde::row2_split(nx, p->rowP, p->rowQ);
     if (p->rowP) {
-        build_twiddles(p->rowP, p->rtwP, FFTPDE_COL2_EMAX);
-        build_twiddles(p->rowQ, p->rtwQ, FFTPDE_COL2_EMAX);
-        build_plain_twiddles(nx, p->rtwN);
+        build_twiddles(p->rowP, p->rtwP, 16);
+        build_twiddles(p->rowQ, p->rtwQ, 16);
+        build_split_twiddles(nx, p->rowP, p->rowQ, p->rtwN);
     }
 
     const size_t er = elem_real(p), ec = elem_cplx(p);
@@ -692,7 +750,10 @@ fftpde_status fftpde_destroy(fftpde_plan plan)
     for (auto &v : plan->pending)
         for (auto &pr : v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     for (cudaEvent_t e : plan->event_pool) cudaEventDestroy(e);
-    for (auto &gr : plan->graphs) cudaGraphExecDestroy(gr.exec);
+    for (auto &gr : plan->graphs) {
+        cudaGraphExecDestroy(gr.exec);
+        for (auto &ev : gr.prof) { cudaEventDestroy(ev.second.first); cudaEventDestroy(ev.second.second); }
+    }
     if (plan->cap_stream) cudaStreamDestroy(plan->cap_stream);
     delete plan;
     return FFTPDE_OK;

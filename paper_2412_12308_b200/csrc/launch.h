@@ -49,11 +49,12 @@ void col2_split(int64_t ny, int64_t nx, int elem_bytes, int64_t &P, int64_t &Q);
 // Split nx = P * Q of the two-level row pass (rows longer than kMaxLen).
 void row2_split(int64_t nx, int64_t &P, int64_t &Q);
 
-// Two-level row pass (nx = P Q > kMaxLen): inverse != 0 selects the conjugate
-// kernel (unscaled).  Tables: stage tables of P and Q, plain w_nx^m.
+// Long-row pass (nx = P Q > kMaxLen, row2d.cuh): dir = ROW_FWD, ROW_INV
+// (unscaled) or ROW_MID (inverse -> out2, then forward -> out).  Tables (ColTw):
+// twP, twQ = radix-16 stage tables of P and Q; twN = split inter-phase table.
 template <typename T>
-cudaError_t launch_rows2(int64_t nx, const void *in, void *out, int64_t ny, int64_t stride,
-                         int64_t batch, int inverse, const ColTw &tw, cudaStream_t st);
+cudaError_t launch_rows2(int64_t nx, const void *in, void *out, void *out2, int64_t ny, int64_t stride,
+                         int64_t batch, int dir, const ColTw &tw, cudaStream_t st);
 
 // Column pass along y (length ny) over nx columns, op in ColOp.
 template <typename T>
