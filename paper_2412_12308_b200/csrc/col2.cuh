@@ -39,6 +39,42 @@ __device__ __forceinline__ unsigned cluster_rank()
 __device__ __forceinline__ double2 ldcg(const double2 *p) { return __ldcg(p); }
 __device__ __forceinline__ float2 ldcg(const float2 *p) { return __ldcg(p); }
 
+// L2 eviction-priority policies: the four-step intermediate should stay in L2
+// between phases (evict_last); the input read once and the final result are
+// streamed (evict_first).
+__device__ __forceinline__ uint64_t l2_policy_last()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_first()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double2 ldcg_h(const double2 *p, uint64_t pol)
+{
+    double2 r;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ float2 ldcg_h(const float2 *p, uint64_t pol)
+{
+    float2 r;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(r.x), "=f"(r.y) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ void st_h(double2 *p, double2 v, uint64_t pol)
+{
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_h(float2 *p, float2 v, uint64_t pol)
+{
+    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y), "l"(pol) : "memory");
+}
+
 template <typename C> struct Col2Geom {
     static constexpr int W = 128 / (int)sizeof(C);      // columns per block: one 128-byte line
 };
@@ -116,11 +152,15 @@ col2_kernel(Col2Args<T> g, OpTables<T> tab)
             return src + base + (int64_t)(n1 + P * t) * g.nx + c;
         };
         int it = (int)rank * IA::SLOTS + slot;
+        // forward phase A: input streamed in, intermediate kept in L2;
+        // inverse phase A': intermediate read for the last time, result streamed out
+        const uint64_t pol_ld = l2_policy_first();
+        const uint64_t pol_st = inverse ? l2_policy_first() : l2_policy_last();
         C v[E], nv[E];
         if (it < ITEMS) {
             const C *s0 = item_src(it);
 #pragma unroll
-            for (int e = 0; e < E; ++e) v[e] = ldcg(s0 + e * rstep);
+            for (int e = 0; e < E; ++e) v[e] = ldcg_h(s0 + e * rstep, pol_ld);
         }
         for (; it < ITEMS; it += STEP) {
             // prefetch the next item of this slot while this one is transformed
@@ -128,7 +168,7 @@ col2_kernel(Col2Args<T> g, OpTables<T> tab)
             if (more) {
                 const C *s1 = item_src(it + STEP);
 #pragma unroll
-                for (int e = 0; e < E; ++e) nv[e] = ldcg(s1 + e * rstep);
+                for (int e = 0; e < E; ++e) nv[e] = ldcg_h(s1 + e * rstep, pol_ld);
             }
             const int f = it / P, n1 = it - f * P;
             C *F = f ? g.V : g.U;
@@ -143,7 +183,7 @@ col2_kernel(Col2Args<T> g, OpTables<T> tab)
             }
             C *dst = opaque_ptr(F + base + (int64_t)(n1 + P * t) * g.nx + c);
 #pragma unroll
-            for (int e = 0; e < E; ++e) dst[e * rstep] = v[e];
+            for (int e = 0; e < E; ++e) st_h(dst + e * rstep, v[e], pol_st);
             if (more) {
 #pragma unroll
                 for (int e = 0; e < E; ++e) v[e] = nv[e];
@@ -164,11 +204,12 @@ col2_kernel(Col2Args<T> g, OpTables<T> tab)
         const int64_t rstep = (int64_t)TPT * g.nx;
         const int64_t a = col0 + c;
         int k1 = (int)rank * IB::SLOTS + slot;
+        const uint64_t pol = l2_policy_last();
         C u[E], nu[E];
         if (k1 < Q) {
             const C *s0 = g.U + base + (int64_t)(P * k1 + t) * g.nx + c;
 #pragma unroll
-            for (int e = 0; e < E; ++e) u[e] = ldcg(s0 + e * rstep);
+            for (int e = 0; e < E; ++e) u[e] = ldcg_h(s0 + e * rstep, pol);
         }
         for (; k1 < Q; k1 += STEP) {
             const int64_t r0 = base + (int64_t)(P * k1 + t) * g.nx + c;
@@ -176,13 +217,13 @@ col2_kernel(Col2Args<T> g, OpTables<T> tab)
             if (more) {     // prefetch the next item of this slot (first field)
                 const C *s1 = g.U + r0 + (int64_t)P * STEP * g.nx;
 #pragma unroll
-                for (int e = 0; e < E; ++e) nu[e] = ldcg(s1 + e * rstep);
+                for (int e = 0; e < E; ++e) nu[e] = ldcg_h(s1 + e * rstep, pol);
             }
             fft<P, false, EMAX>(u, sm, t, g.twP, sync);                // X[k1 + Q k2], k2 = t + TPT e
             if constexpr (OP == C2_WAVE) {
                 C w[E];
 #pragma unroll
-                for (int e = 0; e < E; ++e) w[e] = ldcg(g.V + r0 + e * rstep);
+                for (int e = 0; e < E; ++e) w[e] = ldcg_h(g.V + r0 + e * rstep, pol);
                 fft<P, false, EMAX>(w, sm, t, g.twP, sync);
                 const int64_t qa = a <= g.nx - a ? a : g.nx - a;
                 const T *pC = tab.wC + qa * tab.qpitch, *pS1 = tab.wS1 + qa * tab.qpitch,
@@ -199,7 +240,7 @@ col2_kernel(Col2Args<T> g, OpTables<T> tab)
                 fft<P, true, EMAX>(w, sm, t, g.twP, sync);
                 C *dv = opaque_ptr(g.V + r0);
 #pragma unroll
-                for (int e = 0; e < E; ++e) dv[e * rstep] = w[e];
+                for (int e = 0; e < E; ++e) st_h(dv + e * rstep, w[e], pol);
             } else if constexpr (OP == C2_POISSON) {
                 const T kxa = tab.kx2[a];
 #pragma unroll
@@ -216,7 +257,7 @@ col2_kernel(Col2Args<T> g, OpTables<T> tab)
             fft<P, true, EMAX>(u, sm, t, g.twP, sync);
             C *du = opaque_ptr(g.U + r0);
 #pragma unroll
-            for (int e = 0; e < E; ++e) du[e * rstep] = u[e];
+            for (int e = 0; e < E; ++e) st_h(du + e * rstep, u[e], pol);
             if (more) {
 #pragma unroll
                 for (int e = 0; e < E; ++e) u[e] = nu[e];
@@ -325,6 +366,7 @@ col2_phase_kernel(Col2Args<T> g, OpTables<T> tab, int64_t nitems)
     SmemView<C, SL::LOGE, 1> sm{smem + slot * I::SLOT_ELEMS + c * I::S};
     const ItemSync<I::TI> sync{1 + slot};
 
+    const uint64_t pol = l2_policy_last();
     for (int64_t item = (int64_t)blockIdx.x * I::SLOTS + slot; item < nitems;
          item += (int64_t)gridDim.x * I::SLOTS) {
         const int64_t blk = item / PER_BLOCK;
@@ -382,7 +424,7 @@ col2_phase_kernel(Col2Args<T> g, OpTables<T> tab, int64_t nitems)
                 fft<P, true, EMAX>(w, sm, t, g.twP, sync);
                 C *dv = opaque_ptr(g.V + r0);
 #pragma unroll
-                for (int e = 0; e < E; ++e) dv[e * rstep] = w[e];
+                for (int e = 0; e < E; ++e) st_h(dv + e * rstep, w[e], pol);
             } else if constexpr (OP == C2_POISSON) {
                 const T kxa = tab.kx2[a];
 #pragma unroll
