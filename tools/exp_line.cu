@@ -8,10 +8,12 @@
 #include "../paper_2412_12308_b200/csrc/line.cuh"
 #include "../paper_2412_12308_b200/csrc/pipe.cuh"
 #include "../paper_2412_12308_b200/csrc/rr.cuh"
+#include "../paper_2412_12308_b200/csrc/tpipe.cuh"
 using namespace fftpde;
 
 static const char *g_filter = nullptr;
 static int g_reps = 20;
+static cudaStream_t g_stream = nullptr;
 
 template <typename C> static void twiddles(int n, int emax, std::vector<C> &tw)
 {
@@ -63,16 +65,32 @@ template <typename T> static OpTables<T> make_tab(int nx, int ny)
 
 template <typename F> static float timeit(F launch, const char *name, double bytes, int occ, long grid)
 {
+    // launches captured into a CUDA graph: per-kernel time without the ~2 us
+    // stream-launch quantum (graph kernel nodes cost ~0.6 us each)
+    static cudaStream_t s = nullptr;
+    if (!s) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
-    for (int i = 0; i < 3; ++i) launch();
-    cudaEventRecord(e0);
+    cudaStream_t prev = g_stream;
+    g_stream = s;
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed);
     for (int i = 0; i < g_reps; ++i) launch();
-    cudaEventRecord(e1);
+    cudaStreamEndCapture(s, &g);
+    g_stream = prev;
+    cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphLaunch(ge, s);
+    cudaGraphLaunch(ge, s);
+    cudaEventRecord(e0, s);
+    cudaGraphLaunch(ge, s);
+    cudaEventRecord(e1, s);
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     ms /= g_reps;
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
     cudaError_t err = cudaGetLastError();
     printf("%-58s occ %2d grid %6ld : %9.2f us  %7.0f GB/s %s\n", name, occ, grid, ms * 1e3,
            bytes / (ms * 1e-3) / 1e9, err ? cudaGetErrorString(err) : "");
@@ -102,7 +120,7 @@ static void line_var(const void *in, void *out, void *out2, long nx, long ny, lo
     const long grid = batch * a.groups;
     const double fields = OP == LN_MID ? 3.0 : 2.0;
     const double bytes = fields * (double)nx * ny * batch * sizeof(C);
-    timeit([&] { k<<<(unsigned)grid, threads, L::BYTES>>>((const C *)in, (C *)out, a, (const C *)tw, tab); },
+    timeit([&] { k<<<(unsigned)grid, threads, L::BYTES, g_stream>>>((const C *)in, (C *)out, a, (const C *)tw, tab); },
            name, bytes, occ, grid);
 }
 
@@ -123,7 +141,7 @@ static void wave_var(void *U, void *V, long nx, long ny, const void *tw, const O
     LineArgs a{nx, 1, nx, nx * ny, (nx + W - 1) / W, nullptr};
     const long grid = a.groups;
     const double bytes = 4.0 * nx * ny * sizeof(C);
-    timeit([&] { k<<<(unsigned)grid, threads, L::BYTES>>>((C *)U, (C *)V, a, (const C *)tw, tab); }, name, bytes,
+    timeit([&] { k<<<(unsigned)grid, threads, L::BYTES, g_stream>>>((C *)U, (C *)V, a, (const C *)tw, tab); }, name, bytes,
            occ, grid);
 }
 
@@ -151,8 +169,33 @@ static void rr_var(const void *in, void *out, void *out2, long nx, long ny, long
     if (grid > ntiles) grid = ntiles;
     const double fields = OP == LN_MID ? 3.0 : 2.0;
     const double bytes = fields * (double)nx * ny * batch * sizeof(C);
-    timeit([&] { k<<<(unsigned)grid, threads, L::BYTES>>>((const C *)in, (C *)out, a, ntiles, (const C *)tw, tab); },
+    timeit([&] { k<<<(unsigned)grid, threads, L::BYTES, g_stream>>>((const C *)in, (C *)out, a, ntiles, (const C *)tw, tab); },
            name, bytes, occ, grid);
+}
+
+// ---- tpipe_kernel variant (transposed spectrum side)
+template <typename T, int N, int W, int OP, int NBUF, bool TWREG>
+static void tpipe_var(const void *in, void *out, void *out2, long nx, long ny, long batch, const void *tw, const char *tag)
+{
+    using C = typename cplx_t<T>::type;
+    char name[160];
+    snprintf(name, sizeof name, "%s TPIPE op=%d W=%d nbuf=%d", tag, OP, W, NBUF);
+    if (g_filter && !strstr(name, g_filter)) return;
+    using L = PipeSmem<C, N, W, true, NBUF>;
+    auto k = tpipe_kernel<T, N, W, OP, NBUF, TWREG>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    const int threads = W * Shape<N>::TPT;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, L::BYTES);
+    TPipeArgs a{ny, nx, ny, nx * ny, nx * ny, 0, (ny + W - 1) / W, out2};
+    a.ntiles = batch * a.groups;
+    long grid = (long)occ * 148;
+    if (grid > a.ntiles) grid = a.ntiles;
+    const double fields = OP == TP_MID_T ? 3.0 : 2.0;
+    const double bytes = fields * (double)nx * ny * batch * sizeof(C);
+    timeit([&] { k<<<(unsigned)grid, threads, L::BYTES, g_stream>>>((const C *)in, (C *)out, a, (const C *)tw); }, name,
+           bytes, occ, grid);
 }
 
 // ---- pipe_kernel reference (current library configuration)
@@ -179,7 +222,7 @@ static void pipe_ref(const void *in, void *out, void *out2, long nx, long ny, lo
     if (grid > a.ntiles) grid = a.ntiles;
     const double fields = OP == PIPE_MID ? 3.0 : 2.0;
     const double bytes = fields * (double)nx * ny * batch * sizeof(C);
-    timeit([&] { k<<<(unsigned)grid, threads, L::BYTES>>>((const C *)in, (C *)out, a, (const C *)tw, tab); }, name,
+    timeit([&] { k<<<(unsigned)grid, threads, L::BYTES, g_stream>>>((const C *)in, (C *)out, a, (const C *)tw, tab); }, name,
            bytes, occ, grid);
 }
 
@@ -206,8 +249,31 @@ int main(int argc, char **argv)
         line_var<D, 1024, 8, 1, false, LN_MID, 4>(A, B, Cb, 1024, 1024, 1, t8, tab, "c2 rowsMID");
         line_var<D, 1024, 8, 4, false, LN_MID, 1>(A, B, Cb, 1024, 1024, 1, t8, tab, "c2 rowsMID");
         line_var<D, 1024, 4, 1, false, LN_MID, 4>(A, B, Cb, 1024, 1024, 1, t4, tab, "c2 rowsMID");
+        line_var<D, 1024, 16, 1, false, LN_MID, 7>(A, B, Cb, 1024, 1024, 1, t16, tab, "c2 rowsMID");
+        line_var<D, 1024, 16, 1, false, LN_MID, 4>(A, B, Cb, 1024, 1024, 1, t16, tab, "c2 rowsMID");
+        line_var<D, 1024, 8, 1, false, LN_MID, 7>(A, B, Cb, 1024, 1024, 1, t8, tab, "c2 rowsMID");
+        line_var<D, 1024, 16, 1, true, LN_DIFFUSE, 7>(B, B, nullptr, 1024, 1024, 1, t16, tab, "c2 colsDIF");
+        line_var<D, 1024, 16, 1, true, LN_DIFFUSE, 4>(B, B, nullptr, 1024, 1024, 1, t16, tab, "c2 colsDIF");
+        line_var<D, 1024, 8, 1, true, LN_DIFFUSE, 7>(B, B, nullptr, 1024, 1024, 1, t8, tab, "c2 colsDIF");
+        line_var<D, 1024, 16, 2, true, LN_DIFFUSE, 4>(B, B, nullptr, 1024, 1024, 1, t16, tab, "c2 colsDIF");
+        line_var<D, 1024, 8, 2, true, LN_DIFFUSE, 4>(B, B, nullptr, 1024, 1024, 1, t8, tab, "c2 colsDIF");
         line_var<D, 1024, 4, 1, false, LN_MID, 6>(A, B, Cb, 1024, 1024, 1, t4, tab, "c2 rowsMID");
         pipe_ref<D, 1024, 4, true, PIPE_DIFFUSE, 2, true>(B, B, nullptr, 1024, 1024, 1, t16, tab, "c2 colsDIF");
+        pipe_ref<D, 1024, 2, true, PIPE_DIFFUSE, 2, true>(B, B, nullptr, 1024, 1024, 1, t16, tab, "c2 colsDIF");
+        pipe_ref<D, 1024, 2, true, PIPE_DIFFUSE, 3, true>(B, B, nullptr, 1024, 1024, 1, t16, tab, "c2 colsDIF");
+        pipe_ref<D, 1024, 1, true, PIPE_DIFFUSE, 3, true>(B, B, nullptr, 1024, 1024, 1, t16, tab, "c2 colsDIF");
+        pipe_ref<D, 1024, 2, false, PIPE_MID, 2, true>(A, B, Cb, 1024, 1024, 1, t16, tab, "c2 rowsMID");
+        tpipe_var<D, 1024, 4, TP_MID_T, 2, true>(A, B, Cb, 1024, 1024, 1, t16, "c2 T");
+        tpipe_var<D, 1024, 2, TP_MID_T, 2, true>(A, B, Cb, 1024, 1024, 1, t16, "c2 T");
+        tpipe_var<D, 1024, 2, TP_MID_T, 3, true>(A, B, Cb, 1024, 1024, 1, t16, "c2 T");
+        tpipe_var<D, 1024, 4, TP_FWD_T, 2, true>(A, B, nullptr, 1024, 1024, 1, t16, "c2 T");
+        tpipe_var<D, 1024, 4, TP_INV_T, 2, true>(A, B, nullptr, 1024, 1024, 1, t16, "c2 T");
+        pipe_ref<D, 1024, 4, false, PIPE_DIFFUSE, 2, true>(B, B, nullptr, 1024, 1024, 1, t16, tab, "c2 TrowsDIF");
+        pipe_ref<D, 1024, 2, false, PIPE_DIFFUSE, 2, true>(B, B, nullptr, 1024, 1024, 1, t16, tab, "c2 TrowsDIF");
+        line_var<D, 1024, 16, 1, false, LN_DIFFUSE, 7>(B, B, nullptr, 1024, 1024, 1, t16, tab, "c2 TrowsDIF");
+        line_var<D, 1024, 16, 2, false, LN_DIFFUSE, 2>(B, B, nullptr, 1024, 1024, 1, t16, tab, "c2 TrowsDIF");
+        pipe_ref<D, 1024, 2, false, PIPE_MID, 3, true>(A, B, Cb, 1024, 1024, 1, t16, tab, "c2 rowsMID");
+        pipe_ref<D, 1024, 1, false, PIPE_MID, 3, true>(A, B, Cb, 1024, 1024, 1, t16, tab, "c2 rowsMID");
         line_var<D, 1024, 16, 2, true, LN_DIFFUSE, 1>(B, B, nullptr, 1024, 1024, 1, t16, tab, "c2 colsDIF");
         line_var<D, 1024, 16, 2, true, LN_DIFFUSE, 2>(B, B, nullptr, 1024, 1024, 1, t16, tab, "c2 colsDIF");
         line_var<D, 1024, 16, 4, true, LN_DIFFUSE, 1>(B, B, nullptr, 1024, 1024, 1, t16, tab, "c2 colsDIF");
