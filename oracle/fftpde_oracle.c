@@ -18,6 +18,8 @@
  *   Diffusion u^ = f^ e^{-w^2 t} (coefficient D per DESIGN.md R6)  solCalorFourier PAPER.md:376-386
  *   Wave     u^ = f^ cos(wt) + (g^/w) sin(wt);  w=0: u^ = g^ t + f^ eq:OmegaZero/NonZero PAPER.md:459-471
  *            v^ = d u^/dt
+ *   Wave with a time-dependent source: RK4 on du^/dt = v^,
+ *            dv^/dt = -w^2 u^ + s^(t), orbiting Gaussian source
  *
  * Readings of silent / garbled points are DESIGN.md R1..R16:
  *   forward sign +, unnormalised; inverse 1/N per axis; natural order with
@@ -439,6 +441,104 @@ int oracle_wave(int64_t nx, int64_t ny, int64_t batch, double Lx, double Ly,
         }
     }
     free(C); free(S1); free(S2); free(k2); free(wx); free(wy);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Orbiting Gaussian source ("Example with Source"):        */
+/*   s(t,x,y) = A exp(-[(x - x0)^2 + (y - y0)^2] / sigma^2) cos(gamma t),     */
+/*   x0 = rs cos(Omega t),  y0 = rs sin(Omega t),                             */
+/* sampled at x_j = xmin + j Lx/nx, y_k = ymin + k Ly/ny; on the periodic     */
+/* domain x - x0 and y - y0 are minimum images in [-L/2, L/2) (R21).*/
+static double min_image(double d, double L) { return d - L * floor(d / L + 0.5); }
+
+int oracle_orbit_source(int64_t nx, int64_t ny, double Lx, double Ly, double xmin, double ymin,
+                        double A, double sigma, double Omega, double gamma, double rs, double t,
+                        double *out)
+{
+    if (nx < 1 || ny < 1 || !out || !(Lx > 0.0) || !(Ly > 0.0) || !(sigma > 0.0)) return -1;
+    double x0 = rs * cos(Omega * t), y0 = rs * sin(Omega * t);
+    double amp = A * cos(gamma * t);
+    cplx *o = (cplx *)out;
+    for (int64_t k = 0; k < ny; ++k) {
+        double y = ymin + (double)k * Ly / (double)ny;
+        double dy = min_image(y - y0, Ly);
+        for (int64_t j = 0; j < nx; ++j) {
+            double x = xmin + (double)j * Lx / (double)nx;
+            double dx = min_image(x - x0, Lx);
+            o[k * nx + j].re = amp * exp(-(dx * dx + dy * dy) / (sigma * sigma));
+            o[k * nx + j].im = 0.0;
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Wave equation with a time-dependent source, u_tt = c^2 nabla^2 u + s      */
+/* (eq:wave_equation PAPER.md:417-424), in Fourier space the first-order     */
+/* system (eq:SystemOfODEsForWaveEquation PAPER.md:448-454)                   */
+/*   du^/dt = v^,   dv^/dt = -kappa^2 u^ + s^(t),   kappa = c|k|,             */
+/* integrated with the classical Runge-Kutta 4 scheme (stages   */
+/* combined as (k1 + 2 k2 + 2 k3 + k4)/6), the source re-sampled and           */
+/* transformed (path 2) at each stage time t, t + dt/2, t + dt (DESIGN.md     */
+/* R22).  u, ut: physical fields at t0 on entry, at t0 + nsteps dt on exit    */
+/* (inverse transforms).  means (nsteps + 1 complex, may be */
+/* NULL): the grid mean of u at t0 + n dt, = u^(0,0) / (nx ny).               */
+int oracle_wave_rk4(int64_t nx, int64_t ny, double Lx, double Ly, double xmin, double ymin, double c,
+                    double A, double sigma, double Omega, double gamma, double rs,
+                    double t0, double dt, int64_t nsteps, double *u, double *ut, double *means)
+{
+    int rc = check_grid(nx, ny, 1, 2);
+    if (rc) return rc;
+    if (!u || !ut || nsteps < 0 || !(Lx > 0.0) || !(Ly > 0.0) || c < 0.0 || !(sigma > 0.0)) return -1;
+    size_t plane = (size_t)(nx * ny);
+    cplx *wx = root_table(nx), *wy = root_table(ny);
+    double *k2 = ksq_table(nx, ny, Lx, Ly);
+    cplx *U = (cplx *)u, *V = (cplx *)ut;
+    cplx *s0 = (cplx *)malloc(sizeof(cplx) * plane);
+    cplx *sh = (cplx *)malloc(sizeof(cplx) * plane);
+    cplx *s1 = (cplx *)malloc(sizeof(cplx) * plane);
+    double inv_area = 1.0 / ((double)nx * (double)ny);
+    transform2d(nx, ny, U, 0, 2, wx, wy);                   /* u^ = F{f} */
+    transform2d(nx, ny, V, 0, 2, wx, wy);                   /* v^ = F{g} */
+    if (means) { means[0] = U[0].re * inv_area; means[1] = U[0].im * inv_area; }
+    for (int64_t n = 0; n < nsteps; ++n) {
+        double t = t0 + (double)n * dt;
+        oracle_orbit_source(nx, ny, Lx, Ly, xmin, ymin, A, sigma, Omega, gamma, rs, t, (double *)s0);
+        oracle_orbit_source(nx, ny, Lx, Ly, xmin, ymin, A, sigma, Omega, gamma, rs, t + 0.5 * dt, (double *)sh);
+        oracle_orbit_source(nx, ny, Lx, Ly, xmin, ymin, A, sigma, Omega, gamma, rs, t + dt, (double *)s1);
+        transform2d(nx, ny, s0, 0, 2, wx, wy);
+        transform2d(nx, ny, sh, 0, 2, wx, wy);
+        transform2d(nx, ny, s1, 0, 2, wx, wy);
+        for (size_t i = 0; i < plane; ++i) {
+            double w2 = c * c * k2[i];                        /* kappa^2 */
+            cplx u0 = U[i], v0 = V[i];
+            /* k1 = f(t, y) */
+            cplx k1u = v0;
+            cplx k1v = c_add(c_scale(u0, -w2), s0[i]);
+            /* k2 = f(t + dt/2, y + dt/2 k1) */
+            cplx u2 = c_add(u0, c_scale(k1u, 0.5 * dt)), v2 = c_add(v0, c_scale(k1v, 0.5 * dt));
+            cplx k2u = v2;
+            cplx k2v = c_add(c_scale(u2, -w2), sh[i]);
+            /* k3 = f(t + dt/2, y + dt/2 k2) */
+            cplx u3 = c_add(u0, c_scale(k2u, 0.5 * dt)), v3 = c_add(v0, c_scale(k2v, 0.5 * dt));
+            cplx k3u = v3;
+            cplx k3v = c_add(c_scale(u3, -w2), sh[i]);
+            /* k4 = f(t + dt, y + dt k3) */
+            cplx u4 = c_add(u0, c_scale(k3u, dt)), v4 = c_add(v0, c_scale(k3v, dt));
+            cplx k4u = v4;
+            cplx k4v = c_add(c_scale(u4, -w2), s1[i]);
+            /* y(t + dt) = y + dt/6 (k1 + 2 k2 + 2 k3 + k4) */
+            cplx su = c_add(c_add(k1u, c_scale(k2u, 2.0)), c_add(c_scale(k3u, 2.0), k4u));
+            cplx sv = c_add(c_add(k1v, c_scale(k2v, 2.0)), c_add(c_scale(k3v, 2.0), k4v));
+            U[i] = c_add(u0, c_scale(su, dt / 6.0));
+            V[i] = c_add(v0, c_scale(sv, dt / 6.0));
+        }
+        if (means) { means[2 * (n + 1)] = U[0].re * inv_area; means[2 * (n + 1) + 1] = U[0].im * inv_area; }
+    }
+    transform2d(nx, ny, U, 1, 2, wx, wy);
+    transform2d(nx, ny, V, 1, 2, wx, wy);
+    free(s0); free(sh); free(s1); free(k2); free(wx); free(wy);
     return 0;
 }
 

@@ -54,6 +54,9 @@ def lib():
                                ctypes.c_int, ctypes.c_int],
             "oracle_wave": [i64, i64, i64, dbl, dbl, dbl, dbl, i64, p, p,
                             ctypes.c_int, ctypes.c_int],
+            "oracle_orbit_source": [i64, i64, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, p],
+            "oracle_wave_rk4": [i64, i64, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, i64,
+                                p, p, p],
             "oracle_set_threads": [ctypes.c_int],
             "oracle_get_threads": [],
         }
@@ -188,3 +191,30 @@ def wave(u, ut, c: float, dt: float, nsteps: int, Lx: float = 1.0, Ly: float = 1
     _check(lib().oracle_wave(nx, ny, B, Lx, Ly, c, dt, int(nsteps), U.ctypes.data,
                              V.ctypes.data, int(collapsed), path), "wave")
     return U, V
+
+
+def orbit_source(nx: int, ny: int, t: float, Lx: float = 4.0, Ly: float = 4.0, xmin: float = -2.0,
+                 ymin: float = -2.0, A: float = 1.0, sigma: float = 0.1, Omega: float = 5.0,
+                 gamma: float = 10.0, rs: float = 0.5) -> np.ndarray:
+    """Orbiting Gaussian source s(t, x_j, y_k), [ny, nx] complex128."""
+    out = np.empty((ny, nx), np.complex128)
+    _check(lib().oracle_orbit_source(nx, ny, Lx, Ly, xmin, ymin, A, sigma, Omega, gamma, rs, t,
+                                     out.ctypes.data), "orbit_source")
+    return out
+
+
+def wave_rk4(u, ut, dt: float, nsteps: int, c: float = 1.0, t0: float = 0.0, Lx: float = 4.0,
+             Ly: float = 4.0, xmin: float = -2.0, ymin: float = -2.0, A: float = 1.0,
+             sigma: float = 0.1, Omega: float = 5.0, gamma: float = 10.0, rs: float = 0.5):
+    """RK4 on du^/dt = v^, dv^/dt = -(c|k|)^2 u^ + s^(t) with the orbiting source
+    (PAPER.md:448-456, 516-523).  Returns (u, ut, means) at t0 + nsteps dt; means[n]
+    is the grid mean of u at t0 + n dt."""
+    u = _c128(u).copy()
+    ut = _c128(ut).copy()
+    if u.ndim != 2 or u.shape != ut.shape:
+        raise OracleError("wave_rk4 expects two [ny, nx] fields")
+    ny, nx = u.shape
+    means = np.empty(nsteps + 1, np.complex128)
+    _check(lib().oracle_wave_rk4(nx, ny, Lx, Ly, xmin, ymin, c, A, sigma, Omega, gamma, rs, t0, dt,
+                                 nsteps, u.ctypes.data, ut.ctypes.data, means.ctypes.data), "wave_rk4")
+    return u, ut, means
