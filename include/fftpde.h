@@ -98,7 +98,8 @@ int64_t fftpde_launch_count(fftpde_plan plan);
 #define FFTPDE_KERNEL_COL 1       /* column pass (transform, or forward + operator + inverse along y) */
 #define FFTPDE_KERNEL_WAVE_COL 2  /* wave column pass (both fields) */
 #define FFTPDE_KERNEL_SMALL 3     /* single-CTA whole-grid solve */
-#define FFTPDE_KERNEL_CLASSES 4
+#define FFTPDE_KERNEL_POINTWISE 4 /* pointwise k-space / source kernels (RK4 path) */
+#define FFTPDE_KERNEL_CLASSES 5
 fftpde_status fftpde_set_profiling(fftpde_plan plan, int enable);
 fftpde_status fftpde_read_profile(fftpde_plan plan, int kernel_class, double *total_ms, int64_t *launches);
 
@@ -150,6 +151,31 @@ fftpde_status fftpde_diffuse_batched(fftpde_plan plan, const void *u0, void *u,
 fftpde_status fftpde_wave_step_batched(fftpde_plan plan, void *u, void *ut,
                                        int64_t batch, int64_t stride,
                                        double c, double dt, int64_t nsteps);
+
+/* ---- time-dependent source: RK4 ------------------------
+ * fftpde_wave_rk4: nsteps RK4 steps of dt (dt > 0) of the wave equation with the
+ *   paper's orbiting Gaussian source, u_tt = c^2 nabla^2 u + s(t, x, y),
+ *     s = A exp(-[(x - x0)^2 + (y - y0)^2]/sigma^2) cos(gamma t),
+ *     x0 = rs cos(Omega t), y0 = rs sin(Omega t),
+ *   sampled at x_j = xmin + j Lx/nx, y_k = ymin + k Ly/ny with periodic minimum
+ *   images (R21), integrated in Fourier space as the first-order
+ *   system du^/dt = v^, dv^/dt = -c^2|k|^2 u^ + s^(t) (eq:SystemOfODEsForWaveEquation,
+ *   PAPER.md:448-454) with classical RK4, the source re-sampled and
+ *   transformed at t, t + dt/2, t + dt of every step (R22).
+ *   u, ut: the plan's grid (batch 1), physical fields at t0 on entry and at
+ *   t0 + nsteps dt on exit (in place).  means: NULL or nsteps + 1 complex
+ *   elements of the plan's dtype on the device, means[n] = grid mean of u at
+ *   t0 + n dt (= u^(0,0)/(nx ny); the quantity of the paper's self-convergence
+ *   test, eq:SCF PAPER.md:533-553).  scratch: >= fftpde_wave_rk4_scratch_size()
+ *   bytes of device memory (5 spectra), caller-owned.
+ *   Errors: FFTPDE_ERR_UNSUPPORTED for a batched plan; FFTPDE_ERR_INVALID_ARG for
+ *   dt <= 0, nsteps < 0, c < 0, sigma <= 0, non-finite parameters, u == ut;
+ *   FFTPDE_ERR_WORKSPACE if scratch is missing or too small. */
+size_t fftpde_wave_rk4_scratch_size(fftpde_plan plan);
+fftpde_status fftpde_wave_rk4(fftpde_plan plan, void *u, void *ut, double c,
+                              double xmin, double ymin, double A, double sigma, double Omega,
+                              double gamma, double rs, double t0, double dt, int64_t nsteps,
+                              void *means, void *scratch, size_t scratch_bytes);
 
 /* ---- slab (sharded) building blocks ------------------------------------------
  * The slab decomposition of SURVEY.md 8(e): rank r of P owns rows

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <utility>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -416,6 +417,44 @@ template <typename T> struct Passes {
                 if (e == cudaSuccess) e = rows(SV, V, 1);
             }
         }
+        return e;
+    }
+    // RK4 with the orbiting source (rk4.cu): state (u^, v^) and three source
+    // spectra in the caller's scratch; the source transform reuses forward().
+    cudaError_t wave_rk4(void *u, void *ut, double c, const SrcParams &base, double A, double Omega, double gamma,
+                         double rs, double t0, double dt, int64_t nsteps, void *means, void *scratch)
+    {
+        const size_t fb = (size_t)(p->nx * p->ny) * elem_cplx(p);
+        unsigned char *sc = (unsigned char *)scratch;
+        void *Uh = sc, *Vh = sc + fb, *S[3] = {sc + 2 * fb, sc + 3 * fb, sc + 4 * fb};
+        auto source_spectrum = [&](double t, void *dst) {
+            SrcParams q = base;
+            q.x0 = rs * std::cos(Omega * t);
+            q.y0 = rs * std::sin(Omega * t);
+            q.amp = A * std::cos(gamma * t);
+            cudaError_t e = launch(p, FFTPDE_KERNEL_POINTWISE,
+                                   [&] { return launch_source<T>(dst, p->nx, p->ny, q, p->stream); });
+            return e == cudaSuccess ? forward(dst, dst) : e;
+        };
+        cudaError_t e = forward(u, Uh);
+        if (e == cudaSuccess) e = forward(ut, Vh);
+        if (e == cudaSuccess && means) { ++p->launches; e = launch_mean<T>(Uh, means, p->nx, p->ny, p->stream); }
+        if (e == cudaSuccess) e = source_spectrum(t0, S[0]);
+        int i0 = 0, ih = 1, i1 = 2;
+        for (int64_t n = 0; n < nsteps && e == cudaSuccess; ++n) {
+            const double t = t0 + (double)n * dt;
+            e = source_spectrum(t + 0.5 * dt, S[ih]);
+            if (e == cudaSuccess) e = source_spectrum(t + dt, S[i1]);
+            if (e != cudaSuccess) break;
+            void *mo = means ? (unsigned char *)means + (size_t)(n + 1) * elem_cplx(p) : nullptr;
+            e = launch(p, FFTPDE_KERNEL_POINTWISE, [&] {
+                return launch_rk4<T>(Uh, Vh, S[i0], S[ih], S[i1], p->nx, p->ny, p->ws + p->o_kx2, p->ws + p->o_ky2,
+                                     c, dt, mo, p->stream);
+            });
+            std::swap(i0, i1);                      // s^(t + dt) is the next step's s^(t)
+        }
+        if (e == cudaSuccess) e = inverse(Uh, u);
+        if (e == cudaSuccess) e = inverse(Vh, ut);
         return e;
     }
 };
@@ -947,6 +986,49 @@ fftpde_status fftpde_pack_blocks(fftpde_plan p, const void *in, void *out, int64
     if (!g.ok) return FFTPDE_ERR_CUDA;
     ++p->launches;
     return cuda_status(launch_pack(in, out, nrows, nblocks, bytes, direction, p->stream));
+}
+
+// ---- time-dependent source: RK4 ----------------------------------------------
+size_t fftpde_wave_rk4_scratch_size(fftpde_plan p)
+{
+    return p ? 5 * (size_t)(p->nx * p->ny) * elem_cplx(p) : 0;
+}
+
+fftpde_status fftpde_wave_rk4(fftpde_plan p, void *u, void *ut, double c, double xmin, double ymin, double A,
+                              double sigma, double Omega, double gamma, double rs, double t0, double dt,
+                              int64_t nsteps, void *means, void *scratch, size_t scratch_bytes)
+{
+    if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (!p->ws) return FFTPDE_ERR_WORKSPACE;
+    if (p->batch != 1) return FFTPDE_ERR_UNSUPPORTED;
+    fftpde_status s = check_ptr(p, u);
+    if (s == FFTPDE_OK) s = check_ptr(p, ut);
+    if (s != FFTPDE_OK) return s;
+    if (u == ut) return FFTPDE_ERR_INVALID_ARG;
+    const double prm[] = {c, xmin, ymin, A, sigma, Omega, gamma, rs, t0, dt};
+    for (double v : prm)
+        if (!std::isfinite(v)) return FFTPDE_ERR_INVALID_ARG;
+    if (c < 0 || !(sigma > 0) || !(dt > 0) || nsteps < 0) return FFTPDE_ERR_INVALID_ARG;
+    if (means && ((uintptr_t)means % elem_cplx(p))) return FFTPDE_ERR_INVALID_ARG;
+    if (!scratch || scratch_bytes < fftpde_wave_rk4_scratch_size(p) || ((uintptr_t)scratch & 255u))
+        return FFTPDE_ERR_WORKSPACE;
+    SrcParams base{xmin, ymin, p->Lx, p->Ly, 0.0, 0.0, 0.0, sigma};
+    // the stage times and source positions are kernel arguments baked into the
+    // captured graph: every parameter is part of the graph key
+    uint64_t hsh = 1469598103934665603ull;
+    auto mix = [&](const void *d, size_t n) {
+        const unsigned char *b = (const unsigned char *)d;
+        for (size_t i = 0; i < n; ++i) { hsh ^= b[i]; hsh *= 1099511628211ull; }
+    };
+    mix(prm, sizeof prm);
+    mix(&scratch, sizeof scratch);
+    const std::array<uint64_t, 6> key{3, (uint64_t)(uintptr_t)u, (uint64_t)(uintptr_t)ut, (uint64_t)(uintptr_t)means,
+                                      (uint64_t)nsteps, hsh};
+    return run_graphed(p, key, [&] {
+        return dispatch(p, 1, p->nx * p->ny, [&](auto &ps) {
+            return ps.wave_rk4(u, ut, c, base, A, Omega, gamma, rs, t0, dt, nsteps, means, scratch);
+        });
+    });
 }
 
 // ---- whole-plan entry points --------------------------------------------------

@@ -75,6 +75,23 @@ cudaError_t launch_small(int64_t nx, int64_t ny, const void *in, void *out, int6
                          int64_t batch, int op, const void *twx, const void *twy,
                          const OpTables<T> &tab, cudaStream_t st);
 
+// ---- time-dependent source path (rk4.cu) ----
+// Orbiting Gaussian source at one time t: the host evaluates
+// x0 = rs cos(Omega t), y0 = rs sin(Omega t), amp = A cos(gamma t) in fp64.
+struct SrcParams {
+    double xmin, ymin, Lx, Ly;   // grid x_j = xmin + j Lx/nx, y_k = ymin + k Ly/ny
+    double x0, y0, amp, sigma;
+};
+template <typename T>
+cudaError_t launch_source(void *s, int64_t nx, int64_t ny, const SrcParams &p, cudaStream_t st);
+// One RK4 step of du^/dt = v^, dv^/dt = -c^2 |k|^2 u^ + s^ on every mode, given
+// s^ at t, t + dt/2, t + dt; optional mean_out <- u^(0,0)/(nx ny) after the step.
+template <typename T>
+cudaError_t launch_rk4(void *U, void *V, const void *S0, const void *Sh, const void *S1, int64_t nx, int64_t ny,
+                       const void *kx2, const void *ky2, double c, double dt, void *mean_out, cudaStream_t st);
+template <typename T>
+cudaError_t launch_mean(const void *U, void *out, int64_t nx, int64_t ny, cudaStream_t st);
+
 // Block transpose of the sharded path (pack.cu); bw_bytes a multiple of 16.
 cudaError_t launch_pack(const void *in, void *out, int64_t nrows, int64_t nblocks, int64_t bw_bytes,
                         int direction, cudaStream_t st);

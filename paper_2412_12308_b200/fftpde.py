@@ -20,7 +20,7 @@ import torch
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libfftpde.so")
 
-KERNEL_CLASSES = {0: "row_pass", 1: "col_pass", 2: "wave_col_pass", 3: "small_solve"}
+KERNEL_CLASSES = {0: "row_pass", 1: "col_pass", 2: "wave_col_pass", 3: "small_solve", 4: "pointwise"}
 
 # fftpde_status
 OK, ERR_INVALID_ARG, ERR_EMPTY, ERR_NOT_POW2_X, ERR_NOT_POW2_Y, ERR_UNSUPPORTED, ERR_WORKSPACE, \
@@ -35,6 +35,7 @@ EXPORTS = [
     "fftpde_forward_batched", "fftpde_inverse_batched", "fftpde_poisson_batched",
     "fftpde_diffuse_batched", "fftpde_wave_step_batched",
     "fftpde_rows", "fftpde_cols_slab", "fftpde_pack_blocks",
+    "fftpde_wave_rk4_scratch_size", "fftpde_wave_rk4",
 ]
 OP_POISSON, OP_DIFFUSE = 2, 3
 
@@ -82,6 +83,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fftpde_rows": (st, [p, p, p, i64, u]),
         "fftpde_cols_slab": (st, [p, p, p, i64, i64, u, dbl, dbl]),
         "fftpde_pack_blocks": (st, [p, p, p, i64, i64, i64, u]),
+        "fftpde_wave_rk4_scratch_size": (ctypes.c_size_t, [p]),
+        "fftpde_wave_rk4": (st, [p, p, p, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, i64, p, p,
+                                 ctypes.c_size_t]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -269,6 +273,31 @@ class Plan:
         if host:
             return self._finish(ud, True), self._finish(vd, True)
         return ud, vd
+
+    def wave_rk4(self, u: torch.Tensor, ut: torch.Tensor, dt: float, nsteps: int, c: float = 1.0,
+                 t0: float = 0.0, xmin: float = 0.0, ymin: float = 0.0, A: float = 1.0,
+                 sigma: float = 0.1, Omega: float = 5.0, gamma: float = 10.0, rs: float = 0.5):
+        """nsteps RK4 steps of u_tt = c^2 nabla^2 u + s with the orbiting Gaussian
+        source on the plan's grid x_j = xmin + j Lx/nx.
+
+        (u, ut) are device tensors updated in place; returns the grid means of u at
+        t0 + n dt, n = 0..nsteps (a device tensor of the plan's dtype)."""
+        if self._grid(u, "u") != 1 or self._grid(ut, "ut") != 1 or u.dim() != 2:
+            raise ValueError("wave_rk4: expects [ny, nx] fields (batch 1)")
+        for x, name in ((u, "u"), (ut, "ut")):
+            if x.device != self.device or not x.is_contiguous():
+                raise ValueError(f"wave_rk4 updates in place: {name} must be a contiguous device tensor")
+        nbytes = int(self.lib.fftpde_wave_rk4_scratch_size(self._h))
+        if getattr(self, "_rk4_scratch", None) is None or self._rk4_scratch.numel() < nbytes:
+            self._rk4_scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        means = torch.empty(int(nsteps) + 1, dtype=self.dtype, device=self.device)
+        self._bind_stream()
+        _check(self.lib.fftpde_wave_rk4(self._h, u.data_ptr(), ut.data_ptr(), float(c), float(xmin),
+                                        float(ymin), float(A), float(sigma), float(Omega), float(gamma),
+                                        float(rs), float(t0), float(dt), int(nsteps), means.data_ptr(),
+                                        self._rk4_scratch.data_ptr(), self._rk4_scratch.numel()),
+               "fftpde_wave_rk4")
+        return means
 
     # -- slab (sharded) building blocks ------------------------------------------------
     def rows(self, x: torch.Tensor, out: torch.Tensor, inverse: bool = False):

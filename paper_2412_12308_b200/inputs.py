@@ -55,6 +55,14 @@ C4 = Workload("c4_batched_poisson_256x512", "poisson", 512, 512, 256, "c64")
 C5 = Workload("c5_diffusion_32768", "diffuse", 32768, 32768, 1, "c128", nsteps=20, D=1e-4, dt=0.01)
 WORKLOADS = {"c1": C1, "c2": C2, "c3": C3, "c4": C4, "c5": C5}
 
+# SURVEY.md 8(f) row 1 (not a BASELINE config): the paper's orbiting-source wave run,
+# D = [-2, 2]^2, dt = 0.25 h, t in [0, 2.5], and a B200-sized variant.
+RK4 = Workload("rk4_orbit_256", "rk4", 256, 256, 1, "c128", nsteps=640, dt=0.25 * 4.0 / 256, c=1.0,
+               Lx=4.0, Ly=4.0)
+RK4_BIG = Workload("rk4_orbit_4096", "rk4", 4096, 4096, 1, "c128", nsteps=50, dt=0.25 * 4.0 / 4096, c=1.0,
+                   Lx=4.0, Ly=4.0)
+EXTRA_WORKLOADS = {"rk4": RK4, "rk4big": RK4_BIG}
+
 
 def rng_for(config_index: int) -> np.random.Generator:
     """PCG64 stream for config i (1-based, BASELINE.json configs[i-1])."""
