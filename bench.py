@@ -58,7 +58,9 @@ def parse_args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "rk4", "rk4big"],
+                    help="c1-c5: BASELINE.json configs[0..4]; rk4/rk4big: the paper's orbiting-source "
+                         "RK4 run (SURVEY.md 8(f) row 1, not a BASELINE config)")
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -82,6 +84,9 @@ def make_inputs(wl):
         return (w.u, w.ut)
     if wl.name.startswith("c4"):
         return (I.c4_inputs(wl.nx, wl.batch).astype(np.complex64),)
+    if wl.op == "rk4":                      # from rest (R19)
+        z = np.zeros((wl.ny, wl.nx), np.complex128)
+        return (z, z.copy())
     raise ValueError(wl.name)
 
 
@@ -108,6 +113,10 @@ def alg_bytes_per_launch(wl, kernel_class):
     field = wl.nx * wl.ny * wl.batch * esz
     if kernel_class == "wave_col_pass":
         return 2 * 2 * field
+    if wl.op == "rk4":
+        # per step: 2 source samplings (1 write each) and the RK4 kernel (u^, v^, 3 source
+        # spectra read, u^, v^ written); the transforms are plain forward passes
+        return 3 * field if kernel_class == "pointwise" else 2 * field
     if kernel_class == "row_pass" and wl.op in ("diffuse", "wave") and wl.nsteps > 1:
         n = wl.nsteps                      # per field: 1 FWD + (n-1) MID + 1 INV launches
         return (2 * field * 2 + 3 * field * (n - 1)) / (n + 1)
@@ -212,12 +221,14 @@ def run_solve(plan, wl, dev_in, out):
         plan.poisson(dev_in[0], out=out[0])
     elif wl.op == "diffuse":
         plan.diffuse(dev_in[0], wl.D, wl.dt, wl.nsteps, out=out[0])
+    elif wl.op == "rk4":
+        plan.wave_rk4(out[0], out[1], wl.dt, wl.nsteps, c=wl.c, xmin=-0.5 * wl.Lx, ymin=-0.5 * wl.Ly)
     else:  # wave: advance a working copy (reset from the input outside the events)
         plan.wave_step(out[0], out[1], wl.c, wl.dt, wl.nsteps)
 
 
 def reset_wave(wl, dev_in, out):
-    if wl.op == "wave":
+    if wl.op in ("wave", "rk4"):
         out[0].copy_(dev_in[0])
         out[1].copy_(dev_in[1])
 
@@ -325,6 +336,13 @@ def native(args, wl, world, rank, local):
                 plan.poisson(host_in[0], out=host_out[0])
             elif wl.op == "diffuse":
                 plan.diffuse(host_in[0], wl.D, wl.dt, wl.nsteps, out=host_out[0])
+            elif wl.op == "rk4":            # in place on device copies of the host fields
+                for d, h in zip(out, host_in):
+                    d.copy_(h, non_blocking=True)
+                plan.wave_rk4(out[0], out[1], wl.dt, wl.nsteps, c=wl.c, xmin=-0.5 * wl.Lx, ymin=-0.5 * wl.Ly)
+                for h, d in zip(host_out, out):
+                    h.copy_(d, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
             else:
                 plan.wave_step(host_in[0], host_in[1], wl.c, wl.dt, wl.nsteps)
         e2e_step()
@@ -437,7 +455,7 @@ def alg_step_bytes(wl):
     """Algorithmic bytes of one bench step: each state field read + written once per
     solve step."""
     esz = 16 if wl.dtype == "c128" else 8
-    fields = 2 if wl.op == "wave" else 1
+    fields = 2 if wl.op in ("wave", "rk4") else 1
     steps = wl.nsteps if wl.op != "poisson" else 1
     return 2 * fields * wl.nx * wl.ny * wl.batch * esz * steps
 
@@ -450,6 +468,10 @@ def workload_config(wl, world):
         cfg.update({"nsteps": wl.nsteps, "D": wl.D, "dt": wl.dt})
     if wl.op == "wave":
         cfg.update({"nsteps": wl.nsteps, "c": wl.c, "dt": wl.dt})
+    if wl.op == "rk4":
+        cfg.update({"nsteps": wl.nsteps, "c": wl.c, "dt": wl.dt, "domain": "[-2,2]^2",
+                    "source": "orbiting Gaussian A=1 sigma=0.1 Omega=5 gamma=10 r_s=0.5 (PAPER.md:516-523)",
+                    "baseline_config": False})
     return cfg
 
 
@@ -481,6 +503,16 @@ def oracle_sample(wl, host, budget_s=12.0):
         O.diffuse(host[0], wl.D, wl.dt, k, wl.Lx, wl.Ly)
         dt = time.perf_counter() - t0
         return wl.nx * wl.ny * k / dt, f"{k} of {wl.nsteps} stepped diffusion steps ({wl.ny}x{wl.nx}, full grid)"
+    if wl.op == "rk4":
+        src = dict(Lx=wl.Lx, Ly=wl.Ly, xmin=-0.5 * wl.Lx, ymin=-0.5 * wl.Ly)
+        t0 = time.perf_counter()
+        O.wave_rk4(host[0], host[1], wl.dt, 1, c=wl.c, **src)
+        one = time.perf_counter() - t0
+        k = max(1, min(wl.nsteps, int(budget_s / max(one, 1e-6))))
+        t0 = time.perf_counter()
+        O.wave_rk4(host[0], host[1], wl.dt, k, c=wl.c, **src)
+        dt = time.perf_counter() - t0
+        return wl.nx * wl.ny * k / dt, f"{k} of {wl.nsteps} RK4 steps ({wl.ny}x{wl.nx})"
     t0 = time.perf_counter()
     O.wave(host[0], host[1], wl.c, wl.dt, 1, wl.Lx, wl.Ly)
     one = time.perf_counter() - t0
@@ -546,7 +578,7 @@ def main():
     args = parse_args()
     import torch
     from paper_2412_12308_b200 import inputs as I
-    wl = I.WORKLOADS[args.workload]
+    wl = I.WORKLOADS.get(args.workload) or I.EXTRA_WORKLOADS[args.workload]
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         world = int(os.environ.get("WORLD_SIZE", "1"))
