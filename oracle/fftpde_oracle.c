@@ -18,6 +18,8 @@
  *   Diffusion u^ = f^ e^{-w^2 t} (coefficient D per DESIGN.md R6)  solCalorFourier PAPER.md:376-386
  *   Wave     u^ = f^ cos(wt) + (g^/w) sin(wt);  w=0: u^ = g^ t + f^ eq:OmegaZero/NonZero PAPER.md:459-471
  *            v^ = d u^/dt
+ *   Diagonal operators  F^-1{(-i w)^k F{u}}: Laplacian, d/dx, d/dy
+ *   Diffusion + static source: exact integrator of du^/dt = -D w^2 u^ + s^
  *   Wave with a time-dependent source: RK4 on du^/dt = v^,
  *            dv^/dt = -w^2 u^ + s^(t), orbiting Gaussian source
  *
@@ -441,6 +443,86 @@ int oracle_wave(int64_t nx, int64_t ny, int64_t batch, double Lx, double Ly,
         }
     }
     free(C); free(S1); free(S2); free(k2); free(wx); free(wy);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Diagonal k-space operators:  out = F^-1{ m F{in} }  */
+/* with F{d^k u/dx^k} = (-i omega)^k F{u} under the forward */
+/* sign + (R1); omega = 2 pi fold(a)/L, Nyquist bin +N/2 (R2, R24): */
+/*   op 0  Laplacian      m = -(kx^2 + ky^2)                                  */
+/*   op 1  d/dx           m = -i kx                                            */
+/*   op 2  d/dy           m = -i ky                                            */
+int oracle_kspace_apply(int64_t nx, int64_t ny, int64_t batch, double Lx, double Ly, int op,
+                        const double *in, double *out)
+{
+    int rc = check_grid(nx, ny, batch, 2);
+    if (rc) return rc;
+    if (!in || !out || !(Lx > 0.0) || !(Ly > 0.0) || op < 0 || op > 2) return -1;
+    size_t plane = (size_t)(nx * ny);
+    cplx *wx = root_table(nx), *wy = root_table(ny);
+    double *kx = (double *)malloc(sizeof(double) * (size_t)nx);
+    double *ky = (double *)malloc(sizeof(double) * (size_t)ny);
+    oracle_wavenumbers(nx, Lx, kx);
+    oracle_wavenumbers(ny, Ly, ky);
+    if (out != in) memcpy(out, in, sizeof(cplx) * plane * (size_t)batch);
+    for (int64_t bi = 0; bi < batch; ++bi) {
+        cplx *g = (cplx *)out + bi * plane;
+        transform2d(nx, ny, g, 0, 2, wx, wy);
+        for (int64_t b = 0; b < ny; ++b)
+            for (int64_t a = 0; a < nx; ++a) {
+                cplx v = g[b * nx + a], r;
+                if (op == 0) {
+                    r = c_scale(v, -(kx[a] * kx[a] + ky[b] * ky[b]));
+                } else {
+                    double k = op == 1 ? kx[a] : ky[b];
+                    r.re = k * v.im;                      /* (-i k) (x + i y) = k y - i k x */
+                    r.im = -k * v.re;
+                }
+                g[b * nx + a] = r;
+            }
+        transform2d(nx, ny, g, 1, 2, wx, wy);
+    }
+    free(kx); free(ky); free(wx); free(wy);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Diffusion with a static source, u_t = D nabla^2 u + s (eq. EcuacionDeCalor */
+/* PAPER.md:355-367; coefficient D per R6).  In Fourier space                 */
+/* du^/dt = -D w^2 u^ + s^ (eq:DiffusionIVPFS PAPER.md:369-376), integrated   */
+/* exactly over each step (the closed form of solCalorFourier extended by the */
+/* constant forcing):                                                          */
+/*   u^(t + dt) = E u^(t) + Phi s^,   E = exp(-D w^2 dt),                      */
+/*   Phi = -expm1(-D w^2 dt) / (D w^2)   (w != 0, D > 0),   Phi = dt otherwise.*/
+/* Stepped: nsteps x (forward u, update, inverse) materialising u (R8); s^ is */
+/* the transform of the source, computed once.  In place on u.                 */
+int oracle_diffuse_source(int64_t nx, int64_t ny, int64_t batch, double Lx, double Ly, double D,
+                          double dt, int64_t nsteps, double *u, const double *src)
+{
+    int rc = check_grid(nx, ny, batch, 2);
+    if (rc) return rc;
+    if (!u || !src || nsteps < 0 || !(Lx > 0.0) || !(Ly > 0.0) || D < 0.0 || dt < 0.0) return -1;
+    size_t plane = (size_t)(nx * ny);
+    cplx *wx = root_table(nx), *wy = root_table(ny);
+    double *k2 = ksq_table(nx, ny, Lx, Ly);
+    cplx *S = (cplx *)malloc(sizeof(cplx) * plane);
+    for (int64_t bi = 0; bi < batch; ++bi) {
+        cplx *U = (cplx *)u + bi * plane;
+        memcpy(S, (const cplx *)src + bi * plane, sizeof(cplx) * plane);
+        transform2d(nx, ny, S, 0, 2, wx, wy);
+        for (int64_t n = 0; n < nsteps; ++n) {
+            transform2d(nx, ny, U, 0, 2, wx, wy);
+            for (size_t i = 0; i < plane; ++i) {
+                double x = D * k2[i] * dt;
+                double E = exp(-x);
+                double Phi = x > 0.0 ? -expm1(-x) / (D * k2[i]) : dt;
+                U[i] = c_add(c_scale(U[i], E), c_scale(S[i], Phi));
+            }
+            transform2d(nx, ny, U, 1, 2, wx, wy);
+        }
+    }
+    free(S); free(k2); free(wx); free(wy);
     return 0;
 }
 

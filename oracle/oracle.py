@@ -54,6 +54,8 @@ def lib():
                                ctypes.c_int, ctypes.c_int],
             "oracle_wave": [i64, i64, i64, dbl, dbl, dbl, dbl, i64, p, p,
                             ctypes.c_int, ctypes.c_int],
+            "oracle_kspace_apply": [i64, i64, i64, dbl, dbl, ctypes.c_int, p, p],
+            "oracle_diffuse_source": [i64, i64, i64, dbl, dbl, dbl, dbl, i64, p, p],
             "oracle_orbit_source": [i64, i64, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, p],
             "oracle_wave_rk4": [i64, i64, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, i64,
                                 p, p, p],
@@ -218,3 +220,27 @@ def wave_rk4(u, ut, dt: float, nsteps: int, c: float = 1.0, t0: float = 0.0, Lx:
     _check(lib().oracle_wave_rk4(nx, ny, Lx, Ly, xmin, ymin, c, A, sigma, Omega, gamma, rs, t0, dt,
                                  nsteps, u.ctypes.data, ut.ctypes.data, means.ctypes.data), "wave_rk4")
     return u, ut, means
+
+
+KOPS = {"laplacian": 0, "dx": 1, "dy": 2}
+
+
+def kspace_apply(p, op: str, Lx: float = 1.0, Ly: float = 1.0) -> np.ndarray:
+    """F^-1{m F{p}}, m = -|k|^2 (laplacian), -i kx (dx), -i ky (dy)."""
+    p, B, ny, nx = _grid(p)
+    out = np.empty_like(p)
+    _check(lib().oracle_kspace_apply(nx, ny, B, Lx, Ly, KOPS[op], p.ctypes.data, out.ctypes.data),
+           "kspace_apply")
+    return out
+
+
+def diffuse_source(u0, s, D: float, dt: float, nsteps: int, Lx: float = 1.0, Ly: float = 1.0) -> np.ndarray:
+    """nsteps exact steps of u_t = D nabla^2 u + s, static s."""
+    u, B, ny, nx = _grid(u0)
+    u = u.copy()
+    s, Bs, nys, nxs = _grid(s)
+    if (Bs, nys, nxs) != (B, ny, nx):
+        raise OracleError("diffuse_source: u0 and s shapes differ")
+    _check(lib().oracle_diffuse_source(nx, ny, B, Lx, Ly, D, dt, nsteps, u.ctypes.data, s.ctypes.data),
+           "diffuse_source")
+    return u
