@@ -58,7 +58,7 @@ def parse_args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "rk4", "rk4big"],
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "rk4", "rk4big", "dsrc"],
                     help="c1-c5: BASELINE.json configs[0..4]; rk4/rk4big: the paper's orbiting-source "
                          "RK4 run (SURVEY.md 8(f) row 1, not a BASELINE config)")
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
@@ -84,6 +84,9 @@ def make_inputs(wl):
         return (w.u, w.ut)
     if wl.name.startswith("c4"):
         return (I.c4_inputs(wl.nx, wl.batch).astype(np.complex64),)
+    if wl.op == "dsrc":                     # C2 Gaussians as initial field and as the static source
+        g = I.c2_inputs(wl.nx).u0
+        return (g, np.ascontiguousarray(0.5 * g))
     if wl.op == "rk4":                      # from rest (R19)
         z = np.zeros((wl.ny, wl.nx), np.complex128)
         return (z, z.copy())
@@ -113,6 +116,9 @@ def alg_bytes_per_launch(wl, kernel_class):
     field = wl.nx * wl.ny * wl.batch * esz
     if kernel_class == "wave_col_pass":
         return 2 * 2 * field
+    if wl.op == "dsrc":
+        # per step: forward (rows, columns), u^ <- E u^ + Phi s^ (u^, s^ in, u^ out), inverse
+        return 3 * field if kernel_class == "pointwise" else 2 * field
     if wl.op == "rk4":
         # per step: 2 source samplings (1 write each) and the RK4 kernel (u^, v^, 3 source
         # spectra read, u^, v^ written); the transforms are plain forward passes
@@ -223,6 +229,8 @@ def run_solve(plan, wl, dev_in, out):
         plan.diffuse(dev_in[0], wl.D, wl.dt, wl.nsteps, out=out[0])
     elif wl.op == "rk4":
         plan.wave_rk4(out[0], out[1], wl.dt, wl.nsteps, c=wl.c, xmin=-0.5 * wl.Lx, ymin=-0.5 * wl.Ly)
+    elif wl.op == "dsrc":
+        plan.diffuse_source(dev_in[0], dev_in[1], wl.D, wl.dt, wl.nsteps, out=out[0])
     else:  # wave: advance a working copy (reset from the input outside the events)
         plan.wave_step(out[0], out[1], wl.c, wl.dt, wl.nsteps)
 
@@ -336,6 +344,8 @@ def native(args, wl, world, rank, local):
                 plan.poisson(host_in[0], out=host_out[0])
             elif wl.op == "diffuse":
                 plan.diffuse(host_in[0], wl.D, wl.dt, wl.nsteps, out=host_out[0])
+            elif wl.op == "dsrc":
+                plan.diffuse_source(host_in[0], host_in[1], wl.D, wl.dt, wl.nsteps, out=host_out[0])
             elif wl.op == "rk4":            # in place on device copies of the host fields
                 for d, h in zip(out, host_in):
                     d.copy_(h, non_blocking=True)
@@ -464,8 +474,10 @@ def workload_config(wl, world):
     cfg = {"workload": wl.name, "nx": wl.nx, "ny": wl.ny, "batch": wl.batch, "dtype": wl.dtype,
            "op": wl.op, "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
            "l2": "flushed between timed steps (256 MiB write)"}
-    if wl.op == "diffuse":
+    if wl.op in ("diffuse", "dsrc"):
         cfg.update({"nsteps": wl.nsteps, "D": wl.D, "dt": wl.dt})
+    if wl.op == "dsrc":
+        cfg.update({"source": "static: 0.5 x the C2 Gaussians", "baseline_config": False})
     if wl.op == "wave":
         cfg.update({"nsteps": wl.nsteps, "c": wl.c, "dt": wl.dt})
     if wl.op == "rk4":
@@ -503,6 +515,15 @@ def oracle_sample(wl, host, budget_s=12.0):
         O.diffuse(host[0], wl.D, wl.dt, k, wl.Lx, wl.Ly)
         dt = time.perf_counter() - t0
         return wl.nx * wl.ny * k / dt, f"{k} of {wl.nsteps} stepped diffusion steps ({wl.ny}x{wl.nx}, full grid)"
+    if wl.op == "dsrc":
+        t0 = time.perf_counter()
+        O.diffuse_source(host[0], host[1], wl.D, wl.dt, 1)
+        one = time.perf_counter() - t0
+        k = max(1, min(wl.nsteps, int(budget_s / max(one, 1e-6))))
+        t0 = time.perf_counter()
+        O.diffuse_source(host[0], host[1], wl.D, wl.dt, k)
+        dt = time.perf_counter() - t0
+        return wl.nx * wl.ny * k / dt, f"{k} of {wl.nsteps} sourced diffusion steps ({wl.ny}x{wl.nx})"
     if wl.op == "rk4":
         src = dict(Lx=wl.Lx, Ly=wl.Ly, xmin=-0.5 * wl.Lx, ymin=-0.5 * wl.Ly)
         t0 = time.perf_counter()

@@ -152,6 +152,29 @@ fftpde_status fftpde_wave_step_batched(fftpde_plan plan, void *u, void *ut,
                                        int64_t batch, int64_t stride,
                                        double c, double dt, int64_t nsteps);
 
+/* ---- diagonal k-space operators ------------------------
+ * fftpde_apply: out = iDFT2( m .* DFT2(in) ) over the plan's batch, with
+ *   F{d^k u/dx^k} = (-i w)^k F{u} under the forward sign + (R1):
+ *   FFTPDE_KOP_LAPLACIAN  m = -(kx^2 + ky^2)
+ *   FFTPDE_KOP_DX         m = -i kx          (spectral d/dx)
+ *   FFTPDE_KOP_DY         m = -i ky          (spectral d/dy)
+ *   kx = 2 pi fold(a)/Lx with the Nyquist bin at +nx/2 (R2): odd operators see
+ *   that choice (R24).  in == out allowed.  Unknown op:
+ *   FFTPDE_ERR_INVALID_ARG.
+ * fftpde_diffuse_source: nsteps exact steps of u_t = D nabla^2 u + s with a static
+ *   source s (coefficient D per R6): per step u^ <- E u^ + Phi s^,
+ *   E = exp(-D|k|^2 dt), Phi = (1 - E)/(D|k|^2) (k != 0, D > 0) or dt, each step
+ *   materialising u (R8).  u0, s, u: [batch][ny][nx] (u0 == u allowed); scratch:
+ *   >= fftpde_diffuse_source_scratch_size() bytes of device memory (two spectra
+ *   per grid), caller-owned.  D >= 0, dt >= 0, nsteps >= 0 (0 copies u0). */
+#define FFTPDE_KOP_LAPLACIAN 0
+#define FFTPDE_KOP_DX 1
+#define FFTPDE_KOP_DY 2
+fftpde_status fftpde_apply(fftpde_plan plan, const void *in, void *out, int op);
+size_t fftpde_diffuse_source_scratch_size(fftpde_plan plan);
+fftpde_status fftpde_diffuse_source(fftpde_plan plan, const void *u0, const void *s, void *u, double D,
+                                    double dt, int64_t nsteps, void *scratch, size_t scratch_bytes);
+
 /* ---- time-dependent source: RK4 ------------------------
  * fftpde_wave_rk4: nsteps RK4 steps of dt (dt > 0) of the wave equation with the
  *   paper's orbiting Gaussian source, u_tt = c^2 nabla^2 u + s(t, x, y),

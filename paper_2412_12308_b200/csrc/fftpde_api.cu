@@ -33,7 +33,7 @@ struct fftpde_plan_s {
     unsigned char *ws = nullptr;
     size_t ws_bytes = 0;
     // workspace offsets (bytes)
-    size_t o_twx = 0, o_twy = 0, o_twx8 = 0, o_twy8 = 0, o_kx2 = 0, o_ky2 = 0, o_ex = 0, o_ey = 0, o_wc = 0, o_ws1 = 0, o_ws2 = 0;
+    size_t o_twx = 0, o_twy = 0, o_twx8 = 0, o_twy8 = 0, o_kx = 0, o_ky = 0, o_kx2 = 0, o_ky2 = 0, o_ex = 0, o_ey = 0, o_wc = 0, o_ws1 = 0, o_ws2 = 0;
     size_t o_twP = 0, o_twQ = 0, o_twN = 0;   // two-level column pass tables (P, Q > 0)
     size_t o_scr = 0;                          // scratch: row spectra of 2 fields (multi-step solves)
     int64_t colP = 0, colQ = 0;
@@ -47,6 +47,7 @@ struct fftpde_plan_s {
     std::vector<double> twx, twy;   // interleaved re, im (radix-16 stage tables)
     std::vector<double> twx8, twy8; // radix-8 stage tables (line_kernel E = 8)
     std::vector<double> kx2, ky2;
+    std::vector<double> kx, ky;     // signed 2 pi fold(a)/L (odd operators)
     bool diff_valid = false;
     double diff_D = 0, diff_dt = 0;
     bool wave_valid = false;
@@ -127,6 +128,14 @@ void build_twiddles(int64_t n, std::vector<double> &tw, int64_t emax = 16)
         for (int64_t m = 0; m < n / ns; ++m)
             for (int64_t j = 0; j < ns; ++j) put(n, m * j);
     if (tw.empty()) { tw.push_back(1.0); tw.push_back(0.0); }
+}
+
+// 2 pi fold(a) / L, fold(a) = a for a <= n/2 else a - n (Nyquist at +n/2, R2)
+void build_k(int64_t n, double L, std::vector<double> &k)
+{
+    k.resize((size_t)n);
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int64_t a = 0; a < n; ++a) k[(size_t)a] = two_pi * (double)((2 * a <= n) ? a : a - n) / L;
 }
 
 // (2 pi fold(a) / L)^2, fold(a) = a for a <= n/2 else a - n
@@ -419,6 +428,36 @@ template <typename T> struct Passes {
         }
         return e;
     }
+    cudaError_t kop(void *X, const void *S, int op, double D, double dt)
+    {
+        return launch(p, FFTPDE_KERNEL_POINTWISE, [&] {
+            return launch_kop<T>(X, S, p->nx, p->ny, batch, stride, op, p->ws + p->o_kx, p->ws + p->o_ky,
+                                 p->ws + p->o_kx2, p->ws + p->o_ky2, D, dt, p->stream);
+        });
+    }
+    // out = iDFT2(m .* DFT2(in)), m a diagonal operator (kspace.cu)
+    cudaError_t apply(const void *in, void *out, int op)
+    {
+        cudaError_t e = forward(in, out);
+        if (e == cudaSuccess) e = kop(out, nullptr, op, 0.0, 0.0);
+        if (e == cudaSuccess) e = inverse(out, out);
+        return e;
+    }
+    // exact steps of u_t = D nabla^2 u + s (static s): s^ once, then per step
+    // forward u, u^ <- E u^ + Phi s^, inverse (materialising u)
+    cudaError_t diffuse_source(const void *u0, const void *src, void *u, double D, double dt, int64_t nsteps,
+                               void *scratch)
+    {
+        const size_t fb = (size_t)(batch * stride) * elem_cplx(p);
+        void *Sh = scratch, *Uh = (unsigned char *)scratch + fb;
+        cudaError_t e = forward(src, Sh);
+        for (int64_t n = 0; n < nsteps && e == cudaSuccess; ++n) {
+            e = forward(n == 0 ? u0 : u, Uh);
+            if (e == cudaSuccess) e = kop(Uh, Sh, KOP_DIFFSRC, D, dt);
+            if (e == cudaSuccess) e = inverse(Uh, u);
+        }
+        return e;
+    }
     // RK4 with the orbiting source (rk4.cu): state (u^, v^) and three source
     // spectra in the caller's scratch; the source transform reuses forward().
     cudaError_t wave_rk4(void *u, void *ut, double c, const SrcParams &base, double A, double Omega, double gamma,
@@ -689,6 +728,8 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     build_twiddles(ny, p->twy8, 8);
     build_k2(nx, Lx, p->kx2);
     build_k2(ny, Ly, p->ky2);
+    build_k(nx, Lx, p->kx);
+    build_k(ny, Ly, p->ky);
     fftpde::col2_split(ny, nx, dtype == FFTPDE_C128 ? 16 : 8, p->colP, p->colQ);
     if (p->colP) {
         build_twiddles(p->colP, p->twP, FFTPDE_COL2_EMAX);
@@ -711,6 +752,8 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     p->o_twy8 = take(p->twy8.size() / 2 * ec);
     p->o_kx2 = take((size_t)nx * er);
     p->o_ky2 = take((size_t)ny * er);
+    p->o_kx = take((size_t)nx * er);
+    p->o_ky = take((size_t)ny * er);
     p->o_ex = take((size_t)nx * er);
     p->o_ey = take((size_t)ny * er);
     const size_t q = (size_t)(p->qx * p->qy) * er;
@@ -779,6 +822,8 @@ fftpde_status fftpde_set_workspace(fftpde_plan plan, void *dev_ptr, size_t bytes
     }
     if (s == FFTPDE_OK) s = upload(plan, plan->o_kx2, plan->kx2);
     if (s == FFTPDE_OK) s = upload(plan, plan->o_ky2, plan->ky2);
+    if (s == FFTPDE_OK) s = upload(plan, plan->o_kx, plan->kx);
+    if (s == FFTPDE_OK) s = upload(plan, plan->o_ky, plan->ky);
     if (s != FFTPDE_OK) plan->ws = nullptr;
     return s;
 }
@@ -986,6 +1031,50 @@ fftpde_status fftpde_pack_blocks(fftpde_plan p, const void *in, void *out, int64
     if (!g.ok) return FFTPDE_ERR_CUDA;
     ++p->launches;
     return cuda_status(launch_pack(in, out, nrows, nblocks, bytes, direction, p->stream));
+}
+
+// ---- diagonal k-space operators ----------------------------------------------------
+fftpde_status fftpde_apply(fftpde_plan p, const void *in, void *out, int op)
+{
+    if (!p) return FFTPDE_ERR_INVALID_ARG;
+    fftpde_status s = check_call(p, p->batch, p->nx * p->ny);
+    if (s == FFTPDE_OK) s = check_ptr(p, in);
+    if (s == FFTPDE_OK) s = check_ptr(p, out);
+    if (s != FFTPDE_OK) return s;
+    if (op != FFTPDE_KOP_LAPLACIAN && op != FFTPDE_KOP_DX && op != FFTPDE_KOP_DY) return FFTPDE_ERR_INVALID_ARG;
+    return dispatch(p, p->batch, p->nx * p->ny, [&](auto &ps) { return ps.apply(in, out, op); });
+}
+
+size_t fftpde_diffuse_source_scratch_size(fftpde_plan p)
+{
+    return p ? 2 * (size_t)(p->batch * p->nx * p->ny) * elem_cplx(p) : 0;
+}
+
+fftpde_status fftpde_diffuse_source(fftpde_plan p, const void *u0, const void *src, void *u, double D, double dt,
+                                    int64_t nsteps, void *scratch, size_t scratch_bytes)
+{
+    if (!p) return FFTPDE_ERR_INVALID_ARG;
+    fftpde_status s = check_call(p, p->batch, p->nx * p->ny);
+    if (s == FFTPDE_OK) s = check_ptr(p, u0);
+    if (s == FFTPDE_OK) s = check_ptr(p, src);
+    if (s == FFTPDE_OK) s = check_ptr(p, u);
+    if (s != FFTPDE_OK) return s;
+    if (!std::isfinite(D) || !std::isfinite(dt) || D < 0 || dt < 0 || nsteps < 0) return FFTPDE_ERR_INVALID_ARG;
+    if (src == u && u != u0) return FFTPDE_ERR_INVALID_ARG;
+    if (nsteps == 0) return copy_grids(p, u0, u, p->batch, p->nx * p->ny);
+    if (!scratch || scratch_bytes < fftpde_diffuse_source_scratch_size(p) || ((uintptr_t)scratch & 255u))
+        return FFTPDE_ERR_WORKSPACE;
+    uint64_t hsh = 1469598103934665603ull;
+    const double prm[2] = {D, dt};
+    const void *ptrs[2] = {src, scratch};
+    for (const unsigned char *b : {(const unsigned char *)prm, (const unsigned char *)ptrs})
+        for (size_t i = 0; i < 16; ++i) { hsh ^= b[i]; hsh *= 1099511628211ull; }
+    const std::array<uint64_t, 6> key{4, (uint64_t)(uintptr_t)u0, (uint64_t)(uintptr_t)u, (uint64_t)p->batch,
+                                      (uint64_t)nsteps, hsh};
+    return run_graphed(p, key, [&] {
+        return dispatch(p, p->batch, p->nx * p->ny,
+                        [&](auto &ps) { return ps.diffuse_source(u0, src, u, D, dt, nsteps, scratch); });
+    });
 }
 
 // ---- time-dependent source: RK4 ----------------------------------------------

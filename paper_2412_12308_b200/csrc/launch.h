@@ -92,6 +92,13 @@ cudaError_t launch_rk4(void *U, void *V, const void *S0, const void *Sh, const v
 template <typename T>
 cudaError_t launch_mean(const void *U, void *out, int64_t nx, int64_t ny, cudaStream_t st);
 
+// ---- diagonal k-space operators (kspace.cu) ----
+enum KOp { KOP_LAPLACIAN = 0, KOP_DX = 1, KOP_DY = 2, KOP_DIFFSRC = 3 };
+template <typename T>
+cudaError_t launch_kop(void *X, const void *S, int64_t nx, int64_t ny, int64_t batch, int64_t stride, int op,
+                       const void *kx, const void *ky, const void *kx2, const void *ky2, double D, double dt,
+                       cudaStream_t st);
+
 // Block transpose of the sharded path (pack.cu); bw_bytes a multiple of 16.
 cudaError_t launch_pack(const void *in, void *out, int64_t nrows, int64_t nblocks, int64_t bw_bytes,
                         int direction, cudaStream_t st);

@@ -36,7 +36,9 @@ EXPORTS = [
     "fftpde_diffuse_batched", "fftpde_wave_step_batched",
     "fftpde_rows", "fftpde_cols_slab", "fftpde_pack_blocks",
     "fftpde_wave_rk4_scratch_size", "fftpde_wave_rk4",
+    "fftpde_apply", "fftpde_diffuse_source_scratch_size", "fftpde_diffuse_source",
 ]
+KOP = {"laplacian": 0, "dx": 1, "dy": 2}
 OP_POISSON, OP_DIFFUSE = 2, 3
 
 
@@ -84,6 +86,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fftpde_cols_slab": (st, [p, p, p, i64, i64, u, dbl, dbl]),
         "fftpde_pack_blocks": (st, [p, p, p, i64, i64, i64, u]),
         "fftpde_wave_rk4_scratch_size": (ctypes.c_size_t, [p]),
+        "fftpde_apply": (st, [p, p, p, u]),
+        "fftpde_diffuse_source_scratch_size": (ctypes.c_size_t, [p]),
+        "fftpde_diffuse_source": (st, [p, p, p, p, dbl, dbl, i64, p, ctypes.c_size_t]),
         "fftpde_wave_rk4": (st, [p, p, p, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, i64, p, p,
                                  ctypes.c_size_t]),
     }
@@ -273,6 +278,34 @@ class Plan:
         if host:
             return self._finish(ud, True), self._finish(vd, True)
         return ud, vd
+
+    def apply(self, x: torch.Tensor, op: str, out=None) -> torch.Tensor:
+        """iDFT2(m .* DFT2(x)): m = -|k|^2 ("laplacian"), -i kx ("dx"), -i ky ("dy")
+        (F{du/dx} = -i w F{u}) over the plan's whole batch."""
+        if self._grid(x, "x") != self.batch:
+            raise ValueError("apply acts on the plan's whole batch")
+        xd, host = self._to_dev(x)
+        o = self._out(xd, None if host else out)
+        self._bind_stream()
+        _check(self.lib.fftpde_apply(self._h, xd.data_ptr(), o.data_ptr(), KOP[op]), "fftpde_apply")
+        return self._finish(o, host, out if host else None)
+
+    def diffuse_source(self, u0: torch.Tensor, s: torch.Tensor, D: float, dt: float, nsteps: int,
+                       out=None) -> torch.Tensor:
+        """nsteps exact steps of u_t = D nabla^2 u + s, static s."""
+        if self._grid(u0, "u0") != self.batch or self._grid(s, "s") != self.batch:
+            raise ValueError("diffuse_source acts on the plan's whole batch")
+        ud, host = self._to_dev(u0)
+        sd, _ = self._to_dev(s)
+        o = self._out(ud, None if host else out)
+        nbytes = int(self.lib.fftpde_diffuse_source_scratch_size(self._h))
+        if getattr(self, "_ds_scratch", None) is None or self._ds_scratch.numel() < nbytes:
+            self._ds_scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self._bind_stream()
+        _check(self.lib.fftpde_diffuse_source(self._h, ud.data_ptr(), sd.data_ptr(), o.data_ptr(), float(D),
+                                              float(dt), int(nsteps), self._ds_scratch.data_ptr(),
+                                              self._ds_scratch.numel()), "fftpde_diffuse_source")
+        return self._finish(o, host, out if host else None)
 
     def wave_rk4(self, u: torch.Tensor, ut: torch.Tensor, dt: float, nsteps: int, c: float = 1.0,
                  t0: float = 0.0, xmin: float = 0.0, ymin: float = 0.0, A: float = 1.0,

@@ -61,7 +61,10 @@ RK4 = Workload("rk4_orbit_256", "rk4", 256, 256, 1, "c128", nsteps=640, dt=0.25 
                Lx=4.0, Ly=4.0)
 RK4_BIG = Workload("rk4_orbit_4096", "rk4", 4096, 4096, 1, "c128", nsteps=50, dt=0.25 * 4.0 / 4096, c=1.0,
                    Lx=4.0, Ly=4.0)
-EXTRA_WORKLOADS = {"rk4": RK4, "rk4big": RK4_BIG}
+# SURVEY.md 8(f) row 2 (not a BASELINE config): diffusion with a static source, the C2
+# grid and Gaussians as both the initial field and the source (exact integrator per step)
+DSRC = Workload("dsrc_diffusion_1024", "dsrc", 1024, 1024, 1, "c128", nsteps=200, D=1e-3, dt=0.01)
+EXTRA_WORKLOADS = {"rk4": RK4, "rk4big": RK4_BIG, "dsrc": DSRC}
 
 
 def rng_for(config_index: int) -> np.random.Generator:
