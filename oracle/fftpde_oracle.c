@@ -18,6 +18,7 @@
  *   Diffusion u^ = f^ e^{-w^2 t} (coefficient D per DESIGN.md R6)  solCalorFourier PAPER.md:376-386
  *   Wave     u^ = f^ cos(wt) + (g^/w) sin(wt);  w=0: u^ = g^ t + f^ eq:OmegaZero/NonZero PAPER.md:459-471
  *            v^ = d u^/dt
+ *   3D transform, Poisson and diffusion (n-D extension)
  *   Diagonal operators  F^-1{(-i w)^k F{u}}: Laplacian, d/dx, d/dy
  *   Diffusion + static source: exact integrator of du^/dt = -D w^2 u^ + s^
  *   Wave with a time-dependent source: RK4 on du^/dt = v^,
@@ -443,6 +444,82 @@ int oracle_wave(int64_t nx, int64_t ny, int64_t batch, double Lx, double Ly,
         }
     }
     free(C); free(S1); free(S2); free(k2); free(wx); free(wy);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* 3D: the n-D extension of the 2D recipe, "extended analogously" to further  */
+/* dimensions: sequential 1D transforms along x (rows), y and  */
+/* z.  Grid [nz][ny][nx], x fastest.  Forward sign +, inverse 1/N per axis.   */
+static void transform3d(int64_t nx, int64_t ny, int64_t nz, cplx *g, int inverse,
+                        const cplx *wx, const cplx *wy, const cplx *wz)
+{
+    size_t plane = (size_t)(nx * ny);
+    for (int64_t z = 0; z < nz; ++z) transform2d(nx, ny, g + (size_t)z * plane, inverse, 2, wx, wy);
+    #pragma omp parallel
+    {
+        cplx *a = (cplx *)malloc(sizeof(cplx) * (size_t)nz);
+        cplx *b = (cplx *)malloc(sizeof(cplx) * (size_t)nz);
+        cplx *t = (cplx *)malloc(sizeof(cplx) * (size_t)nz);
+        #pragma omp for schedule(static)
+        for (int64_t c = 0; c < nx * ny; ++c) {
+            for (int64_t z = 0; z < nz; ++z) a[z] = g[(size_t)z * plane + c];
+            fft1_path2(nz, a, b, inverse, wz, t);
+            for (int64_t z = 0; z < nz; ++z) g[(size_t)z * plane + c] = b[z];
+        }
+        free(a); free(b); free(t);
+    }
+}
+
+int oracle_fft3(int64_t nx, int64_t ny, int64_t nz, const double *in, double *out, int inverse)
+{
+    int rc = check_grid(nx, ny, nz, 2);
+    if (rc) return rc;
+    if (!is_pow2(nz)) return -2;
+    if (!in || !out) return -1;
+    cplx *wx = root_table(nx), *wy = root_table(ny), *wz = root_table(nz);
+    if (out != in) memcpy(out, in, sizeof(cplx) * (size_t)(nx * ny * nz));
+    transform3d(nx, ny, nz, (cplx *)out, inverse, wx, wy, wz);
+    free(wx); free(wy); free(wz);
+    return 0;
+}
+
+/* 3D Poisson (op 0: m = -1/|k|^2, k = 0 zeroed, eq:SolutionPoisson PAPER.md: */
+/* 329-331) and exact diffusion steps (op 1: m = exp(-D |k|^2 dt), PAPER.md:  */
+/* 378-386, stepped nsteps times materialising u, R8), |k|^2 = kx^2 + ky^2 +  */
+/* kz^2.  In place on u.                                                       */
+int oracle_solve3(int64_t nx, int64_t ny, int64_t nz, double Lx, double Ly, double Lz, int op,
+                  double D, double dt, int64_t nsteps, double *u)
+{
+    int rc = check_grid(nx, ny, nz, 2);
+    if (rc) return rc;
+    if (!is_pow2(nz)) return -2;
+    if (!u || !(Lx > 0.0) || !(Ly > 0.0) || !(Lz > 0.0) || op < 0 || op > 1 || nsteps < 0) return -1;
+    size_t plane = (size_t)(nx * ny), vol = plane * (size_t)nz;
+    cplx *wx = root_table(nx), *wy = root_table(ny), *wz = root_table(nz);
+    double *kx = (double *)malloc(sizeof(double) * (size_t)nx);
+    double *ky = (double *)malloc(sizeof(double) * (size_t)ny);
+    double *kz = (double *)malloc(sizeof(double) * (size_t)nz);
+    oracle_wavenumbers(nx, Lx, kx);
+    oracle_wavenumbers(ny, Ly, ky);
+    oracle_wavenumbers(nz, Lz, kz);
+    double *m = (double *)malloc(sizeof(double) * vol);
+    for (int64_t z = 0; z < nz; ++z)
+        for (int64_t y = 0; y < ny; ++y)
+            for (int64_t x = 0; x < nx; ++x) {
+                double k2 = kx[x] * kx[x] + ky[y] * ky[y] + kz[z] * kz[z];
+                size_t i = (size_t)z * plane + (size_t)y * (size_t)nx + (size_t)x;
+                if (op == 0) m[i] = k2 == 0.0 ? 0.0 : -1.0 / k2;
+                else m[i] = exp(-D * k2 * dt);
+            }
+    int64_t reps = op == 0 ? 1 : nsteps;
+    cplx *g = (cplx *)u;
+    for (int64_t s = 0; s < reps; ++s) {
+        transform3d(nx, ny, nz, g, 0, wx, wy, wz);
+        for (size_t i = 0; i < vol; ++i) g[i] = c_scale(g[i], m[i]);
+        transform3d(nx, ny, nz, g, 1, wx, wy, wz);
+    }
+    free(m); free(kx); free(ky); free(kz); free(wx); free(wy); free(wz);
     return 0;
 }
 

@@ -54,6 +54,8 @@ def lib():
                                ctypes.c_int, ctypes.c_int],
             "oracle_wave": [i64, i64, i64, dbl, dbl, dbl, dbl, i64, p, p,
                             ctypes.c_int, ctypes.c_int],
+            "oracle_fft3": [i64, i64, i64, p, p, ctypes.c_int],
+            "oracle_solve3": [i64, i64, i64, dbl, dbl, dbl, ctypes.c_int, dbl, dbl, i64, p],
             "oracle_kspace_apply": [i64, i64, i64, dbl, dbl, ctypes.c_int, p, p],
             "oracle_diffuse_source": [i64, i64, i64, dbl, dbl, dbl, dbl, i64, p, p],
             "oracle_orbit_source": [i64, i64, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, p],
@@ -243,4 +245,36 @@ def diffuse_source(u0, s, D: float, dt: float, nsteps: int, Lx: float = 1.0, Ly:
         raise OracleError("diffuse_source: u0 and s shapes differ")
     _check(lib().oracle_diffuse_source(nx, ny, B, Lx, Ly, D, dt, nsteps, u.ctypes.data, s.ctypes.data),
            "diffuse_source")
+    return u
+
+
+def _vol(a):
+    a = _c128(a)
+    if a.ndim != 3:
+        raise OracleError("expected a [nz, ny, nx] volume")
+    return a, a.shape[2], a.shape[1], a.shape[0]
+
+
+def fft3(p, inverse: bool = False) -> np.ndarray:
+    """3D transform by sequential 1D transforms along x, y, z."""
+    p, nx, ny, nz = _vol(p)
+    out = np.empty_like(p)
+    _check(lib().oracle_fft3(nx, ny, nz, p.ctypes.data, out.ctypes.data, int(inverse)), "fft3")
+    return out
+
+
+def poisson3(rho, Lx: float = 1.0, Ly: float = 1.0, Lz: float = 1.0) -> np.ndarray:
+    """3D Poisson, -1/|k|^2 with k = 0 zeroed (eq:SolutionPoisson extended)."""
+    u, nx, ny, nz = _vol(rho)
+    u = u.copy()
+    _check(lib().oracle_solve3(nx, ny, nz, Lx, Ly, Lz, 0, 0.0, 0.0, 1, u.ctypes.data), "poisson3")
+    return u
+
+
+def diffuse3(u0, D: float, dt: float, nsteps: int, Lx: float = 1.0, Ly: float = 1.0,
+             Lz: float = 1.0) -> np.ndarray:
+    """nsteps exact 3D diffusion steps exp(-D|k|^2 dt)."""
+    u, nx, ny, nz = _vol(u0)
+    u = u.copy()
+    _check(lib().oracle_solve3(nx, ny, nz, Lx, Ly, Lz, 1, D, dt, nsteps, u.ctypes.data), "diffuse3")
     return u
