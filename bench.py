@@ -58,7 +58,7 @@ def parse_args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "rk4", "rk4big", "dsrc"],
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "rk4", "rk4big", "dsrc", "p3d", "d3d"],
                     help="c1-c5: BASELINE.json configs[0..4]; rk4/rk4big: the paper's orbiting-source "
                          "RK4 run (SURVEY.md 8(f) row 1, not a BASELINE config)")
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
@@ -84,6 +84,8 @@ def make_inputs(wl):
         return (w.u, w.ut)
     if wl.name.startswith("c4"):
         return (I.c4_inputs(wl.nx, wl.batch).astype(np.complex64),)
+    if wl.nz > 1:                           # 3D workloads: seeded Gaussians on [0,1)^3
+        return (I.gaussians_3d(wl.nx),)
     if wl.op == "dsrc":                     # C2 Gaussians as initial field and as the static source
         g = I.c2_inputs(wl.nx).u0
         return (g, np.ascontiguousarray(0.5 * g))
@@ -113,7 +115,7 @@ def alg_bytes_per_launch(wl, kernel_class):
     + forward rows of step s+1: one read, two writes), the first and last are
     plain forward / inverse rows (one read, one write)."""
     esz = 16 if wl.dtype == "c128" else 8
-    field = wl.nx * wl.ny * wl.batch * esz
+    field = wl.nx * wl.ny * wl.nz * wl.batch * esz
     if kernel_class == "wave_col_pass":
         return 2 * 2 * field
     if wl.op == "dsrc":
@@ -251,7 +253,10 @@ def native(args, wl, world, rank, local):
     if host is None:          # C5: host copies only where needed (e2e / cpu baseline are bounded)
         args.no_e2e = True
     out = [torch.empty_like(d) for d in dev_in]
-    plan = F.Plan(wl.nx, wl.ny, batch=wl.batch, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly)
+    if wl.nz > 1:
+        plan = F.Plan3D(wl.nx, wl.ny, wl.nz, dtype=dtype)
+    else:
+        plan = F.Plan(wl.nx, wl.ny, batch=wl.batch, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly)
     stream = torch.cuda.current_stream()
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
@@ -283,7 +288,7 @@ def native(args, wl, world, rank, local):
     ms_rank = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     ms_total = max_over_ranks(world, ms_rank)
     ms_per_step = ms_total / args.steps
-    pts_per_step = wl.nx * wl.ny * wl.batch * (wl.nsteps if wl.op != "poisson" else 1)
+    pts_per_step = wl.points * (wl.nsteps if wl.op != "poisson" else 1)
     value = world * pts_per_step * args.steps / (ms_total * 1e-3)
 
     # ---- per-kernel timing (same calls, events around every launch)
@@ -467,11 +472,12 @@ def alg_step_bytes(wl):
     esz = 16 if wl.dtype == "c128" else 8
     fields = 2 if wl.op in ("wave", "rk4") else 1
     steps = wl.nsteps if wl.op != "poisson" else 1
-    return 2 * fields * wl.nx * wl.ny * wl.batch * esz * steps
+    return 2 * fields * wl.points * esz * steps
 
 
 def workload_config(wl, world):
-    cfg = {"workload": wl.name, "nx": wl.nx, "ny": wl.ny, "batch": wl.batch, "dtype": wl.dtype,
+    cfg = {"workload": wl.name, "nx": wl.nx, "ny": wl.ny, **({"nz": wl.nz} if wl.nz > 1 else {}),
+           "batch": wl.batch, "dtype": wl.dtype,
            "op": wl.op, "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
            "l2": "flushed between timed steps (256 MiB write)"}
     if wl.op in ("diffuse", "dsrc"):
@@ -493,6 +499,16 @@ def oracle_sample(wl, host, budget_s=12.0):
     """Time the oracle on a bounded sample of the workload; returns (pts/s, desc)."""
     import numpy as np
     from oracle import oracle as O
+    if wl.nz > 1:
+        t0 = time.perf_counter()
+        if wl.op == "poisson":
+            O.poisson3(host[0])
+            k, what = 1, "1 3D Poisson solve"
+        else:
+            O.diffuse3(host[0], wl.D, wl.dt, 1)
+            k, what = 1, f"1 of {wl.nsteps} 3D diffusion steps"
+        dt = time.perf_counter() - t0
+        return wl.points * k / dt, f"{what} ({wl.nz}x{wl.ny}x{wl.nx})"
     if wl.op == "poisson":
         grids = host[0].astype(np.complex128)
         if grids.ndim == 2:
@@ -583,7 +599,7 @@ def reference(args, wl, world, rank):
         vals.append(v)
         descs.append(d)
     value = statistics.median(vals)
-    pts_step = wl.nx * wl.ny * wl.batch * (wl.nsteps if wl.op != "poisson" else 1)
+    pts_step = wl.points * (wl.nsteps if wl.op != "poisson" else 1)
     return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": pts_step / value * 1e3,

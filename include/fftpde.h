@@ -59,7 +59,8 @@ typedef enum {
     FFTPDE_ERR_UNSUPPORTED = 5,  /* axis longer than this build supports, or batch outside the plan */
     FFTPDE_ERR_WORKSPACE = 6,    /* workspace missing or smaller than fftpde_workspace_size() */
     FFTPDE_ERR_CUDA = 7,         /* a CUDA runtime call or kernel launch failed */
-    FFTPDE_ERR_NCCL = 8          /* reserved for the sharded path */
+    FFTPDE_ERR_NCCL = 8,         /* reserved for the sharded path */
+    FFTPDE_ERR_NOT_POW2_Z = 9    /* nz not a power of two (3D plans) */
 } fftpde_status;
 
 /* Create a plan for batch grids of ny x nx points on the periodic domain
@@ -69,6 +70,17 @@ typedef enum {
  * error. */
 fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t batch,
                              fftpde_dtype dtype, double Lx, double Ly, int device);
+
+/* 3D plan (the n-D extension): [nz][ny][nx] grids on
+ * [0,Lx) x [0,Ly) x [0,Lz), x fastest.  Transforms are sequential 1D passes
+ * along x, y and z; the whole-plan calls fftpde_forward / fftpde_inverse /
+ * fftpde_poisson (-1/|k|^2, k = 0 zeroed) / fftpde_diffuse (exp(-D|k|^2 dt),
+ * |k|^2 = kx^2 + ky^2 + kz^2) act on the volume; fftpde_wave_step, the
+ * *_batched calls and the other operators return FFTPDE_ERR_UNSUPPORTED.
+ * nz <= 1024 in this build (single-level z-pass); nx, ny as fftpde_plan_2d.
+ * Errors as fftpde_plan_2d, plus FFTPDE_ERR_NOT_POW2_Z. */
+fftpde_status fftpde_plan_3d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t nz, fftpde_dtype dtype,
+                             double Lx, double Ly, double Lz, int device);
 
 /* Bytes of device workspace the plan needs (tables + operator tables). */
 size_t fftpde_workspace_size(fftpde_plan plan);

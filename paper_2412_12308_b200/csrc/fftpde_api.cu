@@ -53,6 +53,15 @@ struct fftpde_plan_s {
     bool wave_valid = false;
     double wave_c = 0, wave_dt = 0;
     int64_t launches = 0;
+    // 3D plans (fftpde_plan_3d): the 2D machinery runs with batch = nz slabs; the
+    // z-pass is a column pass of length nz over the nx*ny lines of the volume
+    bool is3d = false;
+    int64_t nz = 1;
+    double Lz = 1.0;
+    std::vector<double> twz, twz8, kz2, kxy2;
+    size_t o_twz = 0, o_twz8 = 0, o_kz2 = 0, o_kxy2 = 0, o_exy = 0, o_ez = 0;
+    bool diff3_valid = false;
+    double diff3_D = 0, diff3_dt = 0;
     // optional per-launch timing (fftpde_set_profiling): event pairs per kernel class
     bool profiling = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[FFTPDE_KERNEL_CLASSES];
@@ -248,6 +257,7 @@ fftpde_status check_ptr(fftpde_plan p, const void *ptr)
 fftpde_status check_call(fftpde_plan p, int64_t batch, int64_t stride)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (p->is3d) return FFTPDE_ERR_UNSUPPORTED;     // 3D plans: the whole-plan entry points only
     if (!p->ws) return FFTPDE_ERR_WORKSPACE;
     if (batch == 0) return FFTPDE_ERR_EMPTY;
     if (batch < 0 || stride < p->nx * p->ny) return FFTPDE_ERR_INVALID_ARG;
@@ -425,6 +435,78 @@ template <typename T> struct Passes {
                 e = rows(SU, U, 1);
                 if (e == cudaSuccess) e = rows(SV, V, 1);
             }
+        }
+        return e;
+    }
+    // ---- 3D (fftpde_plan_3d): this Passes runs with batch = nz, stride = nx ny ----
+    template <bool ZOP> OpTables<T> tables3(T scale) const
+    {
+        OpTables<T> t = tables<T>(p);
+        if (ZOP) {            // z-pass: line index = x + nx y, element index = z
+            t.kx2 = (const T *)(p->ws + p->o_kxy2);
+            t.ky2 = (const T *)(p->ws + p->o_kz2);
+            t.ex = (const T *)(p->ws + p->o_exy);
+            t.ey = (const T *)(p->ws + p->o_ez);
+        }
+        t.scale = scale;
+        return t;
+    }
+    T scale3() const { return (T)(1.0 / ((double)p->nx * (double)p->ny * (double)p->nz)); }
+    cudaError_t ypass(const void *in, void *out, int op)
+    {
+        // forward, or the inverse left unscaled (1/(nx ny nz) is applied in the z-pass)
+        return launch(p, FFTPDE_KERNEL_COL, [&] {
+            return launch_cols<T>(p->ny, in, out, p->nx, stride, batch, op, ctw(), tables3<false>((T)1), p->stream);
+        });
+    }
+    cudaError_t zpass(const void *in, void *out, int op)
+    {
+        const ColTw ztw{p->ws + p->o_twz, nullptr, nullptr, nullptr, p->ws + p->o_twz8};
+        return launch(p, FFTPDE_KERNEL_COL, [&] {
+            return launch_cols<T>(p->nz, in, out, p->nx * p->ny, p->nx * p->ny * p->nz, 1, op, ztw,
+                                  tables3<true>(scale3()), p->stream);
+        });
+    }
+    // The two-level y-pass's plain forward / inverse are out of place (col2.cuh),
+    // so with p->colP they go through the scratch; the operator passes are in place.
+    cudaError_t forward3(const void *in, void *out)
+    {
+        void *A = p->colP ? scratch(0) : out;
+        cudaError_t e = rows(in, A, 0);
+        if (e == cudaSuccess) e = ypass(A, out, COL_FWD);
+        if (e == cudaSuccess) e = zpass(out, out, COL_FWD);
+        return e;
+    }
+    cudaError_t inverse3(const void *in, void *out)
+    {
+        void *B = p->colP ? scratch(0) : out;
+        cudaError_t e = zpass(in, out, COL_INV);
+        if (e == cudaSuccess) e = ypass(out, B, COL_INV);
+        if (e == cudaSuccess) e = rows(B, out, 1);
+        return e;
+    }
+    cudaError_t poisson3(const void *in, void *out)
+    {
+        void *Y = p->colP ? scratch(0) : out;
+        cudaError_t e = rows(in, Y, 0);
+        if (e == cudaSuccess) e = ypass(Y, out, COL_FWD);
+        if (e == cudaSuccess) e = zpass(out, out, COL_POISSON);
+        if (e == cudaSuccess) e = ypass(out, Y, COL_INV);
+        if (e == cudaSuccess) e = rows(Y, out, 1);
+        return e;
+    }
+    // nsteps exact diffusion steps; the x-spectrum of the volume lives in the
+    // scratch, the MID row pass materialises u between steps (as the 2D diffuse)
+    cudaError_t diffuse3(const void *u0, void *u, int64_t nsteps)
+    {
+        void *S0 = scratch(0), *S1 = p->colP ? scratch(1) : scratch(0);
+        cudaError_t e = rows(u0, S0, 0);
+        for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) {
+            e = ypass(S0, S1, COL_FWD);
+            if (e == cudaSuccess) e = zpass(S1, S1, COL_DIFFUSE);
+            if (e == cudaSuccess) e = ypass(S1, S0, COL_INV);
+            if (e != cudaSuccess) break;
+            e = (k + 1 < nsteps) ? rows_mid(S0, S0, u) : rows(S0, u, 1);
         }
         return e;
     }
@@ -692,6 +774,7 @@ const char *fftpde_status_string(fftpde_status s)
     case FFTPDE_ERR_WORKSPACE: return "workspace missing or too small";
     case FFTPDE_ERR_CUDA: return "CUDA error";
     case FFTPDE_ERR_NCCL: return "NCCL error";
+    case FFTPDE_ERR_NOT_POW2_Z: return "nz is not a power of two (radix-2 restriction)";
     }
     return "unknown status";
 }
@@ -824,6 +907,13 @@ fftpde_status fftpde_set_workspace(fftpde_plan plan, void *dev_ptr, size_t bytes
     if (s == FFTPDE_OK) s = upload(plan, plan->o_ky2, plan->ky2);
     if (s == FFTPDE_OK) s = upload(plan, plan->o_kx, plan->kx);
     if (s == FFTPDE_OK) s = upload(plan, plan->o_ky, plan->ky);
+    if (s == FFTPDE_OK && plan->is3d) {
+        plan->diff3_valid = false;
+        s = upload(plan, plan->o_twz, plan->twz);
+        if (s == FFTPDE_OK) s = upload(plan, plan->o_twz8, plan->twz8);
+        if (s == FFTPDE_OK) s = upload(plan, plan->o_kz2, plan->kz2);
+        if (s == FFTPDE_OK) s = upload(plan, plan->o_kxy2, plan->kxy2);
+    }
     if (s != FFTPDE_OK) plan->ws = nullptr;
     return s;
 }
@@ -956,6 +1046,7 @@ fftpde_status fftpde_wave_step_batched(fftpde_plan p, void *u, void *ut, int64_t
 fftpde_status fftpde_rows(fftpde_plan p, const void *in, void *out, int64_t nrows, int inverse)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (p->is3d) return FFTPDE_ERR_UNSUPPORTED;
     if (!p->ws) return FFTPDE_ERR_WORKSPACE;
     if (nrows == 0) return FFTPDE_ERR_EMPTY;
     if (nrows < 0) return FFTPDE_ERR_INVALID_ARG;
@@ -985,6 +1076,7 @@ fftpde_status fftpde_cols_slab(fftpde_plan p, const void *in, void *out, int64_t
                                int op, double D, double dt)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (p->is3d) return FFTPDE_ERR_UNSUPPORTED;
     if (!p->ws) return FFTPDE_ERR_WORKSPACE;
     if (ncols == 0) return FFTPDE_ERR_EMPTY;
     if (ncols < 0 || !is_pow2(ncols) || p->nx % ncols || col0 < 0 || col0 % ncols || col0 + ncols > p->nx)
@@ -1089,7 +1181,7 @@ fftpde_status fftpde_wave_rk4(fftpde_plan p, void *u, void *ut, double c, double
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
     if (!p->ws) return FFTPDE_ERR_WORKSPACE;
-    if (p->batch != 1) return FFTPDE_ERR_UNSUPPORTED;
+    if (p->batch != 1 || p->is3d) return FFTPDE_ERR_UNSUPPORTED;
     fftpde_status s = check_ptr(p, u);
     if (s == FFTPDE_OK) s = check_ptr(p, ut);
     if (s != FFTPDE_OK) return s;
@@ -1120,30 +1212,127 @@ fftpde_status fftpde_wave_rk4(fftpde_plan p, void *u, void *ut, double c, double
     });
 }
 
+// ---- 3D plans ---------------------------------------------------------------------
+fftpde_status fftpde_plan_3d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t nz, fftpde_dtype dtype, double Lx,
+                             double Ly, double Lz, int device)
+{
+    if (!plan) return FFTPDE_ERR_INVALID_ARG;
+    *plan = nullptr;
+    if (nz == 0) return FFTPDE_ERR_EMPTY;
+    if (nz < 0) return FFTPDE_ERR_INVALID_ARG;
+    if (!std::isfinite(Lz) || !(Lz > 0)) return FFTPDE_ERR_INVALID_ARG;
+    fftpde_status s = fftpde_plan_2d(plan, nx, ny, nz, dtype, Lx, Ly, device);   // batch = nz slabs
+    if (s != FFTPDE_OK) return s;
+    fftpde_plan p = *plan;
+    auto fail = [&](fftpde_status st) { fftpde_destroy(p); *plan = nullptr; return st; };
+    if (!is_pow2(nz)) return fail(FFTPDE_ERR_NOT_POW2_Z);
+    // the z-pass is single-level (nz <= 1024); its tables cover nx*ny lines
+    if (nz > 1024 || nx * ny > ((int64_t)1 << 26)) return fail(FFTPDE_ERR_UNSUPPORTED);
+    p->is3d = true;
+    p->nz = nz;
+    p->Lz = Lz;
+    build_twiddles(nz, p->twz);
+    build_twiddles(nz, p->twz8, 8);
+    build_k2(nz, Lz, p->kz2);
+    p->kxy2.resize((size_t)(nx * ny));
+    for (int64_t y = 0; y < ny; ++y)
+        for (int64_t x = 0; x < nx; ++x) p->kxy2[(size_t)(y * nx + x)] = p->kx2[(size_t)x] + p->ky2[(size_t)y];
+    const size_t er = elem_real(p), ec = elem_cplx(p);
+    size_t off = p->need;
+    auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return o; };
+    p->o_twz = take(p->twz.size() / 2 * ec);
+    p->o_twz8 = take(p->twz8.size() / 2 * ec);
+    p->o_kz2 = take((size_t)nz * er);
+    p->o_ez = take((size_t)nz * er);
+    p->o_kxy2 = take((size_t)(nx * ny) * er);
+    p->o_exy = take((size_t)(nx * ny) * er);
+    p->need = off;
+    return FFTPDE_OK;
+}
+
+} // extern "C"
+namespace {
+fftpde_status ensure_diffusion_tables3(fftpde_plan p, double D, double dt)
+{
+    if (p->diff3_valid && p->diff3_D == D && p->diff3_dt == dt) return FFTPDE_OK;
+    const double scale = 1.0 / ((double)p->nx * (double)p->ny * (double)p->nz);
+    std::vector<double> exy(p->kxy2.size()), ez((size_t)p->nz);
+    for (size_t i = 0; i < exy.size(); ++i) exy[i] = std::exp(-D * p->kxy2[i] * dt) * scale;
+    for (int64_t z = 0; z < p->nz; ++z) ez[(size_t)z] = std::exp(-D * p->kz2[(size_t)z] * dt);
+    fftpde_status s = upload(p, p->o_exy, exy);
+    if (s == FFTPDE_OK) s = upload(p, p->o_ez, ez);
+    if (s != FFTPDE_OK) return s;
+    p->diff3_valid = true;
+    p->diff3_D = D;
+    p->diff3_dt = dt;
+    return FFTPDE_OK;
+}
+
+fftpde_status check3(fftpde_plan p, const void *a, const void *b)
+{
+    if (!p->ws) return FFTPDE_ERR_WORKSPACE;
+    fftpde_status s = check_ptr(p, a);
+    return s == FFTPDE_OK ? check_ptr(p, b) : s;
+}
+
+template <typename F> fftpde_status dispatch3(fftpde_plan p, F &&f)
+{
+    return dispatch(p, p->nz, p->nx * p->ny, std::forward<F>(f));
+}
+} // namespace
+extern "C" {
+
 // ---- whole-plan entry points --------------------------------------------------
 fftpde_status fftpde_forward(fftpde_plan p, const void *in, void *out)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (p->is3d) {
+        fftpde_status s = check3(p, in, out);
+        return s != FFTPDE_OK ? s : dispatch3(p, [&](auto &ps) { return ps.forward3(in, out); });
+    }
     return fftpde_forward_batched(p, in, out, p->batch, p->nx * p->ny);
 }
 fftpde_status fftpde_inverse(fftpde_plan p, const void *in, void *out)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (p->is3d) {
+        fftpde_status s = check3(p, in, out);
+        return s != FFTPDE_OK ? s : dispatch3(p, [&](auto &ps) { return ps.inverse3(in, out); });
+    }
     return fftpde_inverse_batched(p, in, out, p->batch, p->nx * p->ny);
 }
 fftpde_status fftpde_poisson(fftpde_plan p, const void *rho, void *u)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (p->is3d) {
+        fftpde_status s = check3(p, rho, u);
+        return s != FFTPDE_OK ? s : dispatch3(p, [&](auto &ps) { return ps.poisson3(rho, u); });
+    }
     return fftpde_poisson_batched(p, rho, u, p->batch, p->nx * p->ny);
 }
 fftpde_status fftpde_diffuse(fftpde_plan p, const void *u0, void *u, double D, double dt, int64_t nsteps)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (p->is3d) {
+        fftpde_status s = check3(p, u0, u);
+        if (s != FFTPDE_OK) return s;
+        if (!std::isfinite(D) || !std::isfinite(dt) || D < 0 || dt < 0 || nsteps < 0) return FFTPDE_ERR_INVALID_ARG;
+        if (nsteps == 0) return copy_grids(p, u0, u, p->nz, p->nx * p->ny);
+        {
+            DeviceGuard g(p->device);
+            s = ensure_diffusion_tables3(p, D, dt);
+        }
+        if (s != FFTPDE_OK) return s;
+        const std::array<uint64_t, 6> key{5, (uint64_t)(uintptr_t)u0, (uint64_t)(uintptr_t)u, (uint64_t)p->nz,
+                                          (uint64_t)p->nx, (uint64_t)nsteps};
+        return run_graphed(p, key, [&] { return dispatch3(p, [&](auto &ps) { return ps.diffuse3(u0, u, nsteps); }); });
+    }
     return fftpde_diffuse_batched(p, u0, u, p->batch, p->nx * p->ny, D, dt, nsteps);
 }
 fftpde_status fftpde_wave_step(fftpde_plan p, void *u, void *ut, double c, double dt, int64_t nsteps)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (p->is3d) return FFTPDE_ERR_UNSUPPORTED;
     return fftpde_wave_step_batched(p, u, ut, p->batch, p->nx * p->ny, c, dt, nsteps);
 }
 

@@ -24,7 +24,7 @@ KERNEL_CLASSES = {0: "row_pass", 1: "col_pass", 2: "wave_col_pass", 3: "small_so
 
 # fftpde_status
 OK, ERR_INVALID_ARG, ERR_EMPTY, ERR_NOT_POW2_X, ERR_NOT_POW2_Y, ERR_UNSUPPORTED, ERR_WORKSPACE, \
-    ERR_CUDA, ERR_NCCL = range(9)
+    ERR_CUDA, ERR_NCCL, ERR_NOT_POW2_Z = range(10)
 C64, C128 = 0, 1
 
 EXPORTS = [
@@ -37,6 +37,7 @@ EXPORTS = [
     "fftpde_rows", "fftpde_cols_slab", "fftpde_pack_blocks",
     "fftpde_wave_rk4_scratch_size", "fftpde_wave_rk4",
     "fftpde_apply", "fftpde_diffuse_source_scratch_size", "fftpde_diffuse_source",
+    "fftpde_plan_3d",
 ]
 KOP = {"laplacian": 0, "dx": 1, "dy": 2}
 OP_POISSON, OP_DIFFUSE = 2, 3
@@ -87,6 +88,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fftpde_pack_blocks": (st, [p, p, p, i64, i64, i64, u]),
         "fftpde_wave_rk4_scratch_size": (ctypes.c_size_t, [p]),
         "fftpde_apply": (st, [p, p, p, u]),
+        "fftpde_plan_3d": (st, [ctypes.POINTER(p), i64, i64, i64, u, dbl, dbl, dbl, u]),
         "fftpde_diffuse_source_scratch_size": (ctypes.c_size_t, [p]),
         "fftpde_diffuse_source": (st, [p, p, p, p, dbl, dbl, i64, p, ctypes.c_size_t]),
         "fftpde_wave_rk4": (st, [p, p, p, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, i64, p, p,
@@ -360,3 +362,62 @@ class Plan:
         _check(self.lib.fftpde_pack_blocks(self._h, x.data_ptr(), out.data_ptr(), int(nrows), int(nblocks),
                                            int(bw), int(direction)), "fftpde_pack_blocks")
         return out
+
+
+class Plan3D(Plan):
+    """A 3D plan for [nz, ny, nx] volumes on [0,Lx) x [0,Ly) x [0,Lz) (the n-D
+    extension): forward / inverse / poisson / diffuse act on the
+    whole volume (fftpde_plan_3d)."""
+
+    def __init__(self, nx: int, ny: int, nz: int, dtype=torch.complex128, Lx: float = 1.0,
+                 Ly: float = 1.0, Lz: float = 1.0, device=None):
+        if dtype not in _DT:
+            raise TypeError("dtype must be torch.complex128 or torch.complex64")
+        if not torch.cuda.is_available():
+            raise RuntimeError("fftpde needs a CUDA device (no CPU fallback)")
+        self.lib = load_library()
+        self.device = torch.device(device if device is not None else "cuda")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self.nx, self.ny, self.nz, self.dtype = int(nx), int(ny), int(nz), dtype
+        self.batch = 1
+        self.Lx, self.Ly, self.Lz = float(Lx), float(Ly), float(Lz)
+        h = ctypes.c_void_p()
+        _check(self.lib.fftpde_plan_3d(ctypes.byref(h), self.nx, self.ny, self.nz, _DT[dtype], self.Lx,
+                                       self.Ly, self.Lz, self.device.index), "fftpde_plan_3d")
+        self._h = h
+        nbytes = self.lib.fftpde_workspace_size(h)
+        self.workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        self._bind_stream()
+        _check(self.lib.fftpde_set_workspace(h, self.workspace.data_ptr(), self.workspace.numel()),
+               "fftpde_set_workspace")
+
+    def _vol(self, x: torch.Tensor, name: str):
+        if x.dtype != self.dtype:
+            raise TypeError(f"{name}: dtype {x.dtype} does not match the plan's {self.dtype}")
+        if tuple(x.shape) != (self.nz, self.ny, self.nx):
+            raise ValueError(f"{name}: shape {tuple(x.shape)} does not match plan ({self.nz}, {self.ny}, {self.nx})")
+
+    def _call3(self, fn, x, out, *args):
+        self._vol(x, "x")
+        xd, host = self._to_dev(x)
+        o = self._out(xd, None if host else out)
+        self._bind_stream()
+        _check(fn(self._h, xd.data_ptr(), o.data_ptr(), *args), fn.__name__)
+        return self._finish(o, host, out if host else None)
+
+    def forward(self, x, out=None):
+        """3D DFT, + sign, unnormalised (PAPER.md:246-249 extended, :275)."""
+        return self._call3(self.lib.fftpde_forward, x, out)
+
+    def inverse(self, X, out=None):
+        """3D iDFT, conjugate kernel x 1/(nx ny nz)."""
+        return self._call3(self.lib.fftpde_inverse, X, out)
+
+    def poisson(self, rho, out=None):
+        """nabla^2 u = rho - mean(rho) in 3D (-1/|k|^2, k = 0 zeroed)."""
+        return self._call3(self.lib.fftpde_poisson, rho, out)
+
+    def diffuse(self, u0, D: float, dt: float, nsteps: int, out=None):
+        """nsteps exact 3D diffusion steps exp(-D|k|^2 dt)."""
+        return self._call3(self.lib.fftpde_diffuse, u0, out, float(D), float(dt), int(nsteps))

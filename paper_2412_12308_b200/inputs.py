@@ -41,10 +41,11 @@ class Workload:
     c: float = 0.0
     Lx: float = 1.0
     Ly: float = 1.0
+    nz: int = 1            # 3D workloads
 
     @property
     def points(self) -> int:
-        return self.nx * self.ny * self.batch
+        return self.nx * self.ny * self.nz * self.batch
 
 
 # BASELINE.json configs[0..4]
@@ -64,7 +65,10 @@ RK4_BIG = Workload("rk4_orbit_4096", "rk4", 4096, 4096, 1, "c128", nsteps=50, dt
 # SURVEY.md 8(f) row 2 (not a BASELINE config): diffusion with a static source, the C2
 # grid and Gaussians as both the initial field and the source (exact integrator per step)
 DSRC = Workload("dsrc_diffusion_1024", "dsrc", 1024, 1024, 1, "c128", nsteps=200, D=1e-3, dt=0.01)
-EXTRA_WORKLOADS = {"rk4": RK4, "rk4big": RK4_BIG, "dsrc": DSRC}
+# SURVEY.md 8(f) row 4 (not a BASELINE config): the 3D extension on 256^3
+P3D = Workload("p3d_poisson_256", "poisson", 256, 256, 1, "c128", nz=256)
+D3D = Workload("d3d_diffusion_256", "diffuse", 256, 256, 1, "c128", nsteps=20, D=1e-3, dt=0.01, nz=256)
+EXTRA_WORKLOADS = {"rk4": RK4, "rk4big": RK4_BIG, "dsrc": DSRC, "p3d": P3D, "d3d": D3D}
 
 
 def rng_for(config_index: int) -> np.random.Generator:
@@ -267,3 +271,18 @@ def white_noise(shape, seed: int, dtype=np.complex128, complex_valued: bool = Tr
     re = rng.standard_normal(shape)
     im = rng.standard_normal(shape) if complex_valued else np.zeros(shape)
     return (re + 1j * im).astype(dtype)
+
+
+def gaussians_3d(n: int = 256, m: int = 16, seed_index: int = 6) -> np.ndarray:
+    """Sum of m seeded 3D Gaussians A exp(-d^2/sigma^2) on [0,1)^3 (minimum image,
+    the C2 recipe extended to 3D), mean subtracted; [n, n, n] complex128."""
+    rng = rng_for(seed_index)
+    centres = rng.random((m, 3))
+    sigmas = rng.uniform(0.02, 0.08, m)
+    amps = rng.uniform(0.0, 1.0, m)
+    f = np.zeros((n, n, n))
+    for (cx, cy, cz), s, a in zip(centres, sigmas, amps):
+        gx, gy, gz = gaussian_1d(n, cx, s), gaussian_1d(n, cy, s), gaussian_1d(n, cz, s)
+        f += a * gz[:, None, None] * gy[None, :, None] * gx[None, None, :]
+    f -= f.mean()
+    return f.astype(np.complex128)
