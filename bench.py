@@ -58,7 +58,8 @@ def parse_args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "rk4", "rk4big", "dsrc", "p3d", "d3d"],
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "rk4", "rk4big", "dsrc", "p3d", "d3d",
+                             "c2r", "c3r", "c4r"],
                     help="c1-c5: BASELINE.json configs[0..4]; rk4/rk4big: the paper's orbiting-source "
                          "RK4 run (SURVEY.md 8(f) row 1, not a BASELINE config)")
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
@@ -75,6 +76,10 @@ def make_inputs(wl):
     """Seeded synthetic input of the workload (numpy, host) -- paper_2412_12308_b200.inputs."""
     import numpy as np
     from paper_2412_12308_b200 import inputs as I
+    if wl.dtype in ("f64", "f32"):          # real storage of the complex recipes (R12)
+        base = {"c2r": "c2", "c3r": "c3", "c4r": "c4"}[wl.name[:3]]
+        rt = np.float64 if wl.dtype == "f64" else np.float32
+        return tuple(np.ascontiguousarray(h.real).astype(rt) for h in make_inputs(I.WORKLOADS[base]))
     if wl.name.startswith("c1"):
         return (I.c1_inputs(wl.nx).rho,)
     if wl.name.startswith("c2"):
@@ -114,8 +119,8 @@ def alg_bytes_per_launch(wl, kernel_class):
     passes are MID passes (inverse rows of step s stored as the physical field
     + forward rows of step s+1: one read, two writes), the first and last are
     plain forward / inverse rows (one read, one write)."""
-    esz = 16 if wl.dtype == "c128" else 8
-    field = wl.nx * wl.ny * wl.nz * wl.batch * esz
+    esz = {"c128": 16, "c64": 8, "f64": 8, "f32": 4}[wl.dtype]
+    field = wl.nx * wl.ny * wl.nz * wl.batch * esz      # real fields: the half spectrum has ~ the same bytes
     if kernel_class == "wave_col_pass":
         return 2 * 2 * field
     if wl.op == "dsrc":
@@ -248,12 +253,15 @@ def native(args, wl, world, rank, local):
     import torch
     from paper_2412_12308_b200 import fftpde as F
 
-    dtype = torch.complex128 if wl.dtype == "c128" else torch.complex64
+    dtype = {"c128": torch.complex128, "c64": torch.complex64, "f64": torch.float64,
+             "f32": torch.float32}[wl.dtype]
     dev_in, host = make_device_inputs(wl, dtype)
     if host is None:          # C5: host copies only where needed (e2e / cpu baseline are bounded)
         args.no_e2e = True
     out = [torch.empty_like(d) for d in dev_in]
-    if wl.nz > 1:
+    if wl.dtype in ("f64", "f32"):
+        plan = F.PlanR2C(wl.nx, wl.ny, batch=wl.batch, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly)
+    elif wl.nz > 1:
         plan = F.Plan3D(wl.nx, wl.ny, wl.nz, dtype=dtype)
     else:
         plan = F.Plan(wl.nx, wl.ny, batch=wl.batch, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly)
@@ -345,6 +353,21 @@ def native(args, wl, world, rank, local):
         host_out = [torch.empty(h.shape, dtype=dtype, pin_memory=True) for h in host_in]
 
         def e2e_step():
+            if wl.dtype in ("f64", "f32"):   # real plans take device tensors: copies in the timed region
+                for d, h in zip(out, host_in):
+                    d.copy_(h, non_blocking=True)
+                if wl.op == "poisson":
+                    r = plan.poisson(out[0])
+                    host_out[0].copy_(r, non_blocking=True)
+                elif wl.op == "diffuse":
+                    r = plan.diffuse(out[0], wl.D, wl.dt, wl.nsteps)
+                    host_out[0].copy_(r, non_blocking=True)
+                else:
+                    plan.wave_step(out[0], out[1], wl.c, wl.dt, wl.nsteps)
+                    for h, d in zip(host_out, out):
+                        h.copy_(d, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                return
             if wl.op == "poisson":
                 plan.poisson(host_in[0], out=host_out[0])
             elif wl.op == "diffuse":
@@ -387,7 +410,7 @@ def native(args, wl, world, rank, local):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if wl.dtype == "c128" else "f32",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if wl.dtype in ("c128", "f64") else "f32",
         "data": "synthetic (seeded, BASELINE.json recipe; paper_2412_12308_b200/inputs.py)",
         "config": workload_config(wl, world),
         "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
@@ -469,7 +492,7 @@ def sharded_native(args, wl, world, rank, local):
 def alg_step_bytes(wl):
     """Algorithmic bytes of one bench step: each state field read + written once per
     solve step."""
-    esz = 16 if wl.dtype == "c128" else 8
+    esz = {"c128": 16, "c64": 8, "f64": 8, "f32": 4}[wl.dtype]
     fields = 2 if wl.op in ("wave", "rk4") else 1
     steps = wl.nsteps if wl.op != "poisson" else 1
     return 2 * fields * wl.points * esz * steps

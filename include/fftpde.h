@@ -71,6 +71,20 @@ typedef enum {
 fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t batch,
                              fftpde_dtype dtype, double Lx, double Ly, int device);
 
+/* Real-field plan: real [batch][ny][nx] fields (FFTPDE_C128
+ * plans take double data, FFTPDE_C64 plans float), whose spectra are Hermitian,
+ * X_{n-a} = conj(X_a), so only a <= nx/2 is stored: fftpde_forward returns the half
+ * spectrum [batch][ny][nx/2 + 1] (complex of the plan's precision, natural order,
+ * + sign, unnormalised), fftpde_inverse takes it back to real (x 1/(nx ny));
+ * fftpde_poisson, fftpde_diffuse and fftpde_wave_step act on real fields with the
+ * same operators as the complex plans, moving half the bytes.  A real row of nx
+ * values is transformed as nx/2 complex pairs and untangled with the even/odd split
+ * of eq:FFTpairodd.  16 <= nx <= 16384 (complex128) /
+ * 32 <= nx <= 16384 (complex64); ny as fftpde_plan_2d; whole-plan calls only
+ * (the *_batched calls and the other operators return FFTPDE_ERR_UNSUPPORTED). */
+fftpde_status fftpde_plan_2d_r2c(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t batch, fftpde_dtype dtype,
+                                 double Lx, double Ly, int device);
+
 /* 3D plan (the n-D extension): [nz][ny][nx] grids on
  * [0,Lx) x [0,Ly) x [0,Lz), x fastest.  Transforms are sequential 1D passes
  * along x, y and z; the whole-plan calls fftpde_forward / fftpde_inverse /

@@ -225,7 +225,7 @@ col2_kernel(Col2Args<T> g, OpTables<T> tab)
 #pragma unroll
                 for (int e = 0; e < E; ++e) w[e] = ldcg_h(g.V + r0 + e * rstep, pol);
                 fft<P, false, EMAX>(w, sm, t, g.twP, sync);
-                const int64_t qa = a <= g.nx - a ? a : g.nx - a;
+                const int64_t qa = a <= tab.nfold - a ? a : tab.nfold - a;
                 const T *pC = tab.wC + qa * tab.qpitch, *pS1 = tab.wS1 + qa * tab.qpitch,
                         *pS2 = tab.wS2 + qa * tab.qpitch;
 #pragma unroll
@@ -409,7 +409,7 @@ col2_phase_kernel(Col2Args<T> g, OpTables<T> tab, int64_t nitems)
 #pragma unroll
                 for (int e = 0; e < E; ++e) w[e] = g.V[r0 + e * rstep];
                 fft<P, false, EMAX>(w, sm, t, g.twP, sync);
-                const int64_t qa = a <= g.nx - a ? a : g.nx - a;
+                const int64_t qa = a <= tab.nfold - a ? a : tab.nfold - a;
                 const T *pC = tab.wC + qa * tab.qpitch, *pS1 = tab.wS1 + qa * tab.qpitch,
                         *pS2 = tab.wS2 + qa * tab.qpitch;
 #pragma unroll

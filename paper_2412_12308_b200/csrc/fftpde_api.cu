@@ -56,6 +56,11 @@ struct fftpde_plan_s {
     // 3D plans (fftpde_plan_3d): the 2D machinery runs with batch = nz slabs; the
     // z-pass is a column pass of length nz over the nx*ny lines of the volume
     bool is3d = false;
+    // real plans (fftpde_plan_2d_r2c): half spectrum [batch][ny][pitch], pitch = nx/2 + LPP
+    bool is_real = false;
+    int64_t pitch = 0;
+    std::vector<double> twm, twr;   // radix-16 stage table of nx/2; w_nx^a, a <= nx/2
+    size_t o_twm = 0, o_twr = 0;
     int64_t nz = 1;
     double Lz = 1.0;
     std::vector<double> twz, twz8, kz2, kxy2;
@@ -242,6 +247,7 @@ template <typename T> OpTables<T> tables(fftpde_plan p)
     t.wS1 = (const T *)(p->ws + p->o_ws1);
     t.wS2 = (const T *)(p->ws + p->o_ws2);
     t.qpitch = p->qy;
+    t.nfold = p->nx;
     t.scale = (T)(1.0 / ((double)p->nx * (double)p->ny));
     return t;
 }
@@ -257,7 +263,7 @@ fftpde_status check_ptr(fftpde_plan p, const void *ptr)
 fftpde_status check_call(fftpde_plan p, int64_t batch, int64_t stride)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
-    if (p->is3d) return FFTPDE_ERR_UNSUPPORTED;     // 3D plans: the whole-plan entry points only
+    if (p->is3d || p->is_real) return FFTPDE_ERR_UNSUPPORTED;   // 3D / real plans: whole-plan entry points only
     if (!p->ws) return FFTPDE_ERR_WORKSPACE;
     if (batch == 0) return FFTPDE_ERR_EMPTY;
     if (batch < 0 || stride < p->nx * p->ny) return FFTPDE_ERR_INVALID_ARG;
@@ -434,6 +440,87 @@ template <typename T> struct Passes {
             } else {
                 e = rows(SU, U, 1);
                 if (e == cudaSuccess) e = rows(SV, V, 1);
+            }
+        }
+        return e;
+    }
+    // ---- real plans (fftpde_plan_2d_r2c): half spectrum of pitch p->pitch -----------
+    int64_t hstride() const { return p->ny * p->pitch; }
+    void *hscr(int i) const { return p->ws + p->o_scr + (size_t)i * (size_t)(batch * hstride()) * elem_cplx(p); }
+    cudaError_t rc(const void *in, void *out, void *out2, int op)
+    {
+        return launch(p, FFTPDE_KERNEL_ROW, [&] {
+            return launch_rc_rows<T>(p->nx, in, out, out2, p->ny * batch, p->pitch, op, p->ws + p->o_twm,
+                                     p->ws + p->o_twr, p->stream);
+        });
+    }
+    cudaError_t colsr(const void *in, void *out, int op)
+    {
+        return launch(p, FFTPDE_KERNEL_COL, [&] {
+            return launch_cols<T>(p->ny, in, out, p->pitch, hstride(), batch, op, ctw(), tables<T>(p), p->stream);
+        });
+    }
+    cudaError_t wave_colsr(void *U, void *V)
+    {
+        return launch(p, FFTPDE_KERNEL_WAVE_COL, [&] {
+            return launch_wave_cols<T>(p->ny, U, V, p->pitch, hstride(), batch, ctw(), tables<T>(p), p->stream);
+        });
+    }
+    cudaError_t copy_half(const void *src, size_t spitch, void *dst, size_t dpitch)
+    {
+        const size_t ec = elem_cplx(p);
+        return cudaMemcpy2DAsync(dst, dpitch * ec, src, spitch * ec, (size_t)(p->nx / 2 + 1) * ec,
+                                 (size_t)(p->ny * batch), cudaMemcpyDeviceToDevice, p->stream);
+    }
+    // real -> compact half spectrum [batch][ny][nx/2 + 1]
+    cudaError_t forward_real(const void *in, void *out)
+    {
+        void *S = hscr(0), *Tm = p->colP ? hscr(1) : hscr(0);      // two-level FWD is out of place
+        cudaError_t e = rc(in, S, nullptr, RC_FWD);
+        if (e == cudaSuccess) e = colsr(S, Tm, COL_FWD);
+        if (e == cudaSuccess) e = copy_half(Tm, p->pitch, out, p->nx / 2 + 1);
+        return e;
+    }
+    cudaError_t inverse_real(const void *in, void *out)
+    {
+        void *S = hscr(0), *Tm = p->colP ? hscr(1) : hscr(0);
+        cudaError_t e = copy_half(in, p->nx / 2 + 1, S, p->pitch);
+        if (e == cudaSuccess) e = colsr(S, Tm, COL_INV);
+        if (e == cudaSuccess) e = rc(Tm, out, nullptr, RC_INV);
+        return e;
+    }
+    cudaError_t poisson_real(const void *in, void *out)
+    {
+        void *S = hscr(0);
+        cudaError_t e = rc(in, S, nullptr, RC_FWD);
+        if (e == cudaSuccess) e = colsr(S, S, COL_POISSON);
+        if (e == cudaSuccess) e = rc(S, out, nullptr, RC_INV);
+        return e;
+    }
+    cudaError_t diffuse_real(const void *u0, void *u, int64_t nsteps)
+    {
+        void *S = hscr(0);
+        cudaError_t e = rc(u0, S, nullptr, RC_FWD);
+        for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) {
+            e = colsr(S, S, COL_DIFFUSE);
+            if (e == cudaSuccess) e = (k + 1 < nsteps) ? rc(S, S, u, RC_MID) : rc(S, u, nullptr, RC_INV);
+        }
+        return e;
+    }
+    cudaError_t wave_real(void *U, void *V, int64_t nsteps)
+    {
+        void *SU = hscr(0), *SV = hscr(1);
+        cudaError_t e = rc(U, SU, nullptr, RC_FWD);
+        if (e == cudaSuccess) e = rc(V, SV, nullptr, RC_FWD);
+        for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) {
+            e = wave_colsr(SU, SV);
+            if (e != cudaSuccess) break;
+            if (k + 1 < nsteps) {
+                e = rc(SU, SU, U, RC_MID);
+                if (e == cudaSuccess) e = rc(SV, SV, V, RC_MID);
+            } else {
+                e = rc(SU, U, nullptr, RC_INV);
+                if (e == cudaSuccess) e = rc(SV, V, nullptr, RC_INV);
             }
         }
         return e;
@@ -907,6 +994,10 @@ fftpde_status fftpde_set_workspace(fftpde_plan plan, void *dev_ptr, size_t bytes
     if (s == FFTPDE_OK) s = upload(plan, plan->o_ky2, plan->ky2);
     if (s == FFTPDE_OK) s = upload(plan, plan->o_kx, plan->kx);
     if (s == FFTPDE_OK) s = upload(plan, plan->o_ky, plan->ky);
+    if (s == FFTPDE_OK && plan->is_real) {
+        s = upload(plan, plan->o_twm, plan->twm);
+        if (s == FFTPDE_OK) s = upload(plan, plan->o_twr, plan->twr);
+    }
     if (s == FFTPDE_OK && plan->is3d) {
         plan->diff3_valid = false;
         s = upload(plan, plan->o_twz, plan->twz);
@@ -1076,7 +1167,7 @@ fftpde_status fftpde_cols_slab(fftpde_plan p, const void *in, void *out, int64_t
                                int op, double D, double dt)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
-    if (p->is3d) return FFTPDE_ERR_UNSUPPORTED;
+    if (p->is3d || p->is_real) return FFTPDE_ERR_UNSUPPORTED;
     if (!p->ws) return FFTPDE_ERR_WORKSPACE;
     if (ncols == 0) return FFTPDE_ERR_EMPTY;
     if (ncols < 0 || !is_pow2(ncols) || p->nx % ncols || col0 < 0 || col0 % ncols || col0 + ncols > p->nx)
@@ -1181,7 +1272,7 @@ fftpde_status fftpde_wave_rk4(fftpde_plan p, void *u, void *ut, double c, double
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
     if (!p->ws) return FFTPDE_ERR_WORKSPACE;
-    if (p->batch != 1 || p->is3d) return FFTPDE_ERR_UNSUPPORTED;
+    if (p->batch != 1 || p->is3d || p->is_real) return FFTPDE_ERR_UNSUPPORTED;
     fftpde_status s = check_ptr(p, u);
     if (s == FFTPDE_OK) s = check_ptr(p, ut);
     if (s != FFTPDE_OK) return s;
@@ -1210,6 +1301,40 @@ fftpde_status fftpde_wave_rk4(fftpde_plan p, void *u, void *ut, double c, double
             return ps.wave_rk4(u, ut, c, base, A, Omega, gamma, rs, t0, dt, nsteps, means, scratch);
         });
     });
+}
+
+// ---- real plans -------------------------------------------------------------------
+fftpde_status fftpde_plan_2d_r2c(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t batch, fftpde_dtype dtype,
+                                 double Lx, double Ly, int device)
+{
+    if (!plan) return FFTPDE_ERR_INVALID_ARG;
+    *plan = nullptr;
+    fftpde_status s = fftpde_plan_2d(plan, nx, ny, batch, dtype, Lx, Ly, device);
+    if (s != FFTPDE_OK) return s;
+    fftpde_plan p = *plan;
+    const int64_t lpp = 128 / (int64_t)elem_cplx(p);                 // columns per 128-byte segment
+    if (nx < 2 * lpp || nx / 2 > kMaxLen) {                           // row pass: nx/2 <= 8192 points
+        fftpde_destroy(p);
+        *plan = nullptr;
+        return FFTPDE_ERR_UNSUPPORTED;
+    }
+    p->is_real = true;
+    p->pitch = nx / 2 + lpp;            // multiple of the 128-byte column block, <= nx
+    build_twiddles(nx / 2, p->twm);
+    p->twr.clear();
+    for (int64_t a = 0; a <= nx / 2; ++a) {
+        double re, im;
+        unit_root(nx, a, re, im);
+        p->twr.push_back(re);
+        p->twr.push_back(im);
+    }
+    const size_t ec = elem_cplx(p);
+    size_t off = p->need;
+    auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return o; };
+    p->o_twm = take(p->twm.size() / 2 * ec);
+    p->o_twr = take(p->twr.size() / 2 * ec);
+    p->need = off;
+    return FFTPDE_OK;
 }
 
 // ---- 3D plans ---------------------------------------------------------------------
@@ -1283,9 +1408,21 @@ template <typename F> fftpde_status dispatch3(fftpde_plan p, F &&f)
 extern "C" {
 
 // ---- whole-plan entry points --------------------------------------------------
+} // extern "C"
+namespace {
+template <typename F> fftpde_status dispatch_real(fftpde_plan p, F &&f)
+{
+    return dispatch(p, p->batch, p->nx * p->ny, std::forward<F>(f));
+}
+} // namespace
+extern "C" {
 fftpde_status fftpde_forward(fftpde_plan p, const void *in, void *out)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (p->is_real) {
+        fftpde_status s = check3(p, in, out);
+        return s != FFTPDE_OK ? s : dispatch_real(p, [&](auto &ps) { return ps.forward_real(in, out); });
+    }
     if (p->is3d) {
         fftpde_status s = check3(p, in, out);
         return s != FFTPDE_OK ? s : dispatch3(p, [&](auto &ps) { return ps.forward3(in, out); });
@@ -1295,6 +1432,10 @@ fftpde_status fftpde_forward(fftpde_plan p, const void *in, void *out)
 fftpde_status fftpde_inverse(fftpde_plan p, const void *in, void *out)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (p->is_real) {
+        fftpde_status s = check3(p, in, out);
+        return s != FFTPDE_OK ? s : dispatch_real(p, [&](auto &ps) { return ps.inverse_real(in, out); });
+    }
     if (p->is3d) {
         fftpde_status s = check3(p, in, out);
         return s != FFTPDE_OK ? s : dispatch3(p, [&](auto &ps) { return ps.inverse3(in, out); });
@@ -1304,6 +1445,10 @@ fftpde_status fftpde_inverse(fftpde_plan p, const void *in, void *out)
 fftpde_status fftpde_poisson(fftpde_plan p, const void *rho, void *u)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (p->is_real) {
+        fftpde_status s = check3(p, rho, u);
+        return s != FFTPDE_OK ? s : dispatch_real(p, [&](auto &ps) { return ps.poisson_real(rho, u); });
+    }
     if (p->is3d) {
         fftpde_status s = check3(p, rho, u);
         return s != FFTPDE_OK ? s : dispatch3(p, [&](auto &ps) { return ps.poisson3(rho, u); });
@@ -1313,6 +1458,25 @@ fftpde_status fftpde_poisson(fftpde_plan p, const void *rho, void *u)
 fftpde_status fftpde_diffuse(fftpde_plan p, const void *u0, void *u, double D, double dt, int64_t nsteps)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (p->is_real) {
+        fftpde_status s = check3(p, u0, u);
+        if (s != FFTPDE_OK) return s;
+        if (!std::isfinite(D) || !std::isfinite(dt) || D < 0 || dt < 0 || nsteps < 0) return FFTPDE_ERR_INVALID_ARG;
+        if (nsteps == 0) {
+            if (u0 == u) return FFTPDE_OK;
+            DeviceGuard g(p->device);
+            return cuda_status(cudaMemcpyAsync(u, u0, (size_t)(p->batch * p->nx * p->ny) * elem_real(p),
+                                               cudaMemcpyDeviceToDevice, p->stream));
+        }
+        {
+            DeviceGuard g(p->device);
+            s = ensure_diffusion_tables(p, D, dt);
+        }
+        if (s != FFTPDE_OK) return s;
+        const std::array<uint64_t, 6> key{6, (uint64_t)(uintptr_t)u0, (uint64_t)(uintptr_t)u, (uint64_t)p->batch,
+                                          (uint64_t)p->nx, (uint64_t)nsteps};
+        return run_graphed(p, key, [&] { return dispatch_real(p, [&](auto &ps) { return ps.diffuse_real(u0, u, nsteps); }); });
+    }
     if (p->is3d) {
         fftpde_status s = check3(p, u0, u);
         if (s != FFTPDE_OK) return s;
@@ -1333,6 +1497,20 @@ fftpde_status fftpde_wave_step(fftpde_plan p, void *u, void *ut, double c, doubl
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
     if (p->is3d) return FFTPDE_ERR_UNSUPPORTED;
+    if (p->is_real) {
+        fftpde_status s = check3(p, u, ut);
+        if (s != FFTPDE_OK) return s;
+        if (u == ut || !std::isfinite(c) || !std::isfinite(dt) || c < 0 || nsteps < 0) return FFTPDE_ERR_INVALID_ARG;
+        if (nsteps == 0) return FFTPDE_OK;
+        {
+            DeviceGuard g(p->device);
+            s = ensure_wave_tables(p, c, dt);
+        }
+        if (s != FFTPDE_OK) return s;
+        const std::array<uint64_t, 6> key{7, (uint64_t)(uintptr_t)u, (uint64_t)(uintptr_t)ut, (uint64_t)p->batch,
+                                          (uint64_t)p->nx, (uint64_t)nsteps};
+        return run_graphed(p, key, [&] { return dispatch_real(p, [&](auto &ps) { return ps.wave_real(u, ut, nsteps); }); });
+    }
     return fftpde_wave_step_batched(p, u, ut, p->batch, p->nx * p->ny, c, dt, nsteps);
 }
 

@@ -70,7 +70,7 @@ col_wave_kernel(typename cplx_t<T>::type *U, typename cplx_t<T>::type *V,
     fft<N, false>(v, sm, t, tw, SyncCTA{});
     asm volatile("" ::: "memory");   // keep the table loads below the transform (register pressure)
     // quadrant index: qa = |fold(a)|, qb = |fold(b)|
-    const int64_t qa = active ? (a <= nx - a ? a : nx - a) : 0;
+    const int64_t qa = active ? (a <= tab.nfold - a ? a : tab.nfold - a) : 0;
     const T *pC = tab.wC + qa * tab.qpitch;
     const T *pS1 = tab.wS1 + qa * tab.qpitch;
     const T *pS2 = tab.wS2 + qa * tab.qpitch;

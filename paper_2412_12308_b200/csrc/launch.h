@@ -14,6 +14,8 @@ template <typename T> struct OpTables {
     const T *ex, *ey;        // exp(-D kx^2 dt)/(nx ny), exp(-D ky^2 dt)    (diffusion)
     const T *wC, *wS1, *wS2; // wave quadrant tables [qa][qb], scale folded in
     int64_t qpitch;          // ny/2 + 1
+    int64_t nfold;           // x length for the quadrant index qa = min(a, nfold - a) (nx; real plans
+                             // run the column passes over a padded half spectrum, so not the column count)
     T scale;                 // 1/(nx ny)
 };
 
@@ -91,6 +93,12 @@ cudaError_t launch_rk4(void *U, void *V, const void *S0, const void *Sh, const v
                        const void *kx2, const void *ky2, double c, double dt, void *mean_out, cudaStream_t st);
 template <typename T>
 cudaError_t launch_mean(const void *U, void *out, int64_t nx, int64_t ny, cudaStream_t st);
+
+// ---- real-to-complex row passes (rc.cu) ----
+enum RcOp { RC_FWD = 0, RC_INV = 1, RC_MID = 2 };
+template <typename T>
+cudaError_t launch_rc_rows(int64_t nx, const void *in, void *out, void *out2, int64_t nrows, int64_t pitch, int op,
+                           const void *tw, const void *twr, cudaStream_t st);
 
 // ---- diagonal k-space operators (kspace.cu) ----
 enum KOp { KOP_LAPLACIAN = 0, KOP_DX = 1, KOP_DY = 2, KOP_DIFFSRC = 3 };

@@ -170,7 +170,7 @@ wave_line_kernel(typename cplx_t<T>::type *U, typename cplx_t<T>::type *V, LineA
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = active ? V[base + e * estep] : C{0, 0};
     fft_tw<N, false, E>(v, sm, t, twp, sync);
-    const int64_t qa = active ? (col <= a.nlines - col ? col : a.nlines - col) : 0;
+    const int64_t qa = active ? (col <= tab.nfold - col ? col : tab.nfold - col) : 0;
     const T *pC = tab.wC + qa * tab.qpitch, *pS1 = tab.wS1 + qa * tab.qpitch, *pS2 = tab.wS2 + qa * tab.qpitch;
 #pragma unroll
     for (int e = 0; e < E; ++e) {

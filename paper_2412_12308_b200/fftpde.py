@@ -37,7 +37,7 @@ EXPORTS = [
     "fftpde_rows", "fftpde_cols_slab", "fftpde_pack_blocks",
     "fftpde_wave_rk4_scratch_size", "fftpde_wave_rk4",
     "fftpde_apply", "fftpde_diffuse_source_scratch_size", "fftpde_diffuse_source",
-    "fftpde_plan_3d",
+    "fftpde_plan_3d", "fftpde_plan_2d_r2c",
 ]
 KOP = {"laplacian": 0, "dx": 1, "dy": 2}
 OP_POISSON, OP_DIFFUSE = 2, 3
@@ -89,6 +89,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fftpde_wave_rk4_scratch_size": (ctypes.c_size_t, [p]),
         "fftpde_apply": (st, [p, p, p, u]),
         "fftpde_plan_3d": (st, [ctypes.POINTER(p), i64, i64, i64, u, dbl, dbl, dbl, u]),
+        "fftpde_plan_2d_r2c": (st, [ctypes.POINTER(p), i64, i64, i64, u, dbl, dbl, u]),
         "fftpde_diffuse_source_scratch_size": (ctypes.c_size_t, [p]),
         "fftpde_diffuse_source": (st, [p, p, p, p, dbl, dbl, i64, p, ctypes.c_size_t]),
         "fftpde_wave_rk4": (st, [p, p, p, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, i64, p, p,
@@ -421,3 +422,76 @@ class Plan3D(Plan):
     def diffuse(self, u0, D: float, dt: float, nsteps: int, out=None):
         """nsteps exact 3D diffusion steps exp(-D|k|^2 dt)."""
         return self._call3(self.lib.fftpde_diffuse, u0, out, float(D), float(dt), int(nsteps))
+
+
+_REAL = {torch.float64: (C128, torch.complex128), torch.float32: (C64, torch.complex64)}
+
+
+class PlanR2C(Plan):
+    """A plan for REAL fields [ny, nx] / [B, ny, nx]: Hermitian
+    spectra are stored as half spectra [.., ny, nx/2 + 1]; the solves take and return
+    real tensors and move half the bytes of the complex path (fftpde_plan_2d_r2c)."""
+
+    def __init__(self, nx: int, ny: int, batch: int = 1, dtype=torch.float64, Lx: float = 1.0,
+                 Ly: float = 1.0, device=None):
+        if dtype not in _REAL:
+            raise TypeError("dtype must be torch.float64 or torch.float32")
+        if not torch.cuda.is_available():
+            raise RuntimeError("fftpde needs a CUDA device (no CPU fallback)")
+        self.lib = load_library()
+        self.device = torch.device(device if device is not None else "cuda")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self.nx, self.ny, self.batch = int(nx), int(ny), int(batch)
+        self.real_dtype, (code, self.dtype) = dtype, _REAL[dtype]
+        self.Lx, self.Ly = float(Lx), float(Ly)
+        h = ctypes.c_void_p()
+        _check(self.lib.fftpde_plan_2d_r2c(ctypes.byref(h), self.nx, self.ny, self.batch, code, self.Lx, self.Ly,
+                                           self.device.index), "fftpde_plan_2d_r2c")
+        self._h = h
+        nbytes = self.lib.fftpde_workspace_size(h)
+        self.workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        self._bind_stream()
+        _check(self.lib.fftpde_set_workspace(h, self.workspace.data_ptr(), self.workspace.numel()),
+               "fftpde_set_workspace")
+
+    def _shape(self, last):
+        return ((self.batch,) if self.batch > 1 else ()) + (self.ny, last)
+
+    def _chk(self, x, dtype, last, name):
+        if x.dtype != dtype or tuple(x.shape) != self._shape(last):
+            raise ValueError(f"{name}: expected {dtype} {self._shape(last)}, got {x.dtype} {tuple(x.shape)}")
+        if x.device != self.device or not x.is_contiguous():
+            raise ValueError(f"{name}: expected a contiguous tensor on {self.device}")
+
+    def _call(self, fn, x, xdt, xl, odt, ol, out, *args):
+        self._chk(x, xdt, xl, "input")
+        o = torch.empty(self._shape(ol), dtype=odt, device=self.device) if out is None else out
+        self._chk(o, odt, ol, "out")
+        self._bind_stream()
+        _check(fn(self._h, x.data_ptr(), o.data_ptr(), *args), fn.__name__)
+        return o
+
+    def forward(self, x, out=None):
+        """Half spectrum X[.., b, a], a <= nx/2, of a real field (+ sign, unnormalised)."""
+        return self._call(self.lib.fftpde_forward, x, self.real_dtype, self.nx, self.dtype, self.nx // 2 + 1, out)
+
+    def inverse(self, X, out=None):
+        """Real field from its half spectrum (x 1/(nx ny))."""
+        return self._call(self.lib.fftpde_inverse, X, self.dtype, self.nx // 2 + 1, self.real_dtype, self.nx, out)
+
+    def poisson(self, rho, out=None):
+        return self._call(self.lib.fftpde_poisson, rho, self.real_dtype, self.nx, self.real_dtype, self.nx, out)
+
+    def diffuse(self, u0, D: float, dt: float, nsteps: int, out=None):
+        return self._call(self.lib.fftpde_diffuse, u0, self.real_dtype, self.nx, self.real_dtype, self.nx, out,
+                          float(D), float(dt), int(nsteps))
+
+    def wave_step(self, u, ut, c: float, dt: float, nsteps: int):
+        """In place on the real fields (u, ut)."""
+        self._chk(u, self.real_dtype, self.nx, "u")
+        self._chk(ut, self.real_dtype, self.nx, "ut")
+        self._bind_stream()
+        _check(self.lib.fftpde_wave_step(self._h, u.data_ptr(), ut.data_ptr(), float(c), float(dt), int(nsteps)),
+               "fftpde_wave_step")
+        return u, ut

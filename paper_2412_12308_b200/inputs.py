@@ -68,7 +68,13 @@ DSRC = Workload("dsrc_diffusion_1024", "dsrc", 1024, 1024, 1, "c128", nsteps=200
 # SURVEY.md 8(f) row 4 (not a BASELINE config): the 3D extension on 256^3
 P3D = Workload("p3d_poisson_256", "poisson", 256, 256, 1, "c128", nz=256)
 D3D = Workload("d3d_diffusion_256", "diffuse", 256, 256, 1, "c128", nsteps=20, D=1e-3, dt=0.01, nz=256)
-EXTRA_WORKLOADS = {"rk4": RK4, "rk4big": RK4_BIG, "dsrc": DSRC, "p3d": P3D, "d3d": D3D}
+# SURVEY.md 8(f) row 3 (not BASELINE configs): the C2 / C3 / C4 recipes on REAL storage
+# (their data are real, R12), through the half-spectrum path
+C2R = dataclasses.replace(C2, name="c2r_diffusion_1024_real", dtype="f64")
+C3R = dataclasses.replace(C3, name="c3r_wave_4096_real", dtype="f64")
+C4R = dataclasses.replace(C4, name="c4r_batched_poisson_256x512_real", dtype="f32")
+EXTRA_WORKLOADS = {"rk4": RK4, "rk4big": RK4_BIG, "dsrc": DSRC, "p3d": P3D, "d3d": D3D,
+                   "c2r": C2R, "c3r": C3R, "c4r": C4R}
 
 
 def rng_for(config_index: int) -> np.random.Generator:
