@@ -67,6 +67,9 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="c5: use the slab-decomposed path even on one GPU (P = 1 process group)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="sharded c5: pack + NCCL all-to-all, or direct peer stores into torch "
+                         "symmetric memory (fftpde_peer_transpose, SURVEY.md 8(e) N10)")
     return ap.parse_args()
 
 
@@ -433,7 +436,10 @@ def sharded_native(args, wl, world, rank, local):
     del full
     torch.cuda.empty_cache()
     ops = S.CudaLocalOps(wl.nx, wl.ny, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly)
-    solver = S.SlabSolver(wl.nx, wl.ny, S.DistComm(), ops)
+    if args.exchange == "peer":
+        solver = S.PeerSlabSolver(wl.nx, wl.ny, S.SymmetricPeerComm(), ops)
+    else:
+        solver = S.SlabSolver(wl.nx, wl.ny, S.DistComm(), ops)
     out = [torch.empty_like(slab)]
     for _ in range(args.warmup):
         solver.diffuse([slab], wl.D, wl.dt, wl.nsteps, outs=out)
@@ -478,7 +484,9 @@ def sharded_native(args, wl, world, rank, local):
         "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded C5 recipe, built on device)",
-        "config": {**workload_config(wl, world), "parallelism": f"slab x{world} (NCCL all-to-all)",
+        "config": {**workload_config(wl, world),
+                   "parallelism": f"slab x{world} " + ("(peer-store exchange, symmetric memory)" if args.exchange == "peer"
+                                                       else "(NCCL all-to-all)"),
                    "l2": "field (16 GiB) larger than L2"},
         "e2e": None, "cpu_baseline": None, "clocks": clk.summary(),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

@@ -243,6 +243,24 @@ fftpde_status fftpde_wave_rk4(fftpde_plan plan, void *u, void *ut, double c,
  * fftpde_pack_blocks: direction 0: [nrows][nblocks][bw] -> [nblocks][nrows][bw]
  *   (row slab -> per-peer send blocks); direction 1: the inverse.  bw in
  *   elements, bw * element size a multiple of 16 bytes. */
+/* fftpde_peer_transpose: the exchange step itself as direct stores into the
+ *   other ranks' buffers over NVLink (the fused alternative to
+ *   fftpde_pack_blocks + an all-to-all): one kernel per rank, local coalesced
+ *   reads, contiguous bw-element runs written to peer memory.
+ *   direction 0: src = this rank's row-slab spectrum [R][P bw] (P bw = nx);
+ *     columns [q bw, (q+1) bw) of row k go to peers[q] at row rank R + k of its
+ *     column slab [P R][bw] (P R = ny).
+ *   direction 1: src = this rank's column slab [P R][bw]; rows [s R, (s+1) R)
+ *     go to peers[s]'s row slab [R][P bw] at columns [rank bw, (rank+1) bw).
+ *   peers: host array of npeers (= P, <= 16) device pointers the calling device
+ *   can store to (torch symmetric memory, CUDA IPC, or one device's buffers in a
+ *   single-process emulation); rank < npeers; bw * element size a multiple of 16
+ *   bytes.  Asynchronous on the plan's stream; the caller orders the phases across
+ *   ranks with a stream-ordered barrier (every rank's stores complete before any
+ *   rank reads its slab). */
+fftpde_status fftpde_peer_transpose(fftpde_plan plan, const void *src, void *const *peers, int npeers, int rank,
+                                    int64_t R, int64_t bw, int direction);
+
 #define FFTPDE_OP_POISSON 2
 #define FFTPDE_OP_DIFFUSE 3
 fftpde_status fftpde_rows(fftpde_plan plan, const void *in, void *out, int64_t nrows, int inverse);

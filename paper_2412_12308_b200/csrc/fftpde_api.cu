@@ -1303,6 +1303,25 @@ fftpde_status fftpde_wave_rk4(fftpde_plan p, void *u, void *ut, double c, double
     });
 }
 
+fftpde_status fftpde_peer_transpose(fftpde_plan p, const void *src, void *const *peers, int npeers, int rank,
+                                    int64_t R, int64_t bw, int direction)
+{
+    if (!p || !src || !peers || npeers < 1 || npeers > kMaxPeers || rank < 0 || rank >= npeers || R < 0 || bw <= 0 ||
+        (direction != 0 && direction != 1))
+        return FFTPDE_ERR_INVALID_ARG;
+    const int64_t bytes = bw * (int64_t)elem_cplx(p);
+    if (bytes % 16 || ((uintptr_t)src & 15u)) return FFTPDE_ERR_INVALID_ARG;
+    PeerPtrs pp{};
+    for (int q = 0; q < npeers; ++q) {
+        if (!peers[q] || ((uintptr_t)peers[q] & 15u)) return FFTPDE_ERR_INVALID_ARG;
+        pp.p[q] = peers[q];
+    }
+    DeviceGuard g(p->device);
+    if (!g.ok) return FFTPDE_ERR_CUDA;
+    ++p->launches;
+    return cuda_status(launch_peer_transpose(src, pp, npeers, rank, R, bytes, direction, p->stream));
+}
+
 // ---- real plans -------------------------------------------------------------------
 fftpde_status fftpde_plan_2d_r2c(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t batch, fftpde_dtype dtype,
                                  double Lx, double Ly, int device)

@@ -107,6 +107,14 @@ cudaError_t launch_kop(void *X, const void *S, int64_t nx, int64_t ny, int64_t b
                        const void *kx, const void *ky, const void *kx2, const void *ky2, double D, double dt,
                        cudaStream_t st);
 
+// Peer pointers of the slab exchange (pack.cu), passed by value.
+constexpr int kMaxPeers = 16;
+struct PeerPtrs {
+    void *p[kMaxPeers];
+};
+cudaError_t launch_peer_transpose(const void *src, const PeerPtrs &peers, int P, int rank, int64_t R,
+                                  int64_t bw_bytes, int direction, cudaStream_t st);
+
 // Block transpose of the sharded path (pack.cu); bw_bytes a multiple of 16.
 cudaError_t launch_pack(const void *in, void *out, int64_t nrows, int64_t nblocks, int64_t bw_bytes,
                         int direction, cudaStream_t st);

@@ -42,4 +42,46 @@ cudaError_t launch_pack(const void *in, void *out, int64_t nrows, int64_t nblock
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Slab exchange as direct stores into the peers' buffers:
+// the transpose of the slab decomposition done by one kernel per rank with
+// NVLink peer stores (P2P-mapped pointers), instead of a pack pass plus an
+// all-to-all.  Reads are local and coalesced; every destination run is a
+// contiguous bw-element segment of a peer's buffer.
+//   direction 0: src = this rank's row slab [R][P*bw]; element (k, q*bw + c)
+//                -> peers[q][(rank*R + k)*bw + c]        (the peer's column slab [P*R][bw])
+//   direction 1: src = this rank's column slab [P*R][bw]; element (s*R + k, c)
+//                -> peers[s][k*(P*bw) + rank*bw + c]      (the peer's row slab [R][P*bw])
+__global__ void peer_transpose_kernel(const int4 *__restrict__ src, PeerPtrs peers, int P, int rank, int64_t R,
+                                      int64_t bwv, int direction)
+{
+    const int64_t total = R * P * bwv;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = i % bwv;           // 16-byte vector within a bw segment
+        const int64_t seg = i / bwv;         // segment index in src order
+        int4 *dst;
+        if (direction == 0) {                // src [R][P][bwv]: seg = k*P + q
+            const int64_t k = seg / P, q = seg - k * P;
+            dst = (int4 *)peers.p[q] + ((int64_t)rank * R + k) * bwv + v;
+        } else {                             // src [P][R][bwv]: seg = s*R + k
+            const int64_t s = seg / R, k = seg - s * R;
+            dst = (int4 *)peers.p[s] + (k * P + rank) * bwv + v;
+        }
+        *dst = src[i];
+    }
+}
+
+cudaError_t launch_peer_transpose(const void *src, const PeerPtrs &peers, int P, int rank, int64_t R,
+                                  int64_t bw_bytes, int direction, cudaStream_t st)
+{
+    const int64_t bwv = bw_bytes / 16;
+    const int64_t total = R * P * bwv;
+    if (total == 0) return cudaSuccess;
+    int64_t grid = (total + 255) / 256;
+    if (grid > 148 * 16) grid = 148 * 16;
+    peer_transpose_kernel<<<(unsigned)grid, 256, 0, st>>>((const int4 *)src, peers, P, rank, R, bwv, direction);
+    return cudaGetLastError();
+}
+
 } // namespace fftpde

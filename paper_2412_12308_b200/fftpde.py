@@ -37,7 +37,7 @@ EXPORTS = [
     "fftpde_rows", "fftpde_cols_slab", "fftpde_pack_blocks",
     "fftpde_wave_rk4_scratch_size", "fftpde_wave_rk4",
     "fftpde_apply", "fftpde_diffuse_source_scratch_size", "fftpde_diffuse_source",
-    "fftpde_plan_3d", "fftpde_plan_2d_r2c",
+    "fftpde_plan_3d", "fftpde_plan_2d_r2c", "fftpde_peer_transpose",
 ]
 KOP = {"laplacian": 0, "dx": 1, "dy": 2}
 OP_POISSON, OP_DIFFUSE = 2, 3
@@ -90,6 +90,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fftpde_apply": (st, [p, p, p, u]),
         "fftpde_plan_3d": (st, [ctypes.POINTER(p), i64, i64, i64, u, dbl, dbl, dbl, u]),
         "fftpde_plan_2d_r2c": (st, [ctypes.POINTER(p), i64, i64, i64, u, dbl, dbl, u]),
+        "fftpde_peer_transpose": (st, [p, p, ctypes.POINTER(p), u, u, i64, i64, u]),
         "fftpde_diffuse_source_scratch_size": (ctypes.c_size_t, [p]),
         "fftpde_diffuse_source": (st, [p, p, p, p, dbl, dbl, i64, p, ctypes.c_size_t]),
         "fftpde_wave_rk4": (st, [p, p, p, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, i64, p, p,
@@ -355,6 +356,14 @@ class Plan:
         _check(self.lib.fftpde_cols_slab(self._h, x.data_ptr(), out.data_ptr(), int(col0), x.shape[1],
                                          int(op), float(D), float(dt)), "fftpde_cols_slab")
         return out
+
+    def peer_transpose(self, src: torch.Tensor, peers, rank: int, R: int, bw: int, direction: int):
+        """Slab exchange by direct stores into the peers' buffers (fftpde_peer_transpose);
+        peers: device pointers (ints) of every rank's destination buffer."""
+        arr = (ctypes.c_void_p * len(peers))(*[int(x) for x in peers])
+        self._bind_stream()
+        _check(self.lib.fftpde_peer_transpose(self._h, src.data_ptr(), arr, len(peers), int(rank), int(R), int(bw),
+                                              int(direction)), "fftpde_peer_transpose")
 
     def pack_blocks(self, x: torch.Tensor, out: torch.Tensor, nrows: int, nblocks: int, bw: int,
                     direction: int):

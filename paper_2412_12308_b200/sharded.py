@@ -47,6 +47,9 @@ class CudaLocalOps:
     def pack(self, x, out, nrows, nblocks, bw, direction):
         return self.plan.pack_blocks(x, out, nrows, nblocks, bw, direction)
 
+    def peer_transpose(self, src, peers, rank, R, bw, direction):
+        return self.plan.peer_transpose(src, peers, rank, R, bw, direction)
+
     @property
     def launches(self):
         return self.plan.launches
@@ -136,6 +139,90 @@ class SlabSolver:
         outs = outs if outs is not None else [torch.empty_like(s) for s in slabs]
         self._step(slabs, outs, F.OP_POISSON, 0.0, 0.0)
         return outs
+
+
+class LoopbackPeerComm:
+    """P virtual ranks in one process for the peer-store exchange: every rank's
+    buffers live on this device, so a "peer store" is a store into another
+    virtual rank's buffer; the phases are ordered by the single stream."""
+
+    def __init__(self, world):
+        self.world = world
+
+    def local_ranks(self):
+        return list(range(self.world))
+
+    def alloc(self, shape, dtype, device):
+        bufs = [torch.empty(shape, dtype=dtype, device=device) for _ in range(self.world)]
+        return bufs, [b.data_ptr() for b in bufs]
+
+    def barrier(self):
+        pass
+
+
+class SymmetricPeerComm:
+    """One rank per GPU: buffers from torch symmetric memory (peer-mapped over
+    NVLink), barrier = the symmetric-memory stream-ordered device barrier."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.dist, self.symm = dist, symm
+        self.group = group if group is not None else dist.group.WORLD
+        self.rank = dist.get_rank(self.group)
+        self.world = dist.get_world_size(self.group)
+        self._handles = []
+
+    def local_ranks(self):
+        return [self.rank]
+
+    def alloc(self, shape, dtype, device):
+        t = self.symm.empty(*shape, dtype=dtype, device=device)
+        h = self.symm.rendezvous(t, self.group)
+        self._handles.append(h)
+        return [t], list(h.buffer_ptrs)
+
+    def barrier(self):
+        self._handles[0].barrier(channel=0)
+
+
+class PeerSlabSolver:
+    """The slab decomposition with the exchange done by peer stores
+    (fftpde_peer_transpose) instead of pack + all-to-all: per step
+        rows forward            row slab -> A (local)
+        peer transpose 0        A -> every rank's column slab Cs     | barrier
+        column pass             Cs in place (global wavenumbers)
+        peer transpose 1        Cs -> every rank's A                 | barrier
+        rows inverse            A -> the output row slab
+    Two barriers and no pack passes per step."""
+
+    def __init__(self, nx, ny, comm, ops):
+        self.comm = comm
+        self.P = comm.world
+        if ny % self.P or nx % self.P:
+            raise ValueError("the rank count must divide nx and ny")
+        self.nx, self.ny = nx, ny
+        self.R, self.BW = ny // self.P, nx // self.P
+        self.ops = ops
+        self.ranks = comm.local_ranks()
+        self.A, self.A_ptrs = comm.alloc((self.R, nx), ops.dtype, ops.device)
+        self.Cs, self.Cs_ptrs = comm.alloc((ny, self.BW), ops.dtype, ops.device)
+
+    def _step(self, srcs, dsts, op, D, dt):
+        ops, R, BW = self.ops, self.R, self.BW
+        for i, r in enumerate(self.ranks):
+            ops.rows(srcs[i], self.A[i], False)
+            ops.peer_transpose(self.A[i], self.Cs_ptrs, r, R, BW, 0)
+        self.comm.barrier()
+        for i, r in enumerate(self.ranks):
+            ops.cols_slab(self.Cs[i], self.Cs[i], r * BW, op, D, dt)
+            ops.peer_transpose(self.Cs[i], self.A_ptrs, r, R, BW, 1)
+        self.comm.barrier()
+        for i, _ in enumerate(self.ranks):
+            ops.rows(self.A[i], dsts[i], True)
+
+    diffuse = SlabSolver.diffuse
+    poisson = SlabSolver.poisson
 
 
 def slab_rows(ny, world, rank):

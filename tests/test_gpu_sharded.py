@@ -1,7 +1,9 @@
-"""Slab decomposition on one GPU with P virtual ranks (LoopbackComm): the
-libfftpde row / column-slab / pack kernels with the sharded layouts, against
-the fp64 oracle.  The exchange is a block copy here; the multi-process NCCL
-path uses the same SlabSolver with DistComm (gloo-tested on CPU)."""
+"""Slab decomposition on one GPU with P virtual ranks: the libfftpde row /
+column-slab / pack kernels with the sharded layouts (LoopbackComm: the exchange
+is a block copy), and the peer-store exchange kernel (LoopbackPeerComm: every
+virtual rank's buffers on this device), against the fp64 oracle.  The
+multi-process NCCL path uses the same SlabSolver with DistComm (gloo-tested on
+CPU); the multi-GPU peer path uses SymmetricPeerComm (torch symmetric memory)."""
 import numpy as np
 import pytest
 import torch
@@ -17,9 +19,12 @@ def rel(a, b):
     return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / np.linalg.norm(np.ravel(b)))
 
 
-def run(nx, ny, P, dtype, x, D, dt, nsteps, Lx=1.0, Ly=1.0):
+def run(nx, ny, P, dtype, x, D, dt, nsteps, Lx=1.0, Ly=1.0, peer=False):
     ops = S.CudaLocalOps(nx, ny, dtype=dtype, Lx=Lx, Ly=Ly)
-    solver = S.SlabSolver(nx, ny, S.LoopbackComm(P), ops)
+    if peer:     # exchange by peer stores (fftpde_peer_transpose), P virtual ranks on one device
+        solver = S.PeerSlabSolver(nx, ny, S.LoopbackPeerComm(P), ops)
+    else:
+        solver = S.SlabSolver(nx, ny, S.LoopbackComm(P), ops)
     xt = torch.from_numpy(x).to(dtype).cuda()
     R = ny // P
     slabs = [xt[r * R:(r + 1) * R].contiguous() for r in range(P)]
@@ -58,4 +63,24 @@ def test_slab_long_axes_c5_shape_sampled():
     nx, ny, P = 64, 32768, 8
     x = I.white_noise((ny, nx), 6)
     u, p = run(nx, ny, P, torch.complex128, x, 1e-9, 0.01, 2)
+    assert rel(u, O.diffuse(x, 1e-9, 0.01, 2)) <= 1e-12
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.complex128, 1e-12), (torch.complex64, 1e-5)])
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_peer_store_exchange_vs_oracle_and_pack_path(dtype, tol, P):
+    # the fused exchange gives bit-for-bit the pack + all-to-all result
+    nx, ny, D, dt, n = 256, 128, 2e-4, 0.01, 3
+    x = I.white_noise((ny, nx), 101)
+    u, p = run(nx, ny, P, dtype, x, D, dt, n, Lx=1.5, Ly=0.75, peer=True)
+    assert rel(u, O.diffuse(x, D, dt, n, 1.5, 0.75)) <= tol
+    assert rel(p, O.poisson(x, 1.5, 0.75)) <= tol
+    u2, p2 = run(nx, ny, P, dtype, x, D, dt, n, Lx=1.5, Ly=0.75, peer=False)
+    assert np.array_equal(u, u2) and np.array_equal(p, p2)
+
+
+def test_peer_store_exchange_long_axes():
+    nx, ny, P = 32768, 64, 4
+    x = I.white_noise((ny, nx), 8)
+    u, p = run(nx, ny, P, torch.complex128, x, 1e-9, 0.01, 2, peer=True)
     assert rel(u, O.diffuse(x, 1e-9, 0.01, 2)) <= 1e-12
