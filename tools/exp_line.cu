@@ -7,8 +7,8 @@
 #include <vector>
 #include "../paper_2412_12308_b200/csrc/line.cuh"
 #include "../paper_2412_12308_b200/csrc/pipe.cuh"
-#include "../paper_2412_12308_b200/csrc/rr.cuh"
-#include "../paper_2412_12308_b200/csrc/tpipe.cuh"
+#include "experimental/rr.cuh"
+#include "experimental/tpipe.cuh"
 using namespace fftpde;
 
 static const char *g_filter = nullptr;

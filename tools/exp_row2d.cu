@@ -5,7 +5,7 @@
 #include <vector>
 #include <cmath>
 #include <random>
-#include "../paper_2412_12308_b200/csrc/row2.cuh"
+#include "experimental/row2.cuh"
 #include "../paper_2412_12308_b200/csrc/row2d.cuh"
 using namespace fftpde;
 static const char *g_filter = nullptr;

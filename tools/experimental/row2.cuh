@@ -13,7 +13,7 @@
 // The same factorisation as col2.cuh (eq:DFT); the row's
 // intermediate stays in L2 between phases.
 #pragma once
-#include "col2.cuh"
+#include "../../paper_2412_12308_b200/csrc/col2.cuh"
 
 namespace fftpde {
 

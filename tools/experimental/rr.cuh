@@ -19,9 +19,9 @@
 // transform; MID (rows) = the inverse transform of step s
 // stored as the physical field, then the forward transform of step s+1.
 #pragma once
-#include "fft_core.cuh"
-#include "line.cuh"
-#include "pipe.cuh"
+#include "../../paper_2412_12308_b200/csrc/fft_core.cuh"
+#include "../../paper_2412_12308_b200/csrc/line.cuh"
+#include "../../paper_2412_12308_b200/csrc/pipe.cuh"
 
 namespace fftpde {
 

@@ -16,7 +16,7 @@
 // stored through the tile buffer column-fastest, like the column pass.
 // Persistent CTAs, NBUF-deep cp.async ring as in pipe.cuh.
 #pragma once
-#include "pipe.cuh"
+#include "../../paper_2412_12308_b200/csrc/pipe.cuh"
 
 namespace fftpde {
 
