@@ -219,11 +219,13 @@ col2_kernel(Col2Args<T> g, OpTables<T> tab)
 #pragma unroll
                 for (int e = 0; e < E; ++e) nu[e] = ldcg_h(s1 + e * rstep, pol);
             }
-            fft<P, false, EMAX>(u, sm, t, g.twP, sync);                // X[k1 + Q k2], k2 = t + TPT e
-            if constexpr (OP == C2_WAVE) {
-                C w[E];
+            C w[OP == C2_WAVE ? E : 1];
+            if constexpr (OP == C2_WAVE) {       // second field's loads in flight during the first's transform
 #pragma unroll
                 for (int e = 0; e < E; ++e) w[e] = ldcg_h(g.V + r0 + e * rstep, pol);
+            }
+            fft<P, false, EMAX>(u, sm, t, g.twP, sync);                // X[k1 + Q k2], k2 = t + TPT e
+            if constexpr (OP == C2_WAVE) {
                 fft<P, false, EMAX>(w, sm, t, g.twP, sync);
                 const int64_t qa = a <= tab.nfold - a ? a : tab.nfold - a;
                 const T *pC = tab.wC + qa * tab.qpitch, *pS1 = tab.wS1 + qa * tab.qpitch,

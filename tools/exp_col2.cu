@@ -35,7 +35,7 @@ int main() {
     std::vector<double2> tn(n); for (long m = 0; m < n; ++m) { long double a = 2.0L * 3.14159265358979323846264338327950288L * m / n; tn[m] = {(double)cosl(a), (double)sinl(a)}; } double2* dtn = up(tn);
     std::vector<double> k2(n); for (long a = 0; a < n; ++a) { long f = 2 * a <= n ? a : a - n; k2[a] = (2 * M_PI * f) * (2 * M_PI * f); } double* dk2 = up(k2);
     std::vector<double> q((n / 2 + 1) * (n / 2 + 1), 0.5); double* dq = up(q);
-    OpTables<double> tab{}; tab.kx2 = dk2; tab.ky2 = dk2; tab.ex = dk2; tab.ey = dk2; tab.wC = dq; tab.wS1 = dq; tab.wS2 = dq; tab.qpitch = n / 2 + 1; tab.scale = 1.0 / (n * n);
+    OpTables<double> tab{}; tab.kx2 = dk2; tab.ky2 = dk2; tab.ex = dk2; tab.ey = dk2; tab.wC = dq; tab.wS1 = dq; tab.wS2 = dq; tab.qpitch = n / 2 + 1; tab.nfold = n; tab.scale = 1.0 / (n * n);
     Col2Args<double> g{U, V, U, n, n * n, n / 8, dtp, dtp, dtn};
     long nb = n / 8;
     printf("poisson, phase split:\n");

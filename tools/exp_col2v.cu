@@ -69,7 +69,7 @@ int main(int argc, char **argv)
     double *dk2 = up(k2);
     std::vector<double> q((n / 2 + 1) * (n / 2 + 1), 0.5); double *dq = up(q);
     OpTables<double> tab{}; tab.kx2 = dk2; tab.ky2 = dk2; tab.ex = dk2; tab.ey = dk2; tab.wC = dq; tab.wS1 = dq; tab.wS2 = dq;
-    tab.qpitch = n / 2 + 1; tab.scale = 1.0 / (n * n);
+    tab.qpitch = n / 2 + 1; tab.nfold = n; tab.scale = 1.0 / (n * n);
     Col2Args<double> g{U, V, U, n, n * n, n / 8, dtp, dtp, dtn};
     Col2Args<double> g16{U, V, U, n, n * n, n / 8, dtp16, dtp16, dtn};
     var<64, 64, C2_WAVE, 8, 256, 2, 8>(g, tab, n, "wave");
@@ -80,6 +80,8 @@ int main(int argc, char **argv)
     var<64, 64, C2_WAVE, 4, 256, 2, 8>(g, tab, n, "wave");
     var<64, 64, C2_WAVE, 8, 256, 3, 8>(g, tab, n, "wave");
     var<64, 64, C2_WAVE, 8, 128, 4, 8>(g, tab, n, "wave");
+    var<64, 64, C2_WAVE, 8, 128, 3, 8>(g, tab, n, "wave");
+    var<64, 64, C2_WAVE, 8, 128, 2, 8>(g, tab, n, "wave");
     var<64, 64, C2_WAVE, 8, 256, 2, 16>(g16, tab, n, "wave");
     var<64, 64, C2_WAVE, 8, 256, 1, 16>(g16, tab, n, "wave");
     var<64, 64, C2_POISSON, 8, 256, 2, 8>(g, tab, n, "poisson");

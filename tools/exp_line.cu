@@ -59,6 +59,7 @@ template <typename T> static OpTables<T> make_tab(int nx, int ny)
     OpTables<T> t{};
     t.kx2 = d[0]; t.ky2 = d[1]; t.ex = d[2]; t.ey = d[3]; t.wC = d[4]; t.wS1 = d[5]; t.wS2 = d[6];
     t.qpitch = qy;
+    t.nfold = nx;
     t.scale = (T)(1.0 / ((double)nx * ny));
     return t;
 }
