@@ -59,7 +59,7 @@ typedef enum {
     FFTPDE_ERR_UNSUPPORTED = 5,  /* axis longer than this build supports, or batch outside the plan */
     FFTPDE_ERR_WORKSPACE = 6,    /* workspace missing or smaller than fftpde_workspace_size() */
     FFTPDE_ERR_CUDA = 7,         /* a CUDA runtime call or kernel launch failed */
-    FFTPDE_ERR_NCCL = 8,         /* reserved for the sharded path */
+    FFTPDE_ERR_NCCL = 8,         /* NCCL missing or failed (sharded plans) */
     FFTPDE_ERR_NOT_POW2_Z = 9    /* nz not a power of two (3D plans) */
 } fftpde_status;
 
@@ -84,6 +84,27 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
  * (the *_batched calls and the other operators return FFTPDE_ERR_UNSUPPORTED). */
 fftpde_status fftpde_plan_2d_r2c(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t batch, fftpde_dtype dtype,
                                  double Lx, double Ly, int device);
+
+/* Sharded plan: the slab decomposition of an nx x ny grid over
+ * `nranks` processes (one GPU each), NCCL inside the library.  Every rank calls it
+ * collectively with the same nx, ny, dtype, L and the same 128-byte NCCL unique id
+ * (from fftpde_nccl_unique_id on rank 0, broadcast by the caller, e.g. over the
+ * torch process group).  Rank r owns rows [r ny/P, (r+1) ny/P) (its "row slab",
+ * [ny/P][nx]).  Whole-plan calls on a sharded plan are collective, in the same
+ * order on every rank:
+ *   fftpde_poisson / fftpde_diffuse: row slab in -> row slab out (u0 == u allowed);
+ *     per step rows -> pack -> grouped ncclSend/ncclRecv (an all-to-all over
+ *     NVLink) -> column-slab pass (forward along y, multiplier at the global
+ *     wavenumbers, inverse) -> all-to-all -> unpack -> inverse rows;
+ *   fftpde_forward: row slab -> this rank's column slab of the spectrum
+ *     [ny][nx/P] (spectral columns a in [r nx/P, (r+1) nx/P)), in != out;
+ *   fftpde_inverse: column slab -> row slab (x 1/(nx ny)).
+ * P must divide nx and ny, (nx/P) * element size a multiple of 16 bytes, and for
+ * ny > 8192 nx/P at least one 128-byte column block.  FFTPDE_ERR_NCCL when NCCL
+ * cannot be loaded (libnccl.so.2, dlopen) or the communicator fails. */
+fftpde_status fftpde_nccl_unique_id(void *out_128_bytes);
+fftpde_status fftpde_plan_2d_sharded(fftpde_plan *plan, int64_t nx, int64_t ny, fftpde_dtype dtype, double Lx,
+                                     double Ly, int device, const void *nccl_unique_id, int rank, int nranks);
 
 /* 3D plan (the n-D extension): [nz][ny][nx] grids on
  * [0,Lx) x [0,Ly) x [0,Lz), x fastest.  Transforms are sequential 1D passes

@@ -224,6 +224,26 @@ template <int N, typename C, int EMAX = 16> struct TwL1 {
     }
 };
 
+// As TwL1, reading a copy of the table staged in shared memory (short kernels
+// whose critical path would otherwise wait on L2 twiddle loads every stage).
+template <int N, typename C, int EMAX = 16> struct TwSmem {
+    const C *tw;
+    int t;
+    __device__ __forceinline__ C mid(int s, int m) const
+    {
+        using S = Shape<N, EMAX>;
+        int ns = S::E, off = 0;
+#pragma unroll
+        for (int i = 1; i < s; ++i) { off += S::E * ns; ns *= S::E; }
+        return tw[off + (t & (ns - 1)) + m * ns];
+    }
+    __device__ __forceinline__ C last(int q, int m) const
+    {
+        using S = Shape<N, EMAX>;
+        return tw[S::TW_LAST_OFF + t + q * S::TPT + m * S::NS_LAST];
+    }
+};
+
 template <int N, typename C, int EMAX = 16> struct TwReg {
     using S = Shape<N, EMAX>;
     static constexpr int NMID = S::STAGES > 1 ? (S::STAGES - 1) * (S::E - 1) : 1;

@@ -18,6 +18,8 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>   // types only: NCCL is loaded at run time (dlopen), not linked
 
 #include "../../include/fftpde.h"
 #include "launch.h"
@@ -55,6 +57,12 @@ struct fftpde_plan_s {
     int64_t launches = 0;
     // 3D plans (fftpde_plan_3d): the 2D machinery runs with batch = nz slabs; the
     // z-pass is a column pass of length nz over the nx*ny lines of the volume
+    // sharded plans (fftpde_plan_2d_sharded): this rank's row slab [R][nx], R = ny/P
+    bool sharded = false;
+    int P = 1, rank = 0;
+    ncclComm_t comm = nullptr;
+    int64_t R = 0, BW = 0;
+    size_t o_shA = 0, o_shB = 0, o_shC = 0;
     bool is3d = false;
     // real plans (fftpde_plan_2d_r2c): half spectrum [batch][ny][pitch], pitch = nx/2 + LPP
     bool is_real = false;
@@ -263,7 +271,7 @@ fftpde_status check_ptr(fftpde_plan p, const void *ptr)
 fftpde_status check_call(fftpde_plan p, int64_t batch, int64_t stride)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
-    if (p->is3d || p->is_real) return FFTPDE_ERR_UNSUPPORTED;   // 3D / real plans: whole-plan entry points only
+    if (p->is3d || p->is_real || p->sharded) return FFTPDE_ERR_UNSUPPORTED;   // whole-plan entry points only
     if (!p->ws) return FFTPDE_ERR_WORKSPACE;
     if (batch == 0) return FFTPDE_ERR_EMPTY;
     if (batch < 0 || stride < p->nx * p->ny) return FFTPDE_ERR_INVALID_ARG;
@@ -300,6 +308,38 @@ template <typename F> cudaError_t launch(fftpde_plan p, int cls, F &&f)
 }
 
 // ---- pass sequences --------------------------------------------------------
+// ---- NCCL, loaded at run time (the process's libnccl, e.g. the one torch loaded) --
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    ncclResult_t (*send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+};
+const NcclApi &nccl()
+{
+    static NcclApi api = [] {
+        NcclApi a;
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.getUniqueId = (decltype(a.getUniqueId))dlsym(h, "ncclGetUniqueId");
+        a.commInitRank = (decltype(a.commInitRank))dlsym(h, "ncclCommInitRank");
+        a.commDestroy = (decltype(a.commDestroy))dlsym(h, "ncclCommDestroy");
+        a.groupStart = (decltype(a.groupStart))dlsym(h, "ncclGroupStart");
+        a.groupEnd = (decltype(a.groupEnd))dlsym(h, "ncclGroupEnd");
+        a.send = (decltype(a.send))dlsym(h, "ncclSend");
+        a.recv = (decltype(a.recv))dlsym(h, "ncclRecv");
+        a.ok = a.getUniqueId && a.commInitRank && a.commDestroy && a.groupStart && a.groupEnd && a.send && a.recv;
+        return a;
+    }();
+    return api;
+}
+
 template <typename T> struct Passes {
     fftpde_plan p;
     int64_t batch, stride;
@@ -442,6 +482,79 @@ template <typename T> struct Passes {
                 if (e == cudaSuccess) e = rows(SV, V, 1);
             }
         }
+        return e;
+    }
+    // ---- sharded plans: the slab decomposition with NCCL inside ----
+    // rank r owns rows [r R, (r+1) R); after the exchange, spectral columns
+    // [r BW, (r+1) BW) of all ny rows.  Grouped point-to-point send/recv = all-to-all.
+    void *shA() const { return p->ws + p->o_shA; }
+    void *shB() const { return p->ws + p->o_shB; }
+    void *shC() const { return p->ws + p->o_shC; }
+    cudaError_t rows_sh(const void *in, void *out, int inverse)
+    {
+        return launch(p, FFTPDE_KERNEL_ROW, [&] {
+            if (p->rowP)
+                return launch_rows2<T>(p->nx, in, out, nullptr, p->R, p->R * p->nx, 1, inverse ? ROW_INV : ROW_FWD,
+                                       rtw(), p->stream);
+            return launch_rows<T>(p->nx, in, out, nullptr, p->R, p->R * p->nx, 1, inverse ? ROW_INV : ROW_FWD,
+                                  rtw(), p->stream);
+        });
+    }
+    cudaError_t pack_sh(const void *in, void *out, int direction)
+    {
+        ++p->launches;
+        return launch_pack(in, out, p->R, p->P, p->BW * (int64_t)elem_cplx(p), direction, p->stream);
+    }
+    cudaError_t cols_sh(const void *in, void *out, int op)
+    {
+        OpTables<T> t = tables<T>(p);
+        t.kx2 += p->rank * p->BW;                        // global wavenumbers of this column slab
+        t.ex += p->rank * p->BW;
+        return launch(p, FFTPDE_KERNEL_COL, [&] {
+            return launch_cols<T>(p->ny, in, out, p->BW, p->ny * p->BW, 1, op, ctw(), t, p->stream);
+        });
+    }
+    // blocks [P][R][BW] (block q for rank q) -> [P][R][BW] (block q from rank q)
+    cudaError_t exchange(const void *send, void *recv)
+    {
+        const NcclApi &n = nccl();
+        const size_t count = (size_t)(p->R * p->BW) * 2;            // complex = 2 reals
+        const ncclDataType_t ty = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+        const size_t blk = (size_t)(p->R * p->BW) * elem_cplx(p);
+        if (n.groupStart() != ncclSuccess) return cudaErrorUnknown;
+        for (int q = 0; q < p->P; ++q) {
+            n.send((const unsigned char *)send + q * blk, count, ty, q, p->comm, p->stream);
+            n.recv((unsigned char *)recv + q * blk, count, ty, q, p->comm, p->stream);
+        }
+        return n.groupEnd() == ncclSuccess ? cudaGetLastError() : cudaErrorUnknown;
+    }
+    // one step on the row slab: rows, pack, exchange, column pass, exchange, unpack, inverse rows
+    cudaError_t step_sh(const void *in, void *out, int op)
+    {
+        cudaError_t e = rows_sh(in, shA(), 0);
+        if (e == cudaSuccess) e = pack_sh(shA(), shB(), 0);
+        if (e == cudaSuccess) e = exchange(shB(), shC());             // -> column slab [ny][BW]
+        if (e == cudaSuccess) e = cols_sh(shC(), shC(), op);
+        if (e == cudaSuccess) e = exchange(shC(), shB());             // -> blocks of the row slab
+        if (e == cudaSuccess) e = pack_sh(shB(), shA(), 1);
+        if (e == cudaSuccess) e = rows_sh(shA(), out, 1);
+        return e;
+    }
+    // forward: row slab -> this rank's column slab of the spectrum [ny][BW]
+    cudaError_t forward_sh(const void *in, void *out)
+    {
+        cudaError_t e = rows_sh(in, shA(), 0);
+        if (e == cudaSuccess) e = pack_sh(shA(), shB(), 0);
+        if (e == cudaSuccess) e = exchange(shB(), shC());
+        if (e == cudaSuccess) e = cols_sh(shC(), out, COL_FWD);       // out of place (two-level pass)
+        return e;
+    }
+    cudaError_t inverse_sh(const void *in, void *out)
+    {
+        cudaError_t e = cols_sh(in, shC(), COL_INV);
+        if (e == cudaSuccess) e = exchange(shC(), shB());
+        if (e == cudaSuccess) e = pack_sh(shB(), shA(), 1);
+        if (e == cudaSuccess) e = rows_sh(shA(), out, 1);
         return e;
     }
     // ---- real plans (fftpde_plan_2d_r2c): half spectrum of pitch p->pitch -----------
@@ -1020,6 +1133,7 @@ fftpde_status fftpde_destroy(fftpde_plan plan)
         for (auto &ev : gr.prof) { cudaEventDestroy(ev.second.first); cudaEventDestroy(ev.second.second); }
     }
     if (plan->cap_stream) cudaStreamDestroy(plan->cap_stream);
+    if (plan->comm && nccl().ok) nccl().commDestroy(plan->comm);
     delete plan;
     return FFTPDE_OK;
 }
@@ -1167,7 +1281,7 @@ fftpde_status fftpde_cols_slab(fftpde_plan p, const void *in, void *out, int64_t
                                int op, double D, double dt)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
-    if (p->is3d || p->is_real) return FFTPDE_ERR_UNSUPPORTED;
+    if (p->is3d || p->is_real || p->sharded) return FFTPDE_ERR_UNSUPPORTED;
     if (!p->ws) return FFTPDE_ERR_WORKSPACE;
     if (ncols == 0) return FFTPDE_ERR_EMPTY;
     if (ncols < 0 || !is_pow2(ncols) || p->nx % ncols || col0 < 0 || col0 % ncols || col0 + ncols > p->nx)
@@ -1272,7 +1386,7 @@ fftpde_status fftpde_wave_rk4(fftpde_plan p, void *u, void *ut, double c, double
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
     if (!p->ws) return FFTPDE_ERR_WORKSPACE;
-    if (p->batch != 1 || p->is3d || p->is_real) return FFTPDE_ERR_UNSUPPORTED;
+    if (p->batch != 1 || p->is3d || p->is_real || p->sharded) return FFTPDE_ERR_UNSUPPORTED;
     fftpde_status s = check_ptr(p, u);
     if (s == FFTPDE_OK) s = check_ptr(p, ut);
     if (s != FFTPDE_OK) return s;
@@ -1320,6 +1434,55 @@ fftpde_status fftpde_peer_transpose(fftpde_plan p, const void *src, void *const 
     if (!g.ok) return FFTPDE_ERR_CUDA;
     ++p->launches;
     return cuda_status(launch_peer_transpose(src, pp, npeers, rank, R, bytes, direction, p->stream));
+}
+
+// ---- sharded plans ---------------------------------------------------------------
+fftpde_status fftpde_nccl_unique_id(void *out)
+{
+    if (!out) return FFTPDE_ERR_INVALID_ARG;
+    if (!nccl().ok) return FFTPDE_ERR_NCCL;
+    ncclUniqueId id;
+    if (nccl().getUniqueId(&id) != ncclSuccess) return FFTPDE_ERR_NCCL;
+    std::memcpy(out, &id, sizeof id);
+    return FFTPDE_OK;
+}
+
+fftpde_status fftpde_plan_2d_sharded(fftpde_plan *plan, int64_t nx, int64_t ny, fftpde_dtype dtype, double Lx,
+                                     double Ly, int device, const void *nccl_unique_id, int rank, int nranks)
+{
+    if (!plan) return FFTPDE_ERR_INVALID_ARG;
+    *plan = nullptr;
+    if (!nccl_unique_id || nranks < 1 || rank < 0 || rank >= nranks) return FFTPDE_ERR_INVALID_ARG;
+    fftpde_status s = fftpde_plan_2d(plan, nx, ny, 1, dtype, Lx, Ly, device);
+    if (s != FFTPDE_OK) return s;
+    fftpde_plan p = *plan;
+    auto fail = [&](fftpde_status st) { fftpde_destroy(p); *plan = nullptr; return st; };
+    const int64_t ec = (int64_t)elem_cplx(p);
+    if (nx % nranks || ny % nranks || ((nx / nranks) * ec) % 16) return fail(FFTPDE_ERR_UNSUPPORTED);
+    int64_t P2, Q2;
+    fftpde::col2_split(ny, nx / nranks, (int)ec, P2, Q2);
+    if (ny > kMaxLen && !P2) return fail(FFTPDE_ERR_UNSUPPORTED);   // column slab too narrow for long columns
+    if (!nccl().ok) return fail(FFTPDE_ERR_NCCL);
+    p->sharded = true;
+    p->P = nranks;
+    p->rank = rank;
+    p->R = ny / nranks;
+    p->BW = nx / nranks;
+    const size_t slab = (size_t)(p->R * nx) * (size_t)ec;
+    size_t off = p->need;
+    auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return o; };
+    p->o_shA = take(slab);
+    p->o_shB = take(slab);
+    p->o_shC = take(slab);
+    p->need = off;
+    {
+        DeviceGuard g(device);
+        if (!g.ok) return fail(FFTPDE_ERR_CUDA);
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_unique_id, sizeof id);
+        if (nccl().commInitRank(&p->comm, nranks, id, rank) != ncclSuccess) return fail(FFTPDE_ERR_NCCL);
+    }
+    return FFTPDE_OK;
 }
 
 // ---- real plans -------------------------------------------------------------------
@@ -1438,6 +1601,11 @@ extern "C" {
 fftpde_status fftpde_forward(fftpde_plan p, const void *in, void *out)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (p->sharded) {
+        fftpde_status s = check3(p, in, out);
+        if (s == FFTPDE_OK && in == out) s = FFTPDE_ERR_INVALID_ARG;
+        return s != FFTPDE_OK ? s : dispatch_real(p, [&](auto &ps) { return ps.forward_sh(in, out); });
+    }
     if (p->is_real) {
         fftpde_status s = check3(p, in, out);
         return s != FFTPDE_OK ? s : dispatch_real(p, [&](auto &ps) { return ps.forward_real(in, out); });
@@ -1451,6 +1619,10 @@ fftpde_status fftpde_forward(fftpde_plan p, const void *in, void *out)
 fftpde_status fftpde_inverse(fftpde_plan p, const void *in, void *out)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (p->sharded) {
+        fftpde_status s = check3(p, in, out);
+        return s != FFTPDE_OK ? s : dispatch_real(p, [&](auto &ps) { return ps.inverse_sh(in, out); });
+    }
     if (p->is_real) {
         fftpde_status s = check3(p, in, out);
         return s != FFTPDE_OK ? s : dispatch_real(p, [&](auto &ps) { return ps.inverse_real(in, out); });
@@ -1464,6 +1636,10 @@ fftpde_status fftpde_inverse(fftpde_plan p, const void *in, void *out)
 fftpde_status fftpde_poisson(fftpde_plan p, const void *rho, void *u)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (p->sharded) {
+        fftpde_status s = check3(p, rho, u);
+        return s != FFTPDE_OK ? s : dispatch_real(p, [&](auto &ps) { return ps.step_sh(rho, u, COL_POISSON); });
+    }
     if (p->is_real) {
         fftpde_status s = check3(p, rho, u);
         return s != FFTPDE_OK ? s : dispatch_real(p, [&](auto &ps) { return ps.poisson_real(rho, u); });
@@ -1477,6 +1653,21 @@ fftpde_status fftpde_poisson(fftpde_plan p, const void *rho, void *u)
 fftpde_status fftpde_diffuse(fftpde_plan p, const void *u0, void *u, double D, double dt, int64_t nsteps)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
+    if (p->sharded) {
+        fftpde_status s = check3(p, u0, u);
+        if (s != FFTPDE_OK) return s;
+        if (!std::isfinite(D) || !std::isfinite(dt) || D < 0 || dt < 0 || nsteps < 0) return FFTPDE_ERR_INVALID_ARG;
+        DeviceGuard g(p->device);
+        if (nsteps == 0)
+            return u0 == u ? FFTPDE_OK
+                           : cuda_status(cudaMemcpyAsync(u, u0, (size_t)(p->R * p->nx) * elem_cplx(p),
+                                                         cudaMemcpyDeviceToDevice, p->stream));
+        s = ensure_diffusion_tables(p, D, dt);
+        if (s != FFTPDE_OK) return s;
+        for (int64_t k = 0; k < nsteps && s == FFTPDE_OK; ++k)
+            s = dispatch_real(p, [&](auto &ps) { return ps.step_sh(k == 0 ? u0 : u, u, COL_DIFFUSE); });
+        return s;
+    }
     if (p->is_real) {
         fftpde_status s = check3(p, u0, u);
         if (s != FFTPDE_OK) return s;
@@ -1515,7 +1706,7 @@ fftpde_status fftpde_diffuse(fftpde_plan p, const void *u0, void *u, double D, d
 fftpde_status fftpde_wave_step(fftpde_plan p, void *u, void *ut, double c, double dt, int64_t nsteps)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
-    if (p->is3d) return FFTPDE_ERR_UNSUPPORTED;
+    if (p->is3d || p->sharded) return FFTPDE_ERR_UNSUPPORTED;
     if (p->is_real) {
         fftpde_status s = check3(p, u, ut);
         if (s != FFTPDE_OK) return s;

@@ -113,7 +113,11 @@ template <typename C, int NX, int NY> struct SmallLayout {
     static constexpr int THREADS_R = NY * Shape<NX>::TPT;
     static constexpr int THREADS_C = NX * Shape<NY>::TPT;
     static constexpr int THREADS = THREADS_R > THREADS_C ? THREADS_R : THREADS_C;
-    static constexpr size_t BYTES = (size_t)NY * PITCH * sizeof(C);
+    static constexpr int TWX = Shape<NX>::TW_SIZE > 0 ? Shape<NX>::TW_SIZE : 1;
+    static constexpr int TWY = Shape<NY>::TW_SIZE > 0 ? Shape<NY>::TW_SIZE : 1;
+    static constexpr size_t GRID = (size_t)NY * PITCH * sizeof(C);
+    // grid + twiddle tables of both axes + the two k^2 / diffusion factor tables
+    static constexpr size_t BYTES = GRID + (size_t)(TWX + TWY) * sizeof(C) + 2 * (size_t)(NX + NY) * sizeof(C) / 2;
 };
 
 template <typename T, int NX, int NY, int OP>
@@ -131,8 +135,21 @@ small_solve_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type 
     constexpr bool SOLVE = OP == COL_POISSON || OP == COL_DIFFUSE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *g = reinterpret_cast<C *>(smem_raw);
+    // tables staged in shared memory once: no L2 round trip on the per-stage critical path
+    C *stx = reinterpret_cast<C *>(smem_raw + L::GRID);
+    C *sty = stx + L::TWX;
+    T *sa = reinterpret_cast<T *>(sty + L::TWY);        // kx2 or ex  [NX]
+    T *sb = sa + NX;                                     // ky2 or ey  [NY]
     const int64_t off = (int64_t)blockIdx.x * stride;
     const int tid = threadIdx.x;
+    for (int i = tid; i < SX::TW_SIZE; i += L::THREADS) stx[i] = twx[i];
+    for (int i = tid; i < SY::TW_SIZE; i += L::THREADS) sty[i] = twy[i];
+    if constexpr (SOLVE) {
+        const T *ta = OP == COL_POISSON ? tab.kx2 : tab.ex;
+        const T *tb = OP == COL_POISSON ? tab.ky2 : tab.ey;
+        for (int i = tid; i < NX; i += L::THREADS) sa[i] = ta[i];
+        for (int i = tid; i < NY; i += L::THREADS) sb[i] = tb[i];
+    }
 
     // ---- phase 1: row transforms (forward, or inverse for COL_INV)
     {
@@ -140,8 +157,9 @@ small_solve_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type 
         C v[SX::E];
 #pragma unroll
         for (int e = 0; e < SX::E; ++e) v[e] = in[off + (int64_t)row * NX + t + SX::TPT * e];
+        __syncthreads();                                 // tables staged
         SmemView<C, SX::LOGE, 1> sm{g + row * L::PITCH};
-        fft<NX, INV>(v, sm, t, twx, SyncCTA{});
+        fft_tw<NX, INV>(v, sm, t, TwSmem<NX, C>{stx, t}, SyncCTA{});
 #pragma unroll
         for (int e = 0; e < SX::E; ++e) sm.at(t + SX::TPT * e) = v[e];
         __syncthreads();
@@ -158,21 +176,22 @@ small_solve_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type 
 #pragma unroll
             for (int e = 0; e < SY::E; ++e) v[e] = cscale(v[e], tab.scale);
         }
-        fft<NY, INV>(v, sm, t, twy, SyncCTA{});
+        const TwSmem<NY, C> twc{sty, t};
+        fft_tw<NY, INV>(v, sm, t, twc, SyncCTA{});
         if constexpr (SOLVE) {
 #pragma unroll
             for (int e = 0; e < SY::E; ++e) {
                 const int b = t + SY::TPT * e;
                 T m;
                 if constexpr (OP == COL_POISSON) {
-                    const T k2 = tab.kx2[col] + tab.ky2[b];
+                    const T k2 = sa[col] + sb[b];
                     m = k2 == (T)0 ? (T)0 : -tab.scale / k2;    // -1/|k|^2, k = 0 zeroed
                 } else {
-                    m = tab.ex[col] * tab.ey[b];                // exp(-D|k|^2 dt)/(nx ny)
+                    m = sa[col] * sb[b];                          // exp(-D|k|^2 dt)/(nx ny)
                 }
                 v[e] = cscale(v[e], m);
             }
-            fft<NY, true>(v, sm, t, twy, SyncCTA{});
+            fft_tw<NY, true>(v, sm, t, twc, SyncCTA{});
         }
 #pragma unroll
         for (int e = 0; e < SY::E; ++e) sm.at(t + SY::TPT * e) = v[e];
@@ -192,7 +211,7 @@ small_solve_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type 
 #pragma unroll
         for (int e = 0; e < SX::E; ++e) v[e] = sm.at(t + SX::TPT * e);
         __syncthreads();
-        fft<NX, true>(v, sm, t, twx, SyncCTA{});
+        fft_tw<NX, true>(v, sm, t, TwSmem<NX, C>{stx, t}, SyncCTA{});
 #pragma unroll
         for (int e = 0; e < SX::E; ++e) out[off + (int64_t)row * NX + t + SX::TPT * e] = v[e];
     }

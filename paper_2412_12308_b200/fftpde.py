@@ -30,7 +30,7 @@ C64, C128 = 0, 1
 EXPORTS = [
     "fftpde_plan_2d", "fftpde_workspace_size", "fftpde_set_workspace", "fftpde_set_stream",
     "fftpde_destroy", "fftpde_status_string", "fftpde_launch_count",
-    "fftpde_set_profiling", "fftpde_read_profile",
+    "fftpde_set_profiling", "fftpde_read_profile", "fftpde_nccl_unique_id", "fftpde_plan_2d_sharded",
     "fftpde_forward", "fftpde_inverse", "fftpde_poisson", "fftpde_diffuse", "fftpde_wave_step",
     "fftpde_forward_batched", "fftpde_inverse_batched", "fftpde_poisson_batched",
     "fftpde_diffuse_batched", "fftpde_wave_step_batched",
@@ -90,6 +90,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fftpde_apply": (st, [p, p, p, u]),
         "fftpde_plan_3d": (st, [ctypes.POINTER(p), i64, i64, i64, u, dbl, dbl, dbl, u]),
         "fftpde_plan_2d_r2c": (st, [ctypes.POINTER(p), i64, i64, i64, u, dbl, dbl, u]),
+        "fftpde_nccl_unique_id": (st, [p]),
+        "fftpde_plan_2d_sharded": (st, [ctypes.POINTER(p), i64, i64, u, dbl, dbl, u, p, u, u]),
         "fftpde_peer_transpose": (st, [p, p, ctypes.POINTER(p), u, u, i64, i64, u]),
         "fftpde_diffuse_source_scratch_size": (ctypes.c_size_t, [p]),
         "fftpde_diffuse_source": (st, [p, p, p, p, dbl, dbl, i64, p, ctypes.c_size_t]),
@@ -372,6 +374,81 @@ class Plan:
         _check(self.lib.fftpde_pack_blocks(self._h, x.data_ptr(), out.data_ptr(), int(nrows), int(nblocks),
                                            int(bw), int(direction)), "fftpde_pack_blocks")
         return out
+
+
+class ShardedPlan(Plan):
+    """The slab decomposition of one ny x nx grid over the ranks of ``group``
+    (fftpde_plan_2d_sharded): NCCL runs inside the library on a
+    communicator of its own, created from a unique id that rank 0 draws
+    (fftpde_nccl_unique_id) and this binding broadcasts over ``group``.  Rank r
+    holds rows [r R, (r+1) R), R = ny / P; every call is collective.  Without an
+    initialised process group it is a P = 1 plan (the full grid, NCCL to self)."""
+
+    def __init__(self, nx: int, ny: int, dtype=torch.complex128, Lx: float = 1.0, Ly: float = 1.0,
+                 device=None, group=None):
+        if dtype not in _DT:
+            raise TypeError("dtype must be torch.complex128 or torch.complex64")
+        if not torch.cuda.is_available():
+            raise RuntimeError("fftpde needs a CUDA device (no CPU fallback)")
+        import torch.distributed as dist
+        self.lib = load_library()
+        self.device = torch.device(device if device is not None else "cuda")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        if dist.is_available() and dist.is_initialized():
+            self.rank, self.P = dist.get_rank(group), dist.get_world_size(group)
+        else:
+            self.rank, self.P = 0, 1
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _check(self.lib.fftpde_nccl_unique_id(uid), "fftpde_nccl_unique_id")
+        if self.P > 1:
+            box = [bytes(uid.raw)]
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            uid = ctypes.create_string_buffer(box[0], 128)
+        self.nx, self.ny, self.batch, self.dtype = int(nx), int(ny), 1, dtype
+        self.Lx, self.Ly = float(Lx), float(Ly)
+        self.R, self.BW = self.ny // self.P, self.nx // self.P
+        h = ctypes.c_void_p()
+        _check(self.lib.fftpde_plan_2d_sharded(ctypes.byref(h), self.nx, self.ny, _DT[dtype], self.Lx, self.Ly,
+                                               self.device.index, uid, self.rank, self.P),
+               "fftpde_plan_2d_sharded")
+        self._h = h
+        nbytes = self.lib.fftpde_workspace_size(h)
+        self.workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        self._bind_stream()
+        _check(self.lib.fftpde_set_workspace(h, self.workspace.data_ptr(), self.workspace.numel()),
+               "fftpde_set_workspace")
+
+    def _slab(self, x, shape, name):
+        if x.dtype != self.dtype or tuple(x.shape) != shape:
+            raise ValueError(f"{name}: expected {self.dtype} {shape}, got {x.dtype} {tuple(x.shape)}")
+        if x.device != self.device or not x.is_contiguous():
+            raise ValueError(f"{name}: expected a contiguous tensor on {self.device}")
+
+    def _run(self, fn, x, xs, os_, out, *args):
+        self._slab(x, xs, "input")
+        o = torch.empty(os_, dtype=self.dtype, device=self.device) if out is None else out
+        self._slab(o, os_, "out")
+        self._bind_stream()
+        _check(fn(self._h, x.data_ptr(), o.data_ptr(), *args), fn.__name__)
+        return o
+
+    def forward(self, x, out=None):
+        """Row slab [R, nx] -> this rank's spectral column slab [ny, nx/P]."""
+        return self._run(self.lib.fftpde_forward, x, (self.R, self.nx), (self.ny, self.BW), out)
+
+    def inverse(self, X, out=None):
+        """Spectral column slab [ny, nx/P] -> row slab [R, nx] (x 1/(nx ny))."""
+        return self._run(self.lib.fftpde_inverse, X, (self.ny, self.BW), (self.R, self.nx), out)
+
+    def poisson(self, rho, out=None):
+        return self._run(self.lib.fftpde_poisson, rho, (self.R, self.nx), (self.R, self.nx), out)
+
+    def diffuse(self, u0, D: float, dt: float, nsteps: int, out=None):
+        return self._run(self.lib.fftpde_diffuse, u0, (self.R, self.nx), (self.R, self.nx), out,
+                         float(D), float(dt), int(nsteps))
 
 
 class Plan3D(Plan):

@@ -100,3 +100,15 @@ def test_product_package_does_not_reference_the_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 bad = re.findall(r"(?:from|import)\s+oracle|liboracle|fftpde_oracle", text)
                 assert not bad, (os.path.join(dirpath, f), bad)
+
+
+def test_sharded_plan_validation(lib):
+    # argument checks happen before NCCL or the device is touched
+    from paper_2412_12308_b200 import fftpde as F
+    h = ctypes.c_void_p()
+    uid = ctypes.create_string_buffer(128)
+    assert lib.fftpde_plan_2d_sharded(ctypes.byref(h), 64, 64, 1, 1.0, 1.0, 0, uid, 2, 2) == F.ERR_INVALID_ARG
+    assert lib.fftpde_plan_2d_sharded(ctypes.byref(h), 64, 64, 1, 1.0, 1.0, 0, None, 0, 1) == F.ERR_INVALID_ARG
+    assert lib.fftpde_plan_2d_sharded(ctypes.byref(h), 64, 64, 1, 1.0, 1.0, 0, uid, 0, 0) == F.ERR_INVALID_ARG
+    assert lib.fftpde_nccl_unique_id(None) == F.ERR_INVALID_ARG
+    assert h.value is None

@@ -84,3 +84,54 @@ def test_peer_store_exchange_long_axes():
     x = I.white_noise((ny, nx), 8)
     u, p = run(nx, ny, P, torch.complex128, x, 1e-9, 0.01, 2, peer=True)
     assert rel(u, O.diffuse(x, 1e-9, 0.01, 2)) <= 1e-12
+
+
+# ---- fftpde_plan_2d_sharded: the whole slab solve inside the C ABI (NCCL in the library) --
+from paper_2412_12308_b200 import fftpde as F  # noqa: E402
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.complex128, 1e-12), (torch.complex64, 1e-5)])
+@pytest.mark.parametrize("nx,ny", [(256, 128), (64, 1024), (2048, 16)])
+def test_sharded_plan_p1_vs_oracle(dtype, tol, nx, ny):
+    # one process: P = 1, the all-to-all is an NCCL send/recv to self
+    x = I.white_noise((ny, nx), 303)
+    p = F.ShardedPlan(nx, ny, dtype=dtype, Lx=1.5, Ly=0.75)
+    assert (p.P, p.R, p.BW) == (1, ny, nx)
+    xd = torch.from_numpy(x).to(dtype).cuda()
+    X = p.forward(xd)
+    assert rel(X.cpu().numpy(), O.fft2(x)) <= tol
+    assert rel(p.inverse(X).cpu().numpy(), x) <= tol
+    assert rel(p.poisson(xd).cpu().numpy(), O.poisson(x, 1.5, 0.75)) <= tol
+    assert rel(p.diffuse(xd, 2e-4, 0.01, 3).cpu().numpy(), O.diffuse(x, 2e-4, 0.01, 3, 1.5, 0.75)) <= tol
+    # in place (u0 == u)
+    u = xd.clone()
+    p.diffuse(u, 2e-4, 0.01, 3, out=u)
+    assert rel(u.cpu().numpy(), O.diffuse(x, 2e-4, 0.01, 3, 1.5, 0.75)) <= tol
+
+
+def test_sharded_plan_p1_long_axes():
+    for nx, ny in ((32768, 16), (64, 16384)):
+        x = I.white_noise((ny, nx), 304)
+        p = F.ShardedPlan(nx, ny)
+        u = p.diffuse(torch.from_numpy(x).cuda(), 1e-9, 0.01, 2).cpu().numpy()
+        assert rel(u, O.diffuse(x, 1e-9, 0.01, 2)) <= 1e-12
+
+
+def test_sharded_plan_matches_loopback_slab_solver():
+    # the in-library path and the Python SlabSolver (same kernels) agree bit for bit at P = 1
+    nx, ny = 512, 256
+    x = I.white_noise((ny, nx), 305)
+    u_lib = F.ShardedPlan(nx, ny).diffuse(torch.from_numpy(x).cuda(), 1e-4, 0.01, 3).cpu().numpy()
+    u_py, _ = run(nx, ny, 1, torch.complex128, x, 1e-4, 0.01, 3)
+    assert np.array_equal(u_lib, u_py)
+
+
+def test_sharded_plan_errors():
+    with pytest.raises(F.FFTPDEError):
+        F.ShardedPlan(100, 64)                           # not a power of two
+    p = F.ShardedPlan(64, 64)
+    x = torch.zeros(64, 64, dtype=torch.complex128, device="cuda")
+    assert p.lib.fftpde_wave_step(p._h, x.data_ptr(), x.data_ptr(), 1.0, 0.1, 1) == F.ERR_UNSUPPORTED
+    assert p.lib.fftpde_rows(p._h, x.data_ptr(), x.data_ptr(), 64, 0) == F.ERR_UNSUPPORTED
+    with pytest.raises(F.FFTPDEError):
+        p.forward(x, out=x)                              # forward is out of place
