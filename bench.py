@@ -67,7 +67,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="c5: use the slab-decomposed path even on one GPU (P = 1 process group)")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer", "lib"],
                     help="sharded c5: pack + NCCL all-to-all, or direct peer stores into torch "
                          "symmetric memory (fftpde_peer_transpose, SURVEY.md 8(e) N10)")
     return ap.parse_args()
@@ -423,6 +423,21 @@ def native(args, wl, world, rank, local):
     return line
 
 
+class _LibSharded:
+    """Adapter: a ShardedPlan with the SlabSolver-style call the sharded bench uses."""
+
+    def __init__(self, plan):
+        self.plan = plan
+
+    @property
+    def launches(self):
+        return self.plan.launches
+
+    def diffuse(self, slabs, D, dt, nsteps, outs):
+        self.plan.diffuse(slabs[0], D, dt, nsteps, out=outs[0])
+        return outs
+
+
 def sharded_native(args, wl, world, rank, local):
     """C5 at N > 1: the slab decomposition, NCCL all-to-all between
     the libfftpde row and column-slab passes; strong scaling (fixed 32768^2 grid)."""
@@ -435,10 +450,15 @@ def sharded_native(args, wl, world, rank, local):
     slab = full[lo:hi].contiguous()
     del full
     torch.cuda.empty_cache()
-    ops = S.CudaLocalOps(wl.nx, wl.ny, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly)
+    if args.exchange == "lib":     # the whole slab solve inside the C ABI (fftpde_plan_2d_sharded)
+        from paper_2412_12308_b200 import fftpde as F
+        ops = _LibSharded(F.ShardedPlan(wl.nx, wl.ny, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly))
+        solver = ops
+    else:
+        ops = S.CudaLocalOps(wl.nx, wl.ny, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly)
     if args.exchange == "peer":
         solver = S.PeerSlabSolver(wl.nx, wl.ny, S.SymmetricPeerComm(), ops)
-    else:
+    elif args.exchange == "nccl":
         solver = S.SlabSolver(wl.nx, wl.ny, S.DistComm(), ops)
     out = [torch.empty_like(slab)]
     for _ in range(args.warmup):
@@ -485,8 +505,10 @@ def sharded_native(args, wl, world, rank, local):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded C5 recipe, built on device)",
         "config": {**workload_config(wl, world),
-                   "parallelism": f"slab x{world} " + ("(peer-store exchange, symmetric memory)" if args.exchange == "peer"
-                                                       else "(NCCL all-to-all)"),
+                   "parallelism": f"slab x{world} " + {
+                       "peer": "(peer-store exchange, symmetric memory)",
+                       "nccl": "(NCCL all-to-all, Python-driven)",
+                       "lib": "(NCCL all-to-all inside libfftpde, fftpde_plan_2d_sharded)"}[args.exchange],
                    "l2": "field (16 GiB) larger than L2"},
         "e2e": None, "cpu_baseline": None, "clocks": clk.summary(),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

@@ -263,7 +263,9 @@ fftpde_status fftpde_wave_rk4(fftpde_plan plan, void *u, void *ut, double c,
  *   ncols must be a power of two dividing nx; col0 a multiple of ncols.
  * fftpde_pack_blocks: direction 0: [nrows][nblocks][bw] -> [nblocks][nrows][bw]
  *   (row slab -> per-peer send blocks); direction 1: the inverse.  bw in
- *   elements, bw * element size a multiple of 16 bytes. */
+ *   elements, bw * element size a multiple of 16 bytes.
+ * fftpde_rows and fftpde_cols_slab take a plain complex 2D plan (fftpde_plan_2d);
+ * 3D, real-field and sharded plans return FFTPDE_ERR_UNSUPPORTED. */
 /* fftpde_peer_transpose: the exchange step itself as direct stores into the
  *   other ranks' buffers over NVLink (the fused alternative to
  *   fftpde_pack_blocks + an all-to-all): one kernel per rank, local coalesced

@@ -1043,7 +1043,6 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     p->o_wc = take(q);
     p->o_ws1 = take(q);
     p->o_ws2 = take(q);
-    p->o_scr = take(2 * (size_t)(batch * nx * ny) * ec);
     if (p->rowP) {
         p->o_rtwP = take(p->rtwP.size() / 2 * ec);
         p->o_rtwQ = take(p->rtwQ.size() / 2 * ec);
@@ -1054,6 +1053,7 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
         p->o_twQ = take(p->twQ.size() / 2 * ec);
         p->o_twN = take(p->twN.size() / 2 * ec);
     }
+    p->o_scr = take(2 * (size_t)(batch * nx * ny) * ec);    // last: sharded plans replace it by slabs
     p->need = off;
     *plan = p;
     return FFTPDE_OK;
@@ -1251,7 +1251,7 @@ fftpde_status fftpde_wave_step_batched(fftpde_plan p, void *u, void *ut, int64_t
 fftpde_status fftpde_rows(fftpde_plan p, const void *in, void *out, int64_t nrows, int inverse)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
-    if (p->is3d) return FFTPDE_ERR_UNSUPPORTED;
+    if (p->is3d || p->is_real || p->sharded) return FFTPDE_ERR_UNSUPPORTED;
     if (!p->ws) return FFTPDE_ERR_WORKSPACE;
     if (nrows == 0) return FFTPDE_ERR_EMPTY;
     if (nrows < 0) return FFTPDE_ERR_INVALID_ARG;
@@ -1469,7 +1469,7 @@ fftpde_status fftpde_plan_2d_sharded(fftpde_plan *plan, int64_t nx, int64_t ny, 
     p->R = ny / nranks;
     p->BW = nx / nranks;
     const size_t slab = (size_t)(p->R * nx) * (size_t)ec;
-    size_t off = p->need;
+    size_t off = p->o_scr;                               // the full-grid scratch is not used: 3 slabs instead
     auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return o; };
     p->o_shA = take(slab);
     p->o_shB = take(slab);
