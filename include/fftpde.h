@@ -85,26 +85,49 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
 fftpde_status fftpde_plan_2d_r2c(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t batch, fftpde_dtype dtype,
                                  double Lx, double Ly, int device);
 
-/* Sharded plan: the slab decomposition of an nx x ny grid over
- * `nranks` processes (one GPU each), NCCL inside the library.  Every rank calls it
- * collectively with the same nx, ny, dtype, L and the same 128-byte NCCL unique id
- * (from fftpde_nccl_unique_id on rank 0, broadcast by the caller, e.g. over the
- * torch process group).  Rank r owns rows [r ny/P, (r+1) ny/P) (its "row slab",
- * [ny/P][nx]).  Whole-plan calls on a sharded plan are collective, in the same
- * order on every rank:
- *   fftpde_poisson / fftpde_diffuse: row slab in -> row slab out (u0 == u allowed);
- *     per step rows -> pack -> grouped ncclSend/ncclRecv (an all-to-all over
- *     NVLink) -> column-slab pass (forward along y, multiplier at the global
- *     wavenumbers, inverse) -> all-to-all -> unpack -> inverse rows;
- *   fftpde_forward: row slab -> this rank's column slab of the spectrum
- *     [ny][nx/P] (spectral columns a in [r nx/P, (r+1) nx/P)), in != out;
- *   fftpde_inverse: column slab -> row slab (x 1/(nx ny)).
- * P must divide nx and ny, (nx/P) * element size a multiple of 16 bytes, and for
- * ny > 8192 nx/P at least one 128-byte column block.  FFTPDE_ERR_NCCL when NCCL
- * cannot be loaded (libnccl.so.2, dlopen) or the communicator fails. */
+/* Sharded plans: the slab decomposition over `nranks`
+ * processes (one GPU each), NCCL inside the library.  Every rank calls the plan
+ * constructor collectively with the same sizes, dtype, L and the same 128-byte
+ * NCCL unique id (from fftpde_nccl_unique_id on rank 0, broadcast by the caller,
+ * e.g. over the torch process group).
+ *
+ * 2D (fftpde_plan_2d_sharded): rank r owns rows [r ny/P, (r+1) ny/P) (its "row
+ * slab", [ny/P][nx]).  Per step: rows -> pack -> grouped ncclSend/ncclRecv (an
+ * all-to-all over NVLink) -> column-slab pass (forward along y, multiplier at the
+ * global wavenumbers, inverse) -> all-to-all -> unpack -> inverse rows.
+ * fftpde_forward: row slab -> the rank's spectral column slab [ny][nx/P]
+ * (columns a in [r nx/P, (r+1) nx/P)), in != out; fftpde_inverse: column slab ->
+ * row slab (x 1/(nx ny)).  P must divide nx and ny, (nx/P) * element size must be
+ * a multiple of 16 bytes, and for ny > 8192 nx/P at least one 128-byte block.
+ *
+ * 3D (fftpde_plan_3d_sharded, SURVEY.md 8(f) row 4 on several GPUs): rank r owns
+ * z-planes [r nz/P, (r+1) nz/P) (its "z-slab", [nz/P][ny][nx]).  Per step: x- and
+ * y-passes of the local planes -> pack -> all-to-all -> z-pass with the multiplier
+ * on the "y-slab" [nz][ny/P][nx] (rows [r ny/P, (r+1) ny/P) of every plane) ->
+ * all-to-all -> unpack -> inverse y- and x-passes.  fftpde_forward returns the
+ * y-slab of the spectrum, fftpde_inverse takes it back (x 1/(nx ny nz)).  P must
+ * divide nz and ny.  One all-to-all per transform: a slab, not a pencil,
+ * decomposition (nz >= P, which holds for every nz <= 1024 at P <= 8).
+ *
+ * Whole-plan calls on a sharded plan (fftpde_forward / _inverse / _poisson /
+ * _diffuse) are collective, in the same order on every rank; u0 == u allowed.
+ * Loopback: nccl_unique_id = NULL and rank = FFTPDE_SHARDED_LOOPBACK builds one
+ * plan that runs all P ranks on its device in a single process (each phase for
+ * every rank in turn, the all-to-all as block copies): the caller's buffers then
+ * hold the P slabs back to back (for row and z-slabs: the natural full field).  It
+ * exercises the same per-rank kernels and index arithmetic as the NCCL path and is
+ * what single-GPU tests use.
+ * Errors: FFTPDE_ERR_INVALID_ARG for rank/nranks/id combinations other than the
+ * two above; FFTPDE_ERR_UNSUPPORTED when P does not divide the sliced axes;
+ * FFTPDE_ERR_NCCL when libnccl.so.2 cannot be loaded (dlopen) or
+ * ncclCommInitRank fails. */
+#define FFTPDE_SHARDED_LOOPBACK (-1)
 fftpde_status fftpde_nccl_unique_id(void *out_128_bytes);
 fftpde_status fftpde_plan_2d_sharded(fftpde_plan *plan, int64_t nx, int64_t ny, fftpde_dtype dtype, double Lx,
                                      double Ly, int device, const void *nccl_unique_id, int rank, int nranks);
+fftpde_status fftpde_plan_3d_sharded(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t nz, fftpde_dtype dtype,
+                                     double Lx, double Ly, double Lz, int device, const void *nccl_unique_id,
+                                     int rank, int nranks);
 
 /* 3D plan (the n-D extension): [nz][ny][nx] grids on
  * [0,Lx) x [0,Ly) x [0,Lz), x fastest.  Transforms are sequential 1D passes

@@ -60,8 +60,9 @@ struct fftpde_plan_s {
     // sharded plans (fftpde_plan_2d_sharded): this rank's row slab [R][nx], R = ny/P
     bool sharded = false;
     int P = 1, rank = 0;
+    bool loopback = false;                     // all P ranks in this one plan (single-process emulation)
     ncclComm_t comm = nullptr;
-    int64_t R = 0, BW = 0;
+    int64_t R = 0, BW = 0, nzl = 0, slab_elems = 0;
     size_t o_shA = 0, o_shB = 0, o_shC = 0;
     bool is3d = false;
     // real plans (fftpde_plan_2d_r2c): half spectrum [batch][ny][pitch], pitch = nx/2 + LPP
@@ -484,77 +485,155 @@ template <typename T> struct Passes {
         }
         return e;
     }
-    // ---- sharded plans: the slab decomposition with NCCL inside ----
-    // rank r owns rows [r R, (r+1) R); after the exchange, spectral columns
-    // [r BW, (r+1) BW) of all ny rows.  Grouped point-to-point send/recv = all-to-all.
-    void *shA() const { return p->ws + p->o_shA; }
-    void *shB() const { return p->ws + p->o_shB; }
-    void *shC() const { return p->ws + p->o_shC; }
+    // ---- sharded plans: the slab decomposition ----------------------
+    // 2D: rank r owns rows [r R, (r+1) R); after the exchange, spectral columns
+    // [r BW, (r+1) BW) of all ny rows.  3D: rank r owns z-planes [r nzl, (r+1) nzl)
+    // ("z-slab" [nzl][ny][nx]); after the exchange, all nz planes of rows
+    // [r R, (r+1) R) ("y-slab" [nz][R][nx]).  With NCCL the plan runs its own rank
+    // (grouped point-to-point send/recv = the all-to-all); in loopback mode one plan
+    // runs all P ranks on one device, every phase for every rank in turn, the
+    // exchange as block copies, and the caller's buffers hold the P slabs back to back.
+    int nloc() const { return p->loopback ? p->P : 1; }
+    int rk(int i) const { return p->loopback ? i : p->rank; }
+    size_t slab_bytes() const { return (size_t)p->slab_elems * elem_cplx(p); }
+    void *at(const void *base, int i) const { return (unsigned char *)base + (p->loopback ? (size_t)i * slab_bytes() : 0); }
+    void *shA(int i) const { return at(p->ws + p->o_shA, i); }
+    void *shB(int i) const { return at(p->ws + p->o_shB, i); }
+    void *shC(int i) const { return at(p->ws + p->o_shC, i); }
+    // rows (the x-pass) of one rank's slab: R rows (2D) or nzl planes of ny rows (3D)
     cudaError_t rows_sh(const void *in, void *out, int inverse)
     {
+        const int64_t nrows = p->is3d ? p->ny : p->R;
+        const int64_t nb = p->is3d ? p->nzl : 1, st = nrows * p->nx;
         return launch(p, FFTPDE_KERNEL_ROW, [&] {
             if (p->rowP)
-                return launch_rows2<T>(p->nx, in, out, nullptr, p->R, p->R * p->nx, 1, inverse ? ROW_INV : ROW_FWD,
-                                       rtw(), p->stream);
-            return launch_rows<T>(p->nx, in, out, nullptr, p->R, p->R * p->nx, 1, inverse ? ROW_INV : ROW_FWD,
-                                  rtw(), p->stream);
+                return launch_rows2<T>(p->nx, in, out, nullptr, nrows, st, nb, inverse ? ROW_INV : ROW_FWD, rtw(),
+                                       p->stream);
+            return launch_rows<T>(p->nx, in, out, nullptr, nrows, st, nb, inverse ? ROW_INV : ROW_FWD, rtw(),
+                                  p->stream);
         });
     }
+    // [nrows][P][blk] <-> [P][nrows][blk]: 2D rows of R x BW blocks; 3D planes of R x nx blocks
     cudaError_t pack_sh(const void *in, void *out, int direction)
     {
         ++p->launches;
-        return launch_pack(in, out, p->R, p->P, p->BW * (int64_t)elem_cplx(p), direction, p->stream);
+        const int64_t nrows = p->is3d ? p->nzl : p->R, bw = p->is3d ? p->R * p->nx : p->BW;
+        return launch_pack(in, out, nrows, p->P, bw * (int64_t)elem_cplx(p), direction, p->stream);
     }
-    cudaError_t cols_sh(const void *in, void *out, int op)
+    // 2D: the column pass of column slab r ([ny][BW], global wavenumbers r BW + c)
+    cudaError_t cols_sh(const void *in, void *out, int op, int r)
     {
         OpTables<T> t = tables<T>(p);
-        t.kx2 += p->rank * p->BW;                        // global wavenumbers of this column slab
-        t.ex += p->rank * p->BW;
+        t.kx2 += r * p->BW;
+        t.ex += r * p->BW;
         return launch(p, FFTPDE_KERNEL_COL, [&] {
             return launch_cols<T>(p->ny, in, out, p->BW, p->ny * p->BW, 1, op, ctw(), t, p->stream);
         });
     }
-    // blocks [P][R][BW] (block q for rank q) -> [P][R][BW] (block q from rank q)
-    cudaError_t exchange(const void *send, void *recv)
+    // 3D: the y-pass of one z-slab (nzl planes), forward or unscaled inverse
+    cudaError_t ypass_sh(const void *in, void *out, int op)
     {
+        return launch(p, FFTPDE_KERNEL_COL, [&] {
+            return launch_cols<T>(p->ny, in, out, p->nx, p->nx * p->ny, p->nzl, op, ctw(), tables3<false>((T)1),
+                                  p->stream);
+        });
+    }
+    // 3D: the z-pass of y-slab r: lines x + nx j (j < R) of length nz, global row r R + j
+    cudaError_t zpass_sh(const void *in, void *out, int op, int r)
+    {
+        OpTables<T> t = tables3<true>(scale3());
+        t.kx2 += r * p->R * p->nx;
+        t.ex += r * p->R * p->nx;
+        const ColTw ztw{p->ws + p->o_twz, nullptr, nullptr, nullptr, p->ws + p->o_twz8};
+        return launch(p, FFTPDE_KERNEL_COL, [&] {
+            return launch_cols<T>(p->nz, in, out, p->R * p->nx, p->nz * p->R * p->nx, 1, op, ztw, t, p->stream);
+        });
+    }
+    // the all-to-all: block q of rank r's send buffer -> block r of rank q's receive buffer
+    cudaError_t exchange(void *(Passes::*send)(int) const, void *(Passes::*recv)(int) const)
+    {
+        const size_t blk = slab_bytes() / (size_t)p->P;
+        if (p->loopback) {
+            for (int r = 0; r < p->P; ++r)
+                for (int q = 0; q < p->P; ++q) {
+                    cudaError_t e = cudaMemcpyAsync((unsigned char *)(this->*recv)(q) + r * blk,
+                                                    (const unsigned char *)(this->*send)(r) + q * blk, blk,
+                                                    cudaMemcpyDeviceToDevice, p->stream);
+                    if (e != cudaSuccess) return e;
+                }
+            return cudaSuccess;
+        }
         const NcclApi &n = nccl();
-        const size_t count = (size_t)(p->R * p->BW) * 2;            // complex = 2 reals
+        const size_t count = blk / sizeof(T);                          // complex = 2 reals
         const ncclDataType_t ty = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
-        const size_t blk = (size_t)(p->R * p->BW) * elem_cplx(p);
+        const unsigned char *sb = (const unsigned char *)(this->*send)(0);
+        unsigned char *rb = (unsigned char *)(this->*recv)(0);
         if (n.groupStart() != ncclSuccess) return cudaErrorUnknown;
         for (int q = 0; q < p->P; ++q) {
-            n.send((const unsigned char *)send + q * blk, count, ty, q, p->comm, p->stream);
-            n.recv((unsigned char *)recv + q * blk, count, ty, q, p->comm, p->stream);
+            n.send(sb + q * blk, count, ty, q, p->comm, p->stream);
+            n.recv(rb + q * blk, count, ty, q, p->comm, p->stream);
         }
         return n.groupEnd() == ncclSuccess ? cudaGetLastError() : cudaErrorUnknown;
     }
-    // one step on the row slab: rows, pack, exchange, column pass, exchange, unpack, inverse rows
-    cudaError_t step_sh(const void *in, void *out, int op)
+    template <typename F> cudaError_t each(F &&f)
     {
-        cudaError_t e = rows_sh(in, shA(), 0);
-        if (e == cudaSuccess) e = pack_sh(shA(), shB(), 0);
-        if (e == cudaSuccess) e = exchange(shB(), shC());             // -> column slab [ny][BW]
-        if (e == cudaSuccess) e = cols_sh(shC(), shC(), op);
-        if (e == cudaSuccess) e = exchange(shC(), shB());             // -> blocks of the row slab
-        if (e == cudaSuccess) e = pack_sh(shB(), shA(), 1);
-        if (e == cudaSuccess) e = rows_sh(shA(), out, 1);
+        for (int i = 0; i < nloc(); ++i) {
+            cudaError_t e = f(i);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
+    // slab in -> slabs shC (2D: column slabs [ny][BW] of the x-spectrum; 3D: y-slabs [nz][R][nx] of the xy-spectrum)
+    cudaError_t to_columns(const void *in)
+    {
+        cudaError_t e = each([&](int i) { return rows_sh(at(in, i), shA(i), 0); });
+        if (p->is3d) {
+            if (e == cudaSuccess) e = each([&](int i) { return ypass_sh(shA(i), shB(i), COL_FWD); });
+            if (e == cudaSuccess) e = each([&](int i) { return pack_sh(shB(i), shA(i), 0); });
+            if (e == cudaSuccess) e = exchange(&Passes::shA, &Passes::shC);
+            return e;
+        }
+        if (e == cudaSuccess) e = each([&](int i) { return pack_sh(shA(i), shB(i), 0); });
+        if (e == cudaSuccess) e = exchange(&Passes::shB, &Passes::shC);
         return e;
     }
-    // forward: row slab -> this rank's column slab of the spectrum [ny][BW]
+    // slabs shC -> slab out (inverse x-pass, and for 3D the inverse y-pass first)
+    cudaError_t from_columns(void *out)
+    {
+        cudaError_t e = exchange(&Passes::shC, &Passes::shB);
+        if (e == cudaSuccess) e = each([&](int i) { return pack_sh(shB(i), shA(i), 1); });
+        if (p->is3d) {
+            if (e == cudaSuccess) e = each([&](int i) { return ypass_sh(shA(i), shB(i), COL_INV); });
+            if (e == cudaSuccess) e = each([&](int i) { return rows_sh(shB(i), at(out, i), 1); });
+            return e;
+        }
+        if (e == cudaSuccess) e = each([&](int i) { return rows_sh(shA(i), at(out, i), 1); });
+        return e;
+    }
+    cudaError_t colpass_sh(const void *in, void *out, int op)
+    {
+        return each([&](int i) {
+            return p->is3d ? zpass_sh(at(in, i), at(out, i), op, rk(i)) : cols_sh(at(in, i), at(out, i), op, rk(i));
+        });
+    }
+    // one step: slab -> exchange -> column-slab pass with the operator -> exchange -> slab
+    cudaError_t step_sh(const void *in, void *out, int op)
+    {
+        cudaError_t e = to_columns(in);
+        if (e == cudaSuccess) e = colpass_sh(shC(0), shC(0), op);
+        if (e == cudaSuccess) e = from_columns(out);
+        return e;
+    }
     cudaError_t forward_sh(const void *in, void *out)
     {
-        cudaError_t e = rows_sh(in, shA(), 0);
-        if (e == cudaSuccess) e = pack_sh(shA(), shB(), 0);
-        if (e == cudaSuccess) e = exchange(shB(), shC());
-        if (e == cudaSuccess) e = cols_sh(shC(), out, COL_FWD);       // out of place (two-level pass)
+        cudaError_t e = to_columns(in);
+        if (e == cudaSuccess) e = colpass_sh(shC(0), out, COL_FWD);     // out of place (two-level pass)
         return e;
     }
     cudaError_t inverse_sh(const void *in, void *out)
     {
-        cudaError_t e = cols_sh(in, shC(), COL_INV);
-        if (e == cudaSuccess) e = exchange(shC(), shB());
-        if (e == cudaSuccess) e = pack_sh(shB(), shA(), 1);
-        if (e == cudaSuccess) e = rows_sh(shA(), out, 1);
+        cudaError_t e = colpass_sh(in, shC(0), COL_INV);
+        if (e == cudaSuccess) e = from_columns(out);
         return e;
     }
     // ---- real plans (fftpde_plan_2d_r2c): half spectrum of pitch p->pitch -----------
@@ -1447,12 +1526,50 @@ fftpde_status fftpde_nccl_unique_id(void *out)
     return FFTPDE_OK;
 }
 
+} // extern "C"
+namespace {
+// the slab buffers (in place of the full-grid scratch, which sharded plans never use) + the communicator
+fftpde_status finish_sharded(fftpde_plan p, int nranks, int rank, const void *uid, int64_t slab_elems)
+{
+    p->sharded = true;
+    p->P = nranks;
+    p->loopback = uid == nullptr;
+    p->rank = p->loopback ? 0 : rank;
+    p->slab_elems = slab_elems;
+    const size_t slab = (size_t)slab_elems * elem_cplx(p) * (size_t)(p->loopback ? nranks : 1);
+    size_t off = p->o_scr;
+    auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return o; };
+    p->o_shA = take(slab);
+    p->o_shB = take(slab);
+    p->o_shC = take(slab);
+    p->need = off;
+    if (p->loopback) return FFTPDE_OK;
+    if (!nccl().ok) return FFTPDE_ERR_NCCL;
+    DeviceGuard g(p->device);
+    if (!g.ok) return FFTPDE_ERR_CUDA;
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof id);
+    if (nccl().commInitRank(&p->comm, nranks, id, rank) != ncclSuccess) {
+        p->comm = nullptr;
+        return FFTPDE_ERR_NCCL;
+    }
+    return FFTPDE_OK;
+}
+bool sharded_args_ok(const void *uid, int rank, int nranks)
+{
+    if (nranks < 1) return false;
+    if (!uid) return rank == FFTPDE_SHARDED_LOOPBACK;
+    return rank >= 0 && rank < nranks;
+}
+} // namespace
+extern "C" {
+
 fftpde_status fftpde_plan_2d_sharded(fftpde_plan *plan, int64_t nx, int64_t ny, fftpde_dtype dtype, double Lx,
                                      double Ly, int device, const void *nccl_unique_id, int rank, int nranks)
 {
     if (!plan) return FFTPDE_ERR_INVALID_ARG;
     *plan = nullptr;
-    if (!nccl_unique_id || nranks < 1 || rank < 0 || rank >= nranks) return FFTPDE_ERR_INVALID_ARG;
+    if (!sharded_args_ok(nccl_unique_id, rank, nranks)) return FFTPDE_ERR_INVALID_ARG;
     fftpde_status s = fftpde_plan_2d(plan, nx, ny, 1, dtype, Lx, Ly, device);
     if (s != FFTPDE_OK) return s;
     fftpde_plan p = *plan;
@@ -1462,27 +1579,29 @@ fftpde_status fftpde_plan_2d_sharded(fftpde_plan *plan, int64_t nx, int64_t ny, 
     int64_t P2, Q2;
     fftpde::col2_split(ny, nx / nranks, (int)ec, P2, Q2);
     if (ny > kMaxLen && !P2) return fail(FFTPDE_ERR_UNSUPPORTED);   // column slab too narrow for long columns
-    if (!nccl().ok) return fail(FFTPDE_ERR_NCCL);
-    p->sharded = true;
-    p->P = nranks;
-    p->rank = rank;
     p->R = ny / nranks;
     p->BW = nx / nranks;
-    const size_t slab = (size_t)(p->R * nx) * (size_t)ec;
-    size_t off = p->o_scr;                               // the full-grid scratch is not used: 3 slabs instead
-    auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return o; };
-    p->o_shA = take(slab);
-    p->o_shB = take(slab);
-    p->o_shC = take(slab);
-    p->need = off;
-    {
-        DeviceGuard g(device);
-        if (!g.ok) return fail(FFTPDE_ERR_CUDA);
-        ncclUniqueId id;
-        std::memcpy(&id, nccl_unique_id, sizeof id);
-        if (nccl().commInitRank(&p->comm, nranks, id, rank) != ncclSuccess) return fail(FFTPDE_ERR_NCCL);
-    }
-    return FFTPDE_OK;
+    s = finish_sharded(p, nranks, rank, nccl_unique_id, p->R * nx);
+    return s == FFTPDE_OK ? s : fail(s);
+}
+
+fftpde_status fftpde_plan_3d_sharded(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t nz, fftpde_dtype dtype,
+                                     double Lx, double Ly, double Lz, int device, const void *nccl_unique_id,
+                                     int rank, int nranks)
+{
+    if (!plan) return FFTPDE_ERR_INVALID_ARG;
+    *plan = nullptr;
+    if (!sharded_args_ok(nccl_unique_id, rank, nranks)) return FFTPDE_ERR_INVALID_ARG;
+    fftpde_status s = fftpde_plan_3d(plan, nx, ny, nz, dtype, Lx, Ly, Lz, device);
+    if (s != FFTPDE_OK) return s;
+    fftpde_plan p = *plan;
+    auto fail = [&](fftpde_status st) { fftpde_destroy(p); *plan = nullptr; return st; };
+    const int64_t ec = (int64_t)elem_cplx(p);
+    if (nz % nranks || ny % nranks || ((ny / nranks) * nx * ec) % 16) return fail(FFTPDE_ERR_UNSUPPORTED);
+    p->R = ny / nranks;
+    p->nzl = nz / nranks;
+    s = finish_sharded(p, nranks, rank, nccl_unique_id, p->nzl * ny * nx);
+    return s == FFTPDE_OK ? s : fail(s);
 }
 
 // ---- real plans -------------------------------------------------------------------
@@ -1545,7 +1664,7 @@ fftpde_status fftpde_plan_3d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     for (int64_t y = 0; y < ny; ++y)
         for (int64_t x = 0; x < nx; ++x) p->kxy2[(size_t)(y * nx + x)] = p->kx2[(size_t)x] + p->ky2[(size_t)y];
     const size_t er = elem_real(p), ec = elem_cplx(p);
-    size_t off = p->need;
+    size_t off = p->o_scr;                     // the 3D tables go before the scratch, which stays last
     auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return o; };
     p->o_twz = take(p->twz.size() / 2 * ec);
     p->o_twz8 = take(p->twz8.size() / 2 * ec);
@@ -1553,6 +1672,7 @@ fftpde_status fftpde_plan_3d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     p->o_ez = take((size_t)nz * er);
     p->o_kxy2 = take((size_t)(nx * ny) * er);
     p->o_exy = take((size_t)(nx * ny) * er);
+    p->o_scr = take(2 * (size_t)(nz * nx * ny) * ec);
     p->need = off;
     return FFTPDE_OK;
 }
@@ -1660,9 +1780,10 @@ fftpde_status fftpde_diffuse(fftpde_plan p, const void *u0, void *u, double D, d
         DeviceGuard g(p->device);
         if (nsteps == 0)
             return u0 == u ? FFTPDE_OK
-                           : cuda_status(cudaMemcpyAsync(u, u0, (size_t)(p->R * p->nx) * elem_cplx(p),
+                           : cuda_status(cudaMemcpyAsync(u, u0, (size_t)p->slab_elems * elem_cplx(p) *
+                                                                         (size_t)(p->loopback ? p->P : 1),
                                                          cudaMemcpyDeviceToDevice, p->stream));
-        s = ensure_diffusion_tables(p, D, dt);
+        s = p->is3d ? ensure_diffusion_tables3(p, D, dt) : ensure_diffusion_tables(p, D, dt);
         if (s != FFTPDE_OK) return s;
         for (int64_t k = 0; k < nsteps && s == FFTPDE_OK; ++k)
             s = dispatch_real(p, [&](auto &ps) { return ps.step_sh(k == 0 ? u0 : u, u, COL_DIFFUSE); });

@@ -31,6 +31,7 @@ EXPORTS = [
     "fftpde_plan_2d", "fftpde_workspace_size", "fftpde_set_workspace", "fftpde_set_stream",
     "fftpde_destroy", "fftpde_status_string", "fftpde_launch_count",
     "fftpde_set_profiling", "fftpde_read_profile", "fftpde_nccl_unique_id", "fftpde_plan_2d_sharded",
+    "fftpde_plan_3d_sharded",
     "fftpde_forward", "fftpde_inverse", "fftpde_poisson", "fftpde_diffuse", "fftpde_wave_step",
     "fftpde_forward_batched", "fftpde_inverse_batched", "fftpde_poisson_batched",
     "fftpde_diffuse_batched", "fftpde_wave_step_batched",
@@ -92,6 +93,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fftpde_plan_2d_r2c": (st, [ctypes.POINTER(p), i64, i64, i64, u, dbl, dbl, u]),
         "fftpde_nccl_unique_id": (st, [p]),
         "fftpde_plan_2d_sharded": (st, [ctypes.POINTER(p), i64, i64, u, dbl, dbl, u, p, u, u]),
+        "fftpde_plan_3d_sharded": (st, [ctypes.POINTER(p), i64, i64, i64, u, dbl, dbl, dbl, u, p, u, u]),
         "fftpde_peer_transpose": (st, [p, p, ctypes.POINTER(p), u, u, i64, i64, u]),
         "fftpde_diffuse_source_scratch_size": (ctypes.c_size_t, [p]),
         "fftpde_diffuse_source": (st, [p, p, p, p, dbl, dbl, i64, p, ctypes.c_size_t]),
@@ -376,50 +378,67 @@ class Plan:
         return out
 
 
-class ShardedPlan(Plan):
-    """The slab decomposition of one ny x nx grid over the ranks of ``group``
-    (fftpde_plan_2d_sharded, SURVEY.md 8(e)): NCCL runs inside the library on a
-    communicator of its own, created from a unique id that rank 0 draws
-    (fftpde_nccl_unique_id) and this binding broadcasts over ``group``.  Rank r
-    holds rows [r R, (r+1) R), R = ny / P; every call is collective.  Without an
-    initialised process group it is a P = 1 plan (the full grid, NCCL to self)."""
+SHARDED_LOOPBACK = -1
 
-    def __init__(self, nx: int, ny: int, dtype=torch.complex128, Lx: float = 1.0, Ly: float = 1.0,
-                 device=None, group=None):
+
+def broadcast_unique_id(draw, group=None) -> bytes:
+    """The 128-byte NCCL unique id for a sharded plan: ``draw()`` on rank 0 of
+    ``group`` (fftpde_nccl_unique_id), broadcast to every rank over the torch
+    process group (any backend)."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    box = [draw() if rank == 0 else None]
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    dist.broadcast_object_list(box, src=src, group=group)
+    if not isinstance(box[0], (bytes, bytearray)) or len(box[0]) != 128:
+        raise RuntimeError("bad NCCL unique id broadcast")
+    return bytes(box[0])
+
+
+class _Sharded(Plan):
+    """Common part of ShardedPlan / ShardedPlan3D: communicator set-up and the
+    collective whole-plan calls.  ``loopback=P`` builds the single-process
+    emulation of P ranks on this device (FFTPDE_SHARDED_LOOPBACK): buffers hold
+    the P slabs back to back."""
+
+    def _setup(self, dtype, device, group, loopback, make):
         if dtype not in _DT:
             raise TypeError("dtype must be torch.complex128 or torch.complex64")
         if not torch.cuda.is_available():
             raise RuntimeError("fftpde needs a CUDA device (no CPU fallback)")
         import torch.distributed as dist
         self.lib = load_library()
+        self.dtype, self.batch = dtype, 1
         self.device = torch.device(device if device is not None else "cuda")
         if self.device.index is None:
             self.device = torch.device("cuda", torch.cuda.current_device())
-        if dist.is_available() and dist.is_initialized():
-            self.rank, self.P = dist.get_rank(group), dist.get_world_size(group)
-        else:
-            self.rank, self.P = 0, 1
-        uid = ctypes.create_string_buffer(128)
-        if self.rank == 0:
-            _check(self.lib.fftpde_nccl_unique_id(uid), "fftpde_nccl_unique_id")
-        if self.P > 1:
-            box = [bytes(uid.raw)]
-            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
-                                       group=group)
-            uid = ctypes.create_string_buffer(box[0], 128)
-        self.nx, self.ny, self.batch, self.dtype = int(nx), int(ny), 1, dtype
-        self.Lx, self.Ly = float(Lx), float(Ly)
-        self.R, self.BW = self.ny // self.P, self.nx // self.P
         h = ctypes.c_void_p()
-        _check(self.lib.fftpde_plan_2d_sharded(ctypes.byref(h), self.nx, self.ny, _DT[dtype], self.Lx, self.Ly,
-                                               self.device.index, uid, self.rank, self.P),
-               "fftpde_plan_2d_sharded")
+        if loopback:
+            self.rank, self.P, self.loopback = 0, int(loopback), True
+            _check(make(h, None, SHARDED_LOOPBACK, self.P), "sharded plan (loopback)")
+        else:
+            self.loopback = False
+            if dist.is_available() and dist.is_initialized():
+                self.rank, self.P = dist.get_rank(group), dist.get_world_size(group)
+            else:
+                self.rank, self.P = 0, 1
+
+            def draw():
+                buf = ctypes.create_string_buffer(128)
+                _check(self.lib.fftpde_nccl_unique_id(buf), "fftpde_nccl_unique_id")
+                return buf.raw
+
+            uid = draw() if self.P == 1 else broadcast_unique_id(draw, group)
+            _check(make(h, ctypes.create_string_buffer(uid, 128), self.rank, self.P), "sharded plan")
         self._h = h
         nbytes = self.lib.fftpde_workspace_size(h)
         self.workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
         self._bind_stream()
         _check(self.lib.fftpde_set_workspace(h, self.workspace.data_ptr(), self.workspace.numel()),
                "fftpde_set_workspace")
+
+    def _lb(self, shape):
+        return ((self.P,) + shape) if self.loopback else shape
 
     def _slab(self, x, shape, name):
         if x.dtype != self.dtype or tuple(x.shape) != shape:
@@ -436,19 +455,59 @@ class ShardedPlan(Plan):
         return o
 
     def forward(self, x, out=None):
-        """Row slab [R, nx] -> this rank's spectral column slab [ny, nx/P]."""
-        return self._run(self.lib.fftpde_forward, x, (self.R, self.nx), (self.ny, self.BW), out)
+        """Physical slab -> this rank's spectral slab (see the class docstring)."""
+        return self._run(self.lib.fftpde_forward, x, self.phys_shape, self.spec_shape, out)
 
     def inverse(self, X, out=None):
-        """Spectral column slab [ny, nx/P] -> row slab [R, nx] (x 1/(nx ny))."""
-        return self._run(self.lib.fftpde_inverse, X, (self.ny, self.BW), (self.R, self.nx), out)
+        return self._run(self.lib.fftpde_inverse, X, self.spec_shape, self.phys_shape, out)
 
     def poisson(self, rho, out=None):
-        return self._run(self.lib.fftpde_poisson, rho, (self.R, self.nx), (self.R, self.nx), out)
+        return self._run(self.lib.fftpde_poisson, rho, self.phys_shape, self.phys_shape, out)
 
     def diffuse(self, u0, D: float, dt: float, nsteps: int, out=None):
-        return self._run(self.lib.fftpde_diffuse, u0, (self.R, self.nx), (self.R, self.nx), out,
+        return self._run(self.lib.fftpde_diffuse, u0, self.phys_shape, self.phys_shape, out,
                          float(D), float(dt), int(nsteps))
+
+
+class ShardedPlan(_Sharded):
+    """The slab decomposition of one ny x nx grid over the ranks of ``group``
+    (fftpde_plan_2d_sharded, SURVEY.md 8(e)): NCCL runs inside the library on a
+    communicator of its own, created from a unique id that rank 0 draws and this
+    binding broadcasts over ``group``.  Rank r holds rows [r R, (r+1) R), R = ny/P
+    (``phys_shape`` [R, nx]); its spectrum slab is columns [r BW, (r+1) BW),
+    BW = nx/P (``spec_shape`` [ny, BW]).  Every call is collective.  Without an
+    initialised process group it is a P = 1 plan (NCCL send/recv to itself);
+    ``loopback=P`` emulates P ranks in this process ([ny, nx] in, [P, ny, BW] spectra)."""
+
+    def __init__(self, nx: int, ny: int, dtype=torch.complex128, Lx: float = 1.0, Ly: float = 1.0,
+                 device=None, group=None, loopback: int = 0):
+        self.nx, self.ny, self.Lx, self.Ly = int(nx), int(ny), float(Lx), float(Ly)
+        self._setup(dtype, device, group, loopback,
+                    lambda h, uid, rank, P: self.lib.fftpde_plan_2d_sharded(
+                        ctypes.byref(h), self.nx, self.ny, _DT[dtype], self.Lx, self.Ly, self.device.index, uid,
+                        rank, P))
+        self.R, self.BW = self.ny // self.P, self.nx // self.P
+        self.phys_shape = (self.ny, self.nx) if self.loopback else (self.R, self.nx)
+        self.spec_shape = self._lb((self.ny, self.BW))
+
+
+class ShardedPlan3D(_Sharded):
+    """The slab decomposition of an nz x ny x nx volume (fftpde_plan_3d_sharded):
+    rank r holds z-planes [r nzl, (r+1) nzl), nzl = nz/P (``phys_shape``
+    [nzl, ny, nx]); its spectrum slab is the y-slab, rows [r R, (r+1) R) of all nz
+    planes (``spec_shape`` [nz, R, nx]).  One all-to-all each way per transform."""
+
+    def __init__(self, nx: int, ny: int, nz: int, dtype=torch.complex128, Lx: float = 1.0, Ly: float = 1.0,
+                 Lz: float = 1.0, device=None, group=None, loopback: int = 0):
+        self.nx, self.ny, self.nz = int(nx), int(ny), int(nz)
+        self.Lx, self.Ly, self.Lz = float(Lx), float(Ly), float(Lz)
+        self._setup(dtype, device, group, loopback,
+                    lambda h, uid, rank, P: self.lib.fftpde_plan_3d_sharded(
+                        ctypes.byref(h), self.nx, self.ny, self.nz, _DT[dtype], self.Lx, self.Ly, self.Lz,
+                        self.device.index, uid, rank, P))
+        self.R, self.nzl = self.ny // self.P, self.nz // self.P
+        self.phys_shape = (self.nz, self.ny, self.nx) if self.loopback else (self.nzl, self.ny, self.nx)
+        self.spec_shape = self._lb((self.nz, self.R, self.nx))
 
 
 class Plan3D(Plan):

@@ -112,3 +112,12 @@ def test_sharded_plan_validation(lib):
     assert lib.fftpde_plan_2d_sharded(ctypes.byref(h), 64, 64, 1, 1.0, 1.0, 0, uid, 0, 0) == F.ERR_INVALID_ARG
     assert lib.fftpde_nccl_unique_id(None) == F.ERR_INVALID_ARG
     assert h.value is None
+
+
+def test_sharded_loopback_argument_forms(lib):
+    from paper_2412_12308_b200 import fftpde as F
+    h = ctypes.c_void_p()
+    # loopback needs rank == FFTPDE_SHARDED_LOOPBACK and nranks >= 1
+    assert lib.fftpde_plan_2d_sharded(ctypes.byref(h), 64, 64, 1, 1.0, 1.0, 0, None, -1, 0) == F.ERR_INVALID_ARG
+    assert lib.fftpde_plan_3d_sharded(ctypes.byref(h), 64, 64, 8, 1, 1.0, 1.0, 1.0, 0, None, 1, 2) == F.ERR_INVALID_ARG
+    assert F.SHARDED_LOOPBACK == -1

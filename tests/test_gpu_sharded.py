@@ -86,8 +86,13 @@ def test_peer_store_exchange_long_axes():
     assert rel(u, O.diffuse(x, 1e-9, 0.01, 2)) <= 1e-12
 
 
-# ---- fftpde_plan_2d_sharded: the whole slab solve inside the C ABI (NCCL in the library) --
+# ---- fftpde_plan_2d_sharded / _3d_sharded: the whole slab solve inside the C ABI ------
 from paper_2412_12308_b200 import fftpde as F  # noqa: E402
+
+
+def spec2_from_slabs(X, P):
+    # [P][ny][BW] column slabs -> the natural [ny][nx] spectrum
+    return np.concatenate(list(X), axis=1) if P > 1 else X
 
 
 @pytest.mark.parametrize("dtype,tol", [(torch.complex128, 1e-12), (torch.complex64, 1e-5)])
@@ -103,32 +108,92 @@ def test_sharded_plan_p1_vs_oracle(dtype, tol, nx, ny):
     assert rel(p.inverse(X).cpu().numpy(), x) <= tol
     assert rel(p.poisson(xd).cpu().numpy(), O.poisson(x, 1.5, 0.75)) <= tol
     assert rel(p.diffuse(xd, 2e-4, 0.01, 3).cpu().numpy(), O.diffuse(x, 2e-4, 0.01, 3, 1.5, 0.75)) <= tol
-    # in place (u0 == u)
-    u = xd.clone()
+    u = xd.clone()                                       # in place (u0 == u)
     p.diffuse(u, 2e-4, 0.01, 3, out=u)
     assert rel(u.cpu().numpy(), O.diffuse(x, 2e-4, 0.01, 3, 1.5, 0.75)) <= tol
 
 
-def test_sharded_plan_p1_long_axes():
-    for nx, ny in ((32768, 16), (64, 16384)):
+@pytest.mark.parametrize("dtype,tol", [(torch.complex128, 1e-12), (torch.complex64, 1e-5)])
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_sharded_plan_loopback_vs_oracle(dtype, tol, P):
+    # P ranks emulated in one plan: the per-rank kernels, wavenumber offsets and
+    # block exchange of the NCCL path, on one device
+    nx, ny = 256, 128
+    x = I.white_noise((ny, nx), 306)
+    p = F.ShardedPlan(nx, ny, dtype=dtype, Lx=1.5, Ly=0.75, loopback=P)
+    xd = torch.from_numpy(x).to(dtype).cuda()
+    X = p.forward(xd)
+    assert tuple(X.shape) == (P, ny, nx // P)
+    assert rel(spec2_from_slabs(X.cpu().numpy(), P), O.fft2(x)) <= tol
+    assert rel(p.inverse(X).cpu().numpy(), x) <= tol
+    assert rel(p.poisson(xd).cpu().numpy(), O.poisson(x, 1.5, 0.75)) <= tol
+    assert rel(p.diffuse(xd, 2e-4, 0.01, 3).cpu().numpy(), O.diffuse(x, 2e-4, 0.01, 3, 1.5, 0.75)) <= tol
+
+
+def test_sharded_plan_loopback_bitwise_equals_python_slab_solver():
+    # the in-library step and the Python SlabSolver (same kernels, same order) agree bit for bit
+    nx, ny = 512, 256
+    x = I.white_noise((ny, nx), 305)
+    for P in (1, 4):
+        u_lib = F.ShardedPlan(nx, ny, loopback=P).diffuse(torch.from_numpy(x).cuda(), 1e-4, 0.01, 3).cpu().numpy()
+        u_py, p_py = run(nx, ny, P, torch.complex128, x, 1e-4, 0.01, 3)
+        assert np.array_equal(u_lib, u_py)
+    u1 = F.ShardedPlan(nx, ny).diffuse(torch.from_numpy(x).cuda(), 1e-4, 0.01, 3).cpu().numpy()
+    assert np.array_equal(u1, u_lib)                     # NCCL P = 1 == loopback P = 4
+
+
+def test_sharded_plan_long_axes():
+    for nx, ny, P in ((32768, 16, 1), (32768, 64, 4), (64, 16384, 1), (64, 16384, 2)):
         x = I.white_noise((ny, nx), 304)
-        p = F.ShardedPlan(nx, ny)
+        p = F.ShardedPlan(nx, ny, loopback=P if P > 1 else 0)
         u = p.diffuse(torch.from_numpy(x).cuda(), 1e-9, 0.01, 2).cpu().numpy()
         assert rel(u, O.diffuse(x, 1e-9, 0.01, 2)) <= 1e-12
 
 
-def test_sharded_plan_matches_loopback_slab_solver():
-    # the in-library path and the Python SlabSolver (same kernels) agree bit for bit at P = 1
-    nx, ny = 512, 256
-    x = I.white_noise((ny, nx), 305)
-    u_lib = F.ShardedPlan(nx, ny).diffuse(torch.from_numpy(x).cuda(), 1e-4, 0.01, 3).cpu().numpy()
-    u_py, _ = run(nx, ny, 1, torch.complex128, x, 1e-4, 0.01, 3)
-    assert np.array_equal(u_lib, u_py)
+def rand3(shape, seed):
+    rng = np.random.default_rng(seed)
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+@pytest.mark.parametrize("P", [0, 2, 4])
+@pytest.mark.parametrize("shape,L", [((16, 32, 64), (1.0, 2.0, 0.5)), ((8, 2048, 16), (1.0, 1.0, 1.0))])
+def test_sharded_3d_vs_oracle(P, shape, L):
+    # P = 0: the NCCL plan at P = 1; P > 1: loopback emulation of P ranks
+    nz, ny, nx = shape
+    x = rand3(shape, 277)
+    p = F.ShardedPlan3D(nx, ny, nz, Lx=L[0], Ly=L[1], Lz=L[2], loopback=P)
+    Pn = max(P, 1)
+    xd = torch.from_numpy(x).cuda()
+    X = p.forward(xd).cpu().numpy()
+    full = np.concatenate(list(X), axis=1) if P else X       # y-slabs -> [nz][ny][nx]
+    assert rel(full, O.fft3(x)) <= 1e-12
+    assert rel(p.inverse(torch.from_numpy(X).cuda()).cpu().numpy(), x) <= 1e-12
+    assert rel(p.poisson(xd).cpu().numpy(), O.poisson3(x, *L)) <= 1e-12
+    assert rel(p.diffuse(xd, 1e-3, 0.01, 3).cpu().numpy(), O.diffuse3(x, 1e-3, 0.01, 3, *L)) <= 1e-12
+    assert p.R == ny // Pn and p.nzl == nz // Pn
+
+
+def test_sharded_3d_c64_and_closeness_to_plan3d():
+    nz, ny, nx = 32, 64, 64
+    x = rand3((nz, ny, nx), 278)
+    p = F.ShardedPlan3D(nx, ny, nz, dtype=torch.complex64, loopback=4)
+    xd = torch.from_numpy(x.astype(np.complex64)).cuda()
+    assert rel(p.poisson(xd).cpu().numpy(), O.poisson3(x.astype(np.complex64).astype(np.complex128))) <= 1e-5
+    q = F.ShardedPlan3D(nx, ny, nz, loopback=8)
+    ref = F.Plan3D(nx, ny, nz)
+    x128 = torch.from_numpy(x).cuda()
+    assert rel(q.diffuse(x128, 1e-3, 0.01, 2).cpu().numpy(), ref.diffuse(x128, 1e-3, 0.01, 2).cpu().numpy()) <= 1e-14
 
 
 def test_sharded_plan_errors():
     with pytest.raises(F.FFTPDEError):
         F.ShardedPlan(100, 64)                           # not a power of two
+    with pytest.raises(F.FFTPDEError) as e:
+        F.ShardedPlan(64, 64, loopback=128)              # P does not divide the axes
+    assert e.value.status == F.ERR_UNSUPPORTED
+    with pytest.raises(F.FFTPDEError) as e:
+        F.ShardedPlan3D(64, 64, 4, loopback=8)           # P does not divide nz
+    assert e.value.status == F.ERR_UNSUPPORTED
     p = F.ShardedPlan(64, 64)
     x = torch.zeros(64, 64, dtype=torch.complex128, device="cuda")
     assert p.lib.fftpde_wave_step(p._h, x.data_ptr(), x.data_ptr(), 1.0, 0.1, 1) == F.ERR_UNSUPPORTED

@@ -103,3 +103,36 @@ def test_slab_diffusion_and_poisson_gloo(world):
     assert np.linalg.norm(u - ref) / np.linalg.norm(ref) <= 1e-12
     refp = O.poisson(src)
     assert np.linalg.norm(pois - refp) / np.linalg.norm(refp) <= 1e-12
+
+
+def _uid_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2412_12308_b200 import fftpde as F
+
+    def draw():
+        if dist.get_rank() != 0:
+            raise AssertionError("only rank 0 draws the NCCL unique id")
+        return bytes(range(128))
+
+    uid = F.broadcast_unique_id(draw)
+    q.put((rank, uid))
+    dist.destroy_process_group()
+
+
+def test_nccl_unique_id_broadcast_gloo():
+    # the host half of fftpde_plan_2d_sharded / _3d_sharded set-up: rank 0 draws the
+    # 128-byte id, every rank receives the same bytes over the process group
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_uid_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got[0] == got[1] == bytes(range(128))

@@ -325,6 +325,14 @@ int main(int argc, char **argv)
         rr_var<D, 4096, 2, true, LN_FWD, 1>(B, B, nullptr, 4096, 4096, 1, t16, tab, "c3 colsFWD");
         rr_var<D, 2048, 4, true, LN_POISSON, 1>(B, B, nullptr, 8192, 2048, 1, t16_2048, tab2048, "c2048 colsPOI");
         rr_var<D, 2048, 2, true, LN_POISSON, 2>(B, B, nullptr, 8192, 2048, 1, t16_2048, tab2048, "c2048 colsPOI");
+        // transposed-spectrum design for C3: W = 2 rows per tile -> 32-byte segments on the T side
+        tpipe_var<D, 4096, 2, TP_MID_T, 1, false>(A, B, Cb, 4096, 4096, 1, t16, "c3 T");
+        tpipe_var<D, 4096, 1, TP_MID_T, 2, false>(A, B, Cb, 4096, 4096, 1, t16, "c3 T");
+        tpipe_var<D, 4096, 2, TP_FWD_T, 1, false>(A, B, nullptr, 4096, 4096, 1, t16, "c3 T");
+        pipe_ref<D, 4096, 2, false, PIPE_DIFFUSE, 1, false>(B, B, nullptr, 4096, 4096, 1, t16, tab, "c3 TrowsDIF");
+        pipe_ref<D, 4096, 1, false, PIPE_DIFFUSE, 2, false>(B, B, nullptr, 4096, 4096, 1, t16, tab, "c3 TrowsDIF");
+        pipe_ref<D, 4096, 1, false, PIPE_DIFFUSE, 2, true>(B, B, nullptr, 4096, 4096, 1, t16, tab, "c3 TrowsDIF");
+        line_var<D, 4096, 16, 1, false, LN_DIFFUSE, 2>(B, B, nullptr, 4096, 4096, 1, t16, tab, "c3 TrowsDIF");
         line_var<D, 4096, 16, 1, false, LN_FWD, 2>(A, B, nullptr, 4096, 4096, 1, t16, tab, "c3 rowsFWD");
         line_var<D, 4096, 16, 1, false, LN_FWD, 3>(A, B, nullptr, 4096, 4096, 1, t16, tab, "c3 rowsFWD");
         line_var<D, 4096, 8, 1, false, LN_FWD, 2>(A, B, nullptr, 4096, 4096, 1, t8, tab, "c3 rowsFWD");
