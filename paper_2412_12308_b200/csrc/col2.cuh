@@ -131,6 +131,8 @@ col2_kernel(Col2Args<T> g, OpTables<T> tab)
     const int64_t col0 = (cid - bidx * g.nblocks) * W;
     const int64_t base = bidx * g.stride + col0;
     const int tid = threadIdx.x;
+    pdl_wait();
+    pdl_trigger();
 
     // ---------------------------------------------------------------- phase A
     // item = (field f, n1); CTA `rank` takes items rank*SLOTS + s + j*CL*SLOTS

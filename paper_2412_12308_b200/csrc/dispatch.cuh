@@ -3,6 +3,8 @@
 #pragma once
 #include <atomic>
 #include <algorithm>
+#include <cstdlib>
+#include <utility>
 #include "kernels.cuh"
 #include "pipe.cuh"
 #include "col2.cuh"
@@ -62,6 +64,40 @@ inline int sm_count()
     return v;
 }
 
+// Launch with programmatic dependent launch (PDL) allowed: the grid may be
+// scheduled while its predecessor on the stream drains; the kernel's pdl_wait()
+// orders its field accesses after the predecessor's completion.  Only kernels
+// that call pdl_wait() before touching field memory go through here.
+// FFTPDE_PDL = bit mask of the launch families that use it (A/B measurements):
+// 1 line passes (pipe / line / small solve), 2 col2, 4 row2d.  Default 5: on
+// B200 PDL gains 3% on C2 (line passes) and 2% on C5 (row2d), while an early
+// launched col2 grid slows C3 by 18% (its clusters are placed while the row
+// pass drains; profiles/r01/pdl_ab.txt), so col2 is launched normally.
+enum PdlFamily { PDL_LINE = 1, PDL_COL2 = 2, PDL_ROW2D = 4 };
+inline bool pdl_enabled(int family = PDL_LINE)
+{
+    static const int mask = [] {
+        const char *e = std::getenv("FFTPDE_PDL");
+        return e ? std::atoi(e) : PDL_LINE | PDL_ROW2D;
+    }();
+    return (mask & family) != 0;
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 template <typename T, int N, bool COLS, int OP>
 cudaError_t pipe_n(const void *in, void *out, PipeArgs args, const void *tw, const OpTables<T> &tab,
                    cudaStream_t st)
@@ -88,8 +124,8 @@ cudaError_t pipe_n(const void *in, void *out, PipeArgs args, const void *tw, con
     const int64_t batch = args.ntiles;                  // caller passes the batch here
     args.ntiles = batch * args.groups;
     const int64_t grid = std::min<int64_t>(args.ntiles, (int64_t)occ * sm_count());
-    k<<<(unsigned)grid, THREADS, smem, st>>>((const C *)in, (C *)out, args, (const C *)tw, tab);
-    return cudaGetLastError();
+    return launch_pdl(k, dim3((unsigned)grid), dim3(THREADS), smem, st, (const C *)in, (C *)out, args, (const C *)tw,
+                      tab);
 }
 
 // ---- occupancy-oriented line pass (line.cuh) ----------------------------------
@@ -114,8 +150,8 @@ cudaError_t line_n(const void *in, void *out, void *out2, int64_t nlines, int64_
     if (e != cudaSuccess) return e;
     LineArgs a{nlines, line_stride, elem_stride, stride, (nlines + W - 1) / W, out2};
     const int64_t grid = batch * a.groups;
-    k<<<(unsigned)grid, W * (N / E), L::BYTES, st>>>((const C *)in, (C *)out, a, (const C *)tw, tab);
-    return cudaGetLastError();
+    return launch_pdl(k, dim3((unsigned)grid), dim3(W * (N / E)), L::BYTES, st, (const C *)in, (C *)out, a,
+                      (const C *)tw, tab);
 }
 
 template <typename T, int N>
@@ -193,9 +229,8 @@ cudaError_t small_op_n(const void *in, void *out, int64_t stride, int64_t batch,
     static SmemOptIn<decltype(k)> opt;
     cudaError_t e = opt(k, L::BYTES);
     if (e != cudaSuccess) return e;
-    k<<<(unsigned)batch, L::THREADS, L::BYTES, st>>>((const C *)in, (C *)out, stride,
-                                                      (const C *)twx, (const C *)twy, tab);
-    return cudaGetLastError();
+    return launch_pdl(k, dim3((unsigned)batch), dim3(L::THREADS), L::BYTES, st, (const C *)in, (C *)out, stride,
+                      (const C *)twx, (const C *)twy, tab);
 }
 
 template <typename T, int N>
@@ -242,13 +277,15 @@ cudaError_t col2_n(Col2Args<T> g, int64_t batch, const OpTables<T> &tab, cudaStr
     cfg.blockDim = dim3(Cfg::NT, 1, 1);
     cfg.dynamicSmemBytes = Cfg::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = Cfg::CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled(PDL_COL2) ? 2 : 1;
     e = cudaLaunchKernelEx(&cfg, k, g, tab);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
@@ -297,11 +334,13 @@ cudaError_t row2d_n(const void *in, void *out, void *out2, int64_t ny, int64_t s
     cfg.blockDim = dim3(G::NT, 1, 1);
     cfg.dynamicSmemBytes = G::BYTES;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     static std::atomic<int> max_clusters{0};
@@ -313,6 +352,7 @@ cudaError_t row2d_n(const void *in, void *out, void *out2, int64_t ny, int64_t s
         if (ncl < 1) ncl = 1;
         max_clusters.store(ncl);
     }
+    cfg.numAttrs = pdl_enabled(PDL_ROW2D) ? 2 : 1;
     const int64_t nrows = ny * batch;
     const int64_t g = std::min<int64_t>(nrows, ncl);          // persistent clusters
     cfg.gridDim = dim3((unsigned)(CL * g), 1, 1);

@@ -190,6 +190,16 @@ template <typename P> __device__ __forceinline__ P *opaque_ptr(P *x)
 
 __device__ __forceinline__ int padidx(int p, int loge) { return p + (p >> loge); }
 
+// Programmatic dependent launch (sm_90+): a pass launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor drains; pdl_wait() blocks until the predecessor grid has completed
+// and its memory is visible (a no-op for a normally launched grid), so every pass
+// calls it before its first access to a field buffer (constant tables may be read
+// before).  pdl_trigger() lets the successor grid launch once every CTA of this
+// grid has triggered or exited.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Exchange buffer of one transform: element p lives at base[pad(p) * STRIDE],
 // pad(p) = p + p / 2^LOGE (one pad slot every E elements).  For an access
 // p0 + d where p0 or d is a multiple of 2^LOGE, pad(p0 + d) = pad(p0) + pad(d),

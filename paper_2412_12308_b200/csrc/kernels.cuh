@@ -150,6 +150,8 @@ small_solve_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type 
         for (int i = tid; i < NX; i += L::THREADS) sa[i] = ta[i];
         for (int i = tid; i < NY; i += L::THREADS) sb[i] = tb[i];
     }
+    pdl_wait();
+    pdl_trigger();
 
     // ---- phase 1: row transforms (forward, or inverse for COL_INV)
     {

@@ -78,6 +78,8 @@ line_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>:
     const LnSync<TPT, COLS> sync{1 + c};
     SmemView<C, S::LOGE, 1> sm{smem + c * L::S};
     const TwL1<N, C, E> twp{tw, t};
+    pdl_wait();
+    pdl_trigger();
 
     C v[E];
     if (active) {
@@ -160,6 +162,8 @@ wave_line_kernel(typename cplx_t<T>::type *U, typename cplx_t<T>::type *V, LineA
     SmemView<C, S::LOGE, 1> sm{smem + c * L::S};
     const TwL1<N, C, E> twp{tw, t};
     auto slot = [&](int e) -> C & { return stash[(t + TPT * e) * W + c]; };
+    pdl_wait();
+    pdl_trigger();
 
     C v[E];
 #pragma unroll

@@ -123,6 +123,7 @@ pipe_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out, P
     TwP twp;
     if constexpr (TWREG) twp.load(tw, t);
     else twp = TwL1<N, C>{tw, t};
+    pdl_wait();
 
     // ring of NBUF tile buffers: tile i lives in slot i % NBUF; the loads of the
     // next NBUF-1 tiles are in flight while tile i is transformed
@@ -136,6 +137,7 @@ pipe_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out, P
     for (int it = 0; tile < a.ntiles; ++it, tile += gridDim.x) {
         const int slot = it % NBUF;
         const int64_t next = tile + (int64_t)(NBUF - 1) * gridDim.x;
+        if (tile + gridDim.x >= a.ntiles) pdl_trigger();   // this CTA's last tile
         if constexpr (NBUF > 1) {
             if (next < a.ntiles) issue(next, (it + NBUF - 1) % NBUF);
             else cp_async_commit();                  // keep the group count uniform

@@ -194,8 +194,10 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
     release_R();
     C nx[16];
     int64_t row = blockIdx.x / CL;
+    pdl_wait();
     if (row < nrows) load_row(row, nx);
     for (; row < nrows; row += ncl) {
+        if (row + ncl >= nrows) pdl_trigger();   // this cluster's last row
         C v[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) v[e] = nx[e];
