@@ -10,6 +10,8 @@
 #include "col2.cuh"
 #include "row2d.cuh"
 #include "line.cuh"
+#include "tmacols.cuh"
+#include <cudaTypedefs.h>
 #ifndef FFTPDE_COL2_MINB
 #define FFTPDE_COL2_MINB 2
 #endif
@@ -176,6 +178,73 @@ cudaError_t rows_n(const void *in, void *out, void *out2, int64_t ny, int64_t st
     return pipe_n<T, N, false, PIPE_FWD>(in, out, a, tw, tab, st);
 }
 
+// ---- TMA column pass (tmacols.cuh): complex128 columns of 256..1024 points ----
+// cuTensorMapEncodeTiled comes from the driver through the runtime's entry-point
+// query (no link-time libcuda dependency); null if unavailable.
+inline PFN_cuTensorMapEncodeTiled_v12000 tma_encoder()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        cudaGetLastError();
+        return (PFN_cuTensorMapEncodeTiled_v12000)f;
+    }();
+    return fn;
+}
+// the field as a 3D tensor of reals {2 nx, ny, batch}; boxes of 2W reals x BOXR rows
+template <typename T>
+bool tma_map(CUtensorMap &m, const void *p, int64_t nx, int64_t ny, int64_t batch, int64_t stride, int W, int boxr)
+{
+    auto enc = tma_encoder();
+    if (!enc) return false;
+    const cuuint64_t esz = 2 * sizeof(T);
+    cuuint64_t dims[3] = {(cuuint64_t)(2 * nx), (cuuint64_t)ny, (cuuint64_t)batch};
+    cuuint64_t strides[2] = {(cuuint64_t)nx * esz, (cuuint64_t)stride * esz};
+    cuuint32_t box[3] = {(cuuint32_t)(2 * W), (cuuint32_t)boxr, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(&m, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+               const_cast<void *>(p), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+template <typename T, int N> struct TmaColPolicy {
+    static constexpr bool ON = sizeof(T) == 8 && N >= 256 && N <= 1024;
+    static constexpr int W = 64 / (2 * (int)sizeof(T));
+};
+// returns cudaErrorNotSupported when the shape or the driver does not allow it (caller falls back)
+template <typename T, int N, int OP>
+cudaError_t tma_cols_n(const void *in, void *out, int64_t nx, int64_t stride, int64_t batch, const void *tw,
+                       const OpTables<T> &tab, cudaStream_t st)
+{
+    using C = typename cplx_t<T>::type;
+    constexpr int W = TmaColPolicy<T, N>::W;
+    using L = TmaColSmem<C, N, W>;
+    if (nx < W || nx % W || batch > (int64_t)1 << 31) return cudaErrorNotSupported;
+    CUtensorMap mi, mo;
+    if (!tma_map<T>(mi, in, nx, N, batch, stride, W, L::BOXR)) return cudaErrorNotSupported;
+    if (in == out) mo = mi;
+    else if (!tma_map<T>(mo, out, nx, N, batch, stride, W, L::BOXR)) return cudaErrorNotSupported;
+    auto k = tma_cols_kernel<T, N, W, OP, 1>;
+    static SmemOptIn<decltype(k)> opt;
+    cudaError_t e = opt(k, L::BYTES);
+    if (e != cudaSuccess) return e;
+    constexpr int THREADS = W * Shape<N>::TPT;
+    static std::atomic<int> per_sm{0};
+    int occ = per_sm.load();
+    if (!occ) {
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, THREADS, L::BYTES);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+        per_sm.store(occ);
+    }
+    TmaColArgs a{nx, nx / W, 0};
+    a.ntiles = batch * a.groups;
+    const int64_t grid = std::min<int64_t>(a.ntiles, (int64_t)occ * sm_count());
+    return launch_pdl(k, dim3((unsigned)grid), dim3(THREADS), L::BYTES, st, mi, mo, a, (const C *)tw, tab);
+}
+
 template <typename T, int N>
 cudaError_t cols_n(const void *in, void *out, int64_t nx, int64_t stride, int64_t batch, int op,
                    const ColTw &ctw, const OpTables<T> &tab, cudaStream_t st)
@@ -192,6 +261,17 @@ cudaError_t cols_n(const void *in, void *out, int64_t nx, int64_t stride, int64_
         }
     }
     const void *tw = ctw.tw;
+    if constexpr (TmaColPolicy<T, N>::ON) {
+        cudaError_t e = cudaErrorNotSupported;
+        switch (op) {
+        case COL_FWD: e = tma_cols_n<T, N, PIPE_FWD>(in, out, nx, stride, batch, tw, tab, st); break;
+        case COL_INV: e = tma_cols_n<T, N, PIPE_INV_SCALED>(in, out, nx, stride, batch, tw, tab, st); break;
+        case COL_POISSON: e = tma_cols_n<T, N, PIPE_POISSON>(in, out, nx, stride, batch, tw, tab, st); break;
+        case COL_DIFFUSE: e = tma_cols_n<T, N, PIPE_DIFFUSE>(in, out, nx, stride, batch, tw, tab, st); break;
+        default: return cudaErrorInvalidValue;
+        }
+        if (e != cudaErrorNotSupported) return e;
+    }
     PipeArgs a{nx, 1, nx, stride, batch, 0, op, nullptr};
     switch (op) {
     case COL_FWD: return pipe_n<T, N, true, PIPE_FWD>(in, out, a, tw, tab, st);

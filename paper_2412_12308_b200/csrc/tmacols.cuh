@@ -1,0 +1,176 @@
+// tmacols.cuh -- column pass with TMA tile movement (sm_100a).
+//
+// The y-pass of a field of rows [b][ny][nx]: W adjacent columns (W * sizeof(C)
+// = 64 bytes) form a tile; a tile of N = ny rows is brought into shared memory
+// by the tensor memory accelerator (cp.async.bulk.tensor, boxes of 256 rows x
+// 64 bytes, 64-byte hardware swizzle, completion counted on an mbarrier) and
+// written back the same way, so no thread issues a strided global access and the
+// 64-byte row segments are gathered / scattered by the copy engine.  Per column
+// (PAPER.md:266-273): forward transform along y (eq:DFT sign +), the k-space
+// multiplier of the solve (eq:SolutionPoisson -1/|k|^2, or solCalorFourier
+// exp(-D|k|^2 dt), with 1/(nx ny) folded in), inverse transform.
+//
+// Persistent CTAs, two tile slots: the TMA load of tile i+1 is in flight while
+// tile i is transformed; a slot doubles as the transform's exchange buffer once
+// its tile is in registers, and holds the results for the TMA store.
+#pragma once
+#include <cuda.h>
+#include <type_traits>
+#include "fft_core.cuh"
+#include "launch.h"
+#include "pipe.cuh"
+
+namespace fftpde {
+
+template <typename C, int N, int W> struct TmaColSmem {
+    static_assert(W * sizeof(C) == 64, "tiles are 64-byte column segments (SWIZZLE_64B)");
+    using PS = PipeSmem<C, N, W, true, 1>;                       // exchange pitch of a line
+    static constexpr int BOXR = N < 256 ? N : 256;                  // rows per TMA box
+    static constexpr int NBOX = N / BOXR;
+    static constexpr size_t DENSE = (size_t)N * 64;
+    static constexpr size_t XCH = (size_t)W * PS::S * sizeof(C);
+    static constexpr size_t SLOT = (((DENSE > XCH ? DENSE : XCH) + 1023) / 1024) * 1024;
+    static constexpr size_t BYTES = 2 * SLOT + 1024 + 64;          // + alignment slack + mbarriers
+};
+
+struct TmaColArgs {
+    int64_t ncols;      // columns per grid (nx)
+    int64_t groups;     // ceil(ncols / W)
+    int64_t ntiles;     // batch * groups
+};
+
+__device__ __forceinline__ uint32_t tma_smem(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tma_mbar_init(uint32_t mbar, uint32_t n)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(n) : "memory");
+}
+__device__ __forceinline__ void tma_mbar_expect(uint32_t mbar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_mbar_wait(uint32_t mbar, uint32_t parity)
+{
+    asm volatile("{\n\t.reg .pred p;\n"
+                 "W%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra W%=;\n}" ::"r"(mbar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap *map, int x, int y, int z, uint32_t mbar)
+{
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(z), "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store3(const CUtensorMap *map, int x, int y, int z, uint32_t src)
+{
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];"
+                 ::"l"(map), "r"(x), "r"(y), "r"(z), "r"(src) : "memory");
+}
+__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tma_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_fence_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// byte offset of row r, 16-byte chunk q of a dense 64-byte-row tile under SWIZZLE_64B
+__device__ __forceinline__ uint32_t swz64(uint32_t o) { return o ^ (((o >> 7) & 3u) << 4); }
+
+template <typename T, int N, int W, int OP, int MINB>
+__global__ void __launch_bounds__(W * Shape<N>::TPT, MINB)
+tma_cols_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, TmaColArgs a,
+                const typename cplx_t<T>::type *__restrict__ tw, OpTables<T> tab)
+{
+    using C = typename cplx_t<T>::type;
+    using S = Shape<N>;
+    using L = TmaColSmem<C, N, W>;
+    constexpr int E = S::E, TPT = S::TPT;
+    constexpr bool TWO = OP == PIPE_POISSON || OP == PIPE_DIFFUSE;
+    constexpr bool INV1 = OP == PIPE_INV_SCALED;
+    static_assert(TPT <= 32 || W <= 15, "one named barrier per line");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned char *base = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const uint32_t mbar0 = tma_smem(base + 2 * L::SLOT);
+
+    const int tid = threadIdx.x;
+    const int c = tid / TPT, t = tid % TPT;
+    const LineSync<TPT> lsync{1 + c};
+    constexpr int X2 = 2 * W;                 // box width in reals
+    auto issue = [&](int64_t tile, int slot) {
+        const int64_t b = tile / a.groups;
+        const int x = (int)((tile - b * a.groups) * X2);
+        const uint32_t mb = mbar0 + 8 * slot;
+        tma_mbar_expect(mb, (uint32_t)L::DENSE);
+        const uint32_t dst = tma_smem(base + slot * L::SLOT);
+#pragma unroll
+        for (int k = 0; k < L::NBOX; ++k) tma_load3(dst + k * L::BOXR * 64, &tin, x, k * L::BOXR, (int)b, mb);
+    };
+
+    TwReg<N, C> twp;                          // a thread's twiddles, loaded once for all its tiles
+    twp.load(tw, t);
+    if (tid == 0) {
+        tma_mbar_init(mbar0, 1);
+        tma_mbar_init(mbar0 + 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tin) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tout) : "memory");
+    }
+    __syncthreads();
+    pdl_wait();
+
+    int64_t tile = blockIdx.x;
+    if (tid == 0 && tile < a.ntiles) issue(tile, 0);
+    for (int it = 0; tile < a.ntiles; ++it, tile += gridDim.x) {
+        const int slot = it & 1;
+        const int64_t next = tile + gridDim.x;
+        if (next >= a.ntiles) pdl_trigger();
+        if (tid == 0 && next < a.ntiles) {
+            tma_wait_read0();                 // the other slot's store has read its smem
+            issue(next, slot ^ 1);
+        }
+        tma_mbar_wait(mbar0 + 8 * slot, (uint32_t)(it >> 1) & 1u);
+        unsigned char *sb = base + slot * L::SLOT;
+        const uint32_t cofs = (uint32_t)(c * sizeof(C));
+        C v[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = *reinterpret_cast<const C *>(sb + swz64((uint32_t)(t + TPT * e) * 64u + cofs));
+        if constexpr (OP == PIPE_INV_SCALED) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = cscale(v[e], tab.scale);
+        }
+        __syncthreads();                      // the tile is in registers: the slot is the exchange buffer
+        SmemView<C, S::LOGE, 1> sm{reinterpret_cast<C *>(sb) + c * L::PS::S};
+        fft_tw<N, INV1>(v, sm, t, twp, lsync);
+        if constexpr (TWO) {
+            const int64_t bb = tile / a.groups;
+            int64_t col = (tile - bb * a.groups) * W + c;
+            if (col >= a.ncols) col = 0;
+            if constexpr (OP == PIPE_POISSON) {
+                const T kxa = tab.kx2[col];
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const T k2 = kxa + __ldg(&tab.ky2[t + TPT * e]);
+                    v[e] = cscale(v[e], k2 == (T)0 ? (T)0 : -tab.scale / k2);   // -1/|k|^2, k = 0 zeroed
+                }
+            } else {
+                const T exa = tab.ex[col];
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = cscale(v[e], exa * __ldg(&tab.ey[t + TPT * e]));
+            }
+            fft_tw<N, true>(v, sm, t, twp, lsync);
+        }
+        __syncthreads();                      // every line is done with the exchange buffer
+#pragma unroll
+        for (int e = 0; e < E; ++e) *reinterpret_cast<C *>(sb + swz64((uint32_t)(t + TPT * e) * 64u + cofs)) = v[e];
+        tma_fence_smem();
+        __syncthreads();
+        if (tid == 0) {
+            const int64_t b = tile / a.groups;
+            const int x = (int)((tile - b * a.groups) * X2);
+            const uint32_t src = tma_smem(sb);
+#pragma unroll
+            for (int k = 0; k < L::NBOX; ++k) tma_store3(&tout, x, k * L::BOXR, (int)b, src + k * L::BOXR * 64);
+            tma_commit();
+        }
+    }
+    if (tid == 0) tma_wait0();
+}
+
+} // namespace fftpde
