@@ -135,10 +135,13 @@ cudaError_t pipe_n(const void *in, void *out, PipeArgs args, const void *tw, con
 // (tools/exp_line.cu, profiles/r01/exp_line.txt); E = 0: use pipe_kernel.
 template <typename T, int N, bool COLS> struct LinePolicy {
     static constexpr bool C64 = sizeof(T) == 4;
-    static constexpr int E = (C64 && N == 512) ? (COLS ? 8 : 16) : 0;
-    static constexpr int W = COLS ? 8 : 4;
-    static constexpr int MINB = COLS ? 3 : 2;
+    // complex64 512-point lines (C4); complex128 1024-point lines (C2): radix 32,
+    // one warp per row, 4 adjacent columns per CTA (tools/exp_e32.cu)
+    static constexpr int E = (C64 && N == 512) ? (COLS ? 8 : 16) : (!C64 && N == 1024) ? 32 : 0;
+    static constexpr int W = C64 ? (COLS ? 8 : 4) : (COLS ? 4 : 1);
+    static constexpr int MINB = C64 ? (COLS ? 3 : 2) : (COLS ? 2 : 4);
 };
+template <int E> inline const void *tw_for(const ColTw &c) { return E == 8 ? c.tw8 : E == 32 ? c.tw32 : c.tw; }
 
 template <typename T, int N, int E, int W, bool COLS, int OP, int MINB>
 cudaError_t line_n(const void *in, void *out, void *out2, int64_t nlines, int64_t line_stride, int64_t elem_stride,
@@ -164,12 +167,14 @@ cudaError_t rows_n(const void *in, void *out, void *out2, int64_t ny, int64_t st
     tab.scale = (T)1;
     using LP = LinePolicy<T, N, false>;
     if constexpr (LP::E > 0) {
-        const void *tw = LP::E == 8 ? ctw.tw8 : ctw.tw;
+        const void *tw = tw_for<LP::E>(ctw);
+        if (tw) {   // (a plan without this radix's table takes the pipe pass)
         if (dir == ROW_INV)
             return line_n<T, N, LP::E, LP::W, false, LN_INV, LP::MINB>(in, out, nullptr, ny, N, 1, stride, batch, tw, tab, st);
         if (dir == ROW_MID)
             return line_n<T, N, LP::E, LP::W, false, LN_MID, LP::MINB>(in, out, out2, ny, N, 1, stride, batch, tw, tab, st);
         return line_n<T, N, LP::E, LP::W, false, LN_FWD, LP::MINB>(in, out, nullptr, ny, N, 1, stride, batch, tw, tab, st);
+        }
     }
     const void *tw = ctw.tw;
     PipeArgs a{ny, N, 1, stride, batch, 0, dir, out2};
@@ -209,9 +214,14 @@ bool tma_map(CUtensorMap &m, const void *p, int64_t nx, int64_t ny, int64_t batc
                const_cast<void *>(p), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+// complex128 columns of 256 / 512 points (radix 16, one CTA per SM); complex64
+// columns of 512 points (radix 32, three CTAs per SM) (tools/exp_tma.cu, exp_e32.cu)
 template <typename T, int N> struct TmaColPolicy {
-    static constexpr bool ON = sizeof(T) == 8 && N >= 256 && N <= 1024;
+    static constexpr bool C64 = sizeof(T) == 4;
+    static constexpr bool ON = C64 ? N == 512 : (N >= 256 && N <= 512);
     static constexpr int W = 64 / (2 * (int)sizeof(T));
+    static constexpr int E = C64 ? 32 : 16;
+    static constexpr int MINB = C64 ? 3 : 1;
 };
 // returns cudaErrorNotSupported when the shape or the driver does not allow it (caller falls back)
 template <typename T, int N, int OP>
@@ -219,18 +229,19 @@ cudaError_t tma_cols_n(const void *in, void *out, int64_t nx, int64_t stride, in
                        const OpTables<T> &tab, cudaStream_t st)
 {
     using C = typename cplx_t<T>::type;
-    constexpr int W = TmaColPolicy<T, N>::W;
-    using L = TmaColSmem<C, N, W>;
+    using TP = TmaColPolicy<T, N>;
+    constexpr int W = TP::W;
+    using L = TmaColSmem<C, N, W, TP::E>;
     if (nx < W || nx % W || batch > (int64_t)1 << 31) return cudaErrorNotSupported;
     CUtensorMap mi, mo;
     if (!tma_map<T>(mi, in, nx, N, batch, stride, W, L::BOXR)) return cudaErrorNotSupported;
     if (in == out) mo = mi;
     else if (!tma_map<T>(mo, out, nx, N, batch, stride, W, L::BOXR)) return cudaErrorNotSupported;
-    auto k = tma_cols_kernel<T, N, W, OP, 1>;
+    auto k = tma_cols_kernel<T, N, W, OP, TP::MINB, TP::E>;
     static SmemOptIn<decltype(k)> opt;
     cudaError_t e = opt(k, L::BYTES);
     if (e != cudaSuccess) return e;
-    constexpr int THREADS = W * Shape<N>::TPT;
+    constexpr int THREADS = W * Shape<N, TP::E>::TPT;
     static std::atomic<int> per_sm{0};
     int occ = per_sm.load();
     if (!occ) {
@@ -250,20 +261,11 @@ cudaError_t cols_n(const void *in, void *out, int64_t nx, int64_t stride, int64_
                    const ColTw &ctw, const OpTables<T> &tab, cudaStream_t st)
 {
     using LP = LinePolicy<T, N, true>;
-    if constexpr (LP::E > 0) {
-        const void *tw = LP::E == 8 ? ctw.tw8 : ctw.tw;
-        switch (op) {
-        case COL_FWD: return line_n<T, N, LP::E, LP::W, true, LN_FWD, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st);
-        case COL_INV: return line_n<T, N, LP::E, LP::W, true, LN_INV_SCALED, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st);
-        case COL_POISSON: return line_n<T, N, LP::E, LP::W, true, LN_POISSON, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st);
-        case COL_DIFFUSE: return line_n<T, N, LP::E, LP::W, true, LN_DIFFUSE, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st);
-        default: return cudaErrorInvalidValue;
-        }
-    }
-    const void *tw = ctw.tw;
     if constexpr (TmaColPolicy<T, N>::ON) {
+        using TP = TmaColPolicy<T, N>;
+        const void *tw = tw_for<TP::E>(ctw);
         cudaError_t e = cudaErrorNotSupported;
-        switch (op) {
+        if (tw) switch (op) {
         case COL_FWD: e = tma_cols_n<T, N, PIPE_FWD>(in, out, nx, stride, batch, tw, tab, st); break;
         case COL_INV: e = tma_cols_n<T, N, PIPE_INV_SCALED>(in, out, nx, stride, batch, tw, tab, st); break;
         case COL_POISSON: e = tma_cols_n<T, N, PIPE_POISSON>(in, out, nx, stride, batch, tw, tab, st); break;
@@ -272,6 +274,17 @@ cudaError_t cols_n(const void *in, void *out, int64_t nx, int64_t stride, int64_
         }
         if (e != cudaErrorNotSupported) return e;
     }
+    if constexpr (LP::E > 0) {
+        const void *tw = tw_for<LP::E>(ctw);
+        if (tw) switch (op) {
+        case COL_FWD: return line_n<T, N, LP::E, LP::W, true, LN_FWD, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st);
+        case COL_INV: return line_n<T, N, LP::E, LP::W, true, LN_INV_SCALED, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st);
+        case COL_POISSON: return line_n<T, N, LP::E, LP::W, true, LN_POISSON, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st);
+        case COL_DIFFUSE: return line_n<T, N, LP::E, LP::W, true, LN_DIFFUSE, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st);
+        default: return cudaErrorInvalidValue;
+        }
+    }
+    const void *tw = ctw.tw;
     PipeArgs a{nx, 1, nx, stride, batch, 0, op, nullptr};
     switch (op) {
     case COL_FWD: return pipe_n<T, N, true, PIPE_FWD>(in, out, a, tw, tab, st);

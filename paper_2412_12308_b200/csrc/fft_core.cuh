@@ -124,12 +124,39 @@ template <bool INV, typename C> __device__ __forceinline__ void dft16(C (&v)[16]
     for (int k = 0; k < 16; ++k) v[k] = o[k];
 }
 
+// radix-32 as 2 x 16: n = 16 n1 + n2, k = k1 + 2 k2, internal twiddle w32^{n2 k1}
+template <bool INV, typename C> __device__ __forceinline__ void dft32(C (&v)[32])
+{
+    using T = decltype(v[0].x);
+    // cos / sin (2 pi j / 32), j = 0..8
+    constexpr double cs[9] = {1.0, 0.98078528040323044912618223613424, 0.92387953251128675612818318939679,
+                              0.83146961230254523707878837761791, 0.70710678118654752440084436210485,
+                              0.55557023301960222474283081394853, 0.38268343236508977172845998403040,
+                              0.19509032201612826784828486847702, 0.0};
+#pragma unroll
+    for (int n2 = 0; n2 < 16; ++n2) dft2(v[n2], v[n2 + 16]);       // Y[n2][k1] at v[n2 + 16 k1]
+#pragma unroll
+    for (int n2 = 1; n2 < 16; ++n2) {                               // Y[n2][1] *= w32^{n2}
+        const T c = (T)(n2 <= 8 ? cs[n2] : -cs[16 - n2]);
+        const T s = (T)(n2 <= 8 ? cs[8 - n2] : cs[n2 - 8]);
+        v[16 + n2] = cmulw<INV>(v[16 + n2], C{c, s});
+    }
+    C a[16], b[16];
+#pragma unroll
+    for (int n2 = 0; n2 < 16; ++n2) { a[n2] = v[n2]; b[n2] = v[16 + n2]; }
+    dft16<INV>(a);                                                   // X[2 k2]
+    dft16<INV>(b);                                                   // X[1 + 2 k2]
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) { v[2 * k2] = a[k2]; v[2 * k2 + 1] = b[k2]; }
+}
+
 template <int R, bool INV, typename C> __device__ __forceinline__ void dft_r(C (&v)[R])
 {
     if constexpr (R == 2) dft2(v[0], v[1]);
     else if constexpr (R == 4) dft4<INV>(v[0], v[1], v[2], v[3]);
     else if constexpr (R == 8) dft8<INV>(v);
     else if constexpr (R == 16) dft16<INV>(v);
+    else if constexpr (R == 32) dft32<INV>(v);
     else static_assert(R == 1, "radix");
 }
 
@@ -139,7 +166,7 @@ template <int N_, int EMAX = 16> struct Shape {
     static constexpr int N = N_;
     static constexpr int E = N_ < EMAX ? N_ : EMAX;    // elements per thread (the radix)
     static constexpr int TPT = N_ / E;                   // threads per transform
-    static constexpr int LOGE = E == 16 ? 4 : E == 8 ? 3 : E == 4 ? 2 : E == 2 ? 1 : 0;
+    static constexpr int LOGE = E == 32 ? 5 : E == 16 ? 4 : E == 8 ? 3 : E == 4 ? 2 : E == 2 ? 1 : 0;
     // padded smem index: one pad slot every E elements (conflict-free stage-1 scatter)
     static constexpr int PADDED = N_ + (N_ >> LOGE);
     // number of full radix-E stages before the last one, and the last radix

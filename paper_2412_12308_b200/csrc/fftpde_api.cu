@@ -35,7 +35,7 @@ struct fftpde_plan_s {
     unsigned char *ws = nullptr;
     size_t ws_bytes = 0;
     // workspace offsets (bytes)
-    size_t o_twx = 0, o_twy = 0, o_twx8 = 0, o_twy8 = 0, o_kx = 0, o_ky = 0, o_kx2 = 0, o_ky2 = 0, o_ex = 0, o_ey = 0, o_wc = 0, o_ws1 = 0, o_ws2 = 0;
+    size_t o_twx = 0, o_twy = 0, o_twx8 = 0, o_twy8 = 0, o_twx32 = 0, o_twy32 = 0, o_kx = 0, o_ky = 0, o_kx2 = 0, o_ky2 = 0, o_ex = 0, o_ey = 0, o_wc = 0, o_ws1 = 0, o_ws2 = 0;
     size_t o_twP = 0, o_twQ = 0, o_twN = 0;   // two-level column pass tables (P, Q > 0)
     size_t o_scr = 0;                          // scratch: row spectra of 2 fields (multi-step solves)
     int64_t colP = 0, colQ = 0;
@@ -48,6 +48,7 @@ struct fftpde_plan_s {
     // host tables (fp64)
     std::vector<double> twx, twy;   // interleaved re, im (radix-16 stage tables)
     std::vector<double> twx8, twy8; // radix-8 stage tables (line_kernel E = 8)
+    std::vector<double> twx32, twy32; // radix-32 stage tables
     std::vector<double> kx2, ky2;
     std::vector<double> kx, ky;     // signed 2 pi fold(a)/L (odd operators)
     bool diff_valid = false;
@@ -348,7 +349,8 @@ template <typename T> struct Passes {
     const void *twy() const { return p->ws + p->o_twy; }
     ColTw rtw() const
     {
-        return ColTw{twx(), p->ws + p->o_rtwP, p->ws + p->o_rtwQ, p->ws + p->o_rtwN, p->ws + p->o_twx8};
+        return ColTw{twx(), p->ws + p->o_rtwP, p->ws + p->o_rtwQ, p->ws + p->o_rtwN, p->ws + p->o_twx8,
+                     p->ws + p->o_twx32};
     }
     cudaError_t rows(const void *in, void *out, int inverse)
     {
@@ -375,7 +377,8 @@ template <typename T> struct Passes {
     }
     ColTw ctw() const
     {
-        return ColTw{twy(), p->ws + p->o_twP, p->ws + p->o_twQ, p->ws + p->o_twN, p->ws + p->o_twy8};
+        return ColTw{twy(), p->ws + p->o_twP, p->ws + p->o_twQ, p->ws + p->o_twN, p->ws + p->o_twy8,
+                     p->ws + p->o_twy32};
     }
     cudaError_t cols(const void *in, void *out, int op)
     {
@@ -1088,6 +1091,8 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     build_twiddles(ny, p->twy);
     build_twiddles(nx, p->twx8, 8);
     build_twiddles(ny, p->twy8, 8);
+    build_twiddles(nx, p->twx32, 32);
+    build_twiddles(ny, p->twy32, 32);
     build_k2(nx, Lx, p->kx2);
     build_k2(ny, Ly, p->ky2);
     build_k(nx, Lx, p->kx);
@@ -1112,6 +1117,8 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     p->o_twy = take(p->twy.size() / 2 * ec);
     p->o_twx8 = take(p->twx8.size() / 2 * ec);
     p->o_twy8 = take(p->twy8.size() / 2 * ec);
+    p->o_twx32 = take(p->twx32.size() / 2 * ec);
+    p->o_twy32 = take(p->twy32.size() / 2 * ec);
     p->o_kx2 = take((size_t)nx * er);
     p->o_ky2 = take((size_t)ny * er);
     p->o_kx = take((size_t)nx * er);
@@ -1172,6 +1179,8 @@ fftpde_status fftpde_set_workspace(fftpde_plan plan, void *dev_ptr, size_t bytes
     }
     if (s == FFTPDE_OK) s = upload(plan, plan->o_twx8, plan->twx8);
     if (s == FFTPDE_OK) s = upload(plan, plan->o_twy8, plan->twy8);
+    if (s == FFTPDE_OK) s = upload(plan, plan->o_twx32, plan->twx32);
+    if (s == FFTPDE_OK) s = upload(plan, plan->o_twy32, plan->twy32);
     if (s == FFTPDE_OK && plan->rowP) {
         s = upload(plan, plan->o_rtwP, plan->rtwP);
         if (s == FFTPDE_OK) s = upload(plan, plan->o_rtwQ, plan->rtwQ);
@@ -1381,7 +1390,8 @@ fftpde_status fftpde_cols_slab(fftpde_plan p, const void *in, void *out, int64_t
     DeviceGuard g(p->device);
     if (!g.ok) return FFTPDE_ERR_CUDA;
     cudaError_t e;
-    const ColTw ctw{p->ws + p->o_twy, p->ws + p->o_twP, p->ws + p->o_twQ, p->ws + p->o_twN, p->ws + p->o_twy8};
+    const ColTw ctw{p->ws + p->o_twy, p->ws + p->o_twP, p->ws + p->o_twQ, p->ws + p->o_twN, p->ws + p->o_twy8,
+                    p->ws + p->o_twy32};
     auto run = [&](auto tag) {
         using T = decltype(tag);
         OpTables<T> t = tables<T>(p);

@@ -44,6 +44,7 @@ struct ColTw {
     const void *tw;      // stage table of the axis (radix 16)
     const void *twP, *twQ, *twN;
     const void *tw8;     // stage table of the axis (radix 8, line_kernel E = 8)
+    const void *tw32 = nullptr;   // stage table of the axis (radix 32)
 };
 
 // Split ny = P * Q used by the two-level column pass (P = Q = 0: not used).

@@ -19,12 +19,13 @@
 #include "fft_core.cuh"
 #include "launch.h"
 #include "pipe.cuh"
+#include "line.cuh"
 
 namespace fftpde {
 
-template <typename C, int N, int W> struct TmaColSmem {
+template <typename C, int N, int W, int E = 16> struct TmaColSmem {
     static_assert(W * sizeof(C) == 64, "tiles are 64-byte column segments (SWIZZLE_64B)");
-    using PS = PipeSmem<C, N, W, true, 1>;                       // exchange pitch of a line
+    using PS = LineSmem<C, N, E, W, true>;                       // exchange pitch of a line
     static constexpr int BOXR = N < 256 ? N : 256;                  // rows per TMA box
     static constexpr int NBOX = N / BOXR;
     static constexpr size_t DENSE = (size_t)N * 64;
@@ -73,14 +74,14 @@ __device__ __forceinline__ void tma_fence_smem() { asm volatile("fence.proxy.asy
 // byte offset of row r, 16-byte chunk q of a dense 64-byte-row tile under SWIZZLE_64B
 __device__ __forceinline__ uint32_t swz64(uint32_t o) { return o ^ (((o >> 7) & 3u) << 4); }
 
-template <typename T, int N, int W, int OP, int MINB>
-__global__ void __launch_bounds__(W * Shape<N>::TPT, MINB)
+template <typename T, int N, int W, int OP, int MINB, int EX = 16>
+__global__ void __launch_bounds__(W * Shape<N, EX>::TPT, MINB)
 tma_cols_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, TmaColArgs a,
                 const typename cplx_t<T>::type *__restrict__ tw, OpTables<T> tab)
 {
     using C = typename cplx_t<T>::type;
-    using S = Shape<N>;
-    using L = TmaColSmem<C, N, W>;
+    using S = Shape<N, EX>;
+    using L = TmaColSmem<C, N, W, EX>;
     constexpr int E = S::E, TPT = S::TPT;
     constexpr bool TWO = OP == PIPE_POISSON || OP == PIPE_DIFFUSE;
     constexpr bool INV1 = OP == PIPE_INV_SCALED;
@@ -103,8 +104,10 @@ tma_cols_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__
         for (int k = 0; k < L::NBOX; ++k) tma_load3(dst + k * L::BOXR * 64, &tin, x, k * L::BOXR, (int)b, mb);
     };
 
-    TwReg<N, C> twp;                          // a thread's twiddles, loaded once for all its tiles
-    twp.load(tw, t);
+    using TwP = std::conditional_t<(EX > 16), TwL1<N, C, EX>, TwReg<N, C, EX>>;   // radix 32: no room for TwReg
+    TwP twp;
+    if constexpr (EX > 16) twp = TwP{tw, t};
+    else twp.load(tw, t);
     if (tid == 0) {
         tma_mbar_init(mbar0, 1);
         tma_mbar_init(mbar0 + 8, 1);
@@ -137,7 +140,7 @@ tma_cols_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__
         }
         __syncthreads();                      // the tile is in registers: the slot is the exchange buffer
         SmemView<C, S::LOGE, 1> sm{reinterpret_cast<C *>(sb) + c * L::PS::S};
-        fft_tw<N, INV1>(v, sm, t, twp, lsync);
+        fft_tw<N, INV1, EX>(v, sm, t, twp, lsync);
         if constexpr (TWO) {
             const int64_t bb = tile / a.groups;
             int64_t col = (tile - bb * a.groups) * W + c;
@@ -154,7 +157,7 @@ tma_cols_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__
 #pragma unroll
                 for (int e = 0; e < E; ++e) v[e] = cscale(v[e], exa * __ldg(&tab.ey[t + TPT * e]));
             }
-            fft_tw<N, true>(v, sm, t, twp, lsync);
+            fft_tw<N, true, EX>(v, sm, t, twp, lsync);
         }
         __syncthreads();                      // every line is done with the exchange buffer
 #pragma unroll
