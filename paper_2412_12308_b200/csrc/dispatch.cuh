@@ -201,7 +201,8 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tma_encoder()
 }
 // the field as a 3D tensor of reals {2 nx, ny, batch}; boxes of 2W reals x BOXR rows
 template <typename T>
-bool tma_map(CUtensorMap &m, const void *p, int64_t nx, int64_t ny, int64_t batch, int64_t stride, int W, int boxr)
+bool tma_map(CUtensorMap &m, const void *p, int64_t nx, int64_t ny, int64_t batch, int64_t stride, int W, int boxr,
+             CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_64B, CUtensorMapL2promotion prom = CU_TENSOR_MAP_L2_PROMOTION_L2_128B)
 {
     auto enc = tma_encoder();
     if (!enc) return false;
@@ -211,8 +212,8 @@ bool tma_map(CUtensorMap &m, const void *p, int64_t nx, int64_t ny, int64_t batc
     cuuint32_t box[3] = {(cuuint32_t)(2 * W), (cuuint32_t)boxr, 1};
     cuuint32_t es[3] = {1, 1, 1};
     return enc(&m, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
-               const_cast<void *>(p), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+               const_cast<void *>(p), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, prom,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 // complex128 columns of 256 / 512 points (radix 16, one CTA per SM); complex64
 // columns of 512 points (radix 32, three CTAs per SM) (tools/exp_tma.cu, exp_e32.cu)
@@ -509,12 +510,54 @@ cudaError_t launch_cols(int64_t ny, const void *in, void *out, int64_t nx, int64
     }
 }
 
+// Wave column pass on cluster pairs with TMA (tmacols.cuh, tools/exp_wave.cu):
+// complex128 columns of 2048 / 4096 points, radix 32; cudaErrorNotSupported
+// when the driver's tensor-map encoder is unavailable (the caller falls back).
+template <typename T, int N>
+cudaError_t tma_wave2_n(void *U, void *V, int64_t nx, int64_t stride, int64_t batch, const void *tw,
+                        const OpTables<T> &tab, cudaStream_t st)
+{
+    using C = typename cplx_t<T>::type;
+    constexpr int EX = 32;
+    using L = TmaWave2Smem<C, N, EX>;
+    if (batch > (int64_t)1 << 31 || nx * batch > (int64_t)1 << 30) return cudaErrorNotSupported;
+    CUtensorMap mu, mv;
+    if (!tma_map<T>(mu, U, nx, N, batch, stride, 1, L::BOXR, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) ||
+        !tma_map<T>(mv, V, nx, N, batch, stride, 1, L::BOXR, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
+        return cudaErrorNotSupported;
+    auto k = tma_wave2_cols_kernel<T, N, EX, 1>;
+    static SmemOptIn<decltype(k)> opt;
+    cudaError_t e = opt(k, L::BYTES);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * nx * batch), 1, 1);
+    cfg.blockDim = dim3(Shape<N, EX>::TPT, 1, 1);
+    cfg.dynamicSmemBytes = L::BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled(PDL_COL2) ? 2 : 1;
+    e = cudaLaunchKernelEx(&cfg, k, mu, mv, nx, (const C *)tw, tab);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_wave_cols(int64_t ny, void *U, void *V, int64_t nx, int64_t stride,
                              int64_t batch, const ColTw &ctw, const OpTables<T> &tab,
                              cudaStream_t st)
 {
     using C = typename cplx_t<T>::type;
+    if (sizeof(T) == 8 && (ny == 2048 || ny == 4096) && ctw.tw32) {
+        const cudaError_t e = ny == 2048 ? tma_wave2_n<T, 2048>(U, V, nx, stride, batch, ctw.tw32, tab, st)
+                                         : tma_wave2_n<T, 4096>(U, V, nx, stride, batch, ctw.tw32, tab, st);
+        if (e != cudaErrorNotSupported) return e;
+    }
     int64_t P = 0, Q = 0;
     col2_split(ny, nx, (int)sizeof(C), P, Q);
     if (P) {

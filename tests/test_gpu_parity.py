@@ -230,6 +230,19 @@ def test_wave_shapes_reversal(dtype):
     assert rel(host(u), u0) <= 10 * TOL[dtype]
 
 
+@pytest.mark.parametrize("nx,ny,batch", [(8, 2048, 2), (16, 4096, 1), (2, 4096, 3)])
+def test_wave_long_columns_batched_vs_stepped_oracle(nx, ny, batch):
+    # 2048 / 4096-point columns: the cluster-pair TMA wave pass (one column of
+    # U and V per CTA pair, 16-byte boxes), batched and narrow grids
+    u0 = noise((batch, ny, nx), 41)
+    v0 = noise((batch, ny, nx), 42)
+    p = F.Plan(nx, ny, batch=batch, Lx=0.8, Ly=2.0)
+    u, v = dev(u0), dev(v0)
+    p.wave_step(u, v, 1.3, 2e-3, 4)
+    uo, vo = O.wave(u0, v0, 1.3, 2e-3, 4, 0.8, 2.0)
+    assert rel(host(u), uo) <= 1e-12 and rel(host(v), vo) <= 1e-12
+
+
 def test_wave_zero_speed_and_zero_steps():
     ny, nx = 32, 32
     u0, v0 = noise((ny, nx), 31), noise((ny, nx), 32)
