@@ -149,8 +149,12 @@ class Plan:
 
     # -- plumbing -----------------------------------------------------------------
     def _bind_stream(self):
-        s = torch.cuda.current_stream(self.device).cuda_stream
-        _check(self.lib.fftpde_set_stream(self._h, s), "fftpde_set_stream")
+        # the raw cudaStream_t of torch's current stream; the library is told only
+        # when it changes (a per-call set_stream would cost host time per solve)
+        s = torch._C._cuda_getCurrentRawStream(self.device.index)
+        if s != getattr(self, "_stream", None):
+            _check(self.lib.fftpde_set_stream(self._h, s), "fftpde_set_stream")
+            self._stream = s
 
     def close(self):
         if getattr(self, "_h", None):

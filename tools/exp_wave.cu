@@ -188,7 +188,7 @@ int main(int argc, char **argv)
     cudaMemcpy(U, h.data(), cnt * 16, cudaMemcpyHostToDevice); cudaMemcpy(V, g.data(), cnt * 16, cudaMemcpyHostToDevice);
     cudaMemcpy(U2, h.data(), cnt * 16, cudaMemcpyHostToDevice); cudaMemcpy(V2, g.data(), cnt * 16, cudaMemcpyHostToDevice);
     OpTables<double> tab = make_tab<double>(n, n);
-    void *t16 = upload_tw<double2>(n, 16), *t32 = upload_tw<double2>(n, 32);
+    void *t16 = upload_tw<double2>(n, 16), *t32 = upload_tw<double2>(n, 32), *t8 = upload_tw<double2>(n, 8);
     {   // reference: col_wave_kernel (single CTA per column, radix 16)
         using WS = WaveSmem<double2, 4096, 1>;
         auto k = col_wave_kernel<double, 4096, 1>;
@@ -210,7 +210,13 @@ int main(int argc, char **argv)
     run_tma_wave2<32, 1>(U2, V2, n, t32, tab, "", false);
     cudaDeviceSynchronize();
     printf("TMA wave2 E32 vs col_wave: U %.3e V %.3e %s\n", maxrel(U2, U, cnt), maxrel(V2, V, cnt), cudaGetErrorString(cudaGetLastError()));
+    cudaMemcpy(U2, h.data(), cnt * 16, cudaMemcpyHostToDevice); cudaMemcpy(V2, g.data(), cnt * 16, cudaMemcpyHostToDevice);
+    run_tma_wave2<8, 2>(U2, V2, n, t8, tab, "", false);
+    cudaDeviceSynchronize();
+    printf("TMA wave2 E8 vs col_wave: U %.3e V %.3e %s\n", maxrel(U2, U, cnt), maxrel(V2, V, cnt), cudaGetErrorString(cudaGetLastError()));
     run_tma_wave2<16, 2>(U, V, n, t16, tab, "c3", true);
+    run_tma_wave2<8, 2>(U, V, n, t8, tab, "c3", true);
+    run_tma_wave2<8, 3>(U, V, n, t8, tab, "c3", true);
     run_tma_wave2<16, 3>(U, V, n, t16, tab, "c3", true);
     run_tma_wave2<16, 1>(U, V, n, t16, tab, "c3", true);
     run_tma_wave2<32, 1>(U, V, n, t32, tab, "c3", true);
