@@ -88,7 +88,9 @@ tma_cols_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__
     constexpr bool INV1 = OP == PIPE_INV_SCALED;
     static_assert(TPT <= 32 || W <= 15, "one named barrier per line");
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    unsigned char *base = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // aligned by an offset from the __shared__ array (keeps the shared address space:
+    // LDS/STS, not generic loads and stores)
+    unsigned char *base = smem_raw + ((1024u - (tma_smem(smem_raw) & 1023u)) & 1023u);
     const uint32_t mbar0 = tma_smem(base + 2 * L::SLOT);
 
     const int tid = threadIdx.x;
@@ -209,7 +211,7 @@ tma_wave_cols_kernel(const __grid_constant__ CUtensorMap mu, const __grid_consta
     using L = TmaWaveSmem<C, N, EX>;
     constexpr int E = S::E, TPT = S::TPT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    unsigned char *base = (unsigned char *)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+    unsigned char *base = smem_raw + ((128u - (tma_smem(smem_raw) & 127u)) & 127u);
     const uint32_t mbar = tma_smem(base + 2 * L::LINE);
     const int tid = threadIdx.x;
     const int f = tid / TPT, t = tid % TPT;               // field (0: U, 1: V), thread of its line
@@ -319,7 +321,7 @@ tma_wave2_cols_kernel(const __grid_constant__ CUtensorMap mu, const __grid_const
     using L = TmaWave2Smem<C, N, EX>;
     constexpr int E = S::E, TPT = S::TPT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    unsigned char *base = (unsigned char *)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+    unsigned char *base = smem_raw + ((128u - (tma_smem(smem_raw) & 127u)) & 127u);
     C *line = reinterpret_cast<C *>(base);
     const uint32_t mbar = tma_smem(base + L::LINE);
     const int t = threadIdx.x;

@@ -87,9 +87,12 @@ def test_forward_inverse_every_length_both_axes(dtype, n):
         assert rel(xb, O.fft2(Xo, inverse=True)) <= TOL[dtype], (ny, nx)
 
 
-@pytest.mark.parametrize("dtype", [C128, C64])
-def test_in_place_and_strided_batch(dtype):
-    ny, nx, B = 128, 256, 4
+@pytest.mark.parametrize("dtype,ny,nx", [(C128, 128, 256), (C64, 128, 256),
+                                         (C128, 256, 64), (C128, 512, 32), (C128, 1024, 16), (C64, 512, 64)])
+def test_in_place_and_strided_batch(dtype, ny, nx):
+    # ny = 256 / 512 (c128) and 512 (c64): the TMA column pass (3D tensor maps with
+    # the batch stride); ny = 1024 (c128): the radix-32 column pass
+    B = 4
     p = F.Plan(nx, ny, batch=B, dtype=dtype)
     x = noise((B, ny, nx), 7, dtype)
     t = dev(x, dtype)

@@ -34,12 +34,14 @@ def classify(name):
         return "small_solve"
     if base in ("row2d_kernel", "rc_rows_kernel"):
         return "row_pass"
-    if base in ("wave_line_kernel", "col_wave_kernel"):
+    if base in ("wave_line_kernel", "col_wave_kernel", "tma_wave_cols_kernel", "tma_wave2_cols_kernel"):
         return "wave_col_pass"
     if base in ("col2_kernel", "col2_phase_kernel"):
         return "wave_col_pass" if len(a) > 3 and a[3] == "4" else "col_pass"
     if base == "pipe_kernel":            # <T, N, W, COLS, OP, ...>
         return "col_pass" if len(a) > 3 and a[3] in ("1", "true") else "row_pass"
+    if base == "tma_cols_kernel":
+        return "col_pass"
     if base == "line_kernel":            # <T, N, E, W, COLS, OP, MINB>
         return "col_pass" if len(a) > 4 and a[4] in ("1", "true") else "row_pass"
     if base in ("kop_kernel", "src_kernel", "rk4_kernel", "mean_kernel"):
