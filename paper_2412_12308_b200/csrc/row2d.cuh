@@ -91,7 +91,11 @@ template <typename C, int P, int Q, int CL> struct Row2dGeom {
     static constexpr int RE = QB * (P + 1) > PA * (Q + 1) ? QB * (P + 1) : PA * (Q + 1);
     // per-CTA twiddle slices (inter-phase w_N^{n1 k1} = S1 S2 for the CTA's n1,
     // and = U1 U2 for the CTA's k1): PA*(16 + Q/16) + QB*(16 + P/16) entries
-    static constexpr int TWE = PA * (16 + Q / 16) + QB * (16 + P / 16);
+    // slice pitches padded by one element: lanes of a warp hold consecutive items
+    // and read the same column, so an unpadded power-of-two pitch would put them
+    // all on the same banks
+    static constexpr int A1 = 17, A2 = Q / 16 + 1, B1 = 17, B2 = P / 16 + 1;
+    static constexpr int TWE = PA * (A1 + A2) + QB * (B1 + B2);
     static constexpr size_t BYTES = (size_t)(XE + RE + TWE) * sizeof(C) + 16;   // + mbarrier
     static_assert(NT == QB * TB, "thread counts of the phases must agree");
     static_assert(PA >= 1 && QB >= 1, "cluster too large for the split");
@@ -117,11 +121,11 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *X = reinterpret_cast<C *>(smem_raw);
     C *R = X + G::XE;
-    C *TWA1 = R + G::RE;                    // [PA][16]
-    C *TWA2 = TWA1 + PA * 16;               // [PA][Q/16]
-    C *TWB1 = TWA2 + PA * (Q / 16);         // [QB][16]
-    C *TWB2 = TWB1 + QB * 16;               // [QB][P/16]
-    const uint32_t mbar = smem_addr(TWB2 + QB * (P / 16));
+    C *TWA1 = R + G::RE;                    // [PA][16]    (pitch A1)
+    C *TWA2 = TWA1 + PA * G::A1;            // [PA][Q/16]  (pitch A2)
+    C *TWB1 = TWA2 + PA * G::A2;            // [QB][16]    (pitch B1)
+    C *TWB2 = TWB1 + QB * G::B1;            // [QB][P/16]  (pitch B2)
+    const uint32_t mbar = smem_addr(TWB2 + QB * G::B2);
     const uint32_t rank = cl_rank();
     const int tid = threadIdx.x;
     // phase A layout: item ia (n1 = rank PA + ia) fastest across lanes
@@ -139,10 +143,12 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
     // twiddle slices of this CTA -> smem (once)
     {
         const C *S1 = twS, *S2 = twS + P * 16, *U1 = S2 + P * (Q / 16), *U2 = U1 + Q * 16;
-        for (int i = tid; i < PA * 16; i += NT) TWA1[i] = S1[(int)rank * PA * 16 + i];
-        for (int i = tid; i < PA * (Q / 16); i += NT) TWA2[i] = S2[(int)rank * PA * (Q / 16) + i];
-        for (int i = tid; i < QB * 16; i += NT) TWB1[i] = U1[(int)rank * QB * 16 + i];
-        for (int i = tid; i < QB * (P / 16); i += NT) TWB2[i] = U2[(int)rank * QB * (P / 16) + i];
+        for (int i = tid; i < PA * 16; i += NT) TWA1[(i / 16) * G::A1 + i % 16] = S1[(int)rank * PA * 16 + i];
+        for (int i = tid; i < PA * (Q / 16); i += NT)
+            TWA2[(i / (Q / 16)) * G::A2 + i % (Q / 16)] = S2[(int)rank * PA * (Q / 16) + i];
+        for (int i = tid; i < QB * 16; i += NT) TWB1[(i / 16) * G::B1 + i % 16] = U1[(int)rank * QB * 16 + i];
+        for (int i = tid; i < QB * (P / 16); i += NT)
+            TWB2[(i / (P / 16)) * G::B2 + i % (P / 16)] = U2[(int)rank * QB * (P / 16) + i];
     }
     if (tid == 0) {
         mbar_init(mbar, 1);
@@ -153,11 +159,11 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
     cl_wait_acquire();                       // every CTA's mbarrier is initialised
     uint32_t phase = 0;
     auto twA = [&](int k) -> C {             // w_N^{n1 k}, n1 = this thread's phase-A item
-        const C a = TWA1[ia * 16 + (k & 15)], b = TWA2[ia * (Q / 16) + (k >> 4)];
+        const C a = TWA1[ia * G::A1 + (k & 15)], b = TWA2[ia * G::A2 + (k >> 4)];
         return C{a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
     };
     auto twB = [&](int n) -> C {             // w_N^{n k1}, k1 = this thread's phase-B item
-        const C a = TWB1[jb * 16 + (n & 15)], b = TWB2[jb * (P / 16) + (n >> 4)];
+        const C a = TWB1[jb * G::B1 + (n & 15)], b = TWB2[jb * G::B2 + (n >> 4)];
         return C{a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
     };
     auto row_ptr = [&](const C *base, int64_t row) -> const C * {
