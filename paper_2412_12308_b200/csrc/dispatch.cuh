@@ -426,12 +426,18 @@ cudaError_t row2d_n(const void *in, void *out, void *out2, int64_t ny, int64_t s
                     const ColTw &tw, cudaStream_t st)
 {
     using C = typename cplx_t<T>::type;
-    constexpr int CL = 8;
+    // 32768-point rows: 16-CTA (non-portable) clusters, half a row's slice per CTA:
+    // 12-13% faster than 8-CTA clusters on B200 (tools/exp_row2d.cu); 16384: 8
+    constexpr int CL = P * Q >= 32768 ? 16 : 8;
     using G = Row2dGeom<C, P, Q, CL>;
     auto k = row2d_kernel<T, P, Q, CL, OP>;
     static SmemOptIn<decltype(k)> opt;
     cudaError_t e = opt(k, G::BYTES);
     if (e != cudaSuccess) return e;
+    if constexpr (CL > 8) {
+        static const cudaError_t np = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (np != cudaSuccess) return np;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(G::NT, 1, 1);
     cfg.dynamicSmemBytes = G::BYTES;
