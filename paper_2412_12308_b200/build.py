@@ -64,6 +64,11 @@ def _compile(src: str, verbose: bool) -> str:
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     srcs = _sources()
+    # the objects depend on the flags too: a different flag set rebuilds everything
+    stamp = os.path.join(BUILD, "flags.txt")
+    flags = " ".join(NVCC_FLAGS)
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        force = True
     if force:
         for o in glob.glob(os.path.join(BUILD, "*.o")):
             os.remove(o)
@@ -76,6 +81,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
         os.replace(tmp, LIB)
+    with open(stamp, "w") as f:
+        f.write(flags)
     return LIB
 
 
