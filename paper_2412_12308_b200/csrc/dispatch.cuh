@@ -50,7 +50,11 @@ template <typename T, int N, bool COLS> struct PipeCfg {
     static constexpr int NBUF = PipeSmem<C, N, W, COLS, 2>::BYTES <= 200 * 1024 ? 2 : 1;
     // a persistent thread's twiddles stay in registers when the budget allows
     static constexpr bool TWREG = W * TPT <= 256 && Shape<N>::STAGES <= 2;
+    // rows of >= 2048 points arrive as one bulk copy per row (tools/exp_line.cu:
+    // 4096-point rows FWD 118 -> 99 us, MID 194 -> 185 us; 2048 MID 175 -> 157 us)
+    static constexpr bool BULK = !COLS && N >= 2048;
     using L = PipeSmem<C, N, W, COLS, NBUF>;
+    static constexpr size_t SMEM = L::BYTES + (BULK ? 8 * NBUF * W : 0);
 };
 
 inline int sm_count()
@@ -108,8 +112,8 @@ cudaError_t pipe_n(const void *in, void *out, PipeArgs args, const void *tw, con
     using Cfg = PipeCfg<T, N, COLS>;
     constexpr int W = Cfg::W;
     constexpr int THREADS = W * Shape<N>::TPT;
-    const size_t smem = Cfg::L::BYTES;
-    auto k = pipe_kernel<T, N, W, COLS, OP, Cfg::NBUF, 1, Cfg::TWREG>;
+    const size_t smem = Cfg::SMEM;
+    auto k = pipe_kernel<T, N, W, COLS, OP, Cfg::NBUF, 1, Cfg::TWREG, Cfg::BULK>;
     static SmemOptIn<decltype(k)> opt;
     cudaError_t e = opt(k, smem);
     if (e != cudaSuccess) return e;

@@ -75,7 +75,29 @@ template <int TPT> struct LineSync {
 // TPT <= 32) and the W lines of a tile progress independently.  Column tiles
 // are loaded and stored column-fastest (W*sizeof(C)-byte row segments), with
 // the results staged through the tile buffer for the store.
-template <typename T, int N, int W, bool COLS, int OP, int NBUF, int MINB = 1, bool TWREG = false>
+// BULK (rows only): each line of a tile arrives as ONE bulk copy (cp.async.bulk,
+// the 1D form of the tensor memory accelerator) issued by the line's first
+// thread and counted on a per-(slot, line) mbarrier, instead of E 16-byte
+// cp.async per thread: no per-element copy instructions in the memory pipeline.
+// The row lands dense at the start of its line buffer and is read dense.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void bulk_expect(uint32_t mbar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_wait(uint32_t mbar, uint32_t parity)
+{
+    asm volatile("{\n\t.reg .pred p;\n"
+                 "BW%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra BW%=;\n}" ::"r"(mbar), "r"(parity) : "memory");
+}
+
+template <typename T, int N, int W, bool COLS, int OP, int NBUF, int MINB = 1, bool TWREG = false, bool BULK = false>
 __global__ void __launch_bounds__(W * Shape<N>::TPT, MINB)
 pipe_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out, PipeArgs a,
             const typename cplx_t<T>::type *__restrict__ tw, OpTables<T> tab)
@@ -105,7 +127,21 @@ pipe_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out, P
         return b * a.batch_stride + line * a.line_stride + (int64_t)tt * a.elem_stride;
     };
     auto buf = [&](int slot, int cc) { return buf0 + (size_t)slot * (L::BUF / sizeof(C)) + cc * L::S; };
+    static_assert(!BULK || !COLS, "bulk copies load whole rows");
+    // BULK: mbarrier of (slot, line) at the end of the ring buffers
+    const uint32_t mbar0 = (uint32_t)__cvta_generic_to_shared(smem_raw + (BULK ? L::BYTES : 0));
     auto issue = [&](int64_t tile, int slot) {
+        if constexpr (BULK) {
+            if (t == 0) {
+                const int64_t base = line_base(tile, c, 0);
+                if (base >= 0) {
+                    const uint32_t mb = mbar0 + 8u * (uint32_t)(slot * W + c);
+                    bulk_expect(mb, (uint32_t)(N * sizeof(C)));
+                    bulk_g2s((uint32_t)__cvta_generic_to_shared(buf(slot, c)), in + base, (uint32_t)(N * sizeof(C)), mb);
+                }
+            }
+            return;
+        }
         const int64_t base = line_base(tile, lc, lt);
         if (base >= 0) {
             C *dst = buf(slot, lc) + padidx(lt, S::LOGE);
@@ -123,6 +159,11 @@ pipe_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out, P
     TwP twp;
     if constexpr (TWREG) twp.load(tw, t);
     else twp = TwL1<N, C>{tw, t};
+    if constexpr (BULK) {
+        if (tid < NBUF * W) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar0 + 8u * tid) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        __syncthreads();
+    }
     pdl_wait();
 
     // ring of NBUF tile buffers: tile i lives in slot i % NBUF; the loads of the
@@ -138,7 +179,11 @@ pipe_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out, P
         const int slot = it % NBUF;
         const int64_t next = tile + (int64_t)(NBUF - 1) * gridDim.x;
         if (tile + gridDim.x >= a.ntiles) pdl_trigger();   // this CTA's last tile
-        if constexpr (NBUF > 1) {
+        if constexpr (BULK) {
+            if (NBUF > 1 && next < a.ntiles) issue(next, (it + NBUF - 1) % NBUF);
+            if (NBUF == 1 && it == 0) issue(tile, 0);
+            if (line_base(tile, c, 0) >= 0) bulk_wait(mbar0 + 8u * (uint32_t)(slot * W + c), (uint32_t)(it / NBUF) & 1u);
+        } else if constexpr (NBUF > 1) {
             if (next < a.ntiles) issue(next, (it + NBUF - 1) % NBUF);
             else cp_async_commit();                  // keep the group count uniform
             cp_async_wait<NBUF - 1>();               // this thread's copies of `tile` landed
@@ -150,7 +195,11 @@ pipe_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out, P
 
         SmemView<C, S::LOGE, 1> sm{buf(slot, c)};
         C v[E];
-        if constexpr (TPT % E == 0) {                // inactive lines read (unused) garbage
+        if constexpr (BULK) {                        // the row arrived dense
+            const C *rp = buf(slot, c);
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = rp[t + TPT * e];
+        } else if constexpr (TPT % E == 0) {         // inactive lines read (unused) garbage
             const C *rp = sm.ptr(t);
 #pragma unroll
             for (int e = 0; e < E; ++e) v[e] = rp[decltype(sm)::off(TPT * e)];
@@ -234,7 +283,7 @@ pipe_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out, P
             if (nxt < a.ntiles) issue(nxt, 0);       // the buffer is free after the last use
         }
     }
-    cp_async_wait<0>();
+    if constexpr (!BULK) cp_async_wait<0>();
 }
 
 } // namespace fftpde

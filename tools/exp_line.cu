@@ -200,21 +200,22 @@ static void tpipe_var(const void *in, void *out, void *out2, long nx, long ny, l
 }
 
 // ---- pipe_kernel reference (current library configuration)
-template <typename T, int N, int W, bool COLS, int OP, int NBUF, bool TWREG>
+template <typename T, int N, int W, bool COLS, int OP, int NBUF, bool TWREG, bool BULK = false>
 static void pipe_ref(const void *in, void *out, void *out2, long nx, long ny, long batch, const void *tw,
                      const OpTables<T> &tab, const char *tag)
 {
     using C = typename cplx_t<T>::type;
     char name[160];
-    snprintf(name, sizeof name, "%s PIPE W=%d nbuf=%d", tag, W, NBUF);
+    snprintf(name, sizeof name, "%s PIPE%s W=%d nbuf=%d", tag, BULK ? " BULK" : "", W, NBUF);
     if (g_filter && !strstr(name, g_filter)) return;
-    using L = PipeSmem<C, N, W, COLS, NBUF>;
-    auto k = pipe_kernel<T, N, W, COLS, OP, NBUF, 1, TWREG>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+    using L0 = PipeSmem<C, N, W, COLS, NBUF>;
+    constexpr size_t SMB = L0::BYTES + (BULK ? 8 * NBUF * W : 0);
+    auto k = pipe_kernel<T, N, W, COLS, OP, NBUF, 1, TWREG, BULK>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMB);
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     const int threads = W * Shape<N>::TPT;
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, L::BYTES);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, SMB);
     PipeArgs a;
     if (COLS) a = PipeArgs{nx, 1, nx, nx * ny, 0, (nx + W - 1) / W, OP, out2};
     else a = PipeArgs{ny, nx, 1, nx * ny, 0, (ny + W - 1) / W, OP, out2};
@@ -223,7 +224,7 @@ static void pipe_ref(const void *in, void *out, void *out2, long nx, long ny, lo
     if (grid > a.ntiles) grid = a.ntiles;
     const double fields = OP == PIPE_MID ? 3.0 : 2.0;
     const double bytes = fields * (double)nx * ny * batch * sizeof(C);
-    timeit([&] { k<<<(unsigned)grid, threads, L::BYTES, g_stream>>>((const C *)in, (C *)out, a, (const C *)tw, tab); }, name,
+    timeit([&] { k<<<(unsigned)grid, threads, SMB, g_stream>>>((const C *)in, (C *)out, a, (const C *)tw, tab); }, name,
            bytes, occ, grid);
 }
 
@@ -325,6 +326,10 @@ int main(int argc, char **argv)
         rr_var<D, 4096, 2, true, LN_FWD, 1>(B, B, nullptr, 4096, 4096, 1, t16, tab, "c3 colsFWD");
         rr_var<D, 2048, 4, true, LN_POISSON, 1>(B, B, nullptr, 8192, 2048, 1, t16_2048, tab2048, "c2048 colsPOI");
         rr_var<D, 2048, 2, true, LN_POISSON, 2>(B, B, nullptr, 8192, 2048, 1, t16_2048, tab2048, "c2048 colsPOI");
+        pipe_ref<D, 4096, 1, false, PIPE_MID, 2, true, true>(A, B, Cb, 4096, 4096, 1, t16, tab, "c3 rowsMID");
+        pipe_ref<D, 4096, 1, false, PIPE_FWD, 2, true, true>(A, B, nullptr, 4096, 4096, 1, t16, tab, "c3 rowsFWD");
+        pipe_ref<D, 2048, 2, false, PIPE_MID, 2, true, false>(A, B, Cb, 2048, 8192, 1, t16_2048, tab2048, "c2048 rowsMID");
+        pipe_ref<D, 2048, 2, false, PIPE_MID, 2, true, true>(A, B, Cb, 2048, 8192, 1, t16_2048, tab2048, "c2048 rowsMID");
         // transposed-spectrum design for C3: W = 2 rows per tile -> 32-byte segments on the T side
         tpipe_var<D, 4096, 2, TP_MID_T, 1, false>(A, B, Cb, 4096, 4096, 1, t16, "c3 T");
         tpipe_var<D, 4096, 1, TP_MID_T, 2, false>(A, B, Cb, 4096, 4096, 1, t16, "c3 T");
