@@ -194,6 +194,8 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tma_encoder()
 {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         void *f = nullptr;
+        const char *env = std::getenv("FFTPDE_TMA");      // FFTPDE_TMA=0: the non-TMA passes (tests)
+        if (env && env[0] == '0') return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
             q != cudaDriverEntryPointSuccess)

@@ -324,3 +324,44 @@ def test_errors_are_reported():
     assert e.value.status == F.ERR_INVALID_ARG
     with pytest.raises(TypeError):
         p.poisson(dev(noise((64, 64), 1), C64))
+
+
+_NO_TMA_SCRIPT = r"""
+import numpy as np, torch
+from oracle import oracle as O
+from paper_2412_12308_b200 import fftpde as F
+rng = np.random.default_rng(5)
+def noise(shape):
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+worst = 0.0
+for ny, nx, B in ((256, 32, 2), (512, 16, 1)):           # column passes without TMA (pipe_kernel)
+    x = noise((B, ny, nx))
+    p = F.Plan(nx, ny, batch=B)
+    worst = max(worst, rel(p.poisson(torch.from_numpy(x).cuda()).cpu().numpy(), O.poisson(x)))
+    worst = max(worst, rel(p.diffuse(torch.from_numpy(x).cuda(), 1e-3, 0.01, 3).cpu().numpy(),
+                           O.diffuse(x, 1e-3, 0.01, 3)))
+u0, v0 = noise((4096, 8)), noise((4096, 8))                # wave columns without TMA (col2 four-step)
+p = F.Plan(8, 4096)
+u, v = torch.from_numpy(u0).cuda(), torch.from_numpy(v0).cuda()
+p.wave_step(u, v, 1.1, 2e-3, 3)
+uo, vo = O.wave(u0, v0, 1.1, 2e-3, 3)
+worst = max(worst, rel(u.cpu().numpy(), uo), rel(v.cpu().numpy(), vo))
+print("WORST", worst)
+"""
+
+
+def test_fallback_passes_without_tma(tmp_path):
+    # FFTPDE_TMA=0, FFTPDE_PDL=0: the library takes its non-TMA column passes (the path a
+    # driver without the tensor-map encoder would get); same parity bar
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FFTPDE_TMA="0", FFTPDE_PDL="0", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", _NO_TMA_SCRIPT], env=env, cwd=root, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    worst = float(r.stdout.strip().split()[-1])
+    assert worst <= 1e-12
