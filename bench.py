@@ -259,8 +259,8 @@ def native(args, wl, world, rank, local):
     dtype = {"c128": torch.complex128, "c64": torch.complex64, "f64": torch.float64,
              "f32": torch.float32}[wl.dtype]
     dev_in, host = make_device_inputs(wl, dtype)
-    if host is None:          # C5: host copies only where needed (e2e / cpu baseline are bounded)
-        args.no_e2e = True
+    # C5 (16 GiB field): built on the device; the e2e leg copies it once into pinned
+    # host memory (outside the timed region), the CPU baseline takes a bounded sample
     out = [torch.empty_like(d) for d in dev_in]
     if wl.dtype in ("f64", "f32"):
         plan = F.PlanR2C(wl.nx, wl.ny, batch=wl.batch, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly)
@@ -352,7 +352,14 @@ def native(args, wl, world, rank, local):
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        host_in = [torch.from_numpy(np.ascontiguousarray(h)).to(dtype).pin_memory() for h in host]
+        if host is not None:
+            host_in = [torch.from_numpy(np.ascontiguousarray(h)).to(dtype).pin_memory() for h in host]
+        else:
+            host_in = []
+            for d in dev_in:
+                h = torch.empty(d.shape, dtype=d.dtype, pin_memory=True)
+                h.copy_(d)
+                host_in.append(h)
         host_out = [torch.empty(h.shape, dtype=dtype, pin_memory=True) for h in host_in]
 
         def e2e_step():
