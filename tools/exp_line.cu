@@ -200,17 +200,17 @@ static void tpipe_var(const void *in, void *out, void *out2, long nx, long ny, l
 }
 
 // ---- pipe_kernel reference (current library configuration)
-template <typename T, int N, int W, bool COLS, int OP, int NBUF, bool TWREG, bool BULK = false>
+template <typename T, int N, int W, bool COLS, int OP, int NBUF, bool TWREG, bool BULK = false, int MINB = 1>
 static void pipe_ref(const void *in, void *out, void *out2, long nx, long ny, long batch, const void *tw,
                      const OpTables<T> &tab, const char *tag)
 {
     using C = typename cplx_t<T>::type;
     char name[160];
-    snprintf(name, sizeof name, "%s PIPE%s W=%d nbuf=%d", tag, BULK ? " BULK" : "", W, NBUF);
+    snprintf(name, sizeof name, "%s PIPE%s W=%d nbuf=%d minb=%d twreg=%d", tag, BULK ? " BULK" : "", W, NBUF, MINB, (int)TWREG);
     if (g_filter && !strstr(name, g_filter)) return;
     using L0 = PipeSmem<C, N, W, COLS, NBUF>;
     constexpr size_t SMB = L0::BYTES + (BULK ? 8 * NBUF * W : 0);
-    auto k = pipe_kernel<T, N, W, COLS, OP, NBUF, 1, TWREG, BULK>;
+    auto k = pipe_kernel<T, N, W, COLS, OP, NBUF, MINB, TWREG, BULK>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMB);
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     const int threads = W * Shape<N>::TPT;
@@ -328,6 +328,9 @@ int main(int argc, char **argv)
         rr_var<D, 2048, 2, true, LN_POISSON, 2>(B, B, nullptr, 8192, 2048, 1, t16_2048, tab2048, "c2048 colsPOI");
         pipe_ref<D, 4096, 1, false, PIPE_MID, 2, true, true>(A, B, Cb, 4096, 4096, 1, t16, tab, "c3 rowsMID");
         pipe_ref<D, 4096, 1, false, PIPE_FWD, 2, true, true>(A, B, nullptr, 4096, 4096, 1, t16, tab, "c3 rowsFWD");
+        pipe_ref<D, 4096, 1, false, PIPE_MID, 1, false, true, 2>(A, B, Cb, 4096, 4096, 1, t16, tab, "c3 rowsMID");
+        pipe_ref<D, 4096, 1, false, PIPE_MID, 2, false, true, 1>(A, B, Cb, 4096, 4096, 1, t16, tab, "c3 rowsMID");
+        pipe_ref<D, 4096, 1, false, PIPE_FWD, 1, false, true, 2>(A, B, nullptr, 4096, 4096, 1, t16, tab, "c3 rowsFWD");
         pipe_ref<D, 2048, 2, false, PIPE_MID, 2, true, false>(A, B, Cb, 2048, 8192, 1, t16_2048, tab2048, "c2048 rowsMID");
         pipe_ref<D, 2048, 2, false, PIPE_MID, 2, true, true>(A, B, Cb, 2048, 8192, 1, t16_2048, tab2048, "c2048 rowsMID");
         // transposed-spectrum design for C3: W = 2 rows per tile -> 32-byte segments on the T side
