@@ -316,13 +316,25 @@ __device__ __forceinline__ void fft_tw(C (&v)[Shape<N, EMAX>::E], const View &sm
 {
     using S = Shape<N, EMAX>;
     constexpr int E = S::E, TPT = S::TPT;
+    // Twiddles fetched from memory (TwL1) are loaded in groups of TG before their
+    // multiplies, so a group's loads are in flight together instead of each load's
+    // latency following the previous multiply (the loads are volatile and ordered).
+    constexpr int TG = E <= 1 ? 1 : E <= 16 ? E - 1 : 8;
     int Ns = 1;
 #pragma unroll
     for (int s = 0; s < S::STAGES; ++s) {
         const int k = t & (Ns - 1);
         if (s > 0) {
 #pragma unroll
-            for (int m = 1; m < E; ++m) v[m] = cmulw<INV>(v[m], tw.mid(s, m));
+            for (int m0 = 1; m0 < E; m0 += TG) {
+                C w[TG];
+#pragma unroll
+                for (int j = 0; j < TG; ++j)
+                    if (m0 + j < E) w[j] = tw.mid(s, m0 + j);
+#pragma unroll
+                for (int j = 0; j < TG; ++j)
+                    if (m0 + j < E) v[m0 + j] = cmulw<INV>(v[m0 + j], w[j]);
+            }
         }
         dft_r<E, INV>(v);
         // scatter X_m of butterfly t to (t / Ns) Ns E + k + m Ns; base or m Ns is a multiple of E
@@ -351,8 +363,17 @@ __device__ __forceinline__ void fft_tw(C (&v)[Shape<N, EMAX>::E], const View &sm
 #pragma unroll
         for (int m = 0; m < R; ++m) u[m] = v[q + m * Q];
         if (S::NS_LAST > 1) {
+            constexpr int LG = R <= 1 ? 1 : R <= 16 ? R - 1 : 8;
 #pragma unroll
-            for (int m = 1; m < R; ++m) u[m] = cmulw<INV>(u[m], tw.last(q, m));
+            for (int m0 = 1; m0 < R; m0 += LG) {
+                C w[LG];
+#pragma unroll
+                for (int j = 0; j < LG; ++j)
+                    if (m0 + j < R) w[j] = tw.last(q, m0 + j);
+#pragma unroll
+                for (int j = 0; j < LG; ++j)
+                    if (m0 + j < R) u[m0 + j] = cmulw<INV>(u[m0 + j], w[j]);
+            }
         }
         dft_r<R, INV>(u);
 #pragma unroll
