@@ -133,7 +133,11 @@ def alg_bytes_per_launch(wl, kernel_class):
         # per step: 2 source samplings (1 write each) and the RK4 kernel (u^, v^, 3 source
         # spectra read, u^, v^ written); the transforms are plain forward passes
         return 3 * field if kernel_class == "pointwise" else 2 * field
-    if kernel_class == "row_pass" and wl.op in ("diffuse", "wave") and wl.nsteps > 1:
+    # the complex 2D diffusion is separable: each step is one row pass (forward,
+    # x factor, inverse) and one column pass, each reading and writing the field
+    # once; the wave, the real-field and the 3D diffusion keep the MID row pass
+    mid_rows = wl.op == "wave" or (wl.op == "diffuse" and (wl.dtype in ("f64", "f32") or wl.nz > 1))
+    if kernel_class == "row_pass" and mid_rows and wl.nsteps > 1:
         n = wl.nsteps                      # per field: 1 FWD + (n-1) MID + 1 INV launches
         return (2 * field * 2 + 3 * field * (n - 1)) / (n + 1)
     return 2 * field

@@ -165,14 +165,21 @@ cudaError_t line_n(const void *in, void *out, void *out2, int64_t nlines, int64_
 
 template <typename T, int N>
 cudaError_t rows_n(const void *in, void *out, void *out2, int64_t ny, int64_t stride, int64_t batch,
-                   int dir, const ColTw &ctw, cudaStream_t st)
+                   int dir, const ColTw &ctw, cudaStream_t st, RowMul rm)
 {
     OpTables<T> tab{};
     tab.scale = (T)1;
+    if (dir == ROW_DIFF) {                    // operator slot (line, element) = (ones[b], mul[a])
+        if (!rm.mul || !rm.ones) return cudaErrorInvalidValue;
+        tab.ex = (const T *)rm.ones;
+        tab.ey = (const T *)rm.mul;
+    }
     using LP = LinePolicy<T, N, false>;
     if constexpr (LP::E > 0) {
         const void *tw = tw_for<LP::E>(ctw);
         if (tw) {   // (a plan without this radix's table takes the pipe pass)
+        if (dir == ROW_DIFF)
+            return line_n<T, N, LP::E, LP::W, false, LN_DIFFUSE, LP::MINB>(in, out, nullptr, ny, N, 1, stride, batch, tw, tab, st);
         if (dir == ROW_INV)
             return line_n<T, N, LP::E, LP::W, false, LN_INV, LP::MINB>(in, out, nullptr, ny, N, 1, stride, batch, tw, tab, st);
         if (dir == ROW_MID)
@@ -182,6 +189,7 @@ cudaError_t rows_n(const void *in, void *out, void *out2, int64_t ny, int64_t st
     }
     const void *tw = ctw.tw;
     PipeArgs a{ny, N, 1, stride, batch, 0, dir, out2};
+    if (dir == ROW_DIFF) return pipe_n<T, N, false, PIPE_DIFFUSE>(in, out, a, tw, tab, st);
     if (dir == ROW_INV) return pipe_n<T, N, false, PIPE_INV>(in, out, a, tw, tab, st);
     if (dir == ROW_MID) return pipe_n<T, N, false, PIPE_MID>(in, out, a, tw, tab, st);
     return pipe_n<T, N, false, PIPE_FWD>(in, out, a, tw, tab, st);
@@ -429,7 +437,7 @@ cudaError_t launch_col2(int64_t ny, int64_t P, int op, Col2Args<T> g, int64_t ba
 // ---- long rows: DSMEM four-step on a cluster (row2d.cuh) ------------------------
 template <typename T, int P, int Q, int OP>
 cudaError_t row2d_n(const void *in, void *out, void *out2, int64_t ny, int64_t stride, int64_t batch,
-                    const ColTw &tw, cudaStream_t st)
+                    const ColTw &tw, cudaStream_t st, const void *mul = nullptr)
 {
     using C = typename cplx_t<T>::type;
     // 32768-point rows: 16-CTA (non-portable) clusters, half a row's slice per CTA:
@@ -471,15 +479,19 @@ cudaError_t row2d_n(const void *in, void *out, void *out2, int64_t ny, int64_t s
     const int64_t g = std::min<int64_t>(nrows, ncl);          // persistent clusters
     cfg.gridDim = dim3((unsigned)(CL * g), 1, 1);
     e = cudaLaunchKernelEx(&cfg, k, (const C *)in, (C *)out, (C *)out2, nrows, ny, stride, (const C *)tw.twP,
-                           (const C *)tw.twQ, (const C *)tw.twN);
+                           (const C *)tw.twQ, (const C *)tw.twN, (const T *)mul);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
 template <typename T, int P, int Q>
 cudaError_t row2d_dir(const void *in, void *out, void *out2, int64_t ny, int64_t stride, int64_t batch, int dir,
-                      const ColTw &tw, cudaStream_t st)
+                      const ColTw &tw, cudaStream_t st, RowMul rm)
 {
+    if (dir == ROW_DIFF) {
+        if (!rm.mul) return cudaErrorInvalidValue;
+        return row2d_n<T, P, Q, R2D_DIFF>(in, out, nullptr, ny, stride, batch, tw, st, rm.mul);
+    }
     if (dir == ROW_INV) return row2d_n<T, P, Q, R2D_INV>(in, out, nullptr, ny, stride, batch, tw, st);
     if (dir == ROW_MID) return row2d_n<T, P, Q, R2D_MID>(in, out, out2, ny, stride, batch, tw, st);
     return row2d_n<T, P, Q, R2D_FWD>(in, out, nullptr, ny, stride, batch, tw, st);
@@ -487,11 +499,11 @@ cudaError_t row2d_dir(const void *in, void *out, void *out2, int64_t ny, int64_t
 
 template <typename T>
 cudaError_t launch_rows2(int64_t nx, const void *in, void *out, void *out2, int64_t ny, int64_t stride,
-                         int64_t batch, int dir, const ColTw &tw, cudaStream_t st)
+                         int64_t batch, int dir, const ColTw &tw, cudaStream_t st, RowMul rm)
 {
     switch (nx) {
-    case 16384: return row2d_dir<T, 128, 128>(in, out, out2, ny, stride, batch, dir, tw, st);
-    case 32768: return row2d_dir<T, 128, 256>(in, out, out2, ny, stride, batch, dir, tw, st);
+    case 16384: return row2d_dir<T, 128, 128>(in, out, out2, ny, stride, batch, dir, tw, st, rm);
+    case 32768: return row2d_dir<T, 128, 256>(in, out, out2, ny, stride, batch, dir, tw, st, rm);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -499,10 +511,10 @@ cudaError_t launch_rows2(int64_t nx, const void *in, void *out, void *out2, int6
 // ---- length dispatch -------------------------------------------------------
 template <typename T>
 cudaError_t launch_rows(int64_t n, const void *in, void *out, void *out2, int64_t ny, int64_t stride,
-                        int64_t batch, int dir, const ColTw &tw, cudaStream_t st)
+                        int64_t batch, int dir, const ColTw &tw, cudaStream_t st, RowMul rm)
 {
     switch (n) {
-#define X(L) case L: return rows_n<T, L>(in, out, out2, ny, stride, batch, dir, tw, st);
+#define X(L) case L: return rows_n<T, L>(in, out, out2, ny, stride, batch, dir, tw, st, rm);
         FFTPDE_LEN_CASES(X)
 #undef X
     default: return cudaErrorInvalidValue;

@@ -35,7 +35,7 @@ struct fftpde_plan_s {
     unsigned char *ws = nullptr;
     size_t ws_bytes = 0;
     // workspace offsets (bytes)
-    size_t o_twx = 0, o_twy = 0, o_twx8 = 0, o_twy8 = 0, o_twx32 = 0, o_twy32 = 0, o_kx = 0, o_ky = 0, o_kx2 = 0, o_ky2 = 0, o_ex = 0, o_ey = 0, o_wc = 0, o_ws1 = 0, o_ws2 = 0;
+    size_t o_one = 0, o_twx = 0, o_twy = 0, o_twx8 = 0, o_twy8 = 0, o_twx32 = 0, o_twy32 = 0, o_kx = 0, o_ky = 0, o_kx2 = 0, o_ky2 = 0, o_ex = 0, o_ey = 0, o_wc = 0, o_ws1 = 0, o_ws2 = 0;
     size_t o_twP = 0, o_twQ = 0, o_twN = 0;   // two-level column pass tables (P, Q > 0)
     size_t o_scr = 0;                          // scratch: row spectra of 2 fields (multi-step solves)
     int64_t colP = 0, colQ = 0;
@@ -437,6 +437,29 @@ template <typename T> struct Passes {
     // nsteps diffusion steps: the row spectrum lives in the workspace scratch;
     // between column passes one fused row pass writes the physical field of
     // step s (materialised in u) and the row spectrum of step s+1.
+    // Separable diffusion (R17, R26): exp(-D|k|^2 dt) = ex(a) ey(b), so one
+    // step is the 1D diffusion of every row (forward, times ex / (nx ny), inverse)
+    // followed by that of every column (times ey): two passes of one read and one
+    // write each, in place, u materialised after every step.
+    RowMul rowmul() const { return RowMul{p->ws + p->o_ex, p->ws + p->o_one}; }
+    cudaError_t rows_diff(const void *in, void *out)
+    {
+        return launch(p, FFTPDE_KERNEL_ROW, [&] {
+            if (p->rowP)
+                return launch_rows2<T>(p->nx, in, out, nullptr, p->ny, stride, batch, ROW_DIFF, rtw(), p->stream,
+                                       rowmul());
+            return launch_rows<T>(p->nx, in, out, nullptr, p->ny, stride, batch, ROW_DIFF, rtw(), p->stream,
+                                  rowmul());
+        });
+    }
+    cudaError_t cols_diff_y(const void *in, void *out)
+    {
+        OpTables<T> t = tables<T>(p);
+        t.ex = (const T *)(p->ws + p->o_one);               // the x factor was applied by the rows
+        return launch(p, FFTPDE_KERNEL_COL, [&] {
+            return launch_cols<T>(p->ny, in, out, p->nx, stride, batch, COL_DIFFUSE, ctw(), t, p->stream);
+        });
+    }
     cudaError_t diffuse(const void *u0, void *u, int64_t nsteps)
     {
         if (small()) {
@@ -450,12 +473,10 @@ template <typename T> struct Passes {
             for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) e = solve_step(k == 0 ? u0 : u, u, COL_DIFFUSE);
             return e;
         }
-        void *S = scratch(0);
-        cudaError_t e = rows(u0, S, 0);
+        cudaError_t e = cudaSuccess;
         for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) {
-            e = cols(S, S, COL_DIFFUSE);
-            if (e != cudaSuccess) break;
-            e = (k + 1 < nsteps) ? rows_mid(S, S, u) : rows(S, u, 1);
+            e = rows_diff(k == 0 ? u0 : u, u);
+            if (e == cudaSuccess) e = cols_diff_y(u, u);
         }
         return e;
     }
@@ -1119,6 +1140,7 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     p->o_twy8 = take(p->twy8.size() / 2 * ec);
     p->o_twx32 = take(p->twx32.size() / 2 * ec);
     p->o_twy32 = take(p->twy32.size() / 2 * ec);
+    p->o_one = take((size_t)std::max(nx, ny) * er);
     p->o_kx2 = take((size_t)nx * er);
     p->o_ky2 = take((size_t)ny * er);
     p->o_kx = take((size_t)nx * er);
@@ -1191,6 +1213,7 @@ fftpde_status fftpde_set_workspace(fftpde_plan plan, void *dev_ptr, size_t bytes
         if (s == FFTPDE_OK) s = upload(plan, plan->o_twQ, plan->twQ);
         if (s == FFTPDE_OK) s = upload(plan, plan->o_twN, plan->twN);
     }
+    if (s == FFTPDE_OK) s = upload(plan, plan->o_one, std::vector<double>((size_t)std::max(plan->nx, plan->ny), 1.0));
     if (s == FFTPDE_OK) s = upload(plan, plan->o_kx2, plan->kx2);
     if (s == FFTPDE_OK) s = upload(plan, plan->o_ky2, plan->ky2);
     if (s == FFTPDE_OK) s = upload(plan, plan->o_kx, plan->kx);

@@ -31,11 +31,19 @@ constexpr int64_t kMaxLen2 = 32768;  // two-level (cluster) axis length limit
 // Row transforms of `batch` grids: length n along x, ny rows per grid, grids
 // `stride` elements apart.  dir: ROW_FWD, ROW_INV (unscaled), or ROW_MID (inverse
 // stored to out2, then forward stored to out).
-enum RowDir { ROW_FWD = 0, ROW_INV = 4, ROW_MID = 5 };   // == PipeOp values
+// ROW_DIFF: forward transform, times the per-wavenumber multiplier mul[a] (the x
+// factor of a separable operator, 1/(nx ny) folded in), inverse transform, in
+// one pass; `ones` is a table of 1s over the row index (the operator slot of the
+// line kernels is (line, element)-separable).
+enum RowDir { ROW_FWD = 0, ROW_DIFF = 3, ROW_INV = 4, ROW_MID = 5 };   // == PipeOp values
 struct ColTw;
+struct RowMul {
+    const void *mul = nullptr;    // [nx] multiplier over the row's wavenumber index
+    const void *ones = nullptr;   // [>= ny] ones
+};
 template <typename T>
 cudaError_t launch_rows(int64_t n, const void *in, void *out, void *out2, int64_t ny, int64_t stride,
-                        int64_t batch, int dir, const ColTw &tw, cudaStream_t st);
+                        int64_t batch, int dir, const ColTw &tw, cudaStream_t st, RowMul rm = {});
 
 // Twiddle tables of the column axis: the single-level stage table of ny, and for
 // the two-level (cluster) column pass the stage tables of P and Q (ny = P Q)
@@ -57,7 +65,7 @@ void row2_split(int64_t nx, int64_t &P, int64_t &Q);
 // twP, twQ = radix-16 stage tables of P and Q; twN = split inter-phase table.
 template <typename T>
 cudaError_t launch_rows2(int64_t nx, const void *in, void *out, void *out2, int64_t ny, int64_t stride,
-                         int64_t batch, int dir, const ColTw &tw, cudaStream_t st);
+                         int64_t batch, int dir, const ColTw &tw, cudaStream_t st, RowMul rm = {});
 
 // Column pass along y (length ny) over nx columns, op in ColOp.
 template <typename T>

@@ -24,7 +24,9 @@
 
 namespace fftpde {
 
-enum Row2dOp { R2D_FWD = 0, R2D_INV = 1, R2D_MID = 2 };
+// R2D_DIFF: forward transform, times mul[a] (natural wavenumber index a), inverse
+// transform, one store (the x factor of a separable operator, e.g. diffusion)
+enum Row2dOp { R2D_FWD = 0, R2D_INV = 1, R2D_MID = 2, R2D_DIFF = 3 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint32_t mapa_rank(uint32_t a, uint32_t rank)
@@ -113,7 +115,7 @@ __global__ void __launch_bounds__(Row2dGeom<typename cplx_t<T>::type, P, Q, CL>:
 row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>::type *out,
              typename cplx_t<T>::type *out2, int64_t nrows, int64_t ny, int64_t stride,
              const typename cplx_t<T>::type *__restrict__ twP, const typename cplx_t<T>::type *__restrict__ twQ,
-             const typename cplx_t<T>::type *__restrict__ twS)
+             const typename cplx_t<T>::type *__restrict__ twS, const T *__restrict__ mul)
 {
     using C = typename cplx_t<T>::type;
     using G = Row2dGeom<C, P, Q, CL>;
@@ -175,7 +177,7 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
     // into registers while this row is transformed
     auto load_row = [&](int64_t row, C (&u)[16]) {
         const C *src = row_ptr(in, row);
-        if constexpr (OP == R2D_FWD) {
+        if constexpr (OP == R2D_FWD || OP == R2D_DIFF) {
 #pragma unroll
             for (int e = 0; e < 16; ++e) u[e] = src[n1 + P * (ta + TA * e)];
         } else {
@@ -208,7 +210,8 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
 #pragma unroll
         for (int e = 0; e < 16; ++e) v[e] = nx[e];
         if (row + ncl < nrows) load_row(row + ncl, nx);
-        if constexpr (OP != R2D_FWD) {
+        // inverse: v in the phase-B^-1 layout X[k1 + Q (tb + TB e)] -> x[n1 + P (ta + TA e)]
+        auto inv_part = [&](C (&v)[16]) {
             // ---- B^-1: inverse P-point transforms over k2 of items k1, times w_N^{-n1 k1}
             fft<P, true, 16>(v, smB, tb, twP, sync);          // v[e] = Y[n1 = tb + TB e][k1]
 #pragma unroll
@@ -227,11 +230,9 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
             for (int e = 0; e < 16; ++e) v[e] = R[ia * (Q + 1) + ta + TA * e];
             fft<Q, true, 16>(v, smA, ta, twQ, sync);          // v[e] = x[n1 + P (ta + TA e)]
             release_R();                                      // (the transform consumed R)
-            C *dst = const_cast<C *>(row_ptr(OP == R2D_INV ? out : out2, row));
-#pragma unroll
-            for (int e = 0; e < 16; ++e) dst[n1 + P * (ta + TA * e)] = v[e];
-        }
-        if constexpr (OP != R2D_INV) {
+        };
+        // forward: v in the phase-A layout x[n1 + P (ta + TA e)] -> X[k1 + Q (tb + TB e)]
+        auto fwd_part = [&](C (&v)[16]) {
             // ---- A: Q-point transforms over n2 of items n1, times w_N^{n1 k1}
             fft<Q, false, 16>(v, smA, ta, twQ, sync);         // v[e] = Y[n1][k1 = ta + TA e]
 #pragma unroll
@@ -250,9 +251,27 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
             for (int e = 0; e < 16; ++e) v[e] = R[jb * (P + 1) + tb + TB * e];
             fft<P, false, 16>(v, smB, tb, twP, sync);
             release_R();
+        };
+        if constexpr (OP == R2D_INV || OP == R2D_MID) {
+            inv_part(v);
+            C *dst = const_cast<C *>(row_ptr(OP == R2D_INV ? out : out2, row));
+#pragma unroll
+            for (int e = 0; e < 16; ++e) dst[n1 + P * (ta + TA * e)] = v[e];
+        }
+        if constexpr (OP == R2D_FWD || OP == R2D_MID) {
+            fwd_part(v);
             C *dst = const_cast<C *>(row_ptr(out, row));
 #pragma unroll
             for (int e = 0; e < 16; ++e) dst[k1 + Q * (tb + TB * e)] = v[e];
+        }
+        if constexpr (OP == R2D_DIFF) {
+            fwd_part(v);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = cscale(v[e], __ldg(mul + k1 + Q * (tb + TB * e)));
+            inv_part(v);
+            C *dst = const_cast<C *>(row_ptr(out, row));
+#pragma unroll
+            for (int e = 0; e < 16; ++e) dst[n1 + P * (ta + TA * e)] = v[e];
         }
     }
     cl_wait_acquire();                       // no CTA leaves while others may still write its smem

@@ -78,7 +78,7 @@ float run_new(const double2 *in, double2 *out, double2 *out2, long nrows, const 
     if (g < 1) g = 1;
     cfg.gridDim = dim3((unsigned)(g * CL), 1, 1);
     const long N = (long)P * Q;
-    auto f = [&] { cudaLaunchKernelEx(&cfg, k, in, out, out2, nrows, nrows, N * nrows, t.tP16, t.tQ16, t.tS); };
+    auto f = [&] { cudaLaunchKernelEx(&cfg, k, in, out, out2, nrows, nrows, N * nrows, t.tP16, t.tQ16, t.tS, (const double *)nullptr); };
     float ms = timeit(f, reps);
     if (print) {
         const double bytes = (OP == R2D_MID ? 3.0 : 2.0) * N * nrows * 16;
