@@ -74,7 +74,7 @@ struct fftpde_plan_s {
     int64_t nz = 1;
     double Lz = 1.0;
     std::vector<double> twz, twz8, kz2, kxy2;
-    size_t o_twz = 0, o_twz8 = 0, o_kz2 = 0, o_kxy2 = 0, o_exy = 0, o_ez = 0;
+    size_t o_twz = 0, o_twz8 = 0, o_kz2 = 0, o_kxy2 = 0, o_exy = 0, o_ez = 0, o_zscale = 0;
     bool diff3_valid = false;
     double diff3_D = 0, diff3_dt = 0;
     // optional per-launch timing (fftpde_set_profiling): event pairs per kernel class
@@ -798,18 +798,30 @@ template <typename T> struct Passes {
         if (e == cudaSuccess) e = rows(Y, out, 1);
         return e;
     }
-    // nsteps exact diffusion steps; the x-spectrum of the volume lives in the
-    // scratch, the MID row pass materialises u between steps (as the 2D diffuse)
+    // nsteps exact diffusion steps in the separable form (R26): per step the 1D
+    // diffusion along x (rows), y (y-pass) and z (z-pass), in place on u, one read
+    // and one write each; u is materialised after every step
     cudaError_t diffuse3(const void *u0, void *u, int64_t nsteps)
     {
-        void *S0 = scratch(0), *S1 = p->colP ? scratch(1) : scratch(0);
-        cudaError_t e = rows(u0, S0, 0);
+        OpTables<T> ty = tables3<false>((T)1);
+        ty.ex = (const T *)(p->ws + p->o_one);
+        ty.ey = (const T *)(p->ws + p->o_ey);
+        OpTables<T> tz = tables3<true>((T)1);
+        tz.ex = (const T *)(p->ws + p->o_zscale);
+        tz.ey = (const T *)(p->ws + p->o_ez);
+        const ColTw ztw{p->ws + p->o_twz, nullptr, nullptr, nullptr, p->ws + p->o_twz8};
+        cudaError_t e = cudaSuccess;
         for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) {
-            e = ypass(S0, S1, COL_FWD);
-            if (e == cudaSuccess) e = zpass(S1, S1, COL_DIFFUSE);
-            if (e == cudaSuccess) e = ypass(S1, S0, COL_INV);
-            if (e != cudaSuccess) break;
-            e = (k + 1 < nsteps) ? rows_mid(S0, S0, u) : rows(S0, u, 1);
+            e = rows_diff(k == 0 ? u0 : u, u);
+            if (e == cudaSuccess)
+                e = launch(p, FFTPDE_KERNEL_COL, [&] {
+                    return launch_cols<T>(p->ny, u, u, p->nx, stride, batch, COL_DIFFUSE, ctw(), ty, p->stream);
+                });
+            if (e == cudaSuccess)
+                e = launch(p, FFTPDE_KERNEL_COL, [&] {
+                    return launch_cols<T>(p->nz, u, u, p->nx * p->ny, p->nx * p->ny * p->nz, 1, COL_DIFFUSE, ztw, tz,
+                                          p->stream);
+                });
         }
         return e;
     }
@@ -1705,6 +1717,7 @@ fftpde_status fftpde_plan_3d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     p->o_ez = take((size_t)nz * er);
     p->o_kxy2 = take((size_t)(nx * ny) * er);
     p->o_exy = take((size_t)(nx * ny) * er);
+    p->o_zscale = take((size_t)(nx * ny) * er);
     p->o_scr = take(2 * (size_t)(nz * nx * ny) * ec);
     p->need = off;
     return FFTPDE_OK;
@@ -1721,6 +1734,11 @@ fftpde_status ensure_diffusion_tables3(fftpde_plan p, double D, double dt)
     for (int64_t z = 0; z < p->nz; ++z) ez[(size_t)z] = std::exp(-D * p->kz2[(size_t)z] * dt);
     fftpde_status s = upload(p, p->o_exy, exy);
     if (s == FFTPDE_OK) s = upload(p, p->o_ez, ez);
+    // separable form (R26): x factor / (nx ny) in the rows (2D tables), y factor in
+    // the y-pass, z factor / nz in the z-pass (the z-pass operator slot is
+    // (line, element) = (1/nz, ez[c]))
+    if (s == FFTPDE_OK) s = ensure_diffusion_tables(p, D, dt);
+    if (s == FFTPDE_OK) s = upload(p, p->o_zscale, std::vector<double>(p->kxy2.size(), 1.0 / (double)p->nz));
     if (s != FFTPDE_OK) return s;
     p->diff3_valid = true;
     p->diff3_D = D;
