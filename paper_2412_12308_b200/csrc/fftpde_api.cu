@@ -640,9 +640,39 @@ template <typename T> struct Passes {
             return p->is3d ? zpass_sh(at(in, i), at(out, i), op, rk(i)) : cols_sh(at(in, i), at(out, i), op, rk(i));
         });
     }
+    // 2D diffusion step in the separable form (R26): x diffusion of the row slab,
+    // exchange, y diffusion of the column slab, exchange back (one row pass per step
+    // instead of a forward and an inverse one)
+    cudaError_t diff_step_sh(const void *in, void *out)
+    {
+        cudaError_t e = each([&](int i) {
+            return launch(p, FFTPDE_KERNEL_ROW, [&] {
+                if (p->rowP)
+                    return launch_rows2<T>(p->nx, at(in, i), shA(i), nullptr, p->R, p->R * p->nx, 1, ROW_DIFF, rtw(),
+                                           p->stream, rowmul());
+                return launch_rows<T>(p->nx, at(in, i), shA(i), nullptr, p->R, p->R * p->nx, 1, ROW_DIFF, rtw(),
+                                      p->stream, rowmul());
+            });
+        });
+        if (e == cudaSuccess) e = each([&](int i) { return pack_sh(shA(i), shB(i), 0); });
+        if (e == cudaSuccess) e = exchange(&Passes::shB, &Passes::shC);
+        if (e == cudaSuccess)
+            e = each([&](int i) {
+                OpTables<T> t = tables<T>(p);
+                t.ex = (const T *)(p->ws + p->o_one);
+                return launch(p, FFTPDE_KERNEL_COL, [&] {
+                    return launch_cols<T>(p->ny, shC(i), shC(i), p->BW, p->ny * p->BW, 1, COL_DIFFUSE, ctw(), t,
+                                          p->stream);
+                });
+            });
+        if (e == cudaSuccess) e = exchange(&Passes::shC, &Passes::shB);
+        if (e == cudaSuccess) e = each([&](int i) { return pack_sh(shB(i), at(out, i), 1); });
+        return e;
+    }
     // one step: slab -> exchange -> column-slab pass with the operator -> exchange -> slab
     cudaError_t step_sh(const void *in, void *out, int op)
     {
+        if (op == COL_DIFFUSE && !p->is3d) return diff_step_sh(in, out);
         cudaError_t e = to_columns(in);
         if (e == cudaSuccess) e = colpass_sh(shC(0), shC(0), op);
         if (e == cudaSuccess) e = from_columns(out);

@@ -130,16 +130,25 @@ def test_sharded_plan_loopback_vs_oracle(dtype, tol, P):
     assert rel(p.diffuse(xd, 2e-4, 0.01, 3).cpu().numpy(), O.diffuse(x, 2e-4, 0.01, 3, 1.5, 0.75)) <= tol
 
 
-def test_sharded_plan_loopback_bitwise_equals_python_slab_solver():
-    # the in-library step and the Python SlabSolver (same kernels, same order) agree bit for bit
+def test_sharded_plan_rank_count_independence_and_python_slab_solver():
+    # the in-library diffusion step is the separable one (R26: x diffusion of the row
+    # slab, exchange, y diffusion of the column slab): bit-for-bit independent of the
+    # rank count, and within rounding of the Python SlabSolver's 2D multiply; Poisson
+    # takes the same kernels in the same order as the SlabSolver: bit for bit
     nx, ny = 512, 256
     x = I.white_noise((ny, nx), 305)
+    outs = []
     for P in (1, 4):
-        u_lib = F.ShardedPlan(nx, ny, loopback=P).diffuse(torch.from_numpy(x).cuda(), 1e-4, 0.01, 3).cpu().numpy()
+        pl = F.ShardedPlan(nx, ny, loopback=P)
+        u_lib = pl.diffuse(torch.from_numpy(x).cuda(), 1e-4, 0.01, 3).cpu().numpy()
+        p_lib = pl.poisson(torch.from_numpy(x).cuda()).cpu().numpy()
         u_py, p_py = run(nx, ny, P, torch.complex128, x, 1e-4, 0.01, 3)
-        assert np.array_equal(u_lib, u_py)
+        assert rel(u_lib, u_py) <= 1e-14
+        assert np.array_equal(p_lib, p_py)
+        outs.append(u_lib)
+    assert np.array_equal(outs[0], outs[1])
     u1 = F.ShardedPlan(nx, ny).diffuse(torch.from_numpy(x).cuda(), 1e-4, 0.01, 3).cpu().numpy()
-    assert np.array_equal(u1, u_lib)                     # NCCL P = 1 == loopback P = 4
+    assert np.array_equal(u1, outs[1])                   # NCCL P = 1 == loopback P = 4
 
 
 def test_sharded_plan_long_axes():
