@@ -347,6 +347,9 @@ def native(args, wl, world, rank, local):
         "avg_launch_us": round(dom_avg_s * 1e6, 2),
         "share_of_step": round(dom_ms / total_prof, 3) if total_prof else None,
         "alg_bytes_per_launch": alg_bytes_per_launch(wl, dom_name),
+        # DRAM bytes per launch (ncu, caches flushed) / algorithmic bytes: the implied
+        # number of field round trips relative to the one the method needs
+        "traffic_over_alg": round(traffic / alg_bytes_per_launch(wl, dom_name), 3) if traffic else None,
         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
                        else "fallback 6650 GB/s (B200_PROFILING.md)",
         "per_kernel_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in prof.items()},
