@@ -136,7 +136,7 @@ def alg_bytes_per_launch(wl, kernel_class):
     # the complex 2D diffusion is separable: each step is one row pass (forward,
     # x factor, inverse) and one column pass, each reading and writing the field
     # once; the wave, the real-field and the 3D diffusion keep the MID row pass
-    mid_rows = wl.op == "wave" or (wl.op == "diffuse" and wl.dtype in ("f64", "f32"))
+    mid_rows = wl.op == "wave"
     if kernel_class == "row_pass" and mid_rows and wl.nsteps > 1:
         n = wl.nsteps                      # per field: 1 FWD + (n-1) MID + 1 INV launches
         return (2 * field * 2 + 3 * field * (n - 1)) / (n + 1)

@@ -743,13 +743,27 @@ template <typename T> struct Passes {
         if (e == cudaSuccess) e = rc(S, out, nullptr, RC_INV);
         return e;
     }
+    // separable diffusion of real fields (R26): per step the x diffusion of every
+    // real row (half-spectrum round trip inside the row pass, RC_DIFF) and the y
+    // diffusion of every column, done on the real field viewed as nx/2 complex
+    // columns (pairs of real columns: the y operator is real, so it acts on the
+    // pair's real and imaginary parts independently); in place, u materialised
     cudaError_t diffuse_real(const void *u0, void *u, int64_t nsteps)
     {
-        void *S = hscr(0);
-        cudaError_t e = rc(u0, S, nullptr, RC_FWD);
+        OpTables<T> ty = tables<T>(p);
+        ty.ex = (const T *)(p->ws + p->o_one);
+        cudaError_t e = cudaSuccess;
         for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) {
-            e = colsr(S, S, COL_DIFFUSE);
-            if (e == cudaSuccess) e = (k + 1 < nsteps) ? rc(S, S, u, RC_MID) : rc(S, u, nullptr, RC_INV);
+            const void *src = k == 0 ? u0 : u;
+            e = launch(p, FFTPDE_KERNEL_ROW, [&] {
+                return launch_rc_rows<T>(p->nx, src, u, nullptr, p->ny * batch, p->pitch, RC_DIFF, p->ws + p->o_twm,
+                                         p->ws + p->o_twr, p->stream, p->ws + p->o_ex);
+            });
+            if (e == cudaSuccess)
+                e = launch(p, FFTPDE_KERNEL_COL, [&] {
+                    return launch_cols<T>(p->ny, u, u, p->nx / 2, p->ny * (p->nx / 2), batch, COL_DIFFUSE, ctw(), ty,
+                                          p->stream);
+                });
         }
         return e;
     }

@@ -104,10 +104,12 @@ template <typename T>
 cudaError_t launch_mean(const void *U, void *out, int64_t nx, int64_t ny, cudaStream_t st);
 
 // ---- real-to-complex row passes (rc.cu) ----
-enum RcOp { RC_FWD = 0, RC_INV = 1, RC_MID = 2 };
+// RC_DIFF: real row -> half spectrum, times mul[a], -> real row (the x factor of
+// a separable operator), in one pass
+enum RcOp { RC_FWD = 0, RC_INV = 1, RC_MID = 2, RC_DIFF = 3 };
 template <typename T>
 cudaError_t launch_rc_rows(int64_t nx, const void *in, void *out, void *out2, int64_t nrows, int64_t pitch, int op,
-                           const void *tw, const void *twr, cudaStream_t st);
+                           const void *tw, const void *twr, cudaStream_t st, const void *mul = nullptr);
 
 // ---- diagonal k-space operators (kspace.cu) ----
 enum KOp { KOP_LAPLACIAN = 0, KOP_DX = 1, KOP_DY = 2, KOP_DIFFSRC = 3 };
