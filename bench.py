@@ -333,11 +333,13 @@ def native(args, wl, world, rank, local):
         pass
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = alg_bytes_per_launch(wl, dom_name) / dom_avg_s / 1e9
-    traffic = None
+    traffic, pipe_pct = None, None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{wl.name}.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dom_name)
+            tj = json.load(open(tpath))
+            traffic = tj.get(dom_name)
+            pipe_pct = (tj.get("_pipe_pct") or {}).get(dom_name)
         except Exception:
             traffic = None
     roofline = {
@@ -350,6 +352,8 @@ def native(args, wl, world, rank, local):
         # DRAM bytes per launch (ncu, caches flushed) / algorithmic bytes: the implied
         # number of field round trips relative to the one the method needs
         "traffic_over_alg": round(traffic / alg_bytes_per_launch(wl, dom_name), 3) if traffic else None,
+        # FP64 / FP32-FMA pipe utilisation of the dominant class from the same ncu capture
+        "pipe_active_pct": pipe_pct,
         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
                        else "fallback 6650 GB/s (B200_PROFILING.md)",
         "per_kernel_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in prof.items()},

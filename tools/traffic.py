@@ -57,6 +57,9 @@ def main():
     rows = list(csv.reader(txt.splitlines()))
     h = rows[0]
     ki, rd, wr = h.index("Kernel Name"), h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum")
+    fp = next((h.index(m) for m in ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",) if m in h), None)
+    fp32 = next((h.index(m) for m in ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",) if m in h),
+                None)
     units = rows[1]
 
     def val(row, i):
@@ -64,11 +67,17 @@ def main():
         u = units[i].strip().lower()
         return v * {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}.get(u, 1)
 
-    acc = {}
+    acc, pipes = {}, {}
     for row in rows[2:]:
         cls = classify(row[ki])
         acc.setdefault(cls, []).append((val(row, rd) + val(row, wr), row[ki][:160]))
+        if fp is not None:
+            pipes.setdefault(cls, []).append((float(row[fp].replace(",", "")),
+                                              float(row[fp32].replace(",", "")) if fp32 is not None else 0.0))
     res = {c: round(sum(b for b, _ in v) / len(v)) for c, v in acc.items()}
+    # pipe utilisation of the class: FP64 pipe, FP32 FMA pipe, % of peak while active
+    res["_pipe_pct"] = {c: {"fp64": round(sum(a for a, _ in v) / len(v), 1), "fp32_fma": round(sum(b for _, b in v) / len(v), 1)}
+                        for c, v in pipes.items()}
     res["_launches"] = {c: len(v) for c, v in acc.items()}
     res["_kernels"] = {c: sorted({k for _, k in v}) for c, v in acc.items()}
     res["_source"] = ("ncu --set full --clock-control none (caches flushed before each replay): "
@@ -76,7 +85,7 @@ def main():
                       + os.path.basename(rep))
     with open(out, "w") as f:
         json.dump(res, f, indent=1)
-    print(json.dumps({k: v for k, v in res.items() if not k.startswith("_")}))
+    print(json.dumps({k: v for k, v in res.items() if not k.startswith("_") or k == "_pipe_pct"}))
 
 
 if __name__ == "__main__":
