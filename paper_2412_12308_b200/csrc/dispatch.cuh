@@ -377,14 +377,7 @@ cudaError_t col2_n(Col2Args<T> g, int64_t batch, const OpTables<T> &tab, cudaStr
 {
     using Cfg = Col2Cfg<T, P, Q>;
     auto k = col2_kernel<T, P, Q, OP, Cfg::CL, Cfg::NT, Cfg::MINB, Cfg::EMAX>;
-    // FFTPDE_COL2_SMEM (bytes, experiments): reserve more shared memory per CTA than
-    // the kernel uses, which caps the clusters in flight (and with them the
-    // L2-resident intermediates) without recompiling
-    static const size_t smem = [] {
-        const char *e = std::getenv("FFTPDE_COL2_SMEM");
-        const size_t want = e ? (size_t)std::atoll(e) : 0;
-        return want > Cfg::SMEM ? want : Cfg::SMEM;
-    }();
+    constexpr size_t smem = Cfg::SMEM;
     static SmemOptIn<decltype(k)> opt;
     cudaError_t e = opt(k, smem);
     if (e != cudaSuccess) return e;

@@ -3,6 +3,7 @@
 #include <vector>
 #include <cmath>
 #include "../paper_2412_12308_b200/csrc/col2.cuh"
+#include "experimental/col2_phase.cuh"
 using namespace fftpde;
 static void stage_tw(long n, int emax, std::vector<double2>& tw) {
     long E = n < emax ? n : emax; tw.clear();

@@ -10,6 +10,7 @@
 #include "experimental/rr.cuh"
 #include "../paper_2412_12308_b200/csrc/tmacols.cuh"
 #include <cudaTypedefs.h>
+#include "experimental/wave_line.cuh"
 using namespace fftpde;
 
 static const char *g_filter = nullptr;

@@ -9,6 +9,7 @@
 #include "../paper_2412_12308_b200/csrc/pipe.cuh"
 #include "experimental/rr.cuh"
 #include "experimental/tpipe.cuh"
+#include "experimental/wave_line.cuh"
 using namespace fftpde;
 
 static const char *g_filter = nullptr;

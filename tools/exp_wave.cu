@@ -10,6 +10,7 @@
 #include "../paper_2412_12308_b200/csrc/tmacols.cuh"
 #include "../paper_2412_12308_b200/csrc/kernels.cuh"
 #include <cudaTypedefs.h>
+#include "experimental/tma_wave1.cuh"
 using namespace fftpde;
 
 static const char *g_filter = nullptr;
