@@ -312,6 +312,9 @@ int main(int argc, char **argv)
     line_var<D, 1024, 32, 4, false, LN_MID, 2>(X, Y, P, n, n, 1, t32, tab, "c2 rowsMID");
     line_var<D, 1024, 32, 8, false, LN_MID, 1>(X, Y, P, n, n, 1, t32, tab, "c2 rowsMID");
     line_var<D, 1024, 32, 4, true, LN_DIFFUSE, 2>(Y, Y, nullptr, n, n, 1, t32, tab, "c2 colsDIF");
+    line_var<D, 1024, 32, 8, true, LN_DIFFUSE, 1>(Y, Y, nullptr, n, n, 1, t32, tab, "c2 colsDIF");
+    line_var<D, 1024, 32, 1, false, LN_DIFFUSE, 4>(Y, Y, nullptr, n, n, 1, t32, tab, "c2 rowsDIF");
+    line_var<D, 1024, 32, 2, false, LN_DIFFUSE, 4>(Y, Y, nullptr, n, n, 1, t32, tab, "c2 rowsDIF");
     line_var<D, 1024, 32, 2, true, LN_DIFFUSE, 4>(Y, Y, nullptr, n, n, 1, t32, tab, "c2 colsDIF");
     line_var<D, 1024, 32, 1, false, LN_DIFFUSE, 8>(Y, Y, nullptr, n, n, 1, t32, tab, "c2 TrowsDIF");
     line_var<D, 1024, 16, 1, false, LN_DIFFUSE, 7>(Y, Y, nullptr, n, n, 1, t16, tab, "c2 TrowsDIF");
