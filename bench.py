@@ -67,7 +67,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="c5: use the slab-decomposed path even on one GPU (P = 1 process group)")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer", "lib"],
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer", "lib", "fused"],
                     help="sharded c5: pack + NCCL all-to-all, or direct peer stores into torch "
                          "symmetric memory (fftpde_peer_transpose, SURVEY.md 8(e) N10)")
     return ap.parse_args()
@@ -476,6 +476,8 @@ def sharded_native(args, wl, world, rank, local):
         ops = S.CudaLocalOps(wl.nx, wl.ny, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly)
     if args.exchange == "peer":
         solver = S.PeerSlabSolver(wl.nx, wl.ny, S.SymmetricPeerComm(), ops)
+    elif args.exchange == "fused":   # row pass stores straight into the peers' column slabs
+        solver = S.FusedPeerSlabSolver(wl.nx, wl.ny, S.SymmetricPeerComm(), ops)
     elif args.exchange == "nccl":
         solver = S.SlabSolver(wl.nx, wl.ny, S.DistComm(), ops)
     out = [torch.empty_like(slab)]
@@ -525,6 +527,7 @@ def sharded_native(args, wl, world, rank, local):
         "config": {**workload_config(wl, world),
                    "parallelism": f"slab x{world} " + {
                        "peer": "(peer-store exchange, symmetric memory)",
+                       "fused": "(row pass stores into the peers' column slabs, symmetric memory; separable diffusion)",
                        "nccl": "(NCCL all-to-all, Python-driven)",
                        "lib": "(NCCL all-to-all inside libfftpde, fftpde_plan_2d_sharded)"}[args.exchange],
                    "l2": "field (16 GiB) larger than L2"},

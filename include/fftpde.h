@@ -307,8 +307,26 @@ fftpde_status fftpde_wave_rk4(fftpde_plan plan, void *u, void *ut, double c,
 fftpde_status fftpde_peer_transpose(fftpde_plan plan, const void *src, void *const *peers, int npeers, int rank,
                                     int64_t R, int64_t bw, int direction);
 
+/* fftpde_rows_to_peers: the row pass of this rank's slab with the exchange fused
+ *   into its epilogue: the output element a of row k is
+ *   stored straight into peers[a / bw] at row rank R + k, column a mod bw, of
+ *   that rank's column slab [npeers R][bw], bw = nx / npeers (a power of two).
+ *   plan: the plain complex 2D plan of the whole grid (ny = npeers R); in: the
+ *   row slab [R][nx] on the plan's device; peers: npeers peer-mapped device
+ *   pointers (<= 16; symmetric memory, CUDA IPC, or one device's buffers in a
+ *   single-process emulation).  op: FFTPDE_ROWS_FWD (forward transform along x,
+ *   PAPER.md:262-266) or FFTPDE_ROWS_DIFFUSE (forward, times
+ *   exp(-D kx^2 dt)/(nx ny), inverse: the x factor of the separable diffusion
+ *   step, R26; D, dt used).  Asynchronous on the plan's stream; the caller orders
+ *   it against the peers' next phase with a stream-ordered barrier. */
+#define FFTPDE_ROWS_FWD 0
+#define FFTPDE_ROWS_DIFFUSE 3
+fftpde_status fftpde_rows_to_peers(fftpde_plan plan, const void *in, void *const *peers, int npeers, int rank,
+                                   int64_t R, int op, double D, double dt);
+
 #define FFTPDE_OP_POISSON 2
 #define FFTPDE_OP_DIFFUSE 3
+#define FFTPDE_OP_DIFFUSE_Y 5     /* cols_slab: the y factor exp(-D ky^2 dt) alone (R26) */
 fftpde_status fftpde_rows(fftpde_plan plan, const void *in, void *out, int64_t nrows, int inverse);
 fftpde_status fftpde_cols_slab(fftpde_plan plan, const void *in, void *out, int64_t col0, int64_t ncols,
                                int op, double D, double dt);

@@ -106,7 +106,7 @@ cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
 
 template <typename T, int N, bool COLS, int OP>
 cudaError_t pipe_n(const void *in, void *out, PipeArgs args, const void *tw, const OpTables<T> &tab,
-                   cudaStream_t st)
+                   cudaStream_t st, const PeerOut &po = PeerOut{})
 {
     using C = typename cplx_t<T>::type;
     using Cfg = PipeCfg<T, N, COLS>;
@@ -131,7 +131,7 @@ cudaError_t pipe_n(const void *in, void *out, PipeArgs args, const void *tw, con
     args.ntiles = batch * args.groups;
     const int64_t grid = std::min<int64_t>(args.ntiles, (int64_t)occ * sm_count());
     return launch_pdl(k, dim3((unsigned)grid), dim3(THREADS), smem, st, (const C *)in, (C *)out, args, (const C *)tw,
-                      tab);
+                      tab, po);
 }
 
 // ---- occupancy-oriented line pass (line.cuh) ----------------------------------
@@ -149,7 +149,8 @@ template <int E> inline const void *tw_for(const ColTw &c) { return E == 8 ? c.t
 
 template <typename T, int N, int E, int W, bool COLS, int OP, int MINB>
 cudaError_t line_n(const void *in, void *out, void *out2, int64_t nlines, int64_t line_stride, int64_t elem_stride,
-                   int64_t stride, int64_t batch, const void *tw, const OpTables<T> &tab, cudaStream_t st)
+                   int64_t stride, int64_t batch, const void *tw, const OpTables<T> &tab, cudaStream_t st,
+                   const PeerOut &po = PeerOut{})
 {
     using C = typename cplx_t<T>::type;
     using L = LineSmem<C, N, E, W, COLS>;
@@ -160,12 +161,12 @@ cudaError_t line_n(const void *in, void *out, void *out2, int64_t nlines, int64_
     LineArgs a{nlines, line_stride, elem_stride, stride, (nlines + W - 1) / W, out2};
     const int64_t grid = batch * a.groups;
     return launch_pdl(k, dim3((unsigned)grid), dim3(W * (N / E)), L::BYTES, st, (const C *)in, (C *)out, a,
-                      (const C *)tw, tab);
+                      (const C *)tw, tab, po);
 }
 
 template <typename T, int N>
 cudaError_t rows_n(const void *in, void *out, void *out2, int64_t ny, int64_t stride, int64_t batch,
-                   int dir, const ColTw &ctw, cudaStream_t st, RowMul rm)
+                   int dir, const ColTw &ctw, cudaStream_t st, RowMul rm, const PeerOut &po)
 {
     OpTables<T> tab{};
     tab.scale = (T)1;
@@ -179,20 +180,20 @@ cudaError_t rows_n(const void *in, void *out, void *out2, int64_t ny, int64_t st
         const void *tw = tw_for<LP::E>(ctw);
         if (tw) {   // (a plan without this radix's table takes the pipe pass)
         if (dir == ROW_DIFF)
-            return line_n<T, N, LP::E, LP::W, false, LN_DIFFUSE, LP::MINB>(in, out, nullptr, ny, N, 1, stride, batch, tw, tab, st);
+            return line_n<T, N, LP::E, LP::W, false, LN_DIFFUSE, LP::MINB>(in, out, nullptr, ny, N, 1, stride, batch, tw, tab, st, po);
         if (dir == ROW_INV)
-            return line_n<T, N, LP::E, LP::W, false, LN_INV, LP::MINB>(in, out, nullptr, ny, N, 1, stride, batch, tw, tab, st);
+            return line_n<T, N, LP::E, LP::W, false, LN_INV, LP::MINB>(in, out, nullptr, ny, N, 1, stride, batch, tw, tab, st, po);
         if (dir == ROW_MID)
-            return line_n<T, N, LP::E, LP::W, false, LN_MID, LP::MINB>(in, out, out2, ny, N, 1, stride, batch, tw, tab, st);
-        return line_n<T, N, LP::E, LP::W, false, LN_FWD, LP::MINB>(in, out, nullptr, ny, N, 1, stride, batch, tw, tab, st);
+            return line_n<T, N, LP::E, LP::W, false, LN_MID, LP::MINB>(in, out, out2, ny, N, 1, stride, batch, tw, tab, st, po);
+        return line_n<T, N, LP::E, LP::W, false, LN_FWD, LP::MINB>(in, out, nullptr, ny, N, 1, stride, batch, tw, tab, st, po);
         }
     }
     const void *tw = ctw.tw;
     PipeArgs a{ny, N, 1, stride, batch, 0, dir, out2};
-    if (dir == ROW_DIFF) return pipe_n<T, N, false, PIPE_DIFFUSE>(in, out, a, tw, tab, st);
-    if (dir == ROW_INV) return pipe_n<T, N, false, PIPE_INV>(in, out, a, tw, tab, st);
-    if (dir == ROW_MID) return pipe_n<T, N, false, PIPE_MID>(in, out, a, tw, tab, st);
-    return pipe_n<T, N, false, PIPE_FWD>(in, out, a, tw, tab, st);
+    if (dir == ROW_DIFF) return pipe_n<T, N, false, PIPE_DIFFUSE>(in, out, a, tw, tab, st, po);
+    if (dir == ROW_INV) return pipe_n<T, N, false, PIPE_INV>(in, out, a, tw, tab, st, po);
+    if (dir == ROW_MID) return pipe_n<T, N, false, PIPE_MID>(in, out, a, tw, tab, st, po);
+    return pipe_n<T, N, false, PIPE_FWD>(in, out, a, tw, tab, st, po);
 }
 
 // ---- TMA column pass (tmacols.cuh): complex128 columns of 256..1024 points ----
@@ -430,7 +431,7 @@ cudaError_t launch_col2(int64_t ny, int64_t P, int op, Col2Args<T> g, int64_t ba
 // ---- long rows: DSMEM four-step on a cluster (row2d.cuh) ------------------------
 template <typename T, int P, int Q, int OP>
 cudaError_t row2d_n(const void *in, void *out, void *out2, int64_t ny, int64_t stride, int64_t batch,
-                    const ColTw &tw, cudaStream_t st, const void *mul = nullptr)
+                    const ColTw &tw, cudaStream_t st, const void *mul = nullptr, const PeerOut &po = PeerOut{})
 {
     using C = typename cplx_t<T>::type;
     // 32768-point rows: 16-CTA (non-portable) clusters, half a row's slice per CTA:
@@ -472,31 +473,32 @@ cudaError_t row2d_n(const void *in, void *out, void *out2, int64_t ny, int64_t s
     const int64_t g = std::min<int64_t>(nrows, ncl);          // persistent clusters
     cfg.gridDim = dim3((unsigned)(CL * g), 1, 1);
     e = cudaLaunchKernelEx(&cfg, k, (const C *)in, (C *)out, (C *)out2, nrows, ny, stride, (const C *)tw.twP,
-                           (const C *)tw.twQ, (const C *)tw.twN, (const T *)mul);
+                           (const C *)tw.twQ, (const C *)tw.twN, (const T *)mul, po);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
 template <typename T, int P, int Q>
 cudaError_t row2d_dir(const void *in, void *out, void *out2, int64_t ny, int64_t stride, int64_t batch, int dir,
-                      const ColTw &tw, cudaStream_t st, RowMul rm)
+                      const ColTw &tw, cudaStream_t st, RowMul rm, const PeerOut &po)
 {
     if (dir == ROW_DIFF) {
         if (!rm.mul) return cudaErrorInvalidValue;
-        return row2d_n<T, P, Q, R2D_DIFF>(in, out, nullptr, ny, stride, batch, tw, st, rm.mul);
+        return row2d_n<T, P, Q, R2D_DIFF>(in, out, nullptr, ny, stride, batch, tw, st, rm.mul, po);
     }
+    if (po.p[0] && dir != ROW_FWD) return cudaErrorInvalidValue;   // peer output: FWD and DIFF only
     if (dir == ROW_INV) return row2d_n<T, P, Q, R2D_INV>(in, out, nullptr, ny, stride, batch, tw, st);
     if (dir == ROW_MID) return row2d_n<T, P, Q, R2D_MID>(in, out, out2, ny, stride, batch, tw, st);
-    return row2d_n<T, P, Q, R2D_FWD>(in, out, nullptr, ny, stride, batch, tw, st);
+    return row2d_n<T, P, Q, R2D_FWD>(in, out, nullptr, ny, stride, batch, tw, st, nullptr, po);
 }
 
 template <typename T>
 cudaError_t launch_rows2(int64_t nx, const void *in, void *out, void *out2, int64_t ny, int64_t stride,
-                         int64_t batch, int dir, const ColTw &tw, cudaStream_t st, RowMul rm)
+                         int64_t batch, int dir, const ColTw &tw, cudaStream_t st, RowMul rm, PeerOut po)
 {
     switch (nx) {
-    case 16384: return row2d_dir<T, 128, 128>(in, out, out2, ny, stride, batch, dir, tw, st, rm);
-    case 32768: return row2d_dir<T, 128, 256>(in, out, out2, ny, stride, batch, dir, tw, st, rm);
+    case 16384: return row2d_dir<T, 128, 128>(in, out, out2, ny, stride, batch, dir, tw, st, rm, po);
+    case 32768: return row2d_dir<T, 128, 256>(in, out, out2, ny, stride, batch, dir, tw, st, rm, po);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -504,10 +506,10 @@ cudaError_t launch_rows2(int64_t nx, const void *in, void *out, void *out2, int6
 // ---- length dispatch -------------------------------------------------------
 template <typename T>
 cudaError_t launch_rows(int64_t n, const void *in, void *out, void *out2, int64_t ny, int64_t stride,
-                        int64_t batch, int dir, const ColTw &tw, cudaStream_t st, RowMul rm)
+                        int64_t batch, int dir, const ColTw &tw, cudaStream_t st, RowMul rm, PeerOut po)
 {
     switch (n) {
-#define X(L) case L: return rows_n<T, L>(in, out, out2, ny, stride, batch, dir, tw, st, rm);
+#define X(L) case L: return rows_n<T, L>(in, out, out2, ny, stride, batch, dir, tw, st, rm, po);
         FFTPDE_LEN_CASES(X)
 #undef X
     default: return cudaErrorInvalidValue;

@@ -343,6 +343,7 @@ const NcclApi &nccl()
 }
 
 template <typename T> struct Passes {
+    using Real = T;
     fftpde_plan p;
     int64_t batch, stride;
     const void *twx() const { return p->ws + p->o_twx; }
@@ -1453,10 +1454,12 @@ fftpde_status fftpde_cols_slab(fftpde_plan p, const void *in, void *out, int64_t
     if (ncols == 0) return FFTPDE_ERR_EMPTY;
     if (ncols < 0 || !is_pow2(ncols) || p->nx % ncols || col0 < 0 || col0 % ncols || col0 + ncols > p->nx)
         return FFTPDE_ERR_INVALID_ARG;
-    if (op != COL_POISSON && op != COL_DIFFUSE) return FFTPDE_ERR_INVALID_ARG;
+    if (op != COL_POISSON && op != COL_DIFFUSE && op != FFTPDE_OP_DIFFUSE_Y) return FFTPDE_ERR_INVALID_ARG;
     fftpde_status s = check_ptr(p, in);
     if (s == FFTPDE_OK) s = check_ptr(p, out);
     if (s != FFTPDE_OK) return s;
+    const bool yonly = op == FFTPDE_OP_DIFFUSE_Y;     // the y factor alone (separable diffusion, R26)
+    if (yonly) op = COL_DIFFUSE;
     if (op == COL_DIFFUSE) {
         if (!std::isfinite(D) || !std::isfinite(dt) || D < 0 || dt < 0) return FFTPDE_ERR_INVALID_ARG;
         DeviceGuard g(p->device);
@@ -1475,7 +1478,7 @@ fftpde_status fftpde_cols_slab(fftpde_plan p, const void *in, void *out, int64_t
         using T = decltype(tag);
         OpTables<T> t = tables<T>(p);
         t.kx2 += col0;             // global column col0 + c
-        t.ex += col0;
+        t.ex = yonly ? (const T *)(p->ws + p->o_one) : t.ex + col0;
         return launch(p, FFTPDE_KERNEL_COL, [&] {
             return launch_cols<T>(p->ny, in, out, ncols, ncols * p->ny, 1, op, ctw, t, p->stream);
         });
@@ -1602,6 +1605,46 @@ fftpde_status fftpde_peer_transpose(fftpde_plan p, const void *src, void *const 
     if (!g.ok) return FFTPDE_ERR_CUDA;
     ++p->launches;
     return cuda_status(launch_peer_transpose(src, pp, npeers, rank, R, bytes, direction, p->stream));
+}
+
+fftpde_status fftpde_rows_to_peers(fftpde_plan p, const void *in, void *const *peers, int npeers, int rank,
+                                   int64_t R, int op, double D, double dt)
+{
+    if (!p || !in || !peers || npeers < 1 || npeers > kMaxPeers || rank < 0 || rank >= npeers || R <= 0)
+        return FFTPDE_ERR_INVALID_ARG;
+    if (p->is3d || p->is_real || p->sharded) return FFTPDE_ERR_UNSUPPORTED;
+    if (!p->ws) return FFTPDE_ERR_WORKSPACE;
+    if (op != FFTPDE_ROWS_FWD && op != FFTPDE_ROWS_DIFFUSE) return FFTPDE_ERR_INVALID_ARG;
+    if (R * npeers != p->ny || p->nx % npeers || !is_pow2(p->nx / npeers)) return FFTPDE_ERR_INVALID_ARG;
+    fftpde_status s = check_ptr(p, in);
+    if (s != FFTPDE_OK) return s;
+    PeerOut po;
+    for (int q = 0; q < npeers; ++q) {
+        if (!peers[q] || ((uintptr_t)peers[q] & 15u)) return FFTPDE_ERR_INVALID_ARG;
+        po.p[q] = peers[q];
+    }
+    po.rank = rank;
+    po.R = R;
+    while (((int64_t)1 << po.bwlog) < p->nx / npeers) ++po.bwlog;
+    DeviceGuard g(p->device);
+    if (!g.ok) return FFTPDE_ERR_CUDA;
+    if (op == FFTPDE_ROWS_DIFFUSE) {
+        if (!std::isfinite(D) || !std::isfinite(dt) || D < 0 || dt < 0) return FFTPDE_ERR_INVALID_ARG;
+        s = ensure_diffusion_tables(p, D, dt);
+        if (s != FFTPDE_OK) return s;
+    }
+    const int dir = op == FFTPDE_ROWS_DIFFUSE ? ROW_DIFF : ROW_FWD;
+    return dispatch(p, 1, R * p->nx, [&](auto &ps) {
+        using T = typename std::remove_reference_t<decltype(ps)>::Real;
+        (void)sizeof(T);
+        return launch(p, FFTPDE_KERNEL_ROW, [&] {
+            if (p->rowP)
+                return launch_rows2<T>(p->nx, in, nullptr, nullptr, R, R * p->nx, 1, dir, ps.rtw(), p->stream,
+                                       ps.rowmul(), po);
+            return launch_rows<T>(p->nx, in, nullptr, nullptr, R, R * p->nx, 1, dir, ps.rtw(), p->stream,
+                                  ps.rowmul(), po);
+        });
+    });
 }
 
 // ---- sharded plans ---------------------------------------------------------------

@@ -5,6 +5,29 @@
 
 namespace fftpde {
 
+// Peer pointers of the slab exchange (pack.cu), passed by value.
+constexpr int kMaxPeers = 16;
+struct PeerPtrs {
+    void *p[kMaxPeers];
+};
+// Row-pass output scattered straight into the peers' column slabs (the exchange
+// fused into the row pass epilogue): element a of output row
+// k goes to p[a >> bwlog] at row rank R + k, column a & (bw - 1), of a [P R][bw]
+// column slab.  p[0] == nullptr: the ordinary store to `out`.
+struct PeerOut {
+    void *p[kMaxPeers] = {};
+    int rank = 0;
+    int bwlog = 0;
+    int64_t R = 0;
+};
+#ifdef __CUDACC__
+template <typename C> __device__ __forceinline__ C *peer_row_dst(const PeerOut &po, int64_t k, int64_t a)
+{
+    const int64_t bw = (int64_t)1 << po.bwlog;
+    return reinterpret_cast<C *>(po.p[a >> po.bwlog]) + ((int64_t)po.rank * po.R + k) * bw + (a & (bw - 1));
+}
+#endif
+
 enum ColOp { COL_FWD = 0, COL_INV = 1, COL_POISSON = 2, COL_DIFFUSE = 3 };   // == PipeOp
 
 // Device tables of the k-space multipliers; every multiplier includes the
@@ -43,7 +66,8 @@ struct RowMul {
 };
 template <typename T>
 cudaError_t launch_rows(int64_t n, const void *in, void *out, void *out2, int64_t ny, int64_t stride,
-                        int64_t batch, int dir, const ColTw &tw, cudaStream_t st, RowMul rm = {});
+                        int64_t batch, int dir, const ColTw &tw, cudaStream_t st, RowMul rm = {},
+                        PeerOut po = {});
 
 // Twiddle tables of the column axis: the single-level stage table of ny, and for
 // the two-level (cluster) column pass the stage tables of P and Q (ny = P Q)
@@ -65,7 +89,8 @@ void row2_split(int64_t nx, int64_t &P, int64_t &Q);
 // twP, twQ = radix-16 stage tables of P and Q; twN = split inter-phase table.
 template <typename T>
 cudaError_t launch_rows2(int64_t nx, const void *in, void *out, void *out2, int64_t ny, int64_t stride,
-                         int64_t batch, int dir, const ColTw &tw, cudaStream_t st, RowMul rm = {});
+                         int64_t batch, int dir, const ColTw &tw, cudaStream_t st, RowMul rm = {},
+                         PeerOut po = {});
 
 // Column pass along y (length ny) over nx columns, op in ColOp.
 template <typename T>
@@ -118,11 +143,6 @@ cudaError_t launch_kop(void *X, const void *S, int64_t nx, int64_t ny, int64_t b
                        const void *kx, const void *ky, const void *kx2, const void *ky2, double D, double dt,
                        cudaStream_t st);
 
-// Peer pointers of the slab exchange (pack.cu), passed by value.
-constexpr int kMaxPeers = 16;
-struct PeerPtrs {
-    void *p[kMaxPeers];
-};
 cudaError_t launch_peer_transpose(const void *src, const PeerPtrs &peers, int P, int rank, int64_t R,
                                   int64_t bw_bytes, int direction, cudaStream_t st);
 

@@ -54,7 +54,7 @@ template <int TPT, bool COLS> struct LnSync {
 template <typename T, int N, int E, int W, bool COLS, int OP, int MINB>
 __global__ void __launch_bounds__(W * (N / E), MINB)
 line_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>::type *out, LineArgs a,
-            const typename cplx_t<T>::type *__restrict__ tw, OpTables<T> tab)
+            const typename cplx_t<T>::type *__restrict__ tw, OpTables<T> tab, PeerOut po)
 {
     using C = typename cplx_t<T>::type;
     using S = Shape<N, E>;
@@ -120,6 +120,11 @@ line_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>:
         fft_tw<N, false, E>(v, sm, t, twp, sync);
     }
     if (active) {
+        if (!COLS && po.p[0]) {                     // rows scattered into the peers' column slabs
+#pragma unroll
+            for (int e = 0; e < E; ++e) *opaque_ptr(peer_row_dst<C>(po, line, t + TPT * e)) = v[e];
+            return;
+        }
         C *dst = opaque_ptr(out + base);
 #pragma unroll
         for (int e = 0; e < E; ++e) dst[e * estep] = v[e];

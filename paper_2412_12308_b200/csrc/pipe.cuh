@@ -100,7 +100,7 @@ __device__ __forceinline__ void bulk_wait(uint32_t mbar, uint32_t parity)
 template <typename T, int N, int W, bool COLS, int OP, int NBUF, int MINB = 1, bool TWREG = false, bool BULK = false>
 __global__ void __launch_bounds__(W * Shape<N>::TPT, MINB)
 pipe_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out, PipeArgs a,
-            const typename cplx_t<T>::type *__restrict__ tw, OpTables<T> tab)
+            const typename cplx_t<T>::type *__restrict__ tw, OpTables<T> tab, PeerOut po)
 {
     using C = typename cplx_t<T>::type;
     using S = Shape<N>;
@@ -247,7 +247,11 @@ pipe_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out, P
         }
         if constexpr (!COLS) {
             const int64_t base = line_base(tile, c, t);
-            if (base >= 0) {
+            if (base >= 0 && po.p[0]) {              // rows scattered into the peers' column slabs
+                const int64_t k = (tile - (tile / a.groups) * a.groups) * W + c;
+#pragma unroll
+                for (int e = 0; e < E; ++e) *opaque_ptr(peer_row_dst<C>(po, k, t + TPT * e)) = v[e];
+            } else if (base >= 0) {
                 C *dst = opaque_ptr(out + base);
 #pragma unroll
                 for (int e = 0; e < E; ++e) dst[e * estep] = v[e];

@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(Row2dGeom<typename cplx_t<T>::type, P, Q, CL>:
 row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>::type *out,
              typename cplx_t<T>::type *out2, int64_t nrows, int64_t ny, int64_t stride,
              const typename cplx_t<T>::type *__restrict__ twP, const typename cplx_t<T>::type *__restrict__ twQ,
-             const typename cplx_t<T>::type *__restrict__ twS, const T *__restrict__ mul)
+             const typename cplx_t<T>::type *__restrict__ twS, const T *__restrict__ mul, PeerOut po)
 {
     using C = typename cplx_t<T>::type;
     using G = Row2dGeom<C, P, Q, CL>;
@@ -260,19 +260,30 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
         }
         if constexpr (OP == R2D_FWD || OP == R2D_MID) {
             fwd_part(v);
-            C *dst = const_cast<C *>(row_ptr(out, row));
+            if (OP == R2D_FWD && po.p[0]) {          // scattered into the peers' column slabs
 #pragma unroll
-            for (int e = 0; e < 16; ++e) dst[k1 + Q * (tb + TB * e)] = v[e];
+                for (int e = 0; e < 16; ++e) *peer_row_dst<C>(po, row, k1 + Q * (tb + TB * e)) = v[e];
+            } else {
+                C *dst = const_cast<C *>(row_ptr(out, row));
+#pragma unroll
+                for (int e = 0; e < 16; ++e) dst[k1 + Q * (tb + TB * e)] = v[e];
+            }
         }
         if constexpr (OP == R2D_DIFF) {
             fwd_part(v);
 #pragma unroll
             for (int e = 0; e < 16; ++e) v[e] = cscale(v[e], __ldg(mul + k1 + Q * (tb + TB * e)));
             inv_part(v);
-            C *dst = const_cast<C *>(row_ptr(out, row));
+            if (po.p[0]) {                           // scattered into the peers' column slabs
 #pragma unroll
-            for (int e = 0; e < 16; ++e) dst[n1 + P * (ta + TA * e)] = v[e];
+                for (int e = 0; e < 16; ++e) *peer_row_dst<C>(po, row, n1 + P * (ta + TA * e)) = v[e];
+            } else {
+                C *dst = const_cast<C *>(row_ptr(out, row));
+#pragma unroll
+                for (int e = 0; e < 16; ++e) dst[n1 + P * (ta + TA * e)] = v[e];
+            }
         }
+
     }
     cl_wait_acquire();                       // no CTA leaves while others may still write its smem
 }

@@ -38,10 +38,11 @@ EXPORTS = [
     "fftpde_rows", "fftpde_cols_slab", "fftpde_pack_blocks",
     "fftpde_wave_rk4_scratch_size", "fftpde_wave_rk4",
     "fftpde_apply", "fftpde_diffuse_source_scratch_size", "fftpde_diffuse_source",
-    "fftpde_plan_3d", "fftpde_plan_2d_r2c", "fftpde_peer_transpose",
+    "fftpde_plan_3d", "fftpde_plan_2d_r2c", "fftpde_peer_transpose", "fftpde_rows_to_peers",
 ]
 KOP = {"laplacian": 0, "dx": 1, "dy": 2}
-OP_POISSON, OP_DIFFUSE = 2, 3
+OP_POISSON, OP_DIFFUSE, OP_DIFFUSE_Y = 2, 3, 5
+ROWS_FWD, ROWS_DIFFUSE = 0, 3
 
 
 class FFTPDEError(RuntimeError):
@@ -95,6 +96,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fftpde_plan_2d_sharded": (st, [ctypes.POINTER(p), i64, i64, u, dbl, dbl, u, p, u, u]),
         "fftpde_plan_3d_sharded": (st, [ctypes.POINTER(p), i64, i64, i64, u, dbl, dbl, dbl, u, p, u, u]),
         "fftpde_peer_transpose": (st, [p, p, ctypes.POINTER(p), u, u, i64, i64, u]),
+        "fftpde_rows_to_peers": (st, [p, p, ctypes.POINTER(p), u, u, i64, u, dbl, dbl]),
         "fftpde_diffuse_source_scratch_size": (ctypes.c_size_t, [p]),
         "fftpde_diffuse_source": (st, [p, p, p, p, dbl, dbl, i64, p, ctypes.c_size_t]),
         "fftpde_wave_rk4": (st, [p, p, p, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, i64, p, p,
@@ -372,6 +374,18 @@ class Plan:
         self._bind_stream()
         _check(self.lib.fftpde_peer_transpose(self._h, src.data_ptr(), arr, len(peers), int(rank), int(R), int(bw),
                                               int(direction)), "fftpde_peer_transpose")
+
+    def rows_to_peers(self, x: torch.Tensor, peers, rank: int, R: int, op: int = 0, D: float = 0.0,
+                      dt: float = 0.0):
+        """Row pass of this rank's [R, nx] slab with its output stored straight into
+        the peers' [ny, nx/P] column slabs (fftpde_rows_to_peers: the exchange fused
+        into the row pass); op 0 = forward transform, 3 = x diffusion (R26)."""
+        if x.dim() != 2 or tuple(x.shape) != (R, self.nx) or x.dtype != self.dtype or not x.is_contiguous():
+            raise ValueError("rows_to_peers: expected a contiguous [R, nx] slab of the plan's dtype")
+        arr = (ctypes.c_void_p * len(peers))(*[int(q) for q in peers])
+        self._bind_stream()
+        _check(self.lib.fftpde_rows_to_peers(self._h, x.data_ptr(), arr, len(peers), int(rank), int(R), int(op),
+                                             float(D), float(dt)), "fftpde_rows_to_peers")
 
     def pack_blocks(self, x: torch.Tensor, out: torch.Tensor, nrows: int, nblocks: int, bw: int,
                     direction: int):

@@ -50,6 +50,9 @@ class CudaLocalOps:
     def peer_transpose(self, src, peers, rank, R, bw, direction):
         return self.plan.peer_transpose(src, peers, rank, R, bw, direction)
 
+    def rows_to_peers(self, x, peers, rank, R, op, D=0.0, dt=0.0):
+        return self.plan.rows_to_peers(x, peers, rank, R, op, D, dt)
+
     @property
     def launches(self):
         return self.plan.launches
@@ -223,6 +226,54 @@ class PeerSlabSolver:
 
     diffuse = SlabSolver.diffuse
     poisson = SlabSolver.poisson
+
+
+class FusedPeerSlabSolver(PeerSlabSolver):
+    """The peer-store slab decomposition with the first exchange fused into the
+    row pass (fftpde_rows_to_peers: each row's output is stored straight into the
+    owners' column slabs).  Diffusion per step, in the
+    separable form (R26):
+        rows: x diffusion -> peers' column slabs Cs    | barrier
+        column slab: y diffusion in place
+        peer transpose 1: Cs -> every rank's A         | barrier
+    A holds the materialised field after every step; the next step's row pass
+    reads it, the last one is copied to the output slab.  Poisson: forward rows
+    -> peers, column pass (-1/|k|^2), peer transpose back, inverse rows."""
+
+    def diffuse(self, slabs, D, dt, nsteps, outs=None):
+        from . import fftpde as F
+        ops, R, BW = self.ops, self.R, self.BW
+        outs = outs if outs is not None else [ops.empty(s.shape) for s in slabs]
+        if nsteps == 0:
+            for s, o in zip(slabs, outs):
+                o.copy_(s)
+            return outs
+        for k in range(nsteps):
+            for i, r in enumerate(self.ranks):
+                ops.rows_to_peers(slabs[i] if k == 0 else self.A[i], self.Cs_ptrs, r, R, F.ROWS_DIFFUSE, D, dt)
+            self.comm.barrier()
+            for i, r in enumerate(self.ranks):
+                ops.cols_slab(self.Cs[i], self.Cs[i], r * BW, F.OP_DIFFUSE_Y, D, dt)
+                ops.peer_transpose(self.Cs[i], self.A_ptrs, r, R, BW, 1)
+            self.comm.barrier()
+        for i, _ in enumerate(self.ranks):
+            outs[i].copy_(self.A[i])
+        return outs
+
+    def poisson(self, slabs, outs=None):
+        from . import fftpde as F
+        ops, R, BW = self.ops, self.R, self.BW
+        outs = outs if outs is not None else [ops.empty(s.shape) for s in slabs]
+        for i, r in enumerate(self.ranks):
+            ops.rows_to_peers(slabs[i], self.Cs_ptrs, r, R, F.ROWS_FWD)
+        self.comm.barrier()
+        for i, r in enumerate(self.ranks):
+            ops.cols_slab(self.Cs[i], self.Cs[i], r * BW, F.OP_POISSON, 0.0, 0.0)
+            ops.peer_transpose(self.Cs[i], self.A_ptrs, r, R, BW, 1)
+        self.comm.barrier()
+        for i, _ in enumerate(self.ranks):
+            ops.rows(self.A[i], outs[i], True)
+        return outs
 
 
 def slab_rows(ny, world, rank):

@@ -19,9 +19,11 @@ def rel(a, b):
     return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / np.linalg.norm(np.ravel(b)))
 
 
-def run(nx, ny, P, dtype, x, D, dt, nsteps, Lx=1.0, Ly=1.0, peer=False):
+def run(nx, ny, P, dtype, x, D, dt, nsteps, Lx=1.0, Ly=1.0, peer=False, fused=False):
     ops = S.CudaLocalOps(nx, ny, dtype=dtype, Lx=Lx, Ly=Ly)
-    if peer:     # exchange by peer stores (fftpde_peer_transpose), P virtual ranks on one device
+    if fused:    # first exchange fused into the row pass (fftpde_rows_to_peers)
+        solver = S.FusedPeerSlabSolver(nx, ny, S.LoopbackPeerComm(P), ops)
+    elif peer:   # exchange by peer stores (fftpde_peer_transpose), P virtual ranks on one device
         solver = S.PeerSlabSolver(nx, ny, S.LoopbackPeerComm(P), ops)
     else:
         solver = S.SlabSolver(nx, ny, S.LoopbackComm(P), ops)
@@ -209,3 +211,44 @@ def test_sharded_plan_errors():
     assert p.lib.fftpde_rows(p._h, x.data_ptr(), x.data_ptr(), 64, 0) == F.ERR_UNSUPPORTED
     with pytest.raises(F.FFTPDEError):
         p.forward(x, out=x)                              # forward is out of place
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.complex128, 1e-12), (torch.complex64, 1e-5)])
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_fused_row_exchange_vs_oracle_and_library_plan(dtype, tol, P):
+    # the row pass stores its output straight into the owners' column slabs
+    # (SURVEY.md 8(e) N10); the separable diffusion step is the in-library one,
+    # so the result equals ShardedPlan's (pack + exchange) bit for bit
+    nx, ny, D, dt, n = 256, 128, 2e-4, 0.01, 3
+    x = I.white_noise((ny, nx), 111)
+    u, p = run(nx, ny, P, dtype, x, D, dt, n, Lx=1.5, Ly=0.75, fused=True)
+    assert rel(u, O.diffuse(x, D, dt, n, 1.5, 0.75)) <= tol
+    assert rel(p, O.poisson(x, 1.5, 0.75)) <= tol
+    lib = F.ShardedPlan(nx, ny, dtype=dtype, Lx=1.5, Ly=0.75, loopback=P)
+    u_lib = lib.diffuse(torch.from_numpy(x).to(dtype).cuda(), D, dt, n).cpu().numpy()
+    assert np.array_equal(u, u_lib)
+    _, p_peer = run(nx, ny, P, dtype, x, D, dt, n, Lx=1.5, Ly=0.75, peer=True)
+    assert np.array_equal(p, p_peer)                   # same kernels as the unfused peer path
+
+
+def test_fused_row_exchange_long_rows():
+    # 32768-point rows: the row2d cluster pass with its peer-store epilogue
+    nx, ny, P = 32768, 64, 4
+    x = I.white_noise((ny, nx), 112)
+    u, p = run(nx, ny, P, torch.complex128, x, 1e-9, 0.01, 2, fused=True)
+    assert rel(u, O.diffuse(x, 1e-9, 0.01, 2)) <= 1e-12
+    assert rel(p, O.poisson(x)) <= 1e-12
+
+
+def test_rows_to_peers_errors():
+    pl = F.Plan(64, 64)
+    x = torch.zeros(16, 64, dtype=torch.complex128, device="cuda")
+    cs = [torch.zeros(64, 16, dtype=torch.complex128, device="cuda") for _ in range(4)]
+    ptrs = [c.data_ptr() for c in cs]
+    pl.rows_to_peers(x, ptrs, 0, 16, F.ROWS_FWD)        # valid
+    with pytest.raises(F.FFTPDEError):
+        pl.rows_to_peers(x, ptrs[:3], 0, 16, F.ROWS_FWD)  # 3 ranks do not divide nx = 64 into a power of two
+    with pytest.raises(F.FFTPDEError):
+        pl.rows_to_peers(x, ptrs, 4, 16, F.ROWS_FWD)      # rank out of range
+    with pytest.raises(F.FFTPDEError):
+        pl.rows_to_peers(x, ptrs, 0, 16, 7)               # unknown op
