@@ -527,7 +527,7 @@ def sharded_native(args, wl, world, rank, local):
         "config": {**workload_config(wl, world),
                    "parallelism": f"slab x{world} " + {
                        "peer": "(peer-store exchange, symmetric memory)",
-                       "fused": "(row pass stores into the peers' column slabs, symmetric memory; separable diffusion)",
+                       "fused": "(row and column passes store into the peers' slabs, symmetric memory; separable diffusion)",
                        "nccl": "(NCCL all-to-all, Python-driven)",
                        "lib": "(NCCL all-to-all inside libfftpde, fftpde_plan_2d_sharded)"}[args.exchange],
                    "l2": "field (16 GiB) larger than L2"},

@@ -324,6 +324,18 @@ fftpde_status fftpde_peer_transpose(fftpde_plan plan, const void *src, void *con
 fftpde_status fftpde_rows_to_peers(fftpde_plan plan, const void *in, void *const *peers, int npeers, int rank,
                                    int64_t R, int op, double D, double dt);
 
+/* fftpde_cols_to_peers: the column pass of this rank's column slab [npeers R][bw]
+ *   (global columns rank bw .. rank bw + bw - 1) with the return exchange fused
+ *   into its epilogue: the output element of slab row y, local column c, is
+ *   stored straight into peers[y / R] at row y mod R, column rank bw + c, of that
+ *   rank's row slab [R][nx].  op: FFTPDE_OP_POISSON, FFTPDE_OP_DIFFUSE (the 2D
+ *   multiplier at the global wavenumbers) or FFTPDE_OP_DIFFUSE_Y (the y factor of
+ *   the separable step, R26).  The slab is used as the pass's scratch (its contents
+ *   are not preserved).  Same plan, peers and ordering rules as
+ *   fftpde_rows_to_peers. */
+fftpde_status fftpde_cols_to_peers(fftpde_plan plan, void *colslab, void *const *peers, int npeers, int rank,
+                                   int64_t R, int op, double D, double dt);
+
 #define FFTPDE_OP_POISSON 2
 #define FFTPDE_OP_DIFFUSE 3
 #define FFTPDE_OP_DIFFUSE_Y 5     /* cols_slab: the y factor exp(-D ky^2 dt) alone (R26) */

@@ -112,7 +112,7 @@ template <typename T> struct Col2Args {
 
 template <typename T, int P, int Q, int OP, int CL, int NT, int MINB, int EMAX>
 __global__ void __launch_bounds__(NT, MINB)
-col2_kernel(Col2Args<T> g, OpTables<T> tab)
+col2_kernel(Col2Args<T> g, OpTables<T> tab, PeerOut po)
 {
     using C = typename cplx_t<T>::type;
     constexpr int N = P * Q;
@@ -183,9 +183,15 @@ col2_kernel(Col2Args<T> g, OpTables<T> tab)
 #pragma unroll
                 for (int e = 0; e < E; ++e) v[e] = cmulw<false>(v[e], ldtw(g.twN + n1 * (t + TPT * e)));
             }
-            C *dst = opaque_ptr(F + base + (int64_t)(n1 + P * t) * g.nx + c);
+            if (inverse && po.p[0]) {               // final output -> the owners' row slabs
 #pragma unroll
-            for (int e = 0; e < E; ++e) st_h(dst + e * rstep, v[e], pol_st);
+                for (int e = 0; e < E; ++e)
+                    *opaque_ptr(peer_col_dst<C>(po, n1 + P * (t + TPT * e), col0 + c)) = v[e];
+            } else {
+                C *dst = opaque_ptr(F + base + (int64_t)(n1 + P * t) * g.nx + c);
+#pragma unroll
+                for (int e = 0; e < E; ++e) st_h(dst + e * rstep, v[e], pol_st);
+            }
             if (more) {
 #pragma unroll
                 for (int e = 0; e < E; ++e) v[e] = nv[e];

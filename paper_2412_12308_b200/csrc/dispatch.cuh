@@ -274,10 +274,10 @@ cudaError_t tma_cols_n(const void *in, void *out, int64_t nx, int64_t stride, in
 
 template <typename T, int N>
 cudaError_t cols_n(const void *in, void *out, int64_t nx, int64_t stride, int64_t batch, int op,
-                   const ColTw &ctw, const OpTables<T> &tab, cudaStream_t st)
+                   const ColTw &ctw, const OpTables<T> &tab, cudaStream_t st, const PeerOut &po = PeerOut{})
 {
     using LP = LinePolicy<T, N, true>;
-    if constexpr (TmaColPolicy<T, N>::ON) {
+    if constexpr (TmaColPolicy<T, N>::ON) if (!po.p[0]) {   // (peer output: the line / pipe passes)
         using TP = TmaColPolicy<T, N>;
         const void *tw = tw_for<TP::E>(ctw);
         cudaError_t e = cudaErrorNotSupported;
@@ -293,20 +293,20 @@ cudaError_t cols_n(const void *in, void *out, int64_t nx, int64_t stride, int64_
     if constexpr (LP::E > 0) {
         const void *tw = tw_for<LP::E>(ctw);
         if (tw) switch (op) {
-        case COL_FWD: return line_n<T, N, LP::E, LP::W, true, LN_FWD, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st);
-        case COL_INV: return line_n<T, N, LP::E, LP::W, true, LN_INV_SCALED, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st);
-        case COL_POISSON: return line_n<T, N, LP::E, LP::W, true, LN_POISSON, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st);
-        case COL_DIFFUSE: return line_n<T, N, LP::E, LP::W, true, LN_DIFFUSE, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st);
+        case COL_FWD: return line_n<T, N, LP::E, LP::W, true, LN_FWD, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st, po);
+        case COL_INV: return line_n<T, N, LP::E, LP::W, true, LN_INV_SCALED, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st, po);
+        case COL_POISSON: return line_n<T, N, LP::E, LP::W, true, LN_POISSON, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st, po);
+        case COL_DIFFUSE: return line_n<T, N, LP::E, LP::W, true, LN_DIFFUSE, LP::MINB>(in, out, nullptr, nx, 1, nx, stride, batch, tw, tab, st, po);
         default: return cudaErrorInvalidValue;
         }
     }
     const void *tw = ctw.tw;
     PipeArgs a{nx, 1, nx, stride, batch, 0, op, nullptr};
     switch (op) {
-    case COL_FWD: return pipe_n<T, N, true, PIPE_FWD>(in, out, a, tw, tab, st);
-    case COL_INV: return pipe_n<T, N, true, PIPE_INV_SCALED>(in, out, a, tw, tab, st);
-    case COL_POISSON: return pipe_n<T, N, true, PIPE_POISSON>(in, out, a, tw, tab, st);
-    case COL_DIFFUSE: return pipe_n<T, N, true, PIPE_DIFFUSE>(in, out, a, tw, tab, st);
+    case COL_FWD: return pipe_n<T, N, true, PIPE_FWD>(in, out, a, tw, tab, st, po);
+    case COL_INV: return pipe_n<T, N, true, PIPE_INV_SCALED>(in, out, a, tw, tab, st, po);
+    case COL_POISSON: return pipe_n<T, N, true, PIPE_POISSON>(in, out, a, tw, tab, st, po);
+    case COL_DIFFUSE: return pipe_n<T, N, true, PIPE_DIFFUSE>(in, out, a, tw, tab, st, po);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -374,7 +374,7 @@ template <typename T, int P, int Q> struct Col2Cfg {
 };
 
 template <typename T, int P, int Q, int OP>
-cudaError_t col2_n(Col2Args<T> g, int64_t batch, const OpTables<T> &tab, cudaStream_t st)
+cudaError_t col2_n(Col2Args<T> g, int64_t batch, const OpTables<T> &tab, cudaStream_t st, const PeerOut &po = PeerOut{})
 {
     using Cfg = Col2Cfg<T, P, Q>;
     auto k = col2_kernel<T, P, Q, OP, Cfg::CL, Cfg::NT, Cfg::MINB, Cfg::EMAX>;
@@ -396,19 +396,20 @@ cudaError_t col2_n(Col2Args<T> g, int64_t batch, const OpTables<T> &tab, cudaStr
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled(PDL_COL2) ? 2 : 1;
-    e = cudaLaunchKernelEx(&cfg, k, g, tab);
+    e = cudaLaunchKernelEx(&cfg, k, g, tab, po);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
 template <typename T, int P, int Q>
-cudaError_t col2_op(int op, Col2Args<T> g, int64_t batch, const OpTables<T> &tab, cudaStream_t st)
+cudaError_t col2_op(int op, Col2Args<T> g, int64_t batch, const OpTables<T> &tab, cudaStream_t st,
+                    const PeerOut &po = PeerOut{})
 {
     switch (op) {
     case COL_FWD: return col2_n<T, P, Q, C2_FWD>(g, batch, tab, st);
     case COL_INV: return col2_n<T, P, Q, C2_INV_SCALED>(g, batch, tab, st);
-    case COL_POISSON: return col2_n<T, P, Q, C2_POISSON>(g, batch, tab, st);
-    case COL_DIFFUSE: return col2_n<T, P, Q, C2_DIFFUSE>(g, batch, tab, st);
+    case COL_POISSON: return col2_n<T, P, Q, C2_POISSON>(g, batch, tab, st, po);
+    case COL_DIFFUSE: return col2_n<T, P, Q, C2_DIFFUSE>(g, batch, tab, st, po);
     case 4: return col2_n<T, P, Q, C2_WAVE>(g, batch, tab, st);
     default: return cudaErrorInvalidValue;
     }
@@ -416,14 +417,15 @@ cudaError_t col2_op(int op, Col2Args<T> g, int64_t batch, const OpTables<T> &tab
 
 template <typename T>
 cudaError_t launch_col2(int64_t ny, int64_t P, int op, Col2Args<T> g, int64_t batch,
-                        const OpTables<T> &tab, cudaStream_t st)
+                        const OpTables<T> &tab, cudaStream_t st,
+                        const PeerOut &po = PeerOut{})
 {
     switch (ny) {
-    case 2048: return col2_op<T, 32, 64>(op, g, batch, tab, st);
-    case 4096: return col2_op<T, 64, 64>(op, g, batch, tab, st);
-    case 8192: return col2_op<T, 64, 128>(op, g, batch, tab, st);
-    case 16384: return col2_op<T, 128, 128>(op, g, batch, tab, st);
-    case 32768: return col2_op<T, 128, 256>(op, g, batch, tab, st);
+    case 2048: return col2_op<T, 32, 64>(op, g, batch, tab, st, po);
+    case 4096: return col2_op<T, 64, 64>(op, g, batch, tab, st, po);
+    case 8192: return col2_op<T, 64, 128>(op, g, batch, tab, st, po);
+    case 16384: return col2_op<T, 128, 128>(op, g, batch, tab, st, po);
+    case 32768: return col2_op<T, 128, 256>(op, g, batch, tab, st, po);
     default: (void)P; return cudaErrorInvalidValue;
     }
 }
@@ -519,7 +521,7 @@ cudaError_t launch_rows(int64_t n, const void *in, void *out, void *out2, int64_
 template <typename T>
 cudaError_t launch_cols(int64_t ny, const void *in, void *out, int64_t nx, int64_t stride,
                         int64_t batch, int op, const ColTw &ctw, const OpTables<T> &tab,
-                        cudaStream_t st)
+                        cudaStream_t st, PeerOut po)
 {
     using C = typename cplx_t<T>::type;
     int64_t P = 0, Q = 0;
@@ -527,10 +529,10 @@ cudaError_t launch_cols(int64_t ny, const void *in, void *out, int64_t nx, int64
     if (P) {
         Col2Args<T> g{(C *)out, nullptr, (const C *)in, nx, stride, nx / Col2Geom<C>::W,
                       (const C *)ctw.twP, (const C *)ctw.twQ, (const C *)ctw.twN};
-        return launch_col2<T>(ny, P, op, g, batch, tab, st);
+        return launch_col2<T>(ny, P, op, g, batch, tab, st, po);
     }
     switch (ny) {
-#define X(L) case L: return cols_n<T, L>(in, out, nx, stride, batch, op, ctw, tab, st);
+#define X(L) case L: return cols_n<T, L>(in, out, nx, stride, batch, op, ctw, tab, st, po);
         FFTPDE_LEN_CASES(X)
 #undef X
     default: return cudaErrorInvalidValue;

@@ -1445,8 +1445,10 @@ fftpde_status fftpde_rows(fftpde_plan p, const void *in, void *out, int64_t nrow
     return cuda_status(e);
 }
 
-fftpde_status fftpde_cols_slab(fftpde_plan p, const void *in, void *out, int64_t col0, int64_t ncols,
-                               int op, double D, double dt)
+} // extern "C"
+namespace {
+fftpde_status cols_slab_impl(fftpde_plan p, const void *in, void *out, int64_t col0, int64_t ncols, int op, double D,
+                             double dt, const PeerOut &po)
 {
     if (!p) return FFTPDE_ERR_INVALID_ARG;
     if (p->is3d || p->is_real || p->sharded) return FFTPDE_ERR_UNSUPPORTED;
@@ -1480,12 +1482,39 @@ fftpde_status fftpde_cols_slab(fftpde_plan p, const void *in, void *out, int64_t
         t.kx2 += col0;             // global column col0 + c
         t.ex = yonly ? (const T *)(p->ws + p->o_one) : t.ex + col0;
         return launch(p, FFTPDE_KERNEL_COL, [&] {
-            return launch_cols<T>(p->ny, in, out, ncols, ncols * p->ny, 1, op, ctw, t, p->stream);
+            return launch_cols<T>(p->ny, in, out, ncols, ncols * p->ny, 1, op, ctw, t, p->stream, po);
         });
     };
     if (p->colP == 0 && P2) return FFTPDE_ERR_UNSUPPORTED;   // two-level tables not built for this plan
     e = p->dtype == FFTPDE_C128 ? run(0.0) : run(0.0f);
     return cuda_status(e);
+}
+} // namespace
+extern "C" {
+fftpde_status fftpde_cols_slab(fftpde_plan p, const void *in, void *out, int64_t col0, int64_t ncols,
+                               int op, double D, double dt)
+{
+    return cols_slab_impl(p, in, out, col0, ncols, op, D, dt, PeerOut{});
+}
+
+fftpde_status fftpde_cols_to_peers(fftpde_plan p, void *colslab, void *const *peers, int npeers, int rank, int64_t R,
+                                   int op, double D, double dt)
+{
+    if (!p || !colslab || !peers || npeers < 1 || npeers > kMaxPeers || rank < 0 || rank >= npeers || R <= 0)
+        return FFTPDE_ERR_INVALID_ARG;
+    if (R * npeers != p->ny || p->nx % npeers || !is_pow2(p->nx / npeers)) return FFTPDE_ERR_INVALID_ARG;
+    PeerOut po;
+    for (int q = 0; q < npeers; ++q) {
+        if (!peers[q] || ((uintptr_t)peers[q] & 15u)) return FFTPDE_ERR_INVALID_ARG;
+        po.p[q] = peers[q];
+    }
+    const int64_t bw = p->nx / npeers;
+    po.rank = rank;
+    po.R = R;
+    po.nx = p->nx;
+    while (((int64_t)1 << po.bwlog) < bw) ++po.bwlog;
+    // the column pass works in place on the slab (its scratch); the result goes to the peers
+    return cols_slab_impl(p, colslab, colslab, rank * bw, bw, op, D, dt, po);
 }
 
 fftpde_status fftpde_pack_blocks(fftpde_plan p, const void *in, void *out, int64_t nrows, int64_t nblocks,

@@ -10,21 +10,29 @@ constexpr int kMaxPeers = 16;
 struct PeerPtrs {
     void *p[kMaxPeers];
 };
-// Row-pass output scattered straight into the peers' column slabs (the exchange
-// fused into the row pass epilogue): element a of output row
-// k goes to p[a >> bwlog] at row rank R + k, column a & (bw - 1), of a [P R][bw]
-// column slab.  p[0] == nullptr: the ordinary store to `out`.
+// Pass output scattered straight into the peers' slabs (the exchanges of the slab
+// decomposition fused into the pass epilogues).  Row passes:
+// element a of output row k goes to p[a >> bwlog] at row rank R + k, column
+// a & (bw - 1), of a [P R][bw] column slab.  Column passes (on this rank's column
+// slab [P R][bw]): element y of local column c goes to p[y / R] at row y mod R,
+// column rank bw + c, of an [R][nx] row slab.  p[0] == nullptr: the ordinary store.
 struct PeerOut {
     void *p[kMaxPeers] = {};
     int rank = 0;
     int bwlog = 0;
     int64_t R = 0;
+    int64_t nx = 0;          // row-slab length (column passes)
 };
 #ifdef __CUDACC__
 template <typename C> __device__ __forceinline__ C *peer_row_dst(const PeerOut &po, int64_t k, int64_t a)
 {
     const int64_t bw = (int64_t)1 << po.bwlog;
     return reinterpret_cast<C *>(po.p[a >> po.bwlog]) + ((int64_t)po.rank * po.R + k) * bw + (a & (bw - 1));
+}
+template <typename C> __device__ __forceinline__ C *peer_col_dst(const PeerOut &po, int64_t y, int64_t c)
+{
+    const int64_t r = y / po.R;
+    return reinterpret_cast<C *>(po.p[r]) + (y - r * po.R) * po.nx + ((int64_t)po.rank << po.bwlog) + c;
 }
 #endif
 
@@ -96,7 +104,7 @@ cudaError_t launch_rows2(int64_t nx, const void *in, void *out, void *out2, int6
 template <typename T>
 cudaError_t launch_cols(int64_t ny, const void *in, void *out, int64_t nx, int64_t stride,
                         int64_t batch, int op, const ColTw &tw, const OpTables<T> &tab,
-                        cudaStream_t st);
+                        cudaStream_t st, PeerOut po = {});
 
 // Wave column pass: both fields, in place.
 template <typename T>

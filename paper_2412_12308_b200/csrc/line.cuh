@@ -120,9 +120,12 @@ line_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>:
         fft_tw<N, false, E>(v, sm, t, twp, sync);
     }
     if (active) {
-        if (!COLS && po.p[0]) {                     // rows scattered into the peers' column slabs
+        if (po.p[0]) {                              // scattered into the peers' slabs
 #pragma unroll
-            for (int e = 0; e < E; ++e) *opaque_ptr(peer_row_dst<C>(po, line, t + TPT * e)) = v[e];
+            for (int e = 0; e < E; ++e) {
+                C *d = COLS ? peer_col_dst<C>(po, t + TPT * e, line) : peer_row_dst<C>(po, line, t + TPT * e);
+                *opaque_ptr(d) = v[e];
+            }
             return;
         }
         C *dst = opaque_ptr(out + base);

@@ -5,7 +5,7 @@ namespace fftpde {
 template cudaError_t launch_rows<double>(int64_t, const void *, void *, void *, int64_t, int64_t, int64_t, int,
                                      const ColTw &, cudaStream_t, RowMul, PeerOut);
 template cudaError_t launch_cols<double>(int64_t, const void *, void *, int64_t, int64_t, int64_t, int,
-                                     const ColTw &, const OpTables<double> &, cudaStream_t);
+                                     const ColTw &, const OpTables<double> &, cudaStream_t, PeerOut);
 template cudaError_t launch_wave_cols<double>(int64_t, void *, void *, int64_t, int64_t, int64_t,
                                           const ColTw &, const OpTables<double> &, cudaStream_t);
 template cudaError_t launch_rows2<double>(int64_t, const void *, void *, void *, int64_t, int64_t, int64_t, int,

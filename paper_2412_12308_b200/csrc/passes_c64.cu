@@ -5,7 +5,7 @@ namespace fftpde {
 template cudaError_t launch_rows<float>(int64_t, const void *, void *, void *, int64_t, int64_t, int64_t, int,
                                      const ColTw &, cudaStream_t, RowMul, PeerOut);
 template cudaError_t launch_cols<float>(int64_t, const void *, void *, int64_t, int64_t, int64_t, int,
-                                     const ColTw &, const OpTables<float> &, cudaStream_t);
+                                     const ColTw &, const OpTables<float> &, cudaStream_t, PeerOut);
 template cudaError_t launch_wave_cols<float>(int64_t, void *, void *, int64_t, int64_t, int64_t,
                                           const ColTw &, const OpTables<float> &, cudaStream_t);
 template cudaError_t launch_rows2<float>(int64_t, const void *, void *, void *, int64_t, int64_t, int64_t, int,

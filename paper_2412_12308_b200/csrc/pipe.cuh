@@ -268,7 +268,16 @@ pipe_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out, P
             }
             __syncthreads();
             const int64_t base = line_base(tile, lc, lt);
-            if (base >= 0) {
+            if (base >= 0 && po.p[0]) {              // scattered into the owners' row slabs
+                const C *src = buf(slot, lc) + padidx(lt, S::LOGE);
+                const int64_t col = (tile - (tile / a.groups) * a.groups) * W + lc;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int o = TPT % E == 0 ? SmemView<C, S::LOGE, 1>::off(TPT * e)
+                                               : padidx(lt + TPT * e, S::LOGE) - padidx(lt, S::LOGE);
+                    *opaque_ptr(peer_col_dst<C>(po, lt + TPT * e, col)) = src[o];
+                }
+            } else if (base >= 0) {
                 const C *src = buf(slot, lc) + padidx(lt, S::LOGE);
                 C *dst = opaque_ptr(out + base);
 #pragma unroll

@@ -39,6 +39,7 @@ EXPORTS = [
     "fftpde_wave_rk4_scratch_size", "fftpde_wave_rk4",
     "fftpde_apply", "fftpde_diffuse_source_scratch_size", "fftpde_diffuse_source",
     "fftpde_plan_3d", "fftpde_plan_2d_r2c", "fftpde_peer_transpose", "fftpde_rows_to_peers",
+    "fftpde_cols_to_peers",
 ]
 KOP = {"laplacian": 0, "dx": 1, "dy": 2}
 OP_POISSON, OP_DIFFUSE, OP_DIFFUSE_Y = 2, 3, 5
@@ -97,6 +98,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fftpde_plan_3d_sharded": (st, [ctypes.POINTER(p), i64, i64, i64, u, dbl, dbl, dbl, u, p, u, u]),
         "fftpde_peer_transpose": (st, [p, p, ctypes.POINTER(p), u, u, i64, i64, u]),
         "fftpde_rows_to_peers": (st, [p, p, ctypes.POINTER(p), u, u, i64, u, dbl, dbl]),
+        "fftpde_cols_to_peers": (st, [p, p, ctypes.POINTER(p), u, u, i64, u, dbl, dbl]),
         "fftpde_diffuse_source_scratch_size": (ctypes.c_size_t, [p]),
         "fftpde_diffuse_source": (st, [p, p, p, p, dbl, dbl, i64, p, ctypes.c_size_t]),
         "fftpde_wave_rk4": (st, [p, p, p, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, i64, p, p,
@@ -386,6 +388,17 @@ class Plan:
         self._bind_stream()
         _check(self.lib.fftpde_rows_to_peers(self._h, x.data_ptr(), arr, len(peers), int(rank), int(R), int(op),
                                              float(D), float(dt)), "fftpde_rows_to_peers")
+
+    def cols_to_peers(self, cs: torch.Tensor, peers, rank: int, R: int, op: int, D: float = 0.0, dt: float = 0.0):
+        """Column pass of this rank's [ny, nx/P] column slab with its output stored
+        straight into the owners' [R, nx] row slabs (fftpde_cols_to_peers: the return
+        exchange fused into the column pass); the slab is used as scratch."""
+        if cs.dim() != 2 or cs.shape[0] != self.ny or cs.dtype != self.dtype or not cs.is_contiguous():
+            raise ValueError("cols_to_peers: expected a contiguous [ny, nx/P] slab of the plan's dtype")
+        arr = (ctypes.c_void_p * len(peers))(*[int(q) for q in peers])
+        self._bind_stream()
+        _check(self.lib.fftpde_cols_to_peers(self._h, cs.data_ptr(), arr, len(peers), int(rank), int(R), int(op),
+                                             float(D), float(dt)), "fftpde_cols_to_peers")
 
     def pack_blocks(self, x: torch.Tensor, out: torch.Tensor, nrows: int, nblocks: int, bw: int,
                     direction: int):

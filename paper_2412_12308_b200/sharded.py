@@ -53,6 +53,9 @@ class CudaLocalOps:
     def rows_to_peers(self, x, peers, rank, R, op, D=0.0, dt=0.0):
         return self.plan.rows_to_peers(x, peers, rank, R, op, D, dt)
 
+    def cols_to_peers(self, cs, peers, rank, R, op, D=0.0, dt=0.0):
+        return self.plan.cols_to_peers(cs, peers, rank, R, op, D, dt)
+
     @property
     def launches(self):
         return self.plan.launches
@@ -229,16 +232,16 @@ class PeerSlabSolver:
 
 
 class FusedPeerSlabSolver(PeerSlabSolver):
-    """The peer-store slab decomposition with the first exchange fused into the
-    row pass (fftpde_rows_to_peers: each row's output is stored straight into the
-    owners' column slabs).  Diffusion per step, in the
-    separable form (R26):
+    """The peer-store slab decomposition with both exchanges fused into the passes
+    (SURVEY.md 8(e) N10): the row pass stores each output row straight into the
+    owners' column slabs (fftpde_rows_to_peers) and the column pass stores each
+    output column straight back into the owners' row slabs (fftpde_cols_to_peers).
+    Diffusion per step, in the separable form (R26):
         rows: x diffusion -> peers' column slabs Cs    | barrier
-        column slab: y diffusion in place
-        peer transpose 1: Cs -> every rank's A         | barrier
+        columns: y diffusion -> peers' row slabs A     | barrier
     A holds the materialised field after every step; the next step's row pass
     reads it, the last one is copied to the output slab.  Poisson: forward rows
-    -> peers, column pass (-1/|k|^2), peer transpose back, inverse rows."""
+    -> peers, column pass (-1/|k|^2) -> peers, inverse rows."""
 
     def diffuse(self, slabs, D, dt, nsteps, outs=None):
         from . import fftpde as F
@@ -253,8 +256,7 @@ class FusedPeerSlabSolver(PeerSlabSolver):
                 ops.rows_to_peers(slabs[i] if k == 0 else self.A[i], self.Cs_ptrs, r, R, F.ROWS_DIFFUSE, D, dt)
             self.comm.barrier()
             for i, r in enumerate(self.ranks):
-                ops.cols_slab(self.Cs[i], self.Cs[i], r * BW, F.OP_DIFFUSE_Y, D, dt)
-                ops.peer_transpose(self.Cs[i], self.A_ptrs, r, R, BW, 1)
+                ops.cols_to_peers(self.Cs[i], self.A_ptrs, r, R, F.OP_DIFFUSE_Y, D, dt)
             self.comm.barrier()
         for i, _ in enumerate(self.ranks):
             outs[i].copy_(self.A[i])
@@ -268,8 +270,7 @@ class FusedPeerSlabSolver(PeerSlabSolver):
             ops.rows_to_peers(slabs[i], self.Cs_ptrs, r, R, F.ROWS_FWD)
         self.comm.barrier()
         for i, r in enumerate(self.ranks):
-            ops.cols_slab(self.Cs[i], self.Cs[i], r * BW, F.OP_POISSON, 0.0, 0.0)
-            ops.peer_transpose(self.Cs[i], self.A_ptrs, r, R, BW, 1)
+            ops.cols_to_peers(self.Cs[i], self.A_ptrs, r, R, F.OP_POISSON)
         self.comm.barrier()
         for i, _ in enumerate(self.ranks):
             ops.rows(self.A[i], outs[i], True)

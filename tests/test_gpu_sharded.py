@@ -231,6 +231,17 @@ def test_fused_row_exchange_vs_oracle_and_library_plan(dtype, tol, P):
     assert np.array_equal(p, p_peer)                   # same kernels as the unfused peer path
 
 
+@pytest.mark.parametrize("nx,ny,P", [(64, 256, 4), (32, 1024, 2), (16, 16384, 2)])
+def test_fused_exchanges_column_kernels(nx, ny, P):
+    # the column pass's peer-store epilogue through the pipelined (256-point: the
+    # TMA pass is bypassed for peer output), radix-32 line (1024) and col2 (16384)
+    # column passes
+    x = I.white_noise((ny, nx), 113)
+    u, p = run(nx, ny, P, torch.complex128, x, 3e-5, 0.01, 2, fused=True)
+    assert rel(u, O.diffuse(x, 3e-5, 0.01, 2)) <= 1e-12
+    assert rel(p, O.poisson(x)) <= 1e-12
+
+
 def test_fused_row_exchange_long_rows():
     # 32768-point rows: the row2d cluster pass with its peer-store epilogue
     nx, ny, P = 32768, 64, 4
