@@ -190,7 +190,10 @@ fftpde_status fftpde_inverse(fftpde_plan plan, const void *in, void *out);
  *   zero mean.
  * fftpde_diffuse: nsteps exact steps of u_t = D nabla^2 u from u0
  *   (ec:solCalorFourier PAPER.md:376-386, coefficient D per R6): each step is
- *   DFT2, multiply by exp(-D |k|^2 dt), iDFT2, and materialises u (R8).
+ *   DFT2, multiply by exp(-D |k|^2 dt), iDFT2, and materialises u (R8).  The
+ *   multiplier is separable, exp(-D kx^2 dt) exp(-D ky^2 dt), so a step is
+ *   computed as the 1D diffusion of every row followed by that of every column
+ *   (the same operator, R26; one read and one write of u per axis).
  *   D >= 0, dt >= 0, nsteps >= 0 (0 copies u0 to u).  k = 0 is kept.
  * fftpde_wave_step: nsteps exact steps of u_tt = c^2 nabla^2 u (s = 0,
  *   eq:wave_equation PAPER.md:417-424) on the state (u, ut) in place: with
