@@ -12,7 +12,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,temperature.gpu -
 for w in c2 c1 c3 c4 c5 c2r c3r c4r rk4 rk4big dsrc p3d d3d; do
   timeout 900 python bench.py --workload $w > "$OUT/bench_$w.json" 2> "$OUT/bench_$w.err"; echo "bench $w $?"
 done
-for ex in lib peer nccl; do
+for ex in lib peer nccl fused; do
   timeout 600 python bench.py --workload c5 --sharded --exchange $ex > "$OUT/bench_c5_sharded_p1_$ex.json" 2> "$OUT/bench_c5_sh_$ex.err"; echo "c5 sharded $ex $?"
 done
 for w in d3d p3d; do
