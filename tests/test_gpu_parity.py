@@ -194,6 +194,18 @@ def test_diffusion_shapes_and_zero_steps(dtype):
     assert np.array_equal(u0, x.astype(np.complex128))           # nsteps = 0 copies
 
 
+@pytest.mark.parametrize("dtype,ny,nx,B", [(C128, 1024, 1024, 2), (C128, 512, 128, 3), (C128, 256, 2048, 2),
+                                           (C64, 512, 512, 3), (C128, 2048, 64, 2), (C64, 1024, 32, 2)])
+def test_separable_diffusion_batched_across_kernel_families(dtype, ny, nx, B):
+    # the separable step (R26) through every row / column pass family, batched:
+    # radix-32 lines (1024 c128), TMA columns (256 / 512), pipelined rows
+    # (bulk-copied at 2048), c64 TMA radix-32 columns (512), col2 (2048 columns)
+    x = noise((B, ny, nx), 17, dtype)
+    p = F.Plan(nx, ny, batch=B, dtype=dtype, Lx=1.3, Ly=0.7)
+    u = host(p.diffuse(dev(x, dtype), 2e-3, 0.01, 3))
+    assert rel(u, O.diffuse(x.astype(np.complex128), 2e-3, 0.01, 3, 1.3, 0.7)) <= TOL[dtype]
+
+
 # ---------------------------------------------------------------- C3 wave
 
 def test_c3_wave_prefix_vs_stepped_oracle():
