@@ -163,7 +163,14 @@ class ClockSampler:
                 stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
-        time.sleep(0.3)
+        # wait for the first sample: nvidia-smi's NVML start-up (which takes driver
+        # locks) must be over before the timed region starts
+        t0 = time.perf_counter()
+        while self.proc is not None and time.perf_counter() - t0 < 5.0:
+            if os.path.getsize(self.path) > 0:
+                break
+            time.sleep(0.05)
+        time.sleep(0.15)
         return self
 
     def __exit__(self, *exc):
@@ -291,6 +298,11 @@ def native(args, wl, world, rank, local):
     vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
     smi_index = int(vis[gpu_index]) if len(vis) > gpu_index and vis[gpu_index].isdigit() else gpu_index
     with ClockSampler(smi_index) as clk:
+        # one more untimed step right before the timed ones: the GPU idled while the
+        # clock sampler started, and the first kernel after an idle period runs slow
+        reset_wave(wl, dev_in, out)
+        flush.zero_()
+        run_solve(plan, wl, dev_in, out)
         for i in range(args.steps):
             reset_wave(wl, dev_in, out)
             flush.zero_()
