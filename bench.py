@@ -303,6 +303,7 @@ def native(args, wl, world, rank, local):
         reset_wave(wl, dev_in, out)
         flush.zero_()
         run_solve(plan, wl, dev_in, out)
+        launches0 = plan.launches            # count the timed steps' launches only
         for i in range(args.steps):
             reset_wave(wl, dev_in, out)
             flush.zero_()
