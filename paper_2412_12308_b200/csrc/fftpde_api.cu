@@ -1183,8 +1183,8 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     }
     fftpde::row2_split(nx, p->rowP, p->rowQ);
     if (p->rowP) {
-        build_twiddles(p->rowP, p->rtwP, 16);
-        build_twiddles(p->rowQ, p->rtwQ, 16);
+        build_twiddles(p->rowP, p->rtwP, FFTPDE_R2D_E);
+        build_twiddles(p->rowQ, p->rtwQ, FFTPDE_R2D_E);
         build_split_twiddles(nx, p->rowP, p->rowQ, p->rtwN);
     }
 

@@ -55,6 +55,10 @@ constexpr int64_t kMaxLen2 = 32768;  // two-level (cluster) axis length limit
 
 // radix (elements per thread) of the sub-transforms of the two-level column pass;
 // the host builds its P and Q twiddle tables for the same factorisation
+// row2d (long rows): points per thread / radix of its in-register stages
+#ifndef FFTPDE_R2D_E
+#define FFTPDE_R2D_E 16
+#endif
 #ifndef FFTPDE_COL2_EMAX
 #define FFTPDE_COL2_EMAX 8
 #endif

@@ -12,7 +12,7 @@
 // and the A -> B exchange (7/8 of the row for CL = 8) goes CTA-to-CTA through
 // distributed shared memory (st.shared::cluster into the owner's receive
 // buffer), not through L2: HBM and L2 see one read and one write of the row.
-// Every thread holds 16 points in both phases (N/CL = 16 x threads).
+// Every thread holds R2E points in both phases (N/CL = R2E x threads).
 //
 // The inverse runs the phases in reverse (B^-1 then A^-1, conjugate kernels),
 // so its output is distributed exactly like the forward input: MID (inverse
@@ -79,15 +79,19 @@ __device__ __forceinline__ uint32_t cl_rank()
     return r;
 }
 
+// points per thread (the radix of the in-register stages) in both phases
+// (FFTPDE_R2D_E, launch.h: the host builds the stage tables with the same radix)
+constexpr int R2E = FFTPDE_R2D_E;
+
 template <typename C, int P, int Q, int CL> struct Row2dGeom {
     static constexpr int N = P * Q;
     static constexpr int PA = P / CL, QB = Q / CL;           // items per CTA in phases A and B
-    static constexpr int TA = Q / 16, TB = P / 16;           // threads per item
-    static constexpr int NT = PA * TA;                       // == QB * TB == N / (16 CL)
+    static constexpr int TA = Q / R2E, TB = P / R2E;         // threads per item
+    static constexpr int NT = PA * TA;                       // == QB * TB == N / (R2E CL)
     static constexpr int LPP = 128 / (int)sizeof(C);
     // exchange buffer: item-interleaved lanes -> pitch = 1 mod LPP/ (16 B lanes per phase)
-    static constexpr int SA = ((Shape<Q, 16>::PADDED + LPP - 1) / LPP) * LPP + 1;
-    static constexpr int SB = ((Shape<P, 16>::PADDED + LPP - 1) / LPP) * LPP + 1;
+    static constexpr int SA = ((Shape<Q, R2E>::PADDED + LPP - 1) / LPP) * LPP + 1;
+    static constexpr int SB = ((Shape<P, R2E>::PADDED + LPP - 1) / LPP) * LPP + 1;
     static constexpr int XE = PA * SA > QB * SB ? PA * SA : QB * SB;
     // receive buffer: phase-B input [jb][n1] (pitch P+1) or phase-A^-1 input [ia][k1] (pitch Q+1)
     static constexpr int RE = QB * (P + 1) > PA * (Q + 1) ? QB * (P + 1) : PA * (Q + 1);
@@ -98,12 +102,25 @@ template <typename C, int P, int Q, int CL> struct Row2dGeom {
     // all on the same banks
     static constexpr int A1 = 17, A2 = Q / 16 + 1, B1 = 17, B2 = P / 16 + 1;
     static constexpr int TWE = PA * (A1 + A2) + QB * (B1 + B2);
-    static constexpr size_t BYTES = (size_t)(XE + RE + TWE) * sizeof(C) + 16;   // + mbarrier
+    // input staging: the CTA's share of the next row, [e][thread]
+    static constexpr int SE = N / CL;
+    static constexpr size_t BYTES = (size_t)(XE + RE + TWE + SE) * sizeof(C) + 16;   // + mbarrier
     static_assert(NT == QB * TB, "thread counts of the phases must agree");
     static_assert(PA >= 1 && QB >= 1, "cluster too large for the split");
 };
 
-// Tables: twP, twQ = stage tables (radix 16) of P and Q; twS = split inter-phase
+// per-thread asynchronous global -> shared copy of one element (no register
+// destination, so no register scoreboard spans the row it is in flight for)
+__device__ __forceinline__ void r2_cp_async(const void *smem, const double2 *g)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(smem)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void r2_cp_async(const void *smem, const float2 *g)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(smem)), "l"(g) : "memory");
+}
+
+// Tables: twP, twQ = stage tables (radix R2E) of P and Q; twS = split inter-phase
 // twiddles, each entry rounded once from its exact angle:
 //   S1[n1][l] = w_N^{n1 l}      (l < 16)    at twS[n1*16 + l]
 //   S2[n1][h] = w_N^{16 n1 h}   (h < Q/16)  at twS[P*16 + n1*(Q/16) + h]
@@ -111,7 +128,7 @@ template <typename C, int P, int Q, int CL> struct Row2dGeom {
 //   U2[k1][h] = w_N^{16 k1 h}   (h < P/16)  at twS[P*16 + P*(Q/16) + Q*16 + k1*(P/16) + h]
 // w_N^{n1 k1} = S1[n1][k1 & 15] S2[n1][k1 >> 4] = U1[k1][n1 & 15] U2[k1][n1 >> 4].
 template <typename T, int P, int Q, int CL, int OP>
-__global__ void __launch_bounds__(Row2dGeom<typename cplx_t<T>::type, P, Q, CL>::NT)
+__global__ void __launch_bounds__(Row2dGeom<typename cplx_t<T>::type, P, Q, CL>::NT, (R2E <= 8 ? 2 : 1))
 row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>::type *out,
              typename cplx_t<T>::type *out2, int64_t nrows, int64_t ny, int64_t stride,
              const typename cplx_t<T>::type *__restrict__ twP, const typename cplx_t<T>::type *__restrict__ twQ,
@@ -127,7 +144,8 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
     C *TWA2 = TWA1 + PA * G::A1;            // [PA][Q/16]  (pitch A2)
     C *TWB1 = TWA2 + PA * G::A2;            // [QB][16]    (pitch B1)
     C *TWB2 = TWB1 + QB * G::B1;            // [QB][P/16]  (pitch B2)
-    const uint32_t mbar = smem_addr(TWB2 + QB * G::B2);
+    C *S = TWB2 + QB * G::B2;               // [R2E][NT]   next row's input
+    const uint32_t mbar = smem_addr(S + G::SE);
     const uint32_t rank = cl_rank();
     const int tid = threadIdx.x;
     // phase A layout: item ia (n1 = rank PA + ia) fastest across lanes
@@ -136,8 +154,8 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
     // phase B layout: item jb (k1 = rank QB + jb) fastest across lanes
     const int jb = tid % QB, tb = tid / QB;
     const int k1 = (int)rank * QB + jb;
-    SmemView<C, 4, 1> smA{X + ia * G::SA};
-    SmemView<C, 4, 1> smB{X + jb * G::SB};
+    SmemView<C, Shape<R2E>::LOGE, 1> smA{X + ia * G::SA};
+    SmemView<C, Shape<R2E>::LOGE, 1> smB{X + jb * G::SB};
     const SyncCTA sync{};
     const uint32_t Rbase = smem_addr(R);
     constexpr uint32_t RX_BYTES = (uint32_t)(N / CL * sizeof(C));   // bytes received per exchange
@@ -172,18 +190,26 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
         const int64_t b = row / ny;
         return base + b * stride + (row - b * ny) * (int64_t)N;
     };
-    // input of a row: phase-A layout x[n1 + P (ta + TA e)] (FWD) or phase-B^-1
-    // layout X[k1 + Q (tb + TB e)] (INV, MID); the next row's input is loaded
-    // into registers while this row is transformed
-    auto load_row = [&](int64_t row, C (&u)[16]) {
+    // input of a row: phase-A layout x[n1 + P (ta + TA e)] (FWD, DIFF) or phase-B^-1
+    // layout X[k1 + Q (tb + TB e)] (INV, MID).  The next row's input is copied
+    // into the staging buffer (cp.async) while this row is transformed: held in
+    // registers instead, its loads shared a scoreboard with this row's first
+    // butterflies, which then waited out a DRAM latency every row
+    // (ncu, profiles/r01/ncu_full_c5.txt: 9% of the samples on one DADD).
+    // Each thread reads back only the slots it wrote (no barrier needed).
+    auto prefetch = [&](int64_t row) {
         const C *src = row_ptr(in, row);
-        if constexpr (OP == R2D_FWD || OP == R2D_DIFF) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) u[e] = src[n1 + P * (ta + TA * e)];
-        } else {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) u[e] = src[k1 + Q * (tb + TB * e)];
+        for (int e = 0; e < R2E; ++e) {
+            if constexpr (OP == R2D_FWD || OP == R2D_DIFF) r2_cp_async(S + e * NT + tid, src + n1 + P * (ta + TA * e));
+            else r2_cp_async(S + e * NT + tid, src + k1 + Q * (tb + TB * e));
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto take = [&](C (&u)[R2E]) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+        for (int e = 0; e < R2E; ++e) u[e] = S[e * NT + tid];
     };
     // receive-buffer protocol: the receiver arms its mbarrier with the bytes it
     // expects and releases its buffer with a relaxed cluster arrive once the
@@ -200,25 +226,27 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
 
     const int64_t ncl = gridDim.x / CL;
     release_R();
-    C nx[16];
     int64_t row = blockIdx.x / CL;
     pdl_wait();
-    if (row < nrows) load_row(row, nx);
+    if (row < nrows) prefetch(row);
     for (; row < nrows; row += ncl) {
         if (row + ncl >= nrows) pdl_trigger();   // this cluster's last row
-        C v[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) v[e] = nx[e];
-        if (row + ncl < nrows) load_row(row + ncl, nx);
+        C v[R2E];
+        take(v);
+        // the staging slots are rewritten only after the first transform consumed them
+        auto prefetch_next = [&]() {
+            if (row + ncl < nrows) prefetch(row + ncl);
+        };
         // inverse: v in the phase-B^-1 layout X[k1 + Q (tb + TB e)] -> x[n1 + P (ta + TA e)]
-        auto inv_part = [&](C (&v)[16]) {
+        auto inv_part = [&](C (&v)[R2E], bool first) {
             // ---- B^-1: inverse P-point transforms over k2 of items k1, times w_N^{-n1 k1}
-            fft<P, true, 16>(v, smB, tb, twP, sync);          // v[e] = Y[n1 = tb + TB e][k1]
+            fft<P, true, R2E>(v, smB, tb, twP, sync);          // v[e] = Y[n1 = tb + TB e][k1]
+            if (first) prefetch_next();
 #pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = cmulw<true>(v[e], twB(tb + TB * e));
+            for (int e = 0; e < R2E; ++e) v[e] = cmulw<true>(v[e], twB(tb + TB * e));
             cl_wait_acquire();                                // every receive buffer is free
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {                    // -> owner of n1, R[ia'][k1] (pitch Q+1)
+            for (int e = 0; e < R2E; ++e) {                    // -> owner of n1, R[ia'][k1] (pitch Q+1)
                 const int m1 = tb + TB * e;
                 const uint32_t dst = (uint32_t)(m1 % PA) * (Q + 1) + k1;
                 const uint32_t to = (uint32_t)(m1 / PA);
@@ -227,19 +255,20 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
             receive();
             // ---- A^-1: inverse Q-point transforms over k1 of items n1
 #pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = R[ia * (Q + 1) + ta + TA * e];
-            fft<Q, true, 16>(v, smA, ta, twQ, sync);          // v[e] = x[n1 + P (ta + TA e)]
+            for (int e = 0; e < R2E; ++e) v[e] = R[ia * (Q + 1) + ta + TA * e];
+            fft<Q, true, R2E>(v, smA, ta, twQ, sync);          // v[e] = x[n1 + P (ta + TA e)]
             release_R();                                      // (the transform consumed R)
         };
         // forward: v in the phase-A layout x[n1 + P (ta + TA e)] -> X[k1 + Q (tb + TB e)]
-        auto fwd_part = [&](C (&v)[16]) {
+        auto fwd_part = [&](C (&v)[R2E], bool first) {
             // ---- A: Q-point transforms over n2 of items n1, times w_N^{n1 k1}
-            fft<Q, false, 16>(v, smA, ta, twQ, sync);         // v[e] = Y[n1][k1 = ta + TA e]
+            fft<Q, false, R2E>(v, smA, ta, twQ, sync);         // v[e] = Y[n1][k1 = ta + TA e]
+            if (first) prefetch_next();
 #pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = cmulw<false>(v[e], twA(ta + TA * e));
+            for (int e = 0; e < R2E; ++e) v[e] = cmulw<false>(v[e], twA(ta + TA * e));
             cl_wait_acquire();
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {                    // -> owner of k1, R[jb'][n1] (pitch P+1)
+            for (int e = 0; e < R2E; ++e) {                    // -> owner of k1, R[jb'][n1] (pitch P+1)
                 const int m1 = ta + TA * e;
                 const uint32_t dst = (uint32_t)(m1 % QB) * (P + 1) + n1;
                 const uint32_t to = (uint32_t)(m1 / QB);
@@ -248,42 +277,41 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
             receive();
             // ---- B: P-point transforms over n1 of items k1 -> X[k1 + Q k2]
 #pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = R[jb * (P + 1) + tb + TB * e];
-            fft<P, false, 16>(v, smB, tb, twP, sync);
+            for (int e = 0; e < R2E; ++e) v[e] = R[jb * (P + 1) + tb + TB * e];
+            fft<P, false, R2E>(v, smB, tb, twP, sync);
             release_R();
         };
         if constexpr (OP == R2D_INV || OP == R2D_MID) {
-            inv_part(v);
+            inv_part(v, true);
             C *dst = const_cast<C *>(row_ptr(OP == R2D_INV ? out : out2, row));
 #pragma unroll
-            for (int e = 0; e < 16; ++e) dst[n1 + P * (ta + TA * e)] = v[e];
+            for (int e = 0; e < R2E; ++e) dst[n1 + P * (ta + TA * e)] = v[e];
         }
         if constexpr (OP == R2D_FWD || OP == R2D_MID) {
-            fwd_part(v);
+            fwd_part(v, OP == R2D_FWD);
             if (OP == R2D_FWD && po.p[0]) {          // scattered into the peers' column slabs
 #pragma unroll
-                for (int e = 0; e < 16; ++e) *peer_row_dst<C>(po, row, k1 + Q * (tb + TB * e)) = v[e];
+                for (int e = 0; e < R2E; ++e) *peer_row_dst<C>(po, row, k1 + Q * (tb + TB * e)) = v[e];
             } else {
                 C *dst = const_cast<C *>(row_ptr(out, row));
 #pragma unroll
-                for (int e = 0; e < 16; ++e) dst[k1 + Q * (tb + TB * e)] = v[e];
+                for (int e = 0; e < R2E; ++e) dst[k1 + Q * (tb + TB * e)] = v[e];
             }
         }
         if constexpr (OP == R2D_DIFF) {
-            fwd_part(v);
+            fwd_part(v, true);
 #pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = cscale(v[e], __ldg(mul + k1 + Q * (tb + TB * e)));
-            inv_part(v);
+            for (int e = 0; e < R2E; ++e) v[e] = cscale(v[e], __ldg(mul + k1 + Q * (tb + TB * e)));
+            inv_part(v, false);
             if (po.p[0]) {                           // scattered into the peers' column slabs
 #pragma unroll
-                for (int e = 0; e < 16; ++e) *peer_row_dst<C>(po, row, n1 + P * (ta + TA * e)) = v[e];
+                for (int e = 0; e < R2E; ++e) *peer_row_dst<C>(po, row, n1 + P * (ta + TA * e)) = v[e];
             } else {
                 C *dst = const_cast<C *>(row_ptr(out, row));
 #pragma unroll
-                for (int e = 0; e < 16; ++e) dst[n1 + P * (ta + TA * e)] = v[e];
+                for (int e = 0; e < R2E; ++e) dst[n1 + P * (ta + TA * e)] = v[e];
             }
         }
-
     }
     cl_wait_acquire();                       // no CTA leaves while others may still write its smem
 }

@@ -156,6 +156,17 @@ def test_long_axes_solvers(dtype, shape):
     assert rel(host(uu), uo) <= TOL[dtype] and rel(host(vv), vo) <= 10 * TOL[dtype]
 
 
+@pytest.mark.parametrize("dtype,B,ny,nx", [(C128, 5, 32, 32768), (C64, 3, 16, 32768), (C128, 9, 32, 16384)])
+def test_long_row_diffusion_many_rows_per_cluster(dtype, B, ny, nx):
+    # rows >> clusters: the row2d diffusion pass runs its steady state (the next
+    # row's input staged by cp.async while this one is transformed, the mbarrier
+    # cycling through its phases) with ragged per-cluster row counts, batched
+    x = noise((B, ny, nx), 91 + ny, dtype)
+    p = F.Plan(nx, ny, batch=B, dtype=dtype, Lx=1.0, Ly=0.5)
+    u = host(p.diffuse(dev(x, dtype), 3e-7, 0.01, 2))
+    assert rel(u, O.diffuse(x.astype(np.complex128), 3e-7, 0.01, 2, 1.0, 0.5)) <= TOL[dtype]
+
+
 # ---------------------------------------------------------------- C2 diffusion
 
 def test_c2_diffusion_prefix_vs_stepped_oracle():
@@ -354,6 +365,11 @@ for ny, nx, B in ((256, 32, 2), (512, 16, 1)):           # column passes without
     worst = max(worst, rel(p.poisson(torch.from_numpy(x).cuda()).cpu().numpy(), O.poisson(x)))
     worst = max(worst, rel(p.diffuse(torch.from_numpy(x).cuda(), 1e-3, 0.01, 3).cpu().numpy(),
                            O.diffuse(x, 1e-3, 0.01, 3)))
+for ny, nx, B in ((32, 32768, 3), (16, 16384, 5)):       # row2d passes launched without PDL
+    x = noise((B, ny, nx))
+    p = F.Plan(nx, ny, batch=B)
+    worst = max(worst, rel(p.diffuse(torch.from_numpy(x).cuda(), 1e-6, 0.01, 2).cpu().numpy(),
+                           O.diffuse(x, 1e-6, 0.01, 2)))
 u0, v0 = noise((4096, 8)), noise((4096, 8))                # wave columns without TMA (col2 four-step)
 p = F.Plan(8, 4096)
 u, v = torch.from_numpy(u0).cuda(), torch.from_numpy(v0).cuda()
