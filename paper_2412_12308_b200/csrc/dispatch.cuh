@@ -547,14 +547,23 @@ cudaError_t tma_wave2_n(void *U, void *V, int64_t nx, int64_t stride, int64_t ba
                         const OpTables<T> &tab, cudaStream_t st)
 {
     using C = typename cplx_t<T>::type;
-    constexpr int EX = 32;
+    // build parameters for A/B runs (tools/ab_lib.sh): radix 16 with two CTAs per SM
+    // measured equal (C3 wave pass 300 vs 298 us), radix 32 with three CTAs per SM
+    // (register cap, spills) and radix 16 with one CTA per SM slower (357, 416 us)
+#ifndef FFTPDE_WAVE2_EX
+#define FFTPDE_WAVE2_EX 32
+#endif
+#ifndef FFTPDE_WAVE2_MINB
+#define FFTPDE_WAVE2_MINB 1
+#endif
+    constexpr int EX = FFTPDE_WAVE2_EX;
     using L = TmaWave2Smem<C, N, EX>;
     if (batch > (int64_t)1 << 31 || nx * batch > (int64_t)1 << 30) return cudaErrorNotSupported;
     CUtensorMap mu, mv;
     if (!tma_map<T>(mu, U, nx, N, batch, stride, 1, L::BOXR, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) ||
         !tma_map<T>(mv, V, nx, N, batch, stride, 1, L::BOXR, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
         return cudaErrorNotSupported;
-    auto k = tma_wave2_cols_kernel<T, N, EX, 1>;
+    auto k = tma_wave2_cols_kernel<T, N, EX, FFTPDE_WAVE2_MINB>;
     static SmemOptIn<decltype(k)> opt;
     cudaError_t e = opt(k, L::BYTES);
     if (e != cudaSuccess) return e;
@@ -583,8 +592,9 @@ cudaError_t launch_wave_cols(int64_t ny, void *U, void *V, int64_t nx, int64_t s
 {
     using C = typename cplx_t<T>::type;
     if (sizeof(T) == 8 && (ny == 2048 || ny == 4096) && ctw.tw32) {
-        const cudaError_t e = ny == 2048 ? tma_wave2_n<T, 2048>(U, V, nx, stride, batch, ctw.tw32, tab, st)
-                                         : tma_wave2_n<T, 4096>(U, V, nx, stride, batch, ctw.tw32, tab, st);
+        const void *tw = tw_for<FFTPDE_WAVE2_EX>(ctw);
+        const cudaError_t e = ny == 2048 ? tma_wave2_n<T, 2048>(U, V, nx, stride, batch, tw, tab, st)
+                                         : tma_wave2_n<T, 4096>(U, V, nx, stride, batch, tw, tab, st);
         if (e != cudaErrorNotSupported) return e;
     }
     int64_t P = 0, Q = 0;
