@@ -17,6 +17,7 @@
 // Twiddles come from a stage-major table computed on the host in fp64 per
 // index (never by recurrence) and rounded once to fp32 for complex64.
 #pragma once
+#include <type_traits>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -261,6 +262,19 @@ template <int N, typename C, int EMAX = 16> struct TwL1 {
     }
 };
 
+// As TwL1, but the last stage's twiddles w_N^{m j} (m = 2 .. R-1) are formed
+// from the one loaded value w_N^{j} by repeated multiplication (one table load
+// per butterfly instead of R-1; a few ulp of extra rounding): for passes whose
+// last-stage table reads dominate their L2 -> L1 traffic.
+#ifndef FFTPDE_TWPOW
+#define FFTPDE_TWPOW 1
+#endif
+template <int N, typename C, int EMAX = 16> struct TwL1Pow : TwL1<N, C, EMAX> {
+    static constexpr bool LAST_POW = true;
+};
+template <typename Tw, typename = void> struct TwLastPow { static constexpr bool value = false; };
+template <typename Tw> struct TwLastPow<Tw, std::void_t<decltype(Tw::LAST_POW)>> { static constexpr bool value = Tw::LAST_POW; };
+
 // As TwL1, reading a copy of the table staged in shared memory (short kernels
 // whose critical path would otherwise wait on L2 twiddle loads every stage).
 template <int N, typename C, int EMAX = 16> struct TwSmem {
@@ -362,7 +376,15 @@ __device__ __forceinline__ void fft_tw(C (&v)[Shape<N, EMAX>::E], const View &sm
         C u[R];
 #pragma unroll
         for (int m = 0; m < R; ++m) u[m] = v[q + m * Q];
-        if (S::NS_LAST > 1) {
+        if constexpr (S::NS_LAST > 1 && TwLastPow<Tw>::value) {
+            const C w1 = tw.last(q, 1);
+            C wm = w1;
+#pragma unroll
+            for (int m = 1; m < R; ++m) {
+                if (m > 1) wm = C{wm.x * w1.x - wm.y * w1.y, wm.x * w1.y + wm.y * w1.x};
+                u[m] = cmulw<INV>(u[m], wm);
+            }
+        } else if (S::NS_LAST > 1) {
             constexpr int LG = R <= 1 ? 1 : R <= 16 ? R - 1 : 8;
 #pragma unroll
             for (int m0 = 1; m0 < R; m0 += LG) {
@@ -386,6 +408,13 @@ template <int N, bool INV, int EMAX = 16, typename C, typename View, typename Sy
 __device__ __forceinline__ void fft(C (&v)[Shape<N, EMAX>::E], const View &sm, int t,
                                     const C *__restrict__ tw, Sync sync)
 {
+#if FFTPDE_TWPOW
+    // last radix 4 or 8: one table load per butterfly, powers by multiplication
+    // (C5 row and column passes -1%, C3 wave pass -5%; FFTPDE_TWPOW=0 restores the loads)
+    if constexpr (Shape<N, EMAX>::R_LAST <= 8 && Shape<N, EMAX>::R_LAST > 2)
+        fft_tw<N, INV, EMAX>(v, sm, t, TwL1Pow<N, C, EMAX>{{tw, t}}, sync);
+    else
+#endif
     fft_tw<N, INV, EMAX>(v, sm, t, TwL1<N, C, EMAX>{tw, t}, sync);
 }
 

@@ -251,7 +251,11 @@ tma_wave2_cols_kernel(const __grid_constant__ CUtensorMap mu, const __grid_const
     for (int e = 0; e < E; ++e) v[e] = line[t + TPT * e];
     __syncthreads();
     SmemView<C, S::LOGE, 1> sm{line};
+#if FFTPDE_TWPOW
+    const TwL1Pow<N, C, EX> twp{{tw, t}};    // last stage radix 4: w, w^2, w^3 from one load
+#else
     const TwL1<N, C, EX> twp{tw, t};
+#endif
     fft_tw<N, false, EX>(v, sm, t, twp, sync);
 #pragma unroll
     for (int e = 0; e < E; ++e) line[t + TPT * e] = v[e];
