@@ -260,6 +260,9 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
             release_R();                                      // (the transform consumed R)
         };
         // forward: v in the phase-A layout x[n1 + P (ta + TA e)] -> X[k1 + Q (tb + TB e)]
+        // DIFF: the x factors of this thread's phase-B points (the same for every
+        // row), loaded while the exchange is in flight
+        T mrow[OP == R2D_DIFF ? R2E : 1];
         auto fwd_part = [&](C (&v)[R2E], bool first) {
             // ---- A: Q-point transforms over n2 of items n1, times w_N^{n1 k1}
             fft<Q, false, R2E>(v, smA, ta, twQ, sync);         // v[e] = Y[n1][k1 = ta + TA e]
@@ -273,6 +276,10 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
                 const uint32_t dst = (uint32_t)(m1 % QB) * (P + 1) + n1;
                 const uint32_t to = (uint32_t)(m1 / QB);
                 st_async(mapa_rank(Rbase + dst * (uint32_t)sizeof(C), to), v[e], mapa_rank(mbar, to));
+            }
+            if constexpr (OP == R2D_DIFF) {
+#pragma unroll
+                for (int e = 0; e < R2E; ++e) mrow[e] = __ldg(mul + k1 + Q * (tb + TB * e));
             }
             receive();
             // ---- B: P-point transforms over n1 of items k1 -> X[k1 + Q k2]
@@ -301,7 +308,7 @@ row2d_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>
         if constexpr (OP == R2D_DIFF) {
             fwd_part(v, true);
 #pragma unroll
-            for (int e = 0; e < R2E; ++e) v[e] = cscale(v[e], __ldg(mul + k1 + Q * (tb + TB * e)));
+            for (int e = 0; e < R2E; ++e) v[e] = cscale(v[e], mrow[e]);
             inv_part(v, false);
             if (po.p[0]) {                           // scattered into the peers' column slabs
 #pragma unroll
