@@ -369,7 +369,11 @@ def native(args, wl, world, rank, local):
         "pipe_active_pct": pipe_pct,
         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
                        else "fallback 6650 GB/s (B200_PROFILING.md)",
-        "per_kernel_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in prof.items()},
+        # every class's share of the profiled replays x the un-instrumented step time
+        # (sums to ms_per_step); the raw event-instrumented times over-state short kernels
+        "per_kernel_ms_per_step": {k: round(v[0] / total_prof * ms_per_step, 4) if total_prof else None
+                                   for k, v in prof.items()},
+        "per_kernel_event_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in prof.items()},
         "duration_method": "share of the step from CUDA-event-profiled replays x un-instrumented CUDA-event step time",
     }
 
