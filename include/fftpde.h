@@ -33,7 +33,10 @@
  *   next synchronisation.
  * Aliasing: in == out is allowed everywhere; inputs are otherwise not written.
  * Alignment: device pointers must be aligned to one complex element
- *   (16 B for FFTPDE_C128, 8 B for FFTPDE_C64).
+ *   (16 B for FFTPDE_C128, 8 B for FFTPDE_C64); complex64 plans with
+ *   nx >= 2048 (rows loaded by one bulk copy each) need 16-byte aligned
+ *   pointers and, for batch > 1, a batch stride of an even number of
+ *   elements.  Violations return FFTPDE_ERR_INVALID_ARG before any launch.
  * Threads: one host thread per plan at a time; distinct plans are independent.
  */
 #ifndef FFTPDE_H

@@ -62,6 +62,7 @@ struct fftpde_plan_s {
     bool sharded = false;
     int P = 1, rank = 0;
     bool loopback = false;                     // all P ranks in this one plan (single-process emulation)
+    bool nccl_failed = false;                  // an NCCL call of the last exchange did not return ncclSuccess
     ncclComm_t comm = nullptr;
     int64_t R = 0, BW = 0, nzl = 0, slab_elems = 0;
     size_t o_shA = 0, o_shB = 0, o_shC = 0;
@@ -263,10 +264,17 @@ template <typename T> OpTables<T> tables(fftpde_plan p)
 }
 
 // element-aligned device pointer (16 B for complex128, 8 B for complex64)
+// Rows of >= 2048 points are loaded by one cp.async.bulk per row (pipe.cuh BULK),
+// which needs a 16-byte aligned global address: for complex64 plans with such
+// rows the buffers (and the batch stride in bytes) must be 16-byte aligned too,
+// otherwise the copy would fault and poison the context (fftpde.h "Alignment").
+static bool needs_bulk_alignment(fftpde_plan p) { return elem_cplx(p) < 16 && p->nx >= 2048; }
+
 fftpde_status check_ptr(fftpde_plan p, const void *ptr)
 {
     if (!ptr) return FFTPDE_ERR_INVALID_ARG;
     if (((uintptr_t)ptr % elem_cplx(p)) != 0) return FFTPDE_ERR_INVALID_ARG;
+    if (needs_bulk_alignment(p) && ((uintptr_t)ptr % 16) != 0) return FFTPDE_ERR_INVALID_ARG;
     return FFTPDE_OK;
 }
 
@@ -277,6 +285,8 @@ fftpde_status check_call(fftpde_plan p, int64_t batch, int64_t stride)
     if (!p->ws) return FFTPDE_ERR_WORKSPACE;
     if (batch == 0) return FFTPDE_ERR_EMPTY;
     if (batch < 0 || stride < p->nx * p->ny) return FFTPDE_ERR_INVALID_ARG;
+    if (needs_bulk_alignment(p) && batch > 1 && (stride * (int64_t)elem_cplx(p)) % 16 != 0)
+        return FFTPDE_ERR_INVALID_ARG;
     if (batch > p->batch) return FFTPDE_ERR_UNSUPPORTED;
     return FFTPDE_OK;
 }
@@ -593,12 +603,26 @@ template <typename T> struct Passes {
         const ncclDataType_t ty = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
         const unsigned char *sb = (const unsigned char *)(this->*send)(0);
         unsigned char *rb = (unsigned char *)(this->*recv)(0);
-        if (n.groupStart() != ncclSuccess) return cudaErrorUnknown;
-        for (int q = 0; q < p->P; ++q) {
-            n.send(sb + q * blk, count, ty, q, p->comm, p->stream);
-            n.recv(rb + q * blk, count, ty, q, p->comm, p->stream);
+        // every enqueue is checked; groupEnd is still called after a failed one so the
+        // group is closed, and the failure surfaces as FFTPDE_ERR_NCCL (dispatch)
+        ncclResult_t first = n.groupStart();
+        if (first != ncclSuccess) {
+            p->nccl_failed = true;
+            return cudaErrorUnknown;
         }
-        return n.groupEnd() == ncclSuccess ? cudaGetLastError() : cudaErrorUnknown;
+        for (int q = 0; q < p->P; ++q) {
+            const ncclResult_t rs = n.send(sb + q * blk, count, ty, q, p->comm, p->stream);
+            if (first == ncclSuccess) first = rs;
+            const ncclResult_t rr = n.recv(rb + q * blk, count, ty, q, p->comm, p->stream);
+            if (first == ncclSuccess) first = rr;
+        }
+        const ncclResult_t re = n.groupEnd();
+        if (first == ncclSuccess) first = re;
+        if (first != ncclSuccess) {
+            p->nccl_failed = true;
+            return cudaErrorUnknown;
+        }
+        return cudaGetLastError();
     }
     template <typename F> cudaError_t each(F &&f)
     {
@@ -945,6 +969,7 @@ template <typename F> fftpde_status dispatch(fftpde_plan p, int64_t batch, int64
     DeviceGuard g(p->device);
     if (!g.ok) return FFTPDE_ERR_CUDA;
     cudaError_t e;
+    p->nccl_failed = false;
     if (p->dtype == FFTPDE_C128) {
         Passes<double> ps{p, batch, stride};
         e = f(ps);
@@ -952,6 +977,7 @@ template <typename F> fftpde_status dispatch(fftpde_plan p, int64_t batch, int64
         Passes<float> ps{p, batch, stride};
         e = f(ps);
     }
+    if (p->nccl_failed) return FFTPDE_ERR_NCCL;
     return cuda_status(e);
 }
 

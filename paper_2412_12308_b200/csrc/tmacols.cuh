@@ -277,9 +277,13 @@ tma_wave2_cols_kernel(const __grid_constant__ CUtensorMap mu, const __grid_const
             v[e] = C{cc * v[e].x + ss * o.x, cc * v[e].y + ss * o.y};
         }
     }
-    // done reading the partner's buffer: the values are consumed, so a relaxed
-    // arrive suffices (write-after-read only; no memory fence, ncu: ERRBAR 2.5%)
-    cl_arrive_relaxed();
+    // done reading the partner's buffer.  The arrive must be a release: under
+    // the PTX memory model a relaxed barrier.cluster.arrive does not order the
+    // preceding ld.shared::cluster reads, so the partner could pass its wait
+    // and overwrite `line` (the fft_tw below) while a remote read of it is
+    // still in flight (write-after-read race).  The release costs a
+    // few percent of the wave pass (r01: 274 vs 284 ms per 500 steps).
+    cl_arrive_release();
     cl_wait_acquire();
     fft_tw<N, true, EX>(v, sm, t, twp, sync);
 #pragma unroll

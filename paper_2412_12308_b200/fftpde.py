@@ -349,10 +349,22 @@ class Plan:
         return means
 
     # -- slab (sharded) building blocks ------------------------------------------------
+    def _dense(self, name: str, *ts: torch.Tensor, numel: int = 0):
+        """The slab kernels take raw pointers to dense buffers: every tensor must be a
+        contiguous tensor of the plan's dtype on the plan's device holding at least
+        `numel` elements (an undersized buffer would be written out of bounds)."""
+        for t in ts:
+            if not isinstance(t, torch.Tensor) or t.device != self.device or t.dtype != self.dtype \
+                    or not t.is_contiguous():
+                raise ValueError(f"{name}: expected contiguous {self.dtype} tensors on {self.device}")
+            if t.numel() < numel:
+                raise ValueError(f"{name}: buffer of {t.numel()} elements, the call touches {numel}")
+
     def rows(self, x: torch.Tensor, out: torch.Tensor, inverse: bool = False):
         """Transforms along x of the rows of a [nrows, nx] device slab (any nrows)."""
         if x.dim() != 2 or x.shape[1] != self.nx or out.shape != x.shape or x.dtype != self.dtype:
             raise ValueError("rows: expected matching [nrows, nx] tensors of the plan's dtype")
+        self._dense("rows", x, out)
         self._bind_stream()
         _check(self.lib.fftpde_rows(self._h, x.data_ptr(), out.data_ptr(), x.shape[0], int(inverse)),
                "fftpde_rows")
@@ -364,6 +376,7 @@ class Plan:
         [ny, ncols] column slab holding global columns col0 .. col0+ncols-1."""
         if x.dim() != 2 or x.shape[0] != self.ny or out.shape != x.shape or x.dtype != self.dtype:
             raise ValueError("cols_slab: expected matching [ny, ncols] tensors of the plan's dtype")
+        self._dense("cols_slab", x, out)
         self._bind_stream()
         _check(self.lib.fftpde_cols_slab(self._h, x.data_ptr(), out.data_ptr(), int(col0), x.shape[1],
                                          int(op), float(D), float(dt)), "fftpde_cols_slab")
@@ -372,6 +385,9 @@ class Plan:
     def peer_transpose(self, src: torch.Tensor, peers, rank: int, R: int, bw: int, direction: int):
         """Slab exchange by direct stores into the peers' buffers (fftpde_peer_transpose);
         peers: device pointers (ints) of every rank's destination buffer."""
+        self._dense("peer_transpose", src, numel=int(R) * self.nx)
+        if len(peers) < 1 or int(bw) * len(peers) != self.nx:
+            raise ValueError("peer_transpose: expected one destination per rank and bw * P == nx")
         arr = (ctypes.c_void_p * len(peers))(*[int(x) for x in peers])
         self._bind_stream()
         _check(self.lib.fftpde_peer_transpose(self._h, src.data_ptr(), arr, len(peers), int(rank), int(R), int(bw),
@@ -403,6 +419,7 @@ class Plan:
     def pack_blocks(self, x: torch.Tensor, out: torch.Tensor, nrows: int, nblocks: int, bw: int,
                     direction: int):
         """[nrows][nblocks][bw] <-> [nblocks][nrows][bw] (direction 0 / 1)."""
+        self._dense("pack_blocks", x, out, numel=int(nrows) * int(nblocks) * int(bw))
         self._bind_stream()
         _check(self.lib.fftpde_pack_blocks(self._h, x.data_ptr(), out.data_ptr(), int(nrows), int(nblocks),
                                            int(bw), int(direction)), "fftpde_pack_blocks")
