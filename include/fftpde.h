@@ -172,7 +172,8 @@ int64_t fftpde_launch_count(fftpde_plan plan);
 #define FFTPDE_KERNEL_WAVE_COL 2  /* wave column pass (both fields) */
 #define FFTPDE_KERNEL_SMALL 3     /* single-CTA whole-grid solve */
 #define FFTPDE_KERNEL_POINTWISE 4 /* pointwise k-space / source kernels (RK4 path) */
-#define FFTPDE_KERNEL_CLASSES 5
+#define FFTPDE_KERNEL_AA 5        /* four-step high-index pass (32768^2 complex128 diffusion) */
+#define FFTPDE_KERNEL_CLASSES 6
 fftpde_status fftpde_set_profiling(fftpde_plan plan, int enable);
 fftpde_status fftpde_read_profile(fftpde_plan plan, int kernel_class, double *total_ms, int64_t *launches);
 

@@ -174,6 +174,8 @@ cudaError_t rows_n(const void *in, void *out, void *out2, int64_t ny, int64_t st
         if (!rm.mul || !rm.ones) return cudaErrorInvalidValue;
         tab.ex = (const T *)rm.ones;
         tab.ey = (const T *)rm.mul;
+        tab.ey2d = (const T *)rm.mul2d;
+        tab.ey2d_mod = rm.mod;
     }
     using LP = LinePolicy<T, N, false>;
     if constexpr (LP::E > 0) {

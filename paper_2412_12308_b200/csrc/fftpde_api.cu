@@ -43,6 +43,10 @@ struct fftpde_plan_s {
     size_t o_rtwP = 0, o_rtwQ = 0, o_rtwN = 0;   // two-level row pass tables (nx > kMaxLen)
     int64_t rowP = 0, rowQ = 0;
     std::vector<double> rtwP, rtwQ, rtwN;   // row2d: radix-16 stage tables of P, Q; split inter-phase table
+    // four-step diffusion passes (fourstep.cuh; 32768^2 complex128 single grids, R27)
+    bool fs = false;
+    std::vector<double> fs_tw, fs_tw32;   // w_N^{ab} (a < 1024, b < 32); radix-32 stage table of 1024
+    size_t o_fs_tw = 0, o_fs_tw32 = 0, o_fs_mx = 0, o_fs_my = 0;
     size_t need = 0;
     int64_t qx = 0, qy = 0;   // quadrant extents nx/2+1, ny/2+1
     // host tables (fp64)
@@ -202,6 +206,30 @@ void build_split_twiddles(int64_t n, int64_t P, int64_t Q, std::vector<double> &
         for (int64_t l = 0; l < 16; ++l) put(k * l);
     for (int64_t k = 0; k < Q; ++k)
         for (int64_t h = 0; h < P / 16; ++h) put(16 * k * h);
+}
+
+// Tables of the four-step passes (fourstep.cuh, N = 1024 x 32 on both axes):
+// tw[a][b] = w_N^{a b}, a < 1024, b < 32; the radix-32 stage table of 1024 (line passes).
+void build_fourstep_tables(int64_t n, std::vector<double> &tw, std::vector<double> &tw32)
+{
+    tw.clear();
+    double re, im;
+    for (int64_t a = 0; a < 1024; ++a)
+        for (int64_t b = 0; b < 32; ++b) {
+            unit_root(n, a * b, re, im);
+            tw.push_back(re);
+            tw.push_back(im);
+        }
+    build_twiddles(1024, tw32, 32);
+}
+
+// The factor m(k) of an axis in the four-step B-pass order [k1][k2], k = k1 + 32 k2.
+std::vector<double> fourstep_mul_order(const std::vector<double> &m)
+{
+    std::vector<double> o(m.size());
+    for (size_t k1 = 0; k1 < 32; ++k1)
+        for (size_t k2 = 0; k2 < 1024; ++k2) o[k1 * 1024 + k2] = m[k1 + 32 * k2];
+    return o;
 }
 
 template <typename T> std::vector<T> cast_vec(const std::vector<double> &v)
@@ -485,11 +513,50 @@ template <typename T> struct Passes {
             return e;
         }
         cudaError_t e = cudaSuccess;
+        if (p->fs && batch == 1 && nsteps > 0) {   // R27: the four-step passes, field W in the scratch
+            void *Wf = scratch(0);
+            e = fs_aa(0, u0, Wf, nullptr);
+            for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) {
+                e = fs_bx(Wf);
+                if (e == cudaSuccess) e = fs_by(Wf);
+                if (e == cudaSuccess) e = k + 1 < nsteps ? fs_aa(2, Wf, Wf, u) : fs_aa(1, Wf, u, nullptr);
+            }
+            return e;
+        }
         for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) {
             e = rows_diff(k == 0 ? u0 : u, u);
             if (e == cudaSuccess) e = cols_diff_y(u, u);
         }
         return e;
+    }
+    // four-step passes (fourstep.cuh): AA (op 0), AA^-1 (op 1), MID (op 2: AA^-1 -> phys, AA -> out)
+    cudaError_t fs_aa(int op, const void *in, void *out, void *phys)
+    {
+        return launch(p, FFTPDE_KERNEL_AA, [&] { return launch_aa(op, in, out, phys, p->ws + p->o_fs_tw, p->stream); });
+    }
+    ColTw fs_ctw() const
+    {
+        const void *t32 = p->ws + p->o_fs_tw32;
+        return ColTw{t32, nullptr, nullptr, nullptr, nullptr, t32};
+    }
+    // Bx: the 1024-point row segments of fixed k1 (32 per row): line class = segment % 32
+    cudaError_t fs_bx(void *Wf)
+    {
+        RowMul rm{p->ws + p->o_fs_mx, p->ws + p->o_one, p->ws + p->o_fs_mx, 32};
+        return launch(p, FFTPDE_KERNEL_ROW, [&] {
+            return launch_rows<T>(1024, Wf, Wf, nullptr, p->ny * 32, p->nx * p->ny, 1, ROW_DIFF, fs_ctw(),
+                                  p->stream, rm);
+        });
+    }
+    // By: the 1024-row column blocks of fixed l1 (32 per column): batch index = l1
+    cudaError_t fs_by(void *Wf)
+    {
+        OpTables<T> t = tables<T>(p);
+        t.ex = (const T *)(p->ws + p->o_one);
+        t.ey2d = (const T *)(p->ws + p->o_fs_my);
+        return launch(p, FFTPDE_KERNEL_COL, [&] {
+            return launch_cols<T>(1024, Wf, Wf, p->nx, 1024 * p->nx, 32, COL_DIFFUSE, fs_ctw(), t, p->stream);
+        });
     }
     cudaError_t wave(void *U, void *V, int64_t nsteps)
     {
@@ -1068,6 +1135,13 @@ fftpde_status ensure_diffusion_tables(fftpde_plan p, double D, double dt)
     for (int64_t b = 0; b < p->ny; ++b) ey[(size_t)b] = std::exp(-D * p->ky2[(size_t)b] * dt);
     fftpde_status s = upload(p, p->o_ex, ex);
     if (s == FFTPDE_OK) s = upload(p, p->o_ey, ey);
+    if (s == FFTPDE_OK && p->fs) {        // per-axis factors: e^{-D kx^2 dt}/nx, e^{-D ky^2 dt}/ny
+        std::vector<double> mx((size_t)p->nx), my((size_t)p->ny);
+        for (int64_t a = 0; a < p->nx; ++a) mx[(size_t)a] = std::exp(-D * p->kx2[(size_t)a] * dt) / (double)p->nx;
+        for (int64_t b = 0; b < p->ny; ++b) my[(size_t)b] = std::exp(-D * p->ky2[(size_t)b] * dt) / (double)p->ny;
+        s = upload(p, p->o_fs_mx, fourstep_mul_order(mx));
+        if (s == FFTPDE_OK) s = upload(p, p->o_fs_my, fourstep_mul_order(my));
+    }
     if (s != FFTPDE_OK) return s;
     p->diff_valid = true;
     p->diff_D = D;
@@ -1207,6 +1281,9 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
         build_twiddles(p->colQ, p->twQ, FFTPDE_COL2_EMAX);
         build_plain_twiddles(ny, p->twN);
     }
+    p->fs = fftpde::fourstep_supported(nx, ny, batch, dtype == FFTPDE_C128 ? 16 : 8) &&
+            std::getenv("FFTPDE_NO_FOURSTEP") == nullptr;
+    if (p->fs) build_fourstep_tables(nx, p->fs_tw, p->fs_tw32);
     fftpde::row2_split(nx, p->rowP, p->rowQ);
     if (p->rowP) {
         build_twiddles(p->rowP, p->rtwP, FFTPDE_R2D_E);
@@ -1243,6 +1320,12 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
         p->o_twP = take(p->twP.size() / 2 * ec);
         p->o_twQ = take(p->twQ.size() / 2 * ec);
         p->o_twN = take(p->twN.size() / 2 * ec);
+    }
+    if (p->fs) {
+        p->o_fs_tw = take(p->fs_tw.size() / 2 * ec);
+        p->o_fs_tw32 = take(p->fs_tw32.size() / 2 * ec);
+        p->o_fs_mx = take((size_t)nx * er);
+        p->o_fs_my = take((size_t)ny * er);
     }
     p->o_scr = take(2 * (size_t)(batch * nx * ny) * ec);    // last: sharded plans replace it by slabs
     p->need = off;
@@ -1290,6 +1373,10 @@ fftpde_status fftpde_set_workspace(fftpde_plan plan, void *dev_ptr, size_t bytes
         s = upload(plan, plan->o_rtwP, plan->rtwP);
         if (s == FFTPDE_OK) s = upload(plan, plan->o_rtwQ, plan->rtwQ);
         if (s == FFTPDE_OK) s = upload(plan, plan->o_rtwN, plan->rtwN);
+    }
+    if (s == FFTPDE_OK && plan->fs) {
+        s = upload(plan, plan->o_fs_tw, plan->fs_tw);
+        if (s == FFTPDE_OK) s = upload(plan, plan->o_fs_tw32, plan->fs_tw32);
     }
     if (s == FFTPDE_OK && plan->colP) {
         s = upload(plan, plan->o_twP, plan->twP);
@@ -1719,6 +1806,7 @@ namespace {
 fftpde_status finish_sharded(fftpde_plan p, int nranks, int rank, const void *uid, int64_t slab_elems)
 {
     p->sharded = true;
+    p->fs = false;                   // the slab path has its own passes
     p->P = nranks;
     p->loopback = uid == nullptr;
     p->rank = p->loopback ? 0 : rank;

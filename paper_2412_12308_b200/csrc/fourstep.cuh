@@ -1,0 +1,157 @@
+// fourstep.cuh -- the high-index DFT pass of the 2D four-step (Bailey) solve
+// of the 32768 x 32768 complex128 diffusion (C5), sm_100a.
+//
+// Both axes are split N = P Q with P = 1024, Q = 32 (PAPER.md:262-273's row /
+// column split of the 2D sum, applied once more inside each axis):
+//   x = n1 + P n2, kx = k1 + Q k2;   y = m1 + P m2, ky = l1 + Q l2
+//   X[k1 + Q k2] = sum_{n1} w_P^{n1 k2} [ w_N^{n1 k1} sum_{n2} x[n1 + P n2] w_Q^{n2 k1} ]
+// (eq:DFT).  One diffusion step (separable, R26)
+// is then four passes over the field in HBM, each reading and writing it once:
+//   AA     (this kernel)  for every (m1, n1): the Q-point DFTs over n2 and over
+//                         m2 with their twiddles w_N^{n1 k1}, w_N^{m1 l1}
+//   Bx     (line pass)    1024-point rows of fixed k1: DFT over n1, times
+//                         e^{-D kx^2 dt}/nx at kx = k1 + Q k2, inverse DFT
+//   By     (line pass)    1024-point column segments of fixed l1: the same along y
+//   AA^-1  (this kernel)  conjugate twiddles, inverse Q-point DFTs: the
+//                         physical field u (materialised every step, R8)
+// AA^-1 of step s and AA of step s+1 run as one pass (MID): one read, the
+// physical field written, the next step's AA-domain field written.
+//
+// A tile is (m1, 4 consecutive n1) x all (m2, n2): 32 x 32 x 4 points (64 KiB),
+// moved by one 4D tensor-memory-accelerator box per direction (64-byte row
+// segments; no thread issues a global access), transformed along n2 by thread
+// (m2, w) and along m2 by thread (k1, w), each a radix-32 DFT in registers.
+#pragma once
+#include <cuda.h>
+#include "fft_core.cuh"
+#include "tmacols.cuh"
+
+namespace fftpde {
+
+struct FsGeom {
+    static constexpr int N = 32768, P = 1024, Q = 32, W = 4;
+    static constexpr int NT = Q * W;                       // 128 threads
+    static constexpr int TILE = Q * Q * W;                 // 4096 points
+    static constexpr int NCHUNK = P / W;                   // 256 n1-chunks per m1
+    static constexpr size_t BYTES = (size_t)TILE * 16 + 128 + 64;   // tile + alignment slack + mbarrier
+};
+enum FsOp { FS_FWD = 0, FS_INV = 1, FS_MID = 2 };
+
+__device__ __forceinline__ void tma_load4(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
+                                          uint32_t mbar)
+{
+    asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+                 "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store4(const CUtensorMap *map, int c0, int c1, int c2, int c3, uint32_t src)
+{
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
+                 ::"l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(src) : "memory");
+}
+
+// Tables: tw[a][b] = w_N^{a b}, a < P, b < Q (both axes: x and y have the same N).
+// Tile smem layout [row index r][col index c][w] = (r * Q + c) * W + w, where r is
+// m2 (physical) or l1 (AA domain) and c is n2 or k1.
+template <int OP>
+__global__ void __launch_bounds__(FsGeom::NT, 2)
+aa_kernel(const __grid_constant__ CUtensorMap min, const __grid_constant__ CUtensorMap mout,
+          const __grid_constant__ CUtensorMap mphys, const double2 *__restrict__ tw)
+{
+    using G = FsGeom;
+    constexpr int Q = G::Q, W = G::W;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double2 *S = reinterpret_cast<double2 *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
+    const uint32_t mbar = tma_smem(S + G::TILE);
+    const int tid = threadIdx.x;
+    const int m1 = (int)(blockIdx.x / G::NCHUNK), chunk = (int)(blockIdx.x % G::NCHUNK);
+    const int w = tid % W, r = tid / W;                   // (m2 | k1, w) of this thread
+    const int n1 = chunk * W + w;
+    const int c0 = 2 * W * chunk;                         // tensor coordinate (doubles) of the chunk
+    if (tid == 0) {
+        tma_mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_wait();
+    if (tid == 0) {
+        tma_mbar_expect(mbar, (uint32_t)(G::TILE * 16));
+        tma_load4(tma_smem(S), &min, c0, 0, m1, 0, mbar);
+    }
+    pdl_trigger();
+    const double2 *twx = tw + (size_t)n1 * Q;             // w_N^{n1 k1}
+    const double2 *twy = tw + (size_t)m1 * Q;             // w_N^{m1 l1}
+    double2 v[Q];
+    tma_mbar_wait(mbar, 0);
+
+    auto xpass_fwd = [&]() {          // v[n2] (thread (m2, w)) -> v[k1] = w^{n1 k1} DFT_n2
+        dft_r<Q, false>(v);
+#pragma unroll
+        for (int k = 1; k < Q; ++k) v[k] = cmulw<false>(v[k], __ldg(twx + k));
+    };
+    auto ypass_fwd = [&]() {          // thread (k1, w): rows m2 -> l1
+#pragma unroll
+        for (int m = 0; m < Q; ++m) v[m] = S[(m * Q + r) * W + w];
+        dft_r<Q, false>(v);
+#pragma unroll
+        for (int l = 1; l < Q; ++l) v[l] = cmulw<false>(v[l], __ldg(twy + l));
+#pragma unroll
+        for (int l = 0; l < Q; ++l) S[(l * Q + r) * W + w] = v[l];
+    };
+    auto store_tile = [&](const CUtensorMap *map) {
+        tma_fence_smem();
+        __syncthreads();
+        if (tid == 0) {
+            tma_store4(map, c0, 0, m1, 0, tma_smem(S));
+            tma_commit();
+        }
+    };
+
+    if constexpr (OP == FS_FWD) {
+#pragma unroll
+        for (int n = 0; n < Q; ++n) v[n] = S[(r * Q + n) * W + w];
+        xpass_fwd();
+#pragma unroll
+        for (int k = 0; k < Q; ++k) S[(r * Q + k) * W + w] = v[k];
+        __syncthreads();
+        ypass_fwd();
+        store_tile(&mout);
+    } else {
+        // ---- AA^-1: thread (k1, w): rows l1 -> m2 with w^{-m1 l1}
+#pragma unroll
+        for (int l = 0; l < Q; ++l) v[l] = S[(l * Q + r) * W + w];
+#pragma unroll
+        for (int l = 1; l < Q; ++l) v[l] = cmulw<true>(v[l], __ldg(twy + l));
+        dft_r<Q, true>(v);
+#pragma unroll
+        for (int m = 0; m < Q; ++m) S[(m * Q + r) * W + w] = v[m];
+        __syncthreads();
+        // thread (m2, w): k1 -> n2 with w^{-n1 k1}
+#pragma unroll
+        for (int k = 0; k < Q; ++k) v[k] = S[(r * Q + k) * W + w];
+#pragma unroll
+        for (int k = 1; k < Q; ++k) v[k] = cmulw<true>(v[k], __ldg(twx + k));
+        dft_r<Q, true>(v);
+        __syncthreads();                                   // every thread has read its k1 values
+#pragma unroll
+        for (int n = 0; n < Q; ++n) S[(r * Q + n) * W + w] = v[n];
+        if constexpr (OP == FS_INV) {
+            store_tile(&mout);
+        } else {
+            store_tile(&mphys);                            // the physical field of this step
+            // ---- AA of the next step, from the registers
+            xpass_fwd();
+            if (tid == 0) tma_wait_read0();                // the store has read the tile
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < Q; ++k) S[(r * Q + k) * W + w] = v[k];
+            __syncthreads();
+            ypass_fwd();
+            store_tile(&mout);
+        }
+    }
+    if (tid == 0) tma_wait_read0();                        // smem stays valid until the store has read it
+}
+
+} // namespace fftpde

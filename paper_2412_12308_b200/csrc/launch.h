@@ -48,6 +48,11 @@ template <typename T> struct OpTables {
     int64_t nfold;           // x length for the quadrant index qa = min(a, nfold - a) (nx; real plans
                              // run the column passes over a padded half spectrum, so not the column count)
     T scale;                 // 1/(nx ny)
+    // optional 2D row factor of the four-step passes (fourstep.cuh): the element
+    // factor of line class cls is ey2d[cls * N + element], cls = line % ey2d_mod
+    // (rows) or the batch index (columns); ex is then not applied
+    const T *ey2d = nullptr;
+    int64_t ey2d_mod = 1;
 };
 
 constexpr int64_t kMaxLen = 8192;    // single-CTA (one pass) axis length limit
@@ -75,6 +80,8 @@ struct ColTw;
 struct RowMul {
     const void *mul = nullptr;    // [nx] multiplier over the row's wavenumber index
     const void *ones = nullptr;   // [>= ny] ones
+    const void *mul2d = nullptr;  // optional [mod][nx]: the factor of row r is mul2d[r % mod] (OpTables::ey2d)
+    int64_t mod = 1;
 };
 template <typename T>
 cudaError_t launch_rows(int64_t n, const void *in, void *out, void *out2, int64_t ny, int64_t stride,
@@ -157,6 +164,13 @@ cudaError_t launch_kop(void *X, const void *S, int64_t nx, int64_t ny, int64_t b
 
 cudaError_t launch_peer_transpose(const void *src, const PeerPtrs &peers, int P, int rank, int64_t R,
                                   int64_t bw_bytes, int direction, cudaStream_t st);
+
+// ---- four-step (Bailey) passes of the 32768^2 complex128 diffusion (fourstep.cu) ----
+// op: 0 = AA (in -> out), 1 = AA^-1 (in -> out), 2 = MID (AA^-1 -> phys, then AA -> out).
+// tw = w_32768^{a b}, a < 1024, b < 32.  The B passes are launch_rows / launch_cols
+// over 1024-point lines with the 2D factors (OpTables::ey2d).
+bool fourstep_supported(int64_t nx, int64_t ny, int64_t batch, int elem_bytes);
+cudaError_t launch_aa(int op, const void *in, void *out, void *phys, const void *tw, cudaStream_t st);
 
 // Block transpose of the sharded path (pack.cu); bw_bytes a multiple of 16.
 cudaError_t launch_pack(const void *in, void *out, int64_t nrows, int64_t nblocks, int64_t bw_bytes,

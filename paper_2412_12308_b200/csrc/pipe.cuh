@@ -225,6 +225,10 @@ pipe_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out, P
                     const T m = k2 == (T)0 ? (T)0 : -tab.scale / k2;     // -1/|k|^2, k = 0 zeroed
                     v[e] = cscale(v[e], m);
                 }
+            } else if (tab.ey2d) {                   // four-step B pass: factor of line class cls
+                const int64_t cls = COLS ? tile / a.groups : col % tab.ey2d_mod;
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = cscale(v[e], __ldg(&tab.ey2d[cls * N + t + TPT * e]));
             } else {
                 const T exa = tab.ex[col];
 #pragma unroll

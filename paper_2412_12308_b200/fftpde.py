@@ -20,7 +20,8 @@ import torch
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libfftpde.so")
 
-KERNEL_CLASSES = {0: "row_pass", 1: "col_pass", 2: "wave_col_pass", 3: "small_solve", 4: "pointwise"}
+KERNEL_CLASSES = {0: "row_pass", 1: "col_pass", 2: "wave_col_pass", 3: "small_solve", 4: "pointwise",
+                  5: "aa_pass"}
 
 # fftpde_status
 OK, ERR_INVALID_ARG, ERR_EMPTY, ERR_NOT_POW2_X, ERR_NOT_POW2_Y, ERR_UNSUPPORTED, ERR_WORKSPACE, \
