@@ -79,7 +79,10 @@ inline int sm_count()
 // B200 PDL gains 3% on C2 (line passes) and 2% on C5 (row2d), while an early
 // launched col2 grid slows C3 by 18% (its clusters are placed while the row
 // pass drains; profiles/r01/pdl_ab.txt), so col2 is launched normally.
-enum PdlFamily { PDL_LINE = 1, PDL_COL2 = 2, PDL_ROW2D = 4 };
+// PDL_FOURSTEP: the four-step C5 passes (fourstep.cu); off by default: early-launched
+// successors hold SM slots while the predecessor's last tiles drain (C5 solve
+// 660 vs 594 ms per 20 steps with it on).
+enum PdlFamily { PDL_LINE = 1, PDL_COL2 = 2, PDL_ROW2D = 4, PDL_FOURSTEP = 8 };
 inline bool pdl_enabled(int family = PDL_LINE)
 {
     static const int mask = [] {
@@ -87,6 +90,22 @@ inline bool pdl_enabled(int family = PDL_LINE)
         return e ? std::atoi(e) : PDL_LINE | PDL_ROW2D;
     }();
     return (mask & family) != 0;
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_fam(int family, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args &&...args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled(family) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args)
@@ -150,7 +169,7 @@ template <int E> inline const void *tw_for(const ColTw &c) { return E == 8 ? c.t
 template <typename T, int N, int E, int W, bool COLS, int OP, int MINB>
 cudaError_t line_n(const void *in, void *out, void *out2, int64_t nlines, int64_t line_stride, int64_t elem_stride,
                    int64_t stride, int64_t batch, const void *tw, const OpTables<T> &tab, cudaStream_t st,
-                   const PeerOut &po = PeerOut{})
+                   const PeerOut &po = PeerOut{}, int family = PDL_LINE)
 {
     using C = typename cplx_t<T>::type;
     using L = LineSmem<C, N, E, W, COLS>;
@@ -160,7 +179,7 @@ cudaError_t line_n(const void *in, void *out, void *out2, int64_t nlines, int64_
     if (e != cudaSuccess) return e;
     LineArgs a{nlines, line_stride, elem_stride, stride, (nlines + W - 1) / W, out2};
     const int64_t grid = batch * a.groups;
-    return launch_pdl(k, dim3((unsigned)grid), dim3(W * (N / E)), L::BYTES, st, (const C *)in, (C *)out, a,
+    return launch_fam(family, k, dim3((unsigned)grid), dim3(W * (N / E)), L::BYTES, st, (const C *)in, (C *)out, a,
                       (const C *)tw, tab, po);
 }
 
@@ -274,12 +293,21 @@ cudaError_t tma_cols_n(const void *in, void *out, int64_t nx, int64_t stride, in
     return launch_pdl(k, dim3((unsigned)grid), dim3(THREADS), L::BYTES, st, mi, mo, a, (const C *)tw, tab);
 }
 
+inline bool fs_tma_by()
+{
+    // measured slower than the line pass (C5 col pass 11.3 vs 11.0 ms per step): opt-in
+    static const bool on = [] { const char *e = std::getenv("FFTPDE_FS_TMA_BY"); return e && e[0] == '1'; }();
+    return on;
+}
 template <typename T, int N>
 cudaError_t cols_n(const void *in, void *out, int64_t nx, int64_t stride, int64_t batch, int op,
                    const ColTw &ctw, const OpTables<T> &tab, cudaStream_t st, const PeerOut &po = PeerOut{})
 {
     using LP = LinePolicy<T, N, true>;
-    if constexpr (TmaColPolicy<T, N>::ON) if (!po.p[0]) {   // (peer output: the line / pipe passes)
+    // complex128 1024-point columns take the TMA pass only as the four-step By pass of
+    // an HBM-resident field (C5); the L2-resident C2 columns are faster in the line pass
+    constexpr bool TMA_FS = sizeof(T) == 8 && N == 1024;
+    if constexpr (TmaColPolicy<T, N>::ON || TMA_FS) if (!po.p[0] && (TmaColPolicy<T, N>::ON || (tab.ey2d && fs_tma_by()))) {
         using TP = TmaColPolicy<T, N>;
         const void *tw = tw_for<TP::E>(ctw);
         cudaError_t e = cudaErrorNotSupported;

@@ -45,8 +45,8 @@ struct fftpde_plan_s {
     std::vector<double> rtwP, rtwQ, rtwN;   // row2d: radix-16 stage tables of P, Q; split inter-phase table
     // four-step diffusion passes (fourstep.cuh; 32768^2 complex128 single grids, R27)
     bool fs = false;
-    std::vector<double> fs_tw, fs_tw32;   // w_N^{ab} (a < 1024, b < 32); radix-32 stage table of 1024
-    size_t o_fs_tw = 0, o_fs_tw32 = 0, o_fs_mx = 0, o_fs_my = 0;
+    std::vector<double> fs_tw, fs_tw32, fs_tw16;   // w_N^{ab} (a < 1024, b < 32); radix-32 / -16 stage tables of 1024
+    size_t o_fs_tw = 0, o_fs_tw32 = 0, o_fs_tw16 = 0, o_fs_mx = 0, o_fs_my = 0;
     size_t need = 0;
     int64_t qx = 0, qy = 0;   // quadrant extents nx/2+1, ny/2+1
     // host tables (fp64)
@@ -210,7 +210,7 @@ void build_split_twiddles(int64_t n, int64_t P, int64_t Q, std::vector<double> &
 
 // Tables of the four-step passes (fourstep.cuh, N = 1024 x 32 on both axes):
 // tw[a][b] = w_N^{a b}, a < 1024, b < 32; the radix-32 stage table of 1024 (line passes).
-void build_fourstep_tables(int64_t n, std::vector<double> &tw, std::vector<double> &tw32)
+void build_fourstep_tables(int64_t n, std::vector<double> &tw, std::vector<double> &tw32, std::vector<double> &tw16)
 {
     tw.clear();
     double re, im;
@@ -221,6 +221,7 @@ void build_fourstep_tables(int64_t n, std::vector<double> &tw, std::vector<doubl
             tw.push_back(im);
         }
     build_twiddles(1024, tw32, 32);
+    build_twiddles(1024, tw16, 16);
 }
 
 // The factor m(k) of an axis in the four-step B-pass order [k1][k2], k = k1 + 32 k2.
@@ -534,29 +535,20 @@ template <typename T> struct Passes {
     {
         return launch(p, FFTPDE_KERNEL_AA, [&] { return launch_aa(op, in, out, phys, p->ws + p->o_fs_tw, p->stream); });
     }
-    ColTw fs_ctw() const
-    {
-        const void *t32 = p->ws + p->o_fs_tw32;
-        return ColTw{t32, nullptr, nullptr, nullptr, nullptr, t32};
-    }
     // Bx: the 1024-point row segments of fixed k1 (32 per row): line class = segment % 32
     cudaError_t fs_bx(void *Wf)
     {
-        RowMul rm{p->ws + p->o_fs_mx, p->ws + p->o_one, p->ws + p->o_fs_mx, 32};
-        return launch(p, FFTPDE_KERNEL_ROW, [&] {
-            return launch_rows<T>(1024, Wf, Wf, nullptr, p->ny * 32, p->nx * p->ny, 1, ROW_DIFF, fs_ctw(),
-                                  p->stream, rm);
-        });
+        OpTables<double> t{};
+        t.ey2d = (const double *)(p->ws + p->o_fs_mx);
+        t.ey2d_mod = 32;
+        return launch(p, FFTPDE_KERNEL_ROW, [&] { return launch_fs_b(false, Wf, p->ws + p->o_fs_tw32, p->ws + p->o_fs_tw16, t, p->stream); });
     }
-    // By: the 1024-row column blocks of fixed l1 (32 per column): batch index = l1
+    // By: the 1024-row column blocks of fixed l1 (32 per column): class = block l1
     cudaError_t fs_by(void *Wf)
     {
-        OpTables<T> t = tables<T>(p);
-        t.ex = (const T *)(p->ws + p->o_one);
-        t.ey2d = (const T *)(p->ws + p->o_fs_my);
-        return launch(p, FFTPDE_KERNEL_COL, [&] {
-            return launch_cols<T>(1024, Wf, Wf, p->nx, 1024 * p->nx, 32, COL_DIFFUSE, fs_ctw(), t, p->stream);
-        });
+        OpTables<double> t{};
+        t.ey2d = (const double *)(p->ws + p->o_fs_my);
+        return launch(p, FFTPDE_KERNEL_COL, [&] { return launch_fs_b(true, Wf, p->ws + p->o_fs_tw32, p->ws + p->o_fs_tw16, t, p->stream); });
     }
     cudaError_t wave(void *U, void *V, int64_t nsteps)
     {
@@ -1283,7 +1275,7 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     }
     p->fs = fftpde::fourstep_supported(nx, ny, batch, dtype == FFTPDE_C128 ? 16 : 8) &&
             std::getenv("FFTPDE_NO_FOURSTEP") == nullptr;
-    if (p->fs) build_fourstep_tables(nx, p->fs_tw, p->fs_tw32);
+    if (p->fs) build_fourstep_tables(nx, p->fs_tw, p->fs_tw32, p->fs_tw16);
     fftpde::row2_split(nx, p->rowP, p->rowQ);
     if (p->rowP) {
         build_twiddles(p->rowP, p->rtwP, FFTPDE_R2D_E);
@@ -1324,6 +1316,7 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     if (p->fs) {
         p->o_fs_tw = take(p->fs_tw.size() / 2 * ec);
         p->o_fs_tw32 = take(p->fs_tw32.size() / 2 * ec);
+        p->o_fs_tw16 = take(p->fs_tw16.size() / 2 * ec);
         p->o_fs_mx = take((size_t)nx * er);
         p->o_fs_my = take((size_t)ny * er);
     }
@@ -1377,6 +1370,7 @@ fftpde_status fftpde_set_workspace(fftpde_plan plan, void *dev_ptr, size_t bytes
     if (s == FFTPDE_OK && plan->fs) {
         s = upload(plan, plan->o_fs_tw, plan->fs_tw);
         if (s == FFTPDE_OK) s = upload(plan, plan->o_fs_tw32, plan->fs_tw32);
+        if (s == FFTPDE_OK) s = upload(plan, plan->o_fs_tw16, plan->fs_tw16);
     }
     if (s == FFTPDE_OK && plan->colP) {
         s = upload(plan, plan->o_twP, plan->twP);

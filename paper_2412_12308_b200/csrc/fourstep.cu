@@ -31,12 +31,17 @@ static cudaError_t aa_n(const CUtensorMap &mi, const CUtensorMap &mo, const CUte
                         cudaStream_t st)
 {
     using G = FsGeom;
-    auto k = aa_kernel<OP>;
+    using Cfg = FsCfg<FFTPDE_FS_NBUF>;
+    auto k = aa_kernel<OP, FFTPDE_FS_NBUF>;
     static SmemOptIn<decltype(k)> opt;
-    cudaError_t e = opt(k, G::BYTES);
+    cudaError_t e = opt(k, Cfg::BYTES);
     if (e != cudaSuccess) return e;
-    const dim3 grid((unsigned)(G::P * G::NCHUNK));
-    e = launch_pdl(k, grid, dim3(G::NT), G::BYTES, st, mi, mo, mp, (const double2 *)tw);
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, G::NT, Cfg::BYTES);
+    if (e != cudaSuccess) return e;
+    const dim3 grid(Cfg::NBUF == 1 ? (unsigned)G::NTILES    // one tile per CTA
+                                   : (unsigned)std::min<int64_t>(G::NTILES, (int64_t)std::max(occ, 1) * sm_count()));
+    e = launch_fam(PDL_FOURSTEP, k, grid, dim3(G::NT), Cfg::BYTES, st, mi, mo, mp, (const double2 *)tw);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -55,6 +60,36 @@ cudaError_t launch_aa(int op, const void *in, void *out, void *phys, const void 
     case FS_MID: return aa_n<FS_MID>(mi, mo, mp, tw, st);
     default: return cudaErrorInvalidValue;
     }
+}
+
+#ifndef FFTPDE_FS_BY_W
+#define FFTPDE_FS_BY_W 4
+#endif
+#ifndef FFTPDE_FS_BY_E
+#define FFTPDE_FS_BY_E 32
+#endif
+#ifndef FFTPDE_FS_BY_MINB
+#define FFTPDE_FS_BY_MINB 2
+#endif
+#ifndef FFTPDE_FS_BX_W
+#define FFTPDE_FS_BX_W 1
+#endif
+#ifndef FFTPDE_FS_BX_MINB
+#define FFTPDE_FS_BX_MINB 4
+#endif
+// The B passes: 1024-point line diffusion with the 2D factor (OpTables::ey2d).
+// Bx: rows of 1024 points (32 per grid row), line class = row % 32;
+// By: 32 blocks of 1024 rows, W adjacent columns per CTA, class = block.
+cudaError_t launch_fs_b(bool cols, void *f, const void *tw32, const void *tw16, const OpTables<double> &tab,
+                        cudaStream_t st)
+{
+    using G = FsGeom;
+    if (!cols)
+        return line_n<double, 1024, 32, FFTPDE_FS_BX_W, false, LN_DIFFUSE, FFTPDE_FS_BX_MINB>(
+            f, f, nullptr, (int64_t)G::N * G::Q, 1024, 1, (int64_t)G::N * G::N, 1, tw32, tab, st, PeerOut{}, PDL_FOURSTEP);
+    return line_n<double, 1024, FFTPDE_FS_BY_E, FFTPDE_FS_BY_W, true, LN_DIFFUSE, FFTPDE_FS_BY_MINB>(
+        f, f, nullptr, G::N, 1, G::N, (int64_t)1024 * G::N, G::Q, FFTPDE_FS_BY_E == 32 ? tw32 : tw16, tab, st,
+        PeerOut{}, PDL_FOURSTEP);
 }
 
 } // namespace fftpde

@@ -33,7 +33,22 @@ struct FsGeom {
     static constexpr int NT = Q * W;                       // 128 threads
     static constexpr int TILE = Q * Q * W;                 // 4096 points
     static constexpr int NCHUNK = P / W;                   // 256 n1-chunks per m1
-    static constexpr size_t BYTES = (size_t)TILE * 16 + 128 + 64;   // tile + alignment slack + mbarrier
+    static constexpr int NTILES = P * NCHUNK;              // 262144 tiles
+};
+#ifndef FFTPDE_FS_MINB
+#define FFTPDE_FS_MINB 3
+#endif
+#ifndef FFTPDE_FS_NBUF
+#define FFTPDE_FS_NBUF 1
+#endif
+// NB = 1: one tile per CTA, several CTAs per SM (the scheduler overlaps one CTA's
+// TMA traffic with another's transforms); NB = 2: persistent CTAs with the next
+// tile's load in flight
+template <int NB> struct FsCfg {
+    static constexpr int NBUF = NB;
+    static constexpr int MINB = NB == 1 ? FFTPDE_FS_MINB : 1;
+    static constexpr int TWS = FsGeom::W * FsGeom::Q + FsGeom::Q;   // the tile's twiddles: x [w][k1], y [l1]
+    static constexpr size_t BYTES = (size_t)NB * (FsGeom::TILE + TWS) * 16 + 128 + 64;   // + alignment slack + mbarriers
 };
 enum FsOp { FS_FWD = 0, FS_INV = 1, FS_MID = 2 };
 
@@ -54,104 +69,125 @@ __device__ __forceinline__ void tma_store4(const CUtensorMap *map, int c0, int c
 // Tables: tw[a][b] = w_N^{a b}, a < P, b < Q (both axes: x and y have the same N).
 // Tile smem layout [row index r][col index c][w] = (r * Q + c) * W + w, where r is
 // m2 (physical) or l1 (AA domain) and c is n2 or k1.
-template <int OP>
-__global__ void __launch_bounds__(FsGeom::NT, 2)
+template <int OP, int NB>
+__global__ void __launch_bounds__(FsGeom::NT, FsCfg<NB>::MINB)
 aa_kernel(const __grid_constant__ CUtensorMap min, const __grid_constant__ CUtensorMap mout,
           const __grid_constant__ CUtensorMap mphys, const double2 *__restrict__ tw)
 {
     using G = FsGeom;
-    constexpr int Q = G::Q, W = G::W;
+    constexpr int Q = G::Q, W = G::W, NBUF = FsCfg<NB>::NBUF;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double2 *S = reinterpret_cast<double2 *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
-    const uint32_t mbar = tma_smem(S + G::TILE);
+    // 128-byte aligned tile slots (offset kept in the shared window: LDS/STS, not generic loads)
+    const uint32_t pad = (128u - (tma_smem(smem_raw) & 127u)) & 127u;
+    double2 *S0 = reinterpret_cast<double2 *>(smem_raw + pad);
+    double2 *TWS0 = S0 + NBUF * G::TILE;                   // per slot: [w][k1] x twiddles, then [l1] y twiddles
+    const uint32_t mbar0 = tma_smem(TWS0 + NBUF * FsCfg<NB>::TWS);
     const int tid = threadIdx.x;
-    const int m1 = (int)(blockIdx.x / G::NCHUNK), chunk = (int)(blockIdx.x % G::NCHUNK);
     const int w = tid % W, r = tid / W;                   // (m2 | k1, w) of this thread
-    const int n1 = chunk * W + w;
-    const int c0 = 2 * W * chunk;                         // tensor coordinate (doubles) of the chunk
     if (tid == 0) {
-        tma_mbar_init(mbar, 1);
+        for (int i = 0; i < NBUF; ++i) tma_mbar_init(mbar0 + 8u * i, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    auto load = [&](int tile, int slot) {                 // thread 0: the tile, and its twiddles (with TWS bytes)
+        const int m1 = tile / G::NCHUNK, chunk = tile % G::NCHUNK;
+        double2 *ts = TWS0 + slot * FsCfg<NB>::TWS;
+        tma_mbar_expect(mbar0 + 8u * slot, (uint32_t)((G::TILE + FsCfg<NB>::TWS) * 16));
+        tma_load4(tma_smem(S0 + slot * G::TILE), &min, 2 * W * chunk, 0, m1, 0, mbar0 + 8u * slot);
+        bulk_g2s(tma_smem(ts), tw + (size_t)chunk * W * Q, W * Q * 16, mbar0 + 8u * slot);      // w_N^{n1 k1}, 4 n1
+        bulk_g2s(tma_smem(ts + W * Q), tw + (size_t)m1 * Q, Q * 16, mbar0 + 8u * slot);          // w_N^{m1 l1}
+    };
     pdl_wait();
-    if (tid == 0) {
-        tma_mbar_expect(mbar, (uint32_t)(G::TILE * 16));
-        tma_load4(tma_smem(S), &min, c0, 0, m1, 0, mbar);
-    }
-    pdl_trigger();
-    const double2 *twx = tw + (size_t)n1 * Q;             // w_N^{n1 k1}
-    const double2 *twy = tw + (size_t)m1 * Q;             // w_N^{m1 l1}
-    double2 v[Q];
-    tma_mbar_wait(mbar, 0);
-
-    auto xpass_fwd = [&]() {          // v[n2] (thread (m2, w)) -> v[k1] = w^{n1 k1} DFT_n2
-        dft_r<Q, false>(v);
-#pragma unroll
-        for (int k = 1; k < Q; ++k) v[k] = cmulw<false>(v[k], __ldg(twx + k));
-    };
-    auto ypass_fwd = [&]() {          // thread (k1, w): rows m2 -> l1
-#pragma unroll
-        for (int m = 0; m < Q; ++m) v[m] = S[(m * Q + r) * W + w];
-        dft_r<Q, false>(v);
-#pragma unroll
-        for (int l = 1; l < Q; ++l) v[l] = cmulw<false>(v[l], __ldg(twy + l));
-#pragma unroll
-        for (int l = 0; l < Q; ++l) S[(l * Q + r) * W + w] = v[l];
-    };
-    auto store_tile = [&](const CUtensorMap *map) {
-        tma_fence_smem();
-        __syncthreads();
+    int tile = blockIdx.x;
+    if (tid == 0 && tile < G::NTILES) load(tile, 0);
+    for (int it = 0; tile < G::NTILES; ++it, tile += gridDim.x) {
+        const int slot = it % NBUF;
+        const int next = tile + gridDim.x;
         if (tid == 0) {
-            tma_store4(map, c0, 0, m1, 0, tma_smem(S));
-            tma_commit();
+            if (NBUF > 1 && next < G::NTILES) {
+                tma_wait_read0();                          // the last store from that slot has read it
+                load(next, (it + 1) % NBUF);
+            } else if (next >= G::NTILES) {
+                pdl_trigger();
+            }
         }
-    };
+        double2 *S = S0 + slot * G::TILE;
+        const int m1 = tile / G::NCHUNK, chunk = tile % G::NCHUNK;
+        const int n1 = chunk * W + w;
+        const int c0 = 2 * W * chunk;                      // tensor coordinate (doubles) of the chunk
+        const double2 *twx = TWS0 + slot * FsCfg<NB>::TWS + w * Q;    // w_N^{n1 k1}
+        const double2 *twy = TWS0 + slot * FsCfg<NB>::TWS + W * Q;    // w_N^{m1 l1}
+        (void)n1;
+        double2 v[Q];
+        tma_mbar_wait(mbar0 + 8u * slot, (uint32_t)(it / NBUF) & 1u);
 
-    if constexpr (OP == FS_FWD) {
+        auto xpass_fwd = [&]() {      // v[n2] (thread (m2, w)) -> v[k1] = w^{n1 k1} DFT_n2
+            dft_r<Q, false>(v);
 #pragma unroll
-        for (int n = 0; n < Q; ++n) v[n] = S[(r * Q + n) * W + w];
-        xpass_fwd();
+            for (int k = 1; k < Q; ++k) v[k] = cmulw<false>(v[k], twx[k]);
+        };
+        auto ypass_fwd = [&]() {      // thread (k1, w): rows m2 -> l1
 #pragma unroll
-        for (int k = 0; k < Q; ++k) S[(r * Q + k) * W + w] = v[k];
-        __syncthreads();
-        ypass_fwd();
-        store_tile(&mout);
-    } else {
-        // ---- AA^-1: thread (k1, w): rows l1 -> m2 with w^{-m1 l1}
+            for (int m = 0; m < Q; ++m) v[m] = S[(m * Q + r) * W + w];
+            dft_r<Q, false>(v);
 #pragma unroll
-        for (int l = 0; l < Q; ++l) v[l] = S[(l * Q + r) * W + w];
+            for (int l = 1; l < Q; ++l) v[l] = cmulw<false>(v[l], twy[l]);
 #pragma unroll
-        for (int l = 1; l < Q; ++l) v[l] = cmulw<true>(v[l], __ldg(twy + l));
-        dft_r<Q, true>(v);
-#pragma unroll
-        for (int m = 0; m < Q; ++m) S[(m * Q + r) * W + w] = v[m];
-        __syncthreads();
-        // thread (m2, w): k1 -> n2 with w^{-n1 k1}
-#pragma unroll
-        for (int k = 0; k < Q; ++k) v[k] = S[(r * Q + k) * W + w];
-#pragma unroll
-        for (int k = 1; k < Q; ++k) v[k] = cmulw<true>(v[k], __ldg(twx + k));
-        dft_r<Q, true>(v);
-        __syncthreads();                                   // every thread has read its k1 values
-#pragma unroll
-        for (int n = 0; n < Q; ++n) S[(r * Q + n) * W + w] = v[n];
-        if constexpr (OP == FS_INV) {
-            store_tile(&mout);
-        } else {
-            store_tile(&mphys);                            // the physical field of this step
-            // ---- AA of the next step, from the registers
-            xpass_fwd();
-            if (tid == 0) tma_wait_read0();                // the store has read the tile
+            for (int l = 0; l < Q; ++l) S[(l * Q + r) * W + w] = v[l];
+        };
+        auto store_tile = [&](const CUtensorMap *map) {
+            tma_fence_smem();
             __syncthreads();
+            if (tid == 0) {
+                tma_store4(map, c0, 0, m1, 0, tma_smem(S));
+                tma_commit();
+            }
+        };
+
+        if constexpr (OP == FS_FWD) {
+#pragma unroll
+            for (int n = 0; n < Q; ++n) v[n] = S[(r * Q + n) * W + w];
+            xpass_fwd();
 #pragma unroll
             for (int k = 0; k < Q; ++k) S[(r * Q + k) * W + w] = v[k];
             __syncthreads();
             ypass_fwd();
             store_tile(&mout);
+        } else {
+            // ---- AA^-1: thread (k1, w): rows l1 -> m2 with w^{-m1 l1} (own slots only)
+#pragma unroll
+            for (int l = 0; l < Q; ++l) v[l] = S[(l * Q + r) * W + w];
+#pragma unroll
+            for (int l = 1; l < Q; ++l) v[l] = cmulw<true>(v[l], twy[l]);
+            dft_r<Q, true>(v);
+#pragma unroll
+            for (int m = 0; m < Q; ++m) S[(m * Q + r) * W + w] = v[m];
+            __syncthreads();
+            // thread (m2, w): k1 -> n2 with w^{-n1 k1} (own slots only)
+#pragma unroll
+            for (int k = 0; k < Q; ++k) v[k] = S[(r * Q + k) * W + w];
+#pragma unroll
+            for (int k = 1; k < Q; ++k) v[k] = cmulw<true>(v[k], twx[k]);
+            dft_r<Q, true>(v);
+#pragma unroll
+            for (int n = 0; n < Q; ++n) S[(r * Q + n) * W + w] = v[n];
+            if constexpr (OP == FS_INV) {
+                store_tile(&mout);
+            } else {
+                store_tile(&mphys);                        // the physical field of this step
+                // ---- AA of the next step, from the registers
+                xpass_fwd();
+                if (tid == 0) tma_wait_read0();            // the stores have read their slots
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < Q; ++k) S[(r * Q + k) * W + w] = v[k];
+                __syncthreads();
+                ypass_fwd();
+                store_tile(&mout);
+            }
         }
     }
-    if (tid == 0) tma_wait_read0();                        // smem stays valid until the store has read it
+    if (tid == 0) tma_wait_read0();                        // smem stays valid until the stores have read it
 }
 
 } // namespace fftpde

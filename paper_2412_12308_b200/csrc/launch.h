@@ -171,6 +171,8 @@ cudaError_t launch_peer_transpose(const void *src, const PeerPtrs &peers, int P,
 // over 1024-point lines with the 2D factors (OpTables::ey2d).
 bool fourstep_supported(int64_t nx, int64_t ny, int64_t batch, int elem_bytes);
 cudaError_t launch_aa(int op, const void *in, void *out, void *phys, const void *tw, cudaStream_t st);
+cudaError_t launch_fs_b(bool cols, void *f, const void *tw32, const void *tw16, const OpTables<double> &tab,
+                        cudaStream_t st);
 
 // Block transpose of the sharded path (pack.cu); bw_bytes a multiple of 16.
 cudaError_t launch_pack(const void *in, void *out, int64_t nrows, int64_t nblocks, int64_t bw_bytes,

@@ -155,6 +155,10 @@ tma_cols_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__
                     const T k2 = kxa + __ldg(&tab.ky2[t + TPT * e]);
                     v[e] = cscale(v[e], k2 == (T)0 ? (T)0 : -tab.scale / k2);   // -1/|k|^2, k = 0 zeroed
                 }
+            } else if (tab.ey2d) {                   // four-step By pass: the factor of batch (block) bb
+                const T *m = tab.ey2d + bb * N;
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = cscale(v[e], __ldg(m + t + TPT * e));
             } else {
                 const T exa = tab.ex[col];
 #pragma unroll
