@@ -1,31 +1,41 @@
 """bench.py -- timed run of the 2D FFT-PDE hot path (arXiv 2412.12308) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5] [--impl reference]
 
 A *step* is one pass of the whole hot path over one batch of synthetic input
-(SURVEY.md 8(a) a1-a5): for the default workload c2 (BASELINE.json configs[1])
-that is one ``fftpde_diffuse`` call of 200 exact diffusion steps on a
-1024 x 1024 complex128 grid (each step a forward 2D FFT, the k-space
-multiply and an inverse 2D FFT, 3 kernel launches).  The metric is grid-points
-per second (nx*ny*batch*nsteps / time) for the whole job; rank 0 prints one
-JSON line.
+(SURVEY.md 8(a) a1-a5).  The default workload is C5 (BASELINE.json configs[4]),
+the largest configuration that fits one GPU: one ``fftpde_diffuse`` call of 20
+exact diffusion steps on a 32768 x 32768 complex128 grid (16 GiB; each solve
+step a forward 2D FFT, the k-space multiply and an inverse 2D FFT, the field
+materialised every step).  The metric is grid-points per second
+(nx*ny*batch*nsteps / time) for the whole job; rank 0 prints one JSON line.
+
+Multi-GPU: ``--gpus N`` with N > 1 launches N ranks itself (torch.distributed.run,
+127.0.0.1) unless WORLD_SIZE is already set, and checks WORLD_SIZE == N.  C5 at
+N > 1 runs the row-slab decomposition of SURVEY.md 8(e) (strong scaling, fixed
+32768^2 grid); the default exchange is ``fused`` (the row and column passes store
+straight into the peers' slabs over NVLink).  C1-C4 at N > 1 run independent
+replicas (weak scaling, no collective on the data path).
 
 Timing: W untimed warm-up steps, then exactly K steps, each bracketed by CUDA
 events on the plan's stream; L2 (126 MB) is flushed with a 256 MiB write
-between timed steps (outside the events).  Barrier + synchronize on both sides
-of the timed region; the per-rank device time is reduced with MAX over ranks.
-Multi-GPU (torchrun, one process per GPU): c1-c4 fit one GPU, so N > 1 runs N
-independent replicas (weak scaling, no collective on the data path).
+between timed steps (outside the events; C5's field is larger than L2 anyway).
+Barrier + synchronize on both sides of the timed region; the per-rank device
+time is reduced with MAX over ranks.
 
-Extra keys: ``e2e`` (the same metric through the public API with host buffers:
-pinned host -> device copy, solve, device -> host copy, every step),
-``roofline`` (dominant kernel class, algorithmic bytes / its CUDA-event time vs
-MEASURED_PEAKS.json hbm_gbs), ``cpu_baseline`` (the fp64 oracle on this host's
-cores, bounded sample; rank 0, N = 1), ``clocks`` (nvidia-smi sampled during
-the timed region), ``gpu_launches`` (library kernels in the timed region).
+Extra keys: ``e2e`` (the same metric through the public API with pinned host
+buffers: host -> device copy, solve, device -> host copy, every step),
+``roofline`` (every kernel class's share-scaled launch time against the HBM
+and the FP64 roofs, the binding one computed per class; the step against the
+method's algorithmic bytes), ``parity`` (C5: the periodic heat kernel at
+sampled points and the mean drift; C1-C4: relative L2 against the fp64 oracle,
+computed in the cpu_baseline leg), ``cpu_baseline`` (the fp64 oracle on this
+host's cores, bounded sample; rank 0, N = 1), ``clocks`` (nvidia-smi sampled
+during the timed region), ``gpu_launches`` (library kernels in the timed region).
 
-``--impl reference`` times the CPU oracle (the reference arm of this tier) on
-the same workload, metric and unit, each step a bounded sample.
+``--impl reference`` times the CPU oracle (the reference arm of this tier) with
+the same ``config``, metric and unit, each step a bounded sample named in
+``cpu_baseline.sample``.
 """
 from __future__ import annotations
 
@@ -33,6 +43,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -45,6 +56,8 @@ sys.path.insert(0, ROOT)
 METRIC = "2D FFT-PDE solve grid-points/sec and achieved HBM GB/s vs peak (1/2/4/8 GPU)"
 UNIT = "grid-points/s"
 L2_FLUSH_BYTES = 256 << 20
+NVLINK_GBS = 770.0            # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+FALLBACK_HBM_GBS = 6650.0     # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
 
 THROTTLE_BITS = {
     0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
@@ -56,21 +69,36 @@ THROTTLE_BITS = {
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "rk4", "rk4big", "dsrc", "p3d", "d3d",
-                             "c2r", "c3r", "c4r"],
-                    help="c1-c5: BASELINE.json configs[0..4]; rk4/rk4big: the paper's orbiting-source "
-                         "RK4 run (SURVEY.md 8(f) row 1, not a BASELINE config)")
+    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "rk4", "rk4big", "dsrc", "p3d",
+                                                        "d3d", "c2r", "c3r", "c4r"],
+                    help="c1-c5: BASELINE.json configs[0..4] (default c5, the largest single-GPU config); "
+                         "rk4/rk4big: the paper's orbiting-source RK4 run (SURVEY.md 8(f) row 1, not a BASELINE config)")
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="c5: use the slab-decomposed path even on one GPU (P = 1 process group)")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer", "lib", "fused"],
-                    help="sharded c5: pack + NCCL all-to-all, or direct peer stores into torch "
-                         "symmetric memory (fftpde_peer_transpose, SURVEY.md 8(e) N10)")
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl", "peer", "lib"],
+                    help="sharded c5: exchanges fused into the row / column passes (peer stores into torch "
+                         "symmetric memory, default), pack + NCCL all-to-all, a separate peer-store "
+                         "transpose, or NCCL inside libfftpde (fftpde_plan_2d_sharded)")
     return ap.parse_args()
+
+
+def free_port():
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args):
+    """--gpus N without a launcher: run this script under torch.distributed.run with N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 # ---------------------------------------------------------------------------- inputs
@@ -109,38 +137,89 @@ def make_device_inputs(wl, dtype):
     import torch
     from paper_2412_12308_b200 import inputs as I
     if wl.name.startswith("c5"):
-        f, _, _, _ = I.c5_field_torch(wl.nx, dtype=dtype)
-        return [f], None
+        f, centres, sigmas, amps = I.c5_field_torch(wl.nx, dtype=dtype)
+        return [f], None, (centres, sigmas, amps)
     host = make_inputs(wl)
-    return [torch.from_numpy(np.ascontiguousarray(h)).to(dtype).cuda() for h in host], host
+    return [torch.from_numpy(np.ascontiguousarray(h)).to(dtype).cuda() for h in host], host, None
 
 
-def alg_bytes_per_launch(wl, kernel_class):
-    """Algorithmic HBM bytes of one launch, averaged over the launches of a
-    solve: every field the pass touches is read once and written once
-    (SURVEY.md 8(d)); in a multi-step solve the row passes between column
-    passes are MID passes (inverse rows of step s stored as the physical field
-    + forward rows of step s+1: one read, two writes), the first and last are
-    plain forward / inverse rows (one read, one write)."""
-    esz = {"c128": 16, "c64": 8, "f64": 8, "f32": 4}[wl.dtype]
-    field = wl.nx * wl.ny * wl.nz * wl.batch * esz      # real fields: the half spectrum has ~ the same bytes
+def esize(wl):
+    return {"c128": 16, "c64": 8, "f64": 8, "f32": 4}[wl.dtype]
+
+
+def field_bytes(wl):
+    return wl.nx * wl.ny * wl.nz * wl.batch * esize(wl)
+
+
+def pass_bytes_per_launch(wl, kernel_class):
+    """Bytes a launch of the class must move by its own function, averaged over the
+    launches of a solve: every field it touches read once and written once; a MID
+    pass (inverse of step s stored as the physical field + forward of step s+1)
+    reads once and writes twice.  Summed over the step these are the design's
+    bytes; the method's own minimum is alg_step_bytes."""
+    field = field_bytes(wl)
+    n = wl.nsteps
     if kernel_class == "wave_col_pass":
         return 2 * 2 * field
+    if kernel_class == "aa_pass":          # C5 four-step: 1 AA, n-1 MID, 1 AA^-1 per solve
+        return (2 * field * 2 + 3 * field * (n - 1)) / (n + 1) if n > 1 else 2 * field
     if wl.op == "dsrc":
-        # per step: forward (rows, columns), u^ <- E u^ + Phi s^ (u^, s^ in, u^ out), inverse
         return 3 * field if kernel_class == "pointwise" else 2 * field
     if wl.op == "rk4":
-        # per step: 2 source samplings (1 write each) and the RK4 kernel (u^, v^, 3 source
-        # spectra read, u^, v^ written); the transforms are plain forward passes
         return 3 * field if kernel_class == "pointwise" else 2 * field
-    # the complex 2D diffusion is separable: each step is one row pass (forward,
-    # x factor, inverse) and one column pass, each reading and writing the field
-    # once; the wave, the real-field and the 3D diffusion keep the MID row pass
-    mid_rows = wl.op == "wave"
-    if kernel_class == "row_pass" and mid_rows and wl.nsteps > 1:
-        n = wl.nsteps                      # per field: 1 FWD + (n-1) MID + 1 INV launches
+    if kernel_class == "row_pass" and wl.op == "wave" and n > 1:
         return (2 * field * 2 + 3 * field * (n - 1)) / (n + 1)
     return 2 * field
+
+
+def alg_step_bytes(wl):
+    """The method's algorithmic bytes of one bench step: each state field read and
+    written once per solve step (SURVEY.md 8(d) table, 32 B/pt/step for one c128 field)."""
+    fields = 2 if wl.op in ("wave", "rk4") else 1
+    steps = wl.nsteps if wl.op != "poisson" else 1
+    return 2 * fields * wl.points * esize(wl) * steps
+
+
+def survey_design_passes(wl):
+    """the 3-pass design roof (1 pass for the single-CTA C1 grid)."""
+    return 1 if wl.name.startswith("c1") else 3
+
+
+# ---------------------------------------------------------------------------- peaks
+
+def load_peaks():
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = peaks.get("hbm_gbs")
+    src = "MEASURED_PEAKS.json hbm_gbs (measured copy)" if hbm else "fallback 6650 GB/s (B200_PROFILING.md)"
+    # FP64 / FP32 instruction roofs measured on this pool (tools/fp64_peak.cu, profiles/r02/fp64_peak.jsonl)
+    dp, sp, alu_src = 18.46e12, 36.20e12, "profiles/r02/fp64_peak.jsonl (measured DADD / FADD rate, 1965 MHz)"
+    try:
+        for line in open(os.path.join(ROOT, "profiles", "r02", "fp64_peak.jsonl")):
+            d = json.loads(line)
+            if d.get("kind") == "dadd":
+                dp = d["ginst_per_s"] * 1e9
+            if d.get("kind") == "fadd":
+                sp = d["ginst_per_s"] * 1e9
+    except Exception:
+        alu_src = "vendor lane counts: 64 FP64 / 128 FP32 lanes per SM x 148 SMs x 1965 MHz"
+    return {"hbm_gbs": hbm or FALLBACK_HBM_GBS, "hbm_src": src, "dp_inst_s": dp, "sp_inst_s": sp, "alu_src": alu_src}
+
+
+def load_counts(wl):
+    """Per-launch ncu counts of each kernel class (tools/kernel_counts.py): DRAM bytes
+    and FP64 / FP32 thread instructions; None where no capture is committed."""
+    for name in (f"counts_{wl.name}.json", f"traffic_{wl.name}.json"):
+        p = os.path.join(ROOT, "profiles", name)
+        if os.path.exists(p):
+            try:
+                return json.load(open(p)), name
+            except Exception:
+                pass
+    return {}, None
 
 
 # ---------------------------------------------------------------------------- clocks
@@ -208,9 +287,16 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def smi_index():
+    import torch
+    gpu_index = torch.cuda.current_device()
+    vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+    return int(vis[gpu_index]) if len(vis) > gpu_index and vis[gpu_index].isdigit() else gpu_index
+
+
 # ---------------------------------------------------------------------------- dist
 
-def dist_setup(n_gpus):
+def dist_setup():
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -230,14 +316,179 @@ def barrier(world):
         dist.barrier()
 
 
-def max_over_ranks(world, value):
+def reduce_over_ranks(world, value, op="max"):
     if world == 1:
         return value
     import torch
     import torch.distributed as dist
     t = torch.tensor([value], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op={"max": dist.ReduceOp.MAX, "sum": dist.ReduceOp.SUM}[op])
     return float(t.item())
+
+
+# ---------------------------------------------------------------------------- roofline
+
+def roofline_block(wl, prof, ms_per_step, steps, world=1, slab_fraction=1.0, extra=None):
+    """Every kernel class against the HBM and the FP64 (FP32 for complex64) roofs.
+
+    Per class: the launch time is the class's share of the profiled replays x the
+    un-instrumented CUDA-event step time / launches per step; T_hbm = the pass's own
+    bytes / peak HBM; T_alu = its FP64 (FP32) instructions per launch (ncu counts,
+    tools/kernel_counts.py) / the measured instruction rate; the binding roof is the
+    larger of the two and frac = T_bound / launch time.  The dominant class (largest
+    share) fills the contract keys.  `step` compares the whole step with the method's
+    algorithmic bytes (one read + one write of each state field per solve step) and
+    with the survey's 3-pass design roof, so no pass is counted against the method twice."""
+    peaks = load_peaks()
+    counts, counts_src = load_counts(wl)
+    fp32 = wl.dtype in ("c64", "f32")
+    alu_peak = peaks["sp_inst_s"] if fp32 else peaks["dp_inst_s"]
+    classes = {k: v for k, v in prof.items() if v[1] > 0}
+    total = sum(v[0] for v in classes.values()) or 1.0
+    per = {}
+    for k, (ms, n) in classes.items():
+        lps = n / steps
+        share = ms / total
+        t_launch = share * ms_per_step * 1e-3 / lps
+        pb = pass_bytes_per_launch(wl, k) * slab_fraction
+        t_hbm = pb / (peaks["hbm_gbs"] * 1e9)
+        c = counts.get(k) if isinstance(counts.get(k), dict) else None
+        inst = None
+        if c:
+            inst = c.get("sp_inst" if fp32 else "dp_inst")
+        t_alu = inst * slab_fraction / alu_peak if inst else None
+        bound = "alu" if (t_alu is not None and t_alu > t_hbm) else "hbm"
+        traffic = c.get("dram_bytes") if c else (counts.get(k) if isinstance(counts.get(k), (int, float)) else None)
+        per[k] = {
+            "share_of_step": round(share, 4), "launches_per_step": lps, "ms_per_launch": round(t_launch * 1e3, 4),
+            "pass_bytes_per_launch": pb, "gbs": round(pb / t_launch / 1e9, 1),
+            "hbm_frac": round(t_hbm / t_launch, 4),
+            "fp_inst_per_launch": inst, "alu_frac": round(t_alu / t_launch, 4) if t_alu else None,
+            "bound": bound, "traffic": traffic,
+            "traffic_over_pass_bytes": round(traffic / pb, 3) if traffic else None,
+        }
+    dom = max(per, key=lambda k: per[k]["share_of_step"])
+    d = per[dom]
+    t_launch = d["ms_per_launch"] * 1e-3
+    if d["bound"] == "alu":
+        achieved = d["fp_inst_per_launch"] * slab_fraction / t_launch / 1e9
+        peak, unit = alu_peak / 1e9, ("GFP32inst/s" if fp32 else "GFP64inst/s")
+        peak_src = peaks["alu_src"]
+    else:
+        achieved = d["pass_bytes_per_launch"] / t_launch / 1e9
+        peak, unit, peak_src = peaks["hbm_gbs"], "GB/s", peaks["hbm_src"]
+    step_s = ms_per_step * 1e-3
+    alg = alg_step_bytes(wl) * slab_fraction
+    design = sum(v["pass_bytes_per_launch"] * v["launches_per_step"] for v in per.values())
+    t3 = survey_design_passes(wl) * alg / (peaks["hbm_gbs"] * 1e9)
+    out = {
+        "bound": d["bound"], "achieved": round(achieved, 1), "peak": peak, "unit": unit,
+        "frac": round(achieved / peak, 4), "traffic": d["traffic"], "kernel": dom,
+        "peak_source": peak_src, "counts_source": counts_src,
+        "alg_bytes_per_launch": d["pass_bytes_per_launch"],
+        "duration_method": "class share of CUDA-event-profiled replays x un-instrumented CUDA-event step time",
+        "per_kernel": per,
+        "step": {
+            "alg_bytes": alg, "alg_gbs": round(alg / step_s / 1e9, 1),
+            "alg_frac": round(alg / step_s / 1e9 / peaks["hbm_gbs"], 4),
+            "design_bytes": design, "design_round_trips": round(design / alg, 3),
+            "design_gbs": round(design / step_s / 1e9, 1),
+            "design_frac": round(design / step_s / 1e9 / peaks["hbm_gbs"], 4),
+            "survey_3pass_ms": round(t3 * 1e3, 4), "survey_3pass_frac": round(t3 / step_s, 4),
+            "note": "alg_frac: the method's one round trip per solve step (SURVEY.md 8(d)); "
+                    "survey_3pass_frac: the survey's 3-pass design roof / step time (north_star's >= 60% bar)",
+        },
+    }
+    if extra:
+        out.update(extra)
+    return out
+
+
+# ---------------------------------------------------------------------------- parity
+
+def heat_kernel_points(ks, js, n, centres, sigmas, amps, D, T):
+    """The exact solution of u_t = D nabla^2 u from a sum of Gaussians A e^{-d^2/sigma^2}
+    (PAPER.md:390-398), summed over the periodic images +-1 (R9):
+    u = sum_i A_i sigma_i^2 / (sigma_i^2 + 4 D T) exp(-d^2 / (sigma_i^2 + 4 D T))."""
+    import numpy as np
+    x, y = js / n, ks / n
+    out = np.zeros(len(ks))
+    for (cx, cy), s, a in zip(centres, sigmas, amps):
+        s2 = s * s + 4 * D * T
+        for ix in (-1, 0, 1):
+            for iy in (-1, 0, 1):
+                dx = x - cx + ix
+                dy = y - cy + iy
+                out += a * (s * s / s2) * np.exp(-(dx * dx + dy * dy) / s2)
+    return out
+
+
+def c5_parity(u_dev, u0_dev, params, wl, row0=0):
+    """Heat kernel at sampled points of this rank's rows [row0, row0 + rows) and the
+    sums for the mean drift (Fig. 4)."""
+    import numpy as np
+    import torch
+    centres, sigmas, amps = params
+    n = wl.nx
+    rows = u_dev.shape[0]
+    rng = np.random.default_rng(5 + row0)
+    ks = rng.integers(0, rows, 1500)
+    js = rng.integers(0, n, 1500)
+    near = [(round(cy * n) % n - row0, round(cx * n) % n) for (cx, cy) in centres[:400]
+            if 0 <= round(cy * n) % n - row0 < rows]
+    if near:
+        ks = np.concatenate([ks, np.array([k for k, _ in near])])
+        js = np.concatenate([js, np.array([j for _, j in near])])
+    got = u_dev[torch.from_numpy(ks).cuda(), torch.from_numpy(js).cuda()].cpu().numpy()
+    exact = heat_kernel_points(ks + row0, js, n, centres, sigmas, amps, wl.D, wl.nsteps * wl.dt)
+    return {"err2": float(np.sum(np.abs(got - exact) ** 2)), "ref2": float(np.sum(exact ** 2)),
+            "max_imag": float(np.max(np.abs(got.imag))), "points": int(len(ks)),
+            "sum_u": float(u_dev.real.double().sum().item()), "sum_u0": float(u0_dev.real.double().sum().item())}
+
+
+def finish_c5_parity(parts, world):
+    import math as m
+    err2 = reduce_over_ranks(world, parts["err2"], "sum")
+    ref2 = reduce_over_ranks(world, parts["ref2"], "sum")
+    su = reduce_over_ranks(world, parts["sum_u"], "sum")
+    su0 = reduce_over_ranks(world, parts["sum_u0"], "sum")
+    mi = reduce_over_ranks(world, parts["max_imag"], "max")
+    pts = reduce_over_ranks(world, parts["points"], "sum")
+    return {"kind": "closed form: periodic heat kernel at sampled points (PAPER.md:376-398) + mean drift (Fig. 4)",
+            "rel_l2": m.sqrt(err2 / ref2), "points": int(pts), "mean_drift": abs(su / su0 - 1.0),
+            "max_abs_imag": mi, "tolerance": 1e-12, "pass": m.sqrt(err2 / ref2) <= 1e-12 and abs(su / su0 - 1) <= 1e-12}
+
+
+def rel_l2(a, b):
+    import numpy as np
+    a = np.asarray(a, np.complex128).ravel()
+    b = np.asarray(b, np.complex128).ravel()
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def oracle_parity(wl, host, outs):
+    """C1-C4 parity against the fp64 oracle on the same input bytes (cpu_baseline leg)."""
+    import numpy as np
+    from oracle import oracle as O
+    tol = 1e-5 if wl.dtype == "c64" else 1e-12
+    got = [o.cpu().numpy() for o in outs]
+    if wl.name.startswith("c1"):
+        return {"kind": "oracle, full solve", "rel_l2": rel_l2(got[0], O.poisson(host[0])), "tolerance": tol}
+    if wl.name.startswith("c2"):
+        ref = O.diffuse(host[0], wl.D, wl.dt, wl.nsteps)
+        mean0 = float(np.mean(host[0].real))
+        return {"kind": "oracle, full stepped solve", "rel_l2": rel_l2(got[0], ref), "tolerance": tol,
+                "mean_drift": abs(float(np.mean(got[0].real)) / mean0 - 1.0)}
+    if wl.name.startswith("c3"):
+        U, V = O.wave(host[0], host[1], wl.c, wl.dt, wl.nsteps, collapsed=True)
+        mean0 = float(np.mean(host[0].real))
+        return {"kind": "oracle, collapsed (one propagator at T = nsteps dt)", "rel_l2_u": rel_l2(got[0], U),
+                "rel_l2_ut": rel_l2(got[1], V), "tolerance": tol,
+                "mean_drift": abs(float(np.mean(got[0].real)) / mean0 - 1.0)}
+    if wl.name.startswith("c4"):
+        errs = [rel_l2(got[0][g], O.poisson(host[0][g].astype(np.complex128))) for g in (0, 85, 170, 255)]
+        return {"kind": "oracle, grids 0/85/170/255 (upcast input)", "rel_l2_max": max(errs), "tolerance": tol}
+    return None
 
 
 # ---------------------------------------------------------------------------- native arm
@@ -262,6 +513,37 @@ def reset_wave(wl, dev_in, out):
         out[1].copy_(dev_in[1])
 
 
+def timed_steps(args, world, stream, flush, body, pre=None):
+    """W warm-up steps, one untimed step after the clock sampler starts, then K
+    event-bracketed steps (L2 flushed before each).  Returns (per-step ms, clocks)."""
+    import torch
+    for _ in range(args.warmup):
+        if pre:
+            pre()
+        body()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(smi_index()) as clk:
+        # the GPU idled while the sampler started: one more untimed step
+        if pre:
+            pre()
+        flush.zero_()
+        body()
+        for i in range(args.steps):
+            if pre:
+                pre()
+            flush.zero_()
+            starts[i].record(stream)
+            body()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    return [s.elapsed_time(e) for s, e in zip(starts, ends)], clk.summary()
+
+
 def native(args, wl, world, rank, local):
     import numpy as np
     import torch
@@ -269,9 +551,7 @@ def native(args, wl, world, rank, local):
 
     dtype = {"c128": torch.complex128, "c64": torch.complex64, "f64": torch.float64,
              "f32": torch.float32}[wl.dtype]
-    dev_in, host = make_device_inputs(wl, dtype)
-    # C5 (16 GiB field): built on the device; the e2e leg copies it once into pinned
-    # host memory (outside the timed region), the CPU baseline takes a bounded sample
+    dev_in, host, c5params = make_device_inputs(wl, dtype)
     out = [torch.empty_like(d) for d in dev_in]
     if wl.dtype in ("f64", "f32"):
         plan = F.PlanR2C(wl.nx, wl.ny, batch=wl.batch, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly)
@@ -282,42 +562,24 @@ def native(args, wl, world, rank, local):
     stream = torch.cuda.current_stream()
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
-    # warm-up (also uploads the operator tables for this (D, dt) / (c, dt))
-    for _ in range(args.warmup):
-        reset_wave(wl, dev_in, out)
-        run_solve(plan, wl, dev_in, out)
-    torch.cuda.synchronize()
+    launches = {}
 
-    # ---- timed region: K steps, events per step, L2 flushed between steps
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    launches0 = plan.launches
-    gpu_index = torch.cuda.current_device()
-    barrier(world)
-    torch.cuda.synchronize()
-    vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
-    smi_index = int(vis[gpu_index]) if len(vis) > gpu_index and vis[gpu_index].isdigit() else gpu_index
-    with ClockSampler(smi_index) as clk:
-        # one more untimed step right before the timed ones: the GPU idled while the
-        # clock sampler started, and the first kernel after an idle period runs slow
-        reset_wave(wl, dev_in, out)
-        flush.zero_()
+    def body():
         run_solve(plan, wl, dev_in, out)
-        launches0 = plan.launches            # count the timed steps' launches only
-        for i in range(args.steps):
-            reset_wave(wl, dev_in, out)
-            flush.zero_()
-            starts[i].record(stream)
-            run_solve(plan, wl, dev_in, out)
-            ends[i].record(stream)
-        torch.cuda.synchronize()
-    barrier(world)
-    launches = plan.launches - launches0
-    ms_rank = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    ms_total = max_over_ranks(world, ms_rank)
+
+    l0 = plan.launches
+    times, clocks = timed_steps(args, world, stream, flush, body, pre=lambda: reset_wave(wl, dev_in, out))
+    launches = (plan.launches - l0) * args.steps // (args.warmup + 1 + args.steps)
+    ms_rank = sum(times)
+    ms_total = reduce_over_ranks(world, ms_rank)
     ms_per_step = ms_total / args.steps
     pts_per_step = wl.points * (wl.nsteps if wl.op != "poisson" else 1)
     value = world * pts_per_step * args.steps / (ms_total * 1e-3)
+
+    # ---- parity of the last timed step's output (outside the timed region)
+    parity = None
+    if not args.no_parity and c5params is not None:
+        parity = finish_c5_parity(c5_parity(out[0], dev_in[0], c5params, wl), world)
 
     # ---- per-kernel timing (same calls, events around every launch)
     plan.read_profile()
@@ -329,53 +591,7 @@ def native(args, wl, world, rank, local):
     torch.cuda.synchronize()
     prof = plan.read_profile()
     plan.set_profiling(False)
-    dom = max(prof.items(), key=lambda kv: kv[1][0])
-    dom_name, (dom_ms, dom_n) = dom
-    total_prof = sum(v[0] for v in prof.values())
-    # Event nodes between kernels slow a graph replay down (each costs about a
-    # kernel boundary), so the profiled run fixes each kernel class's SHARE of
-    # the step and the un-instrumented timed region fixes the step time:
-    # dominant launch duration = share x (timed ms/step) / launches per step.
-    share = dom_ms / total_prof if total_prof else 1.0
-    dom_launches_per_step = dom_n / args.steps
-    dom_avg_s = share * ms_per_step * 1e-3 / dom_launches_per_step
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = alg_bytes_per_launch(wl, dom_name) / dom_avg_s / 1e9
-    traffic, pipe_pct = None, None
-    tpath = os.path.join(ROOT, "profiles", f"traffic_{wl.name}.json")
-    if os.path.exists(tpath):
-        try:
-            tj = json.load(open(tpath))
-            traffic = tj.get(dom_name)
-            pipe_pct = (tj.get("_pipe_pct") or {}).get(dom_name)
-        except Exception:
-            traffic = None
-    roofline = {
-        "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-        "frac": round(achieved / peak, 4), "traffic": traffic,
-        "kernel": dom_name, "launches_per_step": dom_n // args.steps,
-        "avg_launch_us": round(dom_avg_s * 1e6, 2),
-        "share_of_step": round(dom_ms / total_prof, 3) if total_prof else None,
-        "alg_bytes_per_launch": alg_bytes_per_launch(wl, dom_name),
-        # DRAM bytes per launch (ncu, caches flushed) / algorithmic bytes: the implied
-        # number of field round trips relative to the one the method needs
-        "traffic_over_alg": round(traffic / alg_bytes_per_launch(wl, dom_name), 3) if traffic else None,
-        # FP64 / FP32-FMA pipe utilisation of the dominant class from the same ncu capture
-        "pipe_active_pct": pipe_pct,
-        "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
-                       else "fallback 6650 GB/s (B200_PROFILING.md)",
-        # every class's share of the profiled replays x the un-instrumented step time
-        # (sums to ms_per_step); the raw event-instrumented times over-state short kernels
-        "per_kernel_ms_per_step": {k: round(v[0] / total_prof * ms_per_step, 4) if total_prof else None
-                                   for k, v in prof.items()},
-        "per_kernel_event_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in prof.items()},
-        "duration_method": "share of the step from CUDA-event-profiled replays x un-instrumented CUDA-event step time",
-    }
+    roofline = roofline_block(wl, prof, ms_per_step, args.steps)
 
     # ---- e2e through the public API with host buffers
     e2e = None
@@ -433,25 +649,33 @@ def native(args, wl, world, rank, local):
             torch.cuda.synchronize()
             tot += time.perf_counter() - t0
         barrier(world)
-        tot = max_over_ranks(world, tot)
+        tot = reduce_over_ranks(world, tot)
         nbytes = sum(h.numel() * h.element_size() for h in host_in)
         e2e = {"value": world * pts_per_step * args.steps / tot, "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                "timer": "host perf_counter around the public-API call (pinned host buffers)"}
+        del host_in, host_out
 
-    # ---- CPU oracle baseline (rank 0, N = 1)
+    # ---- CPU oracle baseline (rank 0, N = 1); C1-C4 parity against the oracle
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(wl, host if host is not None else None)
+        cpu = cpu_baseline(wl, host)
+        if not args.no_parity and host is not None and wl.name[:2] in ("c1", "c2", "c3", "c4") and wl.nz == 1 \
+                and wl.dtype in ("c128", "c64"):
+            reset_wave(wl, dev_in, out)
+            run_solve(plan, wl, dev_in, out)
+            torch.cuda.synchronize()
+            parity = oracle_parity(wl, host, out)
 
-    clocks = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if wl.dtype in ("c128", "f64") else "f32",
+        "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "median_ms_per_step": reduce_over_ranks(world, statistics.median(times)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if wl.dtype in ("c128", "f64") else "f32",
         "data": "synthetic (seeded, BASELINE.json recipe; paper_2412_12308_b200/inputs.py)",
         "config": workload_config(wl, world),
-        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+        "e2e": e2e, "roofline": roofline, "parity": parity, "cpu_baseline": cpu, "clocks": clocks,
         "gpu_launches": launches,
         "hbm_gbs_alg": round(world * alg_step_bytes(wl) * args.steps / (ms_total * 1e-3) / 1e9, 1),
     }
@@ -474,86 +698,89 @@ class _LibSharded:
 
 
 def sharded_native(args, wl, world, rank, local):
-    """C5 at N > 1: the slab decomposition, NCCL all-to-all between
-    the libfftpde row and column-slab passes; strong scaling (fixed 32768^2 grid)."""
+    """C5 at N > 1 (or --sharded): the row-slab decomposition; strong
+    scaling (fixed 32768^2 grid).  Roofline: max(T_HBM, T_NVL) per rank with the
+    variant's own pass count (SURVEY.md 8(e) table and HBM-cost note)."""
     import torch
     from paper_2412_12308_b200 import inputs as I
     from paper_2412_12308_b200 import sharded as S
     dtype = torch.complex128
-    full, _, _, _ = I.c5_field_torch(wl.nx, dtype=dtype)
+    full, centres, sigmas, amps = I.c5_field_torch(wl.nx, dtype=dtype)
     lo, hi = S.slab_rows(wl.ny, world, rank)
     slab = full[lo:hi].contiguous()
     del full
     torch.cuda.empty_cache()
-    if args.exchange == "lib":     # the whole slab solve inside the C ABI (fftpde_plan_2d_sharded)
+    exchange = args.exchange
+    if exchange == "lib":     # the whole slab solve inside the C ABI (fftpde_plan_2d_sharded)
         from paper_2412_12308_b200 import fftpde as F
         ops = _LibSharded(F.ShardedPlan(wl.nx, wl.ny, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly))
         solver = ops
     else:
         ops = S.CudaLocalOps(wl.nx, wl.ny, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly)
-    if args.exchange == "peer":
-        solver = S.PeerSlabSolver(wl.nx, wl.ny, S.SymmetricPeerComm(), ops)
-    elif args.exchange == "fused":   # row pass stores straight into the peers' column slabs
-        solver = S.FusedPeerSlabSolver(wl.nx, wl.ny, S.SymmetricPeerComm(), ops)
-    elif args.exchange == "nccl":
-        solver = S.SlabSolver(wl.nx, wl.ny, S.DistComm(), ops)
+        if exchange == "peer":
+            solver = S.PeerSlabSolver(wl.nx, wl.ny, S.SymmetricPeerComm(), ops)
+        elif exchange == "fused":   # row and column passes store straight into the peers' slabs
+            solver = S.FusedPeerSlabSolver(wl.nx, wl.ny, S.SymmetricPeerComm(), ops)
+        else:
+            solver = S.SlabSolver(wl.nx, wl.ny, S.DistComm(), ops)
     out = [torch.empty_like(slab)]
-    for _ in range(args.warmup):
-        solver.diffuse([slab], wl.D, wl.dt, wl.nsteps, outs=out)
-    torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
     l0 = ops.launches
-    barrier(world)
-    torch.cuda.synchronize()
-    gpu_index = torch.cuda.current_device()
-    vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
-    smi_index = int(vis[gpu_index]) if len(vis) > gpu_index and vis[gpu_index].isdigit() else gpu_index
-    with ClockSampler(smi_index) as clk:
-        for i in range(args.steps):
-            starts[i].record(stream)
-            solver.diffuse([slab], wl.D, wl.dt, wl.nsteps, outs=out)
-            ends[i].record(stream)
-        torch.cuda.synchronize()
-    barrier(world)
-    ms_total = max_over_ranks(world, sum(a.elapsed_time(b) for a, b in zip(starts, ends)))
+
+    def body():
+        solver.diffuse([slab], wl.D, wl.dt, wl.nsteps, outs=out)
+
+    times, clocks = timed_steps(args, world, stream, flush, body)
+    launches = (ops.launches - l0) * args.steps // (args.warmup + 1 + args.steps)
+    ms_total = reduce_over_ranks(world, sum(times))
+    ms_per_step = ms_total / args.steps
     pts = wl.nx * wl.ny * wl.nsteps
     value = pts * args.steps / (ms_total * 1e-3)
+    parity = None
+    if not args.no_parity:
+        parity = finish_c5_parity(c5_parity(out[0], slab, (centres, sigmas, amps), wl, row0=lo), world)
     ops.plan.read_profile()
     ops.plan.set_profiling(True)
     solver.diffuse([slab], wl.D, wl.dt, wl.nsteps, outs=out)
     torch.cuda.synchronize()
     prof = ops.plan.read_profile()
     ops.plan.set_profiling(False)
-    dom_name, (dom_ms, dom_n) = max(prof.items(), key=lambda kv: kv[1][0])
+    # per rank and step: HBM = passes x (read + write) of the slab, NVLink = the
+    # bytes leaving the rank in the two exchanges (per direction)
     slab_bytes = (hi - lo) * wl.nx * 16
-    achieved = 2 * slab_bytes / (dom_ms / dom_n * 1e-3) / 1e9
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    peak = peaks.get("hbm_gbs", 6650.0)
-    a2a_bytes = slab_bytes * (world - 1) // world
+    hbm_passes = {"fused": 2, "peer": 3, "nccl": 5, "lib": 5}[exchange]
+    nvl_bytes = 2 * slab_bytes * (world - 1) // world
+    peaks = load_peaks()
+    t_hbm = hbm_passes * 2 * slab_bytes / (peaks["hbm_gbs"] * 1e9)
+    t_nvl = nvl_bytes / (NVLINK_GBS * 1e9)
+    step_s = ms_per_step * 1e-3 / wl.nsteps
+    prof_steps = {k: (v[0], v[1]) for k, v in prof.items()}
+    extra = {"sharded": {
+        "exchange": exchange, "ranks": world, "slab_bytes": slab_bytes,
+        "hbm_bytes_per_rank_step": hbm_passes * 2 * slab_bytes, "nvlink_bytes_per_rank_step": nvl_bytes,
+        "nvlink_gbs_per_rank": round(nvl_bytes / step_s / 1e9, 1) if world > 1 else 0.0,
+        "t_hbm_ms": round(t_hbm * 1e3, 4), "t_nvl_ms": round(t_nvl * 1e3, 4),
+        "roof": "nvlink" if t_nvl > t_hbm else "hbm",
+        "frac_of_max_roof": round(max(t_hbm, t_nvl) / step_s, 4),
+        "nvlink_peak_gbs": NVLINK_GBS, "nvlink_peak_source": "B200_PROFILING.md measured peer copy per direction",
+    }}
+    roofline = roofline_block(wl, prof_steps, ms_per_step, 1, world, slab_fraction=(hi - lo) / wl.ny, extra=extra)
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "median_ms_per_step": reduce_over_ranks(world, statistics.median(times)),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded C5 recipe, built on device)",
         "config": {**workload_config(wl, world),
                    "parallelism": f"slab x{world} " + {
                        "peer": "(peer-store exchange, symmetric memory)",
                        "fused": "(row and column passes store into the peers' slabs, symmetric memory; separable diffusion)",
                        "nccl": "(NCCL all-to-all, Python-driven)",
-                       "lib": "(NCCL all-to-all inside libfftpde, fftpde_plan_2d_sharded)"}[args.exchange],
-                   "l2": "field (16 GiB) larger than L2"},
-        "e2e": None, "cpu_baseline": None, "clocks": clk.summary(),
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None, "kernel": dom_name,
-                     "per_kernel_ms_per_solve": {k: round(v[0], 3) for k, v in prof.items()},
-                     "alltoall_bytes_per_rank": a2a_bytes, "alltoalls_per_solve": 2 * wl.nsteps},
-        "gpu_launches": ops.launches - l0,
+                       "lib": "(NCCL all-to-all inside libfftpde, fftpde_plan_2d_sharded)"}[exchange],
+                   "l2": "field (16 GiB) larger than L2; 256 MiB buffer zeroed between timed steps"},
+        "e2e": None, "cpu_baseline": None, "clocks": clocks, "parity": parity,
+        "roofline": roofline, "gpu_launches": launches,
     }
 
 
@@ -569,44 +796,26 @@ def sharded3d_native(args, wl, world, rank, local):
     plan = F.ShardedPlan3D(wl.nx, wl.ny, wl.nz, dtype=torch.complex128, Lx=wl.Lx, Ly=wl.Ly)
     out = torch.empty_like(slab)
 
-    def solve():
+    def body():
         if wl.op == "poisson":
             plan.poisson(slab, out=out)
         else:
             plan.diffuse(slab, wl.D, wl.dt, wl.nsteps, out=out)
 
-    for _ in range(args.warmup):
-        solve()
-    torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
     l0 = plan.launches
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    barrier(world)
-    torch.cuda.synchronize()
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        for i in range(args.steps):
-            flush.zero_()
-            starts[i].record(stream)
-            solve()
-            ends[i].record(stream)
-        torch.cuda.synchronize()
-    barrier(world)
-    ms_total = max_over_ranks(world, sum(a.elapsed_time(b) for a, b in zip(starts, ends)))
+    times, clocks = timed_steps(args, world, stream, flush, body)
+    launches = (plan.launches - l0) * args.steps // (args.warmup + 1 + args.steps)
+    ms_total = reduce_over_ranks(world, sum(times))
     pts = wl.points * (wl.nsteps if wl.op != "poisson" else 1)
     plan.read_profile()
     plan.set_profiling(True)
-    solve()
+    body()
     torch.cuda.synchronize()
     prof = plan.read_profile()
     plan.set_profiling(False)
-    dom_name, (dom_ms, dom_n) = max(prof.items(), key=lambda kv: kv[1][0])
-    total = sum(v[0] for v in prof.values())
-    dom_avg_s = dom_ms / total * (ms_total / args.steps) * 1e-3 / dom_n if total else dom_ms / dom_n * 1e-3
-    achieved = 2 * slab.numel() * 16 / dom_avg_s / 1e9
-    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0) \
-        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    roofline = roofline_block(wl, prof, ms_total / args.steps, 1, world, slab_fraction=1.0 / world)
     return {
         "metric": METRIC, "value": pts * args.steps / (ms_total * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
@@ -615,22 +824,9 @@ def sharded3d_native(args, wl, world, rank, local):
         "config": {**workload_config(wl, world),
                    "parallelism": f"z-slab x{world} (NCCL all-to-all inside libfftpde, fftpde_plan_3d_sharded)",
                    "l2": "256 MiB buffer zeroed between timed steps"},
-        "e2e": None, "cpu_baseline": None, "clocks": clk.summary(),
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None, "kernel": dom_name,
-                     "per_kernel_ms_per_solve": {k: round(v[0], 3) for k, v in prof.items()},
-                     "alltoalls_per_solve": 2 * (wl.nsteps if wl.op != "poisson" else 1)},
-        "gpu_launches": plan.launches - l0,
+        "e2e": None, "cpu_baseline": None, "clocks": clocks, "parity": None,
+        "roofline": roofline, "gpu_launches": launches,
     }
-
-
-def alg_step_bytes(wl):
-    """Algorithmic bytes of one bench step: each state field read + written once per
-    solve step."""
-    esz = {"c128": 16, "c64": 8, "f64": 8, "f32": 4}[wl.dtype]
-    fields = 2 if wl.op in ("wave", "rk4") else 1
-    steps = wl.nsteps if wl.op != "poisson" else 1
-    return 2 * fields * wl.points * esz * steps
 
 
 def workload_config(wl, world):
@@ -652,6 +848,16 @@ def workload_config(wl, world):
 
 
 # ---------------------------------------------------------------------------- CPU oracle
+
+def c5_sample_workload(wl):
+    """C5's bounded oracle sample: one stepped diffusion step of an 8192^2 grid with the
+    C5 recipe (the full 32768^2 step needs ~50 GiB of host memory and about a minute)."""
+    import dataclasses
+    from paper_2412_12308_b200 import inputs as I
+    sub = dataclasses.replace(wl, nx=8192, ny=8192, nsteps=1)
+    g = I.c2_inputs(8192, m=64, sig_lo=0.002, sig_hi=0.01)
+    return sub, (g.u0,)
+
 
 def oracle_sample(wl, host, budget_s=12.0):
     """Time the oracle on a bounded sample of the workload; returns (pts/s, desc)."""
@@ -685,9 +891,12 @@ def oracle_sample(wl, host, budget_s=12.0):
         O.diffuse(host[0], wl.D, wl.dt, 1, wl.Lx, wl.Ly)
         one = time.perf_counter() - t0
         k = max(1, min(wl.nsteps, int(budget_s / max(one, 1e-6))))
-        t0 = time.perf_counter()
-        O.diffuse(host[0], wl.D, wl.dt, k, wl.Lx, wl.Ly)
-        dt = time.perf_counter() - t0
+        if k > 1:
+            t0 = time.perf_counter()
+            O.diffuse(host[0], wl.D, wl.dt, k, wl.Lx, wl.Ly)
+            dt = time.perf_counter() - t0
+        else:
+            dt = one
         return wl.nx * wl.ny * k / dt, f"{k} of {wl.nsteps} stepped diffusion steps ({wl.ny}x{wl.nx}, full grid)"
     if wl.op == "dsrc":
         t0 = time.perf_counter()
@@ -724,14 +933,11 @@ def oracle_sample(wl, host, budget_s=12.0):
 def cpu_baseline(wl, host):
     from oracle import oracle as O
     O.set_threads(os.cpu_count() or 1)
-    if host is None:   # C5: time the oracle on one 8192^2 diffusion step of the same recipe
-        import dataclasses
-        from paper_2412_12308_b200 import inputs as I
-        sub = dataclasses.replace(wl, nx=8192, ny=8192, nsteps=1)
-        g = I.c2_inputs(8192, m=64, sig_lo=0.002, sig_hi=0.01)
-        v, desc = oracle_sample(sub, (g.u0,))
+    if host is None:   # C5: the oracle on a bounded sample of the same recipe
+        sub, h = c5_sample_workload(wl)
+        v, desc = oracle_sample(sub, h)
         return {"value": v, "unit": UNIT, "cores": O.get_threads(), "kind": "oracle",
-                "sample": "1 stepped diffusion step on an 8192^2 sub-problem of the C5 recipe: " + desc}
+                "sample": "bounded sample of c5_diffusion_32768: " + desc + " (C5 recipe, same D and dt)"}
     v, desc = oracle_sample(wl, host)
     out = {"value": v, "unit": UNIT, "cores": O.get_threads(), "kind": "oracle", "sample": desc}
     if wl.name.split("_")[0] in ("c1", "c2", "c4"):      # also a 1-thread time for C1, C2, C4
@@ -746,23 +952,23 @@ def cpu_baseline(wl, host):
 
 
 def reference(args, wl, world, rank):
-    """The reference arm of this tier: the fp64 CPU oracle, as it stands."""
+    """The reference arm of this tier: the fp64 CPU oracle, as it stands, with the
+    native arm's config; each step a bounded sample (named in cpu_baseline.sample)."""
     if rank != 0:
         return None
     from oracle import oracle as O
     O.set_threads(os.cpu_count() or 1)
     if wl.name.startswith("c5"):
-        import dataclasses
-        from paper_2412_12308_b200 import inputs as I
-        wl = dataclasses.replace(wl, nx=8192, ny=8192, nsteps=1)
-        host = (I.c2_inputs(8192, m=64, sig_lo=0.002, sig_hi=0.01).u0,)
+        swl, host = c5_sample_workload(wl)
+        prefix = "bounded sample of c5_diffusion_32768: "
     else:
-        host = make_inputs(wl)
+        swl, host = wl, make_inputs(wl)
+        prefix = ""
     for _ in range(args.warmup):
-        oracle_sample(wl, host, budget_s=2.0)
+        oracle_sample(swl, host, budget_s=2.0)
     vals, descs = [], []
     for _ in range(args.steps):
-        v, d = oracle_sample(wl, host, budget_s=8.0)
+        v, d = oracle_sample(swl, host, budget_s=8.0)
         vals.append(v)
         descs.append(d)
     value = statistics.median(vals)
@@ -770,32 +976,38 @@ def reference(args, wl, world, rank):
     return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": pts_step / value * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded, BASELINE.json recipe)", "config": workload_config(wl, 1),
+        "higher_is_better": True, "scaling": "strong" if (wl.name.startswith("c5") and world > 1) else "weak",
+        "vs_baseline": None, "dtype": "f64" if wl.dtype in ("c128", "f64") else "f32",
+        "data": "synthetic (seeded, BASELINE.json recipe)", "config": workload_config(wl, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.get_threads(), "kind": "oracle",
-                         "sample": descs[0] + "; median over steps"},
+                         "sample": prefix + descs[0] + "; median over steps"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
 def main():
     args = parse_args()
-    import torch
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     from paper_2412_12308_b200 import inputs as I
     wl = I.WORKLOADS.get(args.workload) or I.EXTRA_WORKLOADS[args.workload]
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if world_env != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world_env}")
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
-        world = int(os.environ.get("WORLD_SIZE", "1"))
-        line = reference(args, wl, world, rank)
+        line = reference(args, wl, world_env, rank)
         if line is not None:
             print(json.dumps(line), flush=True)
         return
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
-    world, rank, local = dist_setup(args.gpus)
+    import torch
+    world, rank, local = dist_setup()
+    assert world == args.gpus, (world, args.gpus)
     if args.sharded and world == 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29533", rank=0, world_size=1,
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{free_port()}", rank=0, world_size=1,
                                 device_id=torch.device("cuda", 0))
     if wl.name.startswith("c5") and (world > 1 or args.sharded):
         line = sharded_native(args, wl, world, rank, local)

@@ -32,8 +32,14 @@ def test_native_line():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 1024 * 1024 * 16 and e["d2h_bytes_per_step"] > 0
     r = d["roofline"]
-    assert r["bound"] in ("hbm", "tensor", "alu") and r["unit"] == "GB/s"
-    assert 0 < r["frac"] < 1 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    assert r["bound"] in ("hbm", "alu") and r["unit"] == ("GB/s" if r["bound"] == "hbm" else "GFP64inst/s")
+    assert 0 < r["frac"] < 1.2 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    st = r["step"]                                     # the whole step against the method's own bytes
+    assert st["alg_bytes"] == 2 * 200 * 1024 * 1024 * 16 and 0 < st["alg_frac"] <= st["design_frac"]
+    for k in r["per_kernel"].values():
+        assert k["bound"] in ("hbm", "alu") and k["ms_per_launch"] > 0
+    p = d["parity"]                                     # the oracle on the same input (cpu_baseline leg)
+    assert p["rel_l2"] <= 1e-12 and p["mean_drift"] <= 1e-12
     c = d["cpu_baseline"]
     assert c["kind"] == "oracle" and c["cores"] >= 1 and c["value"] > 0 and c["sample"]
     assert d["clocks"]["sm_mhz"] > 0 and isinstance(d["clocks"]["reasons"], list)
@@ -43,5 +49,17 @@ def test_native_line():
 def test_reference_line():
     d = bench("--impl", "reference", "--workload", "c2", "--steps", "1", "--warmup", "3")
     assert d["impl"] == "reference" and d["value"] > 0
+    assert d["config"]["workload"] == "c2_diffusion_1024" and d["metric"].startswith("2D FFT-PDE")
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+def test_default_is_c5_with_parity_and_same_config_reference():
+    """The default line is C5 (the largest single-GPU config), with the closed-form
+    parity and a reference arm carrying the identical config."""
+    d = bench("--steps", "1", "--warmup", "3", "--no-e2e", "--no-cpu-baseline")
+    assert d["config"]["workload"] == "c5_diffusion_32768" and d["n_gpus"] == 1
+    assert d["parity"]["rel_l2"] <= 1e-12 and d["parity"]["mean_drift"] <= 1e-12 and d["parity"]["pass"]
+    assert d["roofline"]["kernel"] in d["roofline"]["per_kernel"]
+    ref = bench("--impl", "reference", "--steps", "1", "--warmup", "3")
+    assert ref["config"] == d["config"] and "c5_diffusion_32768" in ref["cpu_baseline"]["sample"]
