@@ -62,6 +62,61 @@ cudaError_t launch_aa(int op, const void *in, void *out, void *phys, const void 
     }
 }
 
+
+#ifndef FFTPDE_FS_BY_TMA
+#define FFTPDE_FS_BY_TMA 1
+#endif
+#ifndef FFTPDE_FS_BYT_MINB
+#define FFTPDE_FS_BYT_MINB 2
+#endif
+// the field as a 3D tensor {2 N doubles, N rows, 1}; boxes of 64 bytes x 256 rows
+static bool by_map(CUtensorMap &m, const void *p)
+{
+    using G = FsGeom;
+    auto enc = tma_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)(2 * G::N), (cuuint64_t)G::N, 1};
+    cuuint64_t strides[2] = {(cuuint64_t)G::N * 16, (cuuint64_t)G::N * G::N * 16};
+    cuuint32_t box[3] = {(cuuint32_t)(2 * ByGeom::W), (cuuint32_t)ByGeom::BOXR, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void *>(p), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static cudaError_t launch_by_tma(void *f, const void *tw32, const double *my2d, cudaStream_t st)
+{
+    CUtensorMap m;
+    if (!by_map(m, f)) return cudaErrorNotSupported;
+    auto k = by_kernel<FFTPDE_FS_BYT_MINB>;
+    static SmemOptIn<decltype(k)> opt;
+    cudaError_t e = opt(k, ByGeom::BYTES);
+    if (e != cudaSuccess) return e;
+    e = launch_fam(PDL_FOURSTEP, k, dim3((unsigned)(FsGeom::Q * ByGeom::NGROUP)), dim3(ByGeom::NT), ByGeom::BYTES, st,
+                   m, (const double2 *)tw32, my2d);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+
+#ifndef FFTPDE_FS_BX_BULK
+#define FFTPDE_FS_BX_BULK 0
+#endif
+#ifndef FFTPDE_FS_BXB_MINB
+#define FFTPDE_FS_BXB_MINB 2
+#endif
+static cudaError_t launch_bx_bulk(void *f, const void *tw32, const double *mx2d, cudaStream_t st)
+{
+    auto k = bx_kernel<FFTPDE_FS_BXB_MINB>;
+    static SmemOptIn<decltype(k)> opt;
+    cudaError_t e = opt(k, BxGeom::BYTES);
+    if (e != cudaSuccess) return e;
+    e = launch_fam(PDL_FOURSTEP, k, dim3((unsigned)BxGeom::NTILES), dim3(BxGeom::NT), BxGeom::BYTES, st,
+                   (double2 *)f, (const double2 *)tw32, mx2d);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
 #ifndef FFTPDE_FS_BY_W
 #define FFTPDE_FS_BY_W 4
 #endif
@@ -74,6 +129,9 @@ cudaError_t launch_aa(int op, const void *in, void *out, void *phys, const void 
 #ifndef FFTPDE_FS_BX_W
 #define FFTPDE_FS_BX_W 1
 #endif
+#ifndef FFTPDE_FS_BX_E
+#define FFTPDE_FS_BX_E 32
+#endif
 #ifndef FFTPDE_FS_BX_MINB
 #define FFTPDE_FS_BX_MINB 4
 #endif
@@ -84,9 +142,15 @@ cudaError_t launch_fs_b(bool cols, void *f, const void *tw32, const void *tw16, 
                         cudaStream_t st)
 {
     using G = FsGeom;
+    if (!cols && FFTPDE_FS_BX_BULK) return launch_bx_bulk(f, tw32, tab.ey2d, st);
     if (!cols)
-        return line_n<double, 1024, 32, FFTPDE_FS_BX_W, false, LN_DIFFUSE, FFTPDE_FS_BX_MINB>(
-            f, f, nullptr, (int64_t)G::N * G::Q, 1024, 1, (int64_t)G::N * G::N, 1, tw32, tab, st, PeerOut{}, PDL_FOURSTEP);
+        return line_n<double, 1024, FFTPDE_FS_BX_E, FFTPDE_FS_BX_W, false, LN_DIFFUSE, FFTPDE_FS_BX_MINB>(
+            f, f, nullptr, (int64_t)G::N * G::Q, 1024, 1, (int64_t)G::N * G::N, 1, FFTPDE_FS_BX_E == 32 ? tw32 : tw16,
+            tab, st, PeerOut{}, PDL_FOURSTEP);
+    if (FFTPDE_FS_BY_TMA) {
+        const cudaError_t e = launch_by_tma(f, tw32, tab.ey2d, st);
+        if (e != cudaErrorNotSupported) return e;
+    }
     return line_n<double, 1024, FFTPDE_FS_BY_E, FFTPDE_FS_BY_W, true, LN_DIFFUSE, FFTPDE_FS_BY_MINB>(
         f, f, nullptr, G::N, 1, G::N, (int64_t)1024 * G::N, G::Q, FFTPDE_FS_BY_E == 32 ? tw32 : tw16, tab, st,
         PeerOut{}, PDL_FOURSTEP);

@@ -25,6 +25,7 @@
 #include <cuda.h>
 #include "fft_core.cuh"
 #include "tmacols.cuh"
+#include "line.cuh"
 
 namespace fftpde {
 
@@ -188,6 +189,153 @@ aa_kernel(const __grid_constant__ CUtensorMap min, const __grid_constant__ CUten
         }
     }
     if (tid == 0) tma_wait_read0();                        // smem stays valid until the stores have read it
+}
+
+
+// ---- By: the 1024-point column segments of the AA-domain field (block l1 = rows
+// [1024 l1, 1024 l1 + 1024)), forward DFT over m1, times e^{-D ky^2 dt}/ny at
+// ky = l1 + Q l2, inverse DFT; a tile of 4 adjacent columns (64 KiB) arrives as
+// 4 TMA boxes of 256 rows x 64 bytes and leaves the same way, one tile per CTA,
+// several CTAs per SM (the line pass issued 32 strided 16-byte loads per thread).
+struct ByGeom {
+    static constexpr int L = 1024, E = 32, W = 4, BOXR = 256;
+    static constexpr int NT = W * (L / E);                         // 128 threads
+    using LS = LineSmem<double2, L, E, W, true>;
+    static constexpr size_t TILE_BYTES = (size_t)L * W * 16;       // 64 KiB dense
+    static constexpr size_t XCH_BYTES = (size_t)W * LS::S * 16;    // exchange buffers
+    static constexpr size_t BUF = TILE_BYTES > XCH_BYTES ? TILE_BYTES : XCH_BYTES;
+    static constexpr size_t BYTES = BUF + 128 + 16;
+    static constexpr int NGROUP = FsGeom::N / W;                   // 8192 column groups per block
+};
+
+template <int MINB>
+__global__ void __launch_bounds__(ByGeom::NT, MINB)
+by_kernel(const __grid_constant__ CUtensorMap map, const double2 *__restrict__ tw32, const double *__restrict__ my2d)
+{
+    using G = ByGeom;
+    constexpr int L = G::L, E = G::E, W = G::W, TPT = L / E;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const uint32_t pad = (128u - (tma_smem(smem_raw) & 127u)) & 127u;
+    double2 *S = reinterpret_cast<double2 *>(smem_raw + pad);
+    const uint32_t mbar = tma_smem(reinterpret_cast<unsigned char *>(S) + G::BUF);
+    const int tid = threadIdx.x;
+    const int c = tid % W, t = tid / W;
+    const int l1 = (int)(blockIdx.x / G::NGROUP), grp = (int)(blockIdx.x % G::NGROUP);
+    const int x0 = 2 * W * grp;                                    // tensor coordinate (doubles)
+    if (tid == 0) {
+        tma_mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_wait();
+    if (tid == 0) {
+        tma_mbar_expect(mbar, (uint32_t)G::TILE_BYTES);
+#pragma unroll
+        for (int k = 0; k < L / G::BOXR; ++k)
+            tma_load3(tma_smem(S) + k * G::BOXR * W * 16, &map, x0, 1024 * l1 + k * G::BOXR, 0, mbar);
+    }
+    pdl_trigger();
+    const TwL1<L, double2, E> twp{tw32, t};
+    const SmemView<double2, Shape<L, E>::LOGE, 1> sm{S + c * G::LS::S};
+    const SyncCTA sync{};
+    double2 v[E];
+    tma_mbar_wait(mbar, 0);
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = S[(t + TPT * e) * W + c];
+    __syncthreads();                                               // the tile buffer becomes the exchange buffers
+    fft_tw<L, false, E>(v, sm, t, twp, sync);                      // v[e] = X[l2 = t + 32 e]
+    {
+        const double *m = my2d + (size_t)l1 * L + t;
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = cscale(v[e], __ldg(m + TPT * e));
+    }
+    fft_tw<L, true, E>(v, sm, t, twp, sync);
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) S[(t + TPT * e) * W + c] = v[e];
+    tma_fence_smem();
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll
+        for (int k = 0; k < L / G::BOXR; ++k)
+            tma_store3(&map, x0, 1024 * l1 + k * G::BOXR, 0, tma_smem(S) + k * G::BOXR * W * 16);
+        tma_commit();
+        tma_wait_read0();
+    }
+}
+
+
+// ---- Bx: 1024-point row segments of the AA-domain field (32 per grid row, line
+// class k1 = segment % 32), forward DFT over n1, times e^{-D kx^2 dt}/nx at
+// kx = k1 + Q k2, inverse DFT; four consecutive segments (64 KiB contiguous) per
+// CTA arrive as one bulk copy and leave as one; one warp per segment (radix 32 x 32,
+// warp-synchronous exchange).
+struct BxGeom {
+    static constexpr int L = 1024, E = 32, W = 4;
+    static constexpr int NT = W * (L / E);                         // 128 threads
+    static constexpr int RAW = Shape<L, E>::PADDED;                // 1056
+    static constexpr size_t TILE_BYTES = (size_t)L * W * 16;       // 64 KiB dense
+    static constexpr size_t XCH_BYTES = (size_t)W * RAW * 16;
+    static constexpr size_t BUF = TILE_BYTES > XCH_BYTES ? TILE_BYTES : XCH_BYTES;
+    static constexpr size_t BYTES = BUF + 128 + 16;
+    static constexpr int64_t NTILES = (int64_t)FsGeom::N * FsGeom::Q / W;   // 262144
+};
+__device__ __forceinline__ void bulk_s2g(void *dst, uint32_t src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+                 : "memory");
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(BxGeom::NT, MINB)
+bx_kernel(double2 *f, const double2 *__restrict__ tw32, const double *__restrict__ mx2d)
+{
+    using G = BxGeom;
+    constexpr int L = G::L, E = G::E, W = G::W, TPT = L / E;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const uint32_t pad = (128u - (tma_smem(smem_raw) & 127u)) & 127u;
+    double2 *S = reinterpret_cast<double2 *>(smem_raw + pad);
+    const uint32_t mbar = tma_smem(reinterpret_cast<unsigned char *>(S) + G::BUF);
+    const int tid = threadIdx.x;
+    const int c = tid / TPT, t = tid % TPT;
+    double2 *g = f + (int64_t)blockIdx.x * (W * L);
+    const int k1 = (int)((int64_t)blockIdx.x * W + c) % FsGeom::Q;  // line class
+    if (tid == 0) {
+        tma_mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_wait();
+    if (tid == 0) {
+        tma_mbar_expect(mbar, (uint32_t)G::TILE_BYTES);
+        bulk_g2s(tma_smem(S), g, (uint32_t)G::TILE_BYTES, mbar);
+    }
+    pdl_trigger();
+    const TwL1<L, double2, E> twp{tw32, t};
+    const SmemView<double2, Shape<L, E>::LOGE, 1> sm{S + c * G::RAW};
+    const SyncWarp sync{};
+    double2 v[E];
+    tma_mbar_wait(mbar, 0);
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = S[c * L + t + TPT * e];
+    __syncthreads();                                               // the tile buffer becomes the exchange buffers
+    fft_tw<L, false, E>(v, sm, t, twp, sync);                      // v[e] = X[k2 = t + 32 e]
+    {
+        const double *m = mx2d + (size_t)k1 * L + t;
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = cscale(v[e], __ldg(m + TPT * e));
+    }
+    fft_tw<L, true, E>(v, sm, t, twp, sync);
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) S[c * L + t + TPT * e] = v[e];
+    tma_fence_smem();
+    __syncthreads();
+    if (tid == 0) {
+        bulk_s2g(g, tma_smem(S), (uint32_t)G::TILE_BYTES);
+        tma_commit();
+        tma_wait_read0();
+    }
 }
 
 } // namespace fftpde
