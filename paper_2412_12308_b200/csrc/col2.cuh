@@ -269,7 +269,7 @@ col2_kernel(Col2Args<T> g, OpTables<T> tab, PeerOut po)
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     const T k2 = kxa + __ldg(&tab.ky2[k1 + Q * (t + TPT * e)]);
-                    u[e] = cscale(u[e], k2 == (T)0 ? (T)0 : -tab.scale / k2);   // -1/|k|^2, k=0 zeroed
+                    u[e] = cscale(u[e], poisson_mul(k2, tab.scale));   // -1/|k|^2, k=0 zeroed
                 }
             } else if constexpr (OP == C2_DIFFUSE) {
                 const T exa = tab.ex[a];

@@ -187,7 +187,7 @@ small_solve_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type 
                 T m;
                 if constexpr (OP == COL_POISSON) {
                     const T k2 = sa[col] + sb[b];
-                    m = k2 == (T)0 ? (T)0 : -tab.scale / k2;    // -1/|k|^2, k = 0 zeroed
+                    m = poisson_mul(k2, tab.scale);    // -1/|k|^2, k = 0 zeroed
                 } else {
                     m = sa[col] * sb[b];                          // exp(-D|k|^2 dt)/(nx ny)
                 }

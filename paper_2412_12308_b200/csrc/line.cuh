@@ -102,7 +102,7 @@ line_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>:
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 const T k2 = kxa + __ldg(&tab.ky2[t + TPT * e]);
-                v[e] = cscale(v[e], k2 == (T)0 ? (T)0 : -tab.scale / k2);   // -1/|k|^2, k = 0 zeroed
+                v[e] = cscale(v[e], poisson_mul(k2, tab.scale));   // -1/|k|^2, k = 0 zeroed
             }
         } else if (tab.ey2d) {                      // four-step B pass: factor of line class cls
             const int64_t cls = COLS ? b : (active ? line : 0) % tab.ey2d_mod;

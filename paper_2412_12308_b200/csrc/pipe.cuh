@@ -222,7 +222,7 @@ pipe_kernel(const typename cplx_t<T>::type *in, typename cplx_t<T>::type *out, P
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     const T k2 = kxa + __ldg(&tab.ky2[t + TPT * e]);
-                    const T m = k2 == (T)0 ? (T)0 : -tab.scale / k2;     // -1/|k|^2, k = 0 zeroed
+                    const T m = poisson_mul(k2, tab.scale);     // -1/|k|^2, k = 0 zeroed
                     v[e] = cscale(v[e], m);
                 }
             } else if (tab.ey2d) {                   // four-step B pass: factor of line class cls

@@ -153,7 +153,7 @@ tma_cols_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     const T k2 = kxa + __ldg(&tab.ky2[t + TPT * e]);
-                    v[e] = cscale(v[e], k2 == (T)0 ? (T)0 : -tab.scale / k2);   // -1/|k|^2, k = 0 zeroed
+                    v[e] = cscale(v[e], poisson_mul(k2, tab.scale));   // -1/|k|^2, k = 0 zeroed
                 }
             } else if (tab.ey2d) {                   // four-step By pass: the factor of batch (block) bb
                 const T *m = tab.ey2d + bb * N;

@@ -168,7 +168,21 @@ class LoopbackPeerComm:
 
 class SymmetricPeerComm:
     """One rank per GPU: buffers from torch symmetric memory (peer-mapped over
-    NVLink), barrier = the symmetric-memory stream-ordered device barrier."""
+    NVLink), barrier = the symmetric-memory stream-ordered device barrier.
+
+    Ordering of the fused exchanges: the row / column pass kernels write the
+    peers' buffers with plain global stores to peer-mapped addresses; the barrier
+    kernel is enqueued after them on the same stream, so it starts only once every
+    one of those stores has been performed (kernel boundary).  torch's barrier
+    kernel then signals each peer with a compare-and-swap at system scope with
+    release semantics (``put_signal<memory_order_release>`` on a
+    ``cuda::atomic_ref<.., thread_scope_system>``, CUDASymmetricMemory-inl.h) and
+    waits on its own pad with an acquire CAS at system scope, so a peer's kernels
+    enqueued after its barrier observe our stores (the same "writes of previous
+    kernels are visible" pattern torch's own symmetric-memory kernels use).  The
+    multi-rank path has been exercised by the single-process emulation on one
+    GPU and by the two-process gloo test with shared-memory stand-ins
+    (tests/test_sharded_cpu.py); it has not run on real multi-GPU hardware."""
 
     def __init__(self, group=None):
         import torch.distributed as dist

@@ -153,7 +153,7 @@ def test_long_axes_solvers(dtype, shape):
     v0 = host(vv)
     p.wave_step(uu, vv, 0.3, 1e-4, 2)
     uo, vo = O.wave(x.astype(np.complex128), v0, 0.3, 1e-4, 2, 1.0, 2.0)
-    assert rel(host(uu), uo) <= TOL[dtype] and rel(host(vv), vo) <= 10 * TOL[dtype]
+    assert rel(host(uu), uo) <= TOL[dtype] and rel(host(vv), vo) <= TOL[dtype]
 
 
 @pytest.mark.parametrize("dtype,B,ny,nx", [(C128, 5, 32, 32768), (C64, 3, 16, 32768), (C128, 9, 32, 16384)])
@@ -229,6 +229,18 @@ def test_c3_wave_prefix_vs_stepped_oracle():
     assert rel(host(v), vo) <= 1e-12
 
 
+def test_c3_wave_prefix_full_size_vs_stepped_oracle():
+    # the C3 workload itself (4096^2, dt = 1e-4) for its first 50 steps against the
+    # stepped oracle (SURVEY.md 8(c) coverage plan); measured 5.7e-15 (u), 9.2e-14 (u_t)
+    w = I.c3_inputs(4096)
+    p = F.Plan(4096, 4096, dtype=C128)
+    u, v = dev(w.u), dev(w.ut)
+    p.wave_step(u, v, 1.0, 1e-4, 50)
+    uo, vo = O.wave(w.u, w.ut, 1.0, 1e-4, 50)
+    assert rel(host(u), uo) <= 1e-12
+    assert rel(host(v), vo) <= 1e-12
+
+
 def test_c3_wave_full_vs_collapsed():
     w = I.c3_inputs(4096)
     p = F.Plan(4096, 4096, dtype=C128)
@@ -251,9 +263,9 @@ def test_wave_shapes_reversal(dtype):
     u, v = dev(u0, dtype), dev(v0, dtype)
     p.wave_step(u, v, 0.7, 3e-3, 9)
     uo, vo = O.wave(u0.astype(np.complex128), v0.astype(np.complex128), 0.7, 3e-3, 9, 1.3, 0.9)
-    assert rel(host(u), uo) <= TOL[dtype] and rel(host(v), vo) <= 4 * TOL[dtype]
-    p.wave_step(u, v, 0.7, -3e-3, 9)                              # time reversal
-    assert rel(host(u), u0) <= 10 * TOL[dtype]
+    assert rel(host(u), uo) <= TOL[dtype] and rel(host(v), vo) <= TOL[dtype]
+    p.wave_step(u, v, 0.7, -3e-3, 9)                              # time reversal: two solves, errors add
+    assert rel(host(u), u0) <= 2 * TOL[dtype]
 
 
 @pytest.mark.parametrize("nx,ny,batch", [(8, 2048, 2), (16, 4096, 1), (2, 4096, 3)])
@@ -319,14 +331,14 @@ def test_c5_diffusion_full_size_sampled_closed_form():
 
 # ---------------------------------------------------------------- C4 batched Poisson
 
-def test_c4_batched_poisson_full_batch_sampled():
+def test_c4_batched_poisson_every_grid():
+    # all 256 grids of the batch against the oracle on the upcast complex64 input;
+    # the bar is the maximum over the grids (measured 2.1e-7)
     s = I.c4_inputs(512, 256)
     p = F.Plan(512, 512, batch=256, dtype=C64)
-    u = p.poisson(dev(s, C64))
-    torch.cuda.synchronize()
-    for g in (0, 1, 77, 128, 200, 255):
-        ref = O.poisson(s[g].astype(np.complex128))
-        assert rel(u[g].cpu().numpy(), ref) <= 1e-5, g
+    u = p.poisson(dev(s, C64)).cpu().numpy()
+    errs = [rel(u[g], O.poisson(s[g].astype(np.complex64).astype(np.complex128))) for g in range(256)]
+    assert max(errs) <= 1e-5, (int(np.argmax(errs)), max(errs))
 
 
 # ---------------------------------------------------------------- errors
@@ -393,3 +405,24 @@ def test_fallback_passes_without_tma(tmp_path):
     assert r.returncode == 0, r.stderr[-2000:]
     worst = float(r.stdout.strip().split()[-1])
     assert worst <= 1e-12
+
+
+# ---------------------------------------------------------------- C5 at full size against the oracle
+
+def test_c5_full_size_separable_rank2_vs_oracle_every_point():
+    # C5's grid and step count through the four-step passes (AA / MID, Bx, By) on a
+    # rank-2 input u0 = g1 f1^T + g2 f2^T of seeded complex white noise (every
+    # wavenumber populated): the separable diffusion (R26) maps it to
+    # (D_y g1)(D_x f1)^T + (D_y g2)(D_x f2)^T, the oracle's own stepped 1D solves
+    # (ny = 1 grids), compared at all 2^30 points
+    n, D, dt, steps = 32768, 1e-4, 0.01, 20
+    f1, g1, f2, g2 = (I.white_noise((n,), 700 + i) for i in range(4))
+    Df1, Dg1, Df2, Dg2 = (O.diffuse(v.reshape(1, n), D, dt, steps).ravel() for v in (f1, g1, f2, g2))
+    t = lambda v: torch.from_numpy(v).cuda()
+    u0 = torch.outer(t(g1), t(f1)) + torch.outer(t(g2), t(f2))
+    p = F.Plan(n, n, dtype=C128)
+    u = p.diffuse(u0, D, dt, steps)
+    del u0
+    ref = torch.outer(t(Dg1), t(Df1)) + torch.outer(t(Dg2), t(Df2))
+    err = (torch.linalg.vector_norm(u - ref) / torch.linalg.vector_norm(ref)).item()
+    assert err <= 1e-12, err
