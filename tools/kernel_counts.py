@@ -48,7 +48,8 @@ def main():
     acc = collections.defaultdict(lambda: collections.Counter())
     for lid, m in per.items():
         k = kname[lid]
-        cls = "aa_pass" if "aa_kernel" in k else classify(k)
+        cls = ("aa_pass" if "aa_kernel" in k else "col_pass" if "by_kernel" in k else "row_pass" if "bx_kernel" in k
+               else classify(k))
         a = acc[cls]
         a["launches"] += 1
         a["dram_bytes"] += m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
@@ -58,7 +59,7 @@ def main():
     out = {cls: {"launches": a["launches"], "dram_bytes": a["dram_bytes"] / a["launches"],
                  "dp_inst": a["dp_inst"] / a["launches"], "sp_inst": a["sp_inst"] / a["launches"],
                  "ncu_ms_per_launch": a["ncu_ms"] / a["launches"]} for cls, a in acc.items()}
-    out["_source"] = {"csv": os.path.relpath(path, ROOT), "metrics": METRICS,
+    out["_source"] = {"csv": "profiles/r02/ncu/" + os.path.basename(path) + ".gz", "metrics": METRICS,
                       "note": "ncu replays with caches flushed: cold-cache DRAM bytes; per-launch means per class"}
     dst = os.path.join(ROOT, "profiles", f"counts_{name}.json")
     json.dump(out, open(dst, "w"), indent=1)
