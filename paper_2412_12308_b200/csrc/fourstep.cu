@@ -5,6 +5,12 @@
 
 namespace fftpde {
 
+#ifndef FFTPDE_FS_PROMO_AA
+#define FFTPDE_FS_PROMO_AA CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+#endif
+#ifndef FFTPDE_FS_PROMO_BY
+#define FFTPDE_FS_PROMO_BY CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+#endif
 bool fourstep_supported(int64_t nx, int64_t ny, int64_t batch, int elem_bytes)
 {
     return elem_bytes == 16 && nx == FsGeom::N && ny == FsGeom::N && batch == 1;
@@ -22,7 +28,7 @@ static bool fs_map(CUtensorMap &m, const void *p)
     cuuint32_t box[4] = {(cuuint32_t)(2 * G::W), (cuuint32_t)G::Q, 1, (cuuint32_t)G::Q};
     cuuint32_t es[4] = {1, 1, 1, 1};
     return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void *>(p), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, FFTPDE_FS_PROMO_AA,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -80,7 +86,7 @@ static bool by_map(CUtensorMap &m, const void *p)
     cuuint32_t box[3] = {(cuuint32_t)(2 * ByGeom::W), (cuuint32_t)ByGeom::BOXR, 1};
     cuuint32_t es[3] = {1, 1, 1};
     return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void *>(p), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, FFTPDE_FS_PROMO_BY,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
