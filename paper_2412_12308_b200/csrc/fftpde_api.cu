@@ -46,7 +46,7 @@ struct fftpde_plan_s {
     // four-step diffusion passes (fourstep.cuh; 32768^2 complex128 single grids, R27)
     bool fs = false;
     std::vector<double> fs_tw, fs_tw32, fs_tw16;   // w_N^{ab} (a < 1024, b < 32); radix-32 / -16 stage tables of 1024
-    size_t o_fs_tw = 0, o_fs_tw32 = 0, o_fs_tw16 = 0, o_fs_mx = 0, o_fs_my = 0;
+    size_t o_fs_tw = 0, o_fs_tw32 = 0, o_fs_tw16 = 0, o_fs_mx = 0, o_fs_my = 0, o_fs_sync = 0;
     size_t need = 0;
     int64_t qx = 0, qy = 0;   // quadrant extents nx/2+1, ny/2+1
     // host tables (fp64)
@@ -518,8 +518,12 @@ template <typename T> struct Passes {
             void *Wf = scratch(0);
             e = fs_aa(0, u0, Wf, nullptr);
             for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) {
-                e = fs_bx(Wf);
-                if (e == cudaSuccess) e = fs_by(Wf);
+                if (fs_bb_enabled()) {
+                    e = fs_bb(Wf);
+                } else {
+                    e = fs_bx(Wf);
+                    if (e == cudaSuccess) e = fs_by(Wf);
+                }
                 if (e == cudaSuccess) e = k + 1 < nsteps ? fs_aa(2, Wf, Wf, u) : fs_aa(1, Wf, u, nullptr);
             }
             return e;
@@ -534,6 +538,14 @@ template <typename T> struct Passes {
     cudaError_t fs_aa(int op, const void *in, void *out, void *phys)
     {
         return launch(p, FFTPDE_KERNEL_AA, [&] { return launch_aa(op, in, out, phys, p->ws + p->o_fs_tw, p->stream); });
+    }
+    // Bx + By fused over L2-resident 1024 x 1024 blocks (bb_kernel)
+    cudaError_t fs_bb(void *Wf)
+    {
+        return launch(p, FFTPDE_KERNEL_COL, [&] {
+            return launch_fs_bb(Wf, p->ws + p->o_fs_tw32, (const double *)(p->ws + p->o_fs_mx),
+                                (const double *)(p->ws + p->o_fs_my), p->ws + p->o_fs_sync, p->stream);
+        });
     }
     // Bx: the 1024-point row segments of fixed k1 (32 per row): line class = segment % 32
     cudaError_t fs_bx(void *Wf)
@@ -1319,6 +1331,7 @@ fftpde_status fftpde_plan_2d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
         p->o_fs_tw16 = take(p->fs_tw16.size() / 2 * ec);
         p->o_fs_mx = take((size_t)nx * er);
         p->o_fs_my = take((size_t)ny * er);
+        p->o_fs_sync = take(1024);                     // team barrier counters of the fused B pass
     }
     p->o_scr = take(2 * (size_t)(batch * nx * ny) * ec);    // last: sharded plans replace it by slabs
     p->need = off;

@@ -123,6 +123,60 @@ static cudaError_t launch_bx_bulk(void *f, const void *tw32, const double *mx2d,
     return cudaGetLastError();
 }
 
+
+#ifndef FFTPDE_FS_BB
+#define FFTPDE_FS_BB 0
+#endif
+#ifndef FFTPDE_FS_TEAMS
+#define FFTPDE_FS_TEAMS 6
+#endif
+// Bx + By fused over L2-resident blocks (bb_kernel): a cooperative launch of the
+// resident grid; `sync` holds 2 counters per team, zeroed before every launch.
+// Opt-in (FFTPDE_FS_BB=1): measured slower than the two passes (C5 B passes 18.8-20.5
+// vs 16.5 ms per step for 2-12 teams, r02): halving their HBM traffic does not pay
+// because the B passes are bound by their FP64 work and latency (ncu: HBM 66%, FP64
+// pipe 50%), and the per-block team barriers add tails.
+cudaError_t launch_fs_bb(void *f, const void *tw32, const double *mx2d, const double *my2d, void *sync,
+                         cudaStream_t st)
+{
+    CUtensorMap m;
+    if (!by_map(m, f)) return cudaErrorNotSupported;
+    auto k = bb_kernel<2>;
+    static SmemOptIn<decltype(k)> opt;
+    cudaError_t e = opt(k, BbGeom::BYTES);
+    if (e != cudaSuccess) return e;
+    static int occ = 0;
+    if (!occ) {
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, BbGeom::NT, BbGeom::BYTES);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) return cudaErrorNotSupported;
+    }
+    int teams = FFTPDE_FS_TEAMS;
+    if (const char *s = std::getenv("FFTPDE_FS_TEAMS")) teams = std::max(1, atoi(s));
+    e = cudaMemsetAsync(sync, 0, 2 * sizeof(unsigned) * (size_t)teams, st);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    int grid = occ * sm_count();
+    if (const char *s = std::getenv("FFTPDE_FS_BB_GRID")) grid = std::max(teams, std::min(grid, atoi(s)));
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(BbGeom::NT);
+    cfg.dynamicSmemBytes = BbGeom::BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k, m, (double2 *)f, (const double2 *)tw32, mx2d, my2d, (unsigned *)sync, teams);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+bool fs_bb_enabled()
+{
+    static const bool on = [] { const char *e = std::getenv("FFTPDE_FS_BB"); return e ? e[0] != '0' : FFTPDE_FS_BB != 0; }();
+    return on;
+}
+
 #ifndef FFTPDE_FS_BY_W
 #define FFTPDE_FS_BY_W 4
 #endif

@@ -338,4 +338,135 @@ bx_kernel(double2 *f, const double2 *__restrict__ tw32, const double *__restrict
     }
 }
 
+
+// ---- BB: the Bx and By passes fused over L2-resident blocks.  A block (l1, k1) =
+// rows [1024 l1, +1024) x columns [1024 k1, +1024) of the AA domain (16 MiB) holds
+// 1024 whole Bx lines (row segment k1 of each of its rows) and 1024 whole By lines
+// (column segments of block l1): it is closed under both passes.  The CTAs of the
+// persistent, cooperatively launched grid form `teams`; a team takes blocks
+// b = team, team + teams, ...: its Bx lines (one warp per line), a team barrier,
+// its By tiles (4 columns x 1024 rows by TMA), a team barrier.  With teams x 16 MiB
+// inside the 126 MB L2, the By pass reads what Bx wrote from L2 and HBM sees one
+// read and one write of the field for both passes (32 B/pt instead of 64).
+struct BbGeom {
+    static constexpr int L = 1024, E = 32, NT = 128;
+    static constexpr int NB = 1024;                                  // blocks (32 x 32)
+    static constexpr size_t BYTES = ByGeom::BUF + 128 + 16;
+};
+
+// team barrier over global memory: release my CTA's writes, count in, wait for the
+// generation to move (acquire), then order later async-proxy (TMA) reads after it
+__device__ __forceinline__ void team_sync(unsigned *cnt, unsigned *gen, unsigned size, unsigned &mygen)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned g = mygen;
+        if (atomicAdd(cnt, 1u) == size - 1) {
+            atomicExch(cnt, 0u);
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            unsigned v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gen) : "memory");
+                if (v == g) __nanosleep(64);
+            } while (v == g);
+        }
+        mygen = g + 1;
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncthreads();
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(BbGeom::NT, MINB)
+bb_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__restrict__ tw32,
+          const double *__restrict__ mx2d, const double *__restrict__ my2d, unsigned *sync, int teams)
+{
+    using G = ByGeom;
+    constexpr int L = G::L, E = G::E, W = G::W, TPT = L / E;
+    constexpr int64_t N = FsGeom::N;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const uint32_t pad = (128u - (tma_smem(smem_raw) & 127u)) & 127u;
+    double2 *S = reinterpret_cast<double2 *>(smem_raw + pad);
+    const uint32_t mbar = tma_smem(reinterpret_cast<unsigned char *>(S) + G::BUF);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int team = (int)blockIdx.x % teams, member = (int)blockIdx.x / teams;
+    const unsigned tsize = (gridDim.x - (unsigned)team + (unsigned)teams - 1) / (unsigned)teams;
+    unsigned *cnt = sync + 2 * team, *gen = cnt + 1;
+    unsigned mygen = 0;
+    if (tid == 0) {
+        tma_mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const TwL1<L, double2, E> twx{tw32, lane};
+    const SmemView<double2, Shape<L, E>::LOGE, 1> smx{S + warp * Shape<L, E>::PADDED};
+    const SyncWarp wsync{};
+    const int c = tid % W, t = tid / W;                              // By thread layout
+    const TwL1<L, double2, E> twy{tw32, t};
+    const SmemView<double2, Shape<L, E>::LOGE, 1> smy{S + c * G::LS::S};
+    const SyncCTA csync{};
+    uint32_t tphase = 0;
+    for (int b = team; b < BbGeom::NB; b += teams) {
+        const int l1 = b / FsGeom::Q, k1 = b % FsGeom::Q;
+        // ---- Bx: row segment k1 of the block's 1024 rows, one warp per line
+        {
+            const double *m = mx2d + (size_t)k1 * L + lane;
+            for (int r = member * 4 + warp; r < L; r += (int)tsize * 4) {
+                double2 *g = f + (int64_t)(1024 * l1 + r) * N + 1024 * k1 + lane;
+                double2 v[E];
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = g[TPT * e];
+                fft_tw<L, false, E>(v, smx, lane, twx, wsync);
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = cscale(v[e], __ldg(m + TPT * e));
+                fft_tw<L, true, E>(v, smx, lane, twx, wsync);
+#pragma unroll
+                for (int e = 0; e < E; ++e) g[TPT * e] = v[e];
+            }
+        }
+        team_sync(cnt, gen, tsize, mygen);
+        // ---- By: 4-column tiles of the block's columns, rows [1024 l1, +1024)
+        {
+            const double *m = my2d + (size_t)l1 * L + t;
+            for (int gi = member; gi < L / W; gi += (int)tsize) {
+                const int x0 = 2 * (1024 * k1 + W * gi);
+                if (tid == 0) {
+                    tma_mbar_expect(mbar, (uint32_t)G::TILE_BYTES);
+#pragma unroll
+                    for (int k = 0; k < L / G::BOXR; ++k)
+                        tma_load3(tma_smem(S) + k * G::BOXR * W * 16, &map, x0, 1024 * l1 + k * G::BOXR, 0, mbar);
+                }
+                tma_mbar_wait(mbar, tphase);
+                tphase ^= 1u;
+                double2 v[E];
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = S[(t + TPT * e) * W + c];
+                __syncthreads();
+                fft_tw<L, false, E>(v, smy, t, twy, csync);
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = cscale(v[e], __ldg(m + TPT * e));
+                fft_tw<L, true, E>(v, smy, t, twy, csync);
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < E; ++e) S[(t + TPT * e) * W + c] = v[e];
+                tma_fence_smem();
+                __syncthreads();
+                if (tid == 0) {
+#pragma unroll
+                    for (int k = 0; k < L / G::BOXR; ++k)
+                        tma_store3(&map, x0, 1024 * l1 + k * G::BOXR, 0, tma_smem(S) + k * G::BOXR * W * 16);
+                    tma_commit();
+                    tma_wait_read0();                                // the tile buffer is free again
+                }
+                __syncthreads();
+            }
+        }
+        if (tid == 0) tma_wait0();                                   // this block's By stores are done
+        team_sync(cnt, gen, tsize, mygen);
+    }
+}
+
 } // namespace fftpde
