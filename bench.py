@@ -52,6 +52,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# NCCL's version banner goes to stdout on rank 0; the contract is one JSON line
+os.environ.setdefault("NCCL_DEBUG", "WARN")
 
 METRIC = "2D FFT-PDE solve grid-points/sec and achieved HBM GB/s vs peak (1/2/4/8 GPU)"
 UNIT = "grid-points/s"
