@@ -105,6 +105,9 @@ static cudaError_t launch_by_tma(void *f, const void *tw32, const double *my2d, 
 }
 
 
+#ifndef FFTPDE_FS_BX_PIPE
+#define FFTPDE_FS_BX_PIPE 0   // the persistent pipe pass for Bx: measured 9.7 vs 8.0 ms per launch, off
+#endif
 #ifndef FFTPDE_FS_BX_BULK
 #define FFTPDE_FS_BX_BULK 0
 #endif
@@ -203,6 +206,11 @@ cudaError_t launch_fs_b(bool cols, void *f, const void *tw32, const void *tw16, 
 {
     using G = FsGeom;
     if (!cols && FFTPDE_FS_BX_BULK) return launch_bx_bulk(f, tw32, tab.ey2d, st);
+    if (!cols && FFTPDE_FS_BX_PIPE) {      // persistent double-buffered pipe pass (radix 16, 4 rows per tile)
+        OpTables<double> t = tab;
+        PipeArgs a{(int64_t)G::N * G::Q, 1024, 1, (int64_t)G::N * G::N, 1, 0, PIPE_DIFFUSE, nullptr};
+        return pipe_n<double, 1024, false, PIPE_DIFFUSE>(f, f, a, tw16, t, st);
+    }
     if (!cols)
         return line_n<double, 1024, FFTPDE_FS_BX_E, FFTPDE_FS_BX_W, false, LN_DIFFUSE, FFTPDE_FS_BX_MINB>(
             f, f, nullptr, (int64_t)G::N * G::Q, 1024, 1, (int64_t)G::N * G::N, 1, FFTPDE_FS_BX_E == 32 ? tw32 : tw16,
