@@ -760,6 +760,38 @@ def sharded_native(args, wl, world, rank, local):
     torch.cuda.synchronize()
     prof = ops.plan.read_profile()
     ops.plan.set_profiling(False)
+    # e2e: every rank's slab from pinned host memory, the solve, the slab back (max over ranks)
+    e2e = None
+    if not args.no_e2e:
+        host_in = torch.empty(slab.shape, dtype=slab.dtype, pin_memory=True)
+        host_in.copy_(slab)
+        host_out = torch.empty_like(host_in, pin_memory=True)
+        dev_in = torch.empty_like(slab)
+
+        def e2e_step():
+            dev_in.copy_(host_in, non_blocking=True)
+            solver.diffuse([dev_in], wl.D, wl.dt, wl.nsteps, outs=out)
+            host_out.copy_(out[0], non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        e2e_step()
+        barrier(world)
+        tot = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            barrier(world)
+            t0 = time.perf_counter()
+            e2e_step()
+            barrier(world)
+            tot += time.perf_counter() - t0
+        tot = reduce_over_ranks(world, tot)
+        nb = host_in.numel() * host_in.element_size()
+        e2e = {"value": pts * args.steps / tot, "unit": UNIT, "h2d_bytes_per_step": nb * world,
+               "d2h_bytes_per_step": nb * world,
+               "timer": "host perf_counter around H2D slab copy + sharded solve + D2H slab copy, barrier-bracketed, "
+                        "max over ranks; bytes summed over ranks"}
+        del host_in, host_out, dev_in
     # per rank and step: HBM = passes x (read + write) of the slab, NVLink = the
     # bytes leaving the rank in the two exchanges (per direction)
     slab_bytes = (hi - lo) * wl.nx * 16
@@ -793,7 +825,7 @@ def sharded_native(args, wl, world, rank, local):
                        "nccl": "(NCCL all-to-all, Python-driven)",
                        "lib": "(NCCL all-to-all inside libfftpde, fftpde_plan_2d_sharded)"}[exchange],
                    "l2": "field (16 GiB) larger than L2; 256 MiB buffer zeroed between timed steps"},
-        "e2e": None, "cpu_baseline": None, "clocks": clocks, "parity": parity,
+        "e2e": e2e, "cpu_baseline": None, "clocks": clocks, "parity": parity,
         "roofline": roofline, "gpu_launches": launches,
     }
 
