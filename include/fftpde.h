@@ -198,6 +198,10 @@ fftpde_status fftpde_inverse(fftpde_plan plan, const void *in, void *out);
  *   multiplier is separable, exp(-D kx^2 dt) exp(-D ky^2 dt), so a step is
  *   computed as the 1D diffusion of every row followed by that of every column
  *   (the same operator, R26; one read and one write of u per axis).
+ *   Single-grid complex128 32768 x 32768 plans split both axes four-step
+ *   (N = 1024 x 32, R27): per step one pass of the high-index DFTs
+ *   (which also writes u), then the 1024-point row and column diffusions; the
+ *   intermediate lives in the workspace scratch.
  *   D >= 0, dt >= 0, nsteps >= 0 (0 copies u0 to u).  k = 0 is kept.
  * fftpde_wave_step: nsteps exact steps of u_tt = c^2 nabla^2 u (s = 0,
  *   eq:wave_equation PAPER.md:417-424) on the state (u, ut) in place: with

@@ -409,13 +409,14 @@ def test_fallback_passes_without_tma(tmp_path):
 
 # ---------------------------------------------------------------- C5 at full size against the oracle
 
-def test_c5_full_size_separable_rank2_vs_oracle_every_point():
-    # C5's grid and step count through the four-step passes (AA / MID, Bx, By) on a
+@pytest.mark.parametrize("steps", [1, 20])
+def test_c5_full_size_separable_rank2_vs_oracle_every_point(steps):
+    # C5's grid (and step count; 1 step: AA, Bx, By, AA^-1 only) through the four-step passes (AA / MID, Bx, By) on a
     # rank-2 input u0 = g1 f1^T + g2 f2^T of seeded complex white noise (every
     # wavenumber populated): the separable diffusion (R26) maps it to
     # (D_y g1)(D_x f1)^T + (D_y g2)(D_x f2)^T, the oracle's own stepped 1D solves
     # (ny = 1 grids), compared at all 2^30 points
-    n, D, dt, steps = 32768, 1e-4, 0.01, 20
+    n, D, dt = 32768, 1e-4, 0.01
     f1, g1, f2, g2 = (I.white_noise((n,), 700 + i) for i in range(4))
     Df1, Dg1, Df2, Dg2 = (O.diffuse(v.reshape(1, n), D, dt, steps).ravel() for v in (f1, g1, f2, g2))
     t = lambda v: torch.from_numpy(v).cuda()
