@@ -11,9 +11,11 @@ namespace fftpde {
 #ifndef FFTPDE_FS_PROMO_BY
 #define FFTPDE_FS_PROMO_BY CU_TENSOR_MAP_L2_PROMOTION_L2_128B
 #endif
+// The four-step passes move their tiles with tensor maps: without the driver's
+// encoder (or with FFTPDE_TMA=0) the plan keeps the round-1 cluster passes.
 bool fourstep_supported(int64_t nx, int64_t ny, int64_t batch, int elem_bytes)
 {
-    return elem_bytes == 16 && nx == FsGeom::N && ny == FsGeom::N && batch == 1;
+    return elem_bytes == 16 && nx == FsGeom::N && ny == FsGeom::N && batch == 1 && tma_encoder() != nullptr;
 }
 
 // The field as the 4D tensor {2 n1 (doubles), n2, m1, m2} of a [y = m1 + P m2][x = n1 + P n2]
@@ -148,11 +150,13 @@ cudaError_t launch_fs_bb(void *f, const void *tw32, const double *mx2d, const do
     static SmemOptIn<decltype(k)> opt;
     cudaError_t e = opt(k, BbGeom::BYTES);
     if (e != cudaSuccess) return e;
-    static int occ = 0;
+    static std::atomic<int> occ_cache{0};
+    int occ = occ_cache.load();
     if (!occ) {
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, BbGeom::NT, BbGeom::BYTES);
         if (e != cudaSuccess) return e;
         if (occ < 1) return cudaErrorNotSupported;
+        occ_cache.store(occ);
     }
     int teams = FFTPDE_FS_TEAMS;
     if (const char *s = std::getenv("FFTPDE_FS_TEAMS")) teams = std::max(1, atoi(s));
