@@ -337,6 +337,9 @@ template <int N, typename C, int EMAX = 16> struct TwReg {
 // v[e] = X[t + TPT e].  INV selects the conjugate kernel (inverse direction,
 // unscaled).  `sync` synchronises the threads sharing the exchange buffer
 // (warp, line or CTA); the buffer is free again when this returns.
+#ifndef FFTPDE_TG32
+#define FFTPDE_TG32 8      // twiddles loaded per group by the radix-32 stages
+#endif
 template <int N, bool INV, int EMAX = 16, typename C, typename View, typename Tw, typename Sync>
 __device__ __forceinline__ void fft_tw(C (&v)[Shape<N, EMAX>::E], const View &sm, int t, const Tw &tw,
                                        Sync sync)
@@ -346,7 +349,7 @@ __device__ __forceinline__ void fft_tw(C (&v)[Shape<N, EMAX>::E], const View &sm
     // Twiddles fetched from memory (TwL1) are loaded in groups of TG before their
     // multiplies, so a group's loads are in flight together instead of each load's
     // latency following the previous multiply (the loads are volatile and ordered).
-    constexpr int TG = E <= 1 ? 1 : E <= 16 ? E - 1 : 8;
+    constexpr int TG = E <= 1 ? 1 : E <= 16 ? E - 1 : FFTPDE_TG32;
     int Ns = 1;
 #pragma unroll
     for (int s = 0; s < S::STAGES; ++s) {

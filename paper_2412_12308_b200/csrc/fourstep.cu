@@ -78,7 +78,7 @@ cudaError_t launch_aa(int op, const void *in, void *out, void *phys, const void 
 #define FFTPDE_FS_BYT_MINB 2
 #endif
 // the field as a 3D tensor {2 N doubles, N rows, 1}; boxes of 64 bytes x 256 rows
-static bool by_map(CUtensorMap &m, const void *p)
+static bool by_map(CUtensorMap &m, const void *p, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE)
 {
     using G = FsGeom;
     auto enc = tma_encoder();
@@ -88,7 +88,7 @@ static bool by_map(CUtensorMap &m, const void *p)
     cuuint32_t box[3] = {(cuuint32_t)(2 * ByGeom::W), (cuuint32_t)ByGeom::BOXR, 1};
     cuuint32_t es[3] = {1, 1, 1};
     return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void *>(p), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, FFTPDE_FS_PROMO_BY,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, swz, FFTPDE_FS_PROMO_BY,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -104,6 +104,39 @@ static cudaError_t launch_by_tma(void *f, const void *tw32, const double *my2d, 
                    m, (const double2 *)tw32, my2d);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
+}
+
+
+// The persistent three-slot B passes (b3_kernel): bit 0 Bx, bit 1 By
+#ifndef FFTPDE_FS_B3
+#define FFTPDE_FS_B3 1      // Bx persistent (-0.3 ms per step); By on by_kernel (b3 By measured equal)
+#endif
+template <bool COLS> static cudaError_t launch_b3(void *f, const void *tw32, const double *m2d, cudaStream_t st)
+{
+    using G = B3Geom<COLS>;
+    CUtensorMap m;
+    if (!by_map(m, f, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorNotSupported;
+    auto k = b3_kernel<COLS>;
+    static SmemOptIn<decltype(k)> opt;
+    cudaError_t e = opt(k, G::BYTES);
+    if (e != cudaSuccess) return e;
+    static std::atomic<int> occ_cache{0};
+    int occ = occ_cache.load(std::memory_order_relaxed);
+    if (occ == 0) {
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, G::NT, G::BYTES);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) return cudaErrorInvalidConfiguration;
+        occ_cache.store(occ, std::memory_order_relaxed);
+    }
+    const unsigned grid = (unsigned)std::min<int64_t>(G::NTILES, (int64_t)occ * sm_count());
+    e = launch_fam(PDL_FOURSTEP, k, dim3(grid), dim3(G::NT), G::BYTES, st, m, (double2 *)f, (const double2 *)tw32, m2d);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+static int fs_b3_mask()
+{
+    static const int v = [] { const char *e = std::getenv("FFTPDE_FS_B3"); return e ? std::atoi(e) : FFTPDE_FS_B3; }();
+    return v;
 }
 
 
@@ -209,6 +242,10 @@ cudaError_t launch_fs_b(bool cols, void *f, const void *tw32, const void *tw16, 
                         cudaStream_t st)
 {
     using G = FsGeom;
+    if (fs_b3_mask() & (cols ? 2 : 1)) {
+        const cudaError_t e = cols ? launch_b3<true>(f, tw32, tab.ey2d, st) : launch_b3<false>(f, tw32, tab.ey2d, st);
+        if (e != cudaErrorNotSupported) return e;
+    }
     if (!cols && FFTPDE_FS_BX_BULK) return launch_bx_bulk(f, tw32, tab.ey2d, st);
     if (!cols && FFTPDE_FS_BX_PIPE) {      // persistent double-buffered pipe pass (radix 16, 4 rows per tile)
         OpTables<double> t = tab;

@@ -42,13 +42,24 @@ struct FsGeom {
 #ifndef FFTPDE_FS_NBUF
 #define FFTPDE_FS_NBUF 1
 #endif
+#ifndef FFTPDE_FS_TWP
+#define FFTPDE_FS_TWP 33
+#endif
+#ifndef FFTPDE_FS_SWZ
+#define FFTPDE_FS_SWZ 1
+#endif
 // NB = 1: one tile per CTA, several CTAs per SM (the scheduler overlaps one CTA's
 // TMA traffic with another's transforms); NB = 2: persistent CTAs with the next
 // tile's load in flight
 template <int NB> struct FsCfg {
     static constexpr int NBUF = NB;
     static constexpr int MINB = NB == 1 ? FFTPDE_FS_MINB : 1;
-    static constexpr int TWS = FsGeom::W * FsGeom::Q + FsGeom::Q;   // the tile's twiddles: x [w][k1], y [l1]
+    // the tile's twiddles: x [w][k1] at row pitch TWP = Q + 1 (the four w rows of one k1
+    // fall in distinct banks: the x-pass loads of a warp are one wavefront, not four),
+    // then y [l1]; TWB = the bytes they bring
+    static constexpr int TWP = FFTPDE_FS_TWP;
+    static constexpr int TWS = FsGeom::W * TWP + FsGeom::Q;
+    static constexpr uint32_t TWB = (uint32_t)(FsGeom::W * FsGeom::Q + FsGeom::Q) * 16;
     static constexpr size_t BYTES = (size_t)NB * (FsGeom::TILE + TWS) * 16 + 128 + 64;   // + alignment slack + mbarriers
 };
 enum FsOp { FS_FWD = 0, FS_INV = 1, FS_MID = 2, FS_COPY = 3, FS_COPY3 = 4 };   // COPY*: traffic-only (experiments)
@@ -107,10 +118,17 @@ aa_kernel(const __grid_constant__ CUtensorMap min, const __grid_constant__ CUten
     auto load = [&](int tile, int slot) {                 // thread 0: the tile, and its twiddles (with TWS bytes)
         const int m1 = tile / G::NCHUNK, chunk = tile % G::NCHUNK;
         double2 *ts = TWS0 + slot * FsCfg<NB>::TWS;
-        tma_mbar_expect(mbar0 + 8u * slot, (uint32_t)((G::TILE + FsCfg<NB>::TWS) * 16));
+        constexpr int TWP = FsCfg<NB>::TWP;
+        tma_mbar_expect(mbar0 + 8u * slot, (uint32_t)(G::TILE * 16) + FsCfg<NB>::TWB);
         tma_load4(tma_smem(S0 + slot * G::TILE), &min, 2 * W * chunk, 0, m1, 0, mbar0 + 8u * slot);
-        bulk_g2s(tma_smem(ts), tw + (size_t)chunk * W * Q, W * Q * 16, mbar0 + 8u * slot);      // w_N^{n1 k1}, 4 n1
-        bulk_g2s(tma_smem(ts + W * Q), tw + (size_t)m1 * Q, Q * 16, mbar0 + 8u * slot);          // w_N^{m1 l1}
+        if constexpr (TWP == Q) {
+            bulk_g2s(tma_smem(ts), tw + (size_t)chunk * W * Q, W * Q * 16, mbar0 + 8u * slot);  // w_N^{n1 k1}, 4 n1
+        } else {
+#pragma unroll
+            for (int i = 0; i < W; ++i)
+                bulk_g2s(tma_smem(ts + i * TWP), tw + ((size_t)chunk * W + i) * Q, Q * 16, mbar0 + 8u * slot);
+        }
+        bulk_g2s(tma_smem(ts + W * TWP), tw + (size_t)m1 * Q, Q * 16, mbar0 + 8u * slot);      // w_N^{m1 l1}
     };
     pdl_wait();
     int tile = blockIdx.x;
@@ -134,10 +152,22 @@ aa_kernel(const __grid_constant__ CUtensorMap min, const __grid_constant__ CUten
         const int m1 = tile / G::NCHUNK, chunk = tile % G::NCHUNK;
         const int n1 = chunk * W + w;
         const int c0 = 2 * W * chunk;                      // tensor coordinate (doubles) of the chunk
-        const double2 *twx = TWS0 + slot * FsCfg<NB>::TWS + w * Q;    // w_N^{n1 k1}
-        const double2 *twy = TWS0 + slot * FsCfg<NB>::TWS + W * Q;    // w_N^{m1 l1}
+        const double2 *twx = TWS0 + slot * FsCfg<NB>::TWS + w * FsCfg<NB>::TWP;   // w_N^{n1 k1}
+        const double2 *twy = TWS0 + slot * FsCfg<NB>::TWS + W * FsCfg<NB>::TWP;   // w_N^{m1 l1}
         (void)n1;
         double2 v[Q];
+        // The intermediate between the x and y DFTs is kept row-swizzled: element
+        // (row, col) at (row, col ^ (row & 1)).  An x-pass warp covers 8 rows x 4 w of
+        // one col, two rows per quarter-warp; dense, those two rows hit the same
+        // banks (two wavefronts per quarter), swizzled they fill both 64-byte halves.
+        // The TMA-facing layouts (tile in, physical field and AA domain out) stay dense.
+        const int rb = FFTPDE_FS_SWZ ? (r & 1) : 0;
+        double2 *const xe = S + (r * Q + rb) * W + w;      // x pass, row r: even cols at xe[n W]
+        double2 *const xo = S + (r * Q - rb) * W + w;      //                odd cols at xo[n W]
+        double2 *const ye = S + r * W + w;                 // y pass, col r: even rows at ye[m Q W]
+        double2 *const yo = S + (FFTPDE_FS_SWZ ? (r ^ 1) : r) * W + w;   //  odd rows at yo[m Q W]
+        auto X = [&](int n) -> double2 & { return (n & 1) ? xo[n * W] : xe[n * W]; };
+        auto Y = [&](int m) -> double2 & { return (m & 1) ? yo[m * Q * W] : ye[m * Q * W]; };
         tma_mbar_wait(mbar0 + 8u * slot, (uint32_t)(it / NBUF) & 1u);
 
         auto xpass_fwd = [&]() {      // v[n2] (thread (m2, w)) -> v[k1] = w^{n1 k1} DFT_n2
@@ -147,7 +177,7 @@ aa_kernel(const __grid_constant__ CUtensorMap min, const __grid_constant__ CUten
         };
         auto ypass_fwd = [&]() {      // thread (k1, w): rows m2 -> l1
 #pragma unroll
-            for (int m = 0; m < Q; ++m) v[m] = S[(m * Q + r) * W + w];
+            for (int m = 0; m < Q; ++m) v[m] = Y(m);
             dft_r<Q, false>(v);
 #pragma unroll
             for (int l = 1; l < Q; ++l) v[l] = cmulw<false>(v[l], twy[l]);
@@ -173,7 +203,7 @@ aa_kernel(const __grid_constant__ CUtensorMap min, const __grid_constant__ CUten
             for (int n = 0; n < Q; ++n) v[n] = S[(r * Q + n) * W + w];
             xpass_fwd();
 #pragma unroll
-            for (int k = 0; k < Q; ++k) S[(r * Q + k) * W + w] = v[k];
+            for (int k = 0; k < Q; ++k) X(k) = v[k];
             __syncthreads();
             ypass_fwd();
             store_tile(&mout);
@@ -185,11 +215,11 @@ aa_kernel(const __grid_constant__ CUtensorMap min, const __grid_constant__ CUten
             for (int l = 1; l < Q; ++l) v[l] = cmulw<true>(v[l], twy[l]);
             dft_r<Q, true>(v);
 #pragma unroll
-            for (int m = 0; m < Q; ++m) S[(m * Q + r) * W + w] = v[m];
+            for (int m = 0; m < Q; ++m) Y(m) = v[m];
             __syncthreads();
             // thread (m2, w): k1 -> n2 with w^{-n1 k1} (own slots only)
 #pragma unroll
-            for (int k = 0; k < Q; ++k) v[k] = S[(r * Q + k) * W + w];
+            for (int k = 0; k < Q; ++k) v[k] = X(k);
 #pragma unroll
             for (int k = 1; k < Q; ++k) v[k] = cmulw<true>(v[k], twx[k]);
             dft_r<Q, true>(v);
@@ -204,7 +234,7 @@ aa_kernel(const __grid_constant__ CUtensorMap min, const __grid_constant__ CUten
                 if (tid == 0) tma_wait_read0();            // the stores have read their slots
                 __syncthreads();
 #pragma unroll
-                for (int k = 0; k < Q; ++k) S[(r * Q + k) * W + w] = v[k];
+                for (int k = 0; k < Q; ++k) X(k) = v[k];
                 __syncthreads();
                 ypass_fwd();
                 store_tile(&mout);
@@ -370,6 +400,129 @@ bx_kernel(double2 *f, const double2 *__restrict__ tw32, const double *__restrict
         tma_commit();
         tma_wait_read0();
     }
+}
+
+
+// ---- B3: Bx or By as a persistent pass: one CTA per SM made of two independent
+// 4-warp groups and three 64 KiB tile slots.  Tile j of the CTA (global tile
+// blockIdx.x + j gridDim.x) sits in slot j % 3 and is transformed by group j % 2;
+// the group that finishes tile j stores it, and as soon as the store has read the
+// slot it loads tile j + 3 there.  Two tiles are in the transforms while the third
+// is in flight from HBM, so neither group waits for a load once the pipe is full
+// (the one-tile-per-CTA passes above spend a quarter of their stalls there).
+// Per tile the work is that of by_kernel (COLS) or bx_kernel (rows), one warp per
+// line on either axis: the By tile arrives under the 64-byte hardware swizzle, so
+// lane t reading rows t + 32 e of column c hits eight distinct 16-byte bank groups
+// per phase, and the exchanges are warp-synchronous (no CTA barrier per stage).
+template <bool COLS> struct B3Geom {
+    static constexpr int L = 1024, E = 32, W = 4, BOXR = 256;
+    static constexpr int GT = W * (L / E);                          // 128 threads per group
+    static constexpr int NG = 2, NT = NG * GT, NSLOT = 3;
+    static constexpr int PITCH = Shape<L, E>::PADDED;
+    static constexpr size_t TILE_BYTES = (size_t)L * W * 16;       // 64 KiB dense
+    static constexpr size_t XCH_BYTES = (size_t)W * PITCH * 16;
+    static constexpr size_t SLOT = ((TILE_BYTES > XCH_BYTES ? TILE_BYTES : XCH_BYTES) + 1023) / 1024 * 1024;
+    static constexpr size_t BYTES = NSLOT * SLOT + 1024 + 8 * NSLOT + 4 * NSLOT;
+    static constexpr int NGROUP = FsGeom::N / W;                   // column groups per block (COLS)
+    static constexpr int NTILES = FsGeom::Q * NGROUP;              // 262144 on either axis
+};
+struct SyncGroup {
+    int id;
+    __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
+};
+
+template <bool COLS>
+__global__ void __launch_bounds__(B3Geom<COLS>::NT, 1)
+b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__restrict__ tw32,
+          const double *__restrict__ m2d)
+{
+    using G = B3Geom<COLS>;
+    constexpr int L = G::L, E = G::E, W = G::W, TPT = L / E, NS = G::NSLOT;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const uint32_t pad = (1024u - (tma_smem(smem_raw) & 1023u)) & 1023u;   // the swizzle pattern's alignment
+    unsigned char *base = smem_raw + pad;
+    const uint32_t mbar0 = tma_smem(base + NS * G::SLOT);
+    // issued[s] = the CTA-local index of the last tile loaded into slot s: a group
+    // waits on a slot's mbarrier only once its own tile's load was issued, so the
+    // parity it waits for is never two phases ahead of the barrier
+    volatile int *issued = reinterpret_cast<volatile int *>(base + NS * G::SLOT + 8 * NS);
+    const int grp = threadIdx.x / G::GT, tid = threadIdx.x % G::GT;
+    const int c = tid / TPT, t = tid % TPT;                        // line c of the tile, lane t
+    const SyncGroup gsync{1 + grp};
+    auto slot_ptr = [&](int s) { return reinterpret_cast<double2 *>(base + s * G::SLOT); };
+    auto load = [&](int64_t tile, int s) {
+        const uint32_t mb = mbar0 + 8u * s;
+        tma_mbar_expect(mb, (uint32_t)G::TILE_BYTES);
+        if constexpr (COLS) {
+            const int l1 = (int)(tile / G::NGROUP), g = (int)(tile % G::NGROUP);
+#pragma unroll
+            for (int k = 0; k < L / G::BOXR; ++k)
+                tma_load3(tma_smem(slot_ptr(s)) + k * G::BOXR * W * 16, &map, 2 * W * g, 1024 * l1 + k * G::BOXR, 0, mb);
+        } else {
+            bulk_g2s(tma_smem(slot_ptr(s)), f + tile * (W * L), (uint32_t)G::TILE_BYTES, mb);
+        }
+    };
+    pdl_wait();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) tma_mbar_init(mbar0 + 8u * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int s = 0; s < NS; ++s) {
+            const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
+            issued[s] = s;
+            if (tile < G::NTILES) load(tile, s);
+        }
+    }
+    __syncthreads();
+    pdl_trigger();
+    const TwL1<L, double2, E> twp{tw32, t};
+    for (int j = grp;; j += G::NG) {
+        const int64_t tile = blockIdx.x + (int64_t)j * gridDim.x;
+        if (tile >= G::NTILES) break;
+        const int s = j % NS;
+        double2 *S = slot_ptr(s);
+        while (issued[s] != j) {}
+        tma_mbar_wait(mbar0 + 8u * s, (uint32_t)(j / NS) & 1u);
+        double2 v[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = COLS ? *reinterpret_cast<const double2 *>(
+                                                     reinterpret_cast<const unsigned char *>(S) + swz64((uint32_t)(t + TPT * e) * 64u + 16u * c))
+                                               : S[c * L + t + TPT * e];
+        gsync();                                                   // the tile slot becomes the exchange buffers
+        const SmemView<double2, Shape<L, E>::LOGE, 1> sm{S + c * G::PITCH};
+        const double *m;
+        if constexpr (COLS) m = m2d + (size_t)(tile / G::NGROUP) * L + t;               // class l1
+        else m = m2d + (size_t)((tile * W + c) % FsGeom::Q) * L + t;                     // class k1
+        const SyncWarp wsync{};
+        fft_tw<L, false, E>(v, sm, t, twp, wsync);
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = cscale(v[e], __ldg(m + TPT * e));
+        fft_tw<L, true, E>(v, sm, t, twp, wsync);
+        gsync();                                                   // every line's exchanges are done
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if constexpr (COLS)
+                *reinterpret_cast<double2 *>(reinterpret_cast<unsigned char *>(S) + swz64((uint32_t)(t + TPT * e) * 64u + 16u * c)) = v[e];
+            else S[c * L + t + TPT * e] = v[e];
+        }
+        tma_fence_smem();
+        gsync();
+        if (tid == 0) {
+            if constexpr (COLS) {
+                const int l1 = (int)(tile / G::NGROUP), g = (int)(tile % G::NGROUP);
+#pragma unroll
+                for (int k = 0; k < L / G::BOXR; ++k)
+                    tma_store3(&map, 2 * W * g, 1024 * l1 + k * G::BOXR, 0, tma_smem(S) + k * G::BOXR * W * 16);
+            } else {
+                bulk_s2g(f + tile * (W * L), tma_smem(S), (uint32_t)G::TILE_BYTES);
+            }
+            tma_commit();
+            const int64_t nt = blockIdx.x + (int64_t)(j + NS) * gridDim.x;
+            tma_wait_read0();                                      // the slot is free once the store has read it
+            if (nt < G::NTILES) load(nt, s);
+            issued[s] = j + NS;
+        }
+    }
+    if (tid == 0) tma_wait_read0();
 }
 
 
