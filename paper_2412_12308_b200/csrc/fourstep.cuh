@@ -48,6 +48,9 @@ struct FsGeom {
 #ifndef FFTPDE_FS_SWZ
 #define FFTPDE_FS_SWZ 1
 #endif
+#ifndef FFTPDE_FS_XSEL
+#define FFTPDE_FS_XSEL 1
+#endif
 // NB = 1: one tile per CTA, several CTAs per SM (the scheduler overlaps one CTA's
 // TMA traffic with another's transforms); NB = 2: persistent CTAs with the next
 // tile's load in flight
@@ -63,6 +66,11 @@ template <int NB> struct FsCfg {
     static constexpr size_t BYTES = (size_t)NB * (FsGeom::TILE + TWS) * 16 + 128 + 64;   // + alignment slack + mbarriers
 };
 enum FsOp { FS_FWD = 0, FS_INV = 1, FS_MID = 2, FS_COPY = 3, FS_COPY3 = 4 };   // COPY*: traffic-only (experiments)
+// a 128-thread group's named barrier (id >= 1; 0 is __syncthreads)
+struct SyncGroup {
+    int id;
+    __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
+};
 
 __device__ __forceinline__ void tma_load4(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
                                           uint32_t mbar)
@@ -95,19 +103,147 @@ __device__ __forceinline__ void tma_prefetch3(const CUtensorMap *map, int c0, in
 // Tables: tw[a][b] = w_N^{a b}, a < P, b < Q (both axes: x and y have the same N).
 // Tile smem layout [row index r][col index c][w] = (r * Q + c) * W + w, where r is
 // m2 (physical) or l1 (AA domain) and c is n2 or k1.
+
+// Thread `lead` issues the loads of a tile (TMA box) and of its twiddles into slot
+// S / ts, completing on mbarrier `mb`.
+template <typename Cfg>
+__device__ __forceinline__ void aa_load(const CUtensorMap *min, const double2 *tw, int tile, double2 *S, double2 *ts,
+                                        uint32_t mb)
+{
+    using G = FsGeom;
+    constexpr int Q = G::Q, W = G::W, TWP = Cfg::TWP;
+    const int m1 = tile / G::NCHUNK, chunk = tile % G::NCHUNK;
+    tma_mbar_expect(mb, (uint32_t)(G::TILE * 16) + Cfg::TWB);
+    tma_load4(tma_smem(S), min, 2 * W * chunk, 0, m1, 0, mb);
+    if constexpr (TWP == Q) {
+        bulk_g2s(tma_smem(ts), tw + (size_t)chunk * W * Q, W * Q * 16, mb);     // w_N^{n1 k1}, 4 n1
+    } else {
+#pragma unroll
+        for (int i = 0; i < W; ++i) bulk_g2s(tma_smem(ts + i * TWP), tw + ((size_t)chunk * W + i) * Q, Q * 16, mb);
+    }
+    bulk_g2s(tma_smem(ts + W * TWP), tw + (size_t)m1 * Q, Q * 16, mb);           // w_N^{m1 l1}
+}
+
+// The work on one landed tile by 128 threads (r, w) = (tid / W, tid % W), `sync`
+// their barrier, `lead` the thread that issues the stores.  On return the last
+// store is committed (the caller waits for its read before reusing the slot).
+template <int OP, typename Cfg, typename Sync>
+__device__ __forceinline__ void aa_tile(double2 *S, const double2 *ts, int r, int w, bool lead, int tile,
+                                        const CUtensorMap *mout, const CUtensorMap *mphys, Sync sync)
+{
+    using G = FsGeom;
+    constexpr int Q = G::Q, W = G::W;
+    const int m1 = tile / G::NCHUNK, chunk = tile % G::NCHUNK;
+    const int c0 = 2 * W * chunk;                          // tensor coordinate (doubles) of the chunk
+    const double2 *twx = ts + w * Cfg::TWP;                // w_N^{n1 k1}
+    const double2 *twy = ts + W * Cfg::TWP;                // w_N^{m1 l1}
+    double2 v[Q];
+    // The intermediate between the x and y DFTs is kept row-swizzled: element
+    // (row, col) at (row, col ^ (row & 1)).  An x-pass warp covers 8 rows x 4 w of
+    // one col, two rows per quarter-warp; dense, those two rows hit the same
+    // banks (two wavefronts per quarter), swizzled they fill both 64-byte halves.
+    // The TMA-facing layouts (tile in, physical field and AA domain out) stay dense.
+    const int rb = FFTPDE_FS_SWZ ? (r & 1) : 0;
+    double2 *const xe = S + (r * Q + rb) * W + w;          // x pass, row r: even cols at xe[n W]
+    double2 *const xo = S + (r * Q - rb) * W + w;          //                odd cols at xo[n W]
+    double2 *const ye = S + r * W + w;                     // y pass, col r: even rows at ye[m Q W]
+    double2 *const yo = S + (FFTPDE_FS_SWZ ? (r ^ 1) : r) * W + w;   //      odd rows at yo[m Q W]
+    auto X = [&](int n) -> double2 & { return (n & 1) ? xo[n * W] : xe[n * W]; };
+    auto Y = [&](int m) -> double2 & { return (m & 1) ? yo[m * Q * W] : ye[m * Q * W]; };
+
+    auto xpass_fwd = [&]() {      // v[n2] (thread (m2, w)) -> v[k1] = w^{n1 k1} DFT_n2
+        dft_r<Q, false>(v);
+#pragma unroll
+        for (int k = 1; k < Q; ++k) v[k] = cmulw<false>(v[k], twx[k]);
+    };
+    auto ypass_fwd = [&]() {      // thread (k1, w): rows m2 -> l1
+#pragma unroll
+        for (int m = 0; m < Q; ++m) v[m] = Y(m);
+        dft_r<Q, false>(v);
+#pragma unroll
+        for (int l = 1; l < Q; ++l) v[l] = cmulw<false>(v[l], twy[l]);
+#pragma unroll
+        for (int l = 0; l < Q; ++l) S[(l * Q + r) * W + w] = v[l];
+    };
+    auto store_tile = [&](const CUtensorMap *map) {
+        tma_fence_smem();
+        sync();
+        if (lead) {
+            tma_store4(map, c0, 0, m1, 0, tma_smem(S));
+            tma_commit();
+        }
+    };
+
+    if constexpr (OP == FS_COPY) {                         // the AA / AA^-1 traffic with no arithmetic
+        store_tile(mout);
+    } else if constexpr (OP == FS_COPY3) {                 // the MID traffic: two stores of the tile
+        store_tile(mphys);
+        store_tile(mout);
+    } else if constexpr (OP == FS_FWD) {
+#pragma unroll
+        for (int n = 0; n < Q; ++n) v[n] = S[(r * Q + n) * W + w];
+        xpass_fwd();
+#pragma unroll
+        for (int k = 0; k < Q; ++k) X(k) = v[k];
+        sync();
+        ypass_fwd();
+        store_tile(mout);
+    } else {
+        // ---- AA^-1: thread (k1, w): rows l1 -> m2 with w^{-m1 l1} (own slots only)
+#pragma unroll
+        for (int l = 0; l < Q; ++l) v[l] = S[(l * Q + r) * W + w];
+#pragma unroll
+        for (int l = 1; l < Q; ++l) v[l] = cmulw<true>(v[l], twy[l]);
+        dft_r<Q, true>(v);
+#pragma unroll
+        for (int m = 0; m < Q; ++m) Y(m) = v[m];
+        sync();
+        // thread (m2, w): k1 -> n2 with w^{-n1 k1} (own slots only)
+#pragma unroll
+        for (int k = 0; k < Q; ++k) v[k] = X(k);
+#pragma unroll
+        for (int k = 1; k < Q; ++k) v[k] = cmulw<true>(v[k], twx[k]);
+        dft_r<Q, true>(v);
+        // the physical tile, dense for the TMA store: odd rows write col n ^ 1 in
+        // store n, so each quarter-warp fills both 64-byte halves (conflict-free)
+#pragma unroll
+        for (int n = 0; n < Q; ++n) {
+            if (FFTPDE_FS_XSEL) X(n) = rb ? v[n ^ 1] : v[n];
+            else S[(r * Q + n) * W + w] = v[n];
+        }
+        if constexpr (OP == FS_INV) {
+            store_tile(mout);
+        } else {
+            store_tile(mphys);                             // the physical field of this step
+            // ---- AA of the next step, from the registers
+            xpass_fwd();
+            if (lead) tma_wait_read0();                    // the store has read the slot
+            sync();
+#pragma unroll
+            for (int k = 0; k < Q; ++k) X(k) = v[k];
+            sync();
+            ypass_fwd();
+            store_tile(mout);
+        }
+    }
+}
+
+struct SyncBlock { __device__ __forceinline__ void operator()() const { __syncthreads(); } };
+
 template <int OP, int NB>
 __global__ void __launch_bounds__(FsGeom::NT, FsCfg<NB>::MINB)
 aa_kernel(const __grid_constant__ CUtensorMap min, const __grid_constant__ CUtensorMap mout,
           const __grid_constant__ CUtensorMap mphys, const double2 *__restrict__ tw)
 {
     using G = FsGeom;
-    constexpr int Q = G::Q, W = G::W, NBUF = FsCfg<NB>::NBUF;
+    using Cfg = FsCfg<NB>;
+    constexpr int W = G::W, NBUF = Cfg::NBUF;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     // 128-byte aligned tile slots (offset kept in the shared window: LDS/STS, not generic loads)
     const uint32_t pad = (128u - (tma_smem(smem_raw) & 127u)) & 127u;
     double2 *S0 = reinterpret_cast<double2 *>(smem_raw + pad);
     double2 *TWS0 = S0 + NBUF * G::TILE;                   // per slot: [w][k1] x twiddles, then [l1] y twiddles
-    const uint32_t mbar0 = tma_smem(TWS0 + NBUF * FsCfg<NB>::TWS);
+    const uint32_t mbar0 = tma_smem(TWS0 + NBUF * Cfg::TWS);
     const int tid = threadIdx.x;
     const int w = tid % W, r = tid / W;                   // (m2 | k1, w) of this thread
     if (tid == 0) {
@@ -115,20 +251,8 @@ aa_kernel(const __grid_constant__ CUtensorMap min, const __grid_constant__ CUten
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    auto load = [&](int tile, int slot) {                 // thread 0: the tile, and its twiddles (with TWS bytes)
-        const int m1 = tile / G::NCHUNK, chunk = tile % G::NCHUNK;
-        double2 *ts = TWS0 + slot * FsCfg<NB>::TWS;
-        constexpr int TWP = FsCfg<NB>::TWP;
-        tma_mbar_expect(mbar0 + 8u * slot, (uint32_t)(G::TILE * 16) + FsCfg<NB>::TWB);
-        tma_load4(tma_smem(S0 + slot * G::TILE), &min, 2 * W * chunk, 0, m1, 0, mbar0 + 8u * slot);
-        if constexpr (TWP == Q) {
-            bulk_g2s(tma_smem(ts), tw + (size_t)chunk * W * Q, W * Q * 16, mbar0 + 8u * slot);  // w_N^{n1 k1}, 4 n1
-        } else {
-#pragma unroll
-            for (int i = 0; i < W; ++i)
-                bulk_g2s(tma_smem(ts + i * TWP), tw + ((size_t)chunk * W + i) * Q, Q * 16, mbar0 + 8u * slot);
-        }
-        bulk_g2s(tma_smem(ts + W * TWP), tw + (size_t)m1 * Q, Q * 16, mbar0 + 8u * slot);      // w_N^{m1 l1}
+    auto load = [&](int t, int slot) {
+        aa_load<Cfg>(&min, tw, t, S0 + slot * G::TILE, TWS0 + slot * Cfg::TWS, mbar0 + 8u * slot);
     };
     pdl_wait();
     int tile = blockIdx.x;
@@ -148,101 +272,13 @@ aa_kernel(const __grid_constant__ CUtensorMap min, const __grid_constant__ CUten
                 pdl_trigger();
             }
         }
-        double2 *S = S0 + slot * G::TILE;
-        const int m1 = tile / G::NCHUNK, chunk = tile % G::NCHUNK;
-        const int n1 = chunk * W + w;
-        const int c0 = 2 * W * chunk;                      // tensor coordinate (doubles) of the chunk
-        const double2 *twx = TWS0 + slot * FsCfg<NB>::TWS + w * FsCfg<NB>::TWP;   // w_N^{n1 k1}
-        const double2 *twy = TWS0 + slot * FsCfg<NB>::TWS + W * FsCfg<NB>::TWP;   // w_N^{m1 l1}
-        (void)n1;
-        double2 v[Q];
-        // The intermediate between the x and y DFTs is kept row-swizzled: element
-        // (row, col) at (row, col ^ (row & 1)).  An x-pass warp covers 8 rows x 4 w of
-        // one col, two rows per quarter-warp; dense, those two rows hit the same
-        // banks (two wavefronts per quarter), swizzled they fill both 64-byte halves.
-        // The TMA-facing layouts (tile in, physical field and AA domain out) stay dense.
-        const int rb = FFTPDE_FS_SWZ ? (r & 1) : 0;
-        double2 *const xe = S + (r * Q + rb) * W + w;      // x pass, row r: even cols at xe[n W]
-        double2 *const xo = S + (r * Q - rb) * W + w;      //                odd cols at xo[n W]
-        double2 *const ye = S + r * W + w;                 // y pass, col r: even rows at ye[m Q W]
-        double2 *const yo = S + (FFTPDE_FS_SWZ ? (r ^ 1) : r) * W + w;   //  odd rows at yo[m Q W]
-        auto X = [&](int n) -> double2 & { return (n & 1) ? xo[n * W] : xe[n * W]; };
-        auto Y = [&](int m) -> double2 & { return (m & 1) ? yo[m * Q * W] : ye[m * Q * W]; };
         tma_mbar_wait(mbar0 + 8u * slot, (uint32_t)(it / NBUF) & 1u);
-
-        auto xpass_fwd = [&]() {      // v[n2] (thread (m2, w)) -> v[k1] = w^{n1 k1} DFT_n2
-            dft_r<Q, false>(v);
-#pragma unroll
-            for (int k = 1; k < Q; ++k) v[k] = cmulw<false>(v[k], twx[k]);
-        };
-        auto ypass_fwd = [&]() {      // thread (k1, w): rows m2 -> l1
-#pragma unroll
-            for (int m = 0; m < Q; ++m) v[m] = Y(m);
-            dft_r<Q, false>(v);
-#pragma unroll
-            for (int l = 1; l < Q; ++l) v[l] = cmulw<false>(v[l], twy[l]);
-#pragma unroll
-            for (int l = 0; l < Q; ++l) S[(l * Q + r) * W + w] = v[l];
-        };
-        auto store_tile = [&](const CUtensorMap *map) {
-            tma_fence_smem();
-            __syncthreads();
-            if (tid == 0) {
-                tma_store4(map, c0, 0, m1, 0, tma_smem(S));
-                tma_commit();
-            }
-        };
-
-        if constexpr (OP == FS_COPY) {                     // the AA / AA^-1 traffic with no arithmetic
-            store_tile(&mout);
-        } else if constexpr (OP == FS_COPY3) {             // the MID traffic: two stores of the tile
-            store_tile(&mphys);
-            store_tile(&mout);
-        } else if constexpr (OP == FS_FWD) {
-#pragma unroll
-            for (int n = 0; n < Q; ++n) v[n] = S[(r * Q + n) * W + w];
-            xpass_fwd();
-#pragma unroll
-            for (int k = 0; k < Q; ++k) X(k) = v[k];
-            __syncthreads();
-            ypass_fwd();
-            store_tile(&mout);
-        } else {
-            // ---- AA^-1: thread (k1, w): rows l1 -> m2 with w^{-m1 l1} (own slots only)
-#pragma unroll
-            for (int l = 0; l < Q; ++l) v[l] = S[(l * Q + r) * W + w];
-#pragma unroll
-            for (int l = 1; l < Q; ++l) v[l] = cmulw<true>(v[l], twy[l]);
-            dft_r<Q, true>(v);
-#pragma unroll
-            for (int m = 0; m < Q; ++m) Y(m) = v[m];
-            __syncthreads();
-            // thread (m2, w): k1 -> n2 with w^{-n1 k1} (own slots only)
-#pragma unroll
-            for (int k = 0; k < Q; ++k) v[k] = X(k);
-#pragma unroll
-            for (int k = 1; k < Q; ++k) v[k] = cmulw<true>(v[k], twx[k]);
-            dft_r<Q, true>(v);
-#pragma unroll
-            for (int n = 0; n < Q; ++n) S[(r * Q + n) * W + w] = v[n];
-            if constexpr (OP == FS_INV) {
-                store_tile(&mout);
-            } else {
-                store_tile(&mphys);                        // the physical field of this step
-                // ---- AA of the next step, from the registers
-                xpass_fwd();
-                if (tid == 0) tma_wait_read0();            // the stores have read their slots
-                __syncthreads();
-#pragma unroll
-                for (int k = 0; k < Q; ++k) X(k) = v[k];
-                __syncthreads();
-                ypass_fwd();
-                store_tile(&mout);
-            }
-        }
+        aa_tile<OP, Cfg>(S0 + slot * G::TILE, TWS0 + slot * Cfg::TWS, r, w, tid == 0, tile, &mout, &mphys,
+                         SyncBlock{});
     }
     if (tid == 0) tma_wait_read0();                        // smem stays valid until the stores have read it
 }
+
 
 
 // ---- By: the 1024-point column segments of the AA-domain field (block l1 = rows
@@ -425,10 +461,6 @@ template <bool COLS> struct B3Geom {
     static constexpr size_t BYTES = NSLOT * SLOT + 1024 + 8 * NSLOT + 4 * NSLOT;
     static constexpr int NGROUP = FsGeom::N / W;                   // column groups per block (COLS)
     static constexpr int NTILES = FsGeom::Q * NGROUP;              // 262144 on either axis
-};
-struct SyncGroup {
-    int id;
-    __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
 };
 
 template <bool COLS>
