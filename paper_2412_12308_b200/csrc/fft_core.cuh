@@ -308,6 +308,33 @@ template <int N, typename C, int EMAX = 16> struct TwSmem {
     }
 };
 
+// As TwSmem for complex128, each read a volatile ld.shared at its use (like ldtw:
+// neither kept live across transforms nor hoisted), `base` the table's shared-window
+// address.
+template <int N, int EMAX = 16> struct TwSmemV {
+    uint32_t base;
+    int t;
+    static __device__ __forceinline__ double2 ld(uint32_t a)
+    {
+        double2 r;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"(a));
+        return r;
+    }
+    __device__ __forceinline__ double2 mid(int s, int m) const
+    {
+        using S = Shape<N, EMAX>;
+        int ns = S::E, off = 0;
+#pragma unroll
+        for (int i = 1; i < s; ++i) { off += S::E * ns; ns *= S::E; }
+        return ld(base + 16u * (uint32_t)(off + (t & (ns - 1)) + m * ns));
+    }
+    __device__ __forceinline__ double2 last(int q, int m) const
+    {
+        using S = Shape<N, EMAX>;
+        return ld(base + 16u * (uint32_t)(S::TW_LAST_OFF + t + q * S::TPT + m * S::NS_LAST));
+    }
+};
+
 template <int N, typename C, int EMAX = 16> struct TwReg {
     using S = Shape<N, EMAX>;
     static constexpr int NMID = S::STAGES > 1 ? (S::STAGES - 1) * (S::E - 1) : 1;

@@ -109,7 +109,7 @@ static cudaError_t launch_by_tma(void *f, const void *tw32, const double *my2d, 
 
 // The persistent three-slot B passes (b3_kernel): bit 0 Bx, bit 1 By
 #ifndef FFTPDE_FS_B3
-#define FFTPDE_FS_B3 1      // Bx persistent (-0.3 ms per step); By on by_kernel (b3 By measured equal)
+#define FFTPDE_FS_B3 3      // Bx and By persistent (C5 512 vs 525 ms per 20-step solve against by_kernel / line Bx)
 #endif
 template <bool COLS> static cudaError_t launch_b3(void *f, const void *tw32, const double *m2d, cudaStream_t st)
 {

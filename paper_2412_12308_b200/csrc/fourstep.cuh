@@ -45,6 +45,9 @@ struct FsGeom {
 #ifndef FFTPDE_FS_TWP
 #define FFTPDE_FS_TWP 33
 #endif
+#ifndef FFTPDE_FS_B3TW
+#define FFTPDE_FS_B3TW 1    // b3_kernel: the 1024-point twiddles from shared memory
+#endif
 #ifndef FFTPDE_FS_SWZ
 #define FFTPDE_FS_SWZ 1
 #endif
@@ -458,7 +461,9 @@ template <bool COLS> struct B3Geom {
     static constexpr size_t TILE_BYTES = (size_t)L * W * 16;       // 64 KiB dense
     static constexpr size_t XCH_BYTES = (size_t)W * PITCH * 16;
     static constexpr size_t SLOT = ((TILE_BYTES > XCH_BYTES ? TILE_BYTES : XCH_BYTES) + 1023) / 1024 * 1024;
-    static constexpr size_t BYTES = NSLOT * SLOT + 1024 + 8 * NSLOT + 4 * NSLOT;
+    static constexpr int TWN = Shape<L, E>::TW_SIZE;               // the twiddle table staged in smem
+    static constexpr size_t TWBYTES = FFTPDE_FS_B3TW ? (size_t)TWN * 16 : 0;
+    static constexpr size_t BYTES = NSLOT * SLOT + TWBYTES + 1024 + 8 * NSLOT + 4 * NSLOT;
     static constexpr int NGROUP = FsGeom::N / W;                   // column groups per block (COLS)
     static constexpr int NTILES = FsGeom::Q * NGROUP;              // 262144 on either axis
 };
@@ -473,11 +478,12 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t pad = (1024u - (tma_smem(smem_raw) & 1023u)) & 1023u;   // the swizzle pattern's alignment
     unsigned char *base = smem_raw + pad;
-    const uint32_t mbar0 = tma_smem(base + NS * G::SLOT);
+    double2 *const twS = reinterpret_cast<double2 *>(base + NS * G::SLOT);   // [TWN] twiddles (FFTPDE_FS_B3TW)
+    const uint32_t mbar0 = tma_smem(base + NS * G::SLOT + G::TWBYTES);
     // issued[s] = the CTA-local index of the last tile loaded into slot s: a group
     // waits on a slot's mbarrier only once its own tile's load was issued, so the
     // parity it waits for is never two phases ahead of the barrier
-    volatile int *issued = reinterpret_cast<volatile int *>(base + NS * G::SLOT + 8 * NS);
+    volatile int *issued = reinterpret_cast<volatile int *>(base + NS * G::SLOT + G::TWBYTES + 8 * NS);
     const int grp = threadIdx.x / G::GT, tid = threadIdx.x % G::GT;
     const int c = tid / TPT, t = tid % TPT;                        // line c of the tile, lane t
     const SyncGroup gsync{1 + grp};
@@ -504,9 +510,14 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
             if (tile < G::NTILES) load(tile, s);
         }
     }
+    if constexpr (FFTPDE_FS_B3TW)
+        for (int i = threadIdx.x; i < G::TWN; i += G::NT) twS[i] = tw32[i];
     __syncthreads();
     pdl_trigger();
-    const TwL1<L, double2, E> twp{tw32, t};
+    using TwP = std::conditional_t<FFTPDE_FS_B3TW != 0, TwSmemV<L, E>, TwL1<L, double2, E>>;
+    TwP twp;
+    if constexpr (FFTPDE_FS_B3TW) twp = TwP{tma_smem(twS), t};
+    else twp = TwP{tw32, t};
     for (int j = grp;; j += G::NG) {
         const int64_t tile = blockIdx.x + (int64_t)j * gridDim.x;
         if (tile >= G::NTILES) break;
