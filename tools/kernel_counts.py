@@ -48,8 +48,8 @@ def main():
     acc = collections.defaultdict(lambda: collections.Counter())
     for lid, m in per.items():
         k = kname[lid]
-        cls = ("aa_pass" if "aa_kernel" in k else "col_pass" if "by_kernel" in k else "row_pass" if "bx_kernel" in k
-               else classify(k))
+        cls = ("aa_pass" if "aa_kernel" in k else "col_pass" if "by_kernel" in k or "b3_kernel<1>" in k or "b3_kernel<true>" in k
+               else "row_pass" if "bx_kernel" in k or "b3_kernel<0>" in k or "b3_kernel<false>" in k else classify(k))
         a = acc[cls]
         a["launches"] += 1
         a["dram_bytes"] += m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)

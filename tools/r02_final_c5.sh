@@ -4,7 +4,7 @@ OUT=gpurun_out/${1:-r02o}; mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/smi.txt 2>&1
 timeout 900 python bench.py > $OUT/bench_c5.json 2> $OUT/bench_c5.err; echo "bench exit $?"
 timeout 600 python bench.py --impl reference > $OUT/bench_ref_c5.json 2> $OUT/bench_ref_c5.err; echo "ref exit $?"
-KRE='regex:aa_kernel|line_kernel|by_kernel'
+KRE='regex:aa_kernel|line_kernel|by_kernel|b3_kernel|bx_kernel'
 CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-parity"
 $CMD > $OUT/plain.log 2>&1 && \
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KRE" --csv --log-file $OUT/launches_c5.csv $CMD > $OUT/ncu_launches.log 2>&1; echo "launch list exit $?"
