@@ -594,19 +594,14 @@ cudaError_t tma_wave2_n(void *U, void *V, int64_t nx, int64_t stride, int64_t ba
     if (!tma_map<T>(mu, U, nx, N, batch, stride, 1, L::BOXR, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) ||
         !tma_map<T>(mv, V, nx, N, batch, stride, 1, L::BOXR, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
         return cudaErrorNotSupported;
-#ifndef FFTPDE_WAVE2_PUSH
-#define FFTPDE_WAVE2_PUSH 0
-#endif
-    using LP = TmaWavePushSmem<C, N, EX>;
-    auto k = FFTPDE_WAVE2_PUSH ? tma_wave_push_cols_kernel<T, N, EX, FFTPDE_WAVE2_MINB> : tma_wave2_cols_kernel<T, N, EX, FFTPDE_WAVE2_MINB>;
-    const size_t bytes = FFTPDE_WAVE2_PUSH ? LP::BYTES : L::BYTES;
+    auto k = tma_wave2_cols_kernel<T, N, EX, FFTPDE_WAVE2_MINB>;
     static SmemOptIn<decltype(k)> opt;
-    cudaError_t e = opt(k, bytes);
+    cudaError_t e = opt(k, L::BYTES);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(2 * nx * batch), 1, 1);
     cfg.blockDim = dim3(Shape<N, EX>::TPT, 1, 1);
-    cfg.dynamicSmemBytes = bytes;
+    cfg.dynamicSmemBytes = L::BYTES;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -621,71 +616,12 @@ cudaError_t tma_wave2_n(void *U, void *V, int64_t nx, int64_t stride, int64_t ba
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-// Wave3: the persistent cluster-pair pipeline (tmacols.cuh), complex128 columns of
-// 2048 / 4096 points; grid = the co-resident clusters of two one-CTA-per-SM CTAs.
-#ifndef FFTPDE_WAVE3
-#define FFTPDE_WAVE3 0
-#endif
-static inline bool wave3_enabled()
-{
-    static const bool v = [] { const char *e = std::getenv("FFTPDE_WAVE3"); return e ? std::atoi(e) != 0 : true; }();
-    return v;
-}
-template <int N>
-cudaError_t tma_wave3_n(void *U, void *V, int64_t nx, int64_t stride, int64_t batch, const void *tw,
-                        const OpTables<double> &tab, cudaStream_t st)
-{
-    constexpr int EX = 32;
-    using G = Wave3Geom<double2, N, EX>;
-    if (batch > (int64_t)1 << 31 || nx * batch > (int64_t)1 << 30) return cudaErrorNotSupported;
-    CUtensorMap mu, mv;
-    if (!tma_map<double>(mu, U, nx, N, batch, stride, 1, G::BOXR, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) ||
-        !tma_map<double>(mv, V, nx, N, batch, stride, 1, G::BOXR, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
-        return cudaErrorNotSupported;
-    auto k = tma_wave3_cols_kernel<N, EX>;
-    static SmemOptIn<decltype(k)> opt;
-    cudaError_t e = opt(k, G::BYTES);
-    if (e != cudaSuccess) return e;
-    const int64_t ntiles = nx * batch;
-    cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(G::NT, 1, 1);
-    cfg.dynamicSmemBytes = G::BYTES;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    static std::atomic<int> ncl_cache{0};
-    int ncl = ncl_cache.load(std::memory_order_relaxed);
-    if (ncl == 0) {
-        cfg.gridDim = dim3(2 * (unsigned)sm_count(), 1, 1);
-        e = cudaOccupancyMaxActiveClusters(&ncl, k, &cfg);
-        if (e != cudaSuccess) return e;
-        if (ncl < 1) return cudaErrorNotSupported;
-        ncl_cache.store(ncl, std::memory_order_relaxed);
-        if (std::getenv("FFTPDE_VERBOSE")) std::fprintf(stderr, "fftpde: wave3 N=%d: %d co-resident clusters\n", N, ncl);
-    }
-    cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(ncl, ntiles)), 1, 1);
-    e = cudaLaunchKernelEx(&cfg, k, mu, mv, nx, ntiles, (const double2 *)tw, tab);
-    return e != cudaSuccess ? e : cudaGetLastError();
-}
-
 template <typename T>
 cudaError_t launch_wave_cols(int64_t ny, void *U, void *V, int64_t nx, int64_t stride,
                              int64_t batch, const ColTw &ctw, const OpTables<T> &tab,
                              cudaStream_t st)
 {
     using C = typename cplx_t<T>::type;
-    if constexpr (sizeof(T) == 8 && FFTPDE_WAVE3) {
-        if ((ny == 2048 || ny == 4096) && ctw.tw32 && wave3_enabled()) {
-            const cudaError_t e = ny == 2048 ? tma_wave3_n<2048>(U, V, nx, stride, batch, tw_for<32>(ctw), tab, st)
-                                             : tma_wave3_n<4096>(U, V, nx, stride, batch, tw_for<32>(ctw), tab, st);
-            if (e != cudaErrorNotSupported) return e;
-        }
-    }
     if (sizeof(T) == 8 && (ny == 2048 || ny == 4096) && ctw.tw32) {
         const void *tw = tw_for<FFTPDE_WAVE2_EX>(ctw);
         const cudaError_t e = ny == 2048 ? tma_wave2_n<T, 2048>(U, V, nx, stride, batch, tw, tab, st)

@@ -304,335 +304,4 @@ tma_wave2_cols_kernel(const __grid_constant__ CUtensorMap mu, const __grid_const
 }
 
 
-// ---- Wave2 push: the cluster-pair column pass without cluster barriers per column.
-// As tma_wave2, CTA rank f owns field f of column a; after the forward transforms
-// the pair splits the spectrum by wavenumber half instead of by field: rank 0 keeps
-// b < N/2, rank 1 keeps b >= N/2.  Each CTA pushes the half it does not keep into
-// the partner's receive buffer with st.async (16-byte remote stores that complete on
-// the partner's mbarrier), updates both fields on its half -- U' = C U + S1 V,
-// V' = S2 U + C V -- and pushes the partner's field of its half back into the
-// partner's line buffer.  Every wait is on a local mbarrier whose phase completes
-// when the partner's bytes have landed (complete_tx), so no thread fences at cluster
-// scope and no remote load is in flight when a buffer is reused: the receive buffer
-// is refilled only after the partner has received this CTA's second push, whose data
-// depend on the loads of the receive buffer; the line buffer receives the second push
-// only after the partner received the first, which every thread sends after its
-// forward transform finished with the line.
-template <typename C, int N, int EX> struct TmaWavePushSmem {
-    static constexpr int RAW = Shape<N, EX>::PADDED;
-    static constexpr size_t LINE = ((size_t)RAW * sizeof(C) + 127) / 128 * 128;
-    static constexpr size_t RECV = (size_t)(N / 2) * sizeof(C);
-    static constexpr int BOXR = N < 256 ? N : 256;
-    static constexpr int NBOX = N / BOXR;
-    static constexpr size_t BYTES = LINE + RECV + 128 + 32;
-};
-
-template <typename T, int N, int EX, int MINB>
-__global__ void __launch_bounds__(Shape<N, EX>::TPT, MINB)
-tma_wave_push_cols_kernel(const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mv, int64_t ncols,
-                          const typename cplx_t<T>::type *__restrict__ tw, OpTables<T> tab)
-{
-    using C = typename cplx_t<T>::type;
-    using S = Shape<N, EX>;
-    using L = TmaWavePushSmem<C, N, EX>;
-    constexpr int E = S::E, TPT = S::TPT, H = E / 2;          // element e of thread t is b = t + TPT e
-    static_assert(E % 2 == 0, "the halves b < N/2 and b >= N/2 are e < E/2 and e >= E/2");
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    unsigned char *base = smem_raw + ((128u - (tma_smem(smem_raw) & 127u)) & 127u);
-    C *line = reinterpret_cast<C *>(base);
-    C *recv = reinterpret_cast<C *>(base + L::LINE);
-    const uint32_t mbar = tma_smem(base + L::LINE + L::RECV), m1 = mbar + 8, m2 = mbar + 16;
-    const int t = threadIdx.x;
-    const uint32_t f = cl_rank();                              // field of this CTA; keeps half f
-    const int64_t cid = blockIdx.x / 2;
-    const int64_t bz = cid / ncols;
-    const int64_t a = cid - bz * ncols;
-    const CUtensorMap *map = f ? &mv : &mu;
-    const SyncCTA sync{};
-    if (t == 0) {
-        tma_mbar_init(mbar, 1);
-        tma_mbar_init(m1, 1);
-        tma_mbar_init(m2, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
-    }
-    __syncthreads();
-    cl_arrive_relaxed();                                   // my mbarriers exist (waited on before the first push)
-    pdl_wait();
-    if (t == 0) {
-        tma_mbar_expect(mbar, (uint32_t)(N * sizeof(C)));
-        tma_mbar_expect(m1, (uint32_t)L::RECV);            // the partner's first push
-        tma_mbar_expect(m2, (uint32_t)L::RECV);            // its second
-        const uint32_t d = tma_smem(base);
-#pragma unroll
-        for (int k = 0; k < L::NBOX; ++k) tma_load3(d + k * L::BOXR * (int)sizeof(C), map, (int)(2 * a), k * L::BOXR, (int)bz, mbar);
-    }
-    pdl_trigger();
-    tma_mbar_wait(mbar, 0);
-    C v[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = line[t + TPT * e];
-    __syncthreads();
-    SmemView<C, S::LOGE, 1> sm{line};
-#if FFTPDE_TWPOW
-    const TwL1Pow<N, C, EX> twp{{tw, t}};
-#else
-    const TwL1<N, C, EX> twp{tw, t};
-#endif
-    fft_tw<N, false, EX>(v, sm, t, twp, sync);
-    cl_wait_acquire();                                     // the partner's mbarriers are initialised
-    const uint32_t peer_recv = mapa_rank(tma_smem(recv), f ^ 1u), peer_line = mapa_rank(tma_smem(base), f ^ 1u);
-    const uint32_t peer_m1 = mapa_rank(m1, f ^ 1u), peer_m2 = mapa_rank(m2, f ^ 1u);
-    // first push: the half the partner keeps (rank 0 sends e >= H, rank 1 sends e < H)
-#pragma unroll
-    for (int e = 0; e < E; ++e)
-        if ((e >= H) == (f == 0)) st_async(peer_recv + (uint32_t)((t + TPT * (e % H)) * sizeof(C)), v[e], peer_m1);
-    tma_mbar_wait(m1, 0);
-    const int64_t qa = a <= tab.nfold - a ? a : tab.nfold - a;
-    const T *pC = tab.wC + qa * tab.qpitch, *pS1 = tab.wS1 + qa * tab.qpitch, *pS2 = tab.wS2 + qa * tab.qpitch;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        if ((e < H) != (f == 0)) continue;                 // the half this CTA keeps
-        const int b = t + TPT * e;
-        const int qb = b <= N - b ? b : N - b;
-        const T cc = __ldg(pC + qb), s1 = __ldg(pS1 + qb), s2 = __ldg(pS2 + qb);
-        const C o = recv[t + TPT * (e % H)];               // the partner's field at b
-        const C U = f ? o : v[e], V = f ? v[e] : o;
-        const C Un{cc * U.x + s1 * V.x, cc * U.y + s1 * V.y}, Vn{s2 * U.x + cc * V.x, s2 * U.y + cc * V.y};
-        v[e] = f ? Vn : Un;
-        // second push: the partner's field of this half, into its line buffer
-        st_async(peer_line + (uint32_t)((t + TPT * (e % H)) * sizeof(C)), f ? Un : Vn, peer_m2);
-    }
-    tma_mbar_wait(m2, 0);
-#pragma unroll
-    for (int e = 0; e < E; ++e)
-        if ((e >= H) == (f == 0)) v[e] = line[t + TPT * (e % H)];
-    __syncthreads();                                       // the pushed half is in registers
-    fft_tw<N, true, EX>(v, sm, t, twp, sync);
-#pragma unroll
-    for (int e = 0; e < E; ++e) line[t + TPT * e] = v[e];
-    tma_fence_smem();
-    __syncthreads();
-    if (t == 0) {
-        const uint32_t src = tma_smem(base);
-#pragma unroll
-        for (int k = 0; k < L::NBOX; ++k) tma_store3(map, (int)(2 * a), k * L::BOXR, (int)bz, src + k * L::BOXR * (int)sizeof(C));
-        tma_commit();
-        tma_wait_read0();
-    }
-}
-
-// ---- Wave3: the cluster-pair wave column pass as a persistent pipeline.  One CTA
-// per SM, CTA rank f of the pair owns field f (0: U, 1: V) as in tma_wave2; the
-// CTA is made of two independent 4-warp groups and three column slots.  Column j
-// of the pair's sequence (global column cluster + j * clusters) sits in slot j % 3
-// of both CTAs and is transformed by group j % 2 of both; the group that finished
-// column j stores it and, once the store has read the slot, loads column j + 3
-// there: two columns in the transforms while the third is in flight from HBM, so
-// no group waits for a load once the pipe is full (tma_wave2 spends a fifth of its
-// stall samples on the column's mbarrier).  The pair meets per column, not per
-// CTA: each thread of group g arrives remotely (release.cluster) on the partner's
-// `ready` mbarrier of the slot once its part of the spectrum is in the slot, waits
-// (acquire.cluster) on its own, reads the partner's spectrum over DSMEM for the
-// oscillator update, and arrives on the partner's `freed` mbarrier; the slot is
-// reused for the inverse's exchanges only after its own `freed` completes (the
-// partner's reads of it are done: no write-after-read race).
-#ifndef FFTPDE_WAVE3_SIG1
-#define FFTPDE_WAVE3_SIG1 0     // 1: one elected thread per group signals / waits (after a group barrier)
-#endif
-template <typename C, int N, int EX> struct Wave3Geom {
-    static constexpr int TPT = Shape<N, EX>::TPT;                  // threads per column (a group)
-    static constexpr int NG = 2, NT = NG * TPT, NSLOT = 3;
-    static constexpr int BOXR = N < 256 ? N : 256, NBOX = N / BOXR;
-    static constexpr size_t DENSE = (size_t)N * sizeof(C);
-    static constexpr size_t XCH = (size_t)Shape<N, EX>::PADDED * sizeof(C);
-    static constexpr size_t SLOT = ((DENSE > XCH ? DENSE : XCH) + 1023) / 1024 * 1024;
-    // the middle-stage twiddle blocks staged once per CTA (the last stage's w_N^j
-    // stay in the L1-resident global table, powers by multiplication)
-    static constexpr int TWMID = Shape<N, EX>::TW_LAST_OFF;
-    static constexpr size_t TWB = (size_t)TWMID * sizeof(C);
-    static constexpr size_t BAR = NSLOT * 3 * 8 + NSLOT * 4;      // full / ready / freed mbarriers, issued[]
-    static constexpr size_t BYTES = NSLOT * SLOT + TWB + BAR + 1024;
-};
-
-// middle stages from the shared copy, last stage w_N^j from the global table (L1)
-template <int N, int EMAX> struct TwMidSmemPow {
-    static constexpr bool LAST_POW = true;
-    uint32_t base;
-    const double2 *tw;
-    int t;
-    __device__ __forceinline__ double2 mid(int s, int m) const { return TwSmemV<N, EMAX>{base, t}.mid(s, m); }
-    __device__ __forceinline__ double2 last(int q, int) const
-    {
-        using S = Shape<N, EMAX>;
-        return ldtw(tw + S::TW_LAST_OFF + opaque(t + q * S::TPT) + S::NS_LAST);
-    }
-};
-
-__device__ __forceinline__ void mbar_arrive_remote_release(uint32_t cluster_addr)
-{
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_acquire_cluster(uint32_t mbar, uint32_t parity)
-{
-    asm volatile("{\n\t.reg .pred p;\n"
-                 "W%=:\n\t"
-                 "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-                 "@!p bra W%=;\n}" ::"r"(mbar), "r"(parity) : "memory");
-}
-#ifndef FFTPDE_WAVE3_NA
-#define FFTPDE_WAVE3_NA 1       // propagator rows read without L1 allocation (the CTA's L1 is what smem leaves)
-#endif
-__device__ __forceinline__ double ld_stream(const double *p)
-{
-    double r;
-    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
-    return r;
-}
-struct GroupBar {
-    int id, n;
-    __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-};
-
-template <int N, int EX>
-__global__ void __launch_bounds__(Wave3Geom<double2, N, EX>::NT, 1)
-tma_wave3_cols_kernel(const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mv, int64_t ncols,
-                      int64_t ntiles, const double2 *__restrict__ tw, OpTables<double> tab)
-{
-    using C = double2;
-    using G = Wave3Geom<C, N, EX>;
-    using S = Shape<N, EX>;
-    constexpr int E = S::E, TPT = S::TPT, NS = G::NSLOT;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    unsigned char *base = smem_raw + ((1024u - (tma_smem(smem_raw) & 1023u)) & 1023u);
-    const uint32_t sbase = tma_smem(base);
-    const uint32_t twS = sbase + NS * (uint32_t)G::SLOT;
-    const uint32_t full0 = twS + (uint32_t)G::TWB, ready0 = full0 + 8 * NS, freed0 = ready0 + 8 * NS;
-    volatile int *issued = reinterpret_cast<volatile int *>(base + NS * G::SLOT + G::TWB + 3 * 8 * NS);
-    const uint32_t f = cl_rank();
-    const int64_t cid = blockIdx.x / 2, ncl = gridDim.x / 2;
-    const CUtensorMap *map = f ? &mv : &mu;
-    const int grp = threadIdx.x / TPT, t = threadIdx.x % TPT;
-    const GroupBar gsync{1 + grp, TPT};
-    auto slot_ptr = [&](int s) { return reinterpret_cast<C *>(base + s * G::SLOT); };
-    auto col_of = [&](int64_t q, int &x, int &z) {
-        const int64_t bz = q / ncols;
-        x = (int)(2 * (q - bz * ncols));
-        z = (int)bz;
-    };
-    auto load = [&](int64_t q, int s) {
-        const uint32_t mb = full0 + 8u * s;
-        tma_mbar_expect(mb, (uint32_t)G::DENSE);
-        int x, z;
-        col_of(q, x, z);
-        const uint32_t d = sbase + s * (uint32_t)G::SLOT;
-#pragma unroll
-        for (int k = 0; k < G::NBOX; ++k) tma_load3(d + k * G::BOXR * (int)sizeof(C), map, x, k * G::BOXR, z, mb);
-    };
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NS; ++s) {
-            tma_mbar_init(full0 + 8u * s, 1);
-            tma_mbar_init(ready0 + 8u * s, FFTPDE_WAVE3_SIG1 ? 1 : TPT);
-            tma_mbar_init(freed0 + 8u * s, FFTPDE_WAVE3_SIG1 ? 1 : TPT);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
-    }
-    for (int i = threadIdx.x; i < G::TWMID; i += G::NT) reinterpret_cast<C *>(base + NS * G::SLOT)[i] = tw[i];
-    cl_arrive_release();                 // both CTAs' mbarriers are initialised before any remote arrive
-    cl_wait_acquire();
-    pdl_wait();
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NS; ++s) {
-            const int64_t q = cid + (int64_t)s * ncl;
-            issued[s] = s;
-            if (q < ntiles) load(q, s);
-        }
-    }
-    __syncthreads();
-    pdl_trigger();
-    const TwMidSmemPow<N, EX> twp{twS, tw, t};
-    const uint32_t f_peer = f ^ 1u;
-    for (int j = grp;; j += G::NG) {
-        const int64_t q = cid + (int64_t)j * ncl;
-        if (q >= ntiles) break;
-        const int s = j % NS;
-        const uint32_t ph = (uint32_t)(j / NS) & 1u;
-        C *line = slot_ptr(s);
-        while (issued[s] != j) {}
-        tma_mbar_wait(full0 + 8u * s, ph);
-        C v[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) v[e] = line[t + TPT * e];
-        gsync();                                            // the slot becomes the exchange buffer
-        const SmemView<C, S::LOGE, 1> sm{line};
-        fft_tw<N, false, EX>(v, sm, t, twp, gsync);
-#pragma unroll
-        for (int e = 0; e < E; ++e) line[t + TPT * e] = v[e];
-#if FFTPDE_WAVE3_SIG1
-        gsync();                                            // the group's spectrum is in the slot
-        if (t == 0) {
-            mbar_arrive_remote_release(mapa_rank(ready0 + 8u * s, f_peer));
-            mbar_wait_acquire_cluster(ready0 + 8u * s, ph);
-        }
-        gsync();
-#else
-        mbar_arrive_remote_release(mapa_rank(ready0 + 8u * s, f_peer));   // my part of the spectrum is in the slot
-        mbar_wait_acquire_cluster(ready0 + 8u * s, ph);                    // the partner's spectrum is in its slot
-#endif
-        {
-            const uint32_t peer = mapa_rank(sbase + s * (uint32_t)G::SLOT, f_peer);
-            int x, z;
-            col_of(q, x, z);
-            const int64_t a = x / 2;
-            const int64_t qa = a <= tab.nfold - a ? a : tab.nfold - a;    // |fold(a)|
-            const double *pC = tab.wC + qa * tab.qpitch, *pS = (f ? tab.wS2 : tab.wS1) + qa * tab.qpitch;
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int b = t + TPT * e;
-                const int qb = b <= N - b ? b : N - b;
-#if FFTPDE_WAVE3_NA
-                const double cc = ld_stream(pC + qb), ss = ld_stream(pS + qb);
-#else
-                const double cc = __ldg(pC + qb), ss = __ldg(pS + qb);
-#endif
-                const C o = ld_cluster(peer + (uint32_t)(b * sizeof(C)));
-                // U: C U + S1 V;  V: S2 U + C V
-                v[e] = C{cc * v[e].x + ss * o.x, cc * v[e].y + ss * o.y};
-            }
-        }
-#if FFTPDE_WAVE3_SIG1
-        gsync();                                            // the group is done reading the partner's slot
-        if (t == 0) {
-            mbar_arrive_remote_release(mapa_rank(freed0 + 8u * s, f_peer));
-            mbar_wait_acquire_cluster(freed0 + 8u * s, ph);
-        }
-        gsync();
-#else
-        mbar_arrive_remote_release(mapa_rank(freed0 + 8u * s, f_peer));   // done reading the partner's slot
-        mbar_wait_acquire_cluster(freed0 + 8u * s, ph);                    // the partner is done reading mine
-#endif
-        fft_tw<N, true, EX>(v, sm, t, twp, gsync);
-#pragma unroll
-        for (int e = 0; e < E; ++e) line[t + TPT * e] = v[e];
-        tma_fence_smem();
-        gsync();
-        if (t == 0) {
-            int x, z;
-            col_of(q, x, z);
-            const uint32_t src = sbase + s * (uint32_t)G::SLOT;
-#pragma unroll
-            for (int k = 0; k < G::NBOX; ++k) tma_store3(map, x, k * G::BOXR, z, src + k * G::BOXR * (int)sizeof(C));
-            tma_commit();
-            const int64_t nq = cid + (int64_t)(j + NS) * ncl;
-            tma_wait_read0();                               // the slot is free once the store has read it
-            if (nq < ntiles) load(nq, s);
-            issued[s] = j + NS;
-        }
-    }
-    if (threadIdx.x % TPT == 0) tma_wait0();
-    cl_arrive_release();                 // no CTA leaves while its partner may still signal it
-    cl_wait_acquire();
-}
-
 } // namespace fftpde
