@@ -132,6 +132,30 @@ fftpde_status fftpde_plan_3d_sharded(fftpde_plan *plan, int64_t nx, int64_t ny, 
                                      double Lx, double Ly, double Lz, int device, const void *nccl_unique_id,
                                      int rank, int nranks);
 
+/* 3D pencil plan ("3D extension with pencil decomposition";
+ * the n-D extension of PAPER.md:275, whose per-axis transforms PAPER.md:262-273
+ * apply along x, y and z in turn).  P = pz * py ranks on a pz x py process grid;
+ * rank r = i py + j (i < pz, j < py) owns the x-pencil [nz/pz][ny/py][nx]: planes
+ * [i nz/pz, (i+1) nz/pz), rows [j ny/py, (j+1) ny/py), every x.  Per transform:
+ * x-pass -> all-to-all inside the row group (the py ranks of z-block i) -> the
+ * y-pencil [nz/pz][ny][nx/py] (x-block j) -> y-pass -> all-to-all inside the
+ * column group (the pz ranks of x-block j) -> the z-pencil [nz][ny/pz][nx/py]
+ * (rows [i ny/pz, (i+1) ny/pz) of x-block j) -> z-pass with the multiplier ->
+ * the same back.  Two all-to-alls per 3D transform over sub-groups of sizes py
+ * and pz, so P may exceed nz (the z-slab plan needs P <= nz).
+ * fftpde_forward: x-pencil -> this rank's z-pencil of the spectrum (in != out);
+ * fftpde_inverse: z-pencil -> x-pencil (x 1/(nx ny nz)); fftpde_poisson /
+ * fftpde_diffuse act on x-pencils.  Requires pz | nz, py | ny, py | nx, pz | ny
+ * and (nx/py) * element size a multiple of 16 bytes (else
+ * FFTPDE_ERR_UNSUPPORTED); nccl_unique_id / rank / loopback as for
+ * fftpde_plan_3d_sharded (one NCCL communicator over all P ranks: each group
+ * exchange is a grouped send/recv with the group's ranks).  Loopback: the
+ * caller's buffers hold the P x-pencils (or z-pencils) back to back in rank
+ * order -- not the natural [nz][ny][nx] field. */
+fftpde_status fftpde_plan_3d_pencil(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t nz, fftpde_dtype dtype,
+                                    double Lx, double Ly, double Lz, int device, const void *nccl_unique_id,
+                                    int rank, int pz, int py);
+
 /* 3D plan (the n-D extension): [nz][ny][nx] grids on
  * [0,Lx) x [0,Ly) x [0,Lz), x fastest.  Transforms are sequential 1D passes
  * along x, y and z; the whole-plan calls fftpde_forward / fftpde_inverse /

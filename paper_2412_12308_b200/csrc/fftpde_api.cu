@@ -69,6 +69,13 @@ struct fftpde_plan_s {
     bool nccl_failed = false;                  // an NCCL call of the last exchange did not return ncclSuccess
     ncclComm_t comm = nullptr;
     int64_t R = 0, BW = 0, nzl = 0, slab_elems = 0;
+    // 3D pencil plans (fftpde_plan_3d_pencil): P = Pz x Py ranks, rank r = i Py + j owns
+    // the x-pencil [nzl][nyl][nx] (z-block i, y-block j); the y-pencil [nzl][ny][nxl]
+    // (x-block j) after the row-group exchange; the z-pencil [nz][nyl2][nxl] (y-block i
+    // of ny/Pz) after the column-group exchange
+    bool pencil = false;
+    int Pz = 1, Py = 1;
+    int64_t nyl = 0, nxl = 0, nyl2 = 0;
     size_t o_shA = 0, o_shB = 0, o_shC = 0;
     bool is3d = false;
     // real plans (fftpde_plan_2d_r2c): half spectrum [batch][ny][pitch], pitch = nx/2 + LPP
@@ -609,8 +616,8 @@ template <typename T> struct Passes {
     // rows (the x-pass) of one rank's slab: R rows (2D) or nzl planes of ny rows (3D)
     cudaError_t rows_sh(const void *in, void *out, int inverse)
     {
-        const int64_t nrows = p->is3d ? p->ny : p->R;
-        const int64_t nb = p->is3d ? p->nzl : 1, st = nrows * p->nx;
+        const int64_t nrows = p->pencil ? p->nzl * p->nyl : p->is3d ? p->ny : p->R;
+        const int64_t nb = p->is3d && !p->pencil ? p->nzl : 1, st = nrows * p->nx;
         return launch(p, FFTPDE_KERNEL_ROW, [&] {
             if (p->rowP)
                 return launch_rows2<T>(p->nx, in, out, nullptr, nrows, st, nb, inverse ? ROW_INV : ROW_FWD, rtw(),
@@ -703,9 +710,111 @@ template <typename T> struct Passes {
         }
         return cudaSuccess;
     }
+    // ---- pencils (fftpde_plan_3d_pencil) ----
+    int pi(int r) const { return r / p->Py; }
+    int pj(int r) const { return r % p->Py; }
+    cudaError_t pack_pen(const void *in, void *out, int64_t nrows, int nblocks, int64_t blk_elems, int direction)
+    {
+        ++p->launches;
+        return launch_pack(in, out, nrows, nblocks, blk_elems * (int64_t)elem_cplx(p), direction, p->stream);
+    }
+    // the all-to-all inside a group: kind 0 = the Py ranks of z-block i (row group),
+    // kind 1 = the Pz ranks of x-block j (column group).  Block g of rank r's send
+    // buffer goes to the group's g-th rank, at the position of r within the group.
+    cudaError_t exchange_pen(void *(Passes::*send)(int) const, void *(Passes::*recv)(int) const, int kind)
+    {
+        const int G = kind ? p->Pz : p->Py;
+        const size_t blk = slab_bytes() / (size_t)G;
+        auto peer = [&](int r, int g) { return kind ? g * p->Py + pj(r) : pi(r) * p->Py + g; };
+        auto pos = [&](int r) { return kind ? pi(r) : pj(r); };
+        if (p->loopback) {
+            for (int r = 0; r < p->P; ++r)
+                for (int g = 0; g < G; ++g) {
+                    const int q = peer(r, g);
+                    cudaError_t e = cudaMemcpyAsync((unsigned char *)(this->*recv)(q) + (size_t)pos(r) * blk,
+                                                    (const unsigned char *)(this->*send)(r) + (size_t)g * blk, blk,
+                                                    cudaMemcpyDeviceToDevice, p->stream);
+                    if (e != cudaSuccess) return e;
+                }
+            return cudaSuccess;
+        }
+        const NcclApi &n = nccl();
+        const size_t count = blk / sizeof(T);
+        const ncclDataType_t ty = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+        const unsigned char *sb = (const unsigned char *)(this->*send)(0);
+        unsigned char *rb = (unsigned char *)(this->*recv)(0);
+        ncclResult_t first = n.groupStart();
+        if (first != ncclSuccess) {
+            p->nccl_failed = true;
+            return cudaErrorUnknown;
+        }
+        for (int g = 0; g < G; ++g) {      // the group's g-th rank sends me its block at my position
+            const int q = peer(p->rank, g);
+            const ncclResult_t rs = n.send(sb + (size_t)g * blk, count, ty, q, p->comm, p->stream);
+            if (first == ncclSuccess) first = rs;
+            const ncclResult_t rr = n.recv(rb + (size_t)g * blk, count, ty, q, p->comm, p->stream);
+            if (first == ncclSuccess) first = rr;
+        }
+        const ncclResult_t re = n.groupEnd();
+        if (first == ncclSuccess) first = re;
+        if (first != ncclSuccess) {
+            p->nccl_failed = true;
+            return cudaErrorUnknown;
+        }
+        return cudaGetLastError();
+    }
+    // x-pencil in -> z-pencils shC: x-pass, pack by x-block, row-group exchange,
+    // unpack to [nzl][ny][nxl], y-pass, pack by y-block of ny/Pz, column-group exchange
+    cudaError_t to_zpencils(const void *in)
+    {
+        const int64_t nzl = p->nzl, nyl = p->nyl, nxl = p->nxl, nyl2 = p->nyl2;
+        cudaError_t e = each([&](int i) { return rows_sh(at(in, i), shA(i), 0); });
+        if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shA(i), shB(i), nzl * nyl, p->Py, nxl, 0); });
+        if (e == cudaSuccess) e = exchange_pen(&Passes::shB, &Passes::shC, 0);
+        if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shC(i), shA(i), nzl, p->Py, nyl * nxl, 1); });
+        if (e == cudaSuccess) e = each([&](int i) { return ypass_pen(shA(i), shB(i), COL_FWD); });
+        if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shB(i), shA(i), nzl, p->Pz, nyl2 * nxl, 0); });
+        if (e == cudaSuccess) e = exchange_pen(&Passes::shA, &Passes::shC, 1);
+        return e;
+    }
+    // z-pencils shC -> x-pencil out: the reverse, with the unscaled inverse y- and x-passes
+    cudaError_t from_zpencils(void *out)
+    {
+        const int64_t nzl = p->nzl, nyl = p->nyl, nxl = p->nxl, nyl2 = p->nyl2;
+        cudaError_t e = exchange_pen(&Passes::shC, &Passes::shA, 1);
+        if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shA(i), shB(i), nzl, p->Pz, nyl2 * nxl, 1); });
+        if (e == cudaSuccess) e = each([&](int i) { return ypass_pen(shB(i), shA(i), COL_INV); });
+        if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shA(i), shB(i), nzl, p->Py, nyl * nxl, 0); });
+        if (e == cudaSuccess) e = exchange_pen(&Passes::shB, &Passes::shC, 0);
+        if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shC(i), shA(i), nzl * nyl, p->Py, nxl, 1); });
+        if (e == cudaSuccess) e = each([&](int i) { return rows_sh(shA(i), at(out, i), 1); });
+        return e;
+    }
+    // y-pass of a y-pencil [nzl][ny][nxl]: nxl columns per plane (forward or unscaled inverse)
+    cudaError_t ypass_pen(const void *in, void *out, int op)
+    {
+        return launch(p, FFTPDE_KERNEL_COL, [&] {
+            return launch_cols<T>(p->ny, in, out, p->nxl, p->ny * p->nxl, p->nzl, op, ctw(), tables3<false>((T)1),
+                                  p->stream);
+        });
+    }
+    // z-pass of z-pencil r: lines l = yl2 nxl + xl of length nz; the plan's (x, y)
+    // line tables are stored in pencil order (rank-major), so rank r's lines start at r nyl2 nxl
+    cudaError_t zpass_pen(const void *in, void *out, int op, int r)
+    {
+        OpTables<T> t = tables3<true>(scale3());
+        const int64_t nl = p->nyl2 * p->nxl;
+        t.kx2 += r * nl;
+        t.ex += r * nl;
+        const ColTw ztw{p->ws + p->o_twz, nullptr, nullptr, nullptr, p->ws + p->o_twz8};
+        return launch(p, FFTPDE_KERNEL_COL, [&] {
+            return launch_cols<T>(p->nz, in, out, nl, p->nz * nl, 1, op, ztw, t, p->stream);
+        });
+    }
     // slab in -> slabs shC (2D: column slabs [ny][BW] of the x-spectrum; 3D: y-slabs [nz][R][nx] of the xy-spectrum)
     cudaError_t to_columns(const void *in)
     {
+        if (p->pencil) return to_zpencils(in);
         cudaError_t e = each([&](int i) { return rows_sh(at(in, i), shA(i), 0); });
         if (p->is3d) {
             if (e == cudaSuccess) e = each([&](int i) { return ypass_sh(shA(i), shB(i), COL_FWD); });
@@ -720,6 +829,7 @@ template <typename T> struct Passes {
     // slabs shC -> slab out (inverse x-pass, and for 3D the inverse y-pass first)
     cudaError_t from_columns(void *out)
     {
+        if (p->pencil) return from_zpencils(out);
         cudaError_t e = exchange(&Passes::shC, &Passes::shB);
         if (e == cudaSuccess) e = each([&](int i) { return pack_sh(shB(i), shA(i), 1); });
         if (p->is3d) {
@@ -733,6 +843,7 @@ template <typename T> struct Passes {
     cudaError_t colpass_sh(const void *in, void *out, int op)
     {
         return each([&](int i) {
+            if (p->pencil) return zpass_pen(at(in, i), at(out, i), op, rk(i));
             return p->is3d ? zpass_sh(at(in, i), at(out, i), op, rk(i)) : cols_sh(at(in, i), at(out, i), op, rk(i));
         });
     }
@@ -1883,6 +1994,43 @@ fftpde_status fftpde_plan_3d_sharded(fftpde_plan *plan, int64_t nx, int64_t ny, 
     p->R = ny / nranks;
     p->nzl = nz / nranks;
     s = finish_sharded(p, nranks, rank, nccl_unique_id, p->nzl * ny * nx);
+    return s == FFTPDE_OK ? s : fail(s);
+}
+
+fftpde_status fftpde_plan_3d_pencil(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t nz, fftpde_dtype dtype,
+                                    double Lx, double Ly, double Lz, int device, const void *nccl_unique_id,
+                                    int rank, int pz, int py)
+{
+    if (!plan) return FFTPDE_ERR_INVALID_ARG;
+    *plan = nullptr;
+    if (pz < 1 || py < 1 || pz > 4096 || py > 4096) return FFTPDE_ERR_INVALID_ARG;
+    const int nranks = pz * py;
+    if (!sharded_args_ok(nccl_unique_id, rank, nranks)) return FFTPDE_ERR_INVALID_ARG;
+    fftpde_status s = fftpde_plan_3d(plan, nx, ny, nz, dtype, Lx, Ly, Lz, device);
+    if (s != FFTPDE_OK) return s;
+    fftpde_plan p = *plan;
+    auto fail = [&](fftpde_status st) { fftpde_destroy(p); *plan = nullptr; return st; };
+    const int64_t ec = (int64_t)elem_cplx(p);
+    // every block the packs move is a whole number of 16-byte vectors
+    if (nz % pz || ny % py || nx % py || ny % pz || ((nx / py) * ec) % 16) return fail(FFTPDE_ERR_UNSUPPORTED);
+    p->pencil = true;
+    p->Pz = pz;
+    p->Py = py;
+    p->nzl = nz / pz;
+    p->nyl = ny / py;
+    p->nxl = nx / py;
+    p->nyl2 = ny / pz;
+    // the z-pass line tables in pencil order: rank r = i py + j, line yl2 nxl + xl is the
+    // global line (x, y) = (j nxl + xl, i nyl2 + yl2); exy (diffusion) is derived from it
+    std::vector<double> k((size_t)(nx * ny));
+    for (int r = 0; r < nranks; ++r) {
+        const int64_t i = r / py, j = r % py;
+        for (int64_t yl = 0; yl < p->nyl2; ++yl)
+            for (int64_t xl = 0; xl < p->nxl; ++xl)
+                k[(size_t)((r * p->nyl2 + yl) * p->nxl + xl)] = p->kxy2[(size_t)((i * p->nyl2 + yl) * nx + j * p->nxl + xl)];
+    }
+    p->kxy2.swap(k);
+    s = finish_sharded(p, nranks, rank, nccl_unique_id, p->nzl * p->nyl * nx);
     return s == FFTPDE_OK ? s : fail(s);
 }
 

@@ -32,7 +32,7 @@ EXPORTS = [
     "fftpde_plan_2d", "fftpde_workspace_size", "fftpde_set_workspace", "fftpde_set_stream",
     "fftpde_destroy", "fftpde_status_string", "fftpde_launch_count",
     "fftpde_set_profiling", "fftpde_read_profile", "fftpde_nccl_unique_id", "fftpde_plan_2d_sharded",
-    "fftpde_plan_3d_sharded",
+    "fftpde_plan_3d_sharded", "fftpde_plan_3d_pencil",
     "fftpde_forward", "fftpde_inverse", "fftpde_poisson", "fftpde_diffuse", "fftpde_wave_step",
     "fftpde_forward_batched", "fftpde_inverse_batched", "fftpde_poisson_batched",
     "fftpde_diffuse_batched", "fftpde_wave_step_batched",
@@ -97,6 +97,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fftpde_nccl_unique_id": (st, [p]),
         "fftpde_plan_2d_sharded": (st, [ctypes.POINTER(p), i64, i64, u, dbl, dbl, u, p, u, u]),
         "fftpde_plan_3d_sharded": (st, [ctypes.POINTER(p), i64, i64, i64, u, dbl, dbl, dbl, u, p, u, u]),
+        "fftpde_plan_3d_pencil": (st, [ctypes.POINTER(p), i64, i64, i64, u, dbl, dbl, dbl, u, p, u, u, u]),
         "fftpde_peer_transpose": (st, [p, p, ctypes.POINTER(p), u, u, i64, i64, u]),
         "fftpde_rows_to_peers": (st, [p, p, ctypes.POINTER(p), u, u, i64, u, dbl, dbl]),
         "fftpde_cols_to_peers": (st, [p, p, ctypes.POINTER(p), u, u, i64, u, dbl, dbl]),
@@ -557,6 +558,30 @@ class ShardedPlan3D(_Sharded):
         self.R, self.nzl = self.ny // self.P, self.nz // self.P
         self.phys_shape = (self.nz, self.ny, self.nx) if self.loopback else (self.nzl, self.ny, self.nx)
         self.spec_shape = self._lb((self.nz, self.R, self.nx))
+
+
+class PencilPlan3D(_Sharded):
+    """The pencil decomposition of an nz x ny x nx volume over a pz x py process
+    grid (fftpde_plan_3d_pencil): rank r = i py + j holds the
+    x-pencil [nz/pz, ny/py, nx] of z-block i and y-block j (``phys_shape``); its
+    spectrum is the z-pencil [nz, ny/pz, nx/py] (``spec_shape``).  Two all-to-alls
+    per transform, inside the row group (py ranks) and the column group (pz ranks).
+    ``loopback=True`` emulates the pz*py ranks in this process: buffers are
+    [P, ...] stacks of pencils in rank order."""
+
+    def __init__(self, nx: int, ny: int, nz: int, pz: int, py: int, dtype=torch.complex128, Lx: float = 1.0,
+                 Ly: float = 1.0, Lz: float = 1.0, device=None, group=None, loopback: bool = False):
+        self.nx, self.ny, self.nz, self.pz, self.py = int(nx), int(ny), int(nz), int(pz), int(py)
+        self.Lx, self.Ly, self.Lz = float(Lx), float(Ly), float(Lz)
+
+        def make(h, uid, rank, P):
+            if P != self.pz * self.py:
+                raise ValueError(f"pencil grid {self.pz} x {self.py} needs {self.pz * self.py} ranks, have {P}")
+            return self.lib.fftpde_plan_3d_pencil(ctypes.byref(h), self.nx, self.ny, self.nz, _DT[dtype], self.Lx,
+                                                  self.Ly, self.Lz, self.device.index, uid, rank, self.pz, self.py)
+        self._setup(dtype, device, group, self.pz * self.py if loopback else 0, make)
+        self.phys_shape = self._lb((self.nz // self.pz, self.ny // self.py, self.nx))
+        self.spec_shape = self._lb((self.nz, self.ny // self.pz, self.nx // self.py))
 
 
 class Plan3D(Plan):

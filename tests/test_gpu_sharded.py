@@ -263,3 +263,80 @@ def test_rows_to_peers_errors():
         pl.rows_to_peers(x, ptrs, 4, 16, F.ROWS_FWD)      # rank out of range
     with pytest.raises(F.FFTPDEError):
         pl.rows_to_peers(x, ptrs, 0, 16, 7)               # unknown op
+
+
+# ---- 3D pencil decomposition (fftpde_plan_3d_pencil) ----------
+def to_xpencils(x, pz, py):
+    # [nz][ny][nx] -> [P][nz/pz][ny/py][nx], rank r = i py + j: z-block i, y-block j
+    nz, ny, nx = x.shape
+    return np.ascontiguousarray(x.reshape(pz, nz // pz, py, ny // py, nx).transpose(0, 2, 1, 3, 4)
+                                .reshape(pz * py, nz // pz, ny // py, nx))
+
+
+def from_xpencils(xp, pz, py):
+    P, nzl, nyl, nx = xp.shape
+    return xp.reshape(pz, py, nzl, nyl, nx).transpose(0, 2, 1, 3, 4).reshape(pz * nzl, py * nyl, nx)
+
+
+def from_zpencils(zp, pz, py):
+    # [P][nz][ny/pz][nx/py] (rank i py + j: y-block i of ny/pz, x-block j) -> [nz][ny][nx]
+    P, nz, nyl2, nxl = zp.shape
+    return zp.reshape(pz, py, nz, nyl2, nxl).transpose(2, 0, 3, 1, 4).reshape(nz, pz * nyl2, py * nxl)
+
+
+@pytest.mark.parametrize("pz,py", [(2, 2), (2, 4), (4, 2), (1, 4), (4, 1), (8, 2)])
+@pytest.mark.parametrize("shape,L", [((8, 32, 64), (1.0, 2.0, 0.5)), ((16, 64, 32), (1.0, 1.0, 1.0))])
+def test_pencil_3d_vs_oracle(pz, py, shape, L):
+    nz, ny, nx = shape
+    x = rand3(shape, 331)
+    p = F.PencilPlan3D(nx, ny, nz, pz, py, Lx=L[0], Ly=L[1], Lz=L[2], loopback=True)
+    xp = torch.from_numpy(to_xpencils(x, pz, py)).cuda()
+    X = p.forward(xp)
+    assert tuple(X.shape) == (pz * py, nz, ny // pz, nx // py)
+    assert rel(from_zpencils(X.cpu().numpy(), pz, py), O.fft3(x)) <= 1e-12
+    assert rel(from_xpencils(p.inverse(X).cpu().numpy(), pz, py), x) <= 1e-12
+    assert rel(from_xpencils(p.poisson(xp).cpu().numpy(), pz, py), O.poisson3(x, *L)) <= 1e-12
+    u = p.diffuse(xp, 1e-3, 0.01, 3).cpu().numpy()
+    assert rel(from_xpencils(u, pz, py), O.diffuse3(x, 1e-3, 0.01, 3, *L)) <= 1e-12
+
+
+def test_pencil_more_ranks_than_planes_c64():
+    # P = 16 > nz = 8: beyond the z-slab plan (P <= nz); complex64 at 1e-5
+    nz, ny, nx = 8, 64, 128
+    x = rand3((nz, ny, nx), 332)
+    with pytest.raises(F.FFTPDEError):
+        F.ShardedPlan3D(nx, ny, nz, dtype=torch.complex64, loopback=16)
+    p = F.PencilPlan3D(nx, ny, nz, 2, 8, dtype=torch.complex64, loopback=True)
+    x64 = x.astype(np.complex64)
+    xp = torch.from_numpy(to_xpencils(x64, 2, 8)).cuda()
+    ref = O.poisson3(x64.astype(np.complex128))
+    assert rel(from_xpencils(p.poisson(xp).cpu().numpy(), 2, 8), ref) <= 1e-5
+
+
+def test_pencil_matches_plan3d_and_errors():
+    nz, ny, nx = 16, 32, 32
+    x = rand3((nz, ny, nx), 333)
+    p = F.PencilPlan3D(nx, ny, nz, 4, 2, loopback=True)
+    ref = F.Plan3D(nx, ny, nz).diffuse(torch.from_numpy(x).cuda(), 1e-3, 0.01, 2).cpu().numpy()
+    u = p.diffuse(torch.from_numpy(to_xpencils(x, 4, 2)).cuda(), 1e-3, 0.01, 2).cpu().numpy()
+    assert rel(from_xpencils(u, 4, 2), ref) <= 1e-14
+    with pytest.raises(F.FFTPDEError) as e:
+        F.PencilPlan3D(32, 32, 16, 32, 1, loopback=True)        # pz does not divide nz
+    assert e.value.status == F.ERR_UNSUPPORTED
+    with pytest.raises(F.FFTPDEError) as e:
+        F.PencilPlan3D(16, 64, 16, 2, 16, dtype=torch.complex64, loopback=True)   # nx / py = one 8-byte element
+    assert e.value.status == F.ERR_UNSUPPORTED
+    with pytest.raises(ValueError):
+        F.PencilPlan3D(32, 32, 16, 2, 2)                        # no process group: P = 1 != 4
+
+
+def test_pencil_nccl_p1_vs_oracle():
+    # the NCCL branch of the group exchanges (grouped send/recv to itself) at pz = py = 1
+    nz, ny, nx = 16, 32, 64
+    x = rand3((nz, ny, nx), 334)
+    p = F.PencilPlan3D(nx, ny, nz, 1, 1, Lx=1.0, Ly=2.0, Lz=0.5)
+    xd = torch.from_numpy(x).cuda()
+    X = p.forward(xd)
+    assert rel(X.cpu().numpy(), O.fft3(x)) <= 1e-12
+    assert rel(p.inverse(X).cpu().numpy(), x) <= 1e-12
+    assert rel(p.poisson(xd).cpu().numpy(), O.poisson3(x, 1.0, 2.0, 0.5)) <= 1e-12
