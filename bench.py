@@ -84,6 +84,9 @@ def parse_args():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="c5: use the slab-decomposed path even on one GPU (P = 1 process group)")
+    ap.add_argument("--pencil", default=None, metavar="PZxPY",
+                    help="3D workloads: the pencil decomposition on a PZ x PY process grid (PZ*PY = --gpus; "
+                         "fftpde_plan_3d_pencil) instead of z-slabs")
     ap.add_argument("--exchange", default="fused", choices=["fused", "nccl", "peer", "lib"],
                     help="sharded c5: exchanges fused into the row / column passes (peer stores into torch "
                          "symmetric memory, default), pack + NCCL all-to-all, a separate peer-store "
@@ -903,9 +906,20 @@ def sharded3d_native(args, wl, world, rank, local):
     import torch
     from paper_2412_12308_b200 import fftpde as F
     host = make_inputs(wl)[0]
-    nzl = wl.nz // world
-    slab = torch.from_numpy(host[rank * nzl:(rank + 1) * nzl].copy()).cuda()
-    plan = F.ShardedPlan3D(wl.nx, wl.ny, wl.nz, dtype=torch.complex128, Lx=wl.Lx, Ly=wl.Ly)
+    if args.pencil:
+        pz, py = (int(v) for v in args.pencil.lower().split("x"))
+        if pz * py != world:
+            raise SystemExit(f"--pencil {args.pencil}: {pz * py} ranks, --gpus {world}")
+        i, j = rank // py, rank % py
+        nzl, nyl = wl.nz // pz, wl.ny // py
+        slab = torch.from_numpy(host[i * nzl:(i + 1) * nzl, j * nyl:(j + 1) * nyl].copy()).cuda()
+        plan = F.PencilPlan3D(wl.nx, wl.ny, wl.nz, pz, py, dtype=torch.complex128, Lx=wl.Lx, Ly=wl.Ly)
+        layout = f"pencils {pz}x{py} (two group all-to-alls per transform inside libfftpde, fftpde_plan_3d_pencil)"
+    else:
+        nzl = wl.nz // world
+        slab = torch.from_numpy(host[rank * nzl:(rank + 1) * nzl].copy()).cuda()
+        plan = F.ShardedPlan3D(wl.nx, wl.ny, wl.nz, dtype=torch.complex128, Lx=wl.Lx, Ly=wl.Ly)
+        layout = f"z-slab x{world} (NCCL all-to-all inside libfftpde, fftpde_plan_3d_sharded)"
     out = torch.empty_like(slab)
 
     def body():
@@ -934,7 +948,7 @@ def sharded3d_native(args, wl, world, rank, local):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded 3D Gaussians)",
         "config": {**workload_config(wl, world),
-                   "parallelism": f"z-slab x{world} (NCCL all-to-all inside libfftpde, fftpde_plan_3d_sharded)",
+                   "parallelism": layout,
                    "l2": "256 MiB buffer zeroed between timed steps"},
         "e2e": None, "cpu_baseline": None, "clocks": clocks, "parity": None,
         "roofline": roofline, "gpu_launches": launches,
@@ -1117,19 +1131,19 @@ def main():
     import torch
     world, rank, local = dist_setup()
     assert world == args.gpus, (world, args.gpus)
-    if args.sharded and world == 1:
+    if (args.sharded or args.pencil) and world == 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{free_port()}", rank=0, world_size=1,
                                 device_id=torch.device("cuda", 0))
     if wl.name.startswith("c5") and (world > 1 or args.sharded):
         line = sharded_native(args, wl, world, rank, local)
-    elif wl.nz > 1 and (world > 1 or args.sharded):
+    elif wl.nz > 1 and (world > 1 or args.sharded or args.pencil):
         line = sharded3d_native(args, wl, world, rank, local)
     else:
         line = native(args, wl, world, rank, local)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1 or args.sharded:
+    if world > 1 or args.sharded or args.pencil:
         import torch.distributed as dist
         dist.destroy_process_group()
 
