@@ -122,7 +122,7 @@ static void line_var(const void *in, void *out, void *out2, long nx, long ny, lo
     const long grid = batch * a.groups;
     const double fields = OP == LN_MID ? 3.0 : 2.0;
     const double bytes = fields * (double)nx * ny * batch * sizeof(C);
-    timeit([&] { k<<<(unsigned)grid, threads, L::BYTES, g_stream>>>((const C *)in, (C *)out, a, (const C *)tw, tab); },
+    timeit([&] { k<<<(unsigned)grid, threads, L::BYTES, g_stream>>>((const C *)in, (C *)out, a, (const C *)tw, tab, PeerOut{}); },
            name, bytes, occ, grid);
 }
 
@@ -225,7 +225,7 @@ static void pipe_ref(const void *in, void *out, void *out2, long nx, long ny, lo
     if (grid > a.ntiles) grid = a.ntiles;
     const double fields = OP == PIPE_MID ? 3.0 : 2.0;
     const double bytes = fields * (double)nx * ny * batch * sizeof(C);
-    timeit([&] { k<<<(unsigned)grid, threads, SMB, g_stream>>>((const C *)in, (C *)out, a, (const C *)tw, tab); }, name,
+    timeit([&] { k<<<(unsigned)grid, threads, SMB, g_stream>>>((const C *)in, (C *)out, a, (const C *)tw, tab, PeerOut{}); }, name,
            bytes, occ, grid);
 }
 
@@ -314,6 +314,11 @@ int main(int argc, char **argv)
         line_var<D, 4096, 16, 1, false, LN_MID, 1>(A, B, Cb, 4096, 4096, 1, t16, tab, "c3 rowsMID");
         line_var<D, 4096, 16, 1, false, LN_MID, 2>(A, B, Cb, 4096, 4096, 1, t16, tab, "c3 rowsMID");
         line_var<D, 4096, 16, 1, false, LN_MID, 3>(A, B, Cb, 4096, 4096, 1, t16, tab, "c3 rowsMID");
+        {   // radix 32: one 128-thread CTA per row (round 2)
+            void *t32 = upload_tw<double2>(4096, 32);
+            line_var<D, 4096, 32, 1, false, LN_MID, 1>(A, B, Cb, 4096, 4096, 1, t32, tab, "c3 rowsMID");
+            line_var<D, 4096, 32, 1, false, LN_MID, 2>(A, B, Cb, 4096, 4096, 1, t32, tab, "c3 rowsMID");
+        }
         line_var<D, 4096, 8, 1, false, LN_MID, 1>(A, B, Cb, 4096, 4096, 1, t8, tab, "c3 rowsMID");
         line_var<D, 4096, 8, 1, false, LN_MID, 2>(A, B, Cb, 4096, 4096, 1, t8, tab, "c3 rowsMID");
         line_var<D, 4096, 8, 1, false, LN_MID, 3>(A, B, Cb, 4096, 4096, 1, t8, tab, "c3 rowsMID");
