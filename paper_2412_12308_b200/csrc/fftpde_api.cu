@@ -768,10 +768,15 @@ template <typename T> struct Passes {
     cudaError_t to_zpencils(const void *in)
     {
         const int64_t nzl = p->nzl, nyl = p->nyl, nxl = p->nxl, nyl2 = p->nyl2;
+        // a group of one rank exchanges nothing: py = 1 makes the x-pencil the
+        // y-pencil, pz = 1 the y-pencil the z-pencil (no pack, no copy)
         cudaError_t e = each([&](int i) { return rows_sh(at(in, i), shA(i), 0); });
-        if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shA(i), shB(i), nzl * nyl, p->Py, nxl, 0); });
-        if (e == cudaSuccess) e = exchange_pen(&Passes::shB, &Passes::shC, 0);
-        if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shC(i), shA(i), nzl, p->Py, nyl * nxl, 1); });
+        if (p->Py > 1) {
+            if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shA(i), shB(i), nzl * nyl, p->Py, nxl, 0); });
+            if (e == cudaSuccess) e = exchange_pen(&Passes::shB, &Passes::shC, 0);
+            if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shC(i), shA(i), nzl, p->Py, nyl * nxl, 1); });
+        }
+        if (p->Pz == 1) return e == cudaSuccess ? each([&](int i) { return ypass_pen(shA(i), shC(i), COL_FWD); }) : e;
         if (e == cudaSuccess) e = each([&](int i) { return ypass_pen(shA(i), shB(i), COL_FWD); });
         if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shB(i), shA(i), nzl, p->Pz, nyl2 * nxl, 0); });
         if (e == cudaSuccess) e = exchange_pen(&Passes::shA, &Passes::shC, 1);
@@ -781,12 +786,19 @@ template <typename T> struct Passes {
     cudaError_t from_zpencils(void *out)
     {
         const int64_t nzl = p->nzl, nyl = p->nyl, nxl = p->nxl, nyl2 = p->nyl2;
-        cudaError_t e = exchange_pen(&Passes::shC, &Passes::shA, 1);
-        if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shA(i), shB(i), nzl, p->Pz, nyl2 * nxl, 1); });
-        if (e == cudaSuccess) e = each([&](int i) { return ypass_pen(shB(i), shA(i), COL_INV); });
-        if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shA(i), shB(i), nzl, p->Py, nyl * nxl, 0); });
-        if (e == cudaSuccess) e = exchange_pen(&Passes::shB, &Passes::shC, 0);
-        if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shC(i), shA(i), nzl * nyl, p->Py, nxl, 1); });
+        cudaError_t e = cudaSuccess;
+        if (p->Pz > 1) {
+            e = exchange_pen(&Passes::shC, &Passes::shA, 1);
+            if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shA(i), shB(i), nzl, p->Pz, nyl2 * nxl, 1); });
+            if (e == cudaSuccess) e = each([&](int i) { return ypass_pen(shB(i), shA(i), COL_INV); });
+        } else {
+            e = each([&](int i) { return ypass_pen(shC(i), shA(i), COL_INV); });
+        }
+        if (p->Py > 1) {
+            if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shA(i), shB(i), nzl, p->Py, nyl * nxl, 0); });
+            if (e == cudaSuccess) e = exchange_pen(&Passes::shB, &Passes::shC, 0);
+            if (e == cudaSuccess) e = each([&](int i) { return pack_pen(shC(i), shA(i), nzl * nyl, p->Py, nxl, 1); });
+        }
         if (e == cudaSuccess) e = each([&](int i) { return rows_sh(shA(i), at(out, i), 1); });
         return e;
     }
