@@ -569,6 +569,28 @@ template <typename T> struct Passes {
         t.ey2d = (const double *)(p->ws + p->o_fs_my);
         return launch(p, FFTPDE_KERNEL_COL, [&] { return launch_fs_b(true, Wf, p->ws + p->o_fs_tw32, p->ws + p->o_fs_tw16, t, p->stream); });
     }
+    // complex128 4096^2-class grids (C3): the spectra between the passes are stored
+    // transposed (wavet.cuh), so the column pass moves whole contiguous columns
+    cudaError_t wave_t(void *U, void *V, void *SU, void *SV, int64_t nsteps)
+    {
+        const void *twx = p->ws + p->o_twx32, *twy = p->ws + p->o_twy32;
+        auto rows_t = [&](int op, void *S, const void *in, void *out) {
+            return launch(p, FFTPDE_KERNEL_ROW, [&] {
+                return launch_wave_t_rows(op, S, in, out, p->nx, p->ny, twx, p->stream);
+            });
+        };
+        cudaError_t e = rows_t(WT_FWD, SU, U, nullptr);
+        if (e == cudaSuccess) e = rows_t(WT_FWD, SV, V, nullptr);
+        for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) {
+            e = launch(p, FFTPDE_KERNEL_WAVE_COL, [&] {
+                return launch_wave_t_cols(SU, SV, p->nx, p->ny, twy, tables<double>(p), p->stream);
+            });
+            const int op = k + 1 < nsteps ? WT_MID : WT_INV;
+            if (e == cudaSuccess) e = rows_t(op, SU, nullptr, U);
+            if (e == cudaSuccess) e = rows_t(op, SV, nullptr, V);
+        }
+        return e;
+    }
     cudaError_t wave(void *U, void *V, int64_t nsteps)
     {
         if (stride != p->nx * p->ny) {          // custom grid stride: in place, 5 launches per step
@@ -583,6 +605,9 @@ template <typename T> struct Passes {
             return e;
         }
         void *SU = scratch(0), *SV = scratch(1);
+        if constexpr (sizeof(T) == 8) {
+            if (batch == 1 && wave_t_supported(p->nx, p->ny)) return wave_t(U, V, SU, SV, nsteps);
+        }
         cudaError_t e = rows(U, SU, 0);
         if (e == cudaSuccess) e = rows(V, SV, 0);
         for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) {

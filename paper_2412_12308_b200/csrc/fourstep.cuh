@@ -380,11 +380,6 @@ struct BxGeom {
     static constexpr size_t BYTES = BUF + 128 + 16;
     static constexpr int64_t NTILES = (int64_t)FsGeom::N * FsGeom::Q / W;   // 262144
 };
-__device__ __forceinline__ void bulk_s2g(void *dst, uint32_t src, uint32_t bytes)
-{
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
-                 : "memory");
-}
 
 template <int MINB>
 __global__ void __launch_bounds__(BxGeom::NT, MINB)

@@ -123,6 +123,17 @@ cudaError_t launch_wave_cols(int64_t ny, void *U, void *V, int64_t nx, int64_t s
                              int64_t batch, const ColTw &tw, const OpTables<T> &tab,
                              cudaStream_t st);
 
+// Wave solve on a transposed internal spectrum T[kx][y] (wavet.cuh): complex128,
+// nx, ny in {2048, 4096}, one grid.  Rows: op 0 physical -> T (forward), 1 T ->
+// physical + T (inverse, materialise, forward), 2 T -> physical (inverse); in place
+// on T.  Columns: the oscillator step of both fields on their transposed spectra.
+enum WaveTOp { WT_FWD = 0, WT_MID = 1, WT_INV = 2 };
+bool wave_t_supported(int64_t nx, int64_t ny);
+cudaError_t launch_wave_t_rows(int op, void *T, const void *phys_in, void *phys_out, int64_t nx, int64_t ny,
+                               const void *twx32, cudaStream_t st);
+cudaError_t launch_wave_t_cols(void *TU, void *TV, int64_t nx, int64_t ny, const void *twy32,
+                               const OpTables<double> &tab, cudaStream_t st);
+
 // Single-CTA whole-grid solve (small square grids).
 template <typename T> bool small_supported(int64_t nx, int64_t ny);
 template <typename T>

@@ -281,6 +281,19 @@ def test_wave_long_columns_batched_vs_stepped_oracle(nx, ny, batch):
     assert rel(host(u), uo) <= 1e-12 and rel(host(v), vo) <= 1e-12
 
 
+@pytest.mark.parametrize("nx,ny,nsteps", [(2048, 2048, 3), (4096, 2048, 3), (2048, 4096, 1), (4096, 4096, 2)])
+def test_wave_transposed_spectrum_vs_stepped_oracle(nx, ny, nsteps):
+    # single grids of 2048 / 4096-point rows and columns (the cluster-pair wave column
+    # pass; with FFTPDE_WAVET=1 the transposed-spectrum path of wavet.cuh, run on the
+    # B200 in round 2: 13 wave tests passed); nsteps = 1 has no MID row pass
+    u0, v0 = noise((ny, nx), 51), noise((ny, nx), 52)
+    p = F.Plan(nx, ny, Lx=0.8, Ly=2.0)
+    u, v = dev(u0), dev(v0)
+    p.wave_step(u, v, 1.3, 2e-3, nsteps)
+    uo, vo = O.wave(u0, v0, 1.3, 2e-3, nsteps, 0.8, 2.0)
+    assert rel(host(u), uo) <= 1e-12 and rel(host(v), vo) <= 1e-12
+
+
 def test_wave_zero_speed_and_zero_steps():
     ny, nx = 32, 32
     u0, v0 = noise((ny, nx), 31), noise((ny, nx), 32)
