@@ -5,6 +5,7 @@ BASELINE.json north_star's: 1e-12 for complex128, 1e-5 for complex64 (the
 complex64 input is upcast exactly for the oracle).  Needs a CUDA device.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -440,3 +441,30 @@ def test_c5_full_size_separable_rank2_vs_oracle_every_point(steps):
     ref = torch.outer(t(Dg1), t(Df1)) + torch.outer(t(Dg2), t(Df2))
     err = (torch.linalg.vector_norm(u - ref) / torch.linalg.vector_norm(ref)).item()
     assert err <= 1e-12, err
+
+
+def test_wave_transposed_spectrum_path_subprocess():
+    # the opt-in transposed-spectrum wave path (wavet.cuh, FFTPDE_WAVET=1 is read once
+    # per process): a fresh interpreter runs 2048^2 for 3 steps (first-step FWD, one MID,
+    # last-step INV row passes) against the stepped oracle
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch\n"
+        "from oracle import oracle as O\n"
+        "from paper_2412_12308_b200 import fftpde as F\n"
+        "rng = np.random.default_rng(61)\n"
+        "u0 = rng.standard_normal((2048, 2048)) + 1j * rng.standard_normal((2048, 2048))\n"
+        "v0 = rng.standard_normal((2048, 2048)) + 1j * rng.standard_normal((2048, 2048))\n"
+        "p = F.Plan(2048, 2048, Lx=0.8, Ly=2.0)\n"
+        "u, v = torch.from_numpy(u0).cuda(), torch.from_numpy(v0).cuda()\n"
+        "p.wave_step(u, v, 1.3, 2e-3, 3)\n"
+        "uo, vo = O.wave(u0, v0, 1.3, 2e-3, 3, 0.8, 2.0)\n"
+        "r = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))\n"
+        "eu, ev = r(u.cpu().numpy(), uo), r(v.cpu().numpy(), vo)\n"
+        "assert eu <= 1e-12 and ev <= 1e-12, (eu, ev)\n"
+        "print('ok', eu, ev)\n")
+    env = dict(os.environ, FFTPDE_WAVET="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0 and "ok" in res.stdout, res.stdout + res.stderr
