@@ -287,6 +287,10 @@ template <int N, typename C, int EMAX = 16> struct TwL1Pow : TwL1<N, C, EMAX> {
 };
 template <typename Tw, typename = void> struct TwLastPow { static constexpr bool value = false; };
 template <typename Tw> struct TwLastPow<Tw, std::void_t<decltype(Tw::LAST_POW)>> { static constexpr bool value = Tw::LAST_POW; };
+// LAST_SPLIT (radix-32 last stages): w^{m j}, m = 8 a + b, as the product of the two
+// table values w^{8 a j} and w^{b j} (10 loads instead of 31, one extra rounding)
+template <typename Tw, typename = void> struct TwLastSplit { static constexpr bool value = false; };
+template <typename Tw> struct TwLastSplit<Tw, std::void_t<decltype(Tw::LAST_SPLIT)>> { static constexpr bool value = Tw::LAST_SPLIT; };
 
 // As TwL1, reading a copy of the table staged in shared memory (short kernels
 // whose critical path would otherwise wait on L2 twiddle loads every stage).
@@ -333,6 +337,10 @@ template <int N, int EMAX = 16> struct TwSmemV {
         using S = Shape<N, EMAX>;
         return ld(base + 16u * (uint32_t)(S::TW_LAST_OFF + t + q * S::TPT + m * S::NS_LAST));
     }
+};
+
+template <int N, int EMAX = 16> struct TwSmemVSplit : TwSmemV<N, EMAX> {
+    static constexpr bool LAST_SPLIT = true;
 };
 
 template <int N, typename C, int EMAX = 16> struct TwReg {
@@ -419,7 +427,22 @@ __device__ __forceinline__ void fft_tw(C (&v)[Shape<N, EMAX>::E], const View &sm
         C u[R];
 #pragma unroll
         for (int m = 0; m < R; ++m) u[m] = v[q + m * Q];
-        if constexpr (S::NS_LAST > 1 && TwLastPow<Tw>::value) {
+        if constexpr (S::NS_LAST > 1 && R == 32 && TwLastSplit<Tw>::value) {
+            C wb[8], wa[4];
+#pragma unroll
+            for (int b = 1; b < 8; ++b) wb[b] = tw.last(q, b);
+#pragma unroll
+            for (int a = 1; a < 4; ++a) wa[a] = tw.last(q, 8 * a);
+#pragma unroll
+            for (int m = 1; m < R; ++m) {
+                const int a = m / 8, b = m % 8;
+                C w;
+                if (a == 0) w = wb[b];
+                else if (b == 0) w = wa[a];
+                else w = C{wa[a].x * wb[b].x - wa[a].y * wb[b].y, wa[a].x * wb[b].y + wa[a].y * wb[b].x};
+                u[m] = cmulw<INV>(u[m], w);
+            }
+        } else if constexpr (S::NS_LAST > 1 && TwLastPow<Tw>::value) {
             const C w1 = tw.last(q, 1);
             C wm = w1;
 #pragma unroll

@@ -509,9 +509,13 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
         for (int i = threadIdx.x; i < G::TWN; i += G::NT) twS[i] = tw32[i];
     __syncthreads();
     pdl_trigger();
-    using TwP = std::conditional_t<FFTPDE_FS_B3TW != 0, TwSmemV<L, E>, TwL1<L, double2, E>>;
+#ifndef FFTPDE_FS_B3SPLIT
+#define FFTPDE_FS_B3SPLIT 1    // By: last-stage twiddles as products of two table values (8.09 -> 7.93 ms; Bx +0.8%: off)
+#endif
+    using TwS = std::conditional_t<FFTPDE_FS_B3SPLIT != 0 && COLS, TwSmemVSplit<L, E>, TwSmemV<L, E>>;
+    using TwP = std::conditional_t<FFTPDE_FS_B3TW != 0, TwS, TwL1<L, double2, E>>;
     TwP twp;
-    if constexpr (FFTPDE_FS_B3TW) twp = TwP{tma_smem(twS), t};
+    if constexpr (FFTPDE_FS_B3TW) { twp.base = tma_smem(twS); twp.t = t; }
     else twp = TwP{tw32, t};
     for (int j = grp;; j += G::NG) {
         const int64_t tile = blockIdx.x + (int64_t)j * gridDim.x;
