@@ -285,12 +285,23 @@ template <int N, typename C, int EMAX = 16> struct TwL1 {
 template <int N, typename C, int EMAX = 16> struct TwL1Pow : TwL1<N, C, EMAX> {
     static constexpr bool LAST_POW = true;
 };
+// TwL1 with radix-32 middle / last stages in the split product form (10 table loads
+// per butterfly instead of 31; one extra rounding)
+template <int N, typename C, int EMAX = 16> struct TwL1PowSplit : TwL1<N, C, EMAX> {
+    static constexpr bool LAST_POW = true, MID_SPLIT = true;
+};
+template <int N, typename C, int EMAX = 16> struct TwL1Split : TwL1<N, C, EMAX> {
+    static constexpr bool LAST_SPLIT = true, MID_SPLIT = true;
+};
 template <typename Tw, typename = void> struct TwLastPow { static constexpr bool value = false; };
 template <typename Tw> struct TwLastPow<Tw, std::void_t<decltype(Tw::LAST_POW)>> { static constexpr bool value = Tw::LAST_POW; };
 // LAST_SPLIT (radix-32 last stages): w^{m j}, m = 8 a + b, as the product of the two
 // table values w^{8 a j} and w^{b j} (10 loads instead of 31, one extra rounding)
 template <typename Tw, typename = void> struct TwLastSplit { static constexpr bool value = false; };
 template <typename Tw> struct TwLastSplit<Tw, std::void_t<decltype(Tw::LAST_SPLIT)>> { static constexpr bool value = Tw::LAST_SPLIT; };
+// MID_SPLIT (radix-32 middle stages): the same product form for w_{Ns E}^{m k}
+template <typename Tw, typename = void> struct TwMidSplit { static constexpr bool value = false; };
+template <typename Tw> struct TwMidSplit<Tw, std::void_t<decltype(Tw::MID_SPLIT)>> { static constexpr bool value = Tw::MID_SPLIT; };
 
 // As TwL1, reading a copy of the table staged in shared memory (short kernels
 // whose critical path would otherwise wait on L2 twiddle loads every stage).
@@ -389,7 +400,22 @@ __device__ __forceinline__ void fft_tw(C (&v)[Shape<N, EMAX>::E], const View &sm
 #pragma unroll
     for (int s = 0; s < S::STAGES; ++s) {
         const int k = t & (Ns - 1);
-        if (s > 0) {
+        if (s > 0 && E == 32 && TwMidSplit<Tw>::value) {
+            C wb[8], wa[4];
+#pragma unroll
+            for (int b = 1; b < 8; ++b) wb[b] = tw.mid(s, b);
+#pragma unroll
+            for (int a = 1; a < 4; ++a) wa[a] = tw.mid(s, 8 * a);
+#pragma unroll
+            for (int m = 1; m < E; ++m) {
+                const int a = m / 8, b = m % 8;
+                C w;
+                if (a == 0) w = wb[b];
+                else if (b == 0) w = wa[a];
+                else w = C{wa[a].x * wb[b].x - wa[a].y * wb[b].y, wa[a].x * wb[b].y + wa[a].y * wb[b].x};
+                v[m] = cmulw<INV>(v[m], w);
+            }
+        } else if (s > 0) {
 #pragma unroll
             for (int m0 = 1; m0 < E; m0 += TG) {
                 C w[TG];

@@ -77,7 +77,13 @@ line_kernel(const typename cplx_t<T>::type *__restrict__ in, typename cplx_t<T>:
     constexpr bool INV1 = OP == LN_INV || OP == LN_INV_SCALED || OP == LN_MID;
     const LnSync<TPT, COLS> sync{1 + c};
     SmemView<C, S::LOGE, 1> sm{smem + c * L::S};
-    const TwL1<N, C, E> twp{tw, t};
+#ifndef FFTPDE_LINE_SPLIT
+#define FFTPDE_LINE_SPLIT 1     // complex128 radix-32 lines: split twiddles (C2 4.244 -> 4.214 ms per solve)
+#endif
+    using TwP = std::conditional_t<FFTPDE_LINE_SPLIT != 0 && sizeof(T) == 8, TwL1Split<N, C, E>, TwL1<N, C, E>>;
+    TwP twp;
+    twp.tw = tw;
+    twp.t = t;
     pdl_wait();
     pdl_trigger();
 

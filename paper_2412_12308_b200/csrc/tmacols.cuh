@@ -255,11 +255,17 @@ tma_wave2_cols_kernel(const __grid_constant__ CUtensorMap mu, const __grid_const
     for (int e = 0; e < E; ++e) v[e] = line[t + TPT * e];
     __syncthreads();
     SmemView<C, S::LOGE, 1> sm{line};
-#if FFTPDE_TWPOW
-    const TwL1Pow<N, C, EX> twp{{tw, t}};    // last stage radix 4: w, w^2, w^3 from one load
-#else
-    const TwL1<N, C, EX> twp{tw, t};
+#ifndef FFTPDE_WAVE2_SPLIT
+#define FFTPDE_WAVE2_SPLIT 1    // radix-32 middle-stage twiddles as products of two table values (C3 wave pass 0.559 -> 0.553 ms)
 #endif
+#if FFTPDE_TWPOW
+    using TwP = std::conditional_t<FFTPDE_WAVE2_SPLIT != 0, TwL1PowSplit<N, C, EX>, TwL1Pow<N, C, EX>>;   // last radix 4: w, w^2, w^3 from one load
+#else
+    using TwP = TwL1<N, C, EX>;
+#endif
+    TwP twp;
+    twp.tw = tw;
+    twp.t = t;
     fft_tw<N, false, EX>(v, sm, t, twp, sync);
 #pragma unroll
     for (int e = 0; e < E; ++e) line[t + TPT * e] = v[e];
