@@ -448,6 +448,21 @@ bx_kernel(double2 *f, const double2 *__restrict__ tw32, const double *__restrict
 // line on either axis: the By tile arrives under the 64-byte hardware swizzle, so
 // lane t reading rows t + 32 e of column c hits eight distinct 16-byte bank groups
 // per phase, and the exchanges are warp-synchronous (no CTA barrier per stage).
+// Bx tiles by class (FFTPDE_FS_BXCLS): tile t holds segment s = t / (N/W) of the W
+// grid rows W (t mod N/W) .. + W-1 -- four lines of ONE diffusion-factor class, and a
+// CTA's successive tiles (t + 148 j) keep that class for ~55 tiles, so the class's
+// 8 KiB factor row stays in L1 (tiles of four consecutive segments of one row cycle
+// through all 32 classes: 8 GB of factor reads from L2 per pass)
+#ifndef FFTPDE_FS_BXCLS
+#define FFTPDE_FS_BXCLS 1     // C5 505.6 -> 504.0 ms per solve (Bx 7.79 -> 7.76 ms; SM clock under the power cap 1665 -> 1680 MHz)
+#endif
+__device__ __forceinline__ int64_t bx_class(int64_t tile) { return tile / (FsGeom::N / FsGeom::W); }
+__device__ __forceinline__ int64_t bx_line(int64_t tile, int c)
+{
+    const int64_t yb = tile % (FsGeom::N / FsGeom::W);
+    return (yb * FsGeom::W + c) * FsGeom::Q + bx_class(tile);   // line = grid row * 32 + segment
+}
+
 template <bool COLS> struct B3Geom {
     static constexpr int L = 1024, E = 32, W = 4, BOXR = 256;
     static constexpr int GT = W * (L / E);                          // 128 threads per group
@@ -491,6 +506,10 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
 #pragma unroll
             for (int k = 0; k < L / G::BOXR; ++k)
                 tma_load3(tma_smem(slot_ptr(s)) + k * G::BOXR * W * 16, &map, 2 * W * g, 1024 * l1 + k * G::BOXR, 0, mb);
+        } else if constexpr (FFTPDE_FS_BXCLS) {
+#pragma unroll
+            for (int c = 0; c < W; ++c)
+                bulk_g2s(tma_smem(slot_ptr(s)) + c * L * 16, f + bx_line(tile, c) * L, (uint32_t)(L * 16), mb);
         } else {
             bulk_g2s(tma_smem(slot_ptr(s)), f + tile * (W * L), (uint32_t)G::TILE_BYTES, mb);
         }
@@ -533,6 +552,7 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
         const SmemView<double2, Shape<L, E>::LOGE, 1> sm{S + c * G::PITCH};
         const double *m;
         if constexpr (COLS) m = m2d + (size_t)(tile / G::NGROUP) * L + t;               // class l1
+        else if constexpr (FFTPDE_FS_BXCLS) m = m2d + (size_t)bx_class(tile) * L + t;   // one class per tile
         else m = m2d + (size_t)((tile * W + c) % FsGeom::Q) * L + t;                     // class k1
         const SyncWarp wsync{};
         fft_tw<L, false, E>(v, sm, t, twp, wsync);
@@ -554,6 +574,9 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
 #pragma unroll
                 for (int k = 0; k < L / G::BOXR; ++k)
                     tma_store3(&map, 2 * W * g, 1024 * l1 + k * G::BOXR, 0, tma_smem(S) + k * G::BOXR * W * 16);
+            } else if constexpr (FFTPDE_FS_BXCLS) {
+#pragma unroll
+                for (int c = 0; c < W; ++c) bulk_s2g(f + bx_line(tile, c) * L, tma_smem(S) + c * L * 16, (uint32_t)(L * 16));
             } else {
                 bulk_s2g(f + tile * (W * L), tma_smem(S), (uint32_t)G::TILE_BYTES);
             }

@@ -1,0 +1,11 @@
+set -u
+OUT=gpurun_out/r02s5; mkdir -p $OUT
+L=paper_2412_12308_b200/libfftpde.so
+for v in bxcls; do cp tools/ab/lib_$v.so $L
+  timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "c5 or 32768" > $OUT/pytest_$v.log 2>&1; echo "$v pytest $?"; tail -1 $OUT/pytest_$v.log
+done
+for r in 1 2; do for v in base bxcls; do cp tools/ab/lib_$v.so $L
+  timeout 900 python bench.py --workload c5 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 > $OUT/ab_$v.json
+  python -c "import json; d=json.load(open('$OUT/ab_$v.json')); print('$v', round(d['ms_per_step'],2), d['clocks']['sm_mhz'], d['parity']['rel_l2'], {k: v['ms_per_launch'] for k, v in d['roofline']['per_kernel'].items()})"
+done; done
+cp tools/ab/lib_base.so $L
