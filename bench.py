@@ -13,8 +13,9 @@ materialised every step).  The metric is grid-points per second
 Multi-GPU: ``--gpus N`` with N > 1 launches N ranks itself (torch.distributed.run,
 127.0.0.1) unless WORLD_SIZE is already set, and checks WORLD_SIZE == N.  C5 at
 N > 1 runs the row-slab decomposition of SURVEY.md 8(e) (strong scaling, fixed
-32768^2 grid); the default exchange is ``fused`` (the row and column passes store
-straight into the peers' slabs over NVLink).  C1-C4 at N > 1 run independent
+32768^2 grid); the default exchange is ``lib``: the distributed four-step inside
+libfftpde (R28: each rank runs the single-GPU four-step passes on its
+Y-part / X-part of the field, one NCCL all-to-all per solve step).  C1-C4 at N > 1 run independent
 replicas (weak scaling, no collective on the data path).
 
 Timing: W untimed warm-up steps, then exactly K steps, each bracketed by CUDA
@@ -87,10 +88,11 @@ def parse_args():
     ap.add_argument("--pencil", default=None, metavar="PZxPY",
                     help="3D workloads: the pencil decomposition on a PZ x PY process grid (PZ*PY = --gpus; "
                          "fftpde_plan_3d_pencil) instead of z-slabs")
-    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl", "peer", "lib"],
-                    help="sharded c5: exchanges fused into the row / column passes (peer stores into torch "
-                         "symmetric memory, default), pack + NCCL all-to-all, a separate peer-store "
-                         "transpose, or NCCL inside libfftpde (fftpde_plan_2d_sharded)")
+    ap.add_argument("--exchange", default="lib", choices=["fused", "nccl", "peer", "lib"],
+                    help="sharded c5: the distributed four-step inside libfftpde (fftpde_plan_2d_sharded, one "
+                         "NCCL all-to-all per step; default), or the round-1 slab solvers: exchanges fused into "
+                         "the row / column passes (peer stores into torch symmetric memory), pack + NCCL "
+                         "all-to-all, a separate peer-store transpose")
     return ap.parse_args()
 
 
@@ -862,18 +864,26 @@ def sharded_native(args, wl, world, rank, local):
                         "max over ranks; bytes summed over ranks"}
         del host_in, host_out, dev_in
     # per rank and step: HBM = passes x (read + write) of the slab, NVLink = the
-    # bytes leaving the rank in the two exchanges (per direction)
+    # bytes leaving the rank in the two exchanges (per direction).  lib = the
+    # distributed four-step (R28): per step Bx + By (2 x slab each) and MID
+    # (3 x slab) and ONE all-to-all; per solve the row-slab <-> Y-part conversion (a
+    # permutation and a block swap each way, 8 x slab) and two more all-to-alls
     slab_bytes = (hi - lo) * wl.nx * 16
-    hbm_passes = {"fused": 2, "peer": 3, "nccl": 5, "lib": 5}[exchange]
-    nvl_bytes = 2 * slab_bytes * (world - 1) // world
+    if exchange == "lib":
+        conv = 1 if world > 1 else 0        # P = 1: the parts are the row slab, no conversion
+        hbm_step = (7 + conv * 8 / wl.nsteps) * slab_bytes
+        nvl_bytes = int(slab_bytes * (world - 1) / world * (1 + 2 / wl.nsteps))
+    else:
+        hbm_step = {"fused": 2, "peer": 3, "nccl": 5}[exchange] * 2 * slab_bytes
+        nvl_bytes = 2 * slab_bytes * (world - 1) // world
     peaks = load_peaks()
-    t_hbm = hbm_passes * 2 * slab_bytes / (peaks["hbm_gbs"] * 1e9)
+    t_hbm = hbm_step / (peaks["hbm_gbs"] * 1e9)
     t_nvl = nvl_bytes / (NVLINK_GBS * 1e9)
     step_s = ms_per_step * 1e-3 / wl.nsteps
     prof_steps = {k: (v[0], v[1]) for k, v in prof.items()}
     extra = {"sharded": {
         "exchange": exchange, "ranks": world, "slab_bytes": slab_bytes,
-        "hbm_bytes_per_rank_step": hbm_passes * 2 * slab_bytes, "nvlink_bytes_per_rank_step": nvl_bytes,
+        "hbm_bytes_per_rank_step": int(hbm_step), "nvlink_bytes_per_rank_step": nvl_bytes,
         "nvlink_gbs_per_rank": round(nvl_bytes / step_s / 1e9, 1) if world > 1 else 0.0,
         "t_hbm_ms": round(t_hbm * 1e3, 4), "t_nvl_ms": round(t_nvl * 1e3, 4),
         "roof": "nvlink" if t_nvl > t_hbm else "hbm",
@@ -892,7 +902,8 @@ def sharded_native(args, wl, world, rank, local):
                        "peer": "(peer-store exchange, symmetric memory)",
                        "fused": "(row and column passes store into the peers' slabs, symmetric memory; separable diffusion)",
                        "nccl": "(NCCL all-to-all, Python-driven)",
-                       "lib": "(NCCL all-to-all inside libfftpde, fftpde_plan_2d_sharded)"}[exchange],
+                       "lib": "(distributed four-step inside libfftpde, fftpde_plan_2d_sharded: Y-/X-parts, one NCCL "
+                              "all-to-all per step)"}[exchange],
                    "l2": "field (16 GiB) larger than L2; 256 MiB buffer zeroed between timed steps"},
         "e2e": e2e, "cpu_baseline": None, "clocks": clocks, "parity": parity,
         "roofline": roofline, "gpu_launches": launches,

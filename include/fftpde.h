@@ -102,6 +102,17 @@ fftpde_status fftpde_plan_2d_r2c(fftpde_plan *plan, int64_t nx, int64_t ny, int6
  * (columns a in [r nx/P, (r+1) nx/P)), in != out; fftpde_inverse: column slab ->
  * row slab (x 1/(nx ny)).  P must divide nx and ny, (nx/P) * element size must be
  * a multiple of 16 bytes, and for ny > 8192 nx/P at least one 128-byte block.
+ * fftpde_diffuse on nx = ny = 32768 complex128 with P a power of two <= 32 runs
+ * the distributed four-step instead (R28; the four-step split of
+ * PAPER.md:262-273 applied inside each axis, N = 1024 x 32): rank r holds the
+ * field's rows with (y mod 1024) in [r M, r M + M) ("Y-part", M = 1024/P) or its
+ * columns with (x mod 1024) in that range ("X-part"), both as [P][32][M][32][M];
+ * per solve step the x-axis 1024-point diffusion pass on the Y-part, ONE
+ * all-to-all (Y-part <-> X-part), the y-axis pass on the X-part and the combined
+ * high-index pass that writes the physical field and starts the next step (the
+ * parts alternate step by step).  The caller's row slabs are converted on entry
+ * and exit (a permutation pass, an all-to-all and a block swap each way).
+ * Same results on every P, bit for bit (tests/test_gpu_sharded.py).
  *
  * 3D (fftpde_plan_3d_sharded, SURVEY.md 8(f) row 4 on several GPUs): rank r owns
  * z-planes [r nz/P, (r+1) nz/P) (its "z-slab", [nz/P][ny][nx]).  Per step: x- and

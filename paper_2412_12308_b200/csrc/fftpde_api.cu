@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -45,6 +46,7 @@ struct fftpde_plan_s {
     std::vector<double> rtwP, rtwQ, rtwN;   // row2d: radix-16 stage tables of P, Q; split inter-phase table
     // four-step diffusion passes (fourstep.cuh; 32768^2 complex128 single grids, R27)
     bool fs = false;
+    bool fsd = false;   // sharded 32768^2 complex128 plan: the distributed four-step (R28) with the fs tables
     std::vector<double> fs_tw, fs_tw32, fs_tw16;   // w_N^{ab} (a < 1024, b < 32); radix-32 / -16 stage tables of 1024
     size_t o_fs_tw = 0, o_fs_tw32 = 0, o_fs_tw16 = 0, o_fs_mx = 0, o_fs_my = 0, o_fs_sync = 0;
     size_t need = 0;
@@ -913,6 +915,81 @@ template <typename T> struct Passes {
         if (e == cudaSuccess) e = each([&](int i) { return pack_sh(shB(i), at(out, i), 1); });
         return e;
     }
+    // ---- the distributed four-step diffusion (R28; 32768^2 complex128, P | 32) ----
+    // Rank r's Y-part (rows of m1 in [r M, r M + M)) and X-part (columns of n1 in
+    // [r M, r M + M)) share the 5D layout [blk][Q][M][Q][M] (fourstep.cuh FsPart), so
+    // the Y -> X and X -> Y transposes are the plain all-to-all `exchange` of equal
+    // blocks.  Per step: the B pass of the part the field is in, the exchange, the B
+    // pass of the other axis, then MID (AA^-1 of this step -> the physical field, AA
+    // of the next) in that part: 3 passes and one exchange per step, the parts
+    // alternating.  The caller's row slabs enter and leave through one permutation
+    // pass, one all-to-all and one block transpose each way.
+    cudaError_t fsd_aa(int op, int xmode, int i, const void *in, void *out, void *phys)
+    {
+        return launch(p, FFTPDE_KERNEL_AA, [&] {
+            if (p->P == 1) return launch_aa(op, in, out, phys, p->ws + p->o_fs_tw, p->stream);   // = the plain layout
+            return launch_aa_part(op, p->P, rk(i), xmode, in, out, phys, p->ws + p->o_fs_tw, p->stream);
+        });
+    }
+    cudaError_t fsd_b(bool cols, int i, void *f)
+    {
+        return launch(p, cols ? FFTPDE_KERNEL_COL : FFTPDE_KERNEL_ROW, [&] {
+            if (p->P == 1) {                               // both parts are the single-GPU layout
+                OpTables<double> t{};
+                t.ey2d = (const double *)(p->ws + (cols ? p->o_fs_my : p->o_fs_mx));
+                t.ey2d_mod = 32;
+                return launch_fs_b(cols, f, p->ws + p->o_fs_tw32, p->ws + p->o_fs_tw16, t, p->stream);
+            }
+            return launch_fs_b_part(cols, p->P, rk(i), f, p->ws + p->o_fs_tw32,
+                                    (const double *)(p->ws + (cols ? p->o_fs_my : p->o_fs_mx)), p->stream);
+        });
+    }
+    // [P][P][X] -> [P][P][X] with the two block indices swapped (X = a rank's slab / P^2)
+    cudaError_t fsd_swap(const void *in, void *out)
+    {
+        ++p->launches;
+        return launch_pack(in, out, p->P, p->P, slab_bytes() / ((size_t)p->P * p->P), 0, p->stream);
+    }
+    cudaError_t fsd_perm(const void *in, void *out, int direction)
+    {
+        ++p->launches;
+        return launch_fs_perm(in, out, p->P, direction, p->stream);
+    }
+    cudaError_t diffuse_fsd(const void *u0, void *u, int64_t nsteps)
+    {
+        const bool one = p->P == 1;                        // both parts are the plain layout, no exchange
+        cudaError_t e;
+        if (one) {
+            e = fsd_aa(0, 0, 0, u0, shA(0), nullptr);
+        } else {                                           // row slab -> Y-part in shA
+            e = each([&](int i) { return fsd_perm(at(u0, i), shB(i), 0); });
+            if (e == cudaSuccess) e = exchange(&Passes::shB, &Passes::shC);
+            if (e == cudaSuccess) e = each([&](int i) { return fsd_swap(shC(i), shA(i)); });
+            if (e == cudaSuccess) e = each([&](int i) { return fsd_aa(0, 0, i, shA(i), shA(i), nullptr); });
+        }
+        int x = 0;                                         // the part the AA-domain field is in
+        auto W = [&](int i) { return x && !one ? shC(i) : shA(i); };
+        for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) {
+            e = each([&](int i) { return fsd_b(x != 0, i, W(i)); });
+            if (e == cudaSuccess && !one) e = x ? exchange(&Passes::shC, &Passes::shA) : exchange(&Passes::shA, &Passes::shC);
+            x ^= 1;
+            if (e == cudaSuccess) e = each([&](int i) { return fsd_b(x != 0, i, W(i)); });
+            if (e != cudaSuccess) break;
+            if (k + 1 < nsteps) e = each([&](int i) { return fsd_aa(2, x, i, W(i), W(i), one ? at(u, i) : shB(i)); });
+            else e = each([&](int i) { return fsd_aa(1, x, i, W(i), one ? at(u, i) : shB(i), nullptr); });
+        }
+        if (e != cudaSuccess || one) return e;
+        // the physical field (shB, part x) -> Y-part -> the caller's row slabs
+        if (x) {
+            e = exchange(&Passes::shB, &Passes::shA);
+            if (e == cudaSuccess) e = each([&](int i) { return fsd_swap(shA(i), shB(i)); });
+        } else {
+            e = each([&](int i) { return fsd_swap(shB(i), shA(i)); });
+        }
+        if (e == cudaSuccess) e = x ? exchange(&Passes::shB, &Passes::shC) : exchange(&Passes::shA, &Passes::shC);
+        if (e == cudaSuccess) e = each([&](int i) { return fsd_perm(shC(i), at(u, i), 1); });
+        return e;
+    }
     // one step: slab -> exchange -> column-slab pass with the operator -> exchange -> slab
     cudaError_t step_sh(const void *in, void *out, int op)
     {
@@ -1287,7 +1364,7 @@ fftpde_status ensure_diffusion_tables(fftpde_plan p, double D, double dt)
     for (int64_t b = 0; b < p->ny; ++b) ey[(size_t)b] = std::exp(-D * p->ky2[(size_t)b] * dt);
     fftpde_status s = upload(p, p->o_ex, ex);
     if (s == FFTPDE_OK) s = upload(p, p->o_ey, ey);
-    if (s == FFTPDE_OK && p->fs) {        // per-axis factors: e^{-D kx^2 dt}/nx, e^{-D ky^2 dt}/ny
+    if (s == FFTPDE_OK && (p->fs || p->fsd)) {   // per-axis factors: e^{-D kx^2 dt}/nx, e^{-D ky^2 dt}/ny
         std::vector<double> mx((size_t)p->nx), my((size_t)p->ny);
         for (int64_t a = 0; a < p->nx; ++a) mx[(size_t)a] = std::exp(-D * p->kx2[(size_t)a] * dt) / (double)p->nx;
         for (int64_t b = 0; b < p->ny; ++b) my[(size_t)b] = std::exp(-D * p->ky2[(size_t)b] * dt) / (double)p->ny;
@@ -1528,7 +1605,7 @@ fftpde_status fftpde_set_workspace(fftpde_plan plan, void *dev_ptr, size_t bytes
         if (s == FFTPDE_OK) s = upload(plan, plan->o_rtwQ, plan->rtwQ);
         if (s == FFTPDE_OK) s = upload(plan, plan->o_rtwN, plan->rtwN);
     }
-    if (s == FFTPDE_OK && plan->fs) {
+    if (s == FFTPDE_OK && (plan->fs || plan->fsd)) {
         s = upload(plan, plan->o_fs_tw, plan->fs_tw);
         if (s == FFTPDE_OK) s = upload(plan, plan->o_fs_tw32, plan->fs_tw32);
         if (s == FFTPDE_OK) s = upload(plan, plan->o_fs_tw16, plan->fs_tw16);
@@ -1961,7 +2038,10 @@ namespace {
 fftpde_status finish_sharded(fftpde_plan p, int nranks, int rank, const void *uid, int64_t slab_elems)
 {
     p->sharded = true;
-    p->fs = false;                   // the slab path has its own passes
+    // 2D 32768^2 complex128 with a power-of-two P <= 32: the distributed four-step
+    // (R28) on the plan's four-step tables; otherwise the slab path's own passes
+    p->fsd = p->fs && !p->is3d && !p->pencil && fftpde::fs_dist_supported(nranks);
+    p->fs = false;
     p->P = nranks;
     p->loopback = uid == nullptr;
     p->rank = p->loopback ? 0 : rank;
@@ -2258,6 +2338,11 @@ fftpde_status fftpde_diffuse(fftpde_plan p, const void *u0, void *u, double D, d
                                                          cudaMemcpyDeviceToDevice, p->stream));
         s = p->is3d ? ensure_diffusion_tables3(p, D, dt) : ensure_diffusion_tables(p, D, dt);
         if (s != FFTPDE_OK) return s;
+        if (p->fsd)
+            return dispatch_real(p, [&](auto &ps) {
+                if constexpr (std::is_same_v<std::decay_t<decltype(ps)>, Passes<double>>) return ps.diffuse_fsd(u0, u, nsteps);
+                return cudaErrorNotSupported;
+            });
         for (int64_t k = 0; k < nsteps && s == FFTPDE_OK; ++k)
             s = dispatch_real(p, [&](auto &ps) { return ps.step_sh(k == 0 ? u0 : u, u, COL_DIFFUSE); });
         return s;

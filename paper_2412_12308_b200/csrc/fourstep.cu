@@ -1,5 +1,7 @@
 // fourstep.cu -- launcher of the four-step AA pass (fourstep.cuh).
 #include <cuda.h>
+#include <cstring>
+#include <algorithm>
 #include "fourstep.cuh"
 #include "dispatch.cuh"
 
@@ -34,22 +36,40 @@ static bool fs_map(CUtensorMap &m, const void *p)
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int OP>
+// the rank's part of the distributed four-step (R28) as the 5D tensor
+// {2 M doubles (n1_l), Q, M (m1_l), Q, P (blk)}; boxes of {2 W doubles, Q, 1, Q, 1}
+static bool fs_map5(CUtensorMap &m, const void *p, int M, int P)
+{
+    using G = FsGeom;
+    auto enc = tma_encoder();
+    if (!enc) return false;
+    const cuuint64_t r = (cuuint64_t)M * 16;
+    cuuint64_t dims[5] = {(cuuint64_t)(2 * M), (cuuint64_t)G::Q, (cuuint64_t)M, (cuuint64_t)G::Q, (cuuint64_t)P};
+    cuuint64_t strides[4] = {r, r * G::Q, r * G::Q * M, r * G::Q * M * G::Q};
+    cuuint32_t box[5] = {(cuuint32_t)(2 * G::W), (cuuint32_t)G::Q, 1, (cuuint32_t)G::Q, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void *>(p), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, FFTPDE_FS_PROMO_AA,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int OP, bool DIST = false>
 static cudaError_t aa_n(const CUtensorMap &mi, const CUtensorMap &mo, const CUtensorMap &mp, const void *tw,
-                        cudaStream_t st)
+                        cudaStream_t st, const FsPart &pt = FsPart{})
 {
     using G = FsGeom;
     using Cfg = FsCfg<FFTPDE_FS_NBUF>;
-    auto k = aa_kernel<OP, FFTPDE_FS_NBUF>;
+    auto k = aa_kernel<OP, FFTPDE_FS_NBUF, DIST>;
     static SmemOptIn<decltype(k)> opt;
     cudaError_t e = opt(k, Cfg::BYTES);
     if (e != cudaSuccess) return e;
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, G::NT, Cfg::BYTES);
     if (e != cudaSuccess) return e;
-    const dim3 grid(Cfg::NBUF == 1 ? (unsigned)G::NTILES    // one tile per CTA
-                                   : (unsigned)std::min<int64_t>(G::NTILES, (int64_t)std::max(occ, 1) * sm_count()));
-    e = launch_fam(PDL_FOURSTEP, k, grid, dim3(G::NT), Cfg::BYTES, st, mi, mo, mp, (const double2 *)tw);
+    const int64_t ntiles = DIST ? pt.ntiles : G::NTILES;
+    const dim3 grid(Cfg::NBUF == 1 ? (unsigned)ntiles    // one tile per CTA
+                                   : (unsigned)std::min<int64_t>(ntiles, (int64_t)std::max(occ, 1) * sm_count()));
+    e = launch_fam(PDL_FOURSTEP, k, grid, dim3(G::NT), Cfg::BYTES, st, mi, mo, mp, (const double2 *)tw, pt);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -66,6 +86,51 @@ cudaError_t launch_aa(int op, const void *in, void *out, void *phys, const void 
     case FS_FWD: return aa_n<FS_FWD>(mi, mo, mp, tw, st);
     case FS_INV: return aa_n<FS_INV>(mi, mo, mp, tw, st);
     case FS_MID: return aa_n<FS_MID>(mi, mo, mp, tw, st);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+FsPart fs_part(int P, int rank, int xmode, int pass)
+{
+    using G = FsGeom;
+    FsPart t{};
+    t.M = G::P / P;
+    t.P = P;
+    t.rank = rank;
+    t.xmode = xmode;
+    t.rows = G::Q * t.M;
+    t.ngroup = G::Q * t.M / G::W;
+    t.nb = xmode ? t.M / G::W : G::NCHUNK;
+    t.ntiles = pass == 0 ? G::NTILES / P : (int)((int64_t)G::Q * t.ngroup);   // AA | B passes: 262144 / P tiles
+    auto lg = [](int v) { int l = 0; while ((1 << l) < v) ++l; return l; };
+    t.lgM = lg(t.M);
+    t.lgNb = lg(t.nb);
+    t.lgMW = lg(t.M / G::W);
+    t.lgNg = lg(t.ngroup);          // Bx: rows / W = Q M / W, By: ngroup (the same count)
+    return t;
+}
+
+bool fs_dist_supported(int P)
+{
+    // M = 1024 / P points per rank along the split index, a multiple of the tile
+    // width W = 4, and P <= 32 so that a rank's row slab holds whole m2 rows of 1024
+    return P >= 1 && P <= 32 && (P & (P - 1)) == 0 && tma_encoder() != nullptr;
+}
+
+cudaError_t launch_aa_part(int op, int P, int rank, int xmode, const void *in, void *out, void *phys, const void *tw,
+                           cudaStream_t st)
+{
+    const FsPart pt = fs_part(P, rank, xmode, 0);
+    CUtensorMap mi, mo, mp;
+    if (!fs_map5(mi, in, pt.M, P)) return cudaErrorNotSupported;
+    if (out == in) mo = mi;
+    else if (!fs_map5(mo, out, pt.M, P)) return cudaErrorNotSupported;
+    if (!phys) mp = mo;
+    else if (!fs_map5(mp, phys, pt.M, P)) return cudaErrorNotSupported;
+    switch (op) {
+    case FS_FWD: return aa_n<FS_FWD, true>(mi, mo, mp, tw, st, pt);
+    case FS_INV: return aa_n<FS_INV, true>(mi, mo, mp, tw, st, pt);
+    case FS_MID: return aa_n<FS_MID, true>(mi, mo, mp, tw, st, pt);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -111,12 +176,37 @@ static cudaError_t launch_by_tma(void *f, const void *tw32, const double *my2d, 
 #ifndef FFTPDE_FS_B3
 #define FFTPDE_FS_B3 3      // Bx and By persistent (C5 512 vs 525 ms per 20-step solve against by_kernel / line Bx)
 #endif
-template <bool COLS> static cudaError_t launch_b3(void *f, const void *tw32, const double *m2d, cudaStream_t st)
+// an X-part as the 4D tensor {2 Q M doubles, M rows (m1_l), Q (l1), P (blk)}; boxes of
+// 64 bytes x 256 rows (min(M, 256) rows x max(1, 256 / M) blocks)
+static bool by_map_part(CUtensorMap &m, const void *p, int M, int P)
+{
+    using G = FsGeom;
+    auto enc = tma_encoder();
+    if (!enc) return false;
+    const cuuint64_t row = (cuuint64_t)G::Q * M * 16;
+    cuuint64_t dims[4] = {(cuuint64_t)(2 * G::Q * M), (cuuint64_t)M, (cuuint64_t)G::Q, (cuuint64_t)P};
+    cuuint64_t strides[3] = {row, row * M, row * M * G::Q};
+    cuuint32_t box[4] = {(cuuint32_t)(2 * ByGeom::W), (cuuint32_t)std::min(M, ByGeom::BOXR), 1,
+                         (cuuint32_t)std::max(1, ByGeom::BOXR / M)};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void *>(p), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, FFTPDE_FS_PROMO_BY,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <bool COLS, bool DIST = false>
+static cudaError_t launch_b3(void *f, const void *tw32, const double *m2d, cudaStream_t st, const FsPart &pt = FsPart{})
 {
     using G = B3Geom<COLS>;
     CUtensorMap m;
-    if (!by_map(m, f, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorNotSupported;
-    auto k = b3_kernel<COLS>;
+    if (DIST && COLS) {
+        if (!by_map_part(m, f, pt.M, pt.P)) return cudaErrorNotSupported;
+    } else if (!DIST && !by_map(m, f, CU_TENSOR_MAP_SWIZZLE_64B)) {
+        return cudaErrorNotSupported;
+    } else if (DIST) {
+        std::memset(&m, 0, sizeof m);                        // Bx (DIST) moves its lines by bulk copies
+    }
+    auto k = b3_kernel<COLS, DIST>;
     static SmemOptIn<decltype(k)> opt;
     cudaError_t e = opt(k, G::BYTES);
     if (e != cudaSuccess) return e;
@@ -128,10 +218,17 @@ template <bool COLS> static cudaError_t launch_b3(void *f, const void *tw32, con
         if (occ < 1) return cudaErrorInvalidConfiguration;
         occ_cache.store(occ, std::memory_order_relaxed);
     }
-    const unsigned grid = (unsigned)std::min<int64_t>(G::NTILES, (int64_t)occ * sm_count());
-    e = launch_fam(PDL_FOURSTEP, k, dim3(grid), dim3(G::NT), G::BYTES, st, m, (double2 *)f, (const double2 *)tw32, m2d);
+    const unsigned grid = (unsigned)std::min<int64_t>(DIST ? pt.ntiles : G::NTILES, (int64_t)occ * sm_count());
+    e = launch_fam(PDL_FOURSTEP, k, dim3(grid), dim3(G::NT), G::BYTES, st, m, (double2 *)f, (const double2 *)tw32, m2d,
+                   pt);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
+}
+// the B pass of a rank's part (R28): Bx on a Y-part (cols false), By on an X-part (cols true)
+cudaError_t launch_fs_b_part(bool cols, int P, int rank, void *f, const void *tw32, const double *m2d, cudaStream_t st)
+{
+    const FsPart pt = fs_part(P, rank, cols ? 1 : 0, 1);
+    return cols ? launch_b3<true, true>(f, tw32, m2d, st, pt) : launch_b3<false, true>(f, tw32, m2d, st, pt);
 }
 static int fs_b3_mask()
 {

@@ -99,6 +99,68 @@ __device__ __forceinline__ void tma_prefetch3(const CUtensorMap *map, int c0, in
     asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1),
                  "r"(c2) : "memory");
 }
+// ---- the distributed four-step (sharded plans, R28) -------------------
+// P ranks, M = P_fs / P (m1 or n1 values per rank).  Every rank's part of the field
+// is the 5D array [B][Q][M][Q][M] = [blk][l1|m2][m1_l][k1|n2][n1_l]:
+//   Y-part (xmode 0, rank r): m1 = r M + m1_l, blk = q, n1 = q M + n1_l  (all x, rows of one m1 range)
+//   X-part (xmode 1, rank q): n1 = q M + n1_l, blk = r, m1 = r M + m1_l  (all y, columns of one n1 range)
+// so the global array is G[r][q][..] and the Y -> X exchange is the all-to-all of
+// its first two indices (block q of rank r's Y-part -> block r of rank q's X-part).
+// At P = 1 both parts are the single-GPU layout [y = m1 + P l1][x = n1 + P k1].
+struct FsPart {
+    int M, P, rank, xmode;
+    int ntiles;    // tiles of this pass on this rank
+    int nb;        // AA: tiles per value of the tile's leading index
+    int rows;      // Bx: local rows (Q M)
+    int ngroup;    // By: 4-column groups per 1024-row block (Q M / W)
+    int lgM, lgNb, lgMW, lgNg;   // log2 of M, nb, M / W and of the B pass's tiles per line class
+};
+struct FsTile { int m1, chunk, cx, cm, cb; };     // global m1 and n1-chunk; tensor coordinates
+template <bool DIST> __device__ __forceinline__ FsTile fs_tile(int tile, const FsPart &pt)
+{
+    using G = FsGeom;
+    FsTile t;
+    if constexpr (!DIST) {
+        t.m1 = tile / G::NCHUNK;
+        t.chunk = tile % G::NCHUNK;
+        t.cx = 2 * G::W * t.chunk;
+        t.cm = t.m1;
+        t.cb = 0;
+    } else {
+        const int a = tile >> pt.lgNb, b = tile & ((1 << pt.lgNb) - 1);
+        t.m1 = pt.xmode ? a : (pt.rank << pt.lgM) + a;
+        t.chunk = pt.xmode ? (pt.rank << pt.lgMW) + b : b;
+        t.cx = 2 * G::W * (t.chunk & ((1 << pt.lgMW) - 1));
+        t.cm = t.m1 & (pt.M - 1);
+        t.cb = pt.xmode ? t.m1 >> pt.lgM : t.chunk >> pt.lgMW;
+    }
+    return t;
+}
+__device__ __forceinline__ void tma_load5(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, int c3, int c4,
+                                          uint32_t mbar)
+{
+    asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+                 "r"(c4), "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store5(const CUtensorMap *map, int c0, int c1, int c2, int c3, int c4, uint32_t src)
+{
+    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];"
+                 ::"l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(src) : "memory");
+}
+template <bool DIST> __device__ __forceinline__ void fs_tile_load(uint32_t dst, const CUtensorMap *map, const FsTile &t,
+                                                                  uint32_t mb)
+{
+    if constexpr (DIST) tma_load5(dst, map, t.cx, 0, t.cm, 0, t.cb, mb);
+    else tma_load4(dst, map, t.cx, 0, t.cm, 0, mb);
+}
+template <bool DIST> __device__ __forceinline__ void fs_tile_store(const CUtensorMap *map, const FsTile &t, uint32_t src)
+{
+    if constexpr (DIST) tma_store5(map, t.cx, 0, t.cm, 0, t.cb, src);
+    else tma_store4(map, t.cx, 0, t.cm, 0, src);
+}
+
 #ifndef FFTPDE_FS_PF
 #define FFTPDE_FS_PF 0      // L2 prefetch of the tile one wave ahead: measured +3% (578 vs 561 ms per solve), off
 #endif
@@ -109,15 +171,15 @@ __device__ __forceinline__ void tma_prefetch3(const CUtensorMap *map, int c0, in
 
 // Thread `lead` issues the loads of a tile (TMA box) and of its twiddles into slot
 // S / ts, completing on mbarrier `mb`.
-template <typename Cfg>
-__device__ __forceinline__ void aa_load(const CUtensorMap *min, const double2 *tw, int tile, double2 *S, double2 *ts,
-                                        uint32_t mb)
+template <typename Cfg, bool DIST>
+__device__ __forceinline__ void aa_load(const CUtensorMap *min, const double2 *tw, const FsTile &ti, double2 *S,
+                                        double2 *ts, uint32_t mb)
 {
     using G = FsGeom;
     constexpr int Q = G::Q, W = G::W, TWP = Cfg::TWP;
-    const int m1 = tile / G::NCHUNK, chunk = tile % G::NCHUNK;
+    const int m1 = ti.m1, chunk = ti.chunk;
     tma_mbar_expect(mb, (uint32_t)(G::TILE * 16) + Cfg::TWB);
-    tma_load4(tma_smem(S), min, 2 * W * chunk, 0, m1, 0, mb);
+    fs_tile_load<DIST>(tma_smem(S), min, ti, mb);
     if constexpr (TWP == Q) {
         bulk_g2s(tma_smem(ts), tw + (size_t)chunk * W * Q, W * Q * 16, mb);     // w_N^{n1 k1}, 4 n1
     } else {
@@ -130,14 +192,12 @@ __device__ __forceinline__ void aa_load(const CUtensorMap *min, const double2 *t
 // The work on one landed tile by 128 threads (r, w) = (tid / W, tid % W), `sync`
 // their barrier, `lead` the thread that issues the stores.  On return the last
 // store is committed (the caller waits for its read before reusing the slot).
-template <int OP, typename Cfg, typename Sync>
-__device__ __forceinline__ void aa_tile(double2 *S, const double2 *ts, int r, int w, bool lead, int tile,
+template <int OP, typename Cfg, bool DIST, typename Sync>
+__device__ __forceinline__ void aa_tile(double2 *S, const double2 *ts, int r, int w, bool lead, const FsTile &ti,
                                         const CUtensorMap *mout, const CUtensorMap *mphys, Sync sync)
 {
     using G = FsGeom;
     constexpr int Q = G::Q, W = G::W;
-    const int m1 = tile / G::NCHUNK, chunk = tile % G::NCHUNK;
-    const int c0 = 2 * W * chunk;                          // tensor coordinate (doubles) of the chunk
     const double2 *twx = ts + w * Cfg::TWP;                // w_N^{n1 k1}
     const double2 *twy = ts + W * Cfg::TWP;                // w_N^{m1 l1}
     double2 v[Q];
@@ -172,7 +232,7 @@ __device__ __forceinline__ void aa_tile(double2 *S, const double2 *ts, int r, in
         tma_fence_smem();
         sync();
         if (lead) {
-            tma_store4(map, c0, 0, m1, 0, tma_smem(S));
+            fs_tile_store<DIST>(map, ti, tma_smem(S));
             tma_commit();
         }
     };
@@ -233,10 +293,10 @@ __device__ __forceinline__ void aa_tile(double2 *S, const double2 *ts, int r, in
 
 struct SyncBlock { __device__ __forceinline__ void operator()() const { __syncthreads(); } };
 
-template <int OP, int NB>
+template <int OP, int NB, bool DIST = false>
 __global__ void __launch_bounds__(FsGeom::NT, FsCfg<NB>::MINB)
 aa_kernel(const __grid_constant__ CUtensorMap min, const __grid_constant__ CUtensorMap mout,
-          const __grid_constant__ CUtensorMap mphys, const double2 *__restrict__ tw)
+          const __grid_constant__ CUtensorMap mphys, const double2 *__restrict__ tw, const FsPart pt)
 {
     using G = FsGeom;
     using Cfg = FsCfg<NB>;
@@ -255,29 +315,30 @@ aa_kernel(const __grid_constant__ CUtensorMap min, const __grid_constant__ CUten
     }
     __syncthreads();
     auto load = [&](int t, int slot) {
-        aa_load<Cfg>(&min, tw, t, S0 + slot * G::TILE, TWS0 + slot * Cfg::TWS, mbar0 + 8u * slot);
+        aa_load<Cfg, DIST>(&min, tw, fs_tile<DIST>(t, pt), S0 + slot * G::TILE, TWS0 + slot * Cfg::TWS, mbar0 + 8u * slot);
     };
     pdl_wait();
+    const int ntiles = DIST ? pt.ntiles : G::NTILES;
     int tile = blockIdx.x;
-    if (tid == 0 && tile < G::NTILES) load(tile, 0);
-    if (NBUF == 1 && FFTPDE_FS_PF && tid == 0) {           // the tile one wave of resident CTAs ahead -> L2
+    if (tid == 0 && tile < ntiles) load(tile, 0);
+    if (!DIST && NBUF == 1 && FFTPDE_FS_PF && tid == 0) {           // the tile one wave of resident CTAs ahead -> L2
         const int pf = tile + 3 * 148;
         if (pf < G::NTILES) tma_prefetch4(&min, 2 * W * (pf % G::NCHUNK), 0, pf / G::NCHUNK, 0);
     }
-    for (int it = 0; tile < G::NTILES; ++it, tile += gridDim.x) {
+    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
         const int slot = it % NBUF;
         const int next = tile + gridDim.x;
         if (tid == 0) {
-            if (NBUF > 1 && next < G::NTILES) {
+            if (NBUF > 1 && next < ntiles) {
                 tma_wait_read0();                          // the last store from that slot has read it
                 load(next, (it + 1) % NBUF);
-            } else if (next >= G::NTILES) {
+            } else if (next >= ntiles) {
                 pdl_trigger();
             }
         }
         tma_mbar_wait(mbar0 + 8u * slot, (uint32_t)(it / NBUF) & 1u);
-        aa_tile<OP, Cfg>(S0 + slot * G::TILE, TWS0 + slot * Cfg::TWS, r, w, tid == 0, tile, &mout, &mphys,
-                         SyncBlock{});
+        aa_tile<OP, Cfg, DIST>(S0 + slot * G::TILE, TWS0 + slot * Cfg::TWS, r, w, tid == 0, fs_tile<DIST>(tile, pt),
+                               &mout, &mphys, SyncBlock{});
     }
     if (tid == 0) tma_wait_read0();                        // smem stays valid until the stores have read it
 }
@@ -478,12 +539,24 @@ template <bool COLS> struct B3Geom {
     static constexpr int NTILES = FsGeom::Q * NGROUP;              // 262144 on either axis
 };
 
-template <bool COLS>
+// DIST (sharded plans, R28): Bx on a Y-part (lines of P segments of M points, one
+// per block q: P bulk copies per line each way), By on an X-part (the 4D map
+// {2 Q M doubles, M, Q, P}: 1024 rows of block l1 = P runs of M rows, boxes of 256 rows).
+template <bool COLS, bool DIST = false>
 __global__ void __launch_bounds__(B3Geom<COLS>::NT, 1)
 b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__restrict__ tw32,
-          const double *__restrict__ m2d)
+          const double *__restrict__ m2d, const FsPart pt)
 {
     using G = B3Geom<COLS>;
+    const int64_t ntiles = DIST ? (int64_t)pt.ntiles : (int64_t)G::NTILES;
+    const int ngroup = DIST ? (COLS ? pt.ngroup : pt.rows / G::W) : G::NGROUP;   // tiles per line class
+    // Bx (DIST): segment q of line (row, k1) of the Y-part [q][row][k1][n1_l]; 32-bit
+    // shifts (the lead thread computes these while it issues a tile's copies)
+    auto seg = [&](int64_t tile, int c, int q) -> double2 * {
+        const int ti = (int)tile;
+        const int row = ((ti & (ngroup - 1)) << 2) + c, k1 = ti >> pt.lgNg;
+        return f + ((((int64_t)q * pt.rows + row) << 5) + k1) * pt.M;
+    };
     constexpr int L = G::L, E = G::E, W = G::W, TPT = L / E, NS = G::NSLOT;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t pad = (1024u - (tma_smem(smem_raw) & 1023u)) & 1023u;   // the swizzle pattern's alignment
@@ -501,11 +574,22 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
     auto load = [&](int64_t tile, int s) {
         const uint32_t mb = mbar0 + 8u * s;
         tma_mbar_expect(mb, (uint32_t)G::TILE_BYTES);
-        if constexpr (COLS) {
+        if constexpr (COLS && DIST) {
+            const int l1 = (int)tile >> pt.lgNg, g = (int)tile & (ngroup - 1);
+#pragma unroll
+            for (int k = 0; k < L / G::BOXR; ++k)
+                tma_load4(tma_smem(slot_ptr(s)) + k * G::BOXR * W * 16, &map, 2 * W * g, (k * G::BOXR) & (pt.M - 1), l1,
+                          (k * G::BOXR) >> pt.lgM, mb);
+        } else if constexpr (COLS) {
             const int l1 = (int)(tile / G::NGROUP), g = (int)(tile % G::NGROUP);
 #pragma unroll
             for (int k = 0; k < L / G::BOXR; ++k)
                 tma_load3(tma_smem(slot_ptr(s)) + k * G::BOXR * W * 16, &map, 2 * W * g, 1024 * l1 + k * G::BOXR, 0, mb);
+        } else if constexpr (DIST) {
+#pragma unroll
+            for (int c = 0; c < W; ++c)
+                for (int q = 0; q < pt.P; ++q)
+                    bulk_g2s(tma_smem(slot_ptr(s)) + (c * L + q * pt.M) * 16, seg(tile, c, q), (uint32_t)(pt.M * 16), mb);
         } else if constexpr (FFTPDE_FS_BXCLS) {
 #pragma unroll
             for (int c = 0; c < W; ++c)
@@ -521,7 +605,7 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
         for (int s = 0; s < NS; ++s) {
             const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
             issued[s] = s;
-            if (tile < G::NTILES) load(tile, s);
+            if (tile < ntiles) load(tile, s);
         }
     }
     if constexpr (FFTPDE_FS_B3TW)
@@ -538,7 +622,7 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
     else twp = TwP{tw32, t};
     for (int j = grp;; j += G::NG) {
         const int64_t tile = blockIdx.x + (int64_t)j * gridDim.x;
-        if (tile >= G::NTILES) break;
+        if (tile >= ntiles) break;
         const int s = j % NS;
         double2 *S = slot_ptr(s);
         while (issued[s] != j) {}
@@ -551,7 +635,8 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
         gsync();                                                   // the tile slot becomes the exchange buffers
         const SmemView<double2, Shape<L, E>::LOGE, 1> sm{S + c * G::PITCH};
         const double *m;
-        if constexpr (COLS) m = m2d + (size_t)(tile / G::NGROUP) * L + t;               // class l1
+        if constexpr (DIST) m = m2d + (size_t)((int)tile >> pt.lgNg) * L + t;             // class l1 / k1
+        else if constexpr (COLS) m = m2d + (size_t)(tile / G::NGROUP) * L + t;          // class l1
         else if constexpr (FFTPDE_FS_BXCLS) m = m2d + (size_t)bx_class(tile) * L + t;   // one class per tile
         else m = m2d + (size_t)((tile * W + c) % FsGeom::Q) * L + t;                     // class k1
         const SyncWarp wsync{};
@@ -569,11 +654,22 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
         tma_fence_smem();
         gsync();
         if (tid == 0) {
-            if constexpr (COLS) {
+            if constexpr (COLS && DIST) {
+                const int l1 = (int)tile >> pt.lgNg, g = (int)tile & (ngroup - 1);
+#pragma unroll
+                for (int k = 0; k < L / G::BOXR; ++k)
+                    tma_store4(&map, 2 * W * g, (k * G::BOXR) & (pt.M - 1), l1, (k * G::BOXR) >> pt.lgM,
+                               tma_smem(S) + k * G::BOXR * W * 16);
+            } else if constexpr (COLS) {
                 const int l1 = (int)(tile / G::NGROUP), g = (int)(tile % G::NGROUP);
 #pragma unroll
                 for (int k = 0; k < L / G::BOXR; ++k)
                     tma_store3(&map, 2 * W * g, 1024 * l1 + k * G::BOXR, 0, tma_smem(S) + k * G::BOXR * W * 16);
+            } else if constexpr (DIST) {
+#pragma unroll
+                for (int c = 0; c < W; ++c)
+                    for (int q = 0; q < pt.P; ++q)
+                        bulk_s2g(seg(tile, c, q), tma_smem(S) + (c * L + q * pt.M) * 16, (uint32_t)(pt.M * 16));
             } else if constexpr (FFTPDE_FS_BXCLS) {
 #pragma unroll
                 for (int c = 0; c < W; ++c) bulk_s2g(f + bx_line(tile, c) * L, tma_smem(S) + c * L * 16, (uint32_t)(L * 16));
@@ -583,7 +679,7 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
             tma_commit();
             const int64_t nt = blockIdx.x + (int64_t)(j + NS) * gridDim.x;
             tma_wait_read0();                                      // the slot is free once the store has read it
-            if (nt < G::NTILES) load(nt, s);
+            if (nt < ntiles) load(nt, s);
             issued[s] = j + NS;
         }
     }

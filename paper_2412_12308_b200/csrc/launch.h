@@ -182,6 +182,12 @@ cudaError_t launch_peer_transpose(const void *src, const PeerPtrs &peers, int P,
 // over 1024-point lines with the 2D factors (OpTables::ey2d).
 bool fourstep_supported(int64_t nx, int64_t ny, int64_t batch, int elem_bytes);
 cudaError_t launch_aa(int op, const void *in, void *out, void *phys, const void *tw, cudaStream_t st);
+// the distributed four-step of sharded plans (R28, fourstep.cu / pack.cu)
+bool fs_dist_supported(int P);
+cudaError_t launch_aa_part(int op, int P, int rank, int xmode, const void *in, void *out, void *phys, const void *tw,
+                           cudaStream_t st);
+cudaError_t launch_fs_b_part(bool cols, int P, int rank, void *f, const void *tw32, const double *m2d, cudaStream_t st);
+cudaError_t launch_fs_perm(const void *in, void *out, int P, int direction, cudaStream_t st);
 cudaError_t launch_fs_bb(void *f, const void *tw32, const double *mx2d, const double *my2d, void *sync,
                          cudaStream_t st);
 bool fs_bb_enabled();

@@ -84,4 +84,46 @@ cudaError_t launch_peer_transpose(const void *src, const PeerPtrs &peers, int P,
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// The row slab <-> distributed four-step layout permutation (R28), 16-byte elements:
+//   A = [T][P][M][Q][P][M]  (m2_l, r, m1_l, n2, q, n1_l): a rank's row slab, rows
+//        y = m1 + 1024 m2 with m1 = r M + m1_l, x = n1 + 1024 n2 with n1 = q M + n1_l
+//   B = [P][P][T][M][Q][M]  (r, q, m2_l, m1_l, n2, n1_l): block r is the part of the
+//        slab Y-part rank r owns, ordered as it needs it
+// direction 0: A -> B, direction 1: B -> A.  Runs of M contiguous elements on both sides.
+__global__ void fs_perm_kernel(const int4 *__restrict__ in, int4 *__restrict__ out, int64_t T, int64_t P, int64_t M,
+                               int64_t Q, int direction)
+{
+    const int64_t total = T * P * M * Q * P * M;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = i % M;
+        int64_t s = i / M;
+        int64_t r, q, m2, m1, n2;
+        if (direction == 0) {              // i walks B
+            n2 = s % Q; s /= Q;
+            m1 = s % M; s /= M;
+            m2 = s % T; s /= T;
+            q = s % P; r = s / P;
+            out[i] = in[((((m2 * P + r) * M + m1) * Q + n2) * P + q) * M + e];
+        } else {                           // i walks A
+            q = s % P; s /= P;
+            n2 = s % Q; s /= Q;
+            m1 = s % M; s /= M;
+            r = s % P; m2 = s / P;
+            out[i] = in[((((r * P + q) * T + m2) * M + m1) * Q + n2) * M + e];
+        }
+    }
+}
+
+cudaError_t launch_fs_perm(const void *in, void *out, int P, int direction, cudaStream_t st)
+{
+    const int64_t M = 1024 / P, T = 32 / P, Q = 32;
+    const int64_t total = T * P * M * Q * P * M;
+    int64_t grid = (total + 255) / 256;
+    if (grid > 148 * 16) grid = 148 * 16;
+    fs_perm_kernel<<<(unsigned)grid, 256, 0, st>>>((const int4 *)in, (int4 *)out, T, P, M, Q, direction);
+    return cudaGetLastError();
+}
+
 } // namespace fftpde
