@@ -194,6 +194,26 @@ static bool by_map_part(CUtensorMap &m, const void *p, int M, int P)
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// a Y-part for Bx as the 5D tensor {2 MI doubles, M / MI, Q (k1), Q M (rows), P (q)},
+// MI = min(M, 128) points; one box = a tile: {2 MI, M / MI, 4 k1, 1 row, P} (FFTPDE_FSD_BXK)
+static bool bx_map_part(CUtensorMap &m, const void *p, int M, int P)
+{
+    using G = FsGeom;
+    auto enc = tma_encoder();
+    if (!enc) return false;
+    const int MI = std::min(M, 128);
+    const cuuint64_t e = 16;
+    cuuint64_t dims[5] = {(cuuint64_t)(2 * MI), (cuuint64_t)(M / MI), (cuuint64_t)G::Q, (cuuint64_t)G::Q * M,
+                          (cuuint64_t)P};
+    cuuint64_t strides[4] = {e * MI, e * M, e * M * G::Q, e * M * G::Q * G::Q * M};
+    cuuint32_t box[5] = {(cuuint32_t)(2 * MI), (cuuint32_t)(M / MI), FFTPDE_FSD_BXK ? (cuuint32_t)G::W : 1,
+                         FFTPDE_FSD_BXK ? 1 : (cuuint32_t)G::W, (cuuint32_t)P};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void *>(p), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, FFTPDE_FS_PROMO_BY,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <bool COLS, bool DIST = false>
 static cudaError_t launch_b3(void *f, const void *tw32, const double *m2d, cudaStream_t st, const FsPart &pt = FsPart{})
 {
@@ -203,8 +223,8 @@ static cudaError_t launch_b3(void *f, const void *tw32, const double *m2d, cudaS
         if (!by_map_part(m, f, pt.M, pt.P)) return cudaErrorNotSupported;
     } else if (!DIST && !by_map(m, f, CU_TENSOR_MAP_SWIZZLE_64B)) {
         return cudaErrorNotSupported;
-    } else if (DIST) {
-        std::memset(&m, 0, sizeof m);                        // Bx (DIST) moves its lines by bulk copies
+    } else if (DIST && !bx_map_part(m, f, pt.M, pt.P)) {
+        return cudaErrorNotSupported;
     }
     auto k = b3_kernel<COLS, DIST>;
     static SmemOptIn<decltype(k)> opt;

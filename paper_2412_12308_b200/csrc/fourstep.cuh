@@ -524,6 +524,9 @@ __device__ __forceinline__ int64_t bx_line(int64_t tile, int c)
     return (yb * FsGeom::W + c) * FsGeom::Q + bx_class(tile);   // line = grid row * 32 + segment
 }
 
+#ifndef FFTPDE_FSD_BXK
+#define FFTPDE_FSD_BXK 1
+#endif
 template <bool COLS> struct B3Geom {
     static constexpr int L = 1024, E = 32, W = 4, BOXR = 256;
     static constexpr int GT = W * (L / E);                          // 128 threads per group
@@ -550,13 +553,13 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
     using G = B3Geom<COLS>;
     const int64_t ntiles = DIST ? (int64_t)pt.ntiles : (int64_t)G::NTILES;
     const int ngroup = DIST ? (COLS ? pt.ngroup : pt.rows / G::W) : G::NGROUP;   // tiles per line class
-    // Bx (DIST): segment q of line (row, k1) of the Y-part [q][row][k1][n1_l]; 32-bit
-    // shifts (the lead thread computes these while it issues a tile's copies)
-    auto seg = [&](int64_t tile, int c, int q) -> double2 * {
-        const int ti = (int)tile;
-        const int row = ((ti & (ngroup - 1)) << 2) + c, k1 = ti >> pt.lgNg;
-        return f + ((((int64_t)q * pt.rows + row) << 5) + k1) * pt.M;
-    };
+    // Bx (DIST): the tile arrives as [q][c][n1_l] (segment q of line c at (q W + c) M).
+    // FFTPDE_FSD_BXK: a tile = 4 consecutive k1 of one row (runs of 4 M points per
+    // block q; loopback P = 8 with 4 rows of one k1 -- 2 KiB runs at 64 KiB stride --
+    // cost 226 ms of Bx per solve against 157 at P = 1); else 4 rows of one k1
+    auto bxi = [&](int c, int n1) { return (((n1 >> pt.lgM) << 2) + c) * pt.M + (n1 & (pt.M - 1)); };
+    auto bxk = [&](int ti) { return FFTPDE_FSD_BXK ? (ti & (FsGeom::Q / G::W - 1)) * G::W : ti >> pt.lgNg; };
+    auto bxr = [&](int ti) { return FFTPDE_FSD_BXK ? ti / (FsGeom::Q / G::W) : (ti & (ngroup - 1)) << 2; };
     constexpr int L = G::L, E = G::E, W = G::W, TPT = L / E, NS = G::NSLOT;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t pad = (1024u - (tma_smem(smem_raw) & 1023u)) & 1023u;   // the swizzle pattern's alignment
@@ -585,11 +588,9 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
 #pragma unroll
             for (int k = 0; k < L / G::BOXR; ++k)
                 tma_load3(tma_smem(slot_ptr(s)) + k * G::BOXR * W * 16, &map, 2 * W * g, 1024 * l1 + k * G::BOXR, 0, mb);
-        } else if constexpr (DIST) {
-#pragma unroll
-            for (int c = 0; c < W; ++c)
-                for (int q = 0; q < pt.P; ++q)
-                    bulk_g2s(tma_smem(slot_ptr(s)) + (c * L + q * pt.M) * 16, seg(tile, c, q), (uint32_t)(pt.M * 16), mb);
+        } else if constexpr (DIST) {       // one 5D box: [q][4 lines][n1_l] (bx_map_part)
+            const int ti = (int)tile;
+            tma_load5(tma_smem(slot_ptr(s)), &map, 0, 0, bxk(ti), bxr(ti), 0, mb);
         } else if constexpr (FFTPDE_FS_BXCLS) {
 #pragma unroll
             for (int c = 0; c < W; ++c)
@@ -631,11 +632,13 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
 #pragma unroll
         for (int e = 0; e < E; ++e) v[e] = COLS ? *reinterpret_cast<const double2 *>(
                                                      reinterpret_cast<const unsigned char *>(S) + swz64((uint32_t)(t + TPT * e) * 64u + 16u * c))
+                                          : DIST ? S[bxi(c, t + TPT * e)]
                                                : S[c * L + t + TPT * e];
         gsync();                                                   // the tile slot becomes the exchange buffers
         const SmemView<double2, Shape<L, E>::LOGE, 1> sm{S + c * G::PITCH};
         const double *m;
-        if constexpr (DIST) m = m2d + (size_t)((int)tile >> pt.lgNg) * L + t;             // class l1 / k1
+        if constexpr (DIST && !COLS && FFTPDE_FSD_BXK) m = m2d + (size_t)(bxk((int)tile) + c) * L + t;   // class k1 of line c
+        else if constexpr (DIST) m = m2d + (size_t)((int)tile >> pt.lgNg) * L + t;        // class l1 / k1
         else if constexpr (COLS) m = m2d + (size_t)(tile / G::NGROUP) * L + t;          // class l1
         else if constexpr (FFTPDE_FS_BXCLS) m = m2d + (size_t)bx_class(tile) * L + t;   // one class per tile
         else m = m2d + (size_t)((tile * W + c) % FsGeom::Q) * L + t;                     // class k1
@@ -649,6 +652,7 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
         for (int e = 0; e < E; ++e) {
             if constexpr (COLS)
                 *reinterpret_cast<double2 *>(reinterpret_cast<unsigned char *>(S) + swz64((uint32_t)(t + TPT * e) * 64u + 16u * c)) = v[e];
+            else if constexpr (DIST) S[bxi(c, t + TPT * e)] = v[e];
             else S[c * L + t + TPT * e] = v[e];
         }
         tma_fence_smem();
@@ -666,10 +670,8 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
                 for (int k = 0; k < L / G::BOXR; ++k)
                     tma_store3(&map, 2 * W * g, 1024 * l1 + k * G::BOXR, 0, tma_smem(S) + k * G::BOXR * W * 16);
             } else if constexpr (DIST) {
-#pragma unroll
-                for (int c = 0; c < W; ++c)
-                    for (int q = 0; q < pt.P; ++q)
-                        bulk_s2g(seg(tile, c, q), tma_smem(S) + (c * L + q * pt.M) * 16, (uint32_t)(pt.M * 16));
+                const int ti = (int)tile;
+                tma_store5(&map, 0, 0, bxk(ti), bxr(ti), 0, tma_smem(S));
             } else if constexpr (FFTPDE_FS_BXCLS) {
 #pragma unroll
                 for (int c = 0; c < W; ++c) bulk_s2g(f + bx_line(tile, c) * L, tma_smem(S) + c * L * 16, (uint32_t)(L * 16));
