@@ -13,9 +13,11 @@ materialised every step).  The metric is grid-points per second
 Multi-GPU: ``--gpus N`` with N > 1 launches N ranks itself (torch.distributed.run,
 127.0.0.1) unless WORLD_SIZE is already set, and checks WORLD_SIZE == N.  C5 at
 N > 1 runs the row-slab decomposition of SURVEY.md 8(e) (strong scaling, fixed
-32768^2 grid); the default exchange is ``lib``: the distributed four-step inside
-libfftpde (R28: each rank runs the single-GPU four-step passes on its
-Y-part / X-part of the field, one NCCL all-to-all per solve step).  C1-C4 at N > 1 run independent
+32768^2 grid); the default exchange is ``fs``: the distributed four-step (DESIGN.md
+R28: each rank runs the single-GPU four-step passes on its Y-part / X-part of the
+field) with the part-to-part exchange fused into the B passes (peer stores over
+NVLink into torch symmetric memory, one barrier per solve step); ``lib`` runs the
+same passes inside libfftpde with one NCCL all-to-all per step.  C1-C4 at N > 1 run independent
 replicas (weak scaling, no collective on the data path).
 
 Timing: W untimed warm-up steps, then exactly K steps, each bracketed by CUDA
@@ -88,9 +90,11 @@ def parse_args():
     ap.add_argument("--pencil", default=None, metavar="PZxPY",
                     help="3D workloads: the pencil decomposition on a PZ x PY process grid (PZ*PY = --gpus; "
                          "fftpde_plan_3d_pencil) instead of z-slabs")
-    ap.add_argument("--exchange", default="lib", choices=["fused", "nccl", "peer", "lib"],
-                    help="sharded c5: the distributed four-step inside libfftpde (fftpde_plan_2d_sharded, one "
-                         "NCCL all-to-all per step; default), or the round-1 slab solvers: exchanges fused into "
+    ap.add_argument("--exchange", default="fs", choices=["fs", "lib", "fused", "nccl", "peer"],
+                    help="sharded c5: the distributed four-step with its exchange fused into the B passes (peer "
+                         "stores into torch symmetric memory; default, falls back to lib), the distributed "
+                         "four-step inside libfftpde (fftpde_plan_2d_sharded, one NCCL all-to-all per step), "
+                         "or the round-1 slab solvers: exchanges fused into "
                          "the row / column passes (peer stores into torch symmetric memory), pack + NCCL "
                          "all-to-all, a separate peer-store transpose")
     return ap.parse_args()
@@ -796,7 +800,20 @@ def sharded_native(args, wl, world, rank, local):
     del full
     torch.cuda.empty_cache()
     exchange = args.exchange
-    if exchange == "lib":     # the whole slab solve inside the C ABI (fftpde_plan_2d_sharded)
+    fallback = None
+    if exchange == "fs":      # R28 with the exchange fused into the B passes (peer stores, symmetric memory)
+        try:
+            ops = S.CudaLocalOps(wl.nx, wl.ny, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly)
+            solver = S.FusedFourStepSolver(wl.nx, S.SymmetricPeerComm() if world > 1 else S.LoopbackPeerComm(1),
+                                           ops.plan)
+        except Exception as e:  # no peer-mapped symmetric memory here: the in-library NCCL exchange
+            fallback = f"fs unavailable ({type(e).__name__}: {e}); lib"
+            exchange = "lib"
+            ops = solver = None
+            torch.cuda.empty_cache()
+    if exchange == "fs":
+        pass
+    elif exchange == "lib":     # the whole slab solve inside the C ABI (fftpde_plan_2d_sharded)
         from paper_2412_12308_b200 import fftpde as F
         ops = _LibSharded(F.ShardedPlan(wl.nx, wl.ny, dtype=dtype, Lx=wl.Lx, Ly=wl.Ly))
         solver = ops
@@ -869,7 +886,7 @@ def sharded_native(args, wl, world, rank, local):
     # (3 x slab) and ONE all-to-all; per solve the row-slab <-> Y-part conversion (a
     # permutation and a block swap each way, 8 x slab) and two more all-to-alls
     slab_bytes = (hi - lo) * wl.nx * 16
-    if exchange == "lib":
+    if exchange in ("lib", "fs"):
         conv = 1 if world > 1 else 0        # P = 1: the parts are the row slab, no conversion
         hbm_step = (7 + conv * 8 / wl.nsteps) * slab_bytes
         nvl_bytes = int(slab_bytes * (world - 1) / world * (1 + 2 / wl.nsteps))
@@ -903,7 +920,10 @@ def sharded_native(args, wl, world, rank, local):
                        "fused": "(row and column passes store into the peers' slabs, symmetric memory; separable diffusion)",
                        "nccl": "(NCCL all-to-all, Python-driven)",
                        "lib": "(distributed four-step inside libfftpde, fftpde_plan_2d_sharded: Y-/X-parts, one NCCL "
-                              "all-to-all per step)"}[exchange],
+                              "all-to-all per step)",
+                       "fs": "(distributed four-step, the Y-/X-part exchange fused into the B passes: peer stores "
+                             "into symmetric memory, one barrier per step)"}[exchange]
+                   + (f" [{fallback}]" if fallback else ""),
                    "l2": "field (16 GiB) larger than L2; 256 MiB buffer zeroed between timed steps"},
         "e2e": e2e, "cpu_baseline": None, "clocks": clocks, "parity": parity,
         "roofline": roofline, "gpu_launches": launches,

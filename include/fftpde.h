@@ -353,6 +353,42 @@ fftpde_status fftpde_wave_rk4(fftpde_plan plan, void *u, void *ut, double c,
 fftpde_status fftpde_peer_transpose(fftpde_plan plan, const void *src, void *const *peers, int npeers, int rank,
                                     int64_t R, int64_t bw, int direction);
 
+/* The distributed four-step of the 32768^2 complex128 diffusion (R28;
+ * the four-step split N = 1024 x 32 of each axis, PAPER.md:262-273 applied inside
+ * the axis) as per-rank pieces, for callers that run their own ranks and exchanges
+ * (sharded.FusedFourStepSolver: torch symmetric memory, the exchange fused into
+ * the B passes).  plan: a plain 2D plan of the whole 32768 x 32768 complex128
+ * grid (batch 1); anything else returns FFTPDE_ERR_UNSUPPORTED.  nranks = P, a
+ * power of two <= 32; M = 1024 / P.  A rank's PART is an array of 2^30 / P
+ * complex128 in the layout [P][32][M][32][M]:
+ *   Y-part (xmode 0) of rank r: element (blk q, a, m1_l, b, n1_l) is grid point
+ *     y = (r M + m1_l) + 1024 a, x = (q M + n1_l) + 1024 b;
+ *   X-part (xmode 1) of rank q: element (blk r, a, m1_l, b, n1_l) is the same
+ *     point (r M + m1_l) + 1024 a, (q M + n1_l) + 1024 b;
+ * (in the AA domain a, b are the high-index wavenumbers l1, k1).  So block q of
+ * rank r's Y-part and block r of rank q's X-part hold the same points in the same
+ * order: the Y <-> X transpose is an all-to-all of whole blocks.
+ * fftpde_fs_part_aa: op 0 AA (physical part -> AA domain), 1 AA^-1 (-> physical,
+ *   x 1 / N^2 from the B passes' factors), 2 MID (AA^-1 -> phys, then AA -> out);
+ *   in == out allowed; phys only for op 2.
+ * fftpde_fs_part_b: the 1024-point diffusion of the part's local axis (xmode 0: x
+ *   on a Y-part, xmode 1: y on an X-part) with e^{-D k^2 dt}/32768, in place when
+ *   peers == NULL; with peers (npeers == nranks device pointers, peer-mapped:
+ *   torch symmetric memory, CUDA IPC, or one device's buffers in a single-process
+ *   emulation) the result is stored straight into the OTHER part of every rank
+ *   (block q -> peers[q] at block `rank`; xmode 1 needs nranks <= 8), f is left
+ *   unchanged, and the caller orders the phase against the peers with a
+ *   stream-ordered barrier.
+ * fftpde_fs_part_perm: direction 0: a rank's row slab (rows [r 32768/P, ..)) ->
+ *   [P][P][32/P][M][32][M] (block r = the part of the slab Y-part rank r owns,
+ *   in its order); direction 1 the inverse (in != out).
+ * Pointers 16-byte aligned, on the plan's device; asynchronous on its stream. */
+fftpde_status fftpde_fs_part_aa(fftpde_plan plan, int op, int nranks, int rank, int xmode, const void *in, void *out,
+                                void *phys);
+fftpde_status fftpde_fs_part_b(fftpde_plan plan, int xmode, int nranks, int rank, void *f, double D, double dt,
+                               void *const *peers, int npeers);
+fftpde_status fftpde_fs_part_perm(fftpde_plan plan, int nranks, const void *in, void *out, int direction);
+
 /* fftpde_rows_to_peers: the row pass of this rank's slab with the exchange fused
  *   into its epilogue: the output element a of row k is
  *   stored straight into peers[a / bw] at row rank R + k, column a mod bw, of

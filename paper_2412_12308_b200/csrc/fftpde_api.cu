@@ -1981,6 +1981,76 @@ fftpde_status fftpde_peer_transpose(fftpde_plan p, const void *src, void *const 
     return cuda_status(launch_peer_transpose(src, pp, npeers, rank, R, bytes, direction, p->stream));
 }
 
+// ---- the distributed four-step pieces (R28) on a plain 32768^2 complex128 plan -------
+namespace {
+fftpde_status fs_part_args(fftpde_plan p, int nranks, int rank)
+{
+    if (!p || nranks < 1 || rank < 0 || rank >= nranks) return FFTPDE_ERR_INVALID_ARG;
+    if (p->is3d || p->is_real || p->sharded || !p->fs || !fftpde::fs_dist_supported(nranks)) return FFTPDE_ERR_UNSUPPORTED;
+    if (!p->ws) return FFTPDE_ERR_WORKSPACE;
+    return FFTPDE_OK;
+}
+bool aligned16(const void *q) { return q && ((uintptr_t)q & 15u) == 0; }
+} // namespace
+
+fftpde_status fftpde_fs_part_aa(fftpde_plan p, int op, int nranks, int rank, int xmode, const void *in, void *out,
+                                void *phys)
+{
+    fftpde_status s = fs_part_args(p, nranks, rank);
+    if (s != FFTPDE_OK) return s;
+    if (op < 0 || op > 2 || (xmode != 0 && xmode != 1) || !aligned16(in) || !aligned16(out) ||
+        (op == 2) != (phys != nullptr) || (phys && !aligned16(phys)))
+        return FFTPDE_ERR_INVALID_ARG;
+    return dispatch(p, 1, p->nx * p->ny, [&](auto &) {
+        return launch(p, FFTPDE_KERNEL_AA, [&] {
+            return launch_aa_part(op, nranks, rank, xmode, in, out, phys, p->ws + p->o_fs_tw, p->stream);
+        });
+    });
+}
+
+fftpde_status fftpde_fs_part_b(fftpde_plan p, int xmode, int nranks, int rank, void *f, double D, double dt,
+                               void *const *peers, int npeers)
+{
+    fftpde_status s = fs_part_args(p, nranks, rank);
+    if (s != FFTPDE_OK) return s;
+    if ((xmode != 0 && xmode != 1) || !aligned16(f) || !std::isfinite(D) || !std::isfinite(dt) || D < 0 || dt < 0)
+        return FFTPDE_ERR_INVALID_ARG;
+    PeerPtrs pp{};
+    if (peers) {
+        if (npeers != nranks) return FFTPDE_ERR_INVALID_ARG;
+        if (xmode == 1 && nranks > fftpde::kFsMaxPeerMaps) return FFTPDE_ERR_UNSUPPORTED;
+        for (int q = 0; q < npeers; ++q) {
+            if (!aligned16(peers[q])) return FFTPDE_ERR_INVALID_ARG;
+            pp.p[q] = peers[q];
+        }
+    }
+    {
+        DeviceGuard g(p->device);
+        if (!g.ok) return FFTPDE_ERR_CUDA;
+        s = ensure_diffusion_tables(p, D, dt);
+    }
+    if (s != FFTPDE_OK) return s;
+    return dispatch(p, 1, p->nx * p->ny, [&](auto &) {
+        return launch(p, xmode ? FFTPDE_KERNEL_COL : FFTPDE_KERNEL_ROW, [&] {
+            return launch_fs_b_part(xmode != 0, nranks, rank, f, p->ws + p->o_fs_tw32,
+                                    (const double *)(p->ws + (xmode ? p->o_fs_my : p->o_fs_mx)), p->stream,
+                                    peers ? &pp : nullptr);
+        });
+    });
+}
+
+fftpde_status fftpde_fs_part_perm(fftpde_plan p, int nranks, const void *in, void *out, int direction)
+{
+    fftpde_status s = fs_part_args(p, nranks, 0);
+    if (s != FFTPDE_OK) return s;
+    if (!aligned16(in) || !aligned16(out) || in == out || (direction != 0 && direction != 1))
+        return FFTPDE_ERR_INVALID_ARG;
+    DeviceGuard g(p->device);
+    if (!g.ok) return FFTPDE_ERR_CUDA;
+    ++p->launches;
+    return cuda_status(launch_fs_perm(in, out, nranks, direction, p->stream));
+}
+
 fftpde_status fftpde_rows_to_peers(fftpde_plan p, const void *in, void *const *peers, int npeers, int rank,
                                    int64_t R, int op, double D, double dt)
 {

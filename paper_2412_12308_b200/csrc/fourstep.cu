@@ -214,8 +214,25 @@ static bool bx_map_part(CUtensorMap &m, const void *p, int M, int P)
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// the peer Y-part q as a By store target: by_map_part with boxes of min(M, 256) rows of one block
+static bool by_map_peer(CUtensorMap &m, const void *p, int M, int P)
+{
+    using G = FsGeom;
+    auto enc = tma_encoder();
+    if (!enc) return false;
+    const cuuint64_t row = (cuuint64_t)G::Q * M * 16;
+    cuuint64_t dims[4] = {(cuuint64_t)(2 * G::Q * M), (cuuint64_t)M, (cuuint64_t)G::Q, (cuuint64_t)P};
+    cuuint64_t strides[3] = {row, row * M, row * M * G::Q};
+    cuuint32_t box[4] = {(cuuint32_t)(2 * ByGeom::W), (cuuint32_t)std::min(M, ByGeom::BOXR), 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void *>(p), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, FFTPDE_FS_PROMO_BY,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <bool COLS, bool DIST = false>
-static cudaError_t launch_b3(void *f, const void *tw32, const double *m2d, cudaStream_t st, const FsPart &pt = FsPart{})
+static cudaError_t launch_b3(void *f, const void *tw32, const double *m2d, cudaStream_t st, const FsPart &pt = FsPart{},
+                             const PeerPtrs *peers = nullptr)
 {
     using G = B3Geom<COLS>;
     CUtensorMap m;
@@ -225,6 +242,16 @@ static cudaError_t launch_b3(void *f, const void *tw32, const double *m2d, cudaS
         return cudaErrorNotSupported;
     } else if (DIST && !bx_map_part(m, f, pt.M, pt.P)) {
         return cudaErrorNotSupported;
+    }
+    PeerPtrs pp{};
+    static FsPeerMaps pm;                                    // copied into the launch's parameters
+    std::memset(&pm, 0, sizeof pm);
+    if (DIST && pt.topeer) {
+        if (!peers || pt.P > kMaxPeers || (COLS && pt.P > kFsMaxPeerMaps)) return cudaErrorNotSupported;
+        pp = *peers;
+        if (COLS)
+            for (int r = 0; r < pt.P; ++r)
+                if (!by_map_peer(pm.m[r], pp.p[r], pt.M, pt.P)) return cudaErrorNotSupported;
     }
     auto k = b3_kernel<COLS, DIST>;
     static SmemOptIn<decltype(k)> opt;
@@ -240,15 +267,17 @@ static cudaError_t launch_b3(void *f, const void *tw32, const double *m2d, cudaS
     }
     const unsigned grid = (unsigned)std::min<int64_t>(DIST ? pt.ntiles : G::NTILES, (int64_t)occ * sm_count());
     e = launch_fam(PDL_FOURSTEP, k, dim3(grid), dim3(G::NT), G::BYTES, st, m, (double2 *)f, (const double2 *)tw32, m2d,
-                   pt);
+                   pt, pp, pm);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 // the B pass of a rank's part (R28): Bx on a Y-part (cols false), By on an X-part (cols true)
-cudaError_t launch_fs_b_part(bool cols, int P, int rank, void *f, const void *tw32, const double *m2d, cudaStream_t st)
+cudaError_t launch_fs_b_part(bool cols, int P, int rank, void *f, const void *tw32, const double *m2d, cudaStream_t st,
+                             const PeerPtrs *peers)
 {
-    const FsPart pt = fs_part(P, rank, cols ? 1 : 0, 1);
-    return cols ? launch_b3<true, true>(f, tw32, m2d, st, pt) : launch_b3<false, true>(f, tw32, m2d, st, pt);
+    FsPart pt = fs_part(P, rank, cols ? 1 : 0, 1);
+    pt.topeer = peers != nullptr;
+    return cols ? launch_b3<true, true>(f, tw32, m2d, st, pt, peers) : launch_b3<false, true>(f, tw32, m2d, st, pt, peers);
 }
 static int fs_b3_mask()
 {

@@ -26,6 +26,7 @@
 #include "fft_core.cuh"
 #include "tmacols.cuh"
 #include "line.cuh"
+#include "launch.h"
 
 namespace fftpde {
 
@@ -114,6 +115,11 @@ struct FsPart {
     int rows;      // Bx: local rows (Q M)
     int ngroup;    // By: 4-column groups per 1024-row block (Q M / W)
     int lgM, lgNb, lgMW, lgNg;   // log2 of M, nb, M / W and of the B pass's tiles per line class
+    int topeer;    // B pass: store the result into the peers' other part (the exchange fused, R28)
+};
+// the peers' Y-parts as By store maps ({2 Q M doubles, M, Q, P}, boxes of 64 B x min(M, 256) rows)
+struct FsPeerMaps {
+    CUtensorMap m[kFsMaxPeerMaps];
 };
 struct FsTile { int m1, chunk, cx, cm, cb; };     // global m1 and n1-chunk; tensor coordinates
 template <bool DIST> __device__ __forceinline__ FsTile fs_tile(int tile, const FsPart &pt)
@@ -545,10 +551,16 @@ template <bool COLS> struct B3Geom {
 // DIST (sharded plans, R28): Bx on a Y-part (lines of P segments of M points, one
 // per block q: P bulk copies per line each way), By on an X-part (the 4D map
 // {2 Q M doubles, M, Q, P}: 1024 rows of block l1 = P runs of M rows, boxes of 256 rows).
+// topeer (DIST): the exchange fused into the epilogue.  Block q of this rank's
+// Y-part is block `rank` of rank q's X-part at the same offset inside the block
+// (and the other way round), so Bx stores the tile's run of block q (4 M points)
+// with one bulk copy into peers.p[q], and By stores its rows of m1 block r with
+// TMA boxes through pmaps.m[r] (the peers' Y-parts).
 template <bool COLS, bool DIST = false>
 __global__ void __launch_bounds__(B3Geom<COLS>::NT, 1)
 b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__restrict__ tw32,
-          const double *__restrict__ m2d, const FsPart pt)
+          const double *__restrict__ m2d, const FsPart pt, const PeerPtrs peers,
+          const __grid_constant__ FsPeerMaps pmaps)
 {
     using G = B3Geom<COLS>;
     const int64_t ntiles = DIST ? (int64_t)pt.ntiles : (int64_t)G::NTILES;
@@ -660,10 +672,18 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
         if (tid == 0) {
             if constexpr (COLS && DIST) {
                 const int l1 = (int)tile >> pt.lgNg, g = (int)tile & (ngroup - 1);
+                if (pt.topeer) {                   // rows of m1 block r -> rank r's Y-part, block `rank`
+                    const int br = pt.M < G::BOXR ? pt.M : G::BOXR;
+                    for (int j = 0; j < L / br; ++j) {
+                        const int r = (j * br) >> pt.lgM;
+                        tma_store4(&pmaps.m[r], 2 * W * g, (j * br) & (pt.M - 1), l1, pt.rank, tma_smem(S) + j * br * W * 16);
+                    }
+                } else {
 #pragma unroll
-                for (int k = 0; k < L / G::BOXR; ++k)
-                    tma_store4(&map, 2 * W * g, (k * G::BOXR) & (pt.M - 1), l1, (k * G::BOXR) >> pt.lgM,
-                               tma_smem(S) + k * G::BOXR * W * 16);
+                    for (int k = 0; k < L / G::BOXR; ++k)
+                        tma_store4(&map, 2 * W * g, (k * G::BOXR) & (pt.M - 1), l1, (k * G::BOXR) >> pt.lgM,
+                                   tma_smem(S) + k * G::BOXR * W * 16);
+                }
             } else if constexpr (COLS) {
                 const int l1 = (int)(tile / G::NGROUP), g = (int)(tile % G::NGROUP);
 #pragma unroll
@@ -671,7 +691,14 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
                     tma_store3(&map, 2 * W * g, 1024 * l1 + k * G::BOXR, 0, tma_smem(S) + k * G::BOXR * W * 16);
             } else if constexpr (DIST) {
                 const int ti = (int)tile;
-                tma_store5(&map, 0, 0, bxk(ti), bxr(ti), 0, tma_smem(S));
+                if (pt.topeer) {                   // block q's run (4 k1 x M points) -> rank q's X-part, block `rank`
+                    const int64_t off = (((int64_t)pt.rank * pt.rows + bxr(ti)) * FsGeom::Q + bxk(ti)) * pt.M;
+                    for (int q = 0; q < pt.P; ++q)
+                        bulk_s2g(reinterpret_cast<double2 *>(peers.p[q]) + off, tma_smem(S) + q * W * pt.M * 16,
+                                 (uint32_t)(W * pt.M * 16));
+                } else {
+                    tma_store5(&map, 0, 0, bxk(ti), bxr(ti), 0, tma_smem(S));
+                }
             } else if constexpr (FFTPDE_FS_BXCLS) {
 #pragma unroll
                 for (int c = 0; c < W; ++c) bulk_s2g(f + bx_line(tile, c) * L, tma_smem(S) + c * L * 16, (uint32_t)(L * 16));
@@ -685,7 +712,10 @@ b3_kernel(const __grid_constant__ CUtensorMap map, double2 *f, const double2 *__
             issued[s] = j + NS;
         }
     }
-    if (tid == 0) tma_wait_read0();
+    if (tid == 0) {
+        if (DIST && pt.topeer) tma_wait0();                        // the peer stores are performed
+        else tma_wait_read0();
+    }
 }
 
 

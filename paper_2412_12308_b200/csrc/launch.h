@@ -7,6 +7,7 @@ namespace fftpde {
 
 // Peer pointers of the slab exchange (pack.cu), passed by value.
 constexpr int kMaxPeers = 16;
+constexpr int kFsMaxPeerMaps = 8;   // distributed four-step By peer stores: one tensor map per peer (R28)
 struct PeerPtrs {
     void *p[kMaxPeers];
 };
@@ -186,7 +187,8 @@ cudaError_t launch_aa(int op, const void *in, void *out, void *phys, const void 
 bool fs_dist_supported(int P);
 cudaError_t launch_aa_part(int op, int P, int rank, int xmode, const void *in, void *out, void *phys, const void *tw,
                            cudaStream_t st);
-cudaError_t launch_fs_b_part(bool cols, int P, int rank, void *f, const void *tw32, const double *m2d, cudaStream_t st);
+cudaError_t launch_fs_b_part(bool cols, int P, int rank, void *f, const void *tw32, const double *m2d, cudaStream_t st,
+                             const PeerPtrs *peers = nullptr);   // peers: store into the peers' other part
 cudaError_t launch_fs_perm(const void *in, void *out, int P, int direction, cudaStream_t st);
 cudaError_t launch_fs_bb(void *f, const void *tw32, const double *mx2d, const double *my2d, void *sync,
                          cudaStream_t st);

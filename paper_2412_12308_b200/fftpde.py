@@ -40,7 +40,7 @@ EXPORTS = [
     "fftpde_wave_rk4_scratch_size", "fftpde_wave_rk4",
     "fftpde_apply", "fftpde_diffuse_source_scratch_size", "fftpde_diffuse_source",
     "fftpde_plan_3d", "fftpde_plan_2d_r2c", "fftpde_peer_transpose", "fftpde_rows_to_peers",
-    "fftpde_cols_to_peers",
+    "fftpde_cols_to_peers", "fftpde_fs_part_aa", "fftpde_fs_part_b", "fftpde_fs_part_perm",
 ]
 KOP = {"laplacian": 0, "dx": 1, "dy": 2}
 OP_POISSON, OP_DIFFUSE, OP_DIFFUSE_Y = 2, 3, 5
@@ -101,6 +101,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fftpde_peer_transpose": (st, [p, p, ctypes.POINTER(p), u, u, i64, i64, u]),
         "fftpde_rows_to_peers": (st, [p, p, ctypes.POINTER(p), u, u, i64, u, dbl, dbl]),
         "fftpde_cols_to_peers": (st, [p, p, ctypes.POINTER(p), u, u, i64, u, dbl, dbl]),
+        "fftpde_fs_part_aa": (st, [p, u, u, u, u, p, p, p]),
+        "fftpde_fs_part_b": (st, [p, u, u, u, p, dbl, dbl, ctypes.POINTER(p), u]),
+        "fftpde_fs_part_perm": (st, [p, u, p, p, u]),
         "fftpde_diffuse_source_scratch_size": (ctypes.c_size_t, [p]),
         "fftpde_diffuse_source": (st, [p, p, p, p, dbl, dbl, i64, p, ctypes.c_size_t]),
         "fftpde_wave_rk4": (st, [p, p, p, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, dbl, i64, p, p,
@@ -417,6 +420,45 @@ class Plan:
         self._bind_stream()
         _check(self.lib.fftpde_cols_to_peers(self._h, cs.data_ptr(), arr, len(peers), int(rank), int(R), int(op),
                                              float(D), float(dt)), "fftpde_cols_to_peers")
+
+    # ---- the distributed four-step pieces (R28; 32768^2 complex128 plans) ----
+    def fs_part_aa(self, op: int, P: int, rank: int, xmode: int, x: torch.Tensor, out: torch.Tensor,
+                   phys: torch.Tensor = None):
+        """AA (op 0) / AA^-1 (1) / MID (2) on this rank's part [P][32][M][32][M] (fftpde_fs_part_aa)."""
+        n = self.nx * self.ny // int(P)
+        self._dense("fs_part_aa", x, out, *([phys] if phys is not None else []), numel=n)
+        self._bind_stream()
+        _check(self.lib.fftpde_fs_part_aa(self._h, int(op), int(P), int(rank), int(xmode), x.data_ptr(),
+                                          out.data_ptr(), phys.data_ptr() if phys is not None else None),
+               "fftpde_fs_part_aa")
+
+    def fs_part_b(self, xmode: int, P: int, rank: int, f: torch.Tensor, D: float, dt: float, peers=None):
+        """The 1024-point diffusion pass of the part's local axis, in place or (peers: every
+        rank's other-part pointer) stored straight into the peers' other part (fftpde_fs_part_b)."""
+        self._dense("fs_part_b", f, numel=self.nx * self.ny // int(P))
+        arr = (ctypes.c_void_p * len(peers))(*[int(q) for q in peers]) if peers is not None else None
+        self._bind_stream()
+        _check(self.lib.fftpde_fs_part_b(self._h, int(xmode), int(P), int(rank), f.data_ptr(), float(D), float(dt),
+                                         arr, len(peers) if peers is not None else 0), "fftpde_fs_part_b")
+
+    def fs_part_perm(self, P: int, x: torch.Tensor, out: torch.Tensor, direction: int):
+        """Row slab <-> [P][P][32/P][M][32][M] (fftpde_fs_part_perm)."""
+        self._dense("fs_part_perm", x, out, numel=self.nx * self.ny // int(P))
+        self._bind_stream()
+        _check(self.lib.fftpde_fs_part_perm(self._h, int(P), x.data_ptr(), out.data_ptr(), int(direction)),
+               "fftpde_fs_part_perm")
+
+    def peer_blocks(self, src: torch.Tensor, peers, rank: int):
+        """All-to-all of equal blocks by peer stores: block q of src -> peers[q] at block `rank`
+        (fftpde_peer_transpose with one row)."""
+        P = len(peers)
+        self._dense("peer_blocks", src)
+        if src.numel() % P or (src.numel() // P * src.element_size()) % 16:
+            raise ValueError("peer_blocks: src must split into P blocks of whole 16-byte vectors")
+        arr = (ctypes.c_void_p * P)(*[int(x) for x in peers])
+        self._bind_stream()
+        _check(self.lib.fftpde_peer_transpose(self._h, src.data_ptr(), arr, P, int(rank), 1, src.numel() // P, 0),
+               "fftpde_peer_transpose")
 
     def pack_blocks(self, x: torch.Tensor, out: torch.Tensor, nrows: int, nblocks: int, bw: int,
                     direction: int):

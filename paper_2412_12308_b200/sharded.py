@@ -291,6 +291,82 @@ class FusedPeerSlabSolver(PeerSlabSolver):
         return outs
 
 
+class FusedFourStepSolver:
+    """C5 (32768^2 complex128 diffusion) on P ranks with the distributed four-step
+    (R28) and the Y-part <-> X-part exchange fused into the B passes: the
+    pass that ends in one part stores its tiles straight into every peer's other
+    part over NVLink (fftpde_fs_part_b with peers), so each step is
+        B pass -> peers' other part | barrier | other B pass (in place) | MID
+    with one barrier and no separate exchange; the parts alternate step by step.
+    The caller's row slabs enter and leave through fftpde_fs_part_perm, a block
+    all-to-all by peer stores and a block swap.  comm: LoopbackPeerComm (P virtual
+    ranks on one device) or SymmetricPeerComm (one rank per GPU)."""
+
+    def __init__(self, n, comm, plan):
+        self.comm, self.plan = comm, plan
+        self.P = comm.world
+        self.n = n
+        self.ranks = comm.local_ranks()
+        elems = n * n // self.P
+        dev, dt = plan.device, plan.dtype
+        self.Wy, self.Wy_ptrs = comm.alloc((elems,), dt, dev)     # Y-parts (peer-mapped: By stores into them)
+        self.Wx, self.Wx_ptrs = comm.alloc((elems,), dt, dev)     # X-parts (Bx stores into them)
+        self.T1, self.T1_ptrs = comm.alloc((elems,), dt, dev)     # receive buffer of the conversions
+        self.T2 = [torch.empty(elems, dtype=dt, device=dev) for _ in self.ranks]   # physical field / send buffer
+
+    def _swap(self, i, src, dst):
+        P = self.P
+        self.plan.pack_blocks(src, dst, P, P, src.numel() // (P * P), 0)
+
+    def diffuse(self, slabs, D, dt, nsteps, outs=None):
+        pl, P = self.plan, self.P
+        outs = outs if outs is not None else [torch.empty_like(s) for s in slabs]
+        if nsteps == 0:
+            for s, o in zip(slabs, outs):
+                o.copy_(s)
+            return outs
+        L = range(len(self.ranks))
+        self.comm.barrier()                                  # the peers are done with the last solve's buffers
+        for i in L:                                          # row slab -> Y-part
+            pl.fs_part_perm(P, slabs[i].view(-1), self.T2[i], 0)
+            pl.peer_blocks(self.T2[i], self.T1_ptrs, self.ranks[i])
+        self.comm.barrier()
+        for i in L:
+            self._swap(i, self.T1[i], self.Wy[i])
+            pl.fs_part_aa(0, P, self.ranks[i], 0, self.Wy[i], self.Wy[i])
+        x = 0
+        for k in range(nsteps):
+            W = self.Wx if x else self.Wy
+            for i, r in zip(L, self.ranks):                  # B pass of this part -> the peers' other part
+                pl.fs_part_b(x, P, r, W[i], D, dt, peers=self.Wy_ptrs if x else self.Wx_ptrs)
+            self.comm.barrier()
+            x ^= 1
+            W = self.Wx if x else self.Wy
+            for i, r in zip(L, self.ranks):
+                pl.fs_part_b(x, P, r, W[i], D, dt)
+                if k + 1 < nsteps:
+                    pl.fs_part_aa(2, P, r, x, W[i], W[i], self.T2[i])
+                else:
+                    pl.fs_part_aa(1, P, r, x, W[i], self.T2[i])
+        # the physical field (T2, part x) -> Y-part -> row slabs
+        if x:
+            for i, r in zip(L, self.ranks):
+                pl.peer_blocks(self.T2[i], self.T1_ptrs, r)
+            self.comm.barrier()
+            src = self.T1
+        else:
+            src = self.T2
+        for i in L:
+            self._swap(i, src[i], self.Wx[i])
+        self.comm.barrier()                                  # every rank has read its T1
+        for i, r in zip(L, self.ranks):
+            pl.peer_blocks(self.Wx[i], self.T1_ptrs, r)
+        self.comm.barrier()
+        for i in L:
+            pl.fs_part_perm(P, self.T1[i], outs[i].view(-1), 1)
+        return outs
+
+
 def slab_rows(ny, world, rank):
     """Rows [lo, hi) of rank `rank` (SURVEY.md 8(b) sharded plans)."""
     R = ny // world

@@ -384,3 +384,62 @@ def test_c5_distributed_fourstep_vs_oracle_and_rank_counts(steps):
     ref = torch.outer(t(Dg1), t(Df1)) + torch.outer(t(Dg2), t(Df2))
     err = (torch.linalg.vector_norm(first - ref) / torch.linalg.vector_norm(ref)).item()
     assert err <= 1e-12, err
+
+
+@pytest.mark.parametrize("steps", [1, 2])
+def test_c5_fused_fourstep_peer_solver_vs_oracle(steps):
+    # FusedFourStepSolver: R28 with the exchange fused into the B passes (each rank's
+    # Bx / By epilogue stores its tiles straight into the peers' other part), P
+    # virtual ranks on one device (LoopbackPeerComm).  Every point against the
+    # oracle's stepped 1D solves of a rank-2 input (built row block by row block to
+    # keep the footprint at u0 + plan + 4 part buffers + u), and the same bits on
+    # every P (a strided sample of 2^20 points).
+    n, D, dt = 32768, 1e-4, 0.01
+    f1, g1, f2, g2 = (I.white_noise((n,), 730 + i) for i in range(4))
+    Df1, Dg1, Df2, Dg2 = (torch.from_numpy(O.diffuse(v.reshape(1, n), D, dt, steps).ravel()).cuda()
+                          for v in (f1, g1, f2, g2))
+    t = lambda v: torch.from_numpy(v).cuda()
+    plan = F.Plan(n, n, dtype=torch.complex128)
+    sample = None
+    for P in (1, 2, 8):
+        u0 = torch.outer(t(g1), t(f1)) + torch.outer(t(g2), t(f2))
+        solver = S.FusedFourStepSolver(n, S.LoopbackPeerComm(P), plan)
+        R = n // P
+        slabs = [u0[r * R:(r + 1) * R] for r in range(P)]
+        outs = solver.diffuse(slabs, D, dt, steps)
+        torch.cuda.synchronize()
+        del solver, slabs, u0
+        torch.cuda.empty_cache()
+        u = torch.cat(outs)
+        del outs
+        s = u.view(-1)[::1021].clone()
+        if sample is None:
+            sample = s
+        else:
+            assert torch.equal(s, sample), P
+        num = den = 0.0
+        for b in range(0, n, 4096):                          # the reference row block by row block
+            ref = torch.outer(Dg1[b:b + 4096], Df1) + torch.outer(Dg2[b:b + 4096], Df2)
+            num += torch.linalg.vector_norm(u[b:b + 4096] - ref).item() ** 2
+            den += torch.linalg.vector_norm(ref).item() ** 2
+        del u
+        torch.cuda.empty_cache()
+        assert (num / den) ** 0.5 <= 1e-12, (P, (num / den) ** 0.5)
+
+
+def test_fs_part_errors():
+    n = 32768
+    p = F.Plan(n, n, dtype=torch.complex128)
+    x = torch.zeros(n * n // 2, dtype=torch.complex128, device="cuda")
+    with pytest.raises(F.FFTPDEError):
+        p.fs_part_aa(0, 3, 0, 0, x, x)                       # P not a power of two
+    with pytest.raises(F.FFTPDEError):
+        p.fs_part_aa(2, 2, 0, 0, x, x)                       # MID without phys
+    with pytest.raises(F.FFTPDEError):
+        p.fs_part_b(0, 2, 2, x, 1e-4, 0.01)                  # rank out of range
+    with pytest.raises(F.FFTPDEError):
+        p.fs_part_b(0, 2, 0, x, 1e-4, 0.01, peers=[x.data_ptr()])   # one peer for two ranks
+    small = F.Plan(1024, 1024, dtype=torch.complex128)
+    y = torch.zeros(1024 * 1024, dtype=torch.complex128, device="cuda")
+    with pytest.raises(F.FFTPDEError):
+        small.fs_part_aa(0, 1, 0, 0, y, y)                   # not the 32768^2 grid
