@@ -121,7 +121,7 @@ fftpde_status fftpde_plan_2d_r2c(fftpde_plan *plan, int64_t nx, int64_t ny, int6
  * all-to-all -> unpack -> inverse y- and x-passes.  fftpde_forward returns the
  * y-slab of the spectrum, fftpde_inverse takes it back (x 1/(nx ny nz)).  P must
  * divide nz and ny.  One all-to-all per transform: a slab, not a pencil,
- * decomposition (nz >= P, which holds for every nz <= 1024 at P <= 8).
+ * decomposition (needs nz >= P; fftpde_plan_3d_pencil lifts that).
  *
  * Whole-plan calls on a sharded plan (fftpde_forward / _inverse / _poisson /
  * _diffuse) are collective, in the same order on every rank; u0 == u allowed.
@@ -173,7 +173,11 @@ fftpde_status fftpde_plan_3d_pencil(fftpde_plan *plan, int64_t nx, int64_t ny, i
  * fftpde_poisson (-1/|k|^2, k = 0 zeroed) / fftpde_diffuse (exp(-D|k|^2 dt),
  * |k|^2 = kx^2 + ky^2 + kz^2) act on the volume; fftpde_wave_step, the
  * *_batched calls and the other operators return FFTPDE_ERR_UNSUPPORTED.
- * nz <= 1024 in this build (single-level z-pass); nx, ny as fftpde_plan_2d.
+ * nz <= 32768: up to 1024 a single-level z-pass, beyond it the two-level
+ * column pass (nz = P Q, one 128-byte block of adjacent lines per cluster), which
+ * needs nx*ny * element size to be a multiple of 128 bytes (else
+ * FFTPDE_ERR_UNSUPPORTED; the sharded and pencil plans check their own line
+ * counts the same way); nx, ny as fftpde_plan_2d.
  * Errors as fftpde_plan_2d, plus FFTPDE_ERR_NOT_POW2_Z. */
 fftpde_status fftpde_plan_3d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t nz, fftpde_dtype dtype,
                              double Lx, double Ly, double Lz, int device);

@@ -88,6 +88,9 @@ struct fftpde_plan_s {
     int64_t nz = 1;
     double Lz = 1.0;
     std::vector<double> twz, twz8, kz2, kxy2;
+    int64_t zP = 0, zQ = 0;                    // nz > 1024: the z-pass is the two-level col2 pass, nz = zP zQ
+    std::vector<double> twPz, twQz, twNz;
+    size_t o_twPz = 0, o_twQz = 0, o_twNz = 0;
     size_t o_twz = 0, o_twz8 = 0, o_kz2 = 0, o_kxy2 = 0, o_exy = 0, o_ez = 0, o_zscale = 0;
     bool diff3_valid = false;
     double diff3_D = 0, diff3_dt = 0;
@@ -396,6 +399,12 @@ template <typename T> struct Passes {
     int64_t batch, stride;
     const void *twx() const { return p->ws + p->o_twx; }
     const void *twy() const { return p->ws + p->o_twy; }
+    // the z-pass tables (3D): single-level stage tables, + the col2 tables when nz > 1024
+    ColTw ztw() const
+    {
+        return ColTw{p->ws + p->o_twz, p->zP ? p->ws + p->o_twPz : nullptr, p->zP ? p->ws + p->o_twQz : nullptr,
+                     p->zP ? p->ws + p->o_twNz : nullptr, p->ws + p->o_twz8};
+    }
     ColTw rtw() const
     {
         return ColTw{twx(), p->ws + p->o_rtwP, p->ws + p->o_rtwQ, p->ws + p->o_rtwN, p->ws + p->o_twx8,
@@ -684,7 +693,7 @@ template <typename T> struct Passes {
         OpTables<T> t = tables3<true>(scale3());
         t.kx2 += r * p->R * p->nx;
         t.ex += r * p->R * p->nx;
-        const ColTw ztw{p->ws + p->o_twz, nullptr, nullptr, nullptr, p->ws + p->o_twz8};
+        const ColTw ztw = this->ztw();
         return launch(p, FFTPDE_KERNEL_COL, [&] {
             return launch_cols<T>(p->nz, in, out, p->R * p->nx, p->nz * p->R * p->nx, 1, op, ztw, t, p->stream);
         });
@@ -845,7 +854,7 @@ template <typename T> struct Passes {
         const int64_t nl = p->nyl2 * p->nxl;
         t.kx2 += r * nl;
         t.ex += r * nl;
-        const ColTw ztw{p->ws + p->o_twz, nullptr, nullptr, nullptr, p->ws + p->o_twz8};
+        const ColTw ztw = this->ztw();
         return launch(p, FFTPDE_KERNEL_COL, [&] {
             return launch_cols<T>(p->nz, in, out, nl, p->nz * nl, 1, op, ztw, t, p->stream);
         });
@@ -1129,7 +1138,7 @@ template <typename T> struct Passes {
     }
     cudaError_t zpass(const void *in, void *out, int op)
     {
-        const ColTw ztw{p->ws + p->o_twz, nullptr, nullptr, nullptr, p->ws + p->o_twz8};
+        const ColTw ztw = this->ztw();
         return launch(p, FFTPDE_KERNEL_COL, [&] {
             return launch_cols<T>(p->nz, in, out, p->nx * p->ny, p->nx * p->ny * p->nz, 1, op, ztw,
                                   tables3<true>(scale3()), p->stream);
@@ -1139,6 +1148,12 @@ template <typename T> struct Passes {
     // so with p->colP they go through the scratch; the operator passes are in place.
     cudaError_t forward3(const void *in, void *out)
     {
+        if (p->zP) {                        // the two-level z-pass transforms out of place
+            cudaError_t e = rows(in, scratch(0), 0);
+            if (e == cudaSuccess) e = ypass(scratch(0), scratch(1), COL_FWD);
+            if (e == cudaSuccess) e = zpass(scratch(1), out, COL_FWD);
+            return e;
+        }
         void *A = p->colP ? scratch(0) : out;
         cudaError_t e = rows(in, A, 0);
         if (e == cudaSuccess) e = ypass(A, out, COL_FWD);
@@ -1147,6 +1162,12 @@ template <typename T> struct Passes {
     }
     cudaError_t inverse3(const void *in, void *out)
     {
+        if (p->zP) {
+            cudaError_t e = zpass(in, scratch(0), COL_INV);
+            if (e == cudaSuccess) e = ypass(scratch(0), scratch(1), COL_INV);
+            if (e == cudaSuccess) e = rows(scratch(1), out, 1);
+            return e;
+        }
         void *B = p->colP ? scratch(0) : out;
         cudaError_t e = zpass(in, out, COL_INV);
         if (e == cudaSuccess) e = ypass(out, B, COL_INV);
@@ -1174,7 +1195,7 @@ template <typename T> struct Passes {
         OpTables<T> tz = tables3<true>((T)1);
         tz.ex = (const T *)(p->ws + p->o_zscale);
         tz.ey = (const T *)(p->ws + p->o_ez);
-        const ColTw ztw{p->ws + p->o_twz, nullptr, nullptr, nullptr, p->ws + p->o_twz8};
+        const ColTw ztw = this->ztw();
         cudaError_t e = cudaSuccess;
         for (int64_t k = 0; k < nsteps && e == cudaSuccess; ++k) {
             e = rows_diff(k == 0 ? u0 : u, u);
@@ -1628,6 +1649,11 @@ fftpde_status fftpde_set_workspace(fftpde_plan plan, void *dev_ptr, size_t bytes
         plan->diff3_valid = false;
         s = upload(plan, plan->o_twz, plan->twz);
         if (s == FFTPDE_OK) s = upload(plan, plan->o_twz8, plan->twz8);
+        if (s == FFTPDE_OK && plan->zP) {
+            s = upload(plan, plan->o_twPz, plan->twPz);
+            if (s == FFTPDE_OK) s = upload(plan, plan->o_twQz, plan->twQz);
+            if (s == FFTPDE_OK) s = upload(plan, plan->o_twNz, plan->twNz);
+        }
         if (s == FFTPDE_OK) s = upload(plan, plan->o_kz2, plan->kz2);
         if (s == FFTPDE_OK) s = upload(plan, plan->o_kxy2, plan->kxy2);
     }
@@ -2178,6 +2204,7 @@ fftpde_status fftpde_plan_3d_sharded(fftpde_plan *plan, int64_t nx, int64_t ny, 
     auto fail = [&](fftpde_status st) { fftpde_destroy(p); *plan = nullptr; return st; };
     const int64_t ec = (int64_t)elem_cplx(p);
     if (nz % nranks || ny % nranks || ((ny / nranks) * nx * ec) % 16) return fail(FFTPDE_ERR_UNSUPPORTED);
+    if (p->zP && ((ny / nranks) * nx * ec) % 128) return fail(FFTPDE_ERR_UNSUPPORTED);   // col2 z-pass blocks
     p->R = ny / nranks;
     p->nzl = nz / nranks;
     s = finish_sharded(p, nranks, rank, nccl_unique_id, p->nzl * ny * nx);
@@ -2200,6 +2227,7 @@ fftpde_status fftpde_plan_3d_pencil(fftpde_plan *plan, int64_t nx, int64_t ny, i
     const int64_t ec = (int64_t)elem_cplx(p);
     // every block the packs move is a whole number of 16-byte vectors
     if (nz % pz || ny % py || nx % py || ny % pz || ((nx / py) * ec) % 16) return fail(FFTPDE_ERR_UNSUPPORTED);
+    if (p->zP && ((ny / pz) * (nx / py) * ec) % 128) return fail(FFTPDE_ERR_UNSUPPORTED);   // col2 z-pass blocks
     p->pencil = true;
     p->Pz = pz;
     p->Py = py;
@@ -2269,8 +2297,16 @@ fftpde_status fftpde_plan_3d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     fftpde_plan p = *plan;
     auto fail = [&](fftpde_status st) { fftpde_destroy(p); *plan = nullptr; return st; };
     if (!is_pow2(nz)) return fail(FFTPDE_ERR_NOT_POW2_Z);
-    // the z-pass is single-level (nz <= 1024); its tables cover nx*ny lines
-    if (nz > 1024 || nx * ny > ((int64_t)1 << 26)) return fail(FFTPDE_ERR_UNSUPPORTED);
+    // the z-pass: single-level for nz <= 1024, the two-level col2 pass (nz = zP zQ,
+    // 128-byte blocks of lines) up to 32768; its per-line tables cover nx*ny lines
+    if (nz > 32768 || nx * ny > ((int64_t)1 << 26)) return fail(FFTPDE_ERR_UNSUPPORTED);
+    if (nz > 1024) {
+        fftpde::col2_split(nz, nx * ny, (int)elem_cplx(p), p->zP, p->zQ);
+        if (!p->zP) return fail(FFTPDE_ERR_UNSUPPORTED);
+        build_twiddles(p->zP, p->twPz, FFTPDE_COL2_EMAX);
+        build_twiddles(p->zQ, p->twQz, FFTPDE_COL2_EMAX);
+        build_plain_twiddles(nz, p->twNz);
+    }
     p->is3d = true;
     p->nz = nz;
     p->Lz = Lz;
@@ -2285,6 +2321,11 @@ fftpde_status fftpde_plan_3d(fftpde_plan *plan, int64_t nx, int64_t ny, int64_t 
     auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return o; };
     p->o_twz = take(p->twz.size() / 2 * ec);
     p->o_twz8 = take(p->twz8.size() / 2 * ec);
+    if (p->zP) {
+        p->o_twPz = take(p->twPz.size() / 2 * ec);
+        p->o_twQz = take(p->twQz.size() / 2 * ec);
+        p->o_twNz = take(p->twNz.size() / 2 * ec);
+    }
     p->o_kz2 = take((size_t)nz * er);
     p->o_ez = take((size_t)nz * er);
     p->o_kxy2 = take((size_t)(nx * ny) * er);

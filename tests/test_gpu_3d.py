@@ -67,7 +67,10 @@ def test_3d_errors():
         F.Plan3D(16, 16, 12)
     assert e.value.status == F.ERR_NOT_POW2_Z
     with pytest.raises(F.FFTPDEError) as e:
-        F.Plan3D(16, 16, 2048)
+        F.Plan3D(16, 16, 65536)                   # beyond the two-level z-pass
+    assert e.value.status == F.ERR_UNSUPPORTED
+    with pytest.raises(F.FFTPDEError) as e:
+        F.Plan3D(2, 2, 2048)                      # 4 lines: less than one 128-byte block for the col2 z-pass
     assert e.value.status == F.ERR_UNSUPPORTED
     p = F.Plan3D(16, 16, 8)
     x = torch.zeros(8, 16, 16, dtype=torch.complex128, device="cuda")
@@ -75,3 +78,23 @@ def test_3d_errors():
     assert st == F.ERR_UNSUPPORTED
     st = p.lib.fftpde_poisson_batched(p._h, x.data_ptr(), x.data_ptr(), 1, 256)
     assert st == F.ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("shape,dtype,tol", [((2048, 4, 16), torch.complex128, 1e-12),
+                                             ((4096, 8, 8), torch.complex128, 1e-12),
+                                             ((32768, 2, 8), torch.complex128, 1e-12),
+                                             ((2048, 8, 16), torch.complex64, 1e-5)])
+def test_3d_long_z_two_level_pass(shape, dtype, tol):
+    # nz > 1024: the z-pass is the two-level column pass (col2, nz = P Q) with the
+    # plan's z tables, against the oracle (fft3 / poisson3 / diffuse3)
+    nz, ny, nx = shape
+    x = rand(shape, 277, np.complex64 if dtype == torch.complex64 else np.complex128)
+    L = (1.0, 2.0, 0.5)
+    p = F.Plan3D(nx, ny, nz, dtype=dtype, Lx=L[0], Ly=L[1], Lz=L[2])
+    xd = torch.from_numpy(x).cuda()
+    x64 = x.astype(np.complex128)
+    assert rel(p.forward(xd).cpu().numpy(), O.fft3(x64)) <= tol
+    assert rel(p.inverse(xd).cpu().numpy(), O.fft3(x64, inverse=True)) <= tol
+    assert rel(p.poisson(xd).cpu().numpy(), O.poisson3(x64, *L)) <= tol
+    assert rel(p.diffuse(xd, 1e-7, 0.01, 3).cpu().numpy(), O.diffuse3(x64, 1e-7, 0.01, 3, *L)) <= tol
+

@@ -443,3 +443,19 @@ def test_fs_part_errors():
     y = torch.zeros(1024 * 1024, dtype=torch.complex128, device="cuda")
     with pytest.raises(F.FFTPDEError):
         small.fs_part_aa(0, 1, 0, 0, y, y)                   # not the 32768^2 grid
+
+
+def test_3d_long_z_sharded_and_pencil():
+    # a 2048-plane volume: the z-pass of the z-slab and pencil plans is the two-level
+    # column pass (fftpde_plan_3d's z tables), loopback ranks, against the oracle
+    nz, ny, nx = 2048, 8, 16
+    x = rand3((nz, ny, nx), 278)
+    ref = O.poisson3(x)
+    xd = torch.from_numpy(x).cuda()
+    for P in (2, 4):
+        p = F.ShardedPlan3D(nx, ny, nz, loopback=P)
+        assert rel(p.poisson(xd).cpu().numpy(), ref) <= 1e-12, P
+        assert rel(p.diffuse(xd, 1e-7, 0.01, 2).cpu().numpy(), O.diffuse3(x, 1e-7, 0.01, 2)) <= 1e-12, P
+    p = F.PencilPlan3D(nx, ny, nz, 2, 2, loopback=True)
+    xp = torch.from_numpy(to_xpencils(x, 2, 2)).cuda()
+    assert rel(from_xpencils(p.poisson(xp).cpu().numpy(), 2, 2), ref) <= 1e-12
