@@ -68,6 +68,19 @@ def _worker(rank, port, case, q):
         xp = torch.from_numpy(np.ascontiguousarray(x[i * nzl:(i + 1) * nzl, j * nyl:(j + 1) * nyl])).cuda()
         out["poisson"] = p.poisson(xp).cpu().numpy()
         out["spectrum"] = p.forward(xp).cpu().numpy()
+    elif case in ("c5lib", "c5fs"):    # the distributed four-step (R28) at C5's grid, rank-2 input
+        n, D, dt, steps = 32768, 1e-4, 0.01, 3
+        f1, g1, f2, g2 = (torch.from_numpy(_rand((n,), 620 + k)).cuda() for k in range(4))
+        R = n // WORLD
+        slab = (torch.outer(g1[rank * R:(rank + 1) * R], f1) + torch.outer(g2[rank * R:(rank + 1) * R], f2))
+        if case == "c5lib":            # NCCL all-to-all inside the library
+            u = F.ShardedPlan(n, n).diffuse(slab, D, dt, steps)
+        else:                          # the exchange fused into the B passes (symmetric memory)
+            plan = F.Plan(n, n)
+            u = S.FusedFourStepSolver(n, S.SymmetricPeerComm(), plan).diffuse([slab], D, dt, steps)[0]
+        torch.cuda.synchronize()
+        out["rows"] = u[::1021].cpu().numpy()          # every 1021st row of the slab
+        out["row0"] = rank * R
     q.put((rank, out))
     dist.barrier()
     dist.destroy_process_group()
@@ -123,3 +136,19 @@ def test_two_gpu_pencil_vs_oracle(case):
         spec[:, i * nyl2:(i + 1) * nyl2, j * nxl:(j + 1) * nxl] = res[r]["spectrum"]
     assert rel(pois, O.poisson3(x, 1.0, 2.0, 0.5)) <= 1e-12
     assert rel(spec, O.fft3(x)) <= 1e-12
+
+
+@needs_two
+@pytest.mark.parametrize("case", ["c5lib", "c5fs"])
+def test_two_gpu_c5_distributed_fourstep_vs_oracle(case):
+    # R28 on two GPUs: rank-2 separable input, the oracle's stepped 1D solves at
+    # sampled rows of both slabs (every point of each sampled row)
+    from oracle import oracle as O
+    res = _run(case)
+    n, D, dt, steps = 32768, 1e-4, 0.01, 3
+    f1, g1, f2, g2 = (_rand((n,), 620 + k) for k in range(4))
+    Df1, Dg1, Df2, Dg2 = (O.diffuse(v.reshape(1, n), D, dt, steps).ravel() for v in (f1, g1, f2, g2))
+    for r in range(WORLD):
+        rows = res[r]["row0"] + np.arange(0, n // WORLD, 1021)
+        ref = np.outer(Dg1[rows], Df1) + np.outer(Dg2[rows], Df2)
+        assert rel(res[r]["rows"], ref) <= 1e-12, r
