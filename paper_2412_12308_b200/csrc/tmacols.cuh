@@ -215,6 +215,22 @@ __device__ __forceinline__ float2 ld_cluster_f(uint32_t a)
     return v;
 }
 
+#ifndef FFTPDE_WAVE2_NA
+#define FFTPDE_WAVE2_NA 0    // 1: the propagator rows (read once per column) bypass L1 so the twiddle table stays there
+#endif
+__device__ __forceinline__ double ld_stream(const double *p)
+{
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_stream(const float *p)
+{
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+
 template <typename T, int N, int EX, int MINB>
 __global__ void __launch_bounds__(Shape<N, EX>::TPT, MINB)
 tma_wave2_cols_kernel(const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mv, int64_t ncols,
@@ -241,6 +257,26 @@ tma_wave2_cols_kernel(const __grid_constant__ CUtensorMap mu, const __grid_const
         asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
     }
     __syncthreads();
+#ifndef FFTPDE_WAVE2_PF
+#define FFTPDE_WAVE2_PF 0    // 1 / 2: prefetch this column's propagator rows into L2 / L1 ahead of the transform
+#endif
+#if FFTPDE_WAVE2_PF
+    {   // the rows C[|a|][.] and S[|a|][.] (plan constants: no dependence on the previous launch) are read
+        // once per column between the two cluster barriers; fetch their 128-byte lines now
+        const int64_t qa0 = a <= tab.nfold - a ? a : tab.nfold - a;
+        const T *r0 = tab.wC + qa0 * tab.qpitch, *r1 = (f ? tab.wS2 : tab.wS1) + qa0 * tab.qpitch;
+        constexpr int PER = 128 / (int)sizeof(T);
+        for (int i = t * PER; i <= N / 2; i += TPT * PER) {
+#if FFTPDE_WAVE2_PF == 2
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(r0 + i) : "memory");
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(r1 + i) : "memory");
+#else
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(r0 + i) : "memory");
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(r1 + i) : "memory");
+#endif
+        }
+    }
+#endif
     pdl_wait();
     if (t == 0) {
         tma_mbar_expect(mbar, (uint32_t)(N * sizeof(C)));
@@ -279,7 +315,11 @@ tma_wave2_cols_kernel(const __grid_constant__ CUtensorMap mu, const __grid_const
         for (int e = 0; e < E; ++e) {
             const int b = t + TPT * e;
             const int qb = b <= N - b ? b : N - b;
+#if FFTPDE_WAVE2_NA
+            const T cc = ld_stream(pC + qb), ss = ld_stream(pS + qb);
+#else
             const T cc = __ldg(pC + qb), ss = __ldg(pS + qb);
+#endif
             C o;
             if constexpr (sizeof(T) == 8) o = ld_cluster(peer + (uint32_t)(b * sizeof(C)));
             else o = ld_cluster_f(peer + (uint32_t)(b * sizeof(C)));
