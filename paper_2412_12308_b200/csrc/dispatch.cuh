@@ -603,16 +603,28 @@ cudaError_t tma_wave2_n(void *U, void *V, int64_t nx, int64_t stride, int64_t ba
     cfg.blockDim = dim3(Shape<N, EX>::TPT, 1, 1);
     cfg.dynamicSmemBytes = L::BYTES;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[3];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    int na = 1;
+    // A/B knob: FFTPDE_WAVE2_SCHED=1 / 2 asks for the spread / load-balancing cluster scheduling policy
+    static const int sched = [] { const char *s = std::getenv("FFTPDE_WAVE2_SCHED"); return s ? std::atoi(s) : 0; }();
+    if (sched == 1 || sched == 2) {
+        attr[na].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+        attr[na].val.clusterSchedulingPolicyPreference =
+            sched == 1 ? cudaClusterSchedulingPolicySpread : cudaClusterSchedulingPolicyLoadBalancing;
+        ++na;
+    }
+    if (pdl_enabled(PDL_COL2)) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled(PDL_COL2) ? 2 : 1;
-    e = cudaLaunchKernelEx(&cfg, k, mu, mv, nx, (const C *)tw, tab);
+    cfg.numAttrs = na;
+    e = cudaLaunchKernelEx(&cfg, k, mu, mv, nx, (const C *)tw, tab, (C *)U, (C *)V, stride);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 

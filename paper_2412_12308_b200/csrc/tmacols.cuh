@@ -234,7 +234,8 @@ __device__ __forceinline__ float ld_stream(const float *p)
 template <typename T, int N, int EX, int MINB>
 __global__ void __launch_bounds__(Shape<N, EX>::TPT, MINB)
 tma_wave2_cols_kernel(const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mv, int64_t ncols,
-                      const typename cplx_t<T>::type *__restrict__ tw, OpTables<T> tab)
+                      const typename cplx_t<T>::type *__restrict__ tw, OpTables<T> tab,
+                      typename cplx_t<T>::type *gU, typename cplx_t<T>::type *gV, int64_t gstride)
 {
     using C = typename cplx_t<T>::type;
     using S = Shape<N, EX>;
@@ -283,6 +284,19 @@ tma_wave2_cols_kernel(const __grid_constant__ CUtensorMap mu, const __grid_const
         const uint32_t d = tma_smem(base);
 #pragma unroll
         for (int k = 0; k < L::NBOX; ++k) tma_load3(d + k * L::BOXR * (int)sizeof(C), map, (int)(2 * a), k * L::BOXR, (int)bz, mbar);
+#ifndef FFTPDE_WAVE2_TPF
+#define FFTPDE_WAVE2_TPF 0   // > 0: L2-prefetch (TMA) the column of the cluster that many clusters ahead (148 = one wave)
+#endif
+#if FFTPDE_WAVE2_TPF
+        const int64_t pc = cid + FFTPDE_WAVE2_TPF;
+        if (pc < (int64_t)(gridDim.x / 2)) {
+            const int64_t pz = pc / ncols, pa = pc - pz * ncols;
+#pragma unroll
+            for (int k = 0; k < L::NBOX; ++k)
+                asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map),
+                             "r"((int)(2 * pa)), "r"(k * L::BOXR), "r"((int)pz) : "memory");
+        }
+#endif
     }
     pdl_trigger();
     tma_mbar_wait(mbar, 0);
@@ -336,6 +350,22 @@ tma_wave2_cols_kernel(const __grid_constant__ CUtensorMap mu, const __grid_const
     cl_arrive_release();
     cl_wait_acquire();
     fft_tw<N, true, EX>(v, sm, t, twp, sync);
+#ifndef FFTPDE_WAVE2_LSUST
+#define FFTPDE_WAVE2_LSUST 0   // 1: the result column leaves through st.global from the registers (the LSU), so the
+#endif                         // TMA unit only carries the column loads (it is request-rate bound on 16-byte rows)
+#if FFTPDE_WAVE2_LSUST
+    {
+        C *g = (f ? gV : gU) + bz * gstride + a + (int64_t)t * ncols;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            C *q = g + (int64_t)(TPT * e) * ncols;
+            if constexpr (sizeof(T) == 8)
+                asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(q), "d"(v[e].x), "d"(v[e].y) : "memory");
+            else
+                asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(q), "f"(v[e].x), "f"(v[e].y) : "memory");
+        }
+    }
+#else
 #pragma unroll
     for (int e = 0; e < E; ++e) line[t + TPT * e] = v[e];
     tma_fence_smem();
@@ -347,6 +377,7 @@ tma_wave2_cols_kernel(const __grid_constant__ CUtensorMap mu, const __grid_const
         tma_commit();
         tma_wait_read0();
     }
+#endif
 }
 
 

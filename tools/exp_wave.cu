@@ -156,7 +156,7 @@ static void run_tma_wave2(double2 *U, double2 *V, long n, const void *tw, const 
     cfg.attrs = at; cfg.numAttrs = 1;
     int ncl = 0;
     cudaOccupancyMaxActiveClusters(&ncl, k, &cfg);
-    auto go = [&] { cfg.stream = g_stream; cudaLaunchKernelEx(&cfg, k, mu, mv, (int64_t)n, (const double2 *)tw, tab); };
+    auto go = [&] { cfg.stream = g_stream; cudaLaunchKernelEx(&cfg, k, mu, mv, (int64_t)n, (const double2 *)tw, tab, U, V, (int64_t)(n * n)); };
     if (!time) { go(); return; }
     char name[128];
     snprintf(name, sizeof name, "%s TMA wave2 E=%d minb=%d clusters=%d", tag, EX, MINB, ncl);
