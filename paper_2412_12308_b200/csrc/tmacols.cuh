@@ -366,17 +366,37 @@ tma_wave2_cols_kernel(const __grid_constant__ CUtensorMap mu, const __grid_const
         }
     }
 #else
+#ifndef FFTPDE_WAVE2_LSUQ
+#define FFTPDE_WAVE2_LSUQ 4    // 4096-point columns: the last 4 of the 16 256-row boxes leave through st.global from
+#endif                         // the registers, the rest through the TMA unit, which is request-rate bound on 16-byte
+                               // rows (C3 wave pass 0.553 -> 0.544 ms; 2 boxes equal, all 16 boxes 0.658 ms; run r02v)
+    constexpr int LSUQ = N == 4096 ? FFTPDE_WAVE2_LSUQ : 0;
+    constexpr int KT = L::NBOX - LSUQ;                      // boxes stored by the TMA unit
+    constexpr int ET = KT * L::BOXR / TPT;                  // slots e < ET lie in those boxes
+    static_assert(LSUQ == 0 || (L::BOXR % TPT == 0 && KT > 0), "box / slot split");
 #pragma unroll
-    for (int e = 0; e < E; ++e) line[t + TPT * e] = v[e];
+    for (int e = 0; e < E; ++e)
+        if (e < ET) line[t + TPT * e] = v[e];
     tma_fence_smem();
     __syncthreads();
     if (t == 0) {
         const uint32_t src = tma_smem(base);
 #pragma unroll
-        for (int k = 0; k < L::NBOX; ++k) tma_store3(map, (int)(2 * a), k * L::BOXR, (int)bz, src + k * L::BOXR * (int)sizeof(C));
+        for (int k = 0; k < KT; ++k) tma_store3(map, (int)(2 * a), k * L::BOXR, (int)bz, src + k * L::BOXR * (int)sizeof(C));
         tma_commit();
-        tma_wait_read0();
     }
+    if constexpr (LSUQ > 0) {
+        C *g = (f ? gV : gU) + bz * gstride + a + (int64_t)t * ncols;
+#pragma unroll
+        for (int e = ET; e < E; ++e) {
+            C *q = g + (int64_t)(TPT * e) * ncols;
+            if constexpr (sizeof(T) == 8)
+                asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(q), "d"(v[e].x), "d"(v[e].y) : "memory");
+            else
+                asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(q), "f"(v[e].x), "f"(v[e].y) : "memory");
+        }
+    }
+    if (t == 0) tma_wait_read0();
 #endif
 }
 
